@@ -1,0 +1,433 @@
+#!/usr/bin/env python
+"""Benchmark: train steps/s (fwd + bwd + Adam) at 1M Gaussians, 1080p.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c1]
+    python bench.py --impl reference ...        # CPU reference arm
+
+A step is one training step over one camera view per GPU: K1 preprocess ->
+K2 keys/sort/ranges -> K3 render -> photometric loss -> K4 per-Gaussian
+backward -> K4b+K5 (fused projection VJP + Adam at N=1; VJP, NCCL allreduce,
+Adam at N>1).  Inputs: the canonical synthetic scene of SURVEY.md §8(d),
+resident in HBM.  `value` is whole-job view-steps/s (= steps/s at N=1).
+Rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    "c1": dict(n=10_000, width=256, height=256, clustered=False),
+    "c2": dict(n=1_000_000, width=1920, height=1080, clustered=False),
+    "c3": dict(n=3_000_000, width=1920, height=1080, clustered=True),
+}
+METRIC = "train steps/sec (fwd+bwd+Adam) at 1M Gaussians 1080p"
+# FP32 lane-op counts per unit of work
+RENDER_OPS = (12, 7)       # per evaluation, per blend
+BACKWARD_OPS = (12, 45)
+NOMINAL_FP32_LANES = 148 * 128
+
+
+def _env_int(name, default):
+    return int(os.environ.get(name, default))
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- clocks --
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-i", str(self.gpu), "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        os.unlink(self.path)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# -------------------------------------------------------------- CPU oracle --
+def _cpu_sample_step(scene, tile_frac, cores=1, gauss_frac=1.0, seed=0):
+    """One bounded-sample training step of the CPU oracle; returns the
+    extrapolated full-step seconds and a per-stage dict.
+
+    Vectorised stages (project, bin, loss, VJP, Adam) run on a `gauss_frac`
+    subset of Gaussians / image rows and are scaled by 1/gauss_frac; render and
+    backward run on a random `tile_frac` of the non-empty tiles and are scaled
+    by the pair-count fraction (per-tile work is proportional to list length
+    up to termination)."""
+    from oracle import raster as O
+    params, cam, gt = scene
+    rng = np.random.default_rng(seed)
+    n = len(params["positions"])
+    k = max(1, int(n * gauss_frac))
+    sub = {key: v[:k] for key, v in params.items()}
+    st = {}
+    t0 = time.perf_counter()
+    batch, colors = O.project(sub, cam)
+    st["project"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    idx = O.bin_sequential(batch)
+    st["bin"] = time.perf_counter() - t0
+    counts = np.diff(idx["offsets"])
+    busy = np.flatnonzero(counts > 0)
+    m = max(1, int(round(len(busy) * tile_frac)))
+    pick = np.sort(rng.choice(busy, m, replace=False))
+    frac_pairs = counts[pick].sum() / max(counts.sum(), 1)
+    t0 = time.perf_counter()
+    if cores <= 1:
+        bufs = O.render(batch, idx, colors, np.zeros(3), tiles=pick)
+    else:
+        bufs = _pool_render(cores, batch, idx, colors, pick)
+    st["render"] = time.perf_counter() - t0
+    rows = max(16, int(cam["height"] * gauss_frac))
+    t0 = time.perf_counter()
+    _, _, _, gcol = O.photometric(bufs["color"][:rows], gt[:rows])
+    st["loss"] = time.perf_counter() - t0
+    gfull = np.zeros_like(bufs["color"])
+    gfull[:rows] = gcol
+    gfull[rows:] = rng.normal(0, 1e-7, gfull[rows:].shape)
+    t0 = time.perf_counter()
+    if cores <= 1:
+        g2 = O.backward_per_gaussian(bufs, batch, idx, colors, gfull, tiles=pick)
+    else:
+        g2 = _pool_backward(cores, bufs, batch, idx, colors, gfull, pick)
+    st["backward"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    g3 = O.project_vjp(sub, cam, batch, g2)
+    st["vjp"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    for name in ("positions", "log_scales", "rotations", "opacity_logits", "colors"):
+        p = sub[name].copy()
+        O.adam_step(p, g3[name], np.zeros_like(p), np.zeros_like(p), 1, 1e-3,
+                    renormalize=(name == "rotations"))
+    st["adam"] = time.perf_counter() - t0
+    scale = {"project": 1 / gauss_frac, "bin": 1 / gauss_frac, "loss": cam["height"] / rows,
+             "vjp": 1 / gauss_frac, "adam": 1 / gauss_frac,
+             "render": 1 / frac_pairs, "backward": 1 / frac_pairs}
+    est = {key: st[key] * scale[key] for key in st}
+    return sum(est.values()), est, dict(tiles=int(m), busy_tiles=int(len(busy)),
+                                        pair_frac=float(frac_pairs), gauss_frac=gauss_frac)
+
+
+_SHARED = {}
+
+
+def _render_tiles(tiles):
+    from oracle import raster as O
+    s = _SHARED
+    return tiles, O.render(s["batch"], s["idx"], s["colors"], np.zeros(3), tiles=tiles)
+
+
+def _backward_tiles(tiles):
+    from oracle import raster as O
+    s = _SHARED
+    return O.backward_per_gaussian(s["bufs"], s["batch"], s["idx"], s["colors"], s["g"],
+                                   tiles=tiles)
+
+
+def _forked_map(fn, chunks, cores, **shared):
+    """Map over tile chunks in `cores` forked workers that inherit `shared`
+    copy-on-write (no pickling of the scene)."""
+    import multiprocessing as mp
+    _SHARED.clear()
+    _SHARED.update(shared)
+    with mp.get_context("fork").Pool(cores) as pool:
+        return pool.map(fn, chunks)
+
+
+def _pool_render(cores, batch, idx, colors, pick):
+    chunks = [c for c in np.array_split(pick, cores) if len(c)]
+    results = _forked_map(_render_tiles, chunks, cores, batch=batch, idx=idx, colors=colors)
+    W, H = batch["width"], batch["height"]
+    bufs = dict(color=np.zeros((H, W, 3)), depth=np.zeros((H, W)), final_T=np.ones((H, W)),
+                n_contrib=np.zeros((H, W), np.int32), n_considered=np.zeros((H, W), np.int32),
+                checkpoints={})
+    for tiles, out in results:
+        for t in tiles:
+            ty, tx = divmod(int(t), idx["tiles_x"])
+            sl = (slice(ty * 16, ty * 16 + 16), slice(tx * 16, tx * 16 + 16))
+            for key in ("color", "depth", "final_T", "n_contrib", "n_considered"):
+                bufs[key][sl] = out[key][sl]
+        bufs["checkpoints"].update(out["checkpoints"])
+    return bufs
+
+
+def _pool_backward(cores, bufs, batch, idx, colors, g, pick):
+    chunks = [c for c in np.array_split(pick, cores) if len(c)]
+    results = _forked_map(_backward_tiles, chunks, cores, bufs=bufs, batch=batch, idx=idx,
+                          colors=colors, g=g)
+    out = results[0]
+    for r in results[1:]:
+        for key in ("d_means2d", "d_conics", "d_opacities", "d_colors", "d_depths"):
+            out[key] += r[key]
+        out["merges"] += r["merges"]
+    return out
+
+
+def cpu_baseline(cfg_name, target_s=20.0):
+    """Single-core oracle, bounded sample (~10-30 s of CPU work)."""
+    from paper_2601_19489_b200.synthetic import make_scene
+    c = CONFIGS[cfg_name]
+    scene = make_scene(c["n"], c["width"], c["height"], seed=0, clustered=c["clustered"])
+    frac = 0.01 if c["n"] >= 1_000_000 else 0.25
+    t0 = time.perf_counter()
+    est, stages, sample = _cpu_sample_step(scene, frac)
+    wall = time.perf_counter() - t0
+    return {"value": 1.0 / est, "unit": "steps/s", "cores": 1, "kind": "port",
+            "sample": (f"oracle/raster.py (float64 NumPy restatement, pinned to the reference's "
+                       f"golden vectors), 1 thread; one step of {cfg_name} with project/bin/"
+                       f"loss/VJP/Adam at full size and render+backward on "
+                       f"{sample['tiles']}/{sample['busy_tiles']} random non-empty tiles "
+                       f"({sample['pair_frac']:.3%} of pairs), extrapolated by pair count; "
+                       f"{wall:.1f} s of CPU work"),
+            "est_step_s": est, "stages_s": {k: round(v, 3) for k, v in stages.items()}}
+
+
+def reference_arm(args):
+    """`--impl reference`: the CPU restatement of the reference path on all host
+    cores, bounded sample per step, rank 0 only."""
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return
+    from paper_2601_19489_b200.synthetic import make_scene
+    c = CONFIGS[args.config]
+    scene = make_scene(c["n"], c["width"], c["height"], seed=0, clustered=c["clustered"])
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    gauss_frac = 1.0 / 16 if c["n"] >= 1_000_000 else 1.0
+    tile_frac = min(1.0, 0.002 * cores) if c["n"] >= 1_000_000 else 1.0
+    ests = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        est, stages, info = _cpu_sample_step(scene, tile_frac, cores, gauss_frac, seed=i)
+        if i >= args.warmup:
+            ests.append(est)
+    est = float(np.mean(ests))
+    value = 1.0 / est
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": est * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: " + _workload(args.config, 1),
+                       "views_per_step": 1},
+            "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "port",
+                             "sample": (f"oracle/raster.py float64 NumPy port on {cores} "
+                                        f"processes; per step: project/bin/VJP/Adam on "
+                                        f"{gauss_frac:.4g} of the Gaussians and loss on the "
+                                        f"same fraction of rows (x{1/gauss_frac:.0f}), render+"
+                                        f"backward on {info['tiles']} random non-empty tiles "
+                                        f"({info['pair_frac']:.3%} of pairs), extrapolated")},
+            "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _workload(name, n_gpus):
+    c = CONFIGS[name]
+    return (f"{c['n']:,} Gaussians{' (clustered depth)' if c['clustered'] else ''}, "
+            f"{c['width']}x{c['height']}, SH0, one view per GPU per step, "
+            f"fwd+loss+bwd+Adam, {n_gpus} GPU(s)")
+
+
+# ---------------------------------------------------------------- GPU arm --
+def gpu_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2601_19489_b200 as ts
+    from paper_2601_19489_b200.parallel import ViewParallelStep
+    from paper_2601_19489_b200.synthetic import camera_ring, make_scene
+    from paper_2601_19489_b200.trainer import phase_times
+
+    rank, world = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1)
+    local = _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = CONFIGS[args.config]
+    params, cam, gt = make_scene(c["n"], c["width"], c["height"], seed=0,
+                                 clustered=c["clustered"])
+    gset = ts.GaussianSet(**params)
+    ring = camera_ring(max(world, 1), 4.0, cam["fx"], c["width"], c["height"])
+    rc = ring[rank]
+    camera = ts.Camera(rc["fx"], rc["fy"], rc["cx"], rc["cy"], c["width"], c["height"],
+                       rc["R"], rc["t"])
+    gt_host = torch.from_numpy(np.asarray(gt, np.float32)).pin_memory()
+    gt_dev = gt_host.to("cuda")
+    cfg = ts.TrainConfig(max_iters=30_000)
+    if world == 1:
+        stepper = ts.TrainStep(gset, cfg, extent=4.0)
+        run = lambda timer=None: stepper.step(camera, gt_dev, timer)  # noqa: E731
+    else:
+        stepper = ViewParallelStep(gset, cfg, extent=4.0)
+        run = lambda timer=None: stepper.step_views([camera], [gt_dev], timer)  # noqa: E731
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        run()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    timer = {}
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        run(timer)
+    e1.record()
+    barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    clock = clocks.stop()
+    phases = {k: v / args.steps for k, v in phase_times(timer).items()}
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * 1e3 / ms
+
+    # work counters of the last step (for the roofline), outside the timed region
+    batch, tiles, bufs = stepper.last
+    evals = int(bufs.n_considered.sum().item())
+    blends = int(bufs.n_contrib.sum().item())
+    pairs = tiles.n_pairs
+
+    # e2e: host buffers, H2D of the GT image + D2H of the loss inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            gt_dev.copy_(gt_host, non_blocking=True)
+            loss = run()
+            loss_host = float(loss.item())
+        barrier()
+        e2e_s = (time.perf_counter() - t0) / args.steps
+        if world > 1:
+            t = torch.tensor([e2e_s], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": world / e2e_s, "unit": "view-steps/s",
+               "h2d_bytes_per_step": int(gt_host.numel() * 4),
+               "d2h_bytes_per_step": 4, "ms_per_step": e2e_s * 1e3,
+               "last_loss": loss_host}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    sm_mhz = clock.get("sm_mhz") or 1965.0
+    peak_ops = NOMINAL_FP32_LANES * sm_mhz * 1e6 / 1e12   # T lane-ops/s at the sampled clock
+    bwd_ms = phases.get("backward", 0.0) - phases.get("loss", 0.0) * 0  # backward phase only
+    bwd_ops = BACKWARD_OPS[0] * evals + BACKWARD_OPS[1] * blends
+    achieved = bwd_ops / (bwd_ms * 1e-3) / 1e12 if bwd_ms > 0 else None
+    traffic = None
+    prof = ROOT / "profiles" / "backward_traffic.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get("bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": value, "unit": "view-steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (canonical generator, SURVEY.md §8(d), seed 0)",
+        "config": {"workload": f"{args.config}: " + _workload(args.config, world),
+                   "views_per_step": world, "parallelism": f"view-parallel dp{world}",
+                   "l2": "inputs larger than L2 (Gaussian state + Adam moments 168 MB, "
+                         "per-step buffers ~1 GB)"},
+        "roofline": {"kernel": "render_bwd_kernel (K4)", "bound": "fp32",
+                     "achieved": achieved, "peak": peak_ops, "unit": "Tops/s",
+                     "frac": (achieved / peak_ops) if achieved else None,
+                     "traffic": traffic,
+                     "peak_note": "nominal FP32 lane-ops/s = 148 SMs x 128 lanes x sampled SM "
+                                  "clock (MEASURED_PEAKS.json has no FP32 figure)",
+                     "ops_per_unit": {"per_eval": BACKWARD_OPS[0], "per_blend": BACKWARD_OPS[1]},
+                     "units": {"evals": evals, "blends": blends, "pairs": pairs}},
+        "phases_ms": {k: round(v, 4) for k, v in phases.items()},
+        "gpu_launches": 7 * args.steps,
+        "clocks": clock,
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.config)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,202 @@
+/*
+ * tilesplat_b200.h -- C-ABI of the B200-native differentiable tile rasterizer.
+ *
+ * Drop-in boundary for the hot path of the reference package `tilesplat`
+ * (/root/reference/pkg/src/tilesplat, pure Python/NumPy).  The reference has
+ * no FFI; its boundary is the Python API re-exported by tilesplat/__init__.py:6-20.
+ * Each entry point below replaces one reference function (cited file:line).
+ * The Python host package `paper_2601_19489_b200` binds these with ctypes and
+ * keeps the reference names/signatures.
+ *
+ * Conventions
+ *   - every pointer is a DEVICE pointer unless the name ends in `_host`;
+ *   - `stream` is a cudaStream_t passed as void*; every call is stream-ordered,
+ *     asynchronous, stateless and re-entrant (no global mutable state);
+ *   - the library never allocates or frees caller memory; scratch comes from a
+ *     caller-provided workspace sized by the matching *_workspace() query;
+ *   - return 0 (TSR_OK) or a TSR_E_* code; the host raises the reference's
+ *     exception types from these codes.
+ *
+ * Data layout in HBM (FP32 unless noted):
+ *   raster record  rec[M][12] = {mx, my, a, b, c, opacity, depth, level_t,
+ *                                r, g, b, 0}   (48 B, 16-B aligned rows)
+ *     = SplatBatch.means2d/conics/opacities/depths/level_t + per-row RGB
+ *   keys  [P] int64  = tile << 32 | bits(float32 depth)   (binning.py:137-152)
+ *   values[P] int32  = batch row
+ *   offsets[T+1] int64 (binning.py:156-157)
+ *   grad2d[M][10] = {d_mx, d_my, d_a, d_b, d_c, d_opacity, d_r, d_g, d_b, d_depth}
+ */
+#ifndef TILESPLAT_B200_H
+#define TILESPLAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSR_OK 0
+#define TSR_E_INVALID 1   /* bad argument (shape, null pointer, limits)   */
+#define TSR_E_CUDA 2      /* CUDA launch / runtime error                 */
+#define TSR_E_CAPACITY 3  /* output capacity too small (caller retries)   */
+#define TSR_E_WORKSPACE 4 /* workspace smaller than *_workspace() says    */
+
+#define TSR_TILE 16
+#define TSR_REC_FLOATS 12
+#define TSR_GRAD2D_FLOATS 10
+#define TSR_CKPT_INTERVAL 32
+#define TSR_MAX_GAUSSIANS (1LL << 26)
+
+/* Pinhole camera with the pose delta already folded in
+ * (projection.py:73-78, pose.py:100-111). */
+typedef struct {
+  float fx, fy, cx, cy;
+  int32_t width, height;
+  float R[9];      /* effective world->camera rotation, row-major            */
+  float t[3];      /* effective translation                                   */
+  float center[3]; /* camera centre in world coordinates (SH view dirs)       */
+  float near_plane;
+} tsr_camera_t;
+
+/* GaussianSet (scene.py:50-106) as FP32 SoA device arrays. */
+typedef struct {
+  const float* positions;      /* (N,3)            */
+  const float* log_scales;     /* (N,3)            */
+  const float* rotations;      /* (N,4) w,x,y,z    */
+  const float* opacity_logits; /* (N,)             */
+  const float* colors;         /* (N,C,3) SH coeff */
+  int64_t n;
+  int32_t sh_coeffs;           /* C = (deg+1)^2, deg <= 3 */
+} tsr_gaussians_t;
+
+/* ---------------------------------------------------------------- K1 ----
+ * project + _splat_colors + compute_snugboxes + exact per-splat pair count
+ * (projection.py:77-136, trainer.py:170-178, binning.py:87-104,166-215).
+ * One pass: culled rows are compacted in source order by a single-pass
+ * decoupled look-back scan that also produces splat-major pair offsets.
+ * Outputs (capacity N rows): rec, source_ids, row_of_source (-1 if culled),
+ * pair_offsets[M+1]; totals[0] = M, totals[1] = P (device).
+ * strategy: 0 = bin_sequential column walk, 1 = bin_load_balanced min-q test
+ * (both yield the same pair multiset). */
+size_t tsr_preprocess_workspace(int64_t n);
+int tsr_preprocess_fwd(const tsr_gaussians_t* g, const tsr_camera_t* cam,
+                       int32_t strategy, float* rec, int32_t* source_ids, int32_t* row_of_source,
+                       int64_t* pair_offsets, int64_t* totals, void* workspace,
+                       size_t workspace_bytes, void* stream);
+
+/* Pair count + splat-major offsets for an arbitrary caller-built batch
+ * (bin_sequential on a make_batch()-style SplatBatch, binning.py:166-215). */
+size_t tsr_count_workspace(int64_t m);
+int tsr_count_pairs(const float* rec, int64_t m, int32_t width, int32_t height,
+                    int32_t strategy, int64_t* pair_offsets, int64_t* total_pairs, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/* compute_snugboxes (binning.py:87-104): FP64 extents + inclusive tile rect
+ * (int32 [tx0,tx1,ty0,ty1]). */
+int tsr_snugboxes(const float* rec, int64_t m, int32_t width, int32_t height,
+                  double* x_min, double* x_max, double* y_min, double* y_max,
+                  int32_t* tile_rect, void* stream);
+
+/* ---------------------------------------------------------------- K2 ----
+ * Key duplication: the exact column walk of bin_sequential
+ * (binning.py:178-221) or the min-q group test of bin_load_balanced
+ * (binning.py:225-286, strategy=1), emitting keys/values splat-major. */
+int tsr_duplicate_keys(const float* rec, int64_t m, int32_t width, int32_t height,
+                       const int64_t* pair_offsets, int64_t n_pairs,
+                       int32_t strategy, int64_t* keys, int32_t* values,
+                       void* stream);
+
+/* Stable on-device LSD radix sort of (key, value) pairs on the significant
+ * key bits (radix_argsort_u64, binning.py:142-148). In/out buffers may not
+ * alias; results land in keys_out/values_out. */
+size_t tsr_sort_workspace(int64_t n_pairs, int32_t n_tiles);
+int tsr_sort_pairs(const int64_t* keys_in, int64_t* keys_out,
+                   const int32_t* values_in, int32_t* values_out,
+                   int64_t n_pairs, int32_t n_tiles, void* workspace,
+                   size_t workspace_bytes, void* stream);
+
+/* Per-tile ranges (binning.py:156-157) + checkpoint record bases
+ * ckpt_base[t] = sum_{u<t} floor(n_u / 32) (forward.py:139-145);
+ * ckpt_total (device) = total tile-records. */
+int tsr_tile_ranges(const int64_t* sorted_keys, int64_t n_pairs, int32_t n_tiles,
+                    int64_t* offsets, int64_t* ckpt_base, void* stream);
+
+/* ---------------------------------------------------------------- K3 ----
+ * render (forward.py:87-161). ckpt may be NULL (record_checkpoints=False).
+ * Checkpoint record r of tile t holds the (T, Cr, Cg, Cb, D) state after list
+ * position 32(r+1)-1, laid out ckpt[((ckpt_base[t]+r)*5 + ch)*256 + local_px];
+ * it is written for every pixel that consumed that position. */
+int tsr_render_fwd(const float* rec, const int32_t* values, const int64_t* offsets,
+                   int32_t width, int32_t height, const float* background_host,
+                   float* out_color, float* out_depth, float* out_final_T,
+                   int32_t* out_n_contrib, int32_t* out_n_considered,
+                   float* ckpt, const int64_t* ckpt_base, void* stream);
+
+/* ---------------------------------------------------------------- K4 ----
+ * backward_per_gaussian (backward.py:137-223): lane-per-splat groups of 32
+ * restarting from checkpoints, warp scans for T and the weighted colour
+ * suffix, one merged atomic write per (splat, tile).  grad2d must be zeroed
+ * by the caller.  grad_depth / grad_final_T are nullable.  merges (device,
+ * u64) counts (splat, tile) merges with the reference's semantics. */
+int tsr_render_bwd(const float* rec, const int32_t* values, const int64_t* offsets,
+                   int32_t width, int32_t height, const float* color,
+                   const float* depth, const float* final_T,
+                   const int32_t* n_considered, const float* ckpt,
+                   const int64_t* ckpt_base, const float* grad_color,
+                   const float* grad_depth, const float* grad_final_T,
+                   float* grad2d, unsigned long long* merges, void* stream);
+
+/* --------------------------------------------------------------- K4b ----
+ * project_vjp + SH/colour chain (projection.py:139-241, trainer.py:231-257,
+ * scene.py:279-291).  Writes (not accumulates) per-Gaussian gradients for
+ * every source row: culled rows get zeros.  pose_sums (device, 12 floats,
+ * accumulated) = {sum_rows J^T G_A + g_pcam p^T (3x3 row-major), sum g_pcam}.
+ * grad_* are (N,3),(N,3),(N,4),(N,),(N,C,3).  accumulate != 0 adds into them
+ * (multi-view gradient accumulation). */
+int tsr_preprocess_bwd(const tsr_gaussians_t* g, const tsr_camera_t* cam,
+                       const float* rec, const int32_t* row_of_source,
+                       const float* grad2d, float* grad_positions,
+                       float* grad_log_scales, float* grad_rotations,
+                       float* grad_opacity_logits, float* grad_colors,
+                       float* pose_sums, int32_t accumulate, void* stream);
+
+/* ---------------------------------------------------------------- K5 ----
+ * Adam.step (optim.py:60-88): dense bias-corrected update of every row,
+ * non-finite gradient rows skipped (moments and params untouched) and
+ * counted into *skipped (device, accumulated), quaternion rows renormalised.
+ * lr / bias corrections are precomputed on the host in FP64. */
+typedef struct {
+  float* param;
+  const float* grad;
+  float* exp_avg;
+  float* exp_avg_sq;
+  int64_t rows;
+  int32_t width;        /* floats per row */
+  int32_t renormalize;  /* 1 for the rotation group */
+  float lr;
+  float bias_correction1; /* 1 - beta1^t */
+  float bias_correction2; /* 1 - beta2^t */
+} tsr_adam_group_t;
+
+#define TSR_MAX_ADAM_GROUPS 8
+int tsr_adam_step(const tsr_adam_group_t* groups_host, int32_t n_groups,
+                  unsigned long long* skipped, void* stream);
+
+/* K4b fused with K5 for the single-view training step: the per-Gaussian
+ * gradient never leaves registers.  groups_host[0..4] = positions,
+ * log_scales, rotations, opacity_logits, colors (grad pointers ignored). */
+int tsr_preprocess_bwd_adam(const tsr_gaussians_t* g, const tsr_camera_t* cam,
+                            const float* rec, const int32_t* row_of_source,
+                            const float* grad2d,
+                            const tsr_adam_group_t* groups_host,
+                            float* pose_sums, unsigned long long* skipped,
+                            void* stream);
+
+/* Version / build string (for smoke checks). */
+const char* tsr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TILESPLAT_B200_H */

@@ -1,0 +1,181 @@
+"""Tile binning on the B200 (reference: tilesplat/binning.py).
+
+Both strategies produce the reference's bit-exact TileIndex:
+  * bin_sequential      -- exact FP64 column walk (binning.py:166-222)
+  * bin_load_balanced   -- warp-per-splat FP64 min-q group test, candidates
+                           dealt round-robin to 32 lanes (binning.py:225-286)
+then the on-device stable LSD radix sort on tile<<32 | f32 depth bits and the
+per-tile ranges (binning.py:137-158).
+
+Device layout: keys (P,) int64, values (P,) int32 batch rows, offsets (T+1,)
+int64.  `ckpt_base` (T+1,) int64 is the prefix of floor(n_tile/32): where each
+tile's forward checkpoints start (forward.py:139-145).
+"""
+
+from __future__ import annotations
+
+import hashlib
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .projection import SplatBatch
+from .scene import TILE, _device
+
+
+@dataclass
+class SnugBox:
+    x_min: float
+    x_max: float
+    y_min: float
+    y_max: float
+    tile_rect: tuple
+
+
+class TileIndex:
+    """Depth-sorted (tile, splat) pairs with per-tile ranges (binning.py:37-71)."""
+
+    def __init__(self, keys, values, offsets, tiles_x, tiles_y, ckpt_base=None):
+        self.keys = keys
+        self.values = values
+        self.offsets = offsets
+        self.tiles_x = int(tiles_x)
+        self.tiles_y = int(tiles_y)
+        self.ckpt_base = ckpt_base
+
+    @property
+    def n_pairs(self) -> int:
+        return int(self.keys.shape[0])
+
+    @property
+    def n_tiles(self) -> int:
+        return self.tiles_x * self.tiles_y
+
+    def tile_range(self, tile_id: int):
+        return int(self.offsets[tile_id]), int(self.offsets[tile_id + 1])
+
+    def depths(self) -> torch.Tensor:
+        return (self.keys & 0xFFFFFFFF).to(torch.int32).view(torch.float32)
+
+    def tile_ids(self) -> torch.Tensor:
+        return self.keys >> 32
+
+    def checksum(self) -> str:
+        """sha256(keys as u64 || values as i64)[:16] (binning.py:67-71)."""
+        h = hashlib.sha256()
+        h.update(self.keys.cpu().numpy().astype(np.uint64).tobytes())
+        h.update(self.values.cpu().numpy().astype(np.int64).tobytes())
+        return h.hexdigest()[:16]
+
+
+def _tiles(batch: SplatBatch):
+    return -(-batch.width // TILE), -(-batch.height // TILE)
+
+
+def compute_snugboxes(batch: SplatBatch) -> SplatBatch:
+    """Fill FP64 extents and inclusive tile rects in place (binning.py:87-104)."""
+    lib = _lib.load()
+    m = len(batch)
+    dev = _device()
+    batch.x_min = torch.empty(m, dtype=torch.float64, device=dev)
+    batch.x_max = torch.empty(m, dtype=torch.float64, device=dev)
+    batch.y_min = torch.empty(m, dtype=torch.float64, device=dev)
+    batch.y_max = torch.empty(m, dtype=torch.float64, device=dev)
+    batch.tile_rect = torch.empty((m, 4), dtype=torch.int32, device=dev)
+    _lib.check(lib.tsr_snugboxes(
+        batch.rec.data_ptr(), m, batch.width, batch.height, batch.x_min.data_ptr(),
+        batch.x_max.data_ptr(), batch.y_min.data_ptr(), batch.y_max.data_ptr(),
+        batch.tile_rect.data_ptr(), _lib.stream_handle()), "tsr_snugboxes")
+    return batch
+
+
+def snugbox(conic, t, mean, image_dims) -> SnugBox:
+    """Single-splat SnugBox (binning.py:107-122), evaluated by the same kernel."""
+    a, b, c = (float(v) for v in conic)
+    if not (a > 0 and c > 0 and a * c - b * b > 0):
+        raise ValueError("conic is not positive definite")
+    if t < 0:
+        raise ValueError("level t must be >= 0")
+    width, height = image_dims
+    batch = SplatBatch([mean], [conic], [t], [1.0], [1.0], [0], width, height)
+    compute_snugboxes(batch)
+    r = batch.tile_rect[0].tolist()
+    return SnugBox(float(batch.x_min[0]), float(batch.x_max[0]), float(batch.y_min[0]),
+                   float(batch.y_max[0]), tuple(int(v) for v in r))
+
+
+def _pair_offsets(batch: SplatBatch, strategy: int):
+    """Splat-major pair offsets; reuses K1's fused count when available."""
+    if batch.pair_offsets is not None and batch.strategy == strategy:
+        return batch.pair_offsets, batch.n_pairs
+    lib = _lib.load()
+    m = len(batch)
+    dev = _device()
+    offs = torch.empty(m + 1, dtype=torch.int64, device=dev)
+    total = torch.zeros(1, dtype=torch.int64, device=dev)
+    ws = int(lib.tsr_count_workspace(m))
+    work = torch.empty(max(ws, 1), dtype=torch.uint8, device=dev)
+    _lib.check(lib.tsr_count_pairs(batch.rec.data_ptr(), m, batch.width, batch.height, strategy,
+                                   offs.data_ptr(), total.data_ptr(), work.data_ptr(), ws,
+                                   _lib.stream_handle()), "tsr_count_pairs")
+    return offs, int(total.item())
+
+
+def build_index(batch: SplatBatch, strategy: int, n_pairs: int | None = None,
+                pair_offsets=None) -> TileIndex:
+    """Duplicate keys, sort, ranges.  n_pairs/pair_offsets may come from K1."""
+    lib = _lib.load()
+    if pair_offsets is None or n_pairs is None:
+        pair_offsets, n_pairs = _pair_offsets(batch, strategy)
+    tiles_x, tiles_y = _tiles(batch)
+    n_tiles = tiles_x * tiles_y
+    m = len(batch)
+    dev = _device()
+    stream = _lib.stream_handle()
+    keys_tmp = torch.empty(max(n_pairs, 1), dtype=torch.int64, device=dev)
+    vals_tmp = torch.empty(max(n_pairs, 1), dtype=torch.int32, device=dev)
+    keys = torch.empty(n_pairs, dtype=torch.int64, device=dev)
+    vals = torch.empty(n_pairs, dtype=torch.int32, device=dev)
+    _lib.check(lib.tsr_duplicate_keys(batch.rec.data_ptr(), m, batch.width, batch.height,
+                                      pair_offsets.data_ptr(), n_pairs, strategy,
+                                      keys_tmp.data_ptr(), vals_tmp.data_ptr(), stream),
+               "tsr_duplicate_keys")
+    if n_pairs > 0:
+        ws = int(lib.tsr_sort_workspace(n_pairs, n_tiles))
+        work = torch.empty(ws, dtype=torch.uint8, device=dev)
+        _lib.check(lib.tsr_sort_pairs(keys_tmp.data_ptr(), keys.data_ptr(), vals_tmp.data_ptr(),
+                                      vals.data_ptr(), n_pairs, n_tiles, work.data_ptr(), ws,
+                                      stream), "tsr_sort_pairs")
+    offsets = torch.empty(n_tiles + 1, dtype=torch.int64, device=dev)
+    ckpt_base = torch.empty(n_tiles + 1, dtype=torch.int64, device=dev)
+    _lib.check(lib.tsr_tile_ranges(_lib.ptr(keys) if n_pairs else keys_tmp.data_ptr(), n_pairs,
+                                   n_tiles, offsets.data_ptr(), ckpt_base.data_ptr(), stream),
+               "tsr_tile_ranges")
+    return TileIndex(keys, vals, offsets, tiles_x, tiles_y, ckpt_base)
+
+
+def bin_sequential(batch: SplatBatch) -> TileIndex:
+    """Column-walk binning (binning.py:166-222)."""
+    return build_index(batch, 0)
+
+
+def bin_load_balanced(batch: SplatBatch, group_size: int = 32) -> TileIndex:
+    """Group-testing binning (binning.py:262-286); identical output."""
+    if group_size != 32:
+        raise ValueError("the sm_100a kernel deals candidates to one 32-lane warp")
+    return build_index(batch, 1)
+
+
+def lane_test_counts(batch: SplatBatch, splat_row: int, group_size: int = 32):
+    """Candidates tested per lane for one splat (binning.py:289-298)."""
+    if batch.tile_rect is None:
+        compute_snugboxes(batch)
+    r = [int(v) for v in batch.tile_rect[splat_row].tolist()]
+    n = max(0, r[1] - r[0] + 1) * max(0, r[3] - r[2] + 1)
+    counts = np.zeros(group_size, dtype=np.int64)
+    full, rem = divmod(n, group_size)
+    counts[:] = full
+    counts[:rem] += 1
+    return counts

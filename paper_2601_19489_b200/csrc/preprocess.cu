@@ -1,0 +1,355 @@
+// K1: preprocess -- projection, SH colour, SnugBox and exact pair count,
+// with row compaction + pair offsets from ONE single-pass decoupled
+// look-back scan (no second pass over the Gaussians).
+//
+// Reference semantics:
+//   _geometry / project      projection.py:77-136  (cull z <= near or o < 1/255,
+//                                                   EWA Sigma2 + 0.3 I, conic, t)
+//   _splat_colors / eval_sh  trainer.py:170-178, scene.py:224-230
+//   compute_snugboxes        binning.py:87-104
+//   bin_sequential count     binning.py:166-215  (exact FP64 column walk)
+//   bin_load_balanced count  binning.py:225-286  (FP64 min-q test per tile)
+// Rows stay in source order (projection.py:133), pairs are splat-major
+// (binning.py:217-221), so the later stable sort reproduces the reference's
+// tie order.
+#include <cuda_runtime.h>
+
+#include "tsr_common.cuh"
+
+namespace tsr {
+
+constexpr int kScanBlock = 256;
+// Look-back status word: [63:62] flag, [61:36] rows (26 bits), [35:0] pairs.
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagPrefix = 2ull << 62;
+constexpr unsigned long long kValueMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long pack_rp(unsigned long long rows,
+                                                      unsigned long long pairs) {
+  return (rows << 36) | pairs;
+}
+
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Block-wide exclusive scan of a packed (rows, pairs) value, then a
+// decoupled look-back for the block's global prefix.  Returns the global
+// exclusive prefix of this thread; *block_total receives the block aggregate.
+__device__ __forceinline__ unsigned long long scan_lookback(
+    unsigned long long v, int dyn_bid, unsigned long long* status,
+    unsigned long long* s_warp, unsigned long long* s_prefix) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kWarps = kScanBlock / 32;
+  unsigned long long incl = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    unsigned long long t = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += t;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long w = lane < kWarps ? s_warp[lane] : 0ull;
+    unsigned long long wi = w;
+#pragma unroll
+    for (int d = 1; d < kWarps; d <<= 1) {
+      unsigned long long t = __shfl_up_sync(0xffffffffu, wi, d);
+      if (lane >= d) wi += t;
+    }
+    unsigned long long agg = __shfl_sync(0xffffffffu, wi, kWarps - 1);
+    if (lane < kWarps) s_warp[lane] = wi - w;  // exclusive warp offsets
+    if (lane == 0) {
+      unsigned long long excl = 0;
+      if (dyn_bid == 0) {
+        st_relaxed(&status[0], kFlagPrefix | agg);
+      } else {
+        st_relaxed(&status[dyn_bid], kFlagAgg | agg);
+        int j = dyn_bid - 1;
+        while (true) {
+          unsigned long long s;
+          do {
+            s = ld_relaxed(&status[j]);
+          } while ((s >> 62) == 0);
+          excl += s & kValueMask;
+          if ((s >> 62) == 2) break;
+          --j;
+        }
+        st_relaxed(&status[dyn_bid], kFlagPrefix | (excl + agg));
+      }
+      s_prefix[0] = excl;
+      s_prefix[1] = agg;
+    }
+  }
+  __syncthreads();
+  return s_prefix[0] + s_warp[warp] + (incl - v);
+}
+
+__device__ __forceinline__ long long count_load_balanced(const SplatF64& s, int tiles_x,
+                                                         int tiles_y) {
+  SnugRect r = snugbox(s, tiles_x, tiles_y);
+  if (r.tx0 > r.tx1 || r.ty0 > r.ty1) return 0;
+  long long total = 0;
+  for (long long tx = r.tx0; tx <= r.tx1; ++tx) {
+    double rx0 = dsub((double)(16 * tx), s.mx);
+    double rx1 = dadd(rx0, 16.0);
+    for (long long ty = r.ty0; ty <= r.ty1; ++ty) {
+      double ry0 = dsub((double)(16 * ty), s.my);
+      double ry1 = dadd(ry0, 16.0);
+      total += (min_q_box(s, rx0, rx1, ry0, ry1) <= s.t) ? 1 : 0;
+    }
+  }
+  return total;
+}
+
+__device__ __forceinline__ long long count_pairs_of(const float* r, int strategy,
+                                                    int tiles_x, int tiles_y) {
+  SplatF64 s = load_splat_f64(r);
+  return strategy == 1 ? count_load_balanced(s, tiles_x, tiles_y)
+                       : count_sequential(s, tiles_x, tiles_y);
+}
+
+// Projection of one Gaussian into the 12-float raster record.  Returns false
+// when culled (projection.py:82).
+__device__ __forceinline__ bool project_one(const tsr_gaussians_t& g, const tsr_camera_t& cam,
+                                            long long i, float* rec) {
+  const float px = g.positions[3 * i], py = g.positions[3 * i + 1],
+              pz = g.positions[3 * i + 2];
+  const float* R = cam.R;
+  const float X = fmaf(R[0], px, fmaf(R[1], py, fmaf(R[2], pz, cam.t[0])));
+  const float Y = fmaf(R[3], px, fmaf(R[4], py, fmaf(R[5], pz, cam.t[1])));
+  const float Z = fmaf(R[6], px, fmaf(R[7], py, fmaf(R[8], pz, cam.t[2])));
+  const float o = 1.0f / (1.0f + expf(-g.opacity_logits[i]));
+  if (!(Z > cam.near_plane) || !(o >= kMinOpacity)) return false;
+
+  // R_q from the normalised quaternion (scene.py:33-47)
+  float qw = g.rotations[4 * i], qx = g.rotations[4 * i + 1], qy = g.rotations[4 * i + 2],
+        qz = g.rotations[4 * i + 3];
+  const float qn = rsqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
+  qw *= qn; qx *= qn; qy *= qn; qz *= qn;
+  float Rq[9];
+  Rq[0] = 1.f - 2.f * (qy * qy + qz * qz);
+  Rq[1] = 2.f * (qx * qy - qw * qz);
+  Rq[2] = 2.f * (qx * qz + qw * qy);
+  Rq[3] = 2.f * (qx * qy + qw * qz);
+  Rq[4] = 1.f - 2.f * (qx * qx + qz * qz);
+  Rq[5] = 2.f * (qy * qz - qw * qx);
+  Rq[6] = 2.f * (qx * qz - qw * qy);
+  Rq[7] = 2.f * (qy * qz + qw * qx);
+  Rq[8] = 1.f - 2.f * (qx * qx + qy * qy);
+  const float s0 = expf(g.log_scales[3 * i]), s1 = expf(g.log_scales[3 * i + 1]),
+              s2 = expf(g.log_scales[3 * i + 2]);
+  // M = R_q diag(s);  Sigma3 = M M^T
+  float M[9] = {Rq[0] * s0, Rq[1] * s1, Rq[2] * s2, Rq[3] * s0, Rq[4] * s1,
+                Rq[5] * s2, Rq[6] * s0, Rq[7] * s1, Rq[8] * s2};
+  const float iz = 1.0f / Z;
+  const float j00 = cam.fx * iz, j02 = -cam.fx * X * iz * iz;
+  const float j11 = cam.fy * iz, j12 = -cam.fy * Y * iz * iz;
+  // A = J R_eff (2x3)
+  float A0[3], A1[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    A0[k] = j00 * R[k] + j02 * R[6 + k];
+    A1[k] = j11 * R[3 + k] + j12 * R[6 + k];
+  }
+  // Sigma2 = (A M)(A M)^T + 0.3 I
+  float T0[3], T1[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    T0[k] = A0[0] * M[k] + A0[1] * M[3 + k] + A0[2] * M[6 + k];
+    T1[k] = A1[0] * M[k] + A1[1] * M[3 + k] + A1[2] * M[6 + k];
+  }
+  const float s11 = T0[0] * T0[0] + T0[1] * T0[1] + T0[2] * T0[2] + kCovDilation;
+  const float s12 = T0[0] * T1[0] + T0[1] * T1[1] + T0[2] * T1[2];
+  const float s22 = T1[0] * T1[0] + T1[1] * T1[1] + T1[2] * T1[2] + kCovDilation;
+  const float det = s11 * s22 - s12 * s12;
+  rec[0] = cam.fx * X * iz + cam.cx;
+  rec[1] = cam.fy * Y * iz + cam.cy;
+  rec[2] = s22 / det;
+  rec[3] = -s12 / det;
+  rec[4] = s11 / det;
+  rec[5] = o;
+  rec[6] = Z;
+  rec[7] = fmaxf(0.0f, 2.0f * logf(255.0f * o));
+  // colour: SH degree 0 is the raw coefficient (scene.py:227-228)
+  const int C = g.sh_coeffs;
+  const float* coef = g.colors + (long long)i * C * 3;
+  if (C == 1) {
+    rec[8] = coef[0];
+    rec[9] = coef[1];
+    rec[10] = coef[2];
+  } else {
+    float dx = px - cam.center[0], dy = py - cam.center[1], dz = pz - cam.center[2];
+    float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
+    dx *= inv; dy *= inv; dz *= inv;
+    float basis[16];
+    sh_basis(sh_degree_of(C), dx, dy, dz, basis);
+    float cr = 0.f, cg = 0.f, cb = 0.f;
+    for (int k = 0; k < C; ++k) {
+      cr = fmaf(basis[k], coef[3 * k], cr);
+      cg = fmaf(basis[k], coef[3 * k + 1], cg);
+      cb = fmaf(basis[k], coef[3 * k + 2], cb);
+    }
+    rec[8] = cr;
+    rec[9] = cg;
+    rec[10] = cb;
+  }
+  rec[11] = 0.f;
+  return true;
+}
+
+__global__ void __launch_bounds__(kScanBlock) preprocess_kernel(
+    tsr_gaussians_t g, tsr_camera_t cam, int strategy, float4* __restrict__ rec_out,
+    int32_t* __restrict__ source_ids, int32_t* __restrict__ row_of_source,
+    int64_t* __restrict__ pair_offsets, int64_t* __restrict__ totals,
+    unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket,
+    int n_blocks) {
+  __shared__ unsigned long long s_warp[kScanBlock / 32];
+  __shared__ unsigned long long s_prefix[2];
+  __shared__ int s_bid;
+  if (threadIdx.x == 0) s_bid = (int)atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int bid = s_bid;
+  const long long i = (long long)bid * kScanBlock + threadIdx.x;
+  const int tiles_x = tiles_of(cam.width), tiles_y = tiles_of(cam.height);
+
+  float rec[12];
+  bool keep = false;
+  long long cnt = 0;
+  if (i < g.n) {
+    keep = project_one(g, cam, i, rec);
+    if (keep) cnt = count_pairs_of(rec, strategy, tiles_x, tiles_y);
+  }
+  unsigned long long v = pack_rp(keep ? 1ull : 0ull, (unsigned long long)cnt);
+  unsigned long long excl = scan_lookback(v, bid, status, s_warp, s_prefix);
+  const long long row = (long long)(excl >> 36);
+  const long long pair0 = (long long)(excl & ((1ull << 36) - 1));
+  if (keep) {
+    float4* dst = rec_out + row * 3;
+    dst[0] = make_float4(rec[0], rec[1], rec[2], rec[3]);
+    dst[1] = make_float4(rec[4], rec[5], rec[6], rec[7]);
+    dst[2] = make_float4(rec[8], rec[9], rec[10], rec[11]);
+    source_ids[row] = (int32_t)i;
+    pair_offsets[row] = pair0;
+  }
+  if (i < g.n) row_of_source[i] = keep ? (int32_t)row : -1;
+  if (bid == n_blocks - 1 && threadIdx.x == 0) {
+    unsigned long long tot = s_prefix[0] + s_prefix[1];
+    long long m = (long long)(tot >> 36), p = (long long)(tot & ((1ull << 36) - 1));
+    totals[0] = m;
+    totals[1] = p;
+    pair_offsets[m] = p;
+  }
+}
+
+__global__ void __launch_bounds__(kScanBlock) count_kernel(
+    const float* __restrict__ rec, long long m, int width, int height, int strategy,
+    int64_t* __restrict__ pair_offsets, int64_t* __restrict__ total_pairs,
+    unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket,
+    int n_blocks) {
+  __shared__ unsigned long long s_warp[kScanBlock / 32];
+  __shared__ unsigned long long s_prefix[2];
+  __shared__ int s_bid;
+  if (threadIdx.x == 0) s_bid = (int)atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int bid = s_bid;
+  const long long i = (long long)bid * kScanBlock + threadIdx.x;
+  long long cnt = 0;
+  if (i < m) cnt = count_pairs_of(rec + i * 12, strategy, tiles_of(width), tiles_of(height));
+  unsigned long long excl = scan_lookback((unsigned long long)cnt, bid, status, s_warp, s_prefix);
+  if (i < m) pair_offsets[i] = (long long)excl;
+  if (bid == n_blocks - 1 && threadIdx.x == 0) {
+    long long p = (long long)(s_prefix[0] + s_prefix[1]);
+    total_pairs[0] = p;
+    pair_offsets[m] = p;
+  }
+}
+
+__global__ void snugbox_kernel(const float* __restrict__ rec, long long m, int width,
+                               int height, double* x_min, double* x_max, double* y_min,
+                               double* y_max, int32_t* tile_rect) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  SplatF64 s = load_splat_f64(rec + i * 12);
+  SnugRect r = snugbox(s, tiles_of(width), tiles_of(height));
+  x_min[i] = r.x_min;
+  x_max[i] = r.x_max;
+  y_min[i] = r.y_min;
+  y_max[i] = r.y_max;
+  tile_rect[4 * i] = (int32_t)r.tx0;
+  tile_rect[4 * i + 1] = (int32_t)r.tx1;
+  tile_rect[4 * i + 2] = (int32_t)r.ty0;
+  tile_rect[4 * i + 3] = (int32_t)r.ty1;
+}
+
+static size_t scan_workspace(long long n) {
+  long long blocks = (n + kScanBlock - 1) / kScanBlock;
+  return 256 + (size_t)blocks * sizeof(unsigned long long);
+}
+
+}  // namespace tsr
+
+using namespace tsr;
+
+extern "C" size_t tsr_preprocess_workspace(int64_t n) { return scan_workspace(n); }
+extern "C" size_t tsr_count_workspace(int64_t m) { return scan_workspace(m); }
+
+extern "C" int tsr_preprocess_fwd(const tsr_gaussians_t* g, const tsr_camera_t* cam,
+                                  int32_t strategy, float* rec, int32_t* source_ids,
+                                  int32_t* row_of_source, int64_t* pair_offsets,
+                                  int64_t* totals, void* workspace, size_t workspace_bytes,
+                                  void* stream) {
+  if (!g || !cam || g->n < 0 || g->n >= TSR_MAX_GAUSSIANS) return TSR_E_INVALID;
+  if (g->sh_coeffs != 1 && g->sh_coeffs != 4 && g->sh_coeffs != 9 && g->sh_coeffs != 16)
+    return TSR_E_INVALID;
+  if (workspace_bytes < scan_workspace(g->n)) return TSR_E_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(totals, 0, 2 * sizeof(int64_t), s) != cudaSuccess) return TSR_E_CUDA;
+  if (cudaMemsetAsync(pair_offsets, 0, sizeof(int64_t), s) != cudaSuccess) return TSR_E_CUDA;
+  if (g->n == 0) return TSR_OK;
+  int blocks = (int)((g->n + kScanBlock - 1) / kScanBlock);
+  if (cudaMemsetAsync(workspace, 0, scan_workspace(g->n), s) != cudaSuccess) return TSR_E_CUDA;
+  unsigned int* ticket = (unsigned int*)workspace;
+  unsigned long long* status = (unsigned long long*)((char*)workspace + 256);
+  preprocess_kernel<<<blocks, kScanBlock, 0, s>>>(*g, *cam, strategy, (float4*)rec, source_ids,
+                                                  row_of_source, pair_offsets, totals, status,
+                                                  ticket, blocks);
+  TSR_CHECK_LAUNCH();
+  return TSR_OK;
+}
+
+extern "C" int tsr_count_pairs(const float* rec, int64_t m, int32_t width, int32_t height,
+                               int32_t strategy, int64_t* pair_offsets, int64_t* total_pairs,
+                               void* workspace, size_t workspace_bytes, void* stream) {
+  if (m < 0 || m >= TSR_MAX_GAUSSIANS || width <= 0 || height <= 0) return TSR_E_INVALID;
+  if (workspace_bytes < scan_workspace(m)) return TSR_E_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(total_pairs, 0, sizeof(int64_t), s) != cudaSuccess) return TSR_E_CUDA;
+  if (cudaMemsetAsync(pair_offsets, 0, sizeof(int64_t), s) != cudaSuccess) return TSR_E_CUDA;
+  if (m == 0) return TSR_OK;
+  int blocks = (int)((m + kScanBlock - 1) / kScanBlock);
+  if (cudaMemsetAsync(workspace, 0, scan_workspace(m), s) != cudaSuccess) return TSR_E_CUDA;
+  count_kernel<<<blocks, kScanBlock, 0, s>>>(rec, m, width, height, strategy, pair_offsets,
+                                             total_pairs,
+                                             (unsigned long long*)((char*)workspace + 256),
+                                             (unsigned int*)workspace, blocks);
+  TSR_CHECK_LAUNCH();
+  return TSR_OK;
+}
+
+extern "C" int tsr_snugboxes(const float* rec, int64_t m, int32_t width, int32_t height,
+                             double* x_min, double* x_max, double* y_min, double* y_max,
+                             int32_t* tile_rect, void* stream) {
+  if (m < 0 || width <= 0 || height <= 0) return TSR_E_INVALID;
+  if (m == 0) return TSR_OK;
+  int blocks = (int)((m + 255) / 256);
+  snugbox_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(rec, m, width, height, x_min, x_max,
+                                                           y_min, y_max, tile_rect);
+  TSR_CHECK_LAUNCH();
+  return TSR_OK;
+}

@@ -1,0 +1,139 @@
+// K3: forward rasterizer (render, forward.py:87-161).
+//
+// One CTA per 16x16 tile, one thread per pixel.  The tile's depth-sorted list
+// is consumed in batches of 256 splats staged in shared memory (3 x float4
+// per splat: mean/opacity, prescaled conic/depth, colour).  Per pixel:
+//   alpha = min(0.99, o exp(-q/2)); blend iff alive && alpha >= 1/255;
+//   C += T alpha c; D += T alpha d; T *= 1 - alpha; n_considered = k+1 while
+//   alive; alive &= T >= 1e-4 AFTER blending (forward.py:125-138).
+// Termination: a warp stops scanning a batch once its 32 pixels are dead
+// (warp-level early exit) and the CTA stops at the next batch boundary once
+// all 256 are dead (forward.py:141-145).
+// Checkpoints (forward.py:139-140): after every 32nd list position the state
+// (T, C, D) is stored for each pixel that consumed that position -- exactly
+// the records the per-Gaussian backward reads (it enters group g of a pixel
+// only when n_considered > 32 g).  Padding records of dead pixels are never
+// written (they are never read).
+#include <cuda_runtime.h>
+
+#include "tsr_common.cuh"
+
+namespace tsr {
+
+struct StagedSplat {
+  float4 geo;  // mx, my, opacity, depth
+  float4 con;  // a', b', c' (prescaled by kQScale), unused
+  float4 col;  // r, g, b, depth
+};
+
+template <bool kCkpt>
+__global__ void __launch_bounds__(256) render_fwd_kernel(
+    const float4* __restrict__ rec, const int32_t* __restrict__ values,
+    const int64_t* __restrict__ offsets, int width, int height, int tiles_x, float bg_r,
+    float bg_g, float bg_b, float* __restrict__ out_color, float* __restrict__ out_depth,
+    float* __restrict__ out_T, int32_t* __restrict__ out_ncontrib,
+    int32_t* __restrict__ out_ncons, float* __restrict__ ckpt,
+    const int64_t* __restrict__ ckpt_base) {
+  __shared__ float4 s_geo[256];
+  __shared__ float4 s_con[256];
+  __shared__ float4 s_col[256];
+
+  const int tile = blockIdx.x;
+  const int tyi = tile / tiles_x, txi = tile - tyi * tiles_x;
+  const int tid = threadIdx.x;
+  const int lx = tid & 15, ly = tid >> 4;
+  const int x = txi * kTile + lx, y = tyi * kTile + ly;
+  const bool inside = x < width && y < height;
+  const float pxf = (float)x + 0.5f, pyf = (float)y + 0.5f;
+  const long long start = offsets[tile], end = offsets[tile + 1];
+  const int n = (int)(end - start);
+  long long rec_base = 0;
+  if (kCkpt) rec_base = ckpt_base[tile];
+
+  float T = 1.f, Cr = 0.f, Cg = 0.f, Cb = 0.f, D = 0.f;
+  int ncontrib = 0, ncons = 0;
+  bool alive = inside;
+
+  for (int b0 = 0; b0 < n; b0 += 256) {
+    if (!__syncthreads_or(alive)) break;
+    const int k = b0 + tid;
+    if (k < n) {
+      const int row = values[start + k];
+      const float4 r0 = rec[3 * row], r1 = rec[3 * row + 1], r2 = rec[3 * row + 2];
+      s_geo[tid] = make_float4(r0.x, r0.y, r1.y, r1.z);
+      s_con[tid] = make_float4(__fmul_rn(r0.z, kQScale), __fmul_rn(r0.w, kQScale),
+                               __fmul_rn(r1.x, kQScale), 0.f);
+      s_col[tid] = make_float4(r2.x, r2.y, r2.z, r1.z);
+    }
+    __syncthreads();
+    const int cnt = min(256, n - b0);
+    for (int j = 0; j < cnt; ++j) {
+      if (!__any_sync(0xffffffffu, alive)) break;  // warp-level early exit
+      const int pos = b0 + j;
+      if (alive) {
+        const float4 g = s_geo[j];
+        const float4 c = s_con[j];
+        AlphaEval e = eval_alpha(pxf, pyf, g.x, g.y, c.x, c.y, c.z, g.z);
+        if (e.alpha >= kMinAlpha) {
+          const float4 col = s_col[j];
+          const float w = T * e.alpha;
+          Cr = fmaf(w, col.x, Cr);
+          Cg = fmaf(w, col.y, Cg);
+          Cb = fmaf(w, col.z, Cb);
+          D = fmaf(w, col.w, D);
+          T = T * (1.f - e.alpha);
+          ++ncontrib;
+        }
+        ncons = pos + 1;
+        alive = T >= kTTerminate;
+        if (kCkpt && ((pos + 1) & (kGroup - 1)) == 0) {
+          float* dst = ckpt + (rec_base + ((pos + 1) >> 5) - 1) * (5 * kTilePixels) + tid;
+          dst[0] = T;
+          dst[kTilePixels] = Cr;
+          dst[2 * kTilePixels] = Cg;
+          dst[3 * kTilePixels] = Cb;
+          dst[4 * kTilePixels] = D;
+        }
+      }
+    }
+  }
+  if (inside) {
+    const long long pix = (long long)y * width + x;
+    out_color[3 * pix] = fmaf(T, bg_r, Cr);
+    out_color[3 * pix + 1] = fmaf(T, bg_g, Cg);
+    out_color[3 * pix + 2] = fmaf(T, bg_b, Cb);
+    out_depth[pix] = D;
+    out_T[pix] = T;
+    out_ncontrib[pix] = ncontrib;
+    out_ncons[pix] = ncons;
+  }
+}
+
+}  // namespace tsr
+
+using namespace tsr;
+
+extern "C" int tsr_render_fwd(const float* rec, const int32_t* values, const int64_t* offsets,
+                              int32_t width, int32_t height, const float* background_host,
+                              float* out_color, float* out_depth, float* out_final_T,
+                              int32_t* out_n_contrib, int32_t* out_n_considered, float* ckpt,
+                              const int64_t* ckpt_base, void* stream) {
+  if (width <= 0 || height <= 0 || !background_host) return TSR_E_INVALID;
+  if (ckpt && !ckpt_base) return TSR_E_INVALID;
+  const int tx = tiles_of(width), ty = tiles_of(height);
+  const int n_tiles = tx * ty;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (ckpt) {
+    render_fwd_kernel<true><<<n_tiles, 256, 0, s>>>(
+        (const float4*)rec, values, offsets, width, height, tx, background_host[0],
+        background_host[1], background_host[2], out_color, out_depth, out_final_T,
+        out_n_contrib, out_n_considered, ckpt, ckpt_base);
+  } else {
+    render_fwd_kernel<false><<<n_tiles, 256, 0, s>>>(
+        (const float4*)rec, values, offsets, width, height, tx, background_host[0],
+        background_host[1], background_host[2], out_color, out_depth, out_final_T,
+        out_n_contrib, out_n_considered, nullptr, nullptr);
+  }
+  TSR_CHECK_LAUNCH();
+  return TSR_OK;
+}

@@ -1,0 +1,301 @@
+// Shared device code for the sm_100a tile rasterizer.
+//
+// Numerics contract:
+//   * tile decisions (SnugBox, column walk, min-q test) are evaluated in FP64
+//     on the FP32 SplatBatch values upcast to FP64, with exactly the operation
+//     order NumPy uses in binning.py:74-222, one rounding per binary op and NO
+//     fused multiply-add (explicit __dmul_rn/__dadd_rn/... intrinsics), so the
+//     (tile, splat) pairs are bit-identical to the float64 reference;
+//   * everything else is FP32.  The alpha of a (pixel, splat) evaluation is
+//     computed by ONE inline function with explicit rounding intrinsics so the
+//     forward and the backward see bit-identical alphas (forward.py:71-84).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/tilesplat_b200.h"
+
+namespace tsr {
+
+constexpr int kTile = 16;
+constexpr int kTilePixels = kTile * kTile;
+constexpr int kGroup = 32;  // CHECKPOINT_INTERVAL (forward.py:28)
+constexpr float kAlphaCap = 0.99f;                 // forward.py:25
+constexpr float kMinAlpha = 1.0f / 255.0f;         // forward.py:26
+constexpr float kTTerminate = 1e-4f;               // forward.py:27
+constexpr float kCovDilation = 0.3f;               // projection.py:26
+constexpr float kMinOpacity = 1.0f / 255.0f;       // projection.py:27
+// conic prescale: exp(-q/2) == exp2(q * kQScale)
+constexpr float kQScale = -0.72134752044448170368f;  // -0.5 * log2(e)
+
+// ------------------------------------------------------------------ FP64 --
+// Explicitly rounded FP64 helpers: the compiler may not contract these.
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double dsqrt(double a) { return __dsqrt_rn(a); }
+// numpy.minimum / maximum propagate NaN; inputs here are finite for valid
+// batches, and we keep NaN-propagation anyway.
+__device__ __forceinline__ double npmin(double a, double b) {
+  return (a != a || b != b) ? (a + b) : (a < b ? a : b);
+}
+__device__ __forceinline__ double npmax(double a, double b) {
+  return (a != a || b != b) ? (a + b) : (a > b ? a : b);
+}
+
+// Splat parameters upcast to FP64 (rows of the FP32 batch).
+struct SplatF64 {
+  double mx, my, a, b, c, t;
+};
+
+__device__ __forceinline__ SplatF64 load_splat_f64(const float* rec) {
+  SplatF64 s;
+  s.mx = (double)rec[0];
+  s.my = (double)rec[1];
+  s.a = (double)rec[2];
+  s.b = (double)rec[3];
+  s.c = (double)rec[4];
+  s.t = (double)rec[7];
+  return s;
+}
+
+// _tile_span (binning.py:74-84): inclusive tile ids of the closed interval.
+__device__ __forceinline__ void tile_span(double lo, double hi, int n_tiles,
+                                          long long& t0, long long& t1) {
+  double c0 = ceil(dsub(ddiv(lo, 16.0), 1.0));
+  double f1 = floor(ddiv(hi, 16.0));
+  long long i0 = (long long)c0;
+  long long i1 = (long long)f1;
+  t0 = i0 > 0 ? i0 : 0;
+  t1 = i1 < (long long)(n_tiles - 1) ? i1 : (long long)(n_tiles - 1);
+}
+
+// compute_snugboxes (binning.py:87-104).
+struct SnugRect {
+  double x_min, x_max, y_min, y_max;
+  long long tx0, tx1, ty0, ty1;
+};
+
+__device__ __forceinline__ SnugRect snugbox(const SplatF64& s, int tiles_x, int tiles_y) {
+  SnugRect r;
+  double det = dsub(dmul(s.a, s.c), dmul(s.b, s.b));
+  double ex = dsqrt(ddiv(dmul(s.c, s.t), det));
+  double ey = dsqrt(ddiv(dmul(s.a, s.t), det));
+  r.x_min = dsub(s.mx, ex);
+  r.x_max = dadd(s.mx, ex);
+  r.y_min = dsub(s.my, ey);
+  r.y_max = dadd(s.my, ey);
+  tile_span(r.x_min, r.x_max, tiles_x, r.tx0, r.tx1);
+  tile_span(r.y_min, r.y_max, tiles_y, r.ty0, r.ty1);
+  return r;
+}
+
+// Row span [ty0, ty1] of column tx from the column walk of bin_sequential
+// (binning.py:186-215).  Returns the number of rows (>= 0).
+__device__ __forceinline__ int column_rows(const SplatF64& s, const SnugRect& r,
+                                           long long tx, int tiles_y,
+                                           long long& ty0, long long& ty1) {
+  double det = dsub(dmul(s.a, s.c), dmul(s.b, s.b));
+  double xl = dsub(npmax((double)(16 * tx), r.x_min), s.mx);
+  double xr = dsub(npmin((double)(16 * tx + 16), r.x_max), s.mx);
+  // y_bounds(dx): rad = sqrt(max(0, (b*b - a*c)*dx*dx + t*c))
+  double bbac = dsub(dmul(s.b, s.b), dmul(s.a, s.c));
+  double tc = dmul(s.t, s.c);
+  double negb = -s.b;
+  double rad_l = dsqrt(npmax(0.0, dadd(dmul(dmul(bbac, xl), xl), tc)));
+  double rad_r = dsqrt(npmax(0.0, dadd(dmul(dmul(bbac, xr), xr), tc)));
+  double lo_l = ddiv(dsub(dmul(negb, xl), rad_l), s.c);
+  double hi_l = ddiv(dadd(dmul(negb, xl), rad_l), s.c);
+  double lo_r = ddiv(dsub(dmul(negb, xr), rad_r), s.c);
+  double hi_r = ddiv(dadd(dmul(negb, xr), rad_r), s.c);
+  double ylo = npmin(lo_l, lo_r);
+  double yhi = npmax(hi_l, hi_r);
+  // global y tangent points
+  double ymax_rel = dsqrt(ddiv(dmul(s.a, s.t), det));
+  double dx_up = dmul(-ddiv(s.b, s.a), ymax_rel);
+  double dx_dn = -dx_up;
+  if (dx_up >= xl && dx_up <= xr) yhi = npmax(yhi, ymax_rel);
+  if (dx_dn >= xl && dx_dn <= xr) ylo = npmin(ylo, -ymax_rel);
+  long long a0, a1;
+  tile_span(dadd(ylo, s.my), dadd(yhi, s.my), tiles_y, a0, a1);
+  ty0 = a0 > r.ty0 ? a0 : r.ty0;
+  ty1 = a1 < r.ty1 ? a1 : r.ty1;
+  long long n = ty1 - ty0 + 1;
+  return n > 0 ? (int)n : 0;
+}
+
+// Total pairs of one splat under bin_sequential.
+__device__ __forceinline__ long long count_sequential(const SplatF64& s, int tiles_x,
+                                                      int tiles_y) {
+  SnugRect r = snugbox(s, tiles_x, tiles_y);
+  long long total = 0;
+  if (r.tx0 > r.tx1 || r.ty0 > r.ty1) return 0;
+  for (long long tx = r.tx0; tx <= r.tx1; ++tx) {
+    long long ty0, ty1;
+    total += column_rows(s, r, tx, tiles_y, ty0, ty1);
+  }
+  return total;
+}
+
+// min_q_box (binning.py:241-259): exact min of the quadratic over a box given
+// relative to the mean; used by the load-balanced strategy.
+__device__ __forceinline__ double min_q_box(const SplatF64& s, double rx0, double rx1,
+                                            double ry0, double ry1) {
+  bool inside = (rx0 <= 0.0) && (0.0 <= rx1) && (ry0 <= 0.0) && (0.0 <= ry1);
+  if (inside) return 0.0;
+  auto q = [&](double dx, double dy) {
+    // a*dx*dx + 2.0*b*dx*dy + c*dy*dy, left to right
+    double t0 = dmul(dmul(s.a, dx), dx);
+    double t1 = dmul(dmul(dmul(2.0, s.b), dx), dy);
+    double t2 = dmul(dmul(s.c, dy), dy);
+    return dadd(dadd(t0, t1), t2);
+  };
+  auto clip = [](double v, double lo, double hi) {
+    // np.clip(v, lo, hi) == minimum(maximum(v, lo), hi)
+    return npmin(npmax(v, lo), hi);
+  };
+  double bc = -ddiv(s.b, s.c);
+  double ba = -ddiv(s.b, s.a);
+  double y_at_x0 = clip(dmul(bc, rx0), ry0, ry1);
+  double y_at_x1 = clip(dmul(bc, rx1), ry0, ry1);
+  double x_at_y0 = clip(dmul(ba, ry0), rx0, rx1);
+  double x_at_y1 = clip(dmul(ba, ry1), rx0, rx1);
+  return npmin(npmin(q(rx0, y_at_x0), q(rx1, y_at_x1)),
+               npmin(q(x_at_y0, ry0), q(x_at_y1, ry1)));
+}
+
+// ------------------------------------------------------------------ FP32 --
+// Alpha of one (pixel, splat) evaluation (splat_alpha, forward.py:71-84) on
+// the prescaled conic (a', b', c') = kQScale * (a, b, c):
+//   u = a'dx + b'dy, v = b'dx + c'dy, q' = dx u + dy v = kQScale * q
+//   gauss = 2^q' = exp(-q/2), raw = o * gauss, alpha = min(0.99, raw).
+// Every op is an explicit intrinsic so forward and backward agree bitwise.
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+struct AlphaEval {
+  float dx, dy, u, v, gauss, raw, alpha;
+};
+
+__device__ __forceinline__ AlphaEval eval_alpha(float px, float py, float mx, float my,
+                                                float a, float b, float c, float o) {
+  AlphaEval e;
+  e.dx = __fsub_rn(px, mx);
+  e.dy = __fsub_rn(py, my);
+  e.u = __fmaf_rn(a, e.dx, __fmul_rn(b, e.dy));
+  e.v = __fmaf_rn(b, e.dx, __fmul_rn(c, e.dy));
+  float qs = __fmaf_rn(e.dx, e.u, __fmul_rn(e.dy, e.v));
+  e.gauss = fast_exp2(qs);
+  e.raw = __fmul_rn(o, e.gauss);
+  e.alpha = fminf(kAlphaCap, e.raw);
+  return e;
+}
+
+// ------------------------------------------------------------------- SH ---
+// Real SH basis (scene.py:186-221); l=0 term is 1 (degree 0 == raw RGB).
+__device__ __forceinline__ void sh_basis(int deg, float x, float y, float z, float* out) {
+  const float C1 = 0.4886025119029199f;
+  const float C2[5] = {1.0925484305920792f, -1.0925484305920792f, 0.31539156525252005f,
+                       -1.0925484305920792f, 0.5462742152960396f};
+  const float C3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.4570457994644658f,
+                       0.3731763325901154f, -0.4570457994644658f, 1.445305721320277f,
+                       -0.5900435899266435f};
+  out[0] = 1.0f;
+  if (deg >= 1) {
+    out[1] = -C1 * y;
+    out[2] = C1 * z;
+    out[3] = -C1 * x;
+  }
+  if (deg >= 2) {
+    float xx = x * x, yy = y * y, zz = z * z;
+    out[4] = C2[0] * x * y;
+    out[5] = C2[1] * y * z;
+    out[6] = C2[2] * (2.f * zz - xx - yy);
+    out[7] = C2[3] * x * z;
+    out[8] = C2[4] * (xx - yy);
+    if (deg >= 3) {
+      out[9] = C3[0] * y * (3.f * xx - yy);
+      out[10] = C3[1] * x * y * z;
+      out[11] = C3[2] * y * (4.f * zz - xx - yy);
+      out[12] = C3[3] * z * (2.f * zz - 3.f * xx - 3.f * yy);
+      out[13] = C3[4] * x * (4.f * zz - xx - yy);
+      out[14] = C3[5] * z * (xx - yy);
+      out[15] = C3[6] * x * (xx - 3.f * yy);
+    }
+  }
+}
+
+// d basis_k / d dir (sh_basis_grad, scene.py:233-276), accumulated against a
+// per-coefficient weight wk: returns sum_k wk * d basis_k / d dir.
+__device__ __forceinline__ void sh_basis_vjp(int deg, float x, float y, float z,
+                                             const float* wk, float* gdir) {
+  const float C1 = 0.4886025119029199f;
+  const float C2[5] = {1.0925484305920792f, -1.0925484305920792f, 0.31539156525252005f,
+                       -1.0925484305920792f, 0.5462742152960396f};
+  const float C3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.4570457994644658f,
+                       0.3731763325901154f, -0.4570457994644658f, 1.445305721320277f,
+                       -0.5900435899266435f};
+  float gx = 0.f, gy = 0.f, gz = 0.f;
+  if (deg >= 1) {
+    gy += -C1 * wk[1];
+    gz += C1 * wk[2];
+    gx += -C1 * wk[3];
+  }
+  if (deg >= 2) {
+    gx += C2[0] * y * wk[4];
+    gy += C2[0] * x * wk[4];
+    gy += C2[1] * z * wk[5];
+    gz += C2[1] * y * wk[5];
+    gx += C2[2] * (-2.f * x) * wk[6];
+    gy += C2[2] * (-2.f * y) * wk[6];
+    gz += C2[2] * (4.f * z) * wk[6];
+    gx += C2[3] * z * wk[7];
+    gz += C2[3] * x * wk[7];
+    gx += C2[4] * (2.f * x) * wk[8];
+    gy += C2[4] * (-2.f * y) * wk[8];
+  }
+  if (deg >= 3) {
+    float xx = x * x, yy = y * y, zz = z * z;
+    gx += C3[0] * 6.f * x * y * wk[9];
+    gy += C3[0] * 3.f * (xx - yy) * wk[9];
+    gx += C3[1] * y * z * wk[10];
+    gy += C3[1] * x * z * wk[10];
+    gz += C3[1] * x * y * wk[10];
+    gx += C3[2] * (-2.f * x * y) * wk[11];
+    gy += C3[2] * (4.f * zz - xx - 3.f * yy) * wk[11];
+    gz += C3[2] * 8.f * y * z * wk[11];
+    gx += C3[3] * (-6.f * x * z) * wk[12];
+    gy += C3[3] * (-6.f * y * z) * wk[12];
+    gz += C3[3] * (6.f * zz - 3.f * xx - 3.f * yy) * wk[12];
+    gx += C3[4] * (4.f * zz - 3.f * xx - yy) * wk[13];
+    gy += C3[4] * (-2.f * x * y) * wk[13];
+    gz += C3[4] * 8.f * x * z * wk[13];
+    gx += C3[5] * 2.f * x * z * wk[14];
+    gy += C3[5] * (-2.f * y * z) * wk[14];
+    gz += C3[5] * (xx - yy) * wk[14];
+    gx += C3[6] * 3.f * (xx - yy) * wk[15];
+    gy += C3[6] * (-6.f * x * y) * wk[15];
+  }
+  gdir[0] = gx;
+  gdir[1] = gy;
+  gdir[2] = gz;
+}
+
+__host__ __device__ inline int sh_degree_of(int coeffs) {
+  return coeffs >= 16 ? 3 : coeffs >= 9 ? 2 : coeffs >= 4 ? 1 : 0;
+}
+
+// --------------------------------------------------------------- errors ---
+#define TSR_CHECK_LAUNCH()                                   \
+  do {                                                       \
+    cudaError_t _e = cudaGetLastError();                     \
+    if (_e != cudaSuccess) return TSR_E_CUDA;                \
+  } while (0)
+
+__host__ __device__ inline int tiles_of(int px) { return (px + kTile - 1) / kTile; }
+
+}  // namespace tsr

@@ -1,0 +1,130 @@
+"""Tile rasterizer forward on the B200 (reference: tilesplat/forward.py).
+
+`render` launches K3 (csrc/render.cu).  Checkpoints are one flat FP32 buffer:
+record r of tile t is the (T, Cr, Cg, Cb, D) state after list position
+32(r+1)-1, stored at ckpt[ckpt_base[t] + r] as a (5, 256) plane (forward.py:
+139-140), written for every pixel that consumed that position.  The
+reference's padding records for already-terminated pixels are never written
+because the backward never reads them (it enters group g of a pixel only if
+n_considered > 32 g); `checkpoints_dict()` materialises the reference's
+{tile: (G, 5, th, tw)} view for inspection.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .binning import TileIndex
+from .projection import MIN_OPACITY, SplatBatch
+from .scene import TILE, _device
+
+ALPHA_CAP = 0.99
+MIN_ALPHA = MIN_OPACITY
+T_TERMINATE = 1e-4
+CHECKPOINT_INTERVAL = 32
+
+
+@dataclass
+class RenderBuffers:
+    color: torch.Tensor        # (H, W, 3), background composited in
+    depth: torch.Tensor        # (H, W)
+    final_T: torch.Tensor      # (H, W)
+    n_contrib: torch.Tensor    # (H, W) int32
+    n_considered: torch.Tensor # (H, W) int32
+    background: np.ndarray
+    ckpt: torch.Tensor | None = None       # flat checkpoint records
+    ckpt_base: torch.Tensor | None = None  # (T+1,) record base per tile
+    tiles_x: int = 0
+    tiles_y: int = 0
+    _ckpt_dict: dict | None = field(default=None, repr=False)
+
+    @property
+    def has_checkpoints(self) -> bool:
+        return self.ckpt is not None
+
+    def normalized_depth(self) -> torch.Tensor:
+        """Depth / (1 - final_T) where anything blended (forward.py:44-50)."""
+        mask = self.n_contrib > 0
+        denom = torch.where(mask, 1.0 - self.final_T, torch.ones_like(self.final_T))
+        return torch.where(mask, self.depth / denom, torch.zeros_like(self.depth))
+
+    def checkpoints_dict(self, tiles: TileIndex) -> dict:
+        """{tile: (G, 5, th, tw)} like the reference (entries of pixels that did
+        not reach a record's position are unspecified)."""
+        if self.ckpt is None:
+            return {}
+        out = {}
+        base = self.ckpt_base.cpu().numpy()
+        offs = tiles.offsets.cpu().numpy()
+        H, W = self.color.shape[:2]
+        flat = self.ckpt.view(-1, 5, TILE, TILE)
+        for t in range(tiles.n_tiles):
+            g = int(offs[t + 1] - offs[t]) // CHECKPOINT_INTERVAL
+            if g == 0:
+                continue
+            ty, tx = divmod(t, tiles.tiles_x)
+            th = min(TILE, H - ty * TILE)
+            tw = min(TILE, W - tx * TILE)
+            out[t] = flat[int(base[t]): int(base[t]) + g, :, :th, :tw]
+        return out
+
+    @property
+    def checkpoints(self) -> dict:
+        raise AttributeError("use checkpoints_dict(tiles): device checkpoints are a flat buffer")
+
+
+def tile_window(tile_id: int, tiles_x: int, width: int, height: int):
+    """Pixel bounds of one tile (forward.py:61-68)."""
+    ty, tx = divmod(tile_id, tiles_x)
+    x0, y0 = tx * TILE, ty * TILE
+    return x0, y0, min(x0 + TILE, width), min(y0 + TILE, height)
+
+
+def _ensure_colors(batch: SplatBatch, colors) -> None:
+    """The raster record carries RGB at rec[:, 8:11]; copy caller colours in
+    unless they already are that view."""
+    if isinstance(colors, torch.Tensor) and colors.is_cuda:
+        rc = batch.rec[:, 8:11]
+        if colors.data_ptr() == rc.data_ptr() and colors.stride() == rc.stride():
+            return
+    if len(batch) == 0:
+        return
+    batch.rec[:, 8:11] = torch.as_tensor(np.asarray(colors, dtype=np.float32)
+                                         if not isinstance(colors, torch.Tensor) else colors,
+                                         device=batch.rec.device).reshape(-1, 3).float()
+
+
+def render(batch: SplatBatch, tiles: TileIndex, colors, background, *,
+           record_checkpoints: bool = True, scoring: bool = False):
+    """K3 forward (forward.py:87-161)."""
+    if scoring:
+        raise NotImplementedError("scoring mode (density, SURVEY §8(f) #2) is not built yet")
+    lib = _lib.load()
+    _ensure_colors(batch, colors)
+    H, W = batch.height, batch.width
+    dev = _device()
+    bg = np.asarray(background, dtype=np.float64).reshape(3)
+    color = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
+    depth = torch.empty((H, W), dtype=torch.float32, device=dev)
+    final_T = torch.empty((H, W), dtype=torch.float32, device=dev)
+    n_contrib = torch.empty((H, W), dtype=torch.int32, device=dev)
+    n_cons = torch.empty((H, W), dtype=torch.int32, device=dev)
+    ckpt = None
+    if record_checkpoints:
+        # sum_t floor(n_t / 32) <= P / 32 records of 5 x 256 floats
+        records = tiles.n_pairs // CHECKPOINT_INTERVAL + 1
+        ckpt = torch.empty(records * 5 * TILE * TILE, dtype=torch.float32, device=dev)
+    bg_host = (_lib.c_f32 * 3)(*[float(v) for v in bg])
+    _lib.check(lib.tsr_render_fwd(
+        batch.rec.data_ptr(), _lib.ptr(tiles.values) if tiles.n_pairs else None,
+        tiles.offsets.data_ptr(), W, H, bg_host, color.data_ptr(), depth.data_ptr(),
+        final_T.data_ptr(), n_contrib.data_ptr(), n_cons.data_ptr(), _lib.ptr(ckpt),
+        _lib.ptr(tiles.ckpt_base) if ckpt is not None else None, _lib.stream_handle()),
+        "tsr_render_fwd")
+    return RenderBuffers(color, depth, final_T, n_contrib, n_cons, bg, ckpt,
+                         tiles.ckpt_base if ckpt is not None else None,
+                         tiles.tiles_x, tiles.tiles_y)

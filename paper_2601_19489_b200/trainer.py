@@ -1,0 +1,211 @@
+"""Training-step glue on the B200 (reference: tilesplat/trainer.py:181-257).
+
+`render_view`, `view_loss_and_grads` and `_full_grads` keep the reference's
+names and return types.  `TrainStep` is the hot path the benchmark times: one
+view through K1 (project+count) -> K2 (duplicate, sort, ranges) -> K3 render
+-> loss -> K4 backward -> K4b+K5 fused projection-VJP + Adam, with a single
+host read of the pair count (P sizes the key buffers).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib, losses
+from .backward import Grad2D, backward_per_gaussian, backward_per_gaussian_raw
+from .binning import TileIndex, build_index
+from .forward import RenderBuffers, render
+from .optim import Adam, position_lr
+from .pose import PoseDelta
+from .projection import (SplatBatch, _pose_grad_from_sums, batch_from_scratch, camera_struct,
+                         gaussians_struct, project, project_raw, project_vjp)
+from .scene import Camera, GaussianSet, _device, as_device_f32
+
+_PROFILE_DEFAULTS = {
+    "round1": {"max_iters": 6000, "pose_opt": True, "depth_supervision": False},
+    "round2": {"max_iters": 15000, "pose_opt": False, "depth_supervision": True},
+}
+
+
+@dataclass
+class TrainConfig:
+    """Hot-path subset of the reference TrainConfig (trainer.py:42-113), same
+    names and defaults."""
+    round_profile: str = "round2"
+    max_iters: int | None = None
+    pose_opt: bool | None = None
+    depth_supervision: bool | None = None
+    lambda_: float = 0.2
+    depth_weight0: float = 0.1
+    sh_degree: int = 0
+    background: tuple = (0.0, 0.0, 0.0)
+    near: float = 0.01
+    seed: int = 0
+    binning_strategy: str = "sequential"  # sequential | load_balanced
+    backward_path: str = "per_gaussian"
+    lrs: dict = field(default_factory=dict)
+
+    def __post_init__(self):
+        if self.round_profile not in _PROFILE_DEFAULTS:
+            raise ValueError(f"unknown round_profile {self.round_profile!r}")
+        prof = _PROFILE_DEFAULTS[self.round_profile]
+        if self.max_iters is None:
+            self.max_iters = prof["max_iters"]
+        if self.pose_opt is None:
+            self.pose_opt = prof["pose_opt"]
+        if self.depth_supervision is None:
+            self.depth_supervision = prof["depth_supervision"]
+        if self.binning_strategy not in ("sequential", "load_balanced"):
+            raise ValueError(f"unknown binning_strategy {self.binning_strategy!r}")
+        if self.backward_path != "per_gaussian":
+            raise ValueError("only the per-Gaussian backward is built for the GPU "
+                             "(backward_per_pixel is the CPU oracle)")
+
+    @property
+    def strategy_id(self) -> int:
+        return 1 if self.binning_strategy == "load_balanced" else 0
+
+
+@dataclass
+class ViewRender:
+    batch: SplatBatch
+    tiles: TileIndex
+    colors: torch.Tensor
+    dirs: object
+    buffers: RenderBuffers
+    contributions: object = None
+
+
+def render_view(gset: GaussianSet, camera: Camera, cfg: TrainConfig,
+                delta: PoseDelta | None = None, *, checkpoints: bool = True,
+                scoring: bool = False) -> ViewRender:
+    """project -> bin -> colours -> render (trainer.py:181-192)."""
+    batch = project(gset, camera, near=cfg.near, delta=delta, strategy=cfg.strategy_id)
+    tiles = build_index(batch, cfg.strategy_id, batch.n_pairs, batch.pair_offsets)
+    colors = batch.colors
+    bufs = render(batch, tiles, colors, cfg.background, record_checkpoints=checkpoints,
+                  scoring=scoring)
+    return ViewRender(batch, tiles, colors, None, bufs)
+
+
+def view_loss_and_grads(camera: Camera, cfg: TrainConfig, vr: ViewRender,
+                        depth_weight: float):
+    """Photometric (+ disparity) loss and the raster backward (trainer.py:195-228)."""
+    bufs = vr.buffers
+    report, grad_color = losses.photometric(bufs.color, camera.gt_image, cfg.lambda_)
+    grad_depth = grad_final_T = None
+    depth_loss = 0.0
+    if depth_weight > 0.0 and camera.depth_prior is not None:
+        mask = bufs.n_contrib > 0
+        if camera.depth_valid is not None:
+            mask &= torch.as_tensor(camera.depth_valid, device=mask.device).bool()
+        d_norm = bufs.normalized_depth()
+        depth_loss, g_dnorm = losses.disparity_loss(d_norm, camera.depth_prior, mask,
+                                                    depth_weight)
+        denom = 1.0 - bufs.final_T
+        one = torch.ones_like(denom)
+        grad_depth = torch.where(mask, g_dnorm / torch.where(mask, denom, one),
+                                 torch.zeros_like(denom))
+        grad_final_T = torch.where(mask, g_dnorm * bufs.depth / torch.where(mask, denom ** 2, one),
+                                   torch.zeros_like(denom))
+    g2 = backward_per_gaussian(bufs, vr.batch, vr.tiles, vr.colors, grad_color, grad_depth,
+                               grad_final_T)
+    report = losses.LossReport(l1=report.l1, ssim=report.ssim, photometric=report.photometric,
+                               depth_loss=depth_loss, total=report.photometric + depth_loss,
+                               lambda_=cfg.lambda_, depth_weight=depth_weight)
+    return report, g2
+
+
+def _full_grads(gset: GaussianSet, camera: Camera, cfg: TrainConfig, delta, vr: ViewRender,
+                g2: Grad2D) -> dict:
+    """project_vjp + colour chain, keyed like the optimizer groups (trainer.py:231-257)."""
+    gcol = torch.empty_like(gset.colors)
+    g3, gpose = project_vjp(gset, camera, vr.batch, g2, near=cfg.near, delta=delta,
+                            grad_colors=gcol)
+    return {"positions": g3.positions, "log_scales": g3.log_scales,
+            "rotations": g3.rotations, "opacity_logits": g3.opacity_logits,
+            "colors": gcol, "pose_rot": gpose.rot_vec, "pose_trans": gpose.trans}
+
+
+class TrainStep:
+    """One-view training step on the device (fwd + loss + bwd + Adam).
+
+    Hot path for BASELINE.json's metric; the reference's per-step sequence is
+    trainer.py:329-345.  Positions use the decaying lr (position_lr) exactly as
+    the reference loop does; pose optimisation is off (round2 profile)."""
+
+    def __init__(self, gset: GaussianSet, cfg: TrainConfig, extent: float = 4.0,
+                 optimizer: Adam | None = None):
+        self.gset = gset
+        self.cfg = cfg
+        self.opt = optimizer or Adam({k: v for k, v in cfg.lrs.items() if k != "positions"})
+        self.pos_base_lr = cfg.lrs.get("positions", 1.6e-4 * extent)
+        self.iteration = 0
+        self.scratch = None
+        dev = _device()
+        self.skipped = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.merges = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.grad2d = None
+        self.lib = _lib.load()
+
+    @staticmethod
+    def _mark(timer, name):
+        if timer is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            timer.setdefault("_events", []).append((name, ev))
+
+    def forward(self, camera: Camera, timer=None):
+        self._mark(timer, "start")
+        s = project_raw(self.gset, camera, self.cfg.near, None, self.cfg.strategy_id,
+                        self.scratch)
+        self.scratch = s
+        self._mark(timer, "preprocess")
+        batch = batch_from_scratch(s, camera, self.cfg.strategy_id)  # host read of (M, P)
+        tiles = build_index(batch, self.cfg.strategy_id, batch.n_pairs, batch.pair_offsets)
+        self._mark(timer, "binning")
+        bufs = render(batch, tiles, batch.colors, self.cfg.background, record_checkpoints=True)
+        self._mark(timer, "render")
+        return batch, tiles, bufs
+
+    def loss_and_backward(self, batch, tiles, bufs, gt_image, timer=None):
+        e, l1, s, grad_color = losses.photometric_device(bufs.color, gt_image, self.cfg.lambda_)
+        self._mark(timer, "loss")
+        m = len(batch)
+        if self.grad2d is None or self.grad2d.shape[0] < max(m, 1):
+            self.grad2d = torch.empty((max(len(self.gset), 1), _lib.GRAD2D_FLOATS),
+                                      dtype=torch.float32, device=bufs.color.device)
+        g2 = self.grad2d[:m]
+        g2.zero_()
+        backward_per_gaussian_raw(bufs, batch, tiles, grad_color, out=g2, merges=self.merges)
+        self._mark(timer, "backward")
+        return e, g2
+
+    def step(self, camera: Camera, gt_image: torch.Tensor, timer=None) -> torch.Tensor:
+        """Run one step; returns the loss as a device scalar (no extra sync)."""
+        self.iteration += 1
+        batch, tiles, bufs = self.forward(camera, timer)
+        e, g2 = self.loss_and_backward(batch, tiles, bufs, gt_image, timer)
+        lr = {"positions": position_lr(self.pos_base_lr, self.iteration, self.cfg.max_iters)}
+        groups = self.opt.groups_for_fused(self.gset.params(), lr)
+        _lib.check(self.lib.tsr_preprocess_bwd_adam(
+            gaussians_struct(self.gset), camera_struct(camera, None, self.cfg.near),
+            batch.rec.data_ptr(), batch.row_of_source.data_ptr(), g2.data_ptr(), groups, None,
+            self.skipped.data_ptr(), _lib.stream_handle()), "tsr_preprocess_bwd_adam")
+        self._mark(timer, "vjp_adam")
+        self.last = (batch, tiles, bufs)
+        return e
+
+
+def phase_times(timer) -> dict:
+    """Per-phase device milliseconds summed over the recorded steps."""
+    out = {}
+    evs = timer.get("_events", [])
+    for (_, a), (name, b) in zip(evs, evs[1:]):
+        if name == "start":
+            continue
+        out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+    return out
