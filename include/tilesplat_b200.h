@@ -193,6 +193,15 @@ int tsr_preprocess_bwd_adam(const tsr_gaussians_t* g, const tsr_camera_t* cam,
                             float* pose_sums, unsigned long long* skipped,
                             void* stream);
 
+/* --------------------------------------------------------------- loss ----
+ * Fused photometric objective (losses.py:44-91): E = (1-lam) mean|r-g| +
+ * lam (1 - SSIM), 11-tap sigma=1.5 Gaussian window, zero padding.  rendered,
+ * gt, grad are (H, W, 3) FP32; out3 (device) = {E, l1, ssim}. */
+size_t tsr_photometric_workspace(int32_t height, int32_t width);
+int tsr_photometric(const float* rendered, const float* gt, int32_t height, int32_t width,
+                    float lam, float* grad, float* out3, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
 /* Version / build string (for smoke checks). */
 const char* tsr_version(void);
 

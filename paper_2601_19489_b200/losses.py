@@ -1,10 +1,10 @@
 """Photometric / depth objectives with analytic gradients (reference:
-tilesplat/losses.py).  Round-1 implementation in device torch ops (SURVEY.md
-§2 row 7: on the training step, not one of the five kernels; the fused loss
-kernel is §8(f) next #1).
+tilesplat/losses.py).
 
-E = (1 - lam) mean|r - g| + lam (1 - SSIM), SSIM with the 11-tap sigma=1.5
-Gaussian window, zero padding, C1 = 0.01^2, C2 = 0.03^2 (losses.py:17-70).
+The photometric objective E = (1 - lam) mean|r - g| + lam (1 - SSIM) and its
+gradient run in one fused CUDA pipeline (csrc/loss.cu):
+11-tap sigma=1.5 Gaussian window, zero padding, C1 = 0.01^2, C2 = 0.03^2
+(losses.py:17-91).
 """
 
 from __future__ import annotations
@@ -13,24 +13,13 @@ from dataclasses import dataclass
 
 import numpy as np
 import torch
-import torch.nn.functional as F
 
+from . import _lib
 from .scene import as_device_f32
 
 SSIM_C1 = 0.01 ** 2
 SSIM_C2 = 0.03 ** 2
 DISPARITY_EPS = 1e-4
-
-_WIN = np.exp(-((np.arange(11) - 5.0) ** 2) / (2.0 * 1.5 ** 2))
-_WIN /= _WIN.sum()
-_win_cache: dict = {}
-
-
-def _window(device):
-    key = (device.type, device.index)
-    if key not in _win_cache:
-        _win_cache[key] = torch.tensor(_WIN, dtype=torch.float32, device=device)
-    return _win_cache[key]
 
 
 @dataclass
@@ -44,58 +33,47 @@ class LossReport:
     depth_weight: float = 0.0
 
 
-def _filter(img: torch.Tensor) -> torch.Tensor:
-    """Separable zero-padded Gaussian filter over H, W of a (C, H, W) stack."""
-    w = _window(img.device)
-    c = img.shape[0]
-    x = img.unsqueeze(0)
-    x = F.conv2d(x, w.view(1, 1, 11, 1).expand(c, 1, 11, 1), padding=(5, 0), groups=c)
-    x = F.conv2d(x, w.view(1, 1, 1, 11).expand(c, 1, 1, 11), padding=(0, 5), groups=c)
-    return x[0]
+class PhotometricWorkspace:
+    """Scratch for the fused loss (planar SSIM backward sources + partials)."""
+
+    def __init__(self):
+        self.buf = None
+        self.key = None
+
+    def get(self, h: int, w: int, device) -> torch.Tensor:
+        if self.key != (h, w, device):
+            n = int(_lib.load().tsr_photometric_workspace(h, w))
+            self.buf = torch.empty(n, dtype=torch.uint8, device=device)
+            self.key = (h, w, device)
+        return self.buf
 
 
-def ssim_device(img1: torch.Tensor, img2: torch.Tensor):
-    """Mean SSIM of (H, W, C) images and its gradient w.r.t. img1 (losses.py:44-70),
-    as device tensors."""
-    a = img1.permute(2, 0, 1)
-    b = img2.permute(2, 0, 1)
-    stack = torch.cat([a, b, a * a, b * b, a * b], 0)
-    f = _filter(stack)
-    c = a.shape[0]
-    mu1, mu2, v1, v2, v12 = f[:c], f[c:2 * c], f[2 * c:3 * c], f[3 * c:4 * c], f[4 * c:]
-    s1 = v1 - mu1 * mu1
-    s2 = v2 - mu2 * mu2
-    s12 = v12 - mu1 * mu2
-    A1 = 2.0 * mu1 * mu2 + SSIM_C1
-    A2 = 2.0 * s12 + SSIM_C2
-    B1 = mu1 * mu1 + mu2 * mu2 + SSIM_C1
-    B2 = s1 + s2 + SSIM_C2
-    smap = (A1 * A2) / (B1 * B2)
-    value = smap.mean()
-    g = 1.0 / smap.numel()
-    dA1 = g * A2 / (B1 * B2)
-    dA2 = g * A1 / (B1 * B2)
-    dB1 = -g * A1 * A2 / (B1 * B1 * B2)
-    dB2 = -g * A1 * A2 / (B1 * B2 * B2)
-    g_mu1 = 2.0 * mu2 * (dA1 - dA2) + 2.0 * mu1 * (dB1 - dB2)
-    back = _filter(torch.cat([g_mu1, dB2, 2.0 * dA2], 0))
-    grad = back[:c] + back[c:2 * c] * 2.0 * a + back[2 * c:] * b
-    return value, grad.permute(1, 2, 0)
+_default_ws = PhotometricWorkspace()
 
 
-def photometric_device(rendered: torch.Tensor, gt: torch.Tensor, lam: float = 0.2):
-    """(E, l1, ssim, dE/drendered) as device tensors; no host synchronisation."""
+def photometric_device(rendered: torch.Tensor, gt: torch.Tensor, lam: float = 0.2,
+                       grad: torch.Tensor | None = None,
+                       workspace: PhotometricWorkspace | None = None):
+    """(E, l1, ssim, dE/drendered): E/l1/ssim are 0-d device tensors; no host
+    synchronisation."""
     if rendered.shape != gt.shape:
         raise ValueError(f"shape mismatch: {tuple(rendered.shape)} vs {tuple(gt.shape)}")
     if not 0.0 <= lam <= 1.0:
         raise ValueError("lambda must be in [0, 1]")
-    diff = rendered - gt
-    l1 = diff.abs().mean()
-    grad_l1 = torch.sign(diff) / diff.numel()
-    s, gs = ssim_device(rendered, gt)
-    e = (1.0 - lam) * l1 + lam * (1.0 - s)
-    grad = (1.0 - lam) * grad_l1 - lam * gs
-    return e, l1, s, grad
+    if rendered.dim() != 3 or rendered.shape[2] != 3:
+        raise ValueError("images must be (H, W, 3)")
+    lib = _lib.load()
+    r = rendered.contiguous()
+    g = gt.contiguous()
+    h, w = int(r.shape[0]), int(r.shape[1])
+    if grad is None:
+        grad = torch.empty_like(r)
+    out = torch.empty(3, dtype=torch.float32, device=r.device)
+    ws = (workspace or _default_ws).get(h, w, r.device)
+    _lib.check(lib.tsr_photometric(r.data_ptr(), g.data_ptr(), h, w, float(lam), grad.data_ptr(),
+                                   out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                   _lib.stream_handle()), "tsr_photometric")
+    return out[0], out[1], out[2], grad
 
 
 def photometric(rendered, gt, lam: float = 0.2):
