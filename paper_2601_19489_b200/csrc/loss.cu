@@ -224,9 +224,14 @@ static Win make_window() {
 
 using namespace tsr;
 
+static size_t q_bytes(int32_t height, int32_t width) {
+  // planar SSIM sources, rounded up so the double partials stay 256-B aligned
+  return ((9 * (size_t)height * width * sizeof(float)) + 255) & ~(size_t)255;
+}
+
 extern "C" size_t tsr_photometric_workspace(int32_t height, int32_t width) {
   const size_t tiles = (size_t)((width + kLT - 1) / kLT) * ((height + kLT - 1) / kLT);
-  return 9 * (size_t)height * width * sizeof(float) + tiles * 2 * sizeof(double) + 256;
+  return q_bytes(height, width) + tiles * 2 * sizeof(double) + 256;
 }
 
 extern "C" int tsr_photometric(const float* rendered, const float* gt, int32_t height,
@@ -240,7 +245,7 @@ extern "C" int tsr_photometric(const float* rendered, const float* gt, int32_t h
   dim3 grid((width + kLT - 1) / kLT, (height + kLT - 1) / kLT);
   const int n_blocks = grid.x * grid.y;
   float* Q = (float*)workspace;
-  double* partials = (double*)((char*)workspace + 9 * (size_t)height * width * sizeof(float));
+  double* partials = (double*)((char*)workspace + q_bytes(height, width));
   const double n = 3.0 * (double)height * width;
   ssim_fwd_kernel<<<grid, 256, 0, s>>>(rendered, gt, height, width, (float)(1.0 / n), Q,
                                        partials, win);

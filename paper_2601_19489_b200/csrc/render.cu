@@ -20,11 +20,25 @@
 
 namespace tsr {
 
-struct StagedSplat {
-  float4 geo;  // mx, my, opacity, depth
-  float4 con;  // a', b', c' (prescaled by kQScale), unused
-  float4 col;  // r, g, b, depth
-};
+
+// One list entry for one pixel, branch-free (predicated): the warp executes
+// it in lockstep, so a per-lane branch would only add reconvergence cost.
+__device__ __forceinline__ void blend_one(const float4 g, const float4 c, const float4 col,
+                                          float pxf, float pyf, int pos, bool& alive, float& T,
+                                          float& Cr, float& Cg, float& Cb, float& D,
+                                          int& ncontrib, int& ncons) {
+  AlphaEval e = eval_alpha(pxf, pyf, g.x, g.y, c.x, c.y, c.z, g.z);
+  const bool blend = alive && (e.alpha >= kMinAlpha);
+  const float w = blend ? T * e.alpha : 0.f;
+  Cr = fmaf(w, col.x, Cr);
+  Cg = fmaf(w, col.y, Cg);
+  Cb = fmaf(w, col.z, Cb);
+  D = fmaf(w, col.w, D);
+  T = blend ? T * (1.f - e.alpha) : T;
+  ncontrib += blend ? 1 : 0;
+  ncons = alive ? pos + 1 : ncons;
+  alive = alive && (T >= kTTerminate);
+}
 
 template <bool kCkpt>
 __global__ void __launch_bounds__(256) render_fwd_kernel(
@@ -47,8 +61,8 @@ __global__ void __launch_bounds__(256) render_fwd_kernel(
   const float pxf = (float)x + 0.5f, pyf = (float)y + 0.5f;
   const long long start = offsets[tile], end = offsets[tile + 1];
   const int n = (int)(end - start);
-  long long rec_base = 0;
-  if (kCkpt) rec_base = ckpt_base[tile];
+  float* ck = nullptr;
+  if (kCkpt) ck = ckpt + ckpt_base[tile] * (5 * kTilePixels) + tid;
 
   float T = 1.f, Cr = 0.f, Cg = 0.f, Cb = 0.f, D = 0.f;
   int ncontrib = 0, ncons = 0;
@@ -59,7 +73,8 @@ __global__ void __launch_bounds__(256) render_fwd_kernel(
     const int k = b0 + tid;
     if (k < n) {
       const int row = values[start + k];
-      const float4 r0 = rec[3 * row], r1 = rec[3 * row + 1], r2 = rec[3 * row + 2];
+      const float4 r0 = __ldg(rec + 3 * row), r1 = __ldg(rec + 3 * row + 1),
+                   r2 = __ldg(rec + 3 * row + 2);
       s_geo[tid] = make_float4(r0.x, r0.y, r1.y, r1.z);
       s_con[tid] = make_float4(__fmul_rn(r0.z, kQScale), __fmul_rn(r0.w, kQScale),
                                __fmul_rn(r1.x, kQScale), 0.f);
@@ -67,33 +82,29 @@ __global__ void __launch_bounds__(256) render_fwd_kernel(
     }
     __syncthreads();
     const int cnt = min(256, n - b0);
-    for (int j = 0; j < cnt; ++j) {
+    // chunks of 32 list positions == one checkpoint interval
+    for (int c0 = 0; c0 < cnt; c0 += kGroup) {
       if (!__any_sync(0xffffffffu, alive)) break;  // warp-level early exit
-      const int pos = b0 + j;
-      if (alive) {
-        const float4 g = s_geo[j];
-        const float4 c = s_con[j];
-        AlphaEval e = eval_alpha(pxf, pyf, g.x, g.y, c.x, c.y, c.z, g.z);
-        if (e.alpha >= kMinAlpha) {
-          const float4 col = s_col[j];
-          const float w = T * e.alpha;
-          Cr = fmaf(w, col.x, Cr);
-          Cg = fmaf(w, col.y, Cg);
-          Cb = fmaf(w, col.z, Cb);
-          D = fmaf(w, col.w, D);
-          T = T * (1.f - e.alpha);
-          ++ncontrib;
-        }
-        ncons = pos + 1;
-        alive = T >= kTTerminate;
-        if (kCkpt && ((pos + 1) & (kGroup - 1)) == 0) {
-          float* dst = ckpt + (rec_base + ((pos + 1) >> 5) - 1) * (5 * kTilePixels) + tid;
+      const int cend = min(kGroup, cnt - c0);
+      const int pos0 = b0 + c0;
+      if (cend == kGroup) {
+#pragma unroll 8
+        for (int j = 0; j < kGroup; ++j)
+          blend_one(s_geo[c0 + j], s_con[c0 + j], s_col[c0 + j], pxf, pyf, pos0 + j, alive, T,
+                    Cr, Cg, Cb, D, ncontrib, ncons);
+        if (kCkpt && ncons == pos0 + kGroup) {
+          // state after list position pos0+31 -> record (pos0+32)/32 - 1
+          float* dst = ck + (long long)(pos0 >> 5) * (5 * kTilePixels);
           dst[0] = T;
           dst[kTilePixels] = Cr;
           dst[2 * kTilePixels] = Cg;
           dst[3 * kTilePixels] = Cb;
           dst[4 * kTilePixels] = D;
         }
+      } else {
+        for (int j = 0; j < cend; ++j)
+          blend_one(s_geo[c0 + j], s_con[c0 + j], s_col[c0 + j], pxf, pyf, pos0 + j, alive, T,
+                    Cr, Cg, Cb, D, ncontrib, ncons);
       }
     }
   }
