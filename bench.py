@@ -352,7 +352,7 @@ def gpu_arm(args):
     value = world * 1e3 / ms
 
     # work counters of the last step (for the roofline), outside the timed region
-    batch, tiles, bufs = stepper.last
+    batch, tiles, bufs = stepper.last_view()
     evals = int(bufs.n_considered.sum().item())
     blends = int(bufs.n_contrib.sum().item())
     pairs = tiles.n_pairs

@@ -74,23 +74,24 @@ typedef struct {
  * project + _splat_colors + compute_snugboxes + exact per-splat pair count
  * (projection.py:77-136, trainer.py:170-178, binning.py:87-104,166-215).
  * One pass: culled rows are compacted in source order by a single-pass
- * decoupled look-back scan that also produces splat-major pair offsets.
- * Outputs (capacity N rows): rec, source_ids, row_of_source (-1 if culled),
- * pair_offsets[M+1]; totals[0] = M, totals[1] = P (device).
+ * decoupled look-back scan.  Outputs (capacity N rows): rec, source_ids,
+ * row_of_source (-1 if culled), counts[M] (pairs per row), depth_bits[M]
+ * (f32 depth bits, binning.py:137-139), spans[M] (16-byte compact column
+ * walk, see sort.cu), totals[0] = M, totals[1] = P (device).
  * strategy: 0 = bin_sequential column walk, 1 = bin_load_balanced min-q test
  * (both yield the same pair multiset). */
 size_t tsr_preprocess_workspace(int64_t n);
-int tsr_preprocess_fwd(const tsr_gaussians_t* g, const tsr_camera_t* cam,
-                       int32_t strategy, float* rec, int32_t* source_ids, int32_t* row_of_source,
-                       int64_t* pair_offsets, int64_t* totals, void* workspace,
+int tsr_preprocess_fwd(const tsr_gaussians_t* g, const tsr_camera_t* cam, int32_t strategy,
+                       float* rec, int32_t* source_ids, int32_t* row_of_source, int32_t* counts,
+                       uint32_t* depth_bits, void* spans, int64_t* totals, void* workspace,
                        size_t workspace_bytes, void* stream);
 
-/* Pair count + splat-major offsets for an arbitrary caller-built batch
- * (bin_sequential on a make_batch()-style SplatBatch, binning.py:166-215). */
-size_t tsr_count_workspace(int64_t m);
+/* Same counts / depth bits / spans for a caller-built batch of m rows
+ * (bin_sequential on a make_batch()-style SplatBatch, binning.py:166-215);
+ * totals[0] = m, totals[1] = P (device). */
 int tsr_count_pairs(const float* rec, int64_t m, int32_t width, int32_t height,
-                    int32_t strategy, int64_t* pair_offsets, int64_t* total_pairs, void* workspace,
-                    size_t workspace_bytes, void* stream);
+                    int32_t strategy, int32_t* counts, uint32_t* depth_bits, void* spans,
+                    int64_t* totals, void* stream);
 
 /* compute_snugboxes (binning.py:87-104): FP64 extents + inclusive tile rect
  * (int32 [tx0,tx1,ty0,ty1]). */
@@ -99,28 +100,20 @@ int tsr_snugboxes(const float* rec, int64_t m, int32_t width, int32_t height,
                   int32_t* tile_rect, void* stream);
 
 /* ---------------------------------------------------------------- K2 ----
- * Key duplication: the exact column walk of bin_sequential
- * (binning.py:178-221) or the min-q group test of bin_load_balanced
- * (binning.py:225-286, strategy=1), emitting keys/values splat-major. */
-int tsr_duplicate_keys(const float* rec, int64_t m, int32_t width, int32_t height,
-                       const int64_t* pair_offsets, int64_t n_pairs,
-                       int32_t strategy, int64_t* keys, int32_t* values,
-                       void* stream);
-
-/* Stable on-device LSD radix sort of (key, value) pairs on the significant
- * key bits (radix_argsort_u64, binning.py:142-148). In/out buffers may not
- * alias; results land in keys_out/values_out. */
-size_t tsr_sort_workspace(int64_t n_pairs, int32_t n_tiles);
-int tsr_sort_pairs(const int64_t* keys_in, int64_t* keys_out,
-                   const int32_t* values_in, int32_t* values_out,
-                   int64_t n_pairs, int32_t n_tiles, void* workspace,
-                   size_t workspace_bytes, void* stream);
-
-/* Per-tile ranges (binning.py:156-157) + checkpoint record bases
- * ckpt_base[t] = sum_{u<t} floor(n_u / 32) (forward.py:139-145);
- * ckpt_total (device) = total tile-records. */
-int tsr_tile_ranges(const int64_t* sorted_keys, int64_t n_pairs, int32_t n_tiles,
-                    int64_t* offsets, int64_t* ckpt_base, void* stream);
+ * TileIndex (binning.py:137-158) without a 64-bit key sort: stable radix sort
+ * of rows by depth bits -> rank-major emission of (tile, rank) pairs ->
+ * stable radix sort by tile -> keys = tile << 32 | depth bits, values = row,
+ * offsets[T+1], ckpt_base[T+1] = prefix of floor(n_tile / 32)
+ * (forward.py:139-145).  M and P are read from `totals` on the device; the
+ * capacities bound every buffer.  If P > p_cap the pairs are clamped and
+ * *overflow (sticky, device int32) is set to 1: the caller re-runs with a
+ * larger capacity. */
+size_t tsr_index_workspace(int64_t m_cap, int64_t p_cap);
+int tsr_build_index(const float* rec, const uint32_t* depth_bits, const void* spans,
+                    const int32_t* counts, const int64_t* totals, int64_t m_cap, int64_t p_cap,
+                    int32_t width, int32_t height, int32_t strategy, int64_t* keys,
+                    int32_t* values, int64_t* offsets, int64_t* ckpt_base, int32_t* overflow,
+                    void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------- K3 ----
  * render (forward.py:87-161). ckpt may be NULL (record_checkpoints=False).

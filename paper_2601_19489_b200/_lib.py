@@ -51,15 +51,12 @@ class AdamGroup_t(ctypes.Structure):
 _SIGNATURES = {
     "tsr_preprocess_workspace": (c_sz, [c_i64]),
     "tsr_preprocess_fwd": (c_i32, [ctypes.POINTER(Gaussians_t), ctypes.POINTER(Camera_t), c_i32,
-                                   c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
-    "tsr_count_workspace": (c_sz, [c_i64]),
-    "tsr_count_pairs": (c_i32, [c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_sz, c_vp]),
+                                   c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "tsr_count_pairs": (c_i32, [c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tsr_snugboxes": (c_i32, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
-    "tsr_duplicate_keys": (c_i32, [c_vp, c_i64, c_i32, c_i32, c_vp, c_i64, c_i32, c_vp, c_vp,
-                                   c_vp]),
-    "tsr_sort_workspace": (c_sz, [c_i64, c_i32]),
-    "tsr_sort_pairs": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_sz, c_vp]),
-    "tsr_tile_ranges": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
+    "tsr_index_workspace": (c_sz, [c_i64, c_i64]),
+    "tsr_build_index": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_i32, c_i32,
+                                c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "tsr_render_fwd": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, ctypes.POINTER(c_f32), c_vp, c_vp,
                                c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tsr_render_bwd": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,

@@ -106,54 +106,66 @@ def snugbox(conic, t, mean, image_dims) -> SnugBox:
                    float(batch.y_max[0]), tuple(int(v) for v in r))
 
 
-def _pair_offsets(batch: SplatBatch, strategy: int):
-    """Splat-major pair offsets; reuses K1's fused count when available."""
-    if batch.pair_offsets is not None and batch.strategy == strategy:
-        return batch.pair_offsets, batch.n_pairs
+def _ensure_counts(batch: SplatBatch, strategy: int) -> None:
+    """Per-row pair counts / depth bits / spans; reuses K1's fused count when
+    it was made with the same strategy."""
+    if batch.counts is not None and batch.strategy == strategy:
+        return
     lib = _lib.load()
     m = len(batch)
     dev = _device()
-    offs = torch.empty(m + 1, dtype=torch.int64, device=dev)
-    total = torch.zeros(1, dtype=torch.int64, device=dev)
-    ws = int(lib.tsr_count_workspace(m))
-    work = torch.empty(max(ws, 1), dtype=torch.uint8, device=dev)
+    batch.counts = torch.empty(max(m, 1), dtype=torch.int32, device=dev)[:m]
+    batch.depth_bits = torch.empty(max(m, 1), dtype=torch.int32, device=dev)[:m]
+    batch.spans = torch.empty((max(m, 1), 4), dtype=torch.int32, device=dev)[:m]
+    batch.totals = torch.zeros(2, dtype=torch.int64, device=dev)
     _lib.check(lib.tsr_count_pairs(batch.rec.data_ptr(), m, batch.width, batch.height, strategy,
-                                   offs.data_ptr(), total.data_ptr(), work.data_ptr(), ws,
+                                   batch.counts.data_ptr(), batch.depth_bits.data_ptr(),
+                                   batch.spans.data_ptr(), batch.totals.data_ptr(),
                                    _lib.stream_handle()), "tsr_count_pairs")
-    return offs, int(total.item())
+    batch.n_pairs = int(batch.totals[1].item())
+    batch.strategy = strategy
 
 
-def build_index(batch: SplatBatch, strategy: int, n_pairs: int | None = None,
-                pair_offsets=None) -> TileIndex:
-    """Duplicate keys, sort, ranges.  n_pairs/pair_offsets may come from K1."""
+class IndexBuffers:
+    """Capacity buffers for K2 (reused across steps by the trainer)."""
+
+    def __init__(self, m_cap: int, p_cap: int, n_tiles: int):
+        dev = _device()
+        lib = _lib.load()
+        self.m_cap, self.p_cap, self.n_tiles = m_cap, p_cap, n_tiles
+        self.keys = torch.empty(max(p_cap, 1), dtype=torch.int64, device=dev)
+        self.values = torch.empty(max(p_cap, 1), dtype=torch.int32, device=dev)
+        self.offsets = torch.empty(n_tiles + 1, dtype=torch.int64, device=dev)
+        self.ckpt_base = torch.empty(n_tiles + 1, dtype=torch.int64, device=dev)
+        self.overflow = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.ws_bytes = int(lib.tsr_index_workspace(m_cap, p_cap))
+        self.workspace = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+
+    def fits(self, m: int, p: int, n_tiles: int) -> bool:
+        return m <= self.m_cap and p <= self.p_cap and n_tiles == self.n_tiles
+
+
+def build_index_raw(batch: SplatBatch, strategy: int, bufs: IndexBuffers) -> None:
+    """Launch K2 into capacity buffers; sizes come from batch.totals on the device."""
     lib = _lib.load()
-    if pair_offsets is None or n_pairs is None:
-        pair_offsets, n_pairs = _pair_offsets(batch, strategy)
+    _lib.check(lib.tsr_build_index(
+        batch.rec.data_ptr(), batch.depth_bits.data_ptr(), batch.spans.data_ptr(),
+        batch.counts.data_ptr(), batch.totals.data_ptr(), bufs.m_cap, bufs.p_cap, batch.width,
+        batch.height, strategy, bufs.keys.data_ptr(), bufs.values.data_ptr(),
+        bufs.offsets.data_ptr(), bufs.ckpt_base.data_ptr(), bufs.overflow.data_ptr(),
+        bufs.workspace.data_ptr(), bufs.ws_bytes, _lib.stream_handle()), "tsr_build_index")
+
+
+def build_index(batch: SplatBatch, strategy: int, bufs: IndexBuffers | None = None) -> TileIndex:
+    """K2 with exact sizes (one host read of P when not already known)."""
+    _ensure_counts(batch, strategy)
     tiles_x, tiles_y = _tiles(batch)
-    n_tiles = tiles_x * tiles_y
-    m = len(batch)
-    dev = _device()
-    stream = _lib.stream_handle()
-    keys_tmp = torch.empty(max(n_pairs, 1), dtype=torch.int64, device=dev)
-    vals_tmp = torch.empty(max(n_pairs, 1), dtype=torch.int32, device=dev)
-    keys = torch.empty(n_pairs, dtype=torch.int64, device=dev)
-    vals = torch.empty(n_pairs, dtype=torch.int32, device=dev)
-    _lib.check(lib.tsr_duplicate_keys(batch.rec.data_ptr(), m, batch.width, batch.height,
-                                      pair_offsets.data_ptr(), n_pairs, strategy,
-                                      keys_tmp.data_ptr(), vals_tmp.data_ptr(), stream),
-               "tsr_duplicate_keys")
-    if n_pairs > 0:
-        ws = int(lib.tsr_sort_workspace(n_pairs, n_tiles))
-        work = torch.empty(ws, dtype=torch.uint8, device=dev)
-        _lib.check(lib.tsr_sort_pairs(keys_tmp.data_ptr(), keys.data_ptr(), vals_tmp.data_ptr(),
-                                      vals.data_ptr(), n_pairs, n_tiles, work.data_ptr(), ws,
-                                      stream), "tsr_sort_pairs")
-    offsets = torch.empty(n_tiles + 1, dtype=torch.int64, device=dev)
-    ckpt_base = torch.empty(n_tiles + 1, dtype=torch.int64, device=dev)
-    _lib.check(lib.tsr_tile_ranges(_lib.ptr(keys) if n_pairs else keys_tmp.data_ptr(), n_pairs,
-                                   n_tiles, offsets.data_ptr(), ckpt_base.data_ptr(), stream),
-               "tsr_tile_ranges")
-    return TileIndex(keys, vals, offsets, tiles_x, tiles_y, ckpt_base)
+    m, p = len(batch), int(batch.n_pairs)
+    if bufs is None or not bufs.fits(m, p, tiles_x * tiles_y):
+        bufs = IndexBuffers(m, p, tiles_x * tiles_y)
+    build_index_raw(batch, strategy, bufs)
+    return TileIndex(bufs.keys[:p], bufs.values[:p], bufs.offsets, tiles_x, tiles_y,
+                     bufs.ckpt_base)
 
 
 def bin_sequential(batch: SplatBatch) -> TileIndex:

@@ -107,11 +107,41 @@ __device__ __forceinline__ long long count_load_balanced(const SplatF64& s, int 
   return total;
 }
 
-__device__ __forceinline__ long long count_pairs_of(const float* r, int strategy,
-                                                    int tiles_x, int tiles_y) {
-  SplatF64 s = load_splat_f64(r);
-  return strategy == 1 ? count_load_balanced(s, tiles_x, tiles_y)
-                       : count_sequential(s, tiles_x, tiles_y);
+// Exact pair count of one splat plus its compact column-span record (read by
+// the rank-major emission in sort.cu, which then needs no FP64 re-walk):
+//   x = tx0 | ncols << 16, y = ty_base | overflow << 31,
+//   z, w = columns 0..7 as (row offset 4 bits | nrows 4 bits) bytes.
+// overflow is set when the span does not fit (the emission then re-walks).
+__device__ __forceinline__ long long count_pairs_of(const float* rp, int strategy, int tiles_x,
+                                                    int tiles_y, uint4& span) {
+  SplatF64 s = load_splat_f64(rp);
+  span = make_uint4(0u, 0u, 0u, 0u);
+  if (strategy == 1) {
+    span.y = 1u << 31;
+    return count_load_balanced(s, tiles_x, tiles_y);
+  }
+  SnugRect r = snugbox(s, tiles_x, tiles_y);
+  if (r.tx0 > r.tx1 || r.ty0 > r.ty1) return 0;
+  const long long ncols = r.tx1 - r.tx0 + 1;
+  bool fits = ncols <= 8;
+  span.x = (uint32_t)(r.tx0 & 0xffff) | ((uint32_t)(ncols < 255 ? ncols : 255) << 16);
+  span.y = (uint32_t)(r.ty0 & 0xffff);
+  long long total = 0;
+  for (long long tx = r.tx0; tx <= r.tx1; ++tx) {
+    long long ty0, ty1;
+    const int nr = column_rows(s, r, tx, tiles_y, ty0, ty1);
+    total += nr;
+    const long long c = tx - r.tx0;
+    const long long off = nr > 0 ? ty0 - r.ty0 : 0;
+    if (nr > 15 || off > 15) fits = false;
+    if (fits && c < 8) {
+      const uint32_t code = ((uint32_t)off & 15u) | ((uint32_t)nr << 4);
+      if (c < 4) span.z |= code << (8 * c);
+      else span.w |= code << (8 * (c - 4));
+    }
+  }
+  if (!fits) span.y |= 1u << 31;
+  return total;
 }
 
 // Projection of one Gaussian into the 12-float raster record.  Returns false
@@ -206,7 +236,8 @@ __device__ __forceinline__ bool project_one(const tsr_gaussians_t& g, const tsr_
 __global__ void __launch_bounds__(kScanBlock) preprocess_kernel(
     tsr_gaussians_t g, tsr_camera_t cam, int strategy, float4* __restrict__ rec_out,
     int32_t* __restrict__ source_ids, int32_t* __restrict__ row_of_source,
-    int64_t* __restrict__ pair_offsets, int64_t* __restrict__ totals,
+    int32_t* __restrict__ counts, uint32_t* __restrict__ depth_bits, uint4* __restrict__ spans,
+    int64_t* __restrict__ totals,
     unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket,
     int n_blocks) {
   __shared__ unsigned long long s_warp[kScanBlock / 32];
@@ -221,9 +252,10 @@ __global__ void __launch_bounds__(kScanBlock) preprocess_kernel(
   float rec[12];
   bool keep = false;
   long long cnt = 0;
+  uint4 span = make_uint4(0u, 0u, 0u, 0u);
   if (i < g.n) {
     keep = project_one(g, cam, i, rec);
-    if (keep) cnt = count_pairs_of(rec, strategy, tiles_x, tiles_y);
+    if (keep) cnt = count_pairs_of(rec, strategy, tiles_x, tiles_y, span);
   }
   unsigned long long v = pack_rp(keep ? 1ull : 0ull, (unsigned long long)cnt);
   unsigned long long excl = scan_lookback(v, bid, status, s_warp, s_prefix);
@@ -235,38 +267,43 @@ __global__ void __launch_bounds__(kScanBlock) preprocess_kernel(
     dst[1] = make_float4(rec[4], rec[5], rec[6], rec[7]);
     dst[2] = make_float4(rec[8], rec[9], rec[10], rec[11]);
     source_ids[row] = (int32_t)i;
-    pair_offsets[row] = pair0;
+    counts[row] = (int32_t)cnt;
+    depth_bits[row] = __float_as_uint(rec[6]);
+    spans[row] = span;
   }
+  (void)pair0;
   if (i < g.n) row_of_source[i] = keep ? (int32_t)row : -1;
   if (bid == n_blocks - 1 && threadIdx.x == 0) {
     unsigned long long tot = s_prefix[0] + s_prefix[1];
-    long long m = (long long)(tot >> 36), p = (long long)(tot & ((1ull << 36) - 1));
-    totals[0] = m;
-    totals[1] = p;
-    pair_offsets[m] = p;
+    totals[0] = (long long)(tot >> 36);
+    totals[1] = (long long)(tot & ((1ull << 36) - 1));
   }
 }
 
+// Pair count + span + depth bits of a caller-built batch; P total by a block
+// reduction + one atomic per CTA.
 __global__ void __launch_bounds__(kScanBlock) count_kernel(
     const float* __restrict__ rec, long long m, int width, int height, int strategy,
-    int64_t* __restrict__ pair_offsets, int64_t* __restrict__ total_pairs,
-    unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket,
-    int n_blocks) {
-  __shared__ unsigned long long s_warp[kScanBlock / 32];
-  __shared__ unsigned long long s_prefix[2];
-  __shared__ int s_bid;
-  if (threadIdx.x == 0) s_bid = (int)atomicAdd(ticket, 1u);
-  __syncthreads();
-  const int bid = s_bid;
-  const long long i = (long long)bid * kScanBlock + threadIdx.x;
+    int32_t* __restrict__ counts, uint32_t* __restrict__ depth_bits, uint4* __restrict__ spans,
+    unsigned long long* __restrict__ total_pairs) {
+  __shared__ unsigned long long s_sum[kScanBlock / 32];
+  const long long i = (long long)blockIdx.x * kScanBlock + threadIdx.x;
   long long cnt = 0;
-  if (i < m) cnt = count_pairs_of(rec + i * 12, strategy, tiles_of(width), tiles_of(height));
-  unsigned long long excl = scan_lookback((unsigned long long)cnt, bid, status, s_warp, s_prefix);
-  if (i < m) pair_offsets[i] = (long long)excl;
-  if (bid == n_blocks - 1 && threadIdx.x == 0) {
-    long long p = (long long)(s_prefix[0] + s_prefix[1]);
-    total_pairs[0] = p;
-    pair_offsets[m] = p;
+  if (i < m) {
+    uint4 span;
+    cnt = count_pairs_of(rec + i * 12, strategy, tiles_of(width), tiles_of(height), span);
+    counts[i] = (int32_t)cnt;
+    depth_bits[i] = __float_as_uint(rec[i * 12 + 6]);
+    spans[i] = span;
+  }
+  unsigned long long v = (unsigned long long)cnt;
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < kScanBlock / 32; ++w) t += s_sum[w];
+    if (t) atomicAdd(total_pairs, t);
   }
 }
 
@@ -297,47 +334,45 @@ static size_t scan_workspace(long long n) {
 using namespace tsr;
 
 extern "C" size_t tsr_preprocess_workspace(int64_t n) { return scan_workspace(n); }
-extern "C" size_t tsr_count_workspace(int64_t m) { return scan_workspace(m); }
 
 extern "C" int tsr_preprocess_fwd(const tsr_gaussians_t* g, const tsr_camera_t* cam,
                                   int32_t strategy, float* rec, int32_t* source_ids,
-                                  int32_t* row_of_source, int64_t* pair_offsets,
-                                  int64_t* totals, void* workspace, size_t workspace_bytes,
-                                  void* stream) {
+                                  int32_t* row_of_source, int32_t* counts, uint32_t* depth_bits,
+                                  void* spans, int64_t* totals, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
   if (!g || !cam || g->n < 0 || g->n >= TSR_MAX_GAUSSIANS) return TSR_E_INVALID;
   if (g->sh_coeffs != 1 && g->sh_coeffs != 4 && g->sh_coeffs != 9 && g->sh_coeffs != 16)
     return TSR_E_INVALID;
   if (workspace_bytes < scan_workspace(g->n)) return TSR_E_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
   if (cudaMemsetAsync(totals, 0, 2 * sizeof(int64_t), s) != cudaSuccess) return TSR_E_CUDA;
-  if (cudaMemsetAsync(pair_offsets, 0, sizeof(int64_t), s) != cudaSuccess) return TSR_E_CUDA;
   if (g->n == 0) return TSR_OK;
   int blocks = (int)((g->n + kScanBlock - 1) / kScanBlock);
   if (cudaMemsetAsync(workspace, 0, scan_workspace(g->n), s) != cudaSuccess) return TSR_E_CUDA;
   unsigned int* ticket = (unsigned int*)workspace;
   unsigned long long* status = (unsigned long long*)((char*)workspace + 256);
   preprocess_kernel<<<blocks, kScanBlock, 0, s>>>(*g, *cam, strategy, (float4*)rec, source_ids,
-                                                  row_of_source, pair_offsets, totals, status,
-                                                  ticket, blocks);
+                                                  row_of_source, counts, depth_bits,
+                                                  (uint4*)spans, totals, status, ticket, blocks);
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }
 
 extern "C" int tsr_count_pairs(const float* rec, int64_t m, int32_t width, int32_t height,
-                               int32_t strategy, int64_t* pair_offsets, int64_t* total_pairs,
-                               void* workspace, size_t workspace_bytes, void* stream) {
-  if (m < 0 || m >= TSR_MAX_GAUSSIANS || width <= 0 || height <= 0) return TSR_E_INVALID;
-  if (workspace_bytes < scan_workspace(m)) return TSR_E_WORKSPACE;
+                               int32_t strategy, int32_t* counts, uint32_t* depth_bits,
+                               void* spans, int64_t* totals, void* stream) {
+  if (m < 0 || m >= TSR_MAX_GAUSSIANS || width <= 0 || height <= 0 || !totals)
+    return TSR_E_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
-  if (cudaMemsetAsync(total_pairs, 0, sizeof(int64_t), s) != cudaSuccess) return TSR_E_CUDA;
-  if (cudaMemsetAsync(pair_offsets, 0, sizeof(int64_t), s) != cudaSuccess) return TSR_E_CUDA;
+  const int64_t host_totals[2] = {m, 0};
+  if (cudaMemcpyAsync(totals, host_totals, sizeof(host_totals), cudaMemcpyHostToDevice, s) !=
+      cudaSuccess)
+    return TSR_E_CUDA;
   if (m == 0) return TSR_OK;
   int blocks = (int)((m + kScanBlock - 1) / kScanBlock);
-  if (cudaMemsetAsync(workspace, 0, scan_workspace(m), s) != cudaSuccess) return TSR_E_CUDA;
-  count_kernel<<<blocks, kScanBlock, 0, s>>>(rec, m, width, height, strategy, pair_offsets,
-                                             total_pairs,
-                                             (unsigned long long*)((char*)workspace + 256),
-                                             (unsigned int*)workspace, blocks);
+  count_kernel<<<blocks, kScanBlock, 0, s>>>(rec, m, width, height, strategy, counts, depth_bits,
+                                             (uint4*)spans,
+                                             (unsigned long long*)(totals + 1));
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }

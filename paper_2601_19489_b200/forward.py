@@ -98,33 +98,51 @@ def _ensure_colors(batch: SplatBatch, colors) -> None:
                                          device=batch.rec.device).reshape(-1, 3).float()
 
 
+class RenderTargets:
+    """Preallocated forward outputs (reused across steps by the trainer)."""
+
+    def __init__(self, height: int, width: int, ckpt_records: int | None):
+        dev = _device()
+        self.color = torch.empty((height, width, 3), dtype=torch.float32, device=dev)
+        self.depth = torch.empty((height, width), dtype=torch.float32, device=dev)
+        self.final_T = torch.empty((height, width), dtype=torch.float32, device=dev)
+        self.n_contrib = torch.empty((height, width), dtype=torch.int32, device=dev)
+        self.n_considered = torch.empty((height, width), dtype=torch.int32, device=dev)
+        self.ckpt = None
+        if ckpt_records is not None:
+            self.ckpt = torch.empty(max(ckpt_records, 1) * 5 * TILE * TILE, dtype=torch.float32,
+                                    device=dev)
+
+
+def render_raw(rec, values, offsets, ckpt_base, width: int, height: int, background,
+               out: RenderTargets) -> None:
+    """Launch K3 into preallocated targets (no host synchronisation)."""
+    lib = _lib.load()
+    bg = np.asarray(background, dtype=np.float64).reshape(3)
+    bg_host = (_lib.c_f32 * 3)(*[float(v) for v in bg])
+    _lib.check(lib.tsr_render_fwd(
+        rec.data_ptr(), _lib.ptr(values), offsets.data_ptr(), width, height, bg_host,
+        out.color.data_ptr(), out.depth.data_ptr(), out.final_T.data_ptr(),
+        out.n_contrib.data_ptr(), out.n_considered.data_ptr(), _lib.ptr(out.ckpt),
+        _lib.ptr(ckpt_base) if out.ckpt is not None else None, _lib.stream_handle()),
+        "tsr_render_fwd")
+
+
 def render(batch: SplatBatch, tiles: TileIndex, colors, background, *,
            record_checkpoints: bool = True, scoring: bool = False):
     """K3 forward (forward.py:87-161)."""
     if scoring:
         raise NotImplementedError("scoring mode (density, SURVEY §8(f) #2) is not built yet")
-    lib = _lib.load()
     _ensure_colors(batch, colors)
     H, W = batch.height, batch.width
-    dev = _device()
     bg = np.asarray(background, dtype=np.float64).reshape(3)
-    color = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
-    depth = torch.empty((H, W), dtype=torch.float32, device=dev)
-    final_T = torch.empty((H, W), dtype=torch.float32, device=dev)
-    n_contrib = torch.empty((H, W), dtype=torch.int32, device=dev)
-    n_cons = torch.empty((H, W), dtype=torch.int32, device=dev)
-    ckpt = None
-    if record_checkpoints:
-        # sum_t floor(n_t / 32) <= P / 32 records of 5 x 256 floats
-        records = tiles.n_pairs // CHECKPOINT_INTERVAL + 1
-        ckpt = torch.empty(records * 5 * TILE * TILE, dtype=torch.float32, device=dev)
-    bg_host = (_lib.c_f32 * 3)(*[float(v) for v in bg])
-    _lib.check(lib.tsr_render_fwd(
-        batch.rec.data_ptr(), _lib.ptr(tiles.values) if tiles.n_pairs else None,
-        tiles.offsets.data_ptr(), W, H, bg_host, color.data_ptr(), depth.data_ptr(),
-        final_T.data_ptr(), n_contrib.data_ptr(), n_cons.data_ptr(), _lib.ptr(ckpt),
-        _lib.ptr(tiles.ckpt_base) if ckpt is not None else None, _lib.stream_handle()),
-        "tsr_render_fwd")
+    # sum_t floor(n_t / 32) <= P / 32 records of 5 x 256 floats
+    out = RenderTargets(H, W, tiles.n_pairs // CHECKPOINT_INTERVAL + 1
+                        if record_checkpoints else None)
+    render_raw(batch.rec, tiles.values if tiles.n_pairs else None, tiles.offsets,
+               tiles.ckpt_base, W, H, bg, out)
+    color, depth, final_T, n_contrib, n_cons, ckpt = (out.color, out.depth, out.final_T,
+                                                      out.n_contrib, out.n_considered, out.ckpt)
     return RenderBuffers(color, depth, final_T, n_contrib, n_cons, bg, ckpt,
                          tiles.ckpt_base if ckpt is not None else None,
                          tiles.tiles_x, tiles.tiles_y)

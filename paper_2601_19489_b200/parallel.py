@@ -70,19 +70,23 @@ class ViewParallelStep(TrainStep):
         self.grads = flat_grad_views(self.flat, gset)
 
     def step_views(self, cameras, gts, timer=None) -> torch.Tensor:
+        if self.index is not None and cameras:
+            self._poll_status(cameras[0])
         self.iteration += 1
         total = None
         for k, (camera, gt) in enumerate(zip(cameras, gts)):
-            batch, tiles, bufs = self.forward(camera, timer)
-            e, g2 = self.loss_and_backward(batch, tiles, bufs, gt, timer)
+            batch = self.forward(camera, timer)
+            e = self.loss_and_backward(batch, camera, gt, timer)
             g = self.grads
             _lib.check(self.lib.tsr_preprocess_bwd(
                 gaussians_struct(self.gset), camera_struct(camera, None, self.cfg.near),
-                batch.rec.data_ptr(), batch.row_of_source.data_ptr(), g2.data_ptr(),
+                batch.rec.data_ptr(), batch.row_of_source.data_ptr(), self.grad2d.data_ptr(),
                 g["positions"].data_ptr(), g["log_scales"].data_ptr(), g["rotations"].data_ptr(),
                 g["opacity_logits"].data_ptr(), g["colors"].data_ptr(), None, 1 if k else 0,
                 _lib.stream_handle()), "tsr_preprocess_bwd")
             total = e if total is None else total + e
+            self._publish_status()
+            self.last_camera = camera
         if not cameras:
             self.flat.zero_()
         self._mark(timer, "vjp")

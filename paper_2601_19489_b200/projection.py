@@ -53,9 +53,12 @@ class SplatBatch:
         self.source_ids = source_ids
         self.x_min, self.x_max, self.y_min, self.y_max = x_min, x_max, y_min, y_max
         self.tile_rect = tile_rect
-        # filled by project(): inverse map and the fused pair count / offsets
+        # filled by project(): inverse map and K1's fused pair count outputs
         self.row_of_source = None
-        self.pair_offsets = None
+        self.counts = None       # (M,) int32 pairs per row
+        self.depth_bits = None   # (M,) int32 view of the f32 depth bits
+        self.spans = None        # (M, 4) int32 compact column walk
+        self.totals = None       # (2,) int64 device [M, P]
         self.n_pairs = None
         self.strategy = None
 
@@ -138,7 +141,9 @@ class ProjectionScratch:
         self.rec = torch.empty((max(n, 1), _lib.REC_FLOATS), dtype=torch.float32, device=dev)
         self.source_ids = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
         self.row_of_source = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-        self.pair_offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        self.counts = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        self.depth_bits = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        self.spans = torch.empty((max(n, 1), 4), dtype=torch.int32, device=dev)
         self.totals = torch.zeros(2, dtype=torch.int64, device=dev)
         self.ws_bytes = int(lib.tsr_preprocess_workspace(n))
         self.workspace = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
@@ -155,9 +160,10 @@ def project_raw(gset: GaussianSet, camera: Camera, near: float, delta, strategy:
     cam = camera_struct(camera, delta, near)
     _lib.check(lib.tsr_preprocess_fwd(
         g, cam, strategy, scratch.rec.data_ptr(), scratch.source_ids.data_ptr(),
-        scratch.row_of_source.data_ptr(), scratch.pair_offsets.data_ptr(),
-        scratch.totals.data_ptr(), scratch.workspace.data_ptr(), scratch.ws_bytes,
-        _lib.stream_handle()), "tsr_preprocess_fwd")
+        scratch.row_of_source.data_ptr(), scratch.counts.data_ptr(),
+        scratch.depth_bits.data_ptr(), scratch.spans.data_ptr(), scratch.totals.data_ptr(),
+        scratch.workspace.data_ptr(), scratch.ws_bytes, _lib.stream_handle()),
+        "tsr_preprocess_fwd")
     return scratch
 
 
@@ -165,11 +171,18 @@ def batch_from_scratch(scratch: ProjectionScratch, camera: Camera, strategy: int
     m, p = (int(v) for v in scratch.totals.tolist())
     batch = SplatBatch(None, None, None, None, None, scratch.source_ids[:m],
                        camera.width, camera.height, _rec=scratch.rec[:m])
+    attach_counts(batch, scratch, m, p, strategy)
+    return batch
+
+
+def attach_counts(batch: SplatBatch, scratch, m: int, p: int, strategy: int) -> None:
     batch.row_of_source = scratch.row_of_source[: scratch.n]
-    batch.pair_offsets = scratch.pair_offsets[: m + 1]
+    batch.counts = scratch.counts[:m]
+    batch.depth_bits = scratch.depth_bits[:m]
+    batch.spans = scratch.spans[:m]
+    batch.totals = scratch.totals
     batch.n_pairs = p
     batch.strategy = strategy
-    return batch
 
 
 def project(gset: GaussianSet, camera: Camera, near: float = 0.01,

@@ -84,7 +84,7 @@ def render_view(gset: GaussianSet, camera: Camera, cfg: TrainConfig,
                 scoring: bool = False) -> ViewRender:
     """project -> bin -> colours -> render (trainer.py:181-192)."""
     batch = project(gset, camera, near=cfg.near, delta=delta, strategy=cfg.strategy_id)
-    tiles = build_index(batch, cfg.strategy_id, batch.n_pairs, batch.pair_offsets)
+    tiles = build_index(batch, cfg.strategy_id)
     colors = batch.colors
     bufs = render(batch, tiles, colors, cfg.background, record_checkpoints=checkpoints,
                   scoring=scoring)
@@ -135,21 +135,40 @@ class TrainStep:
 
     Hot path for BASELINE.json's metric; the reference's per-step sequence is
     trainer.py:329-345.  Positions use the decaying lr (position_lr) exactly as
-    the reference loop does; pose optimisation is off (round2 profile)."""
+    the reference loop does; pose optimisation is off (round2 profile).
+
+    The step never synchronises with the host: every size (M rows, P pairs)
+    stays on the device and all buffers are capacity-allocated.  The pair
+    capacity is sized once (one host read on the first step) with headroom;
+    K2 raises a sticky overflow flag that is polled without blocking (a
+    pinned copy + event from an earlier step) and the capacity grows before it
+    is reached."""
 
     def __init__(self, gset: GaussianSet, cfg: TrainConfig, extent: float = 4.0,
-                 optimizer: Adam | None = None):
+                 optimizer: Adam | None = None, p_headroom: float = 1.5):
         self.gset = gset
         self.cfg = cfg
         self.opt = optimizer or Adam({k: v for k, v in cfg.lrs.items() if k != "positions"})
         self.pos_base_lr = cfg.lrs.get("positions", 1.6e-4 * extent)
         self.iteration = 0
-        self.scratch = None
+        self.p_headroom = p_headroom
+        n = len(gset)
         dev = _device()
+        self.scratch = ProjectionScratch(n)
+        self.index = None
+        self.targets = None
+        self.hw = None
+        self.grad2d = torch.zeros((max(n, 1), _lib.GRAD2D_FLOATS), dtype=torch.float32,
+                                  device=dev)
         self.skipped = torch.zeros(1, dtype=torch.int64, device=dev)
         self.merges = torch.zeros(1, dtype=torch.int64, device=dev)
-        self.grad2d = None
+        self.loss_ws = losses.PhotometricWorkspace()
+        self.grad_color = None
+        self.status_host = torch.zeros(3, dtype=torch.int64).pin_memory()
+        self.status_dev = torch.zeros(3, dtype=torch.int64, device=dev)
+        self.status_event = None
         self.lib = _lib.load()
+        self.last = None
 
     @staticmethod
     def _mark(timer, name):
@@ -158,46 +177,119 @@ class TrainStep:
             ev.record()
             timer.setdefault("_events", []).append((name, ev))
 
-    def forward(self, camera: Camera, timer=None):
-        self._mark(timer, "start")
-        s = project_raw(self.gset, camera, self.cfg.near, None, self.cfg.strategy_id,
-                        self.scratch)
-        self.scratch = s
-        self._mark(timer, "preprocess")
-        batch = batch_from_scratch(s, camera, self.cfg.strategy_id)  # host read of (M, P)
-        tiles = build_index(batch, self.cfg.strategy_id, batch.n_pairs, batch.pair_offsets)
-        self._mark(timer, "binning")
-        bufs = render(batch, tiles, batch.colors, self.cfg.background, record_checkpoints=True)
-        self._mark(timer, "render")
-        return batch, tiles, bufs
+    # -------------------------------------------------------------- capacity
+    def _ensure_capacity(self, camera: Camera) -> None:
+        hw = (camera.height, camera.width)
+        tiles = camera.tiles_x * camera.tiles_y
+        if self.index is not None and self.hw == hw and self.index.n_tiles == tiles:
+            return
+        torch.cuda.current_stream().synchronize()      # once: size P
+        p = int(self.scratch.totals[1].item())
+        self._allocate(camera, int(p * self.p_headroom) + 65536)
 
-    def loss_and_backward(self, batch, tiles, bufs, gt_image, timer=None):
-        e, l1, s, grad_color = losses.photometric_device(bufs.color, gt_image, self.cfg.lambda_)
+    def _allocate(self, camera: Camera, p_cap: int) -> None:
+        from .binning import IndexBuffers
+        from .forward import RenderTargets
+        tiles = camera.tiles_x * camera.tiles_y
+        self.index = IndexBuffers(len(self.gset), p_cap, tiles)
+        self.targets = RenderTargets(camera.height, camera.width, p_cap // 32 + tiles + 1)
+        self.hw = (camera.height, camera.width)
+        self.grad_color = torch.empty((camera.height, camera.width, 3), dtype=torch.float32,
+                                      device=self.grad2d.device)
+
+    def _poll_status(self, camera: Camera) -> None:
+        """Non-blocking check of an earlier step's overflow flag and P."""
+        if self.status_event is None or not self.status_event.query():
+            return
+        overflow, p = int(self.status_host[0]), int(self.status_host[1])
+        self.status_event = None
+        if overflow:
+            raise RuntimeError(f"pair capacity {self.index.p_cap} overflowed (P = {p}); "
+                               "the step results are invalid")
+        if p > 0.8 * self.index.p_cap:
+            self._allocate(camera, int(p * self.p_headroom) + 65536)
+
+    # ------------------------------------------------------------------ step
+    def forward(self, camera: Camera, timer=None):
+        """K1 + K2 + K3 into the capacity buffers (no host synchronisation)."""
+        self._mark(timer, "start")
+        project_raw(self.gset, camera, self.cfg.near, None, self.cfg.strategy_id, self.scratch)
+        self._mark(timer, "preprocess")
+        self._ensure_capacity(camera)
+        s = self.scratch
+        batch = SplatBatch(None, None, None, None, None, s.source_ids, camera.width,
+                           camera.height, _rec=s.rec)
+        batch.row_of_source, batch.counts, batch.depth_bits = s.row_of_source, s.counts, s.depth_bits
+        batch.spans, batch.totals, batch.strategy = s.spans, s.totals, self.cfg.strategy_id
+        from .binning import build_index_raw
+        from .forward import render_raw
+        build_index_raw(batch, self.cfg.strategy_id, self.index)
+        self._mark(timer, "binning")
+        idx, out = self.index, self.targets
+        render_raw(s.rec, idx.values, idx.offsets, idx.ckpt_base, camera.width, camera.height,
+                   self.cfg.background, out)
+        self._mark(timer, "render")
+        return batch
+
+    def loss_and_backward(self, batch, camera: Camera, gt_image, timer=None):
+        out, idx = self.targets, self.index
+        e, l1, s, grad_color = losses.photometric_device(out.color, gt_image, self.cfg.lambda_,
+                                                         grad=self.grad_color,
+                                                         workspace=self.loss_ws)
         self._mark(timer, "loss")
-        m = len(batch)
-        if self.grad2d is None or self.grad2d.shape[0] < max(m, 1):
-            self.grad2d = torch.empty((max(len(self.gset), 1), _lib.GRAD2D_FLOATS),
-                                      dtype=torch.float32, device=bufs.color.device)
-        g2 = self.grad2d[:m]
-        g2.zero_()
-        backward_per_gaussian_raw(bufs, batch, tiles, grad_color, out=g2, merges=self.merges)
+        self.grad2d.zero_()
+        _lib.check(self.lib.tsr_render_bwd(
+            batch.rec.data_ptr(), idx.values.data_ptr(), idx.offsets.data_ptr(), camera.width,
+            camera.height, out.color.data_ptr(), out.depth.data_ptr(), out.final_T.data_ptr(),
+            out.n_considered.data_ptr(), out.ckpt.data_ptr(), idx.ckpt_base.data_ptr(),
+            grad_color.data_ptr(), None, None, self.grad2d.data_ptr(), self.merges.data_ptr(),
+            _lib.stream_handle()), "tsr_render_bwd")
         self._mark(timer, "backward")
-        return e, g2
+        return e
+
+    def _publish_status(self) -> None:
+        self.status_dev[0:1].copy_(self.index.overflow)
+        self.status_dev[1:3].copy_(self.scratch.totals.flip(0))
+        self.status_host.copy_(self.status_dev, non_blocking=True)
+        self.status_event = torch.cuda.Event()
+        self.status_event.record()
 
     def step(self, camera: Camera, gt_image: torch.Tensor, timer=None) -> torch.Tensor:
-        """Run one step; returns the loss as a device scalar (no extra sync)."""
+        """Run one step; returns the loss as a device scalar (no host sync)."""
+        if self.index is not None:
+            self._poll_status(camera)
         self.iteration += 1
-        batch, tiles, bufs = self.forward(camera, timer)
-        e, g2 = self.loss_and_backward(batch, tiles, bufs, gt_image, timer)
+        batch = self.forward(camera, timer)
+        e = self.loss_and_backward(batch, camera, gt_image, timer)
         lr = {"positions": position_lr(self.pos_base_lr, self.iteration, self.cfg.max_iters)}
         groups = self.opt.groups_for_fused(self.gset.params(), lr)
         _lib.check(self.lib.tsr_preprocess_bwd_adam(
             gaussians_struct(self.gset), camera_struct(camera, None, self.cfg.near),
-            batch.rec.data_ptr(), batch.row_of_source.data_ptr(), g2.data_ptr(), groups, None,
-            self.skipped.data_ptr(), _lib.stream_handle()), "tsr_preprocess_bwd_adam")
+            batch.rec.data_ptr(), batch.row_of_source.data_ptr(), self.grad2d.data_ptr(), groups,
+            None, self.skipped.data_ptr(), _lib.stream_handle()), "tsr_preprocess_bwd_adam")
         self._mark(timer, "vjp_adam")
-        self.last = (batch, tiles, bufs)
+        self._publish_status()
+        self.last_camera = camera
         return e
+
+    def last_view(self):
+        """(batch, TileIndex, RenderBuffers) views of the last step (synchronises)."""
+        torch.cuda.current_stream().synchronize()
+        overflow = int(self.index.overflow.item())
+        if overflow:
+            raise RuntimeError("pair capacity overflowed")
+        m, p = (int(v) for v in self.scratch.totals.tolist())
+        cam = self.last_camera
+        s = self.scratch
+        batch = SplatBatch(None, None, None, None, None, s.source_ids[:m], cam.width, cam.height,
+                           _rec=s.rec[:m])
+        tiles = TileIndex(self.index.keys[:p], self.index.values[:p], self.index.offsets,
+                          cam.tiles_x, cam.tiles_y, self.index.ckpt_base)
+        out = self.targets
+        bufs = RenderBuffers(out.color, out.depth, out.final_T, out.n_contrib, out.n_considered,
+                             np.asarray(self.cfg.background, float), out.ckpt,
+                             self.index.ckpt_base, cam.tiles_x, cam.tiles_y)
+        return batch, tiles, bufs
 
 
 def phase_times(timer) -> dict:

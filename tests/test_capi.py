@@ -18,8 +18,8 @@ def declared_symbols():
 
 def test_header_declares_the_pipeline():
     names = declared_symbols()
-    for required in ("tsr_preprocess_fwd", "tsr_duplicate_keys", "tsr_sort_pairs",
-                     "tsr_tile_ranges", "tsr_render_fwd", "tsr_render_bwd",
+    for required in ("tsr_preprocess_fwd", "tsr_count_pairs", "tsr_build_index",
+                     "tsr_render_fwd", "tsr_render_bwd", "tsr_photometric",
                      "tsr_preprocess_bwd", "tsr_adam_step", "tsr_preprocess_bwd_adam"):
         assert required in names
 
@@ -42,7 +42,7 @@ def test_workspace_queries_are_host_only():
     from paper_2601_19489_b200 import _lib
     lib = _lib.load(require_cuda=False)
     assert lib.tsr_preprocess_workspace(1_000_000) > 1_000_000 // 256 * 8
-    assert lib.tsr_count_workspace(0) >= 256
+    assert lib.tsr_index_workspace(1_000_000, 4_000_000) > 8 * 4 * 1_000_000
 
 
 def test_product_path_fails_loudly_without_cuda():
