@@ -178,7 +178,9 @@ int tsr_adam_step(const tsr_adam_group_t* groups_host, int32_t n_groups,
 
 /* K4b fused with K5 for the single-view training step: the per-Gaussian
  * gradient never leaves registers.  groups_host[0..4] = positions,
- * log_scales, rotations, opacity_logits, colors (grad pointers ignored). */
+ * log_scales, rotations, opacity_logits, colors (grad pointers ignored).
+ * For SH degree 0 the consumed grad2d rows are zeroed in place (the buffer
+ * is ready for the next step's K4 without a memset). */
 int tsr_preprocess_bwd_adam(const tsr_gaussians_t* g, const tsr_camera_t* cam,
                             const float* rec, const int32_t* row_of_source,
                             const float* grad2d,

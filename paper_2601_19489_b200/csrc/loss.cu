@@ -20,21 +20,55 @@
 
 namespace tsr {
 
-constexpr int kLT = 32;            // output tile
-constexpr int kLR = 5;             // filter radius
-constexpr int kLIn = kLT + 2 * kLR;  // 42
+constexpr int kLT = 32;              // output tile
+constexpr int kLR = 5;               // filter radius
+constexpr int kLIn = kLT + 2 * kLR;  // 42 rows/cols incl. halo
+constexpr int kLS = 48;              // padded smem row stride (16-B aligned, 4 x float4 reads)
 
 // the window travels as a kernel parameter (constant bank): no device globals
 struct Win {
   float w[11];
 };
 
+// Load a (kLIn x kLIn) halo tile of one channel of an interleaved (H,W,3)
+// image (zero outside) into s[row][col] (row stride kLS).
+// All (up to 7) loads of a thread are issued before any shared store.
+constexpr int kHaloIters = (kLIn * kLIn + 255) / 256;
+__device__ __forceinline__ void load_halo(const float* __restrict__ img, int c, int H, int W,
+                                          int ty0, int tx0, float* s) {
+  float v[kHaloIters];
+  int dst[kHaloIters];
+#pragma unroll
+  for (int k = 0; k < kHaloIters; ++k) {
+    const int i = threadIdx.x + 256 * k;
+    const int yy = i / kLIn, xx = i - yy * kLIn;
+    const int y = ty0 - kLR + yy, x = tx0 - kLR + xx;
+    v[k] = 0.f;
+    dst[k] = i < kLIn * kLIn ? yy * kLS + xx : -1;
+    if (i < kLIn * kLIn && y >= 0 && y < H && x >= 0 && x < W)
+      v[k] = __ldg(img + ((long long)y * W + x) * 3 + c);
+  }
+#pragma unroll
+  for (int k = 0; k < kHaloIters; ++k)
+    if (dst[k] >= 0) s[dst[k]] = v[k];
+}
+
+// 16 consecutive values of a smem row starting at a multiple of 4.
+__device__ __forceinline__ void load16(const float* s, float* v) {
+  const float4* p = reinterpret_cast<const float4*>(s);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float4 q = p[k];
+    v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
+  }
+}
+
 __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__ r,
                                                        const float* __restrict__ g, int H, int W,
                                                        float inv_n, float* __restrict__ Q,
                                                        double* __restrict__ partials, Win win) {
-  __shared__ float s_r[kLIn][kLIn + 1];
-  __shared__ float s_g[kLIn][kLIn + 1];
+  __shared__ __align__(16) float s_r[kLIn * kLS];
+  __shared__ __align__(16) float s_g[kLIn * kLS];
   __shared__ float s_h[5][kLIn][kLT + 1];
   __shared__ double s_red[2][8];
   const int tid = threadIdx.x;
@@ -42,64 +76,84 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
   const long long HW = (long long)H * W;
   double acc_ssim = 0.0, acc_l1 = 0.0;
   for (int c = 0; c < 3; ++c) {
-    for (int i = tid; i < kLIn * kLIn; i += 256) {
-      const int yy = i / kLIn, xx = i - yy * kLIn;
-      const int y = ty0 - kLR + yy, x = tx0 - kLR + xx;
-      float rv = 0.f, gv = 0.f;
-      if (y >= 0 && y < H && x >= 0 && x < W) {
-        const long long p = ((long long)y * W + x) * 3 + c;
-        rv = r[p];
-        gv = g[p];
+    load_halo(r, c, H, W, ty0, tx0, s_r);
+    load_halo(g, c, H, W, ty0, tx0, s_g);
+    __syncthreads();
+    // horizontal: item = (row, 4 consecutive output cols); 42 x 8 items
+    for (int it = tid; it < kLIn * (kLT / 4); it += 256) {
+      const int row = it >> 3, c0 = (it & 7) * 4;
+      float a[16], b[16];
+      load16(s_r + row * kLS + c0, a);
+      load16(s_g + row * kLS + c0, b);
+      float m1[4] = {0, 0, 0, 0}, m2[4] = {0, 0, 0, 0}, q11[4] = {0, 0, 0, 0},
+            q22[4] = {0, 0, 0, 0}, q12[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int k = 0; k < 14; ++k) {
+        const float ak = a[k], bk = b[k], aa = ak * ak, bb = bk * bk, ab = ak * bk;
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+          const int tap = k - o;
+          if (tap >= 0 && tap < 11) {
+            const float w = win.w[tap];
+            m1[o] = fmaf(w, ak, m1[o]);
+            m2[o] = fmaf(w, bk, m2[o]);
+            q11[o] = fmaf(w, aa, q11[o]);
+            q22[o] = fmaf(w, bb, q22[o]);
+            q12[o] = fmaf(w, ab, q12[o]);
+          }
+        }
       }
-      s_r[yy][xx] = rv;
-      s_g[yy][xx] = gv;
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        s_h[0][row][c0 + o] = m1[o];
+        s_h[1][row][c0 + o] = m2[o];
+        s_h[2][row][c0 + o] = q11[o];
+        s_h[3][row][c0 + o] = q22[o];
+        s_h[4][row][c0 + o] = q12[o];
+      }
     }
     __syncthreads();
-    for (int i = tid; i < kLIn * kLT; i += 256) {
-      const int row = i / kLT, col = i - row * kLT;
-      float m1 = 0.f, m2 = 0.f, q11 = 0.f, q22 = 0.f, q12 = 0.f;
+    // vertical: item = (col, 4 consecutive output rows); 32 x 8 items = 256
+    {
+      const int col = tid & 31, r0 = (tid >> 5) * 4;
+      float v[5][4];
 #pragma unroll
-      for (int k = 0; k < 11; ++k) {
-        const float a = s_r[row][col + k], b = s_g[row][col + k], w = win.w[k];
-        m1 = fmaf(w, a, m1);
-        m2 = fmaf(w, b, m2);
-        q11 = fmaf(w, a * a, q11);
-        q22 = fmaf(w, b * b, q22);
-        q12 = fmaf(w, a * b, q12);
+      for (int q = 0; q < 5; ++q)
+#pragma unroll
+        for (int o = 0; o < 4; ++o) v[q][o] = 0.f;
+#pragma unroll
+      for (int k = 0; k < 14; ++k) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+          const float h = s_h[q][r0 + k][col];
+#pragma unroll
+          for (int o = 0; o < 4; ++o) {
+            const int tap = k - o;
+            if (tap >= 0 && tap < 11) v[q][o] = fmaf(win.w[tap], h, v[q][o]);
+          }
+        }
       }
-      s_h[0][row][col] = m1;
-      s_h[1][row][col] = m2;
-      s_h[2][row][col] = q11;
-      s_h[3][row][col] = q22;
-      s_h[4][row][col] = q12;
-    }
-    __syncthreads();
-    for (int i = tid; i < kLT * kLT; i += 256) {
-      const int row = i / kLT, col = i - row * kLT;
-      const int y = ty0 + row, x = tx0 + col;
-      if (y >= H || x >= W) continue;
-      float v[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int k = 0; k < 11; ++k) {
-        const float w = win.w[k];
-#pragma unroll
-        for (int q = 0; q < 5; ++q) v[q] = fmaf(w, s_h[q][row + k][col], v[q]);
-      }
-      const float mu1 = v[0], mu2 = v[1];
-      const float s1 = v[2] - mu1 * mu1, s2 = v[3] - mu2 * mu2, s12 = v[4] - mu1 * mu2;
       const float C1 = 0.0001f, C2 = 0.0009f;
-      const float A1 = 2.f * mu1 * mu2 + C1, A2 = 2.f * s12 + C2;
-      const float B1 = mu1 * mu1 + mu2 * mu2 + C1, B2 = s1 + s2 + C2;
-      const float inv_b = 1.0f / (B1 * B2);
-      const float map = A1 * A2 * inv_b;
-      const float dA1 = inv_n * A2 * inv_b, dA2 = inv_n * A1 * inv_b;
-      const float dB1 = -inv_n * map / B1, dB2 = -inv_n * map / B2;
-      const long long pix = (long long)y * W + x;
-      Q[(c * 3 + 0) * HW + pix] = 2.f * mu2 * (dA1 - dA2) + 2.f * mu1 * (dB1 - dB2);
-      Q[(c * 3 + 1) * HW + pix] = dB2;
-      Q[(c * 3 + 2) * HW + pix] = 2.f * dA2;
-      acc_ssim += (double)map;
-      acc_l1 += (double)fabsf(s_r[row + kLR][col + kLR] - s_g[row + kLR][col + kLR]);
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        const int y = ty0 + r0 + o, x = tx0 + col;
+        if (y >= H || x >= W) continue;
+        const float mu1 = v[0][o], mu2 = v[1][o];
+        const float s1 = v[2][o] - mu1 * mu1, s2 = v[3][o] - mu2 * mu2, s12 = v[4][o] - mu1 * mu2;
+        const float A1 = 2.f * mu1 * mu2 + C1, A2 = 2.f * s12 + C2;
+        const float B1 = mu1 * mu1 + mu2 * mu2 + C1, B2 = s1 + s2 + C2;
+        const float inv_b = 1.0f / (B1 * B2);
+        const float map = A1 * A2 * inv_b;
+        const float dA1 = inv_n * A2 * inv_b, dA2 = inv_n * A1 * inv_b;
+        const float dB1 = -inv_n * map * (B2 * inv_b), dB2 = -inv_n * map * (B1 * inv_b);
+        const long long pix = (long long)y * W + x;
+        Q[(c * 3 + 0) * HW + pix] = 2.f * mu2 * (dA1 - dA2) + 2.f * mu1 * (dB1 - dB2);
+        Q[(c * 3 + 1) * HW + pix] = dB2;
+        Q[(c * 3 + 2) * HW + pix] = 2.f * dA2;
+        acc_ssim += (double)map;
+        const int yy = r0 + o + kLR, xx = col + kLR;
+        acc_l1 += (double)fabsf(s_r[yy * kLS + xx] - s_g[yy * kLS + xx]);
+      }
     }
     __syncthreads();
   }
@@ -115,9 +169,9 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
   }
   __syncthreads();
   if (tid < 2) {
-    double s = 0.0;
-    for (int w = 0; w < 8; ++w) s += s_red[tid][w];
-    partials[2 * (blockIdx.y * gridDim.x + blockIdx.x) + tid] = s;
+    double sum = 0.0;
+    for (int w = 0; w < 8; ++w) sum += s_red[tid][w];
+    partials[2 * (blockIdx.y * gridDim.x + blockIdx.x) + tid] = sum;
   }
 }
 
@@ -126,51 +180,79 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__
                                                        float lam, float inv_n,
                                                        const float* __restrict__ Q,
                                                        float* __restrict__ grad, Win win) {
-  __shared__ float s_q[3][kLIn][kLIn + 1];
+  __shared__ __align__(16) float s_q[3][kLIn * kLS];
   __shared__ float s_h[3][kLIn][kLT + 1];
   const int tid = threadIdx.x;
   const int tx0 = blockIdx.x * kLT, ty0 = blockIdx.y * kLT;
   const long long HW = (long long)H * W;
   for (int c = 0; c < 3; ++c) {
-    for (int i = tid; i < kLIn * kLIn; i += 256) {
-      const int yy = i / kLIn, xx = i - yy * kLIn;
-      const int y = ty0 - kLR + yy, x = tx0 - kLR + xx;
-      const bool in = y >= 0 && y < H && x >= 0 && x < W;
-      const long long pix = (long long)y * W + x;
 #pragma unroll
-      for (int q = 0; q < 3; ++q) s_q[q][yy][xx] = in ? Q[(c * 3 + q) * HW + pix] : 0.f;
-    }
-    __syncthreads();
-    for (int i = tid; i < kLIn * kLT; i += 256) {
-      const int row = i / kLT, col = i - row * kLT;
-      float v[3] = {0.f, 0.f, 0.f};
+    for (int q = 0; q < 3; ++q) {
+      float v[kHaloIters];
+      int dst[kHaloIters];
 #pragma unroll
-      for (int k = 0; k < 11; ++k) {
-        const float w = win.w[k];
-#pragma unroll
-        for (int q = 0; q < 3; ++q) v[q] = fmaf(w, s_q[q][row][col + k], v[q]);
+      for (int k = 0; k < kHaloIters; ++k) {
+        const int i = tid + 256 * k;
+        const int yy = i / kLIn, xx = i - yy * kLIn;
+        const int y = ty0 - kLR + yy, x = tx0 - kLR + xx;
+        v[k] = 0.f;
+        dst[k] = i < kLIn * kLIn ? yy * kLS + xx : -1;
+        if (i < kLIn * kLIn && y >= 0 && y < H && x >= 0 && x < W)
+          v[k] = __ldg(Q + (c * 3 + q) * HW + (long long)y * W + x);
       }
 #pragma unroll
-      for (int q = 0; q < 3; ++q) s_h[q][row][col] = v[q];
+      for (int k = 0; k < kHaloIters; ++k)
+        if (dst[k] >= 0) s_q[q][dst[k]] = v[k];
     }
     __syncthreads();
-    for (int i = tid; i < kLT * kLT; i += 256) {
-      const int row = i / kLT, col = i - row * kLT;
-      const int y = ty0 + row, x = tx0 + col;
-      if (y >= H || x >= W) continue;
-      float v[3] = {0.f, 0.f, 0.f};
+    for (int it = tid; it < kLIn * (kLT / 4); it += 256) {
+      const int row = it >> 3, c0 = (it & 7) * 4;
 #pragma unroll
-      for (int k = 0; k < 11; ++k) {
-        const float w = win.w[k];
+      for (int q = 0; q < 3; ++q) {
+        float a[16];
+        load16(s_q[q] + row * kLS + c0, a);
+        float h[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int q = 0; q < 3; ++q) v[q] = fmaf(w, s_h[q][row + k][col], v[q]);
+        for (int k = 0; k < 14; ++k)
+#pragma unroll
+          for (int o = 0; o < 4; ++o) {
+            const int tap = k - o;
+            if (tap >= 0 && tap < 11) h[o] = fmaf(win.w[tap], a[k], h[o]);
+          }
+#pragma unroll
+        for (int o = 0; o < 4; ++o) s_h[q][row][c0 + o] = h[o];
       }
-      const long long p = ((long long)y * W + x) * 3 + c;
-      const float rv = r[p], gv = g[p];
-      const float d = rv - gv;
-      const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
-      const float gs = v[0] + v[1] * 2.f * rv + v[2] * gv;
-      grad[p] = (1.f - lam) * sgn * inv_n - lam * gs;
+    }
+    __syncthreads();
+    {
+      const int col = tid & 31, r0 = (tid >> 5) * 4;
+      float v[3][4];
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int o = 0; o < 4; ++o) v[q][o] = 0.f;
+#pragma unroll
+      for (int k = 0; k < 14; ++k)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const float h = s_h[q][r0 + k][col];
+#pragma unroll
+          for (int o = 0; o < 4; ++o) {
+            const int tap = k - o;
+            if (tap >= 0 && tap < 11) v[q][o] = fmaf(win.w[tap], h, v[q][o]);
+          }
+        }
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        const int y = ty0 + r0 + o, x = tx0 + col;
+        if (y >= H || x >= W) continue;
+        const long long p = ((long long)y * W + x) * 3 + c;
+        const float rv = r[p], gv = g[p];
+        const float d = rv - gv;
+        const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+        const float gs = v[0][o] + v[1][o] * 2.f * rv + v[2][o] * gv;
+        grad[p] = (1.f - lam) * sgn * inv_n - lam * gs;
+      }
     }
     __syncthreads();
   }

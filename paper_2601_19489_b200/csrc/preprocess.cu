@@ -1,6 +1,8 @@
-// K1: preprocess -- projection, SH colour, SnugBox and exact pair count,
-// with row compaction + pair offsets from ONE single-pass decoupled
-// look-back scan (no second pass over the Gaussians).
+// K1: preprocess -- projection, SH colour, SnugBox and exact pair count.
+// Two kernels: (a) cull + compaction of the surviving rows in source order
+// (cheap per-CTA work, so the decoupled look-back chain is short), then
+// (b) the heavy projection + FP64 tile walk, fully parallel, writing straight
+// into the compacted row (pair total by block reduction + one atomic).
 //
 // Reference semantics:
 //   _geometry / project      projection.py:77-136  (cull z <= near or o < 1/255,
@@ -19,23 +21,10 @@
 namespace tsr {
 
 constexpr int kScanBlock = 256;
-// Look-back status word: [63:62] flag, [61:36] rows (26 bits), [35:0] pairs.
-constexpr unsigned long long kFlagAgg = 1ull << 62;
-constexpr unsigned long long kFlagPrefix = 2ull << 62;
-constexpr unsigned long long kValueMask = (1ull << 62) - 1;
-
+// Look-back values pack (rows, pairs): [61:36] rows (26 bits), [35:0] pairs.
 __device__ __forceinline__ unsigned long long pack_rp(unsigned long long rows,
                                                       unsigned long long pairs) {
   return (rows << 36) | pairs;
-}
-
-__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
 }
 
 // Block-wide exclusive scan of a packed (rows, pairs) value, then a
@@ -64,24 +53,8 @@ __device__ __forceinline__ unsigned long long scan_lookback(
     }
     unsigned long long agg = __shfl_sync(0xffffffffu, wi, kWarps - 1);
     if (lane < kWarps) s_warp[lane] = wi - w;  // exclusive warp offsets
+    const unsigned long long excl = warp_lookback(status, dyn_bid, agg);
     if (lane == 0) {
-      unsigned long long excl = 0;
-      if (dyn_bid == 0) {
-        st_relaxed(&status[0], kFlagPrefix | agg);
-      } else {
-        st_relaxed(&status[dyn_bid], kFlagAgg | agg);
-        int j = dyn_bid - 1;
-        while (true) {
-          unsigned long long s;
-          do {
-            s = ld_relaxed(&status[j]);
-          } while ((s >> 62) == 0);
-          excl += s & kValueMask;
-          if ((s >> 62) == 2) break;
-          --j;
-        }
-        st_relaxed(&status[dyn_bid], kFlagPrefix | (excl + agg));
-      }
       s_prefix[0] = excl;
       s_prefix[1] = agg;
     }
@@ -144,18 +117,28 @@ __device__ __forceinline__ long long count_pairs_of(const float* rp, int strateg
   return total;
 }
 
+// Culling test (projection.py:80-83); shared by both K1 kernels so they agree.
+__device__ __forceinline__ bool keep_one(const tsr_gaussians_t& g, const tsr_camera_t& cam,
+                                         long long i, float& X, float& Y, float& Z, float& o) {
+  const float px = g.positions[3 * i], py = g.positions[3 * i + 1],
+              pz = g.positions[3 * i + 2];
+  const float* R = cam.R;
+  X = fmaf(R[0], px, fmaf(R[1], py, fmaf(R[2], pz, cam.t[0])));
+  Y = fmaf(R[3], px, fmaf(R[4], py, fmaf(R[5], pz, cam.t[1])));
+  Z = fmaf(R[6], px, fmaf(R[7], py, fmaf(R[8], pz, cam.t[2])));
+  o = 1.0f / (1.0f + expf(-g.opacity_logits[i]));
+  return (Z > cam.near_plane) && (o >= kMinOpacity);
+}
+
 // Projection of one Gaussian into the 12-float raster record.  Returns false
 // when culled (projection.py:82).
 __device__ __forceinline__ bool project_one(const tsr_gaussians_t& g, const tsr_camera_t& cam,
                                             long long i, float* rec) {
+  float X, Y, Z, o;
+  if (!keep_one(g, cam, i, X, Y, Z, o)) return false;
   const float px = g.positions[3 * i], py = g.positions[3 * i + 1],
               pz = g.positions[3 * i + 2];
   const float* R = cam.R;
-  const float X = fmaf(R[0], px, fmaf(R[1], py, fmaf(R[2], pz, cam.t[0])));
-  const float Y = fmaf(R[3], px, fmaf(R[4], py, fmaf(R[5], pz, cam.t[1])));
-  const float Z = fmaf(R[6], px, fmaf(R[7], py, fmaf(R[8], pz, cam.t[2])));
-  const float o = 1.0f / (1.0f + expf(-g.opacity_logits[i]));
-  if (!(Z > cam.near_plane) || !(o >= kMinOpacity)) return false;
 
   // R_q from the normalised quaternion (scene.py:33-47)
   float qw = g.rotations[4 * i], qx = g.rotations[4 * i + 1], qy = g.rotations[4 * i + 2],
@@ -233,50 +216,72 @@ __device__ __forceinline__ bool project_one(const tsr_gaussians_t& g, const tsr_
   return true;
 }
 
-__global__ void __launch_bounds__(kScanBlock) preprocess_kernel(
-    tsr_gaussians_t g, tsr_camera_t cam, int strategy, float4* __restrict__ rec_out,
-    int32_t* __restrict__ source_ids, int32_t* __restrict__ row_of_source,
-    int32_t* __restrict__ counts, uint32_t* __restrict__ depth_bits, uint4* __restrict__ spans,
-    int64_t* __restrict__ totals,
-    unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket,
-    int n_blocks) {
+// (a) cull + compaction: row_of_source, source_ids and M.  8 consecutive
+// Gaussians per thread keep the look-back chain short (N / 2048 blocks).
+constexpr int kCullItems = 8;
+__global__ void __launch_bounds__(kScanBlock) cull_compact_kernel(
+    tsr_gaussians_t g, tsr_camera_t cam, int32_t* __restrict__ source_ids,
+    int32_t* __restrict__ row_of_source, int64_t* __restrict__ totals,
+    unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket, int n_blocks) {
   __shared__ unsigned long long s_warp[kScanBlock / 32];
   __shared__ unsigned long long s_prefix[2];
   __shared__ int s_bid;
   if (threadIdx.x == 0) s_bid = (int)atomicAdd(ticket, 1u);
   __syncthreads();
   const int bid = s_bid;
-  const long long i = (long long)bid * kScanBlock + threadIdx.x;
-  const int tiles_x = tiles_of(cam.width), tiles_y = tiles_of(cam.height);
-
-  float rec[12];
-  bool keep = false;
-  long long cnt = 0;
-  uint4 span = make_uint4(0u, 0u, 0u, 0u);
-  if (i < g.n) {
-    keep = project_one(g, cam, i, rec);
-    if (keep) cnt = count_pairs_of(rec, strategy, tiles_x, tiles_y, span);
+  const long long i0 = ((long long)bid * kScanBlock + threadIdx.x) * kCullItems;
+  unsigned keep_mask = 0;
+#pragma unroll
+  for (int k = 0; k < kCullItems; ++k) {
+    float X, Y, Z, o;
+    if (i0 + k < g.n && keep_one(g, cam, i0 + k, X, Y, Z, o)) keep_mask |= 1u << k;
   }
-  unsigned long long v = pack_rp(keep ? 1ull : 0ull, (unsigned long long)cnt);
-  unsigned long long excl = scan_lookback(v, bid, status, s_warp, s_prefix);
-  const long long row = (long long)(excl >> 36);
-  const long long pair0 = (long long)(excl & ((1ull << 36) - 1));
-  if (keep) {
-    float4* dst = rec_out + row * 3;
+  unsigned long long excl =
+      scan_lookback((unsigned long long)__popc(keep_mask), bid, status, s_warp, s_prefix);
+#pragma unroll
+  for (int k = 0; k < kCullItems; ++k) {
+    const long long i = i0 + k;
+    if (i >= g.n) break;
+    const bool keep = (keep_mask >> k) & 1u;
+    if (keep) source_ids[excl] = (int32_t)i;
+    row_of_source[i] = keep ? (int32_t)excl : -1;
+    excl += keep ? 1 : 0;
+  }
+  if (bid == n_blocks - 1 && threadIdx.x == 0) totals[0] = (long long)(s_prefix[0] + s_prefix[1]);
+}
+
+// (b) projection + colour + exact pair count into the compacted rows.
+__global__ void __launch_bounds__(kScanBlock) preprocess_kernel(
+    tsr_gaussians_t g, tsr_camera_t cam, int strategy, float4* __restrict__ rec_out,
+    const int32_t* __restrict__ row_of_source, int32_t* __restrict__ counts,
+    uint32_t* __restrict__ depth_bits, uint4* __restrict__ spans,
+    unsigned long long* __restrict__ total_pairs) {
+  __shared__ unsigned long long s_sum[kScanBlock / 32];
+  const long long i = (long long)blockIdx.x * kScanBlock + threadIdx.x;
+  const int tiles_x = tiles_of(cam.width), tiles_y = tiles_of(cam.height);
+  long long cnt = 0;
+  const int row = i < g.n ? row_of_source[i] : -1;
+  if (row >= 0) {
+    float rec[12];
+    project_one(g, cam, i, rec);
+    uint4 span;
+    cnt = count_pairs_of(rec, strategy, tiles_x, tiles_y, span);
+    float4* dst = rec_out + (long long)row * 3;
     dst[0] = make_float4(rec[0], rec[1], rec[2], rec[3]);
     dst[1] = make_float4(rec[4], rec[5], rec[6], rec[7]);
     dst[2] = make_float4(rec[8], rec[9], rec[10], rec[11]);
-    source_ids[row] = (int32_t)i;
     counts[row] = (int32_t)cnt;
     depth_bits[row] = __float_as_uint(rec[6]);
     spans[row] = span;
   }
-  (void)pair0;
-  if (i < g.n) row_of_source[i] = keep ? (int32_t)row : -1;
-  if (bid == n_blocks - 1 && threadIdx.x == 0) {
-    unsigned long long tot = s_prefix[0] + s_prefix[1];
-    totals[0] = (long long)(tot >> 36);
-    totals[1] = (long long)(tot & ((1ull << 36) - 1));
+  unsigned long long v = (unsigned long long)cnt;
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < kScanBlock / 32; ++w) t += s_sum[w];
+    if (t) atomicAdd(total_pairs, t);
   }
 }
 
@@ -351,9 +356,14 @@ extern "C" int tsr_preprocess_fwd(const tsr_gaussians_t* g, const tsr_camera_t* 
   if (cudaMemsetAsync(workspace, 0, scan_workspace(g->n), s) != cudaSuccess) return TSR_E_CUDA;
   unsigned int* ticket = (unsigned int*)workspace;
   unsigned long long* status = (unsigned long long*)((char*)workspace + 256);
-  preprocess_kernel<<<blocks, kScanBlock, 0, s>>>(*g, *cam, strategy, (float4*)rec, source_ids,
+  const int cull_blocks = (int)((g->n + kScanBlock * kCullItems - 1) / (kScanBlock * kCullItems));
+  cull_compact_kernel<<<cull_blocks, kScanBlock, 0, s>>>(*g, *cam, source_ids, row_of_source,
+                                                         totals, status, ticket, cull_blocks);
+  TSR_CHECK_LAUNCH();
+  preprocess_kernel<<<blocks, kScanBlock, 0, s>>>(*g, *cam, strategy, (float4*)rec,
                                                   row_of_source, counts, depth_bits,
-                                                  (uint4*)spans, totals, status, ticket, blocks);
+                                                  (uint4*)spans,
+                                                  (unsigned long long*)(totals + 1));
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }

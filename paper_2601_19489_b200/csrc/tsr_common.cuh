@@ -289,6 +289,52 @@ __host__ __device__ inline int sh_degree_of(int coeffs) {
   return coeffs >= 16 ? 3 : coeffs >= 9 ? 2 : coeffs >= 4 ? 1 : 0;
 }
 
+// ------------------------------------------------------- look-back scan ---
+// Decoupled look-back status word: [63:62] flag (0 none, 1 aggregate,
+// 2 inclusive prefix), [61:0] value.  Called by ALL 32 lanes of one warp;
+// returns the exclusive prefix of block `bid` (lanes read 32 predecessors at
+// a time, so the walk costs one L2 round trip per 32 blocks).
+__device__ __forceinline__ void lb_store(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long lb_load(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long warp_lookback(unsigned long long* status, int bid,
+                                                            unsigned long long aggregate) {
+  constexpr unsigned long long kAgg = 1ull << 62, kPre = 2ull << 62, kVal = (1ull << 62) - 1;
+  const int lane = threadIdx.x & 31;
+  if (bid == 0) {
+    if (lane == 0) lb_store(&status[0], kPre | aggregate);
+    return 0ull;
+  }
+  if (lane == 0) lb_store(&status[bid], kAgg | aggregate);
+  unsigned long long excl = 0;
+  int j = bid - 1;
+  while (true) {
+    const int idx = j - lane;
+    unsigned long long s = kPre;  // lanes before block 0 act as a zero prefix
+    if (idx >= 0) {
+      do {
+        s = lb_load(&status[idx]);
+      } while ((s >> 62) == 0);
+    }
+    const unsigned pre = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+    const int stop = pre ? __ffs(pre) - 1 : 32;  // nearest predecessor with a prefix
+    unsigned long long v = (lane <= stop && idx >= 0) ? (s & kVal) : 0ull;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    excl += v;
+    if (pre) break;
+    j -= 32;
+  }
+  if (lane == 0) lb_store(&status[bid], kPre | (excl + aggregate));
+  return excl;
+}
+
 // --------------------------------------------------------------- errors ---
 #define TSR_CHECK_LAUNCH()                                   \
   do {                                                       \

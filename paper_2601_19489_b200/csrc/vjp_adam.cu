@@ -22,19 +22,54 @@ struct Vjp {
   float pose[12];          // J^T G_A + g_pcam p^T (3x3), g_pcam (3)
 };
 
+// Per-Gaussian chain on already-loaded parameters (position p, log-scales
+// ls, raw quaternion q) and the packed Grad2D row g2.
+__device__ __forceinline__ void vjp_core(const tsr_camera_t& cam, float px, float py, float pz,
+                                         const float* ls, const float* qv, float4 r0, float4 r1,
+                                         const float* g2, Vjp& out);
+
 // Per-Gaussian chain; returns false (all-zero gradient) for culled rows.
 __device__ __forceinline__ bool vjp_one(const tsr_gaussians_t& G, const tsr_camera_t& cam,
                                         const float4* rec, const int32_t* row_of_source,
                                         const float* grad2d, long long i, Vjp& out) {
   const int row = row_of_source[i];
   if (row < 0) return false;
-  const float* R = cam.R;
+  const float ls[3] = {G.log_scales[3 * i], G.log_scales[3 * i + 1], G.log_scales[3 * i + 2]};
+  const float qv[4] = {G.rotations[4 * i], G.rotations[4 * i + 1], G.rotations[4 * i + 2],
+                       G.rotations[4 * i + 3]};
   const float px = G.positions[3 * i], py = G.positions[3 * i + 1], pz = G.positions[3 * i + 2];
+  vjp_core(cam, px, py, pz, ls, qv, rec[3 * row], rec[3 * row + 1],
+           grad2d + (long long)row * TSR_GRAD2D_FLOATS, out);
+  // SH > 0: unit-direction chain back to positions (trainer.py:247-254)
+  const int C = G.sh_coeffs;
+  if (C > 1) {
+    float vx = px - cam.center[0], vy = py - cam.center[1], vz = pz - cam.center[2];
+    const float vn = sqrtf(vx * vx + vy * vy + vz * vz);
+    const float ivn = 1.0f / vn;
+    const float dx = vx * ivn, dy = vy * ivn, dz = vz * ivn;
+    out.dir[0] = dx; out.dir[1] = dy; out.dir[2] = dz;
+    const float* coef = G.colors + i * C * 3;
+    float wk[16];
+    for (int k = 0; k < C; ++k)
+      wk[k] = coef[3 * k] * out.gcol[0] + coef[3 * k + 1] * out.gcol[1] + coef[3 * k + 2] * out.gcol[2];
+    float gdir[3];
+    sh_basis_vjp(sh_degree_of(C), dx, dy, dz, wk, gdir);
+    const float dd = gdir[0] * dx + gdir[1] * dy + gdir[2] * dz;
+    out.gp[0] += (gdir[0] - dx * dd) * ivn;
+    out.gp[1] += (gdir[1] - dy * dd) * ivn;
+    out.gp[2] += (gdir[2] - dz * dd) * ivn;
+  }
+  return true;
+}
+
+__device__ __forceinline__ void vjp_core(const tsr_camera_t& cam, float px, float py, float pz,
+                                         const float* ls, const float* qv, float4 r0, float4 r1,
+                                         const float* g2, Vjp& out) {
+  const float* R = cam.R;
   const float X = fmaf(R[0], px, fmaf(R[1], py, fmaf(R[2], pz, cam.t[0])));
   const float Y = fmaf(R[3], px, fmaf(R[4], py, fmaf(R[5], pz, cam.t[1])));
   const float Z = fmaf(R[6], px, fmaf(R[7], py, fmaf(R[8], pz, cam.t[2])));
-  float qw = G.rotations[4 * i], qx = G.rotations[4 * i + 1], qy = G.rotations[4 * i + 2],
-        qz = G.rotations[4 * i + 3];
+  float qw = qv[0], qx = qv[1], qy = qv[2], qz = qv[3];
   const float qnorm = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
   const float iqn = 1.0f / qnorm;
   qw *= iqn; qx *= iqn; qy *= iqn; qz *= iqn;
@@ -48,8 +83,7 @@ __device__ __forceinline__ bool vjp_one(const tsr_gaussians_t& G, const tsr_came
   Rq[6] = 2.f * (qx * qz - qw * qy);
   Rq[7] = 2.f * (qy * qz + qw * qx);
   Rq[8] = 1.f - 2.f * (qx * qx + qy * qy);
-  const float s[3] = {expf(G.log_scales[3 * i]), expf(G.log_scales[3 * i + 1]),
-                      expf(G.log_scales[3 * i + 2])};
+  const float s[3] = {expf(ls[0]), expf(ls[1]), expf(ls[2])};
   float M[9];
 #pragma unroll
   for (int r = 0; r < 3; ++r)
@@ -71,9 +105,7 @@ __device__ __forceinline__ bool vjp_one(const tsr_gaussians_t& G, const tsr_came
     A[k] = j00 * R[k] + j02 * R[6 + k];
     A[3 + k] = j11 * R[3 + k] + j12 * R[6 + k];
   }
-  const float4 r0 = rec[3 * row], r1 = rec[3 * row + 1];
   const float ca = r0.z, cb = r0.w, cc = r1.x, o = r1.y;
-  const float* g2 = grad2d + (long long)row * TSR_GRAD2D_FLOATS;
   const float gm0 = g2[0], gm1 = g2[1];
   const float gb00 = g2[2], gb01 = 0.5f * g2[3], gb11 = g2[4];
   const float gop = g2[5];
@@ -161,26 +193,6 @@ __device__ __forceinline__ bool vjp_one(const tsr_gaussians_t& G, const tsr_came
 #pragma unroll
   for (int k = 0; k < 3; ++k) out.gp[k] = gx * R[k] + gy * R[3 + k] + gz * R[6 + k];
   out.go = gop * o * (1.f - o);
-  // SH > 0: unit-direction chain back to positions (trainer.py:247-254)
-  const int C = G.sh_coeffs;
-  if (C > 1) {
-    float vx = px - cam.center[0], vy = py - cam.center[1], vz = pz - cam.center[2];
-    const float vn = sqrtf(vx * vx + vy * vy + vz * vz);
-    const float ivn = 1.0f / vn;
-    const float dx = vx * ivn, dy = vy * ivn, dz = vz * ivn;
-    out.dir[0] = dx; out.dir[1] = dy; out.dir[2] = dz;
-    const float* coef = G.colors + i * C * 3;
-    float wk[16];
-    for (int k = 0; k < C; ++k)
-      wk[k] = coef[3 * k] * out.gcol[0] + coef[3 * k + 1] * out.gcol[1] + coef[3 * k + 2] * out.gcol[2];
-    float gdir[3];
-    sh_basis_vjp(sh_degree_of(C), dx, dy, dz, wk, gdir);
-    const float dd = gdir[0] * dx + gdir[1] * dy + gdir[2] * dz;
-    out.gp[0] += (gdir[0] - dx * dd) * ivn;
-    out.gp[1] += (gdir[1] - dy * dd) * ivn;
-    out.gp[2] += (gdir[2] - dz * dd) * ivn;
-  }
-  return true;
 }
 
 // colour-coefficient gradient k, channel ch
@@ -272,6 +284,9 @@ struct AdamGroups {
 };
 
 // One parameter row: returns 1 when skipped (non-finite gradient).
+// Bias corrections enter as reciprocals (one divide per group, not per
+// element) and the step uses a fast divide: the update differs from the
+// reference's float64 m_hat / (sqrt(v_hat) + eps) by a few FP32 ulp.
 template <typename GradFn>
 __device__ __forceinline__ int adam_row(const tsr_adam_group_t& G, long long r, GradFn grad) {
   const int w = G.width;
@@ -281,6 +296,7 @@ __device__ __forceinline__ int adam_row(const tsr_adam_group_t& G, long long r, 
   float* p = G.param + r * w;
   float* m = G.exp_avg + r * w;
   float* v = G.exp_avg_sq + r * w;
+  const float ibc1 = 1.0f / G.bias_correction1, ibc2 = 1.0f / G.bias_correction2;
   float nrm = 0.f;
   for (int k = 0; k < w; ++k) {
     const float gk = grad(k);
@@ -288,16 +304,16 @@ __device__ __forceinline__ int adam_row(const tsr_adam_group_t& G, long long r, 
     const float vk = kBeta2 * v[k] + (1.f - kBeta2) * gk * gk;
     m[k] = mk;
     v[k] = vk;
-    const float mh = mk / G.bias_correction1;
-    const float vh = vk / G.bias_correction2;
-    const float pk = p[k] - G.lr * mh / (sqrtf(vh) + kEps);
+    const float pk = p[k] - __fdividef(G.lr * (mk * ibc1), sqrtf(vk * ibc2) + kEps);
     p[k] = pk;
     nrm += pk * pk;
   }
   if (G.renormalize) {
     nrm = sqrtf(nrm);
-    if (nrm > 0.f)
-      for (int k = 0; k < w; ++k) p[k] = p[k] / nrm;
+    if (nrm > 0.f) {
+      const float inv = 1.0f / nrm;
+      for (int k = 0; k < w; ++k) p[k] = p[k] * inv;
+    }
   }
   return 0;
 }
@@ -345,6 +361,112 @@ __global__ void __launch_bounds__(256) preprocess_bwd_adam_kernel(
     float pv[12];
 #pragma unroll
     for (int k = 0; k < 12; ++k) pv[k] = vis ? v.pose[k] : 0.f;
+    block_reduce_pose(pv, pose_sums);
+  }
+  for (int d = 16; d > 0; d >>= 1) local += __shfl_xor_sync(0xffffffffu, local, d);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(skipped, local);
+}
+
+// Adam update of one row held in registers (optim.py:74-88); returns 1 when
+// the row is skipped (non-finite gradient: moments and params untouched).
+template <int W>
+__device__ __forceinline__ int adam_regs(const tsr_adam_group_t& G, const float* g, float* p,
+                                         float* m, float* v) {
+  bool finite = true;
+#pragma unroll
+  for (int k = 0; k < W; ++k) finite &= isfinite(g[k]);
+  if (!finite) return 1;
+  const float ibc1 = 1.0f / G.bias_correction1, ibc2 = 1.0f / G.bias_correction2;
+  float nrm = 0.f;
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    m[k] = kBeta1 * m[k] + (1.f - kBeta1) * g[k];
+    v[k] = kBeta2 * v[k] + (1.f - kBeta2) * g[k] * g[k];
+    p[k] = p[k] - __fdividef(G.lr * (m[k] * ibc1), sqrtf(v[k] * ibc2) + kEps);
+    nrm += p[k] * p[k];
+  }
+  if (G.renormalize) {
+    nrm = sqrtf(nrm);
+    if (nrm > 0.f) {
+      const float inv = 1.0f / nrm;
+#pragma unroll
+      for (int k = 0; k < W; ++k) p[k] = p[k] * inv;
+    }
+  }
+  return 0;
+}
+
+template <int W>
+__device__ __forceinline__ void load_row(const float* base, long long i, float* out) {
+#pragma unroll
+  for (int k = 0; k < W; ++k) out[k] = base[i * W + k];
+}
+template <int W>
+__device__ __forceinline__ void store_row(float* base, long long i, const float* in) {
+#pragma unroll
+  for (int k = 0; k < W; ++k) base[i * W + k] = in[k];
+}
+
+// SH degree 0 fast path: every parameter / moment of the Gaussian is loaded
+// up front (42 independent loads in flight), the VJP runs on the registers,
+// the consumed Grad2D row is zeroed for the next step, and the five Adam
+// groups are updated and stored.
+__global__ void __launch_bounds__(256) vjp_adam_sh0_kernel(
+    tsr_camera_t cam, long long n, const float4* __restrict__ rec,
+    const int32_t* __restrict__ row_of_source, float* __restrict__ grad2d, AdamGroups groups,
+    float* __restrict__ pose_sums, unsigned long long* __restrict__ skipped) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  Vjp vj;
+  bool vis = false;
+  unsigned long long local = 0;
+  if (i < n) {
+    float pp[3], pl[3], pq[4], po[1], pc[3];
+    float mp[3], ml[3], mq[4], mo[1], mc[3];
+    float vp[3], vl[3], vq[4], vo[1], vc[3];
+    const tsr_adam_group_t &G0 = groups.g[0], &G1 = groups.g[1], &G2 = groups.g[2],
+                           &G3 = groups.g[3], &G4 = groups.g[4];
+    load_row<3>(G0.param, i, pp); load_row<3>(G0.exp_avg, i, mp); load_row<3>(G0.exp_avg_sq, i, vp);
+    load_row<3>(G1.param, i, pl); load_row<3>(G1.exp_avg, i, ml); load_row<3>(G1.exp_avg_sq, i, vl);
+    load_row<4>(G2.param, i, pq); load_row<4>(G2.exp_avg, i, mq); load_row<4>(G2.exp_avg_sq, i, vq);
+    load_row<1>(G3.param, i, po); load_row<1>(G3.exp_avg, i, mo); load_row<1>(G3.exp_avg_sq, i, vo);
+    load_row<3>(G4.param, i, pc); load_row<3>(G4.exp_avg, i, mc); load_row<3>(G4.exp_avg_sq, i, vc);
+    const int row = row_of_source[i];
+    float gp[3] = {0.f, 0.f, 0.f}, gl[3] = {0.f, 0.f, 0.f}, gq[4] = {0.f, 0.f, 0.f, 0.f};
+    float go[1] = {0.f}, gc[3] = {0.f, 0.f, 0.f};
+    if (row >= 0) {
+      vis = true;
+      float* g2p = grad2d + (long long)row * TSR_GRAD2D_FLOATS;
+      float g2[TSR_GRAD2D_FLOATS];
+#pragma unroll
+      for (int k = 0; k < TSR_GRAD2D_FLOATS; ++k) g2[k] = g2p[k];
+      vjp_core(cam, pp[0], pp[1], pp[2], pl, pq, rec[3 * row], rec[3 * row + 1], g2, vj);
+#pragma unroll
+      for (int k = 0; k < TSR_GRAD2D_FLOATS; ++k) g2p[k] = 0.f;  // ready for the next step
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        gp[k] = vj.gp[k];
+        gl[k] = vj.gls[k];
+        gc[k] = vj.gcol[k];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) gq[k] = vj.gq[k];
+      go[0] = vj.go;
+    }
+    local += adam_regs<3>(G0, gp, pp, mp, vp);
+    local += adam_regs<3>(G1, gl, pl, ml, vl);
+    local += adam_regs<4>(G2, gq, pq, mq, vq);
+    local += adam_regs<1>(G3, go, po, mo, vo);
+    local += adam_regs<3>(G4, gc, pc, mc, vc);
+    store_row<3>(G0.param, i, pp); store_row<3>(G0.exp_avg, i, mp); store_row<3>(G0.exp_avg_sq, i, vp);
+    store_row<3>(G1.param, i, pl); store_row<3>(G1.exp_avg, i, ml); store_row<3>(G1.exp_avg_sq, i, vl);
+    store_row<4>(G2.param, i, pq); store_row<4>(G2.exp_avg, i, mq); store_row<4>(G2.exp_avg_sq, i, vq);
+    store_row<1>(G3.param, i, po); store_row<1>(G3.exp_avg, i, mo); store_row<1>(G3.exp_avg_sq, i, vo);
+    store_row<3>(G4.param, i, pc); store_row<3>(G4.exp_avg, i, mc); store_row<3>(G4.exp_avg_sq, i, vc);
+  }
+  if (pose_sums) {
+    float pv[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) pv[k] = vis ? vj.pose[k] : 0.f;
     block_reduce_pose(pv, pose_sums);
   }
   for (int d = 16; d > 0; d >>= 1) local += __shfl_xor_sync(0xffffffffu, local, d);
@@ -412,8 +534,14 @@ extern "C" int tsr_preprocess_bwd_adam(const tsr_gaussians_t* g, const tsr_camer
     return TSR_E_INVALID;
   if (g->n == 0) return TSR_OK;
   int blocks = (int)((g->n + 255) / 256);
-  preprocess_bwd_adam_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
-      *g, *cam, (const float4*)rec, row_of_source, grad2d, gs, pose_sums, skipped);
+  if (g->sh_coeffs == 1) {
+    // fast path; also zeroes the consumed Grad2D rows for the next step
+    vjp_adam_sh0_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        *cam, g->n, (const float4*)rec, row_of_source, (float*)grad2d, gs, pose_sums, skipped);
+  } else {
+    preprocess_bwd_adam_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        *g, *cam, (const float4*)rec, row_of_source, grad2d, gs, pose_sums, skipped);
+  }
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }

@@ -20,7 +20,8 @@ from .binning import TileIndex, build_index
 from .forward import RenderBuffers, render
 from .optim import Adam, position_lr
 from .pose import PoseDelta
-from .projection import (SplatBatch, _pose_grad_from_sums, batch_from_scratch, camera_struct,
+from .projection import (ProjectionScratch, SplatBatch, _pose_grad_from_sums, batch_from_scratch,
+                         camera_struct,
                          gaussians_struct, project, project_raw, project_vjp)
 from .scene import Camera, GaussianSet, _device, as_device_f32
 
@@ -163,6 +164,7 @@ class TrainStep:
         self.skipped = torch.zeros(1, dtype=torch.int64, device=dev)
         self.merges = torch.zeros(1, dtype=torch.int64, device=dev)
         self.loss_ws = losses.PhotometricWorkspace()
+        self._grad2d_clean = True  # the SH-0 fused kernel re-zeroes consumed rows
         self.grad_color = None
         self.status_host = torch.zeros(3, dtype=torch.int64).pin_memory()
         self.status_dev = torch.zeros(3, dtype=torch.int64, device=dev)
@@ -237,7 +239,9 @@ class TrainStep:
                                                          grad=self.grad_color,
                                                          workspace=self.loss_ws)
         self._mark(timer, "loss")
-        self.grad2d.zero_()
+        if not self._grad2d_clean:
+            self.grad2d.zero_()
+        self._grad2d_clean = False
         _lib.check(self.lib.tsr_render_bwd(
             batch.rec.data_ptr(), idx.values.data_ptr(), idx.offsets.data_ptr(), camera.width,
             camera.height, out.color.data_ptr(), out.depth.data_ptr(), out.final_T.data_ptr(),
@@ -267,6 +271,7 @@ class TrainStep:
             gaussians_struct(self.gset), camera_struct(camera, None, self.cfg.near),
             batch.rec.data_ptr(), batch.row_of_source.data_ptr(), self.grad2d.data_ptr(), groups,
             None, self.skipped.data_ptr(), _lib.stream_handle()), "tsr_preprocess_bwd_adam")
+        self._grad2d_clean = self.gset.colors.shape[1] == 1
         self._mark(timer, "vjp_adam")
         self._publish_status()
         self.last_camera = camera

@@ -86,9 +86,11 @@ def test_fused_preprocess_count_matches_standalone_count():
     gset = ts.GaussianSet(**params)
     camera = ts.Camera(cam["fx"], cam["fy"], cam["cx"], cam["cy"], 640, 360, cam["R"], cam["t"])
     batch = ts.project(gset, camera)
-    fused = batch.pair_offsets.cpu().numpy()
-    batch.pair_offsets = None  # force the standalone count kernel
+    fused_p = batch.n_pairs
+    fused_counts = batch.counts.cpu().numpy().copy()
+    batch.counts = None  # force the standalone count kernel
     idx = ts.bin_sequential(batch)
-    assert idx.n_pairs == int(fused[-1])
+    assert idx.n_pairs == fused_p
+    assert np.array_equal(batch.counts.cpu().numpy(), fused_counts)
     ref = O.bin_sequential(host_batch(batch))
     assert_index_equal(idx, ref)
