@@ -387,6 +387,22 @@ def gpu_arm(args):
     bwd_ms = phases.get("backward", 0.0) - phases.get("loss", 0.0) * 0  # backward phase only
     bwd_ops = BACKWARD_OPS[0] * evals + BACKWARD_OPS[1] * blends
     achieved = bwd_ops / (bwd_ms * 1e-3) / 1e12 if bwd_ms > 0 else None
+    # HBM roofline of the fused projection-VJP + Adam kernel (N=1)
+    hbm_line = None
+    peaks = ROOT / "MEASURED_PEAKS.json"
+    hbm_peak = json.loads(peaks.read_text()).get("hbm_gbs") if peaks.exists() else None
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    if hbm_peak is None:
+        hbm_peak, hbm_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+    if world == 1 and phases.get("vjp_adam"):
+        n = len(gset)
+        algo = n * (14 * 4 * 6 + 4) + len(batch) * (10 * 4 * 2 + 32)
+        ach = algo / (phases["vjp_adam"] * 1e-3) / 1e9
+        hbm_line = {"kernel": "vjp_adam_sh0_kernel (K4b+K5)", "bound": "hbm", "achieved": ach,
+                    "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+                    "algorithmic_bytes": algo, "peak_source": hbm_src,
+                    "bytes_model": "per Gaussian p,m,v read+write (14 x 4 B x 6) + row index 4 B; per row "
+                                   "Grad2D read+zero (80 B) + rec 32 B"}
     traffic = None
     prof = ROOT / "profiles" / "backward_traffic.json"
     if prof.exists():
@@ -408,8 +424,9 @@ def gpu_arm(args):
                                   "clock (MEASURED_PEAKS.json has no FP32 figure)",
                      "ops_per_unit": {"per_eval": BACKWARD_OPS[0], "per_blend": BACKWARD_OPS[1]},
                      "units": {"evals": evals, "blends": blends, "pairs": pairs}},
+        "roofline_hbm": hbm_line,
         "phases_ms": {k: round(v, 4) for k, v in phases.items()},
-        "gpu_launches": 7 * args.steps,
+        "gpu_launches": stepper.kernels_per_step() * args.steps,
         "clocks": clock,
     }
     if e2e is not None:

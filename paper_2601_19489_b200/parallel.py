@@ -69,6 +69,10 @@ class ViewParallelStep(TrainStep):
         self.flat = torch.zeros(grad_numel(gset), dtype=torch.float32, device="cuda")
         self.grads = flat_grad_views(self.flat, gset)
 
+    def kernels_per_step(self, views: int = 1) -> int:
+        """Per view: K1-K4 + K4b; then one K5 (the NCCL allreduce is not ours)."""
+        return views * (super().kernels_per_step() - 1 + 1) + 1
+
     def step_views(self, cameras, gts, timer=None) -> torch.Tensor:
         if self.index is not None and cameras:
             self._poll_status(cameras[0])

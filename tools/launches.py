@@ -12,7 +12,7 @@ for r in rows[hi + 1:]:
     if len(r) <= vi:
         continue
     v = float(r[vi].replace(",", ""))
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+    scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(r[ui], 1.0)
     agg.setdefault(r[ki].split("(")[0][:70], []).append(v * scale)
 tot = sum(sum(v) for v in agg.values())
 for k, v in agg.items():
