@@ -25,7 +25,8 @@
 
 namespace tsr {
 
-constexpr int kBwdWarps = 8;
+constexpr int kBwdWarps = 4;
+constexpr int kBwdThreads = 32 * kBwdWarps;
 
 __device__ __forceinline__ float fast_rcp(float x) {
   float y;
@@ -38,7 +39,7 @@ __device__ __forceinline__ float fast_rcp(float x) {
 constexpr int kPixSlots = kTilePixels + 1;
 constexpr int kListPad = 32;
 
-__global__ void __launch_bounds__(256) render_bwd_kernel(
+__global__ void __launch_bounds__(kBwdThreads) render_bwd_kernel(
     const float4* __restrict__ rec, const int32_t* __restrict__ values,
     const int64_t* __restrict__ offsets, int width, int height, int tiles_x,
     const float* __restrict__ color, const float* __restrict__ depth,
@@ -52,6 +53,7 @@ __global__ void __launch_bounds__(256) render_bwd_kernel(
   __shared__ unsigned short s_list[kBwdWarps][kTilePixels + 2 * kListPad];
   __shared__ float2 s_tr[kBwdWarps][kTilePixels + kListPad];  // (T_ckpt, R_ckpt)
   __shared__ int s_maxnc;
+  __shared__ int s_next_group;
 
   const int tile = blockIdx.x;
   const long long start = offsets[tile], end = offsets[tile + 1];
@@ -59,8 +61,16 @@ __global__ void __launch_bounds__(256) render_bwd_kernel(
   if (n == 0) return;
   const int tyi = tile / tiles_x, txi = tile - tyi * tiles_x;
   const int tid = threadIdx.x;
-  {
-    const int x = txi * kTile + (tid & 15), y = tyi * kTile + (tid >> 4);
+  if (tid == 0) {
+    s_maxnc = 0;
+    s_next_group = kBwdWarps;  // groups 0..kBwdWarps-1 are taken statically
+    s_pa[kTilePixels] = make_float4(-65536.f, -65536.f, 0.f, __int_as_float(0));  // finite: gauss -> 0
+    s_pb[kTilePixels] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  bool nz = false;
+  int my_max = 0;
+  for (int px = tid; px < kTilePixels; px += kBwdThreads) {
+    const int x = txi * kTile + (px & 15), y = tyi * kTile + (px >> 4);
     const bool inside = x < width && y < height;
     float gr = 0.f, gg = 0.f, gb = 0.f, gd = 0.f, gt = 0.f, k = 0.f;
     int nc = 0;
@@ -75,19 +85,15 @@ __global__ void __launch_bounds__(256) render_bwd_kernel(
       k = gr * color[3 * pix] + gg * color[3 * pix + 1] + gb * color[3 * pix + 2] +
           gd * depth[pix] + gt * final_T[pix];
     }
-    const bool nz = (gr != 0.f) || (gg != 0.f) || (gb != 0.f) || (gd != 0.f) || (gt != 0.f);
-    s_pa[tid] = make_float4((float)x + 0.5f, (float)y + 0.5f, gd, __int_as_float(nc));
-    s_pb[tid] = make_float4(gr, gg, gb, k);
-    if (tid == 0) {
-      s_maxnc = 0;
-      s_pa[kTilePixels] = make_float4(-65536.f, -65536.f, 0.f, __int_as_float(0));  // finite: gauss -> 0, no NaN
-      s_pb[kTilePixels] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    // tile skipped when its upstream is all zero (backward.py:156-158)
-    if (!__syncthreads_or(nz)) return;
-    atomicMax(&s_maxnc, nc);
-    if (tid == 0) atomicAdd(merges, (unsigned long long)n);
+    nz |= (gr != 0.f) || (gg != 0.f) || (gb != 0.f) || (gd != 0.f) || (gt != 0.f);
+    my_max = max(my_max, nc);
+    s_pa[px] = make_float4((float)x + 0.5f, (float)y + 0.5f, gd, __int_as_float(nc));
+    s_pb[px] = make_float4(gr, gg, gb, k);
   }
+  // tile skipped when its upstream is all zero (backward.py:156-158)
+  if (!__syncthreads_or(nz)) return;
+  atomicMax(&s_maxnc, my_max);
+  if (tid == 0) atomicAdd(merges, (unsigned long long)n);
   __syncthreads();
   const int n_groups = (s_maxnc + kGroup - 1) / kGroup;
   const int lane = tid & 31, warp = tid >> 5;
@@ -99,7 +105,7 @@ __global__ void __launch_bounds__(256) render_bwd_kernel(
   float2* tr = s_tr[warp];
   list[lane] = (unsigned short)kTilePixels;  // leading sentinels (pipeline fill)
 
-  for (int g = warp; g < n_groups; g += kBwdWarps) {
+  for (int g = warp; g < n_groups;) {
     const int p0 = g * kGroup;
     // invalid lanes (p >= n) never satisfy p < n_considered <= n
     const int p = p0 + lane < n ? p0 + lane : 0x7fffffff;
@@ -183,6 +189,10 @@ __global__ void __launch_bounds__(256) render_bwd_kernel(
       acc_d = fmaf(w, pa.z, acc_d);
     }
     __syncwarp();
+    // next group: dynamic, so warps of a tile finish together
+    int next = 0;
+    if (lane == 0) next = atomicAdd(&s_next_group, 1);
+    g = __shfl_sync(0xffffffffu, next, 0);
     const bool touched = (acc_o != 0.f) | (acc_r != 0.f) | (acc_g != 0.f) | (acc_bl != 0.f) |
                          (acc_d != 0.f) | (acc_a != 0.f);
     if (p0 + lane < n && touched) {
@@ -215,7 +225,7 @@ extern "C" int tsr_render_bwd(const float* rec, const int32_t* values, const int
   if (width <= 0 || height <= 0 || !grad_color || !merges) return TSR_E_INVALID;
   if (ckpt && !ckpt_base) return TSR_E_INVALID;
   const int tx = tiles_of(width), ty = tiles_of(height);
-  render_bwd_kernel<<<tx * ty, 256, 0, (cudaStream_t)stream>>>(
+  render_bwd_kernel<<<tx * ty, kBwdThreads, 0, (cudaStream_t)stream>>>(
       (const float4*)rec, values, offsets, width, height, tx, color, depth, final_T,
       n_considered, ckpt, ckpt_base, grad_color, grad_depth, grad_final_T, grad2d, merges);
   TSR_CHECK_LAUNCH();
