@@ -135,44 +135,55 @@ __global__ void __launch_bounds__(kSB) radix_hist_kernel(const uint32_t* __restr
   hist[(long long)threadIdx.x * n_ctas + blockIdx.x] = s_h[threadIdx.x];
 }
 
+// Block-wide exclusive scan helper (256 threads): returns the exclusive
+// prefix of v; *total receives the block sum.
+template <typename T>
+__device__ __forceinline__ T block_excl_scan_256(T v, T* s_w, T* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T incl = v;
+#pragma unroll
+  for (int k = 1; k < 32; k <<= 1) {
+    const T t = __shfl_up_sync(0xffffffffu, incl, k);
+    if (lane >= k) incl += t;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  T pre = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < kSB / 32; ++w) {
+    pre += w < warp ? s_w[w] : (T)0;
+    tot += s_w[w];
+  }
+  *total = tot;
+  return pre + incl - v;
+}
+
 // Per-digit exclusive scan over CTAs (one CTA per digit): hist_scan[d][c] =
-// sum_{c' < c} hist[d][c'], digit_total[d] = sum_c hist[d][c].  The digit
-// prefix is added by the scatter kernel (no look-back chain needed).
+// sum_{c' < c} hist[d][c'], digit_total[d] = sum_c hist[d][c].  Each thread
+// scans a contiguous run of the row, then one block scan (no loop of
+// barriers); the digit prefix is added by the scatter kernel.
+constexpr int kRowPerThread = 64;  // rows up to 16384 CTAs (33.5M pairs at 8 items)
 __global__ void __launch_bounds__(kSB) radix_digit_scan_kernel(const uint32_t* __restrict__ hist,
                                                                int n_ctas,
                                                                uint32_t* __restrict__ hist_scan,
                                                                uint32_t* __restrict__ digit_total) {
   __shared__ uint32_t s_w[kSB / 32];
-  __shared__ uint32_t s_carry;
-  const int d = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int d = blockIdx.x;
   const uint32_t* row = hist + (long long)d * n_ctas;
   uint32_t* out = hist_scan + (long long)d * n_ctas;
-  if (tid == 0) s_carry = 0;
-  __syncthreads();
-  for (int b0 = 0; b0 < n_ctas; b0 += kSB) {
-    const int c = b0 + tid;
-    const uint32_t v = c < n_ctas ? row[c] : 0u;
-    uint32_t incl = v;
-#pragma unroll
-    for (int k = 1; k < 32; k <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, k);
-      if (lane >= k) incl += t;
-    }
-    if (lane == 31) s_w[warp] = incl;
-    __syncthreads();
-    uint32_t wpre = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < kSB / 32; ++w) {
-      wpre += w < warp ? s_w[w] : 0u;
-      tot += s_w[w];
-    }
-    const uint32_t carry = s_carry;
-    if (c < n_ctas) out[c] = carry + wpre + incl - v;
-    __syncthreads();
-    if (tid == 0) s_carry = carry + tot;
-    __syncthreads();
+  const int per = (n_ctas + kSB - 1) / kSB;  // <= kRowPerThread (checked by the host)
+  const int c0 = threadIdx.x * per;
+  const int c1 = min(c0 + per, n_ctas);
+  uint32_t sum = 0;
+  for (int c = c0; c < c1; ++c) sum += row[c];
+  uint32_t total;
+  uint32_t run = block_excl_scan_256(sum, s_w, &total);
+  for (int c = c0; c < c1; ++c) {  // second read hits L1
+    const uint32_t v = row[c];
+    out[c] = run;
+    run += v;
   }
-  if (tid == 0) digit_total[d] = s_carry;
+  if (threadIdx.x == 0) digit_total[d] = total;
 }
 
 // Stable scatter.  Ranking: warp w owns items [base + 32 ITEMS w, ...),
@@ -366,38 +377,30 @@ __global__ void __launch_bounds__(kSB) tile_ranges_kernel(const int64_t* __restr
 }
 
 // ckpt_base[t] = sum_{u<t} floor(n_u / 32) (forward.py:139-145: one record
-// per completed 32-entry group); ckpt_base[T] = total records.
-__global__ void __launch_bounds__(1024) ckpt_base_kernel(const int64_t* __restrict__ offsets,
-                                                         int n_tiles,
-                                                         int64_t* __restrict__ ckpt_base) {
-  __shared__ long long s_w[32];
-  __shared__ long long s_carry;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
-  for (int base = 0; base < n_tiles; base += 1024) {
-    const int t = base + threadIdx.x;
-    const long long v = t < n_tiles ? (offsets[t + 1] - offsets[t]) / kGroup : 0;
-    long long incl = v;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const long long y = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += y;
-    }
-    if (lane == 31) s_w[warp] = incl;
-    __syncthreads();
-    long long pre = 0, tot = 0;
-    for (int w = 0; w < 32; ++w) {
-      pre += w < warp ? s_w[w] : 0;
-      tot += s_w[w];
-    }
-    const long long carry = s_carry;
-    if (t < n_tiles) ckpt_base[t] = carry + pre + incl - v;
-    __syncthreads();
-    if (threadIdx.x == 0) s_carry = carry + tot;
-    __syncthreads();
+// per completed 32-entry group); ckpt_base[T] = total records.  One CTA,
+// each thread a contiguous run of tiles (up to 65536 tiles).
+constexpr int kTilesPerThread = 64;
+__global__ void __launch_bounds__(kSB) ckpt_base_kernel(const int64_t* __restrict__ offsets,
+                                                        int n_tiles,
+                                                        int64_t* __restrict__ ckpt_base) {
+  __shared__ long long s_w[kSB / 32];
+  const int per = (n_tiles + kSB - 1) / kSB;
+  const int t0 = threadIdx.x * per;
+  long long sum = 0;
+  for (int k = 0; k < per; ++k) {
+    const int t = t0 + k;
+    if (t < n_tiles) sum += (offsets[t + 1] - offsets[t]) / kGroup;
   }
-  if (threadIdx.x == 0) ckpt_base[n_tiles] = s_carry;
+  long long total;
+  long long run = block_excl_scan_256(sum, s_w, &total);
+  for (int k = 0; k < per; ++k) {
+    const int t = t0 + k;
+    if (t < n_tiles) {
+      ckpt_base[t] = run;
+      run += (offsets[t + 1] - offsets[t]) / kGroup;
+    }
+  }
+  if (threadIdx.x == 0) ckpt_base[n_tiles] = total;
 }
 
 // -------------------------------------------------------------- planning --
@@ -468,6 +471,7 @@ static int radix_pass_t(const uint32_t* kin, const V* vin, uint32_t* kout, V* vo
                         long long n_cap, int shift, IndexWorkspace& w, cudaStream_t s) {
   const int ctas = (int)((n_cap + kSB * ITEMS - 1) / (kSB * ITEMS));
   if (ctas == 0) return TSR_OK;
+  if (ctas > kSB * kRowPerThread) return TSR_E_INVALID;  // > 8.4M pairs per pass
   radix_hist_kernel<ITEMS><<<ctas, kSB, 0, s>>>(kin, n_dev, n_cap, shift, ctas, w.hist);
   TSR_CHECK_LAUNCH();
   radix_digit_scan_kernel<<<kBins, kSB, 0, s>>>(w.hist, ctas, w.hist_scan, w.digit_total);
@@ -565,7 +569,7 @@ extern "C" int tsr_build_index(const float* rec, const uint32_t* depth_bits, con
       keys, (const long long*)totals, p_cap, n_tiles, offsets);
   TSR_CHECK_LAUNCH();
   if (ckpt_base) {
-    ckpt_base_kernel<<<1, 1024, 0, s>>>(offsets, n_tiles, ckpt_base);
+    ckpt_base_kernel<<<1, kSB, 0, s>>>(offsets, n_tiles, ckpt_base);
     TSR_CHECK_LAUNCH();
   }
   return rc;

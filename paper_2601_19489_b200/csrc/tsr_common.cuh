@@ -61,20 +61,25 @@ __device__ __forceinline__ SplatF64 load_splat_f64(const float* rec) {
 }
 
 // _tile_span (binning.py:74-84): inclusive tile ids of the closed interval.
+// x / 16 == x * 0.0625 exactly in IEEE (power-of-two scaling rounds the same
+// exact value), so the FP64 division is replaced by a multiply.
 __device__ __forceinline__ void tile_span(double lo, double hi, int n_tiles,
                                           long long& t0, long long& t1) {
-  double c0 = ceil(dsub(ddiv(lo, 16.0), 1.0));
-  double f1 = floor(ddiv(hi, 16.0));
+  double c0 = ceil(dsub(dmul(lo, 0.0625), 1.0));
+  double f1 = floor(dmul(hi, 0.0625));
   long long i0 = (long long)c0;
   long long i1 = (long long)f1;
   t0 = i0 > 0 ? i0 : 0;
   t1 = i1 < (long long)(n_tiles - 1) ? i1 : (long long)(n_tiles - 1);
 }
 
-// compute_snugboxes (binning.py:87-104).
+// compute_snugboxes (binning.py:87-104).  Also carries the per-splat
+// invariants of the column walk (binning.py:189, 205-206): det, ymax_rel
+// (== ey), dx_up.
 struct SnugRect {
   double x_min, x_max, y_min, y_max;
   long long tx0, tx1, ty0, ty1;
+  double det, ymax_rel, dx_up;
 };
 
 __device__ __forceinline__ SnugRect snugbox(const SplatF64& s, int tiles_x, int tiles_y) {
@@ -88,6 +93,9 @@ __device__ __forceinline__ SnugRect snugbox(const SplatF64& s, int tiles_x, int 
   r.y_max = dadd(s.my, ey);
   tile_span(r.x_min, r.x_max, tiles_x, r.tx0, r.tx1);
   tile_span(r.y_min, r.y_max, tiles_y, r.ty0, r.ty1);
+  r.det = det;
+  r.ymax_rel = ey;  // sqrt((a*t)/det), the same expression as binning.py:205
+  r.dx_up = dmul(-ddiv(s.b, s.a), ey);
   return r;
 }
 
@@ -96,7 +104,6 @@ __device__ __forceinline__ SnugRect snugbox(const SplatF64& s, int tiles_x, int 
 __device__ __forceinline__ int column_rows(const SplatF64& s, const SnugRect& r,
                                            long long tx, int tiles_y,
                                            long long& ty0, long long& ty1) {
-  double det = dsub(dmul(s.a, s.c), dmul(s.b, s.b));
   double xl = dsub(npmax((double)(16 * tx), r.x_min), s.mx);
   double xr = dsub(npmin((double)(16 * tx + 16), r.x_max), s.mx);
   // y_bounds(dx): rad = sqrt(max(0, (b*b - a*c)*dx*dx + t*c))
@@ -111,10 +118,9 @@ __device__ __forceinline__ int column_rows(const SplatF64& s, const SnugRect& r,
   double hi_r = ddiv(dadd(dmul(negb, xr), rad_r), s.c);
   double ylo = npmin(lo_l, lo_r);
   double yhi = npmax(hi_l, hi_r);
-  // global y tangent points
-  double ymax_rel = dsqrt(ddiv(dmul(s.a, s.t), det));
-  double dx_up = dmul(-ddiv(s.b, s.a), ymax_rel);
-  double dx_dn = -dx_up;
+  // global y tangent points (per-splat invariants hoisted into SnugRect)
+  const double ymax_rel = r.ymax_rel, dx_up = r.dx_up;
+  const double dx_dn = -dx_up;
   if (dx_up >= xl && dx_up <= xr) yhi = npmax(yhi, ymax_rel);
   if (dx_dn >= xl && dx_dn <= xr) ylo = npmin(ylo, -ymax_rel);
   long long a0, a1;
