@@ -1,24 +1,31 @@
 // K4: per-Gaussian raster backward (backward_per_gaussian, backward.py:137-223).
 //
-// One CTA per tile, 8 warps.  The tile list is cut into groups of 32 list
-// positions (CHECKPOINT_INTERVAL); a warp owns one group at a time, lane j
-// owning list position 32g+j (Taming-GS style: per-Gaussian parallel, no
-// per-pixel atomics).  For a pixel, lane j needs
-//   T_j = T_ckpt * prod_{i<j, part_i} (1 - alpha_i)       and
-//   R_j = Ktot + g_T T_f - K_ckpt - sum_{i<=j} w_i gc_i
-// where gc_i = <g_color, c_i> + g_depth d_i folds the colour and depth
-// suffixes of backward.py:195-205 into ONE scalar per pixel, giving
-//   dL/dalpha_j = T_j gc_j - R_j / (1 - alpha_j)
-// (the g_T channel is backward.py:170,204-205).  Both are computed by a
-// SYSTOLIC pipeline: the group's active pixels (n_considered > 32g) are
-// compacted into a list; at step t lane j works on list entry t-j and takes
-// (T, R) from lane j-1, which finished the same pixel one step earlier -- one
-// shuffle per quantity per step instead of a log-depth warp scan.
+// One CTA per tile, 4 warps.  Per pixel and list position p, with gc_p =
+// <g_color, c_p> + g_depth d_p folding the colour and depth suffixes of
+// backward.py:195-205 into ONE scalar per (pixel, splat):
+//   T_p = T_ckpt * prod_{i<p, part_i} (1 - alpha_i)
+//   R_p = Ktot + g_T T_f - K_ckpt - sum_{i<=p} w_i gc_i
+//   dL/dalpha_p = T_p gc_p - R_p / (1 - alpha_p)
+// (the g_T channel is backward.py:170,204-205).
+//
+// Systolic schedule.  A warp owns a SUPERGROUP of 64 list positions (two
+// 32-entry checkpoint groups, forward.py:28); lane j owns the adjacent pair
+// (64G + 2j, 64G + 2j + 1) and runs both of its splats on the same pixel in
+// one step: the alpha evaluation and every gradient accumulation are packed
+// FP32x2 instructions (FFMA2/FMUL2/FADD2, one issue slot for two splats);
+// only the T/R chain between the two splats is scalar.  The supergroup's
+// active pixels (n_considered > 64G) are compacted into a list; at step t
+// lane j works on list entry t - j and takes (T, R) from lane j - 1 by one
+// shuffle each.  Per position this halves both the issued instructions and
+// the pipeline fill of the one-splat-per-lane form.
+//
 // part = p < n_considered and alpha >= 1/255 (backward.py:189); capped alphas
 // get zero conic/mean/opacity gradient (backward.py:64,72).  Gradients
 // accumulate in registers and are merged once per (splat, tile) with atomics
-// (backward.py:214-222).  The group loop is bounded by the tile's maximum
-// n_considered: later groups contribute exactly zero.
+// (backward.py:214-222).  The supergroup loop is bounded by the tile's
+// maximum n_considered: later positions contribute exactly zero.  Alphas are
+// bit-identical to K3's (same operation sequence; the packed instructions
+// round each half exactly like the scalar ones).
 #include <cuda_runtime.h>
 
 #include "tsr_common.cuh"
@@ -27,6 +34,7 @@ namespace tsr {
 
 constexpr int kBwdWarps = 4;
 constexpr int kBwdThreads = 32 * kBwdWarps;
+constexpr int kSuper = 2 * kGroup;  // positions per warp work unit
 
 __device__ __forceinline__ float fast_rcp(float x) {
   float y;
@@ -34,12 +42,21 @@ __device__ __forceinline__ float fast_rcp(float x) {
   return y;
 }
 
+__device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
+__device__ __forceinline__ float2 bc(float x) { return make_float2(x, x); }
+
 // per-pixel record (index kTilePixels is a dummy pixel with n_considered 0,
 // used as the sentinel of the padded systolic lists)
 constexpr int kPixSlots = kTilePixels + 1;
 constexpr int kListPad = 32;
 
-__global__ void __launch_bounds__(kBwdThreads) render_bwd_kernel(
+struct PixRec {
+  float4 a;  // pixel centre x, y, g_depth, n_considered (int bits)
+  float4 b;  // g_r, g_g, g_b, Ktot + g_T T_final
+};
+
+template <bool kDepth>
+__global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
     const float4* __restrict__ rec, const int32_t* __restrict__ values,
     const int64_t* __restrict__ offsets, int width, int height, int tiles_x,
     const float* __restrict__ color, const float* __restrict__ depth,
@@ -48,12 +65,11 @@ __global__ void __launch_bounds__(kBwdThreads) render_bwd_kernel(
     const float* __restrict__ grad_color, const float* __restrict__ grad_depth,
     const float* __restrict__ grad_final_T, float* __restrict__ grad2d,
     unsigned long long* __restrict__ merges) {
-  __shared__ float4 s_pa[kPixSlots];  // pixel centre x, y, g_depth, n_considered (int bits)
-  __shared__ float4 s_pb[kPixSlots];  // g_r, g_g, g_b, Ktot + g_T T_final
-  __shared__ unsigned short s_list[kBwdWarps][kTilePixels + 2 * kListPad];
+  __shared__ PixRec s_pix[kPixSlots];
+  __shared__ unsigned short s_list[kBwdWarps][kTilePixels + 2 * kListPad];  // byte offsets
   __shared__ float2 s_tr[kBwdWarps][kTilePixels + kListPad];  // (T_ckpt, R_ckpt)
   __shared__ int s_maxnc;
-  __shared__ int s_next_group;
+  __shared__ int s_next;
 
   const int tile = blockIdx.x;
   const long long start = offsets[tile], end = offsets[tile + 1];
@@ -63,9 +79,9 @@ __global__ void __launch_bounds__(kBwdThreads) render_bwd_kernel(
   const int tid = threadIdx.x;
   if (tid == 0) {
     s_maxnc = 0;
-    s_next_group = kBwdWarps;  // groups 0..kBwdWarps-1 are taken statically
-    s_pa[kTilePixels] = make_float4(-65536.f, -65536.f, 0.f, __int_as_float(0));  // finite: gauss -> 0
-    s_pb[kTilePixels] = make_float4(0.f, 0.f, 0.f, 0.f);
+    s_next = kBwdWarps;  // supergroups 0..kBwdWarps-1 are taken statically
+    s_pix[kTilePixels].a = make_float4(-65536.f, -65536.f, 0.f, __int_as_float(0));  // gauss -> 0
+    s_pix[kTilePixels].b = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   bool nz = false;
   int my_max = 0;
@@ -79,134 +95,206 @@ __global__ void __launch_bounds__(kBwdThreads) render_bwd_kernel(
       gr = grad_color[3 * pix];
       gg = grad_color[3 * pix + 1];
       gb = grad_color[3 * pix + 2];
-      if (grad_depth) gd = grad_depth[pix];
+      if (kDepth && grad_depth) gd = grad_depth[pix];
       if (grad_final_T) gt = grad_final_T[pix];
       nc = n_considered[pix];
-      k = gr * color[3 * pix] + gg * color[3 * pix + 1] + gb * color[3 * pix + 2] +
-          gd * depth[pix] + gt * final_T[pix];
+      k = gr * color[3 * pix] + gg * color[3 * pix + 1] + gb * color[3 * pix + 2] + gt * final_T[pix];
+      if (kDepth) k += gd * depth[pix];
     }
     nz |= (gr != 0.f) || (gg != 0.f) || (gb != 0.f) || (gd != 0.f) || (gt != 0.f);
     my_max = max(my_max, nc);
-    s_pa[px] = make_float4((float)x + 0.5f, (float)y + 0.5f, gd, __int_as_float(nc));
-    s_pb[px] = make_float4(gr, gg, gb, k);
+    s_pix[px].a = make_float4((float)x + 0.5f, (float)y + 0.5f, gd, __int_as_float(nc));
+    s_pix[px].b = make_float4(gr, gg, gb, k);
   }
   // tile skipped when its upstream is all zero (backward.py:156-158)
   if (!__syncthreads_or(nz)) return;
   atomicMax(&s_maxnc, my_max);
   if (tid == 0) atomicAdd(merges, (unsigned long long)n);
   __syncthreads();
-  const int n_groups = (s_maxnc + kGroup - 1) / kGroup;
+  const int n_super = (s_maxnc + kSuper - 1) / kSuper;
   const int lane = tid & 31, warp = tid >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
-  const float mean_scale = -2.0f / kQScale;
   long long rbase = 0;
   if (ckpt_base) rbase = ckpt_base[tile];
   unsigned short* list = s_list[warp];
   float2* tr = s_tr[warp];
-  list[lane] = (unsigned short)kTilePixels;  // leading sentinels (pipeline fill)
+  const unsigned short kSentinel = (unsigned short)(kTilePixels * sizeof(PixRec));
+  list[lane] = kSentinel;  // leading sentinels (pipeline fill)
+  const char* pix_base = reinterpret_cast<const char*>(s_pix);
 
-  for (int g = warp; g < n_groups;) {
-    const int p0 = g * kGroup;
-    // invalid lanes (p >= n) never satisfy p < n_considered <= n
-    const int p = p0 + lane < n ? p0 + lane : 0x7fffffff;
-    float mx = 0.f, my = 0.f, a = 0.f, b = 0.f, c = 0.f, o = 0.f, cr = 0.f, cg = 0.f,
-          cb = 0.f, dep = 0.f;
-    int row = 0;
-    if (p0 + lane < n) {
-      row = values[start + p0 + lane];
-      const float4 r0 = __ldg(rec + 3 * row), r1 = __ldg(rec + 3 * row + 1),
-                   r2 = __ldg(rec + 3 * row + 2);
-      mx = r0.x; my = r0.y;
-      a = __fmul_rn(r0.z, kQScale);
-      b = __fmul_rn(r0.w, kQScale);
-      c = __fmul_rn(r1.x, kQScale);
-      o = r1.y; dep = r1.z;
-      cr = r2.x; cg = r2.y; cb = r2.z;
+  for (int G = warp; G < n_super;) {
+    const int P0 = G * kSuper;
+    const int p = P0 + 2 * lane;  // this lane's first position; second is p + 1
+    // splat pair (invalid positions >= n never satisfy p < n_considered <= n)
+    float2 mxn = bc(0.f), myn = bc(0.f), ca = bc(0.f), cb = bc(0.f), cc = bc(0.f), op = bc(0.f);
+    float2 cr = bc(0.f), cg = bc(0.f), cbl = bc(0.f), dep = bc(0.f);
+    int row0 = -1, row1 = -1;
+    if (p < n) row0 = values[start + p];
+    if (p + 1 < n) row1 = values[start + p + 1];
+    if (row0 >= 0) {
+      const float4 r0 = __ldg(rec + 3 * row0), r1 = __ldg(rec + 3 * row0 + 1),
+                   r2 = __ldg(rec + 3 * row0 + 2);
+      mxn.x = -r0.x; myn.x = -r0.y;
+      ca.x = __fmul_rn(r0.z, kQScale);
+      cb.x = __fmul_rn(r0.w, kQScale);
+      cc.x = __fmul_rn(r1.x, kQScale);
+      op.x = r1.y; dep.x = r1.z;
+      cr.x = r2.x; cg.x = r2.y; cbl.x = r2.z;
     }
-    // prologue: compact the pixels that entered this group, with their
-    // checkpoint state (T0, R0 = Ktot + g_T T_f - K_ckpt)
-    int n_act = 0;
-    for (int base = 0; base < kTilePixels; base += 32) {
-      const int px = base + lane;
-      const bool act = __float_as_int(s_pa[px].w) > p0;
-      const unsigned bal = __ballot_sync(0xffffffffu, act);
-      if (act) {
-        const int kk = n_act + __popc(bal & lt_mask);
-        float T0 = 1.f, K0 = 0.f;
-        const float4 gv = s_pb[px];
-        if (g > 0) {
-          const float* src = ckpt + (rbase + g - 1) * (5 * kTilePixels) + px;
-          T0 = src[0];
-          K0 = gv.x * src[kTilePixels] + gv.y * src[2 * kTilePixels] +
-               gv.z * src[3 * kTilePixels] + s_pa[px].z * src[4 * kTilePixels];
+    if (row1 >= 0) {
+      const float4 r0 = __ldg(rec + 3 * row1), r1 = __ldg(rec + 3 * row1 + 1),
+                   r2 = __ldg(rec + 3 * row1 + 2);
+      mxn.y = -r0.x; myn.y = -r0.y;
+      ca.y = __fmul_rn(r0.z, kQScale);
+      cb.y = __fmul_rn(r0.w, kQScale);
+      cc.y = __fmul_rn(r1.x, kQScale);
+      op.y = r1.y; dep.y = r1.z;
+      cr.y = r2.x; cg.y = r2.y; cbl.y = r2.z;
+    }
+    // prologue: compact the pixels that entered this supergroup, with their
+    // checkpoint state (T0, R0 = Ktot + g_T T_f - K_ckpt).  All checkpoint
+    // loads of a lane are issued before any is consumed.
+    {
+      const float* src0 = G > 0 ? ckpt + (rbase + 2 * G - 1) * (5 * kTilePixels) : nullptr;
+      bool act[kTilePixels / 32];
+      float cT[kTilePixels / 32], c1[kTilePixels / 32], c2[kTilePixels / 32],
+          c3[kTilePixels / 32], c4[kTilePixels / 32];
+#pragma unroll
+      for (int s = 0; s < kTilePixels / 32; ++s) {
+        const int px = 32 * s + lane;
+        act[s] = __float_as_int(s_pix[px].a.w) > P0;
+        cT[s] = 1.f; c1[s] = c2[s] = c3[s] = c4[s] = 0.f;
+        if (src0 && act[s]) {
+          cT[s] = src0[px];
+          c1[s] = src0[kTilePixels + px];
+          c2[s] = src0[2 * kTilePixels + px];
+          c3[s] = src0[3 * kTilePixels + px];
+          if (kDepth) c4[s] = src0[4 * kTilePixels + px];
         }
-        list[kListPad + kk] = (unsigned short)px;
-        tr[kk] = make_float2(T0, gv.w - K0);
       }
-      n_act += __popc(bal);
-    }
-    list[kListPad + n_act + lane] = (unsigned short)kTilePixels;  // trailing sentinels
-    __syncwarp();
+      int n_act = 0;
+#pragma unroll
+      for (int s = 0; s < kTilePixels / 32; ++s) {
+        const int px = 32 * s + lane;
+        const unsigned bal = __ballot_sync(0xffffffffu, act[s]);
+        if (act[s]) {
+          const int kk = n_act + __popc(bal & lt_mask);
+          const PixRec pr = s_pix[px];
+          float K0 = pr.b.x * c1[s] + pr.b.y * c2[s] + pr.b.z * c3[s];
+          if (kDepth) K0 += pr.a.z * c4[s];
+          list[kListPad + kk] = (unsigned short)(px * sizeof(PixRec));
+          tr[kk] = make_float2(cT[s], pr.b.w - K0);
+        }
+        n_act += __popc(bal);
+      }
+      list[kListPad + n_act + lane] = kSentinel;  // trailing sentinels
+      __syncwarp();
 
-    float acc_mx = 0.f, acc_my = 0.f, acc_a = 0.f, acc_b = 0.f, acc_c = 0.f, acc_o = 0.f;
-    float acc_r = 0.f, acc_g = 0.f, acc_bl = 0.f, acc_d = 0.f;
-    float T_out = 1.f, R_out = 0.f;
-    const unsigned short* my_list = list + kListPad - lane;
-    const int steps = n_act + 31;
-    for (int t = 0; t < steps; ++t) {
-      const int px = my_list[t];
-      float T_in = __shfl_up_sync(0xffffffffu, T_out, 1);
-      float R_in = __shfl_up_sync(0xffffffffu, R_out, 1);
-      if (lane == 0) {
-        const float2 v = tr[t];
-        T_in = v.x;
-        R_in = v.y;
+      float2 acc_a = bc(0.f), acc_b = bc(0.f), acc_c = bc(0.f), acc_mx = bc(0.f), acc_my = bc(0.f);
+      float2 acc_o = bc(0.f), acc_r = bc(0.f), acc_g = bc(0.f), acc_bl = bc(0.f), acc_d = bc(0.f);
+      float T_out = 1.f, R_out = 0.f;
+      const unsigned short* my_list = list + kListPad - lane;
+      const int steps = n_act + 31;
+      const float2 one = bc(1.f);
+      // software pipeline: the next step's pixel record is loaded while this
+      // step computes
+      float4 pa_n, pb_n;
+      {
+        const PixRec* pr = reinterpret_cast<const PixRec*>(pix_base + my_list[0]);
+        pa_n = pr->a;
+        pb_n = pr->b;
       }
-      const float4 pa = s_pa[px];
-      const float4 pb = s_pb[px];
-      AlphaEval e = eval_alpha(pa.x, pa.y, mx, my, a, b, c, o);
-      const bool part = (p < __float_as_int(pa.w)) && (e.alpha >= kMinAlpha);
-      const float om = __fsub_rn(1.f, e.alpha);
-      const float gcj = fmaf(pb.x, cr, fmaf(pb.y, cg, fmaf(pb.z, cb, pa.z * dep)));
-      const float w = part ? T_in * e.alpha : 0.f;
-      const float num = fmaf(-w, gcj, R_in);
-      const float dLda = fmaf(-num, fast_rcp(om), T_in * gcj);
-      T_out = part ? T_in * om : T_in;
-      R_out = num;
-      const bool live = part && !(e.raw > e.alpha);  // uncapped participant
-      const float ld = live ? dLda : 0.f;
-      const float gq = ld * e.alpha;  // x (-1/2) folded into the merge
-      const float gqdx = gq * e.dx, gqdy = gq * e.dy;
-      acc_a = fmaf(gqdx, e.dx, acc_a);
-      acc_b = fmaf(gqdx, e.dy, acc_b);
-      acc_c = fmaf(gqdy, e.dy, acc_c);
-      acc_mx = fmaf(gq, e.u, acc_mx);
-      acc_my = fmaf(gq, e.v, acc_my);
-      acc_o = fmaf(ld, e.gauss, acc_o);
-      acc_r = fmaf(w, pb.x, acc_r);
-      acc_g = fmaf(w, pb.y, acc_g);
-      acc_bl = fmaf(w, pb.z, acc_bl);
-      acc_d = fmaf(w, pa.z, acc_d);
-    }
-    __syncwarp();
-    // next group: dynamic, so warps of a tile finish together
-    int next = 0;
-    if (lane == 0) next = atomicAdd(&s_next_group, 1);
-    g = __shfl_sync(0xffffffffu, next, 0);
-    const bool touched = (acc_o != 0.f) | (acc_r != 0.f) | (acc_g != 0.f) | (acc_bl != 0.f) |
-                         (acc_d != 0.f) | (acc_a != 0.f);
-    if (p0 + lane < n && touched) {
-      float* dst = grad2d + (long long)row * TSR_GRAD2D_FLOATS;
-      atomicAdd(dst + 0, -0.5f * mean_scale * acc_mx);
-      atomicAdd(dst + 1, -0.5f * mean_scale * acc_my);
-      atomicAdd(dst + 2, -0.5f * acc_a);
-      atomicAdd(dst + 3, -acc_b);
-      atomicAdd(dst + 4, -0.5f * acc_c);
-      atomicAdd(dst + 5, acc_o);
-      atomicAdd(dst + 6, acc_r);
-      atomicAdd(dst + 7, acc_g);
-      atomicAdd(dst + 8, acc_bl);
-      atomicAdd(dst + 9, acc_d);
+      for (int t = 0; t < steps; ++t) {
+        const float4 pa = pa_n;
+        const float4 pb = pb_n;
+        {
+          const PixRec* pr = reinterpret_cast<const PixRec*>(pix_base + my_list[t + 1]);
+          pa_n = pr->a;
+          pb_n = pr->b;
+        }
+        float T_in = __shfl_up_sync(0xffffffffu, T_out, 1);
+        float R_in = __shfl_up_sync(0xffffffffu, R_out, 1);
+        if (lane == 0) {
+          const float2 v = tr[t];
+          T_in = v.x;
+          R_in = v.y;
+        }
+        const int nc = __float_as_int(pa.w);
+        // alpha of both splats at this pixel (eval_alpha, packed)
+        const float2 dx = __fadd2_rn(bc(pa.x), mxn);
+        const float2 dy = __fadd2_rn(bc(pa.y), myn);
+        const float2 u = __ffma2_rn(ca, dx, __fmul2_rn(cb, dy));
+        const float2 v = __ffma2_rn(cb, dx, __fmul2_rn(cc, dy));
+        const float2 qs = __ffma2_rn(dx, u, __fmul2_rn(dy, v));
+        const float2 gauss = f2(fast_exp2(qs.x), fast_exp2(qs.y));
+        const float2 raw = __fmul2_rn(op, gauss);
+        const float2 alpha = f2(fminf(kAlphaCap, raw.x), fminf(kAlphaCap, raw.y));
+        const bool part0 = (p < nc) && (alpha.x >= kMinAlpha);
+        const bool part1 = (p + 1 < nc) && (alpha.y >= kMinAlpha);
+        const float2 om = __fadd2_rn(one, f2(-alpha.x, -alpha.y));
+        float2 gc = __ffma2_rn(bc(pb.x), cr, __ffma2_rn(bc(pb.y), cg, __fmul2_rn(bc(pb.z), cbl)));
+        if (kDepth) gc = __ffma2_rn(bc(pa.z), dep, gc);
+        // scalar chain through the pair
+        const float w0 = part0 ? T_in * alpha.x : 0.f;
+        const float T1 = part0 ? T_in * om.x : T_in;
+        const float w1 = part1 ? T1 * alpha.y : 0.f;
+        T_out = part1 ? T1 * om.y : T1;
+        const float num0 = fmaf(-w0, gc.x, R_in);
+        const float num1 = fmaf(-w1, gc.y, num0);
+        R_out = num1;
+        const float2 rcp = f2(fast_rcp(om.x), fast_rcp(om.y));
+        const float2 dLda = __ffma2_rn(f2(-num0, -num1), rcp, __fmul2_rn(f2(T_in, T1), gc));
+        // uncapped participants only (backward.py:64,72); x(-1/2) folded into the merge
+        const float2 ld = f2(part0 && !(raw.x > alpha.x) ? dLda.x : 0.f,
+                             part1 && !(raw.y > alpha.y) ? dLda.y : 0.f);
+        const float2 gq = __fmul2_rn(ld, alpha);
+        const float2 gqdx = __fmul2_rn(gq, dx), gqdy = __fmul2_rn(gq, dy);
+        acc_a = __ffma2_rn(gqdx, dx, acc_a);
+        acc_b = __ffma2_rn(gqdx, dy, acc_b);
+        acc_c = __ffma2_rn(gqdy, dy, acc_c);
+        acc_mx = __ffma2_rn(gq, u, acc_mx);
+        acc_my = __ffma2_rn(gq, v, acc_my);
+        acc_o = __ffma2_rn(ld, gauss, acc_o);
+        const float2 w = f2(w0, w1);
+        acc_r = __ffma2_rn(w, bc(pb.x), acc_r);
+        acc_g = __ffma2_rn(w, bc(pb.y), acc_g);
+        acc_bl = __ffma2_rn(w, bc(pb.z), acc_bl);
+        if (kDepth) acc_d = __ffma2_rn(w, bc(pa.z), acc_d);
+      }
+      __syncwarp();
+      // next supergroup: dynamic, so the warps of a tile finish together
+      int next = 0;
+      if (lane == 0) next = atomicAdd(&s_next, 1);
+      G = __shfl_sync(0xffffffffu, next, 0);
+      const float ms = 2.0f / kQScale;  // d/dmean of the prescaled quadratic, x(-1/2)
+      if (row0 >= 0 && ((acc_o.x != 0.f) | (acc_r.x != 0.f) | (acc_g.x != 0.f) |
+                        (acc_bl.x != 0.f) | (acc_d.x != 0.f) | (acc_a.x != 0.f))) {
+        float* dst = grad2d + (long long)row0 * TSR_GRAD2D_FLOATS;
+        atomicAdd(dst + 0, ms * 0.5f * acc_mx.x);
+        atomicAdd(dst + 1, ms * 0.5f * acc_my.x);
+        atomicAdd(dst + 2, -0.5f * acc_a.x);
+        atomicAdd(dst + 3, -acc_b.x);
+        atomicAdd(dst + 4, -0.5f * acc_c.x);
+        atomicAdd(dst + 5, acc_o.x);
+        atomicAdd(dst + 6, acc_r.x);
+        atomicAdd(dst + 7, acc_g.x);
+        atomicAdd(dst + 8, acc_bl.x);
+        if (kDepth) atomicAdd(dst + 9, acc_d.x);
+      }
+      if (row1 >= 0 && ((acc_o.y != 0.f) | (acc_r.y != 0.f) | (acc_g.y != 0.f) |
+                        (acc_bl.y != 0.f) | (acc_d.y != 0.f) | (acc_a.y != 0.f))) {
+        float* dst = grad2d + (long long)row1 * TSR_GRAD2D_FLOATS;
+        atomicAdd(dst + 0, ms * 0.5f * acc_mx.y);
+        atomicAdd(dst + 1, ms * 0.5f * acc_my.y);
+        atomicAdd(dst + 2, -0.5f * acc_a.y);
+        atomicAdd(dst + 3, -acc_b.y);
+        atomicAdd(dst + 4, -0.5f * acc_c.y);
+        atomicAdd(dst + 5, acc_o.y);
+        atomicAdd(dst + 6, acc_r.y);
+        atomicAdd(dst + 7, acc_g.y);
+        atomicAdd(dst + 8, acc_bl.y);
+        if (kDepth) atomicAdd(dst + 9, acc_d.y);
+      }
     }
   }
 }
@@ -225,7 +313,8 @@ extern "C" int tsr_render_bwd(const float* rec, const int32_t* values, const int
   if (width <= 0 || height <= 0 || !grad_color || !merges) return TSR_E_INVALID;
   if (ckpt && !ckpt_base) return TSR_E_INVALID;
   const int tx = tiles_of(width), ty = tiles_of(height);
-  render_bwd_kernel<<<tx * ty, kBwdThreads, 0, (cudaStream_t)stream>>>(
+  auto* k = grad_depth ? render_bwd_kernel<true> : render_bwd_kernel<false>;
+  k<<<tx * ty, kBwdThreads, 0, (cudaStream_t)stream>>>(
       (const float4*)rec, values, offsets, width, height, tx, color, depth, final_T,
       n_considered, ckpt, ckpt_base, grad_color, grad_depth, grad_final_T, grad2d, merges);
   TSR_CHECK_LAUNCH();

@@ -1,21 +1,24 @@
 // K3: forward rasterizer (render, forward.py:87-161).
 //
-// One CTA per 16x16 tile, one thread per pixel.  The tile's depth-sorted list
-// is consumed in batches of 256 splats staged in shared memory (3 x float4
-// per splat: mean/opacity, prescaled conic/depth, colour).  Per pixel:
+// One CTA per 16x16 tile, 4 warps; warp w owns an 8x8 pixel block and each
+// lane a vertical pixel PAIR (rows y, y + 4), so every per-pixel operation of
+// the blend is one packed FP32x2 instruction (FFMA2/FMUL2/FADD2: one issue
+// slot for two pixels; dx is shared by the pair).  The tile's depth-sorted
+// list is consumed in batches of 256 splats staged in shared memory.  Per
+// pixel:
 //   alpha = min(0.99, o exp(-q/2)); blend iff alive && alpha >= 1/255;
 //   C += T alpha c; D += T alpha d; T *= 1 - alpha; n_considered = k+1 while
 //   alive; alive &= T >= 1e-4 AFTER blending (forward.py:125-138).
-// Termination: a warp stops scanning a batch once its 32 pixels are dead
-// (warp-level early exit) and the CTA stops at the next batch boundary once
-// all 256 are dead (forward.py:141-145).
-// Culling: a warp owns a 16x2 pixel strip.  For each chunk of 32 staged
-// splats every lane tests one splat against the strip with the exact minimum
-// of its quadratic over the strip's pixel-centre rectangle (min_q_box,
-// binning.py:241-259, in FP32 with a safety margin); only splats that can
-// reach alpha >= 1/255 somewhere in the strip are evaluated.  A skipped splat
-// provably leaves T, C, D unchanged, so the outputs are identical;
-// n_considered is restored from the termination position.
+// Termination: a warp stops scanning once its 64 pixels are dead (warp-level
+// early exit) and the CTA stops at the next batch boundary once all 256 are
+// dead (forward.py:141-145).
+// Culling: for each chunk of 32 staged splats every lane tests one splat
+// against the warp's 8x8 block with the exact minimum of its quadratic over
+// the block's pixel-centre rectangle (min_q_box, binning.py:241-259, in FP32
+// with a safety margin); only splats that can reach alpha >= 1/255 somewhere
+// in the block are evaluated.  A skipped splat provably leaves T, C, D
+// unchanged, so the outputs are identical; n_considered is restored from the
+// termination position.
 // Checkpoints (forward.py:139-140): after every 32nd list position the state
 // (T, C, D) is stored for each pixel that consumed that position -- exactly
 // the records the per-Gaussian backward reads (it enters group g of a pixel
@@ -46,116 +49,168 @@ __device__ __forceinline__ bool strip_hit(float mx, float my, float a, float b, 
   return qmin <= fmaf(t, 1.001f, 1e-3f);
 }
 
-// One list entry for one pixel, branch-free (predicated): the warp executes
-// it in lockstep, so a per-lane branch would only add reconvergence cost.
-__device__ __forceinline__ void blend_one(const float4 g, const float4 c, const float4 col,
-                                          float pxf, float pyf, int pos, bool& alive, float& T,
-                                          float& Cr, float& Cg, float& Cb, float& D,
-                                          int& ncontrib, int& ncons) {
-  AlphaEval e = eval_alpha(pxf, pyf, g.x, g.y, c.x, c.y, c.z, g.z);
-  const bool blend = alive && (e.alpha >= kMinAlpha);
-  const float w = blend ? T * e.alpha : 0.f;
-  Cr = fmaf(w, col.x, Cr);
-  Cg = fmaf(w, col.y, Cg);
-  Cb = fmaf(w, col.z, Cb);
-  D = fmaf(w, col.w, D);
-  T = blend ? T * (1.f - e.alpha) : T;
-  ncontrib += blend ? 1 : 0;
-  ncons = alive ? pos + 1 : ncons;
-  alive = alive && (T >= kTTerminate);
+__device__ __forceinline__ float2 bc2(float x) { return make_float2(x, x); }
+
+// One list entry for a vertical pixel pair (same x, rows y and y + 4) of one
+// lane, branch-free (predicated): the warp executes it in lockstep.  dx is
+// shared; every other per-pixel operation is one packed FP32x2 instruction.
+// The alpha sequence is eval_alpha's, so K4 reproduces these alphas bitwise.
+struct PixPair {
+  float2 T, Cr, Cg, Cb, D;
+  int nc0, nc1, ncons0, ncons1;
+  bool alive0, alive1;
+};
+
+__device__ __forceinline__ void blend_pair(const float4 g, const float4 c, const float4 col,
+                                           float pxf, float2 pyf, int pos, PixPair& s) {
+  const float dx = __fsub_rn(pxf, g.x);
+  const float2 dy = __fadd2_rn(pyf, bc2(-g.y));
+  const float2 u = __ffma2_rn(bc2(c.x), bc2(dx), __fmul2_rn(bc2(c.y), dy));
+  const float2 v = __ffma2_rn(bc2(c.y), bc2(dx), __fmul2_rn(bc2(c.z), dy));
+  const float2 qs = __ffma2_rn(bc2(dx), u, __fmul2_rn(dy, v));
+  const float2 raw = __fmul2_rn(bc2(g.z), make_float2(fast_exp2(qs.x), fast_exp2(qs.y)));
+  const float2 alpha = make_float2(fminf(kAlphaCap, raw.x), fminf(kAlphaCap, raw.y));
+  const bool b0 = s.alive0 && (alpha.x >= kMinAlpha);
+  const bool b1 = s.alive1 && (alpha.y >= kMinAlpha);
+  const float2 wt = __fmul2_rn(s.T, alpha);
+  const float2 w = make_float2(b0 ? wt.x : 0.f, b1 ? wt.y : 0.f);
+  s.Cr = __ffma2_rn(w, bc2(col.x), s.Cr);
+  s.Cg = __ffma2_rn(w, bc2(col.y), s.Cg);
+  s.Cb = __ffma2_rn(w, bc2(col.z), s.Cb);
+  s.D = __ffma2_rn(w, bc2(col.w), s.D);
+  const float2 Tn = __fmul2_rn(s.T, __fadd2_rn(bc2(1.f), make_float2(-alpha.x, -alpha.y)));
+  s.T = make_float2(b0 ? Tn.x : s.T.x, b1 ? Tn.y : s.T.y);
+  s.nc0 += b0 ? 1 : 0;
+  s.nc1 += b1 ? 1 : 0;
+  s.ncons0 = s.alive0 ? pos + 1 : s.ncons0;
+  s.ncons1 = s.alive1 ? pos + 1 : s.ncons1;
+  s.alive0 = s.alive0 && (s.T.x >= kTTerminate);
+  s.alive1 = s.alive1 && (s.T.y >= kTTerminate);
 }
 
+// 4 warps; warp w owns the 8x8 block (bx, by) = (w & 1, w >> 1) of the tile;
+// lane l owns pixels (8 bx + (l & 7), 8 by + (l >> 3)) and the one 4 rows below.
+constexpr int kFwdThreads = 128;
+constexpr int kBatch = 256;
+
 template <bool kCkpt>
-__global__ void __launch_bounds__(256) render_fwd_kernel(
+__global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
     const float4* __restrict__ rec, const int32_t* __restrict__ values,
     const int64_t* __restrict__ offsets, int width, int height, int tiles_x, float bg_r,
     float bg_g, float bg_b, float* __restrict__ out_color, float* __restrict__ out_depth,
     float* __restrict__ out_T, int32_t* __restrict__ out_ncontrib,
     int32_t* __restrict__ out_ncons, float* __restrict__ ckpt,
     const int64_t* __restrict__ ckpt_base) {
-  __shared__ float4 s_geo[256];
-  __shared__ float4 s_con[256];
-  __shared__ float4 s_col[256];
-  __shared__ float4 s_raw[256];   // a, b, c (unscaled), level t
+  __shared__ float4 s_geo[kBatch];  // mx, my, opacity, depth
+  __shared__ float4 s_con[kBatch];  // prescaled conic a', b', c'
+  __shared__ float4 s_col[kBatch];  // r, g, b, depth
+  __shared__ float4 s_raw[kBatch];  // a, b, c (unscaled), level t
 
   const int tile = blockIdx.x;
   const int tyi = tile / tiles_x, txi = tile - tyi * tiles_x;
   const int tid = threadIdx.x;
-  const int lx = tid & 15, ly = tid >> 4;
-  const int x = txi * kTile + lx, y = tyi * kTile + ly;
-  const bool inside = x < width && y < height;
-  const float pxf = (float)x + 0.5f, pyf = (float)y + 0.5f;
-  const int lane = tid & 31;
-  // this warp's strip of pixel centres (rows 2w, 2w+1 of the tile)
-  const float sx0 = (float)(txi * kTile) + 0.5f, sy0 = (float)(tyi * kTile + 2 * (tid >> 5)) + 0.5f;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int bx = warp & 1, by = warp >> 1;
+  const int lx = 8 * bx + (lane & 7), ly0 = 8 * by + (lane >> 3), ly1 = ly0 + 4;
+  const int x = txi * kTile + lx, y0 = tyi * kTile + ly0, y1 = tyi * kTile + ly1;
+  const bool in0 = x < width && y0 < height, in1 = x < width && y1 < height;
+  const float pxf = (float)x + 0.5f;
+  const float2 pyf = make_float2((float)y0 + 0.5f, (float)y1 + 0.5f);
+  // this warp's block of pixel centres
+  const float sx0 = (float)(txi * kTile + 8 * bx) + 0.5f, sy0 = (float)(tyi * kTile + 8 * by) + 0.5f;
   const long long start = offsets[tile], end = offsets[tile + 1];
   const int n = (int)(end - start);
-  float* ck = nullptr;
-  if (kCkpt) ck = ckpt + ckpt_base[tile] * (5 * kTilePixels) + tid;
+  float* ck0 = nullptr;
+  if (kCkpt) ck0 = ckpt + ckpt_base[tile] * (5 * kTilePixels) + ly0 * kTile + lx;
 
-  float T = 1.f, Cr = 0.f, Cg = 0.f, Cb = 0.f, D = 0.f;
-  int ncontrib = 0, ncons = 0;
-  bool alive = inside;
+  PixPair s;
+  s.T = bc2(1.f);
+  s.Cr = s.Cg = s.Cb = s.D = bc2(0.f);
+  s.nc0 = s.nc1 = s.ncons0 = s.ncons1 = 0;
+  s.alive0 = in0;
+  s.alive1 = in1;
 
-  for (int b0 = 0; b0 < n; b0 += 256) {
-    if (!__syncthreads_or(alive)) break;
-    const int k = b0 + tid;
-    if (k < n) {
-      const int row = values[start + k];
-      const float4 r0 = __ldg(rec + 3 * row), r1 = __ldg(rec + 3 * row + 1),
-                   r2 = __ldg(rec + 3 * row + 2);
-      s_geo[tid] = make_float4(r0.x, r0.y, r1.y, r1.z);
-      s_con[tid] = make_float4(__fmul_rn(r0.z, kQScale), __fmul_rn(r0.w, kQScale),
+  for (int b0 = 0; b0 < n; b0 += kBatch) {
+    if (!__syncthreads_or(s.alive0 || s.alive1)) break;
+#pragma unroll
+    for (int h = 0; h < kBatch / kFwdThreads; ++h) {
+      const int i = tid + h * kFwdThreads;
+      const int k = b0 + i;
+      if (k < n) {
+        const int row = values[start + k];
+        const float4 r0 = __ldg(rec + 3 * row), r1 = __ldg(rec + 3 * row + 1),
+                     r2 = __ldg(rec + 3 * row + 2);
+        s_geo[i] = make_float4(r0.x, r0.y, r1.y, r1.z);
+        s_con[i] = make_float4(__fmul_rn(r0.z, kQScale), __fmul_rn(r0.w, kQScale),
                                __fmul_rn(r1.x, kQScale), 0.f);
-      s_col[tid] = make_float4(r2.x, r2.y, r2.z, r1.z);
-      s_raw[tid] = make_float4(r0.z, r0.w, r1.x, r1.w);
+        s_col[i] = make_float4(r2.x, r2.y, r2.z, r1.z);
+        s_raw[i] = make_float4(r0.z, r0.w, r1.x, r1.w);
+      }
     }
     __syncthreads();
-    const int cnt = min(256, n - b0);
+    const int cnt = min(kBatch, n - b0);
     // chunks of 32 list positions == one checkpoint interval
     for (int c0 = 0; c0 < cnt; c0 += kGroup) {
-      if (!__any_sync(0xffffffffu, alive)) break;  // warp-level early exit
+      if (!__any_sync(0xffffffffu, s.alive0 || s.alive1)) break;  // warp-level early exit
       const int cend = min(kGroup, cnt - c0);
       const int pos0 = b0 + c0;
-      // lane j tests splat c0 + j against this warp's 16x2 strip
+      // lane j tests splat c0 + j against this warp's 8x8 block
       bool hit = false;
       if (lane < cend) {
         const float4 g = s_geo[c0 + lane], rw = s_raw[c0 + lane];
-        hit = strip_hit(g.x, g.y, rw.x, rw.y, rw.z, rw.w, sx0, sx0 + 15.f, sy0, sy0 + 1.f);
+        hit = strip_hit(g.x, g.y, rw.x, rw.y, rw.z, rw.w, sx0, sx0 + 7.f, sy0, sy0 + 7.f);
       }
       unsigned mask = __ballot_sync(0xffffffffu, hit);
       while (mask) {
         const int j = __ffs(mask) - 1;
         mask &= mask - 1u;
-        blend_one(s_geo[c0 + j], s_con[c0 + j], s_col[c0 + j], pxf, pyf, pos0 + j, alive, T, Cr,
-                  Cg, Cb, D, ncontrib, ncons);
+        blend_pair(s_geo[c0 + j], s_con[c0 + j], s_col[c0 + j], pxf, pyf, pos0 + j, s);
       }
-      if (cend == kGroup) {
-        // consumed position pos0+31 <=> still alive, or died exactly there
-        if (kCkpt && (alive || ncons == pos0 + kGroup)) {
-          // state after list position pos0+31 -> record (pos0+32)/32 - 1
-          float* dst = ck + (long long)(pos0 >> 5) * (5 * kTilePixels);
-          dst[0] = T;
-          dst[kTilePixels] = Cr;
-          dst[2 * kTilePixels] = Cg;
-          dst[3 * kTilePixels] = Cb;
-          dst[4 * kTilePixels] = D;
+      if (kCkpt && cend == kGroup) {
+        // state after list position pos0+31 -> record (pos0+32)/32 - 1, for
+        // each pixel that consumed that position (still alive, or died there)
+        float* dst = ck0 + (long long)(pos0 >> 5) * (5 * kTilePixels);
+        if (s.alive0 || s.ncons0 == pos0 + kGroup) {
+          dst[0] = s.T.x;
+          dst[kTilePixels] = s.Cr.x;
+          dst[2 * kTilePixels] = s.Cg.x;
+          dst[3 * kTilePixels] = s.Cb.x;
+          dst[4 * kTilePixels] = s.D.x;
+        }
+        if (s.alive1 || s.ncons1 == pos0 + kGroup) {
+          dst += 4 * kTile;
+          dst[0] = s.T.y;
+          dst[kTilePixels] = s.Cr.y;
+          dst[2 * kTilePixels] = s.Cg.y;
+          dst[3 * kTilePixels] = s.Cb.y;
+          dst[4 * kTilePixels] = s.D.y;
         }
       }
     }
   }
   // a pixel that never terminated considered the whole list (skipped
   // entries included); a terminated one stopped at its death position
-  if (alive) ncons = n;
-  if (inside) {
-    const long long pix = (long long)y * width + x;
-    out_color[3 * pix] = fmaf(T, bg_r, Cr);
-    out_color[3 * pix + 1] = fmaf(T, bg_g, Cg);
-    out_color[3 * pix + 2] = fmaf(T, bg_b, Cb);
-    out_depth[pix] = D;
-    out_T[pix] = T;
-    out_ncontrib[pix] = ncontrib;
-    out_ncons[pix] = ncons;
+  if (s.alive0) s.ncons0 = n;
+  if (s.alive1) s.ncons1 = n;
+  if (in0) {
+    const long long pix = (long long)y0 * width + x;
+    out_color[3 * pix] = fmaf(s.T.x, bg_r, s.Cr.x);
+    out_color[3 * pix + 1] = fmaf(s.T.x, bg_g, s.Cg.x);
+    out_color[3 * pix + 2] = fmaf(s.T.x, bg_b, s.Cb.x);
+    out_depth[pix] = s.D.x;
+    out_T[pix] = s.T.x;
+    out_ncontrib[pix] = s.nc0;
+    out_ncons[pix] = s.ncons0;
+  }
+  if (in1) {
+    const long long pix = (long long)y1 * width + x;
+    out_color[3 * pix] = fmaf(s.T.y, bg_r, s.Cr.y);
+    out_color[3 * pix + 1] = fmaf(s.T.y, bg_g, s.Cg.y);
+    out_color[3 * pix + 2] = fmaf(s.T.y, bg_b, s.Cb.y);
+    out_depth[pix] = s.D.y;
+    out_T[pix] = s.T.y;
+    out_ncontrib[pix] = s.nc1;
+    out_ncons[pix] = s.ncons1;
   }
 }
 
@@ -174,12 +229,12 @@ extern "C" int tsr_render_fwd(const float* rec, const int32_t* values, const int
   const int n_tiles = tx * ty;
   cudaStream_t s = (cudaStream_t)stream;
   if (ckpt) {
-    render_fwd_kernel<true><<<n_tiles, 256, 0, s>>>(
+    render_fwd_kernel<true><<<n_tiles, kFwdThreads, 0, s>>>(
         (const float4*)rec, values, offsets, width, height, tx, background_host[0],
         background_host[1], background_host[2], out_color, out_depth, out_final_T,
         out_n_contrib, out_n_considered, ckpt, ckpt_base);
   } else {
-    render_fwd_kernel<false><<<n_tiles, 256, 0, s>>>(
+    render_fwd_kernel<false><<<n_tiles, kFwdThreads, 0, s>>>(
         (const float4*)rec, values, offsets, width, height, tx, background_host[0],
         background_host[1], background_host[2], out_color, out_depth, out_final_T,
         out_n_contrib, out_n_considered, nullptr, nullptr);
