@@ -22,3 +22,9 @@ clean:
 	rm -rf build $(LIB)
 
 .PHONY: all clean
+
+# instrumented K2 (per-phase timestamps) for tools/k2_trace.py only
+trace: build/libtilesplat_b200_trace.so
+build/libtilesplat_b200_trace.so: $(SRCS) $(SRC_DIR)/tsr_common.cuh include/tilesplat_b200.h
+	@mkdir -p build
+	$(NVCC) -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC -cudart shared -Iinclude -DTSR_K2_TRACE -shared -o $@ $(SRCS)

@@ -100,11 +100,12 @@ int tsr_snugboxes(const float* rec, int64_t m, int32_t width, int32_t height,
                   int32_t* tile_rect, void* stream);
 
 /* ---------------------------------------------------------------- K2 ----
- * TileIndex (binning.py:137-158) without a 64-bit key sort: stable radix sort
- * of rows by depth bits -> rank-major emission of (tile, rank) pairs ->
- * stable radix sort by tile -> keys = tile << 32 | depth bits, values = row,
- * offsets[T+1], ckpt_base[T+1] = prefix of floor(n_tile / 32)
- * (forward.py:139-145).  M and P are read from `totals` on the device; the
+ * TileIndex (binning.py:137-158) without a 64-bit key sort: stable one-sweep
+ * radix sort of rows by depth bits -> rank-major emission of (tile, rank)
+ * pairs -> stable one-sweep radix sort by tile -> keys = tile << 32 | depth
+ * bits, values = row, offsets[T+1], ckpt_base[T+1] = offsets >> 5 (record r
+ * of tile t at ckpt_base[t] + r; the tiles' floor(n_tile / 32) records never
+ * overlap, forward.py:139-145).  M and P are read from `totals` on the device; the
  * capacities bound every buffer.  If P > p_cap the pairs are clamped and
  * *overflow (sticky, device int32) is set to 1: the caller re-runs with a
  * larger capacity. */

@@ -14,7 +14,8 @@ from pathlib import Path
 import torch
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libtilesplat_b200.so"
+# TSR_LIB overrides the path (instrumented builds for profiling only)
+LIB_PATH = Path(os.environ.get("TSR_LIB", _HERE / "libtilesplat_b200.so"))
 
 TSR_OK = 0
 TSR_E_INVALID = 1

@@ -8,8 +8,8 @@ then the on-device stable LSD radix sort on tile<<32 | f32 depth bits and the
 per-tile ranges (binning.py:137-158).
 
 Device layout: keys (P,) int64, values (P,) int32 batch rows, offsets (T+1,)
-int64.  `ckpt_base` (T+1,) int64 is the prefix of floor(n_tile/32): where each
-tile's forward checkpoints start (forward.py:139-145).
+int64.  `ckpt_base` (T+1,) int64 = offsets >> 5: where each tile's
+floor(n_tile/32) forward checkpoint records start (forward.py:139-145).
 """
 
 from __future__ import annotations

@@ -4,21 +4,37 @@
 // pair, emitted splat-major, and sorts it with a stable LSD radix sort
 // (binning.py:137-158), so ties resolve by emission (= batch row) order.  The
 // same order is produced here with far less traffic:
-//   1. stable LSD radix sort of the M rows by their 32-bit depth bits
-//      (4 x 8-bit passes over 8 B per row)  -> depth rank r of every row;
-//      rank order == (depth bits, row) order, exactly the reference's tie rule;
-//   2. exclusive scan of pair counts in rank order, then emission of
-//      (tile | depth bits, row) pairs rank-major from K1's compact column
-//      spans (no FP64 re-walk unless a splat's span did not fit the 16-byte
-//      record);
-//   3. stable LSD radix sort of the pairs by tile (8-bit digits, 2 passes
-//      for up to 65536 tiles) -> within a tile, rank order; the last pass
-//      writes the final int64 keys (tile << 32 | depth bits) and int32 rows;
-//   4. per-tile ranges (boundaries of the sorted keys) + checkpoint bases.
-// Every size (M, P) is read from device memory: the whole pipeline runs
-// without a host synchronisation and can be captured in a CUDA graph.  The
-// radix passes are the classic three-kernel form (CTA histograms -> one
-// decoupled look-back scan -> stable scatter ranked with __match_any_sync).
+//   1. stable LSD radix sort of the M rows by their 32-bit depth bits (8-bit
+//      digits; a pass whose digit is the same for every row -- e.g. the
+//      exponent byte -- is skipped) -> depth rank of every row; rank order
+//      == (depth bits, row) order, exactly the reference's tie rule;
+//   2. rank-major emission of (key = tile << 32 | depth bits, value = row)
+//      pairs from K1's compact column spans (rows whose span did not fit the
+//      16-byte record, and the load-balanced strategy, re-walk in FP64),
+//      staged in shared memory so every CTA stores its contiguous output
+//      range coalesced;
+//   3. stable LSD radix sort of the pairs by the tile bits only (1-2 passes
+//      of ~half the tile bits each): within a tile, rank order.  The last
+//      pass writes the final int64 keys and int32 rows;
+//   4. per-tile ranges from the boundaries of the sorted keys; checkpoint
+//      bases ckpt_base[t] = offsets[t] >> 5 (record r of tile t lives at
+//      ckpt_base[t] + r: floor((O + n) / 32) - floor(O / 32) >= floor(n / 32),
+//      so the tiles' record ranges never overlap and the total is <= P / 32).
+//
+// B200 shape: the whole index build is ONE persistent cooperative kernel (all
+// CTAs co-resident, 2 per SM) whose phases are separated by grid barriers.
+// At C2 sizes (1M rows, 4.4M pairs) every phase is latency-bound, so the
+// multi-kernel form (3 launches per radix pass) or a decoupled look-back
+// over ~1000 CTAs costs far more than the bytes.  A radix pass here is:
+//   count   each CTA histograms its contiguous slice (warp-aggregated smem
+//           atomics) -> cnt[cta][digit];                      grid barrier
+//   scan    CTA d scans digit column d over the CTAs -> colscan; grid barrier
+//   scatter each CTA re-reads its slice (L2-resident) in 4096-item sub-tiles,
+//           ranks them stably with a ballot multi-split, stages them digit-sorted
+//           in shared memory and stores each digit run coalesced at
+//           digit_start + colscan + running offset;           grid barrier
+// Every size (M, P) is read from device memory: nothing synchronises with
+// the host, and the call is one memset + one launch.
 #include <cuda_runtime.h>
 
 #include "tsr_common.cuh"
@@ -26,119 +42,103 @@
 namespace tsr {
 
 constexpr int kSB = 256;                 // threads per CTA
-constexpr int kSItemsMax = 16;           // items per thread (large passes)
-constexpr int kSTileMax = kSB * kSItemsMax;
 constexpr int kBins = 256;               // 8-bit digits
-// M-sized passes (1M rows) use 4 items/thread so ~1000 CTAs keep every SM
-// busy; P-sized passes use 8.
-__host__ __device__ constexpr int items_for(long long n_cap) {
-  return n_cap > (1ll << 22) ? 8 : 4;
+constexpr int kItems = 16;               // items per thread per sub-tile
+constexpr int kSub = kSB * kItems;       // 4096-item sub-tiles
+constexpr int kEmitPer = 2;              // ranks per thread per emission block
+constexpr int kEmitRanks = kSB * kEmitPer;
+constexpr int kStage = 4096;             // staged pairs per emission window
+constexpr int kDynSmem = 49152;          // staging: 4096 x (u64 key, u32 row)
+constexpr int kMaxGrid = 2048;
+constexpr int kMaxBarriers = 32;
+constexpr int kMaxTiles = 1 << 16;
+constexpr unsigned long long kNoPair = ~0ull;
+
+struct IndexArgs {
+  const float* rec;
+  const uint32_t* depth_bits;
+  const uint4* spans;
+  const int32_t* counts;
+  const long long* totals;
+  long long m_cap, p_cap;
+  int tiles_x, tiles_y, n_tiles, strategy, tile_bits;
+  int64_t* keys;
+  int32_t* values;
+  int64_t* offsets;
+  int64_t* ckpt_base;
+  int* overflow;
+  uint32_t *dk0, *dv0, *dk1, *dv1;   // depth sort ping-pong (M_cap)
+  unsigned long long *pk0, *pk1;     // pair keys (tile << 32 | depth bits) ping-pong (P_cap)
+  uint32_t *pv0, *pv1;               // pair values (row) ping-pong (P_cap)
+  uint32_t* cnt;                     // kMaxGrid x 256 per-CTA digit counts
+  uint32_t* colscan;                 // kMaxGrid x 256 exclusive prefix over CTAs
+  uint32_t* dtotal;                  // 256 digit totals of the current pass
+  unsigned long long* ptot;          // kMaxGrid emitted pairs per CTA
+  uint32_t* rank_cnt;                // M_cap pair count per rank
+  uint4* rank_span;                  // M_cap column-span record per rank
+  // zeroed by the per-call memset:
+  uint32_t* hist4;                   // 4 x 256 depth-byte histogram
+  unsigned int* bar;                 // kMaxBarriers arrival counters
+};
+
+struct SortSmem {
+  uint32_t cnt[kSB / 32][kBins];  // per-warp digit counters
+  uint32_t run[kBins];            // running global offset of each digit
+  uint32_t lbase[kBins];          // sub-tile-local start of each digit
+  uint32_t h[4][kBins];           // histograms
+  uint32_t w32[kSB / 32];
+  unsigned long long w64[kSB / 32];
+  int skip[4];
+};
+
+__device__ __forceinline__ long long clamp_ll(long long n, long long cap) {
+  return n < cap ? (n > 0 ? n : 0) : cap;
 }
 
-__device__ __forceinline__ long long clamp_n(const long long* n_dev, long long n_cap) {
-  const long long n = *n_dev;
-  return n < n_cap ? (n > 0 ? n : 0) : n_cap;
+// Grid barrier: all CTAs are co-resident (cooperative launch); counter b is
+// used once per call (zeroed by the memset), so no sense reversal is needed.
+#ifdef TSR_K2_TRACE
+// instrumented build only (tools/k2_trace.py): CTA 0 stamps every barrier
+__device__ unsigned long long tsr_k2_trace_buf[64];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
+#define TSR_TRACE_AT(i)                                                        \
+  do {                                                                         \
+    if (blockIdx.x == 0 && threadIdx.x == 0) tsr_k2_trace_buf[i] = gtimer(); \
+  } while (0)
+#else
+#define TSR_TRACE_AT(i) \
+  do {                 \
+  } while (0)
+#endif
 
-// ------------------------------------------------------------ scan (u32) --
-// Exclusive scan with a decoupled look-back; value(i) = in[gather ? gather[i] : i].
-constexpr int kScanItems = 8;
-constexpr int kScanTile = kSB * kScanItems;
-
-__global__ void __launch_bounds__(kSB) scan_u32_kernel(const uint32_t* __restrict__ in,
-                                                       const int32_t* __restrict__ gather,
-                                                       uint32_t* __restrict__ out,
-                                                       const long long* __restrict__ n_dev,
-                                                       long long n_cap,
-                                                       unsigned long long* __restrict__ status,
-                                                       unsigned int* __restrict__ ticket) {
-  __shared__ uint32_t s_warp[kSB / 32];
-  __shared__ uint32_t s_prefix;
-  __shared__ int s_bid;
-  if (threadIdx.x == 0) s_bid = (int)atomicAdd(ticket, 1u);
+__device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int n_ctas) {
   __syncthreads();
-  const int bid = s_bid;
-  const long long n = n_dev ? clamp_n(n_dev, n_cap) : n_cap;
-  const long long base = (long long)bid * kScanTile + (long long)threadIdx.x * kScanItems;
-  uint32_t v[kScanItems];
-  uint32_t sum = 0;
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    const long long i = base + k;
-    uint32_t x = 0;
-    if (i < n) x = in[gather ? (long long)gather[i] : i];
-    v[k] = sum;
-    sum += x;
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t incl = sum;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
-    if (lane >= d) incl += t;
-  }
-  if (lane == 31) s_warp[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    const uint32_t w = lane < kSB / 32 ? s_warp[lane] : 0u;
-    uint32_t wi = w;
-#pragma unroll
-    for (int d = 1; d < kSB / 32; d <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xffffffffu, wi, d);
-      if (lane >= d) wi += t;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    unsigned int v;
+    // relaxed polling (an acquire load per poll would invalidate L1 under
+    // the co-resident CTA), one fence after
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    while (v < n_ctas) {
+      __nanosleep(20);
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
     }
-    const uint32_t agg = __shfl_sync(0xffffffffu, wi, kSB / 32 - 1);
-    if (lane < kSB / 32) s_warp[lane] = wi - w;
-    const uint32_t excl = (uint32_t)warp_lookback(status, bid, agg);
-    if (lane == 0) s_prefix = excl;
+    __threadfence();
+#ifdef TSR_K2_TRACE
+    if (blockIdx.x == 0) tsr_k2_trace_buf[1 + (((uintptr_t)ctr & 127) >> 2)] = gtimer();  // bar is 256-B aligned
+#endif
   }
   __syncthreads();
-  const uint32_t off = s_prefix + s_warp[warp] + (incl - sum);
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    const long long i = base + k;
-    if (i < n) out[i] = off + v[k];
-  }
 }
 
-// ------------------------------------------------------------ radix sort --
-template <int ITEMS>
-__global__ void __launch_bounds__(kSB) radix_hist_kernel(const uint32_t* __restrict__ keys,
-                                                         const long long* __restrict__ n_dev,
-                                                         long long n_cap, int shift, int n_ctas,
-                                                         uint32_t* __restrict__ hist) {
-  __shared__ uint32_t s_h[kBins];
-  s_h[threadIdx.x] = 0;
-  const long long n = clamp_n(n_dev, n_cap);
-  const long long base = (long long)blockIdx.x * (kSB * ITEMS);
-  uint32_t kk[ITEMS];
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {  // all loads in flight first
-    const long long i = base + (long long)k * kSB + threadIdx.x;
-    kk[k] = i < n ? keys[i] : 0xffffffffu;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const long long i = base + (long long)k * kSB + threadIdx.x;
-    const bool valid = i < n;
-    const uint32_t d = (kk[k] >> shift) & (kBins - 1);
-    // skewed digits (e.g. the exponent byte of depths) collapse to one atomic
-    const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
-    if (__all_sync(0xffffffffu, valid && d == d0)) {
-      if ((threadIdx.x & 31) == 0) atomicAdd(&s_h[d], 32u);
-    } else if (valid) {
-      atomicAdd(&s_h[d], 1u);
-    }
-  }
-  __syncthreads();
-  hist[(long long)threadIdx.x * n_ctas + blockIdx.x] = s_h[threadIdx.x];
-}
-
-// Block-wide exclusive scan helper (256 threads): returns the exclusive
-// prefix of v; *total receives the block sum.
+// Block-wide exclusive scan (256 threads); *total receives the block sum.
 template <typename T>
-__device__ __forceinline__ T block_excl_scan_256(T v, T* s_w, T* total) {
+__device__ __forceinline__ T block_excl_scan(T v, T* s_w, T* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   T incl = v;
 #pragma unroll
@@ -146,6 +146,7 @@ __device__ __forceinline__ T block_excl_scan_256(T v, T* s_w, T* total) {
     const T t = __shfl_up_sync(0xffffffffu, incl, k);
     if (lane >= k) incl += t;
   }
+  __syncthreads();  // s_w may still be read by a previous call
   if (lane == 31) s_w[warp] = incl;
   __syncthreads();
   T pre = 0, tot = 0;
@@ -158,348 +159,529 @@ __device__ __forceinline__ T block_excl_scan_256(T v, T* s_w, T* total) {
   return pre + incl - v;
 }
 
-// Per-digit exclusive scan over CTAs (one CTA per digit): hist_scan[d][c] =
-// sum_{c' < c} hist[d][c'], digit_total[d] = sum_c hist[d][c].  Each thread
-// scans a contiguous run of the row, then one block scan (no loop of
-// barriers); the digit prefix is added by the scatter kernel.
-constexpr int kRowPerThread = 64;  // rows up to 16384 CTAs (33.5M pairs at 8 items)
-__global__ void __launch_bounds__(kSB) radix_digit_scan_kernel(const uint32_t* __restrict__ hist,
-                                                               int n_ctas,
-                                                               uint32_t* __restrict__ hist_scan,
-                                                               uint32_t* __restrict__ digit_total) {
-  __shared__ uint32_t s_w[kSB / 32];
-  const int d = blockIdx.x;
-  const uint32_t* row = hist + (long long)d * n_ctas;
-  uint32_t* out = hist_scan + (long long)d * n_ctas;
-  const int per = (n_ctas + kSB - 1) / kSB;  // <= kRowPerThread (checked by the host)
-  const int c0 = threadIdx.x * per;
-  const int c1 = min(c0 + per, n_ctas);
-  uint32_t sum = 0;
-  for (int c = c0; c < c1; ++c) sum += row[c];
-  uint32_t total;
-  uint32_t run = block_excl_scan_256(sum, s_w, &total);
-  for (int c = c0; c < c1; ++c) {  // second read hits L1
-    const uint32_t v = row[c];
-    out[c] = run;
-    run += v;
+// Lanes of the warp holding the same 8-bit digit (ballot multi-split: one
+// ballot per digit bit).  __match_any_sync is emulated in software on this
+// part (a BREV loop per distinct value) and shared-memory atomics cost
+// ~2 cycles per lane, so ranking and counting use ballots plus one
+// non-atomic update per distinct digit.  All 32 lanes must call.
+__device__ __forceinline__ unsigned digit_peers(uint32_t d, int bits, unsigned valid_mask) {
+  unsigned m = valid_mask;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    if (b >= bits) break;  // uniform
+    const bool bit = (d >> b) & 1u;
+    const unsigned bal = __ballot_sync(0xffffffffu, bit);
+    m &= bit ? bal : ~bal;
   }
-  if (threadIdx.x == 0) digit_total[d] = total;
+  return m;
 }
 
-// Stable scatter.  Ranking: warp w owns items [base + 32 ITEMS w, ...),
-// ranked round by round with __match_any_sync against per-warp digit
-// counters; counters are prefixed over warps and digits so the CTA-local
-// order is (digit, input position).  The CTA stages keys/values in shared
-// memory in that order and writes each digit's run contiguously (coalesced).
-// V = uint32_t (depth passes: row) or unsigned long long (tile passes:
-// depth bits << 32 | row).  FINAL writes the TileIndex layout instead:
-// keys64 = tile << 32 | depth bits, values32 = row.
-template <int ITEMS, typename V, bool FINAL>
-__global__ void __launch_bounds__(kSB) radix_scatter_kernel(
-    const uint32_t* __restrict__ keys_in, const V* __restrict__ vals_in,
-    uint32_t* __restrict__ keys_out, V* __restrict__ vals_out, int64_t* __restrict__ keys64,
-    int32_t* __restrict__ values32, const long long* __restrict__ n_dev, long long n_cap,
-    int shift, int n_ctas, const uint32_t* __restrict__ hist_scan,
-    const uint32_t* __restrict__ digit_total) {
-  constexpr int kTileN = kSB * ITEMS;
-  __shared__ uint32_t s_cnt[kSB / 32][kBins];
-  __shared__ uint32_t s_gbase[kBins];  // global start of this CTA's run of digit d
-  __shared__ uint32_t s_lbase[kBins];  // CTA-local start of digit d
-  __shared__ uint32_t s_wsum[kSB / 32];
-  __shared__ uint32_t s_keys[kTileN];
-  __shared__ V s_vals[kTileN];
+// Warp-aggregated shared-memory histogram increment for counting (no order
+// needed): a digit shared by the whole warp (skewed bytes) costs one atomic.
+__device__ __forceinline__ void hist_add(uint32_t* h, uint32_t d, bool valid) {
+  const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
+  if (__all_sync(0xffffffffu, valid && d == d0)) {
+    if ((threadIdx.x & 31) == 0) atomicAdd(&h[d0], 32u);
+  } else if (valid) {
+    atomicAdd(&h[d], 1u);
+  }
+}
+
+__device__ __forceinline__ void slice(long long n, int bid, int G, long long& lo, long long& hi) {
+  lo = n * bid / G;
+  hi = n * (bid + 1) / G;
+}
+
+template <typename K>
+__device__ __forceinline__ uint32_t digit_of(K k, int shift, uint32_t mask) {
+  return (uint32_t)(k >> shift) & mask;
+}
+
+// ---- radix pass, phase 1: per-CTA digit histogram of the slice
+template <typename K>
+__device__ void count_phase(const K* __restrict__ kin, long long lo, long long hi, int shift,
+                            uint32_t mask, uint32_t* __restrict__ cnt_out, SortSmem& sm) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  sm.h[0][tid] = 0;
+  __syncthreads();
+  for (long long base = lo; base < hi; base += kSub) {
+    const long long wb = base + (long long)warp * (32 * kItems);
+    K k[kItems];
 #pragma unroll
-  for (int w = 0; w < kSB / 32; ++w) s_cnt[w][tid] = 0;
-  const long long n = clamp_n(n_dev, n_cap);
-  const long long cta_base = (long long)blockIdx.x * kTileN;
-  if (cta_base >= n) return;  // uniform per CTA
-  {
-    // exclusive prefix of the digit totals (identical in every CTA)
-    const uint32_t v = digit_total[tid];
-    uint32_t incl = v;
-#pragma unroll
-    for (int k = 1; k < 32; k <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, k);
-      if (lane >= k) incl += t;
+    for (int r = 0; r < kItems; ++r) {
+      const long long i = wb + r * 32 + lane;
+      k[r] = i < hi ? kin[i] : (K)0;
     }
-    if (lane == 31) s_wsum[warp] = incl;
-    __syncthreads();
-    uint32_t wpre = 0;
 #pragma unroll
-    for (int w = 0; w < kSB / 32; ++w) wpre += w < warp ? s_wsum[w] : 0u;
-    s_gbase[tid] = wpre + incl - v + hist_scan[(long long)tid * n_ctas + blockIdx.x];
+    for (int r = 0; r < kItems; ++r)
+      hist_add(sm.h[0], digit_of(k[r], shift, mask), wb + r * 32 + lane < hi);
   }
   __syncthreads();
-  const long long wbase = cta_base + (long long)warp * (ITEMS * 32);
+  cnt_out[tid] = sm.h[0][tid];
+}
+
+// ---- radix pass, phase 2: CTA d scans digit column d over the G CTAs
+__device__ void colscan_phase(const uint32_t* __restrict__ cnt, uint32_t* __restrict__ colscan,
+                              uint32_t* __restrict__ dtotal, int G, SortSmem& sm) {
+  const int per = (G + kSB - 1) / kSB;
+  for (int d = blockIdx.x; d < kBins; d += gridDim.x) {
+    const int c0 = threadIdx.x * per;
+    uint32_t v[kMaxGrid / kSB];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int j = 0; j < kMaxGrid / kSB; ++j) {
+      const int c = c0 + j;
+      v[j] = (j < per && c < G) ? cnt[(long long)c * kBins + d] : 0u;
+      sum += v[j];
+    }
+    uint32_t total;
+    uint32_t run = block_excl_scan(sum, sm.w32, &total);
+#pragma unroll
+    for (int j = 0; j < kMaxGrid / kSB; ++j) {
+      const int c = c0 + j;
+      if (j < per && c < G) colscan[(long long)c * kBins + d] = run;
+      run += v[j];
+    }
+    if (threadIdx.x == 0) dtotal[d] = total;
+  }
+}
+
+// ---- radix pass, phase 3: stable scatter of the slice.
+// K = u32 depth bits (values: rows; vin == nullptr -> value = index) or
+// u64 pair keys tile << 32 | depth bits (values: rows).
+template <typename K>
+__device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+                              K* __restrict__ kout, uint32_t* __restrict__ vout, long long lo,
+                              long long hi, int shift, int bits,
+                              const uint32_t* __restrict__ colscan_row,
+                              const uint32_t* __restrict__ dtotal, SortSmem& sm,
+                              unsigned char* dyn) {
+  constexpr bool kVals = true;
+  K* s_keys = reinterpret_cast<K*>(dyn);
+  uint32_t* s_vals = reinterpret_cast<uint32_t*>(dyn + kSub * sizeof(K));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  uint32_t key[ITEMS], packed[ITEMS];
-  V val[ITEMS];
-#pragma unroll
-  for (int r = 0; r < ITEMS; ++r) {  // all loads in flight first
-    const long long i = wbase + r * 32 + lane;
-    key[r] = i < n ? keys_in[i] : 0u;
-    val[r] = i < n ? (vals_in ? vals_in[i] : (V)i) : (V)0;
+  const uint32_t mask = (1u << bits) - 1u;
+  {
+    uint32_t total;
+    const uint32_t dstart = block_excl_scan(dtotal[tid], sm.w32, &total);
+    sm.run[tid] = dstart + colscan_row[tid];
   }
+  for (long long base = lo; base < hi; base += kSub) {
 #pragma unroll
-  for (int r = 0; r < ITEMS; ++r) {
-    const long long i = wbase + r * 32 + lane;
-    const bool valid = i < n;
-    const uint32_t d = (key[r] >> shift) & (kBins - 1);
-    const unsigned peers = __match_any_sync(0xffffffffu, valid ? d : (kBins + lane));
-    const uint32_t before = __popc(peers & lt);
-    uint32_t cnt = 0;
-    if (valid) cnt = s_cnt[warp][d];
-    __syncwarp();
-    if (valid && before == 0) s_cnt[warp][d] = cnt + __popc(peers);
-    __syncwarp();
-    packed[r] = valid ? ((d << 16) | (cnt + before)) : 0xffffffffu;
-  }
-  __syncthreads();
-  // digit tid: exclusive prefix over warps, then over digits
-  uint32_t run = 0;
+    for (int w = 0; w < kSB / 32; ++w) sm.cnt[w][tid] = 0;
+    __syncthreads();
+    const long long wb = base + (long long)warp * (32 * kItems);
+    K key[kItems];
+    uint32_t val[kItems], packed[kItems];
 #pragma unroll
-  for (int w = 0; w < kSB / 32; ++w) {
-    const uint32_t c = s_cnt[w][tid];
-    s_cnt[w][tid] = run;
-    run += c;
-  }
-  uint32_t incl = run;
-#pragma unroll
-  for (int k = 1; k < 32; k <<= 1) {
-    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, k);
-    if (lane >= k) incl += t;
-  }
-  __syncthreads();  // s_wsum reuse
-  if (lane == 31) s_wsum[warp] = incl;
-  __syncthreads();
-  uint32_t wpre = 0;
-#pragma unroll
-  for (int w = 0; w < kSB / 32; ++w) wpre += w < warp ? s_wsum[w] : 0u;
-  s_lbase[tid] = wpre + incl - run;
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < ITEMS; ++r) {
-    if (packed[r] != 0xffffffffu) {
-      const uint32_t d = packed[r] >> 16;
-      const uint32_t local = s_lbase[d] + s_cnt[warp][d] + (packed[r] & 0xffffu);
-      s_keys[local] = key[r];
-      s_vals[local] = val[r];
+    for (int r = 0; r < kItems; ++r) {  // all loads in flight first
+      const long long i = wb + r * 32 + lane;
+      key[r] = i < hi ? kin[i] : (K)0;
+      if (kVals) val[r] = i < hi ? (vin ? vin[i] : (uint32_t)i) : 0u;
     }
-  }
-  __syncthreads();
-  const int cnt_valid = (int)(n - cta_base < kTileN ? n - cta_base : kTileN);
-  for (int i = tid; i < cnt_valid; i += kSB) {
-    const uint32_t k = s_keys[i];
-    const uint32_t d = (k >> shift) & (kBins - 1);
-    const uint32_t g = s_gbase[d] + (uint32_t)i - s_lbase[d];
-    const V v = s_vals[i];
-    if constexpr (FINAL) {
-      keys64[g] = ((long long)k << 32) | (long long)(v >> 32);
-      values32[g] = (int32_t)(uint32_t)v;
-    } else {
-      keys_out[g] = k;
-      vals_out[g] = v;
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+      const bool valid = wb + r * 32 + lane < hi;
+      const uint32_t d = digit_of(key[r], shift, mask);
+      const unsigned peers = digit_peers(d, bits, __ballot_sync(0xffffffffu, valid));
+      const uint32_t before = __popc(peers & lt);
+      uint32_t c = 0;
+      if (valid) c = sm.cnt[warp][d];
+      __syncwarp();
+      if (valid && before == 0) sm.cnt[warp][d] = c + __popc(peers);
+      __syncwarp();
+      packed[r] = valid ? ((d << 16) | (c + before)) : 0xffffffffu;
     }
-  }
-}
-
-// ------------------------------------------------------------- emission --
-__device__ __forceinline__ void emit_one(long long out, long long p_cap, uint32_t tile,
-                                         unsigned long long val, uint32_t* tile_out,
-                                         unsigned long long* val_out) {
-  if (out < p_cap) {
-    tile_out[out] = tile;
-    val_out[out] = val;
-  }
-}
-
-// Rank-major emission.  Compact column-walk record written by K1 (see
-// preprocess.cu):  x = tx0 | ncols << 16,  y = ty_base | overflow << 31,
-// z, w = 8 columns x (row offset 4 bits | nrows 4 bits).
-__global__ void __launch_bounds__(kSB) emit_pairs_kernel(
-    const float* __restrict__ rec, const uint4* __restrict__ spans,
-    const uint32_t* __restrict__ depth_by_rank, const uint32_t* __restrict__ row_by_rank,
-    const uint32_t* __restrict__ off_rank, const long long* __restrict__ totals, long long m_cap,
-    long long p_cap, int tiles_x, int tiles_y, int strategy, uint32_t* __restrict__ tile_out,
-    unsigned long long* __restrict__ val_out, int* __restrict__ overflow) {
-  const long long m = clamp_n(totals, m_cap);
-  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= m) return;
-  if (r == 0 && totals[1] > p_cap && overflow) *overflow = 1;  // sticky
-  const uint32_t row = row_by_rank[r];
-  const unsigned long long val = ((unsigned long long)depth_by_rank[r] << 32) | row;
-  long long out = off_rank[r];
-  const uint4 sp = spans[row];
-  if (strategy == 0 && !(sp.y >> 31)) {
-    const int tx0 = (int)(sp.x & 0xffffu), ncols = (int)(sp.x >> 16);
-    const int ty_base = (int)(sp.y & 0xffffu);
-    for (int c = 0; c < ncols; ++c) {
-      const uint32_t code = ((c < 4 ? sp.z : sp.w) >> (8 * (c & 3))) & 0xffu;
-      const int ty0 = ty_base + (int)(code & 15u), nr = (int)(code >> 4);
-      for (int k = 0; k < nr; ++k, ++out)
-        emit_one(out, p_cap, (uint32_t)((ty0 + k) * tiles_x + tx0 + c), val, tile_out, val_out);
+    __syncthreads();
+    // digit tid: exclusive prefix over warps (input order), sub-tile total
+    uint32_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < kSB / 32; ++w) {
+      const uint32_t c = sm.cnt[w][tid];
+      sm.cnt[w][tid] = tot;
+      tot += c;
     }
-    return;
-  }
-  // exact FP64 re-walk (span overflow, or the load-balanced min-q test)
-  SplatF64 s = load_splat_f64(rec + (long long)row * 12);
-  SnugRect box = snugbox(s, tiles_x, tiles_y);
-  if (box.tx0 > box.tx1 || box.ty0 > box.ty1) return;
-  for (long long tx = box.tx0; tx <= box.tx1; ++tx) {
-    if (strategy == 1) {
-      const double rx0 = dsub((double)(16 * tx), s.mx);
-      for (long long ty = box.ty0; ty <= box.ty1; ++ty) {
-        const double ry0 = dsub((double)(16 * ty), s.my);
-        if (min_q_box(s, rx0, dadd(rx0, 16.0), ry0, dadd(ry0, 16.0)) <= s.t)
-          emit_one(out++, p_cap, (uint32_t)(ty * tiles_x + tx), val, tile_out, val_out);
+    uint32_t dummy;
+    sm.lbase[tid] = block_excl_scan(tot, sm.w32, &dummy);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+      if (packed[r] != 0xffffffffu) {
+        const uint32_t d = packed[r] >> 16;
+        const uint32_t local = sm.lbase[d] + sm.cnt[warp][d] + (packed[r] & 0xffffu);
+        s_keys[local] = key[r];
+        if (kVals) s_vals[local] = val[r];
       }
-    } else {
-      long long ty0, ty1;
-      const int nr = column_rows(s, box, tx, tiles_y, ty0, ty1);
-      for (int k = 0; k < nr; ++k, ++out)
-        emit_one(out, p_cap, (uint32_t)((ty0 + k) * tiles_x + tx), val, tile_out, val_out);
     }
+    __syncthreads();
+    const int n_here = (int)(hi - base < kSub ? hi - base : kSub);
+    for (int i = tid; i < n_here; i += kSB) {
+      const K k = s_keys[i];
+      const uint32_t d = digit_of(k, shift, mask);
+      const uint32_t g = sm.run[d] + (uint32_t)i - sm.lbase[d];
+      kout[g] = k;
+      vout[g] = s_vals[i];
+    }
+    __syncthreads();
+    sm.run[tid] += tot;
   }
 }
 
-// offsets[t] = first sorted index whose tile >= t, t in [0, T] (binning.py:156-157).
-__global__ void __launch_bounds__(kSB) tile_ranges_kernel(const int64_t* __restrict__ keys,
-                                                          const long long* __restrict__ totals,
-                                                          long long p_cap, int n_tiles,
-                                                          int64_t* __restrict__ offsets) {
-  const long long p = clamp_n(totals + 1, p_cap);
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i > p) return;
-  const long long cur = i < p ? (keys[i] >> 32) : (long long)n_tiles;
-  const long long prev = i == 0 ? -1 : (keys[i - 1] >> 32);
-  for (long long t = prev + 1; t <= cur; ++t) offsets[t] = i;
+// ---- one full radix pass (3 phases, 3 grid barriers)
+template <typename K>
+__device__ void radix_pass(const IndexArgs& a, int& nb, const K* kin, const uint32_t* vin,
+                           K* kout, uint32_t* vout, long long n, int shift, int bits,
+                           SortSmem& sm, unsigned char* dyn) {
+  const int G = gridDim.x, bid = blockIdx.x;
+  long long lo, hi;
+  slice(n, bid, G, lo, hi);
+  count_phase<K>(kin, lo, hi, shift, (1u << bits) - 1u, a.cnt + (long long)bid * kBins, sm);
+  grid_barrier(a.bar + nb++, G);
+  colscan_phase(a.cnt, a.colscan, a.dtotal, G, sm);
+  grid_barrier(a.bar + nb++, G);
+  scatter_phase<K>(kin, vin, kout, vout, lo, hi, shift, bits, a.colscan + (long long)bid * kBins,
+                   a.dtotal, sm, dyn);
+  grid_barrier(a.bar + nb++, G);
 }
 
-// ckpt_base[t] = sum_{u<t} floor(n_u / 32) (forward.py:139-145: one record
-// per completed 32-entry group); ckpt_base[T] = total records.  One CTA,
-// each thread a contiguous run of tiles (up to 65536 tiles).
-constexpr int kTilesPerThread = 64;
-__global__ void __launch_bounds__(kSB) ckpt_base_kernel(const int64_t* __restrict__ offsets,
-                                                        int n_tiles,
-                                                        int64_t* __restrict__ ckpt_base) {
-  __shared__ long long s_w[kSB / 32];
-  const int per = (n_tiles + kSB - 1) / kSB;
-  const int t0 = threadIdx.x * per;
-  long long sum = 0;
-  for (int k = 0; k < per; ++k) {
-    const int t = t0 + k;
-    if (t < n_tiles) sum += (offsets[t + 1] - offsets[t]) / kGroup;
+// ---- emission.  Compact column-walk record written by K1 (preprocess.cu):
+//   x = tx0 | ncols << 16,  y = ty_base | overflow << 31,
+//   z, w = 8 columns x (row offset 4 bits | nrows 4 bits).
+__device__ __forceinline__ uint32_t rank_row(const uint32_t* row_by_rank, long long r) {
+  return row_by_rank ? row_by_rank[r] : (uint32_t)r;
+}
+
+__device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, long long O,
+                           long long p_cap, const uint32_t* __restrict__ depth_by_rank,
+                           const uint32_t* __restrict__ row_by_rank, SortSmem& sm,
+                           unsigned char* dyn) {
+  unsigned long long* s_stage = reinterpret_cast<unsigned long long*>(dyn);
+  uint32_t* s_sval = reinterpret_cast<uint32_t*>(dyn + kStage * sizeof(unsigned long long));
+  const int tid = threadIdx.x;
+  const int tiles_x = a.tiles_x, tiles_y = a.tiles_y, strategy = a.strategy;
+  unsigned long long* __restrict__ pairs = a.pk0;
+  uint32_t* __restrict__ pair_rows = a.pv0;
+  for (long long r0 = rlo; r0 < rhi; r0 += kEmitRanks) {
+    uint32_t row[kEmitPer], cnt[kEmitPer], off[kEmitPer], dep[kEmitPer];
+    uint4 sp[kEmitPer];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kEmitPer; ++k) {
+      const long long r = r0 + kEmitPer * tid + k;
+      cnt[k] = 0;
+      sp[k] = make_uint4(0u, 0u, 0u, 0u);
+      if (r < rhi) {
+        cnt[k] = a.rank_cnt[r];
+        sp[k] = a.rank_span[r];
+      }
+      row[k] = r < rhi ? rank_row(row_by_rank, r) : 0u;
+      dep[k] = r < rhi ? depth_by_rank[r] : 0u;
+      sum += cnt[k];
+    }
+    if (r0 == rlo) TSR_TRACE_AT(40);
+    uint32_t total;
+    uint32_t run = block_excl_scan(sum, sm.w32, &total);
+    if (r0 == rlo) TSR_TRACE_AT(41);
+#pragma unroll
+    for (int k = 0; k < kEmitPer; ++k) {
+      off[k] = run;
+      run += cnt[k];
+    }
+    for (uint32_t w0 = 0; w0 < total; w0 += kStage) {
+      const uint32_t w1 = min(total, w0 + (uint32_t)kStage);
+#pragma unroll
+      for (int k = 0; k < kEmitPer; ++k) {
+        const uint32_t lo = off[k], hi = off[k] + cnt[k];
+        if (hi <= w0 || lo >= w1) continue;
+        if (sp[k].y >> 31) {  // written by the FP64 re-walk below
+          for (uint32_t p = max(lo, w0); p < min(hi, w1); ++p) s_stage[p - w0] = kNoPair;
+          continue;
+        }
+        // one flat loop over the rank's pairs (column-major, K1's order);
+        // (column, row-in-column) advance incrementally
+        const unsigned long long depk = dep[k];
+        const uint32_t rowk = row[k];
+        const uint32_t tx0 = sp[k].x & 0xffffu, ty_base = sp[k].y & 0xffffu;
+        unsigned long long codes = ((unsigned long long)sp[k].w << 32) | sp[k].z;
+        uint32_t c = 0, code = (uint32_t)codes & 0xffu;
+        while ((code >> 4) == 0u && c < 7u) {
+          codes >>= 8;
+          code = (uint32_t)codes & 0xffu;
+          ++c;
+        }
+        uint32_t t = (ty_base + (code & 15u)) * (uint32_t)tiles_x + tx0 + c, q = 0;
+#pragma unroll 1
+        for (uint32_t p = lo; p < hi; ++p) {
+          if (p >= w0 && p < w1) {
+            s_stage[p - w0] = ((unsigned long long)t << 32) | depk;
+            s_sval[p - w0] = rowk;
+          }
+          t += (uint32_t)tiles_x;
+          if (++q == (code >> 4) && p + 1 < hi) {  // next non-empty column
+            q = 0;
+            do {
+              codes >>= 8;
+              code = (uint32_t)codes & 0xffu;
+              ++c;
+            } while ((code >> 4) == 0u && c < 7u);
+            t = (ty_base + (code & 15u)) * (uint32_t)tiles_x + tx0 + c;
+          }
+        }
+      }
+      __syncthreads();
+      if (r0 == rlo && w0 == 0) TSR_TRACE_AT(45);
+      for (uint32_t j = tid; j < w1 - w0; j += kSB) {
+        const unsigned long long v = s_stage[j];
+        const long long g = O + w0 + j;
+        if (v != kNoPair && g < p_cap) {
+          pairs[g] = v;
+          pair_rows[g] = s_sval[j];
+        }
+      }
+      __syncthreads();
+      if (r0 == rlo && w0 == 0) TSR_TRACE_AT(46);
+    }
+    if (r0 == rlo) TSR_TRACE_AT(42);
+    // exact FP64 re-walk (span overflow, or the load-balanced min-q test)
+#pragma unroll
+    for (int k = 0; k < kEmitPer; ++k) {
+      if (!(sp[k].y >> 31) || cnt[k] == 0) continue;
+      const unsigned long long depk = dep[k];
+      long long out = O + off[k];
+      SplatF64 s = load_splat_f64(a.rec + (long long)row[k] * 12);
+      SnugRect box = snugbox(s, tiles_x, tiles_y);
+      if (box.tx0 > box.tx1 || box.ty0 > box.ty1) continue;
+      for (long long tx = box.tx0; tx <= box.tx1; ++tx) {
+        if (strategy == 1) {
+          const double rx0 = dsub((double)(16 * tx), s.mx);
+          for (long long ty = box.ty0; ty <= box.ty1; ++ty) {
+            const double ry0 = dsub((double)(16 * ty), s.my);
+            if (min_q_box(s, rx0, dadd(rx0, 16.0), ry0, dadd(ry0, 16.0)) <= s.t) {
+              if (out < p_cap) {
+                pairs[out] = ((unsigned long long)(ty * tiles_x + tx) << 32) | depk;
+                pair_rows[out] = row[k];
+              }
+              ++out;
+            }
+          }
+        } else {
+          long long ty0, ty1;
+          const int nr = column_rows(s, box, tx, tiles_y, ty0, ty1);
+          for (int q = 0; q < nr; ++q, ++out)
+            if (out < p_cap) {
+              pairs[out] = ((unsigned long long)((ty0 + q) * tiles_x + tx) << 32) | depk;
+              pair_rows[out] = row[k];
+            }
+        }
+      }
+    }
+    if (r0 == rlo) TSR_TRACE_AT(43);
+    O += total;
   }
-  long long total;
-  long long run = block_excl_scan_256(sum, s_w, &total);
-  for (int k = 0; k < per; ++k) {
-    const int t = t0 + k;
-    if (t < n_tiles) {
-      ckpt_base[t] = run;
-      run += (offsets[t + 1] - offsets[t]) / kGroup;
+  TSR_TRACE_AT(44);
+}
+
+// ---- the persistent index kernel
+__global__ void __launch_bounds__(kSB, 2) build_index_kernel(IndexArgs a) {
+  __shared__ SortSmem sm;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  const int G = gridDim.x, bid = blockIdx.x, tid = threadIdx.x;
+  int nb = 0;
+  const long long m = clamp_ll(a.totals[0], a.m_cap);
+#ifdef TSR_K2_TRACE
+  if (bid == 0 && tid == 0) tsr_k2_trace_buf[0] = gtimer();
+#endif
+
+  // ---- 1. depth ranks
+  // histogram of all four depth bytes (tells which passes are trivial)
+#pragma unroll
+  for (int b = 0; b < 4; ++b) sm.h[b][tid] = 0;
+  __syncthreads();
+  {
+    long long lo, hi;
+    slice(m, bid, G, lo, hi);
+    const int lane = tid & 31, warp = tid >> 5;
+    for (long long base = lo; base < hi; base += kSub) {
+      const long long wb = base + (long long)warp * (32 * kItems);
+      uint32_t k[kItems];
+#pragma unroll
+      for (int r = 0; r < kItems; ++r) {
+        const long long i = wb + r * 32 + lane;
+        k[r] = i < hi ? a.depth_bits[i] : 0u;
+      }
+#pragma unroll
+      for (int r = 0; r < kItems; ++r) {
+        const bool v = wb + r * 32 + lane < hi;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) hist_add(sm.h[b], (k[r] >> (8 * b)) & 255u, v);
+      }
     }
   }
-  if (threadIdx.x == 0) ckpt_base[n_tiles] = total;
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+    if (sm.h[b][tid]) atomicAdd(&a.hist4[b * kBins + tid], sm.h[b][tid]);
+  grid_barrier(a.bar + nb++, G);
+  if (tid < 4) sm.skip[tid] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+    if ((long long)a.hist4[b * kBins + tid] == m) sm.skip[b] = 1;  // one digit for every row
+  __syncthreads();
+  const uint32_t* dkey = a.depth_bits;
+  const uint32_t* drow = nullptr;  // identity
+  {
+    uint32_t* ko[2] = {a.dk0, a.dk1};
+    uint32_t* vo[2] = {a.dv0, a.dv1};
+    int par = 0;
+    for (int q = 0; q < 4; ++q) {
+      if (sm.skip[q]) continue;
+      radix_pass<uint32_t>(a, nb, dkey, drow, ko[par], vo[par], m, 8 * q, 8, sm, dyn);
+      dkey = ko[par];
+      drow = vo[par];
+      par ^= 1;
+    }
+  }
+
+  // ---- 2. rank-major emission
+  long long rlo, rhi;
+  slice(m, bid, G, rlo, rhi);
+  {
+    // gather each rank's span record once (its pair count follows from the
+    // nibbles; K1's count only for re-walked rows) and store both in rank
+    // order, so the emission reads them coalesced
+    uint32_t sum = 0;
+    for (long long r0 = rlo + tid; r0 < rhi; r0 += 4 * kSB) {
+      uint32_t row[4];
+      uint4 sp[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const long long r = r0 + j * kSB;
+        row[j] = r < rhi ? rank_row(drow, r) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) sp[j] = r0 + j * kSB < rhi ? a.spans[row[j]] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const long long r = r0 + j * kSB;
+        if (r >= rhi) continue;
+        if (a.strategy != 0) sp[j].y |= 1u << 31;
+        uint32_t c;
+        if (sp[j].y >> 31) {
+          c = (uint32_t)a.counts[row[j]];
+        } else {
+          // sum of the 8 nrows nibbles (high nibble of each byte)
+          const uint32_t hz = (sp[j].z >> 4) & 0x0f0f0f0fu, hw = (sp[j].w >> 4) & 0x0f0f0f0fu;
+          c = ((hz + hw) * 0x01010101u) >> 24;
+        }
+        a.rank_cnt[r] = c;
+        a.rank_span[r] = sp[j];
+        sum += c;
+      }
+    }
+    unsigned long long total;
+    block_excl_scan((unsigned long long)sum, sm.w64, &total);
+    if (tid == 0) a.ptot[bid] = total;
+  }
+  grid_barrier(a.bar + nb++, G);
+  long long O, P;
+  {
+    unsigned long long before = 0, all = 0;
+    for (int c = tid; c < G; c += kSB) {
+      const unsigned long long v = a.ptot[c];
+      all += v;
+      if (c < bid) before += v;
+    }
+    unsigned long long t0, t1;
+    block_excl_scan(before, sm.w64, &t0);
+    block_excl_scan(all, sm.w64, &t1);
+    O = (long long)t0;
+    P = (long long)t1;
+  }
+  if (bid == 0 && tid == 0 && P > a.p_cap && a.overflow) *a.overflow = 1;  // sticky
+  emit_phase(a, rlo, rhi, O, a.p_cap, dkey, drow, sm, dyn);
+  grid_barrier(a.bar + nb++, G);
+
+  // ---- 3. stable sort of the pairs by tile; the last pass writes keys/values
+  const long long np = clamp_ll(P, a.p_cap);
+  unsigned long long* keys_out = reinterpret_cast<unsigned long long*>(a.keys);
+  uint32_t* vals_out = reinterpret_cast<uint32_t*>(a.values);
+  if (a.tile_bits > 8) {  // two passes of ~half the tile bits each
+    const int b1 = (a.tile_bits + 1) / 2, b2 = a.tile_bits - b1;
+    radix_pass<unsigned long long>(a, nb, a.pk0, a.pv0, a.pk1, a.pv1, np, 32, b1, sm, dyn);
+    radix_pass<unsigned long long>(a, nb, a.pk1, a.pv1, keys_out, vals_out, np, 32 + b1, b2, sm,
+                                   dyn);
+  } else {
+    radix_pass<unsigned long long>(a, nb, a.pk0, a.pv0, keys_out, vals_out, np, 32, a.tile_bits,
+                                   sm, dyn);
+  }
+
+  // ---- 4. per-tile ranges (binning.py:156-157) + checkpoint bases
+  const int* khi = reinterpret_cast<const int*>(a.keys) + 1;  // tile = high word
+  for (long long i = (long long)bid * kSB + tid; i <= np; i += (long long)G * kSB) {
+    const long long cur = i < np ? khi[2 * i] : (long long)a.n_tiles;
+    const long long prev = i == 0 ? -1 : khi[2 * (i - 1)];
+    for (long long t = prev + 1; t <= cur; ++t) {
+      a.offsets[t] = i;
+      if (a.ckpt_base) a.ckpt_base[t] = i >> 5;
+    }
+  }
 }
 
 // -------------------------------------------------------------- planning --
-struct IndexWorkspace {
-  uint32_t *dk0, *dv0, *dk1, *dv1;    // depth sort ping-pong (M_cap)
-  uint32_t* off_rank;                 // M_cap
-  uint32_t *tk0, *tk1;                // tile keys ping-pong (P_cap)
-  unsigned long long *tv0, *tv1;      // depth bits << 32 | row (P_cap)
-  uint32_t *hist, *hist_scan;         // 256 x max_ctas
-  uint32_t* digit_total;              // 256
-  unsigned long long* status;         // rank-scan look-back status words
-  unsigned int* tickets;
-  size_t bytes;
-  long long max_ctas, scan_blocks;
-};
-
-constexpr int kMaxTiles = 1 << 16;
-
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-static IndexWorkspace plan(void* base, long long m_cap, long long p_cap) {
-  IndexWorkspace w;
+struct Plan {
+  size_t bytes, ctl_off, ctl_bytes;
+  size_t dk0, dv0, dk1, dv1, pk0, pk1, pv0, pv1, cnt, colscan, dtotal, ptot, rank_cnt, rank_span, hist4,
+      bar;
+};
+
+static Plan plan(long long m_cap, long long p_cap) {
+  Plan p;
   const long long mc = m_cap > 0 ? m_cap : 1, pc = p_cap > 0 ? p_cap : 1;
-  const long long ctas_m = (mc + kSB * items_for(mc) - 1) / (kSB * items_for(mc));
-  const long long ctas_p = (pc + kSB * items_for(pc) - 1) / (kSB * items_for(pc));
-  w.max_ctas = ctas_m > ctas_p ? ctas_m : ctas_p;
-  const long long hist_n = (long long)kBins * w.max_ctas;
-  w.scan_blocks = (mc + kScanTile - 1) / kScanTile;
-  char* p = (char*)base;
   size_t off = 0;
   auto take = [&](size_t bytes) {
-    char* q = p ? p + off : nullptr;
+    const size_t q = off;
     off += align256(bytes);
     return q;
   };
-  w.dk0 = (uint32_t*)take(4 * mc);
-  w.dv0 = (uint32_t*)take(4 * mc);
-  w.dk1 = (uint32_t*)take(4 * mc);
-  w.dv1 = (uint32_t*)take(4 * mc);
-  w.off_rank = (uint32_t*)take(4 * mc);
-  w.tk0 = (uint32_t*)take(4 * pc);
-  w.tk1 = (uint32_t*)take(4 * pc);
-  w.tv0 = (unsigned long long*)take(8 * pc);
-  w.tv1 = (unsigned long long*)take(8 * pc);
-  w.hist = (uint32_t*)take(4 * hist_n);
-  w.hist_scan = (uint32_t*)take(4 * hist_n);
-  w.digit_total = (uint32_t*)take(4 * kBins);
-  w.status = (unsigned long long*)take(8 * (size_t)w.scan_blocks);
-  w.tickets = (unsigned int*)take(16 * 4);
-  w.bytes = off;
-  return w;
-}
-
-static int scan_launch(const uint32_t* in, const int32_t* gather, uint32_t* out,
-                       const long long* n_dev, long long n_cap, unsigned long long* status,
-                       unsigned int* ticket, cudaStream_t s) {
-  const long long blocks = (n_cap + kScanTile - 1) / kScanTile;
-  if (blocks == 0) return TSR_OK;
-  scan_u32_kernel<<<(int)blocks, kSB, 0, s>>>(in, gather, out, n_dev, n_cap, status, ticket);
-  TSR_CHECK_LAUNCH();
-  return TSR_OK;
-}
-
-// One stable radix pass over n (device) <= n_cap items.
-template <int ITEMS, typename V, bool FINAL>
-static int radix_pass_t(const uint32_t* kin, const V* vin, uint32_t* kout, V* vout,
-                        int64_t* keys64, int32_t* values32, const long long* n_dev,
-                        long long n_cap, int shift, IndexWorkspace& w, cudaStream_t s) {
-  const int ctas = (int)((n_cap + kSB * ITEMS - 1) / (kSB * ITEMS));
-  if (ctas == 0) return TSR_OK;
-  if (ctas > kSB * kRowPerThread) return TSR_E_INVALID;  // > 8.4M pairs per pass
-  radix_hist_kernel<ITEMS><<<ctas, kSB, 0, s>>>(kin, n_dev, n_cap, shift, ctas, w.hist);
-  TSR_CHECK_LAUNCH();
-  radix_digit_scan_kernel<<<kBins, kSB, 0, s>>>(w.hist, ctas, w.hist_scan, w.digit_total);
-  TSR_CHECK_LAUNCH();
-  radix_scatter_kernel<ITEMS, V, FINAL><<<ctas, kSB, 0, s>>>(
-      kin, vin, kout, vout, keys64, values32, n_dev, n_cap, shift, ctas, w.hist_scan,
-      w.digit_total);
-  TSR_CHECK_LAUNCH();
-  return TSR_OK;
-}
-
-template <typename V, bool FINAL>
-static int radix_pass(const uint32_t* kin, const V* vin, uint32_t* kout, V* vout,
-                      int64_t* keys64, int32_t* values32, const long long* n_dev,
-                      long long n_cap, int shift, IndexWorkspace& w, cudaStream_t s) {
-  return items_for(n_cap) == 8
-             ? radix_pass_t<8, V, FINAL>(kin, vin, kout, vout, keys64, values32, n_dev, n_cap,
-                                         shift, w, s)
-             : radix_pass_t<4, V, FINAL>(kin, vin, kout, vout, keys64, values32, n_dev, n_cap,
-                                         shift, w, s);
+  p.dk0 = take(4 * mc);
+  p.dv0 = take(4 * mc);
+  p.dk1 = take(4 * mc);
+  p.dv1 = take(4 * mc);
+  p.pk0 = take(8 * pc);
+  p.pk1 = take(8 * pc);
+  p.pv0 = take(4 * pc);
+  p.pv1 = take(4 * pc);
+  p.cnt = take(4 * (size_t)kMaxGrid * kBins);
+  p.colscan = take(4 * (size_t)kMaxGrid * kBins);
+  p.dtotal = take(4 * kBins);
+  p.ptot = take(8 * (size_t)kMaxGrid);
+  p.rank_cnt = take(4 * mc);
+  p.rank_span = take(16 * mc);
+  p.ctl_off = off;
+  p.hist4 = take(4 * 4 * kBins);
+  p.bar = take(4 * kMaxBarriers);
+  p.ctl_bytes = off - p.ctl_off;
+  p.bytes = off;
+  return p;
 }
 
 }  // namespace tsr
 
 using namespace tsr;
 
+#ifdef TSR_K2_TRACE
+extern "C" int tsr_k2_trace_read(unsigned long long* host, unsigned int* bar_base) {
+  (void)bar_base;
+  return cudaMemcpyFromSymbol(host, tsr_k2_trace_buf, sizeof(tsr_k2_trace_buf)) == cudaSuccess ? 0 : 2;
+}
+#endif
+
 extern "C" size_t tsr_index_workspace(int64_t m_cap, int64_t p_cap) {
-  return plan(nullptr, m_cap, p_cap).bytes;
+  return plan(m_cap, p_cap).bytes;
 }
 
 extern "C" int tsr_build_index(const float* rec, const uint32_t* depth_bits, const void* spans,
@@ -510,67 +692,63 @@ extern "C" int tsr_build_index(const float* rec, const uint32_t* depth_bits, con
                                size_t workspace_bytes, void* stream) {
   if (m_cap < 0 || p_cap < 0 || width <= 0 || height <= 0 || !totals || !offsets)
     return TSR_E_INVALID;
-  if (workspace_bytes < tsr_index_workspace(m_cap, p_cap)) return TSR_E_WORKSPACE;
+  if (p_cap >= (1ll << 32) || m_cap >= (1ll << 32)) return TSR_E_INVALID;  // u32 offsets
+  if (workspace_bytes < tsr_index_workspace(m_cap, p_cap) || !workspace) return TSR_E_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
-  IndexWorkspace w = plan(workspace, m_cap, p_cap);
-  const int tx = tiles_of(width), ty = tiles_of(height);
-  const int n_tiles = tx * ty;
-  if (n_tiles > kMaxTiles) return TSR_E_INVALID;
-  const long long* M = (const long long*)totals;
-  const long long* P = (const long long*)totals + 1;
-  if (cudaMemsetAsync(w.status, 0, 8 * (size_t)w.scan_blocks, s) != cudaSuccess ||
-      cudaMemsetAsync(w.tickets, 0, 16 * 4, s) != cudaSuccess)
+  const Plan pl = plan(m_cap, p_cap);
+  char* w = (char*)workspace;
+  IndexArgs a;
+  a.rec = rec;
+  a.depth_bits = depth_bits;
+  a.spans = (const uint4*)spans;
+  a.counts = counts;
+  a.totals = (const long long*)totals;
+  a.m_cap = m_cap;
+  a.p_cap = p_cap;
+  a.tiles_x = tiles_of(width);
+  a.tiles_y = tiles_of(height);
+  a.n_tiles = a.tiles_x * a.tiles_y;
+  if (a.n_tiles > kMaxTiles) return TSR_E_INVALID;
+  a.strategy = strategy;
+  a.tile_bits = 1;
+  while ((1 << a.tile_bits) < a.n_tiles) ++a.tile_bits;  // <= 16
+  a.keys = keys;
+  a.values = values;
+  a.offsets = offsets;
+  a.ckpt_base = ckpt_base;
+  a.overflow = overflow;
+  a.dk0 = (uint32_t*)(w + pl.dk0);
+  a.dv0 = (uint32_t*)(w + pl.dv0);
+  a.dk1 = (uint32_t*)(w + pl.dk1);
+  a.dv1 = (uint32_t*)(w + pl.dv1);
+  a.pk0 = (unsigned long long*)(w + pl.pk0);
+  a.pk1 = (unsigned long long*)(w + pl.pk1);
+  a.pv0 = (uint32_t*)(w + pl.pv0);
+  a.pv1 = (uint32_t*)(w + pl.pv1);
+  a.cnt = (uint32_t*)(w + pl.cnt);
+  a.colscan = (uint32_t*)(w + pl.colscan);
+  a.dtotal = (uint32_t*)(w + pl.dtotal);
+  a.ptot = (unsigned long long*)(w + pl.ptot);
+  a.rank_cnt = (uint32_t*)(w + pl.rank_cnt);
+  a.rank_span = (uint4*)(w + pl.rank_span);
+  a.hist4 = (uint32_t*)(w + pl.hist4);
+  a.bar = (unsigned int*)(w + pl.bar);
+
+  int dev = 0, sms = 0, per_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      cudaFuncSetAttribute(build_index_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kDynSmem) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, build_index_kernel, kSB,
+                                                    kDynSmem) != cudaSuccess)
     return TSR_E_CUDA;
-  int rc = TSR_OK;
-  uint32_t* no_k = nullptr;
-  if (m_cap > 0) {
-    // 1. depth ranks: 4 stable 8-bit passes over (depth bits, row)
-    rc = radix_pass<uint32_t, false>(depth_bits, nullptr, w.dk1, w.dv1, nullptr, nullptr, M,
-                                     m_cap, 0, w, s);
-    if (!rc) rc = radix_pass<uint32_t, false>(w.dk1, w.dv1, w.dk0, w.dv0, nullptr, nullptr, M,
-                                              m_cap, 8, w, s);
-    if (!rc) rc = radix_pass<uint32_t, false>(w.dk0, w.dv0, w.dk1, w.dv1, nullptr, nullptr, M,
-                                              m_cap, 16, w, s);
-    if (!rc) rc = radix_pass<uint32_t, false>(w.dk1, w.dv1, w.dk0, w.dv0, nullptr, nullptr, M,
-                                              m_cap, 24, w, s);
-    if (rc) return rc;
-    // 2. rank-order pair offsets and rank-major emission
-    rc = scan_launch((const uint32_t*)counts, (const int32_t*)w.dv0, w.off_rank, M, m_cap,
-                     w.status, w.tickets, s);
-    if (rc) return rc;
-    emit_pairs_kernel<<<(int)((m_cap + kSB - 1) / kSB), kSB, 0, s>>>(
-        rec, (const uint4*)spans, w.dk0, w.dv0, w.off_rank, M, m_cap, p_cap, tx, ty, strategy,
-        w.tk0, w.tv0, overflow);
-    TSR_CHECK_LAUNCH();
-  }
-  // 3. stable sort of the pairs by tile; the last pass writes keys/values
-  if (p_cap > 0) {
-    int passes = 0;
-    while ((n_tiles - 1) >> (8 * passes)) ++passes;
-    if (passes == 0) passes = 1;
-    uint32_t* tk = w.tk0;
-    unsigned long long* tv = w.tv0;
-    for (int q = 0; q < passes; ++q) {
-      uint32_t* ko = tk == w.tk0 ? w.tk1 : w.tk0;
-      unsigned long long* vo = tv == w.tv0 ? w.tv1 : w.tv0;
-      if (q == passes - 1)
-        rc = radix_pass<unsigned long long, true>(tk, tv, no_k, nullptr, keys, values, P, p_cap,
-                                                  8 * q, w, s);
-      else
-        rc = radix_pass<unsigned long long, false>(tk, tv, ko, vo, nullptr, nullptr, P, p_cap,
-                                                   8 * q, w, s);
-      if (rc) return rc;
-      tk = ko;
-      tv = vo;
-    }
-  }
-  // 4. per-tile ranges + checkpoint bases
-  tile_ranges_kernel<<<(int)((p_cap + 1 + kSB - 1) / kSB), kSB, 0, s>>>(
-      keys, (const long long*)totals, p_cap, n_tiles, offsets);
-  TSR_CHECK_LAUNCH();
-  if (ckpt_base) {
-    ckpt_base_kernel<<<1, kSB, 0, s>>>(offsets, n_tiles, ckpt_base);
-    TSR_CHECK_LAUNCH();
-  }
-  return rc;
+  int grid = sms * (per_sm < 2 ? per_sm : 2);
+  if (grid > kMaxGrid) grid = kMaxGrid;
+  if (grid < 1) return TSR_E_CUDA;
+  if (cudaMemsetAsync(w + pl.ctl_off, 0, pl.ctl_bytes, s) != cudaSuccess) return TSR_E_CUDA;
+  void* args[] = {&a};
+  if (cudaLaunchCooperativeKernel((const void*)build_index_kernel, dim3(grid), dim3(kSB), args,
+                                  kDynSmem, s) != cudaSuccess)
+    return TSR_E_CUDA;
+  return TSR_OK;
 }

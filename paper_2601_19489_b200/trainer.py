@@ -278,12 +278,9 @@ class TrainStep:
         return e
 
     def kernels_per_step(self) -> int:
-        """Our kernel launches per step: K1a, K1b; K2 = 4 depth passes x 3 +
-        rank scan + emission + tile passes x 3 + ranges + checkpoint bases; K3;
-        loss (fwd, bwd, finalize); K4; fused K4b+K5."""
-        tiles = self.index.n_tiles if self.index is not None else 1
-        tile_passes = max(1, (max(tiles - 1, 1).bit_length() + 7) // 8)
-        return 2 + (4 * 3 + 2 + 3 * tile_passes + 2) + 1 + 3 + 1 + 1
+        """Our kernel launches per step: K1a, K1b; K2 (one persistent
+        cooperative kernel); K3; loss (fwd, bwd, finalize); K4; fused K4b+K5."""
+        return 2 + 1 + 1 + 3 + 1 + 1
 
     def last_view(self):
         """(batch, TileIndex, RenderBuffers) views of the last step (synchronises)."""

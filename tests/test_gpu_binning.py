@@ -94,3 +94,71 @@ def test_fused_preprocess_count_matches_standalone_count():
     assert np.array_equal(batch.counts.cpu().numpy(), fused_counts)
     ref = O.bin_sequential(host_batch(batch))
     assert_index_equal(idx, ref)
+
+
+def test_single_tile_pass_small_image():
+    """<= 256 tiles: the tile sort is one one-sweep pass."""
+    import paper_2601_19489_b200 as ts
+    b = random_splats(8_000, 7, 200, 150)
+    ref = O.bin_sequential(b)
+    assert_index_equal(ts.bin_sequential(dev_batch(b)), ref)
+
+
+def test_wide_spans_take_the_fp64_rewalk():
+    """Splats wider than K1's 8-column / 15-row span record are re-walked in
+    FP64 by their owner thread, interleaved with cooperatively emitted rows."""
+    import paper_2601_19489_b200 as ts
+    b = random_splats(20_000, 11, 1280, 720)
+    big = random_splats(300, 12, 1280, 720, anisotropy=(1.0, 4.0), minor=(25.0, 90.0))
+    m = {k: (np.concatenate([b[k], big[k]]) if isinstance(b[k], np.ndarray) else b[k])
+         for k in b}
+    m["source_ids"] = np.arange(len(m["depths"]))
+    ref = O.bin_sequential(m)
+    counts = np.bincount(ref["values"], minlength=len(m["depths"]))
+    assert counts[20_000:].max() > 8 * 15  # some rows cannot fit the span record
+    assert_index_equal(ts.bin_sequential(dev_batch(m)), ref)
+
+
+def test_depth_ties_across_many_ctas():
+    """600k rows with only 37 distinct depths: the stable passes must keep
+    row order across CTA boundaries (the reference's tie rule)."""
+    import paper_2601_19489_b200 as ts
+    b = random_splats(600_000, 5, 1920, 1080, minor=(0.5, 1.5))
+    b["depths"] = np.round(b["depths"] * 3.7) / 3.7
+    b["depths"] = np.asarray(b["depths"], np.float32).astype(np.float64)
+    ref = O.bin_sequential(b)
+    assert_index_equal(ts.bin_sequential(dev_batch(b)), ref)
+
+
+def test_checkpoint_bases_are_disjoint():
+    import paper_2601_19489_b200 as ts
+    b = random_splats(50_000, 3, 1920, 1080)
+    idx = ts.bin_sequential(dev_batch(b))
+    off = idx.offsets.cpu().numpy()
+    base = idx.ckpt_base.cpu().numpy()
+    n = np.diff(off)
+    assert np.all(base[:-1] + n // 32 <= base[1:])
+    assert base[-1] <= idx.n_pairs // 32
+
+
+def test_pair_capacity_overflow_is_flagged():
+    """P > p_cap: pairs are clamped (no out-of-bounds writes) and the sticky
+    overflow flag is raised for the caller to grow capacity."""
+    import torch
+    import paper_2601_19489_b200 as ts
+    from paper_2601_19489_b200.binning import IndexBuffers, _ensure_counts, build_index_raw
+    b = random_splats(20_000, 4, 640, 480)
+    db = dev_batch(b)
+    _ensure_counts(db, 0)
+    p = int(db.n_pairs)
+    bufs = IndexBuffers(len(db), p // 2, 40 * 30)
+    build_index_raw(db, 0, bufs)
+    torch.cuda.synchronize()
+    assert int(bufs.overflow.item()) == 1
+    off = bufs.offsets.cpu().numpy()
+    assert off[0] == 0 and off[-1] == p // 2 and np.all(np.diff(off) >= 0)
+    ok = IndexBuffers(len(db), p, 40 * 30)
+    build_index_raw(db, 0, ok)
+    assert int(ok.overflow.item()) == 0
+    assert_index_equal(ts.TileIndex(ok.keys[:p], ok.values[:p], ok.offsets, 40, 30),
+                       O.bin_sequential(b))
