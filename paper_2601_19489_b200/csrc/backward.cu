@@ -50,10 +50,11 @@ __device__ __forceinline__ float2 bc(float x) { return make_float2(x, x); }
 constexpr int kPixSlots = kTilePixels + 1;
 constexpr int kListPad = 32;
 
-struct PixRec {
-  float4 a;  // pixel centre x, y, g_depth, n_considered (int bits)
-  float4 b;  // g_r, g_g, g_b, Ktot + g_T T_final
-};
+// per-pixel record, split in two 16-byte planes (structure of arrays) so the
+// 32 lanes of a systolic step, which read 32 different pixels, spread over
+// all eight 16-byte bank groups:
+//   a = pixel centre x, y, g_depth, n_considered (int bits)
+//   b = g_r, g_g, g_b, Ktot + g_T T_final
 
 template <bool kDepth>
 __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
@@ -65,7 +66,8 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
     const float* __restrict__ grad_color, const float* __restrict__ grad_depth,
     const float* __restrict__ grad_final_T, float* __restrict__ grad2d,
     unsigned long long* __restrict__ merges) {
-  __shared__ PixRec s_pix[kPixSlots];
+  __shared__ float4 s_pa[kPixSlots];
+  __shared__ float4 s_pb[kPixSlots];
   __shared__ unsigned short s_list[kBwdWarps][kTilePixels + 2 * kListPad];  // byte offsets
   __shared__ float2 s_tr[kBwdWarps][kTilePixels + kListPad];  // (T_ckpt, R_ckpt)
   __shared__ int s_maxnc;
@@ -80,8 +82,8 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
   if (tid == 0) {
     s_maxnc = 0;
     s_next = kBwdWarps;  // supergroups 0..kBwdWarps-1 are taken statically
-    s_pix[kTilePixels].a = make_float4(-65536.f, -65536.f, 0.f, __int_as_float(0));  // gauss -> 0
-    s_pix[kTilePixels].b = make_float4(0.f, 0.f, 0.f, 0.f);
+    s_pa[kTilePixels] = make_float4(-65536.f, -65536.f, 0.f, __int_as_float(0));  // gauss -> 0
+    s_pb[kTilePixels] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   bool nz = false;
   int my_max = 0;
@@ -103,8 +105,8 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
     }
     nz |= (gr != 0.f) || (gg != 0.f) || (gb != 0.f) || (gd != 0.f) || (gt != 0.f);
     my_max = max(my_max, nc);
-    s_pix[px].a = make_float4((float)x + 0.5f, (float)y + 0.5f, gd, __int_as_float(nc));
-    s_pix[px].b = make_float4(gr, gg, gb, k);
+    s_pa[px] = make_float4((float)x + 0.5f, (float)y + 0.5f, gd, __int_as_float(nc));
+    s_pb[px] = make_float4(gr, gg, gb, k);
   }
   // tile skipped when its upstream is all zero (backward.py:156-158)
   if (!__syncthreads_or(nz)) return;
@@ -118,9 +120,10 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
   if (ckpt_base) rbase = ckpt_base[tile];
   unsigned short* list = s_list[warp];
   float2* tr = s_tr[warp];
-  const unsigned short kSentinel = (unsigned short)(kTilePixels * sizeof(PixRec));
+  const unsigned short kSentinel = (unsigned short)(kTilePixels * sizeof(float4));
   list[lane] = kSentinel;  // leading sentinels (pipeline fill)
-  const char* pix_base = reinterpret_cast<const char*>(s_pix);
+  const char* pa_base = reinterpret_cast<const char*>(s_pa);
+  const char* pb_base = reinterpret_cast<const char*>(s_pb);
 
   for (int G = warp; G < n_super;) {
     const int P0 = G * kSuper;
@@ -162,7 +165,7 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
 #pragma unroll
       for (int s = 0; s < kTilePixels / 32; ++s) {
         const int px = 32 * s + lane;
-        act[s] = __float_as_int(s_pix[px].a.w) > P0;
+        act[s] = __float_as_int(s_pa[px].w) > P0;
         cT[s] = 1.f; c1[s] = c2[s] = c3[s] = c4[s] = 0.f;
         if (src0 && act[s]) {
           cT[s] = src0[px];
@@ -179,11 +182,11 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
         const unsigned bal = __ballot_sync(0xffffffffu, act[s]);
         if (act[s]) {
           const int kk = n_act + __popc(bal & lt_mask);
-          const PixRec pr = s_pix[px];
-          float K0 = pr.b.x * c1[s] + pr.b.y * c2[s] + pr.b.z * c3[s];
-          if (kDepth) K0 += pr.a.z * c4[s];
-          list[kListPad + kk] = (unsigned short)(px * sizeof(PixRec));
-          tr[kk] = make_float2(cT[s], pr.b.w - K0);
+          const float4 pra = s_pa[px], prb = s_pb[px];
+          float K0 = prb.x * c1[s] + prb.y * c2[s] + prb.z * c3[s];
+          if (kDepth) K0 += pra.z * c4[s];
+          list[kListPad + kk] = (unsigned short)(px * sizeof(float4));
+          tr[kk] = make_float2(cT[s], prb.w - K0);
         }
         n_act += __popc(bal);
       }
@@ -199,18 +202,15 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
       // software pipeline: the next step's pixel record is loaded while this
       // step computes
       float4 pa_n, pb_n;
-      {
-        const PixRec* pr = reinterpret_cast<const PixRec*>(pix_base + my_list[0]);
-        pa_n = pr->a;
-        pb_n = pr->b;
-      }
+      pa_n = *reinterpret_cast<const float4*>(pa_base + my_list[0]);
+      pb_n = *reinterpret_cast<const float4*>(pb_base + my_list[0]);
       for (int t = 0; t < steps; ++t) {
         const float4 pa = pa_n;
         const float4 pb = pb_n;
         {
-          const PixRec* pr = reinterpret_cast<const PixRec*>(pix_base + my_list[t + 1]);
-          pa_n = pr->a;
-          pb_n = pr->b;
+          const unsigned off = my_list[t + 1];
+          pa_n = *reinterpret_cast<const float4*>(pa_base + off);
+          pb_n = *reinterpret_cast<const float4*>(pb_base + off);
         }
         float T_in = __shfl_up_sync(0xffffffffu, T_out, 1);
         float R_in = __shfl_up_sync(0xffffffffu, R_out, 1);

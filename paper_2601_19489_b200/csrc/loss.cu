@@ -23,7 +23,7 @@ namespace tsr {
 constexpr int kLT = 32;              // output tile
 constexpr int kLR = 5;               // filter radius
 constexpr int kLIn = kLT + 2 * kLR;  // 42 rows/cols incl. halo
-constexpr int kLS = 48;              // padded smem row stride (16-B aligned, 4 x float4 reads)
+constexpr int kLS = 48;              // padded smem row stride (8-B aligned float2 reads)
 
 // the window travels as a kernel parameter (constant bank): no device globals
 struct Win {
@@ -53,17 +53,7 @@ __device__ __forceinline__ void load_halo(const float* __restrict__ img, int c, 
     if (dst[k] >= 0) s[dst[k]] = v[k];
 }
 
-// 16 consecutive values of a smem row starting at a multiple of 4.
-__device__ __forceinline__ void load16(const float* s, float* v) {
-  const float4* p = reinterpret_cast<const float4*>(s);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const float4 q = p[k];
-    v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
-  }
-}
-
-__global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__ r,
+__global__ void __launch_bounds__(256, 4) ssim_fwd_kernel(const float* __restrict__ r,
                                                        const float* __restrict__ g, int H, int W,
                                                        float inv_n, float* __restrict__ Q,
                                                        double* __restrict__ partials, Win win) {
@@ -79,19 +69,26 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
     load_halo(r, c, H, W, ty0, tx0, s_r);
     load_halo(g, c, H, W, ty0, tx0, s_g);
     __syncthreads();
-    // horizontal: item = (row, 4 consecutive output cols); 42 x 8 items
-    for (int it = tid; it < kLIn * (kLT / 4); it += 256) {
-      const int row = it >> 3, c0 = (it & 7) * 4;
-      float a[16], b[16];
-      load16(s_r + row * kLS + c0, a);
-      load16(s_g + row * kLS + c0, b);
-      float m1[4] = {0, 0, 0, 0}, m2[4] = {0, 0, 0, 0}, q11[4] = {0, 0, 0, 0},
-            q22[4] = {0, 0, 0, 0}, q12[4] = {0, 0, 0, 0};
+    // horizontal: item = (row, 2 consecutive output cols); 42 x 16 items
+    for (int it = tid; it < kLIn * (kLT / 2); it += 256) {
+      const int row = it >> 4, c0 = (it & 15) * 2;
+      float a[12], b[12];
+      {
+        const float2* pr = reinterpret_cast<const float2*>(s_r + row * kLS + c0);
+        const float2* pg = reinterpret_cast<const float2*>(s_g + row * kLS + c0);
 #pragma unroll
-      for (int k = 0; k < 14; ++k) {
+        for (int k = 0; k < 6; ++k) {
+          const float2 x = pr[k], y = pg[k];
+          a[2 * k] = x.x; a[2 * k + 1] = x.y;
+          b[2 * k] = y.x; b[2 * k + 1] = y.y;
+        }
+      }
+      float m1[2] = {0, 0}, m2[2] = {0, 0}, q11[2] = {0, 0}, q22[2] = {0, 0}, q12[2] = {0, 0};
+#pragma unroll
+      for (int k = 0; k < 12; ++k) {
         const float ak = a[k], bk = b[k], aa = ak * ak, bb = bk * bk, ab = ak * bk;
 #pragma unroll
-        for (int o = 0; o < 4; ++o) {
+        for (int o = 0; o < 2; ++o) {
           const int tap = k - o;
           if (tap >= 0 && tap < 11) {
             const float w = win.w[tap];
@@ -104,7 +101,7 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
         }
       }
 #pragma unroll
-      for (int o = 0; o < 4; ++o) {
+      for (int o = 0; o < 2; ++o) {
         s_h[0][row][c0 + o] = m1[o];
         s_h[1][row][c0 + o] = m2[o];
         s_h[2][row][c0 + o] = q11[o];
@@ -175,7 +172,7 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
   }
 }
 
-__global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__ r,
+__global__ void __launch_bounds__(256, 4) ssim_bwd_kernel(const float* __restrict__ r,
                                                        const float* __restrict__ g, int H, int W,
                                                        float lam, float inv_n,
                                                        const float* __restrict__ Q,
@@ -205,22 +202,27 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__
         if (dst[k] >= 0) s_q[q][dst[k]] = v[k];
     }
     __syncthreads();
-    for (int it = tid; it < kLIn * (kLT / 4); it += 256) {
-      const int row = it >> 3, c0 = (it & 7) * 4;
+    for (int it = tid; it < kLIn * (kLT / 2); it += 256) {
+      const int row = it >> 4, c0 = (it & 15) * 2;
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        float a[16];
-        load16(s_q[q] + row * kLS + c0, a);
-        float h[4] = {0, 0, 0, 0};
+        float a[12];
+        const float2* pq = reinterpret_cast<const float2*>(s_q[q] + row * kLS + c0);
 #pragma unroll
-        for (int k = 0; k < 14; ++k)
+        for (int k = 0; k < 6; ++k) {
+          const float2 x = pq[k];
+          a[2 * k] = x.x; a[2 * k + 1] = x.y;
+        }
+        float h[2] = {0, 0};
 #pragma unroll
-          for (int o = 0; o < 4; ++o) {
+        for (int k = 0; k < 12; ++k)
+#pragma unroll
+          for (int o = 0; o < 2; ++o) {
             const int tap = k - o;
             if (tap >= 0 && tap < 11) h[o] = fmaf(win.w[tap], a[k], h[o]);
           }
 #pragma unroll
-        for (int o = 0; o < 4; ++o) s_h[q][row][c0 + o] = h[o];
+        for (int o = 0; o < 2; ++o) s_h[q][row][c0 + o] = h[o];
       }
     }
     __syncthreads();
