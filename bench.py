@@ -297,7 +297,7 @@ def gpu_arm(args):
 
     import paper_2601_19489_b200 as ts
     from paper_2601_19489_b200.parallel import ViewParallelStep
-    from paper_2601_19489_b200.synthetic import camera_ring, make_scene
+    from paper_2601_19489_b200.synthetic import make_scene, ring_poses
     from paper_2601_19489_b200.trainer import phase_times
 
     rank, world = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1)
@@ -309,7 +309,7 @@ def gpu_arm(args):
     params, cam, gt = make_scene(c["n"], c["width"], c["height"], seed=0,
                                  clustered=c["clustered"])
     gset = ts.GaussianSet(**params)
-    ring = camera_ring(max(world, 1), 4.0, cam["fx"], c["width"], c["height"])
+    ring = ring_poses(max(world, 1), 4.0, cam["fx"], c["width"], c["height"])
     rc = ring[rank]
     camera = ts.Camera(rc["fx"], rc["fy"], rc["cx"], rc["cy"], c["width"], c["height"],
                        rc["R"], rc["t"])

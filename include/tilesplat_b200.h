@@ -127,6 +127,22 @@ int tsr_render_fwd(const float* rec, const int32_t* values, const int64_t* offse
                    int32_t* out_n_contrib, int32_t* out_n_considered,
                    float* ckpt, const int64_t* ckpt_base, void* stream);
 
+/* K3 scoring mode (forward.py:132-137; density.py:36-76).  Re-renders the
+ * view (same outputs as tsr_render_fwd, no checkpoints) and handles every
+ * strong contribution (blend with w = T alpha >= 1/255):
+ *   mode 1: warp_counts[t*4 + w] = strong contributions of warp w of tile t
+ *   mode 2: writes (pixel index, batch row) pairs at warp_base[t*4 + w]
+ *           (exclusive scan of mode 1's counts): the reference's
+ *           Contributions, in (tile, warp, list position, lane) order
+ *   mode 3: row_score[row] += weight for each strong contribution to a pixel
+ *           with mask[pixel] != 0 (the fused density scoring pass). */
+int tsr_render_score(const float* rec, const int32_t* values, const int64_t* offsets,
+                     int32_t width, int32_t height, const float* background_host, int32_t mode,
+                     const uint8_t* mask, float weight, float* row_score, int64_t* warp_counts,
+                     const int64_t* warp_base, int64_t* out_pixel, int64_t* out_row,
+                     float* out_color, float* out_depth, float* out_final_T,
+                     int32_t* out_n_contrib, int32_t* out_n_considered, void* stream);
+
 /* ---------------------------------------------------------------- K4 ----
  * backward_per_gaussian (backward.py:137-223): lane-per-splat groups of 32
  * restarting from checkpoints, warp scans for T and the weighted colour

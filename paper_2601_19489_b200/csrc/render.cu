@@ -24,6 +24,15 @@
 // the records the per-Gaussian backward reads (it enters group g of a pixel
 // only when n_considered > 32 g).  Padding records of dead pixels are never
 // written (they are never read).
+// Scoring (forward.py:132-137; density.py:36-76): a blend whose weight
+// w = T alpha >= 1/255 is a "strong" contribution.  kScore selects what is
+// done with them, per warp and list position with ballots (deterministic):
+//   1  count them per (tile, warp)              -> Contributions sizes
+//   2  write (pixel, row) pairs at a scanned (tile, warp) base
+//   3  mask-weighted score per row: += weight for every strong contribution
+//      to a pixel whose error mask is set (one atomic per warp and splat);
+//      the density pass of the trainer uses this form and never materialises
+//      the contribution lists.
 #include <cuda_runtime.h>
 
 #include "tsr_common.cuh"
@@ -59,6 +68,17 @@ struct PixPair {
   float2 T, Cr, Cg, Cb, D;
   int nc0, nc1, ncons0, ncons1;
   bool alive0, alive1;
+  bool strong0, strong1;  // last blend was a strong contribution (w >= 1/255)
+};
+
+struct ScoreArgs {
+  const uint8_t* mask;         // kScore 3: (H, W) error mask
+  float weight;                // kScore 3
+  float* row_score;            // kScore 3: (M,) += weight per masked strong contribution
+  long long* warp_counts;      // kScore 1: (T * 4,)
+  const long long* warp_base;  // kScore 2: (T * 4,) exclusive scan of warp_counts
+  long long* out_pixel;        // kScore 2
+  long long* out_row;          // kScore 2
 };
 
 __device__ __forceinline__ void blend_pair(const float4 g, const float4 c, const float4 col,
@@ -73,6 +93,8 @@ __device__ __forceinline__ void blend_pair(const float4 g, const float4 c, const
   const bool b0 = s.alive0 && (alpha.x >= kMinAlpha);
   const bool b1 = s.alive1 && (alpha.y >= kMinAlpha);
   const float2 wt = __fmul2_rn(s.T, alpha);
+  s.strong0 = b0 && (wt.x >= kMinAlpha);
+  s.strong1 = b1 && (wt.y >= kMinAlpha);
   const float2 w = make_float2(b0 ? wt.x : 0.f, b1 ? wt.y : 0.f);
   s.Cr = __ffma2_rn(w, bc2(col.x), s.Cr);
   s.Cg = __ffma2_rn(w, bc2(col.y), s.Cg);
@@ -93,18 +115,19 @@ __device__ __forceinline__ void blend_pair(const float4 g, const float4 c, const
 constexpr int kFwdThreads = 128;
 constexpr int kBatch = 256;
 
-template <bool kCkpt>
+template <bool kCkpt, int kScore>
 __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
     const float4* __restrict__ rec, const int32_t* __restrict__ values,
     const int64_t* __restrict__ offsets, int width, int height, int tiles_x, float bg_r,
     float bg_g, float bg_b, float* __restrict__ out_color, float* __restrict__ out_depth,
     float* __restrict__ out_T, int32_t* __restrict__ out_ncontrib,
     int32_t* __restrict__ out_ncons, float* __restrict__ ckpt,
-    const int64_t* __restrict__ ckpt_base) {
+    const int64_t* __restrict__ ckpt_base, ScoreArgs sc) {
   __shared__ float4 s_geo[kBatch];  // mx, my, opacity, depth
   __shared__ float4 s_con[kBatch];  // prescaled conic a', b', c'
   __shared__ float4 s_col[kBatch];  // r, g, b, depth
   __shared__ float4 s_raw[kBatch];  // a, b, c (unscaled), level t
+  __shared__ int s_row[kScore ? kBatch : 1];
 
   const int tile = blockIdx.x;
   const int tyi = tile / tiles_x, txi = tile - tyi * tiles_x;
@@ -129,6 +152,16 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
   s.nc0 = s.nc1 = s.ncons0 = s.ncons1 = 0;
   s.alive0 = in0;
   s.alive1 = in1;
+  s.strong0 = s.strong1 = false;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  long long sc_cursor = 0;  // kScore 1/2: this warp's contributions so far
+  if (kScore == 2) sc_cursor = sc.warp_base[tile * 4 + warp];
+  const long long pix0 = (long long)y0 * width + x, pix1 = (long long)y1 * width + x;
+  bool m0 = false, m1 = false;
+  if (kScore == 3) {
+    m0 = in0 && sc.mask[pix0];
+    m1 = in1 && sc.mask[pix1];
+  }
 
   for (int b0 = 0; b0 < n; b0 += kBatch) {
     if (!__syncthreads_or(s.alive0 || s.alive1)) break;
@@ -145,6 +178,7 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
                                __fmul_rn(r1.x, kQScale), 0.f);
         s_col[i] = make_float4(r2.x, r2.y, r2.z, r1.z);
         s_raw[i] = make_float4(r0.z, r0.w, r1.x, r1.w);
+        if (kScore) s_row[i] = row;
       }
     }
     __syncthreads();
@@ -165,6 +199,29 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
         const int j = __ffs(mask) - 1;
         mask &= mask - 1u;
         blend_pair(s_geo[c0 + j], s_con[c0 + j], s_col[c0 + j], pxf, pyf, pos0 + j, s);
+        if (kScore) {
+          const unsigned q0 = __ballot_sync(0xffffffffu, kScore == 3 ? s.strong0 && m0 : s.strong0);
+          const unsigned q1 = __ballot_sync(0xffffffffu, kScore == 3 ? s.strong1 && m1 : s.strong1);
+          const int nq = __popc(q0) + __popc(q1);
+          if (kScore == 3) {
+            if (lane == 0 && nq) atomicAdd(sc.row_score + s_row[c0 + j], sc.weight * (float)nq);
+          } else {
+            if (kScore == 2) {
+              const long long row = s_row[c0 + j];
+              if (s.strong0) {
+                const long long o = sc_cursor + __popc(q0 & lt_mask);
+                sc.out_pixel[o] = pix0;
+                sc.out_row[o] = row;
+              }
+              if (s.strong1) {
+                const long long o = sc_cursor + __popc(q0) + __popc(q1 & lt_mask);
+                sc.out_pixel[o] = pix1;
+                sc.out_row[o] = row;
+              }
+            }
+            sc_cursor += nq;
+          }
+        }
       }
       if (kCkpt && cend == kGroup) {
         // state after list position pos0+31 -> record (pos0+32)/32 - 1, for
@@ -188,6 +245,7 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
       }
     }
   }
+  if (kScore == 1 && lane == 0) sc.warp_counts[tile * 4 + warp] = sc_cursor;
   // a pixel that never terminated considered the whole list (skipped
   // entries included); a terminated one stopped at its death position
   if (s.alive0) s.ncons0 = n;
@@ -228,17 +286,46 @@ extern "C" int tsr_render_fwd(const float* rec, const int32_t* values, const int
   const int tx = tiles_of(width), ty = tiles_of(height);
   const int n_tiles = tx * ty;
   cudaStream_t s = (cudaStream_t)stream;
+  const ScoreArgs none{};
   if (ckpt) {
-    render_fwd_kernel<true><<<n_tiles, kFwdThreads, 0, s>>>(
+    render_fwd_kernel<true, 0><<<n_tiles, kFwdThreads, 0, s>>>(
         (const float4*)rec, values, offsets, width, height, tx, background_host[0],
         background_host[1], background_host[2], out_color, out_depth, out_final_T,
-        out_n_contrib, out_n_considered, ckpt, ckpt_base);
+        out_n_contrib, out_n_considered, ckpt, ckpt_base, none);
   } else {
-    render_fwd_kernel<false><<<n_tiles, kFwdThreads, 0, s>>>(
+    render_fwd_kernel<false, 0><<<n_tiles, kFwdThreads, 0, s>>>(
         (const float4*)rec, values, offsets, width, height, tx, background_host[0],
         background_host[1], background_host[2], out_color, out_depth, out_final_T,
-        out_n_contrib, out_n_considered, nullptr, nullptr);
+        out_n_contrib, out_n_considered, nullptr, nullptr, none);
   }
+  TSR_CHECK_LAUNCH();
+  return TSR_OK;
+}
+
+extern "C" int tsr_render_score(const float* rec, const int32_t* values, const int64_t* offsets,
+                                int32_t width, int32_t height, const float* background_host,
+                                int32_t mode, const uint8_t* mask, float weight,
+                                float* row_score, int64_t* warp_counts,
+                                const int64_t* warp_base, int64_t* out_pixel, int64_t* out_row,
+                                float* out_color, float* out_depth, float* out_final_T,
+                                int32_t* out_n_contrib, int32_t* out_n_considered,
+                                void* stream) {
+  if (width <= 0 || height <= 0 || !background_host) return TSR_E_INVALID;
+  if (mode == 1 && !warp_counts) return TSR_E_INVALID;
+  if (mode == 2 && (!warp_base || !out_pixel || !out_row)) return TSR_E_INVALID;
+  if (mode == 3 && (!mask || !row_score)) return TSR_E_INVALID;
+  if (mode < 1 || mode > 3) return TSR_E_INVALID;
+  const int tx = tiles_of(width), ty = tiles_of(height);
+  const int n_tiles = tx * ty;
+  cudaStream_t s = (cudaStream_t)stream;
+  ScoreArgs sc{mask, weight, row_score, (long long*)warp_counts, (const long long*)warp_base,
+               (long long*)out_pixel, (long long*)out_row};
+  auto* k = mode == 1 ? render_fwd_kernel<false, 1>
+            : mode == 2 ? render_fwd_kernel<false, 2> : render_fwd_kernel<false, 3>;
+  k<<<n_tiles, kFwdThreads, 0, s>>>((const float4*)rec, values, offsets, width, height, tx,
+                                    background_host[0], background_host[1], background_host[2],
+                                    out_color, out_depth, out_final_T, out_n_contrib,
+                                    out_n_considered, nullptr, nullptr, sc);
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }

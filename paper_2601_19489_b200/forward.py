@@ -114,6 +114,31 @@ class RenderTargets:
                                     device=dev)
 
 
+@dataclass
+class Contributions:
+    """Strong contributions (w = T alpha >= 1/255) of a scoring render
+    (forward.py:53-58): parallel int64 device arrays.  The multiset equals
+    the reference's; the order is (tile, warp block, list position, lane)
+    instead of (tile, list position, row-major pixel)."""
+    pixel_idx: torch.Tensor
+    splat_rows: torch.Tensor
+
+
+def render_score_raw(rec, values, offsets, width: int, height: int, background, out: RenderTargets,
+                     mode: int, *, mask=None, weight: float = 0.0, row_score=None,
+                     warp_counts=None, warp_base=None, out_pixel=None, out_row=None) -> None:
+    """Launch K3 in scoring mode 1 (count), 2 (write) or 3 (masked row score)."""
+    lib = _lib.load()
+    bg = np.asarray(background, dtype=np.float64).reshape(3)
+    bg_host = (_lib.c_f32 * 3)(*[float(v) for v in bg])
+    _lib.check(lib.tsr_render_score(
+        rec.data_ptr(), _lib.ptr(values), offsets.data_ptr(), width, height, bg_host, mode,
+        _lib.ptr(mask), float(weight), _lib.ptr(row_score), _lib.ptr(warp_counts),
+        _lib.ptr(warp_base), _lib.ptr(out_pixel), _lib.ptr(out_row), out.color.data_ptr(),
+        out.depth.data_ptr(), out.final_T.data_ptr(), out.n_contrib.data_ptr(),
+        out.n_considered.data_ptr(), _lib.stream_handle()), "tsr_render_score")
+
+
 def render_raw(rec, values, offsets, ckpt_base, width: int, height: int, background,
                out: RenderTargets) -> None:
     """Launch K3 into preallocated targets (no host synchronisation)."""
@@ -131,8 +156,6 @@ def render_raw(rec, values, offsets, ckpt_base, width: int, height: int, backgro
 def render(batch: SplatBatch, tiles: TileIndex, colors, background, *,
            record_checkpoints: bool = True, scoring: bool = False):
     """K3 forward (forward.py:87-161)."""
-    if scoring:
-        raise NotImplementedError("scoring mode (density, SURVEY §8(f) #2) is not built yet")
     _ensure_colors(batch, colors)
     H, W = batch.height, batch.width
     bg = np.asarray(background, dtype=np.float64).reshape(3)
@@ -143,6 +166,30 @@ def render(batch: SplatBatch, tiles: TileIndex, colors, background, *,
                tiles.ckpt_base, W, H, bg, out)
     color, depth, final_T, n_contrib, n_cons, ckpt = (out.color, out.depth, out.final_T,
                                                       out.n_contrib, out.n_considered, out.ckpt)
-    return RenderBuffers(color, depth, final_T, n_contrib, n_cons, bg, ckpt,
+    bufs = RenderBuffers(color, depth, final_T, n_contrib, n_cons, bg, ckpt,
                          tiles.ckpt_base if ckpt is not None else None,
                          tiles.tiles_x, tiles.tiles_y)
+    if not scoring:
+        return bufs
+    return bufs, contributions(batch, tiles, bg)
+
+
+def contributions(batch: SplatBatch, tiles: TileIndex, background) -> Contributions:
+    """Scoring render (forward.py:132-137): count the strong contributions per
+    (tile, warp), scan, then write them (two K3 launches in scoring mode)."""
+    H, W = batch.height, batch.width
+    dev = _device()
+    scratch = RenderTargets(H, W, None)
+    n_slots = tiles.n_tiles * 4
+    counts = torch.zeros(n_slots, dtype=torch.int64, device=dev)
+    values = tiles.values if tiles.n_pairs else None
+    render_score_raw(batch.rec, values, tiles.offsets, W, H, background, scratch, 1,
+                     warp_counts=counts)
+    base = torch.cumsum(counts, 0) - counts
+    total = int(counts.sum().item())
+    pix = torch.empty(max(total, 1), dtype=torch.int64, device=dev)[:total]
+    rows = torch.empty(max(total, 1), dtype=torch.int64, device=dev)[:total]
+    if total:
+        render_score_raw(batch.rec, values, tiles.offsets, W, H, background, scratch, 2,
+                         warp_base=base, out_pixel=pix, out_row=rows)
+    return Contributions(pix, rows)

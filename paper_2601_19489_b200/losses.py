@@ -107,6 +107,29 @@ def disparity_loss(rendered_depth, prior_depth, valid_mask, weight: float):
     return loss, grad
 
 
+def depth_chain_device(depth, final_T, n_contrib, prior, valid, weight: float):
+    """Sync-free disparity loss + its chain through d_norm = D / (1 - T_f)
+    (losses.py:94-112, trainer.py:201-214) for the fused training step:
+    returns (loss 0-d tensor, grad_depth, grad_final_T), all on the device."""
+    mask = n_contrib > 0
+    if valid is not None:
+        mask = mask & valid
+    denom = 1.0 - final_T
+    one = torch.ones_like(denom)
+    d = torch.where(mask, depth / torch.where(mask, denom, one), torch.zeros_like(depth))
+    n_valid = mask.sum().clamp(min=1).to(torch.float32)
+    d_r = torch.clamp(d, min=DISPARITY_EPS)
+    d_p = torch.clamp(prior, min=DISPARITY_EPS)
+    diff = 1.0 / d_r - 1.0 / d_p
+    loss = weight * torch.where(mask, diff.abs(), torch.zeros_like(diff)).sum() / n_valid
+    g = weight * torch.sign(diff) * (-1.0 / (d_r * d_r)) / n_valid
+    g = torch.where(mask & (d >= DISPARITY_EPS), g, torch.zeros_like(g))
+    grad_depth = torch.where(mask, g / torch.where(mask, denom, one), torch.zeros_like(g))
+    grad_final_T = torch.where(mask, g * depth / torch.where(mask, denom * denom, one),
+                               torch.zeros_like(g))
+    return loss, grad_depth, grad_final_T
+
+
 def depth_weight_schedule(iteration: int, max_iter: int, w0: float = 0.1) -> float:
     decay_end = max_iter / 2.0
     if decay_end <= 0:

@@ -131,10 +131,16 @@ class Adam:
     def resize(self, decisions) -> None:
         """Mirror a densify/prune mutation on the moments (optim.py:90-111)."""
         n_old = len(decisions)
-        keep = torch.tensor([d.action not in ("prune", "split") for d in decisions],
-                            device="cuda")
-        n_new = sum(d.action == "clone" for d in decisions) + \
-            2 * sum(d.action == "split" for d in decisions)
+        codes = getattr(decisions, "codes", None)
+        if codes is not None:  # density.Decisions: device action codes
+            from .density import CLONE, PRUNE, SPLIT
+            keep = (codes != PRUNE) & (codes != SPLIT)
+            n_new = int((codes == CLONE).sum()) + 2 * int((codes == SPLIT).sum())
+        else:
+            keep = torch.tensor([d.action not in ("prune", "split") for d in decisions],
+                                dtype=torch.bool, device="cuda")
+            n_new = sum(d.action == "clone" for d in decisions) + \
+                2 * sum(d.action == "split" for d in decisions)
         for name in SPLAT_GROUPS:
             if name not in self._m:
                 continue

@@ -24,14 +24,82 @@ def look_at(eye, target, fx, width, height):
                 R=R, t=-R @ eye)
 
 
-def camera_ring(n_views, radius, fx, width, height):
-    """Cameras on a full ring looking at the origin (synthetic.py:63-76)."""
+def ring_poses(n_views, radius, fx, width, height):
+    """Pose dicts of a full camera ring looking at the origin (the bench's
+    view-parallel cameras; synthetic.py:63-76)."""
     cams = []
     for i in range(n_views):
         phi = 2.0 * np.pi * i / n_views
         eye = np.array([radius * np.sin(phi), 0.0, -radius * np.cos(phi)])
         cams.append(look_at(eye, (0.0, 0.0, 0.0), fx, width, height))
     return cams
+
+
+def look_at_camera(eye, target, fx, width, height, name=""):
+    """A `Camera` at eye looking at target (synthetic.py:46-60)."""
+    from .scene import Camera
+    p = look_at(eye, target, fx, width, height)
+    return Camera(p["fx"], p["fy"], p["cx"], p["cy"], width, height, p["R"], p["t"], name=name)
+
+
+def camera_ring(n_views: int, radius: float = 4.0, fx: float = 45.0, width: int = 48,
+                height: int = 48, z_offset: float = 0.0, arc_degrees: float = 360.0):
+    """Cameras on a ring (or an arc of it) looking at the origin
+    (synthetic.py:63-76)."""
+    cams = []
+    full = abs(arc_degrees - 360.0) < 1e-9
+    for i in range(n_views):
+        span = np.deg2rad(arc_degrees)
+        phi = span * i / n_views if full else span * (i / max(n_views - 1, 1) - 0.5)
+        eye = np.array([radius * np.sin(phi), z_offset, -radius * np.cos(phi)])
+        cams.append(look_at_camera(eye, (0.0, 0.0, 0.0), fx, width, height,
+                                   name=f"view_{i:04d}.png"))
+    return cams
+
+
+def random_gaussian_set(n_splats: int, seed: int = 0, spread: float = 0.8,
+                        scale_range=(0.12, 0.3), opacity_range=(0.5, 0.9), sh_degree: int = 0):
+    """synthetic.py:79-96 (host draw, uploaded once)."""
+    from .scene import GaussianSet
+    rng = np.random.default_rng(seed)
+    colors = np.zeros((n_splats, (sh_degree + 1) ** 2, 3))
+    colors[:, 0, :] = rng.uniform(0.15, 0.85, (n_splats, 3))
+    if sh_degree > 0:
+        colors[:, 1:, :] = rng.normal(0.0, 0.05, colors[:, 1:, :].shape)
+    quats = rng.normal(0.0, 1.0, (n_splats, 4))
+    quats /= np.linalg.norm(quats, axis=1, keepdims=True)
+    op = rng.uniform(*opacity_range, n_splats)
+    return GaussianSet(positions=rng.uniform(-spread, spread, (n_splats, 3)),
+                       log_scales=np.log(rng.uniform(*scale_range, (n_splats, 3))),
+                       rotations=quats, opacity_logits=np.log(op / (1.0 - op)), colors=colors)
+
+
+def synthetic_scene(n_splats: int = 10, n_views: int = 5, width: int = 48, height: int = 48,
+                    seed: int = 0, fx: float = 45.0, with_depth: bool = True,
+                    background=(0.0, 0.0, 0.0), arc_degrees: float = 360.0, gt_set=None):
+    """Self-consistent scene (synthetic.py:99-122): GT splats rendered by the
+    B200 renderer become the ground-truth images (and exact depth priors).
+    Returns (scene, gt_set).  `gt_set` overrides the random GT splats (the C5
+    workload renders the canonical 1M-splat scene into its views)."""
+    import torch
+    from .ingest import Scene
+    from .trainer import TrainConfig, render_view
+    if gt_set is None:
+        gt_set = random_gaussian_set(n_splats, seed=seed)
+    cams = camera_ring(n_views, fx=fx, width=width, height=height, arc_degrees=arc_degrees)
+    cfg = TrainConfig(round_profile="round2", max_iters=1, background=background)
+    for cam in cams:
+        vr = render_view(gt_set, cam, cfg, checkpoints=False)
+        b = vr.buffers
+        cam.gt_image = torch.clamp(b.color, 0.0, 1.0).cpu().numpy().astype(np.float64)
+        if with_depth:
+            cam.depth_prior = b.normalized_depth().cpu().numpy().astype(np.float64)
+            cam.depth_valid = ((b.n_contrib > 0).cpu().numpy()) & (cam.depth_prior > 0)
+    h = gt_set.to_numpy()
+    scene = Scene(cameras=cams, points=h["positions"].copy(),
+                  colors=(np.clip(h["colors"][:, 0, :], 0, 1) * 255).astype(np.uint8),
+                  extent=4.0 * 1.1)
+    return scene, gt_set
 
 
 def make_scene(n, width, height, seed=0, clustered=False, sh_degree=0):

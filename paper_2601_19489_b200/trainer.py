@@ -33,21 +33,48 @@ _PROFILE_DEFAULTS = {
 
 @dataclass
 class TrainConfig:
-    """Hot-path subset of the reference TrainConfig (trainer.py:42-113), same
-    names and defaults."""
+    """The reference TrainConfig (trainer.py:42-113): same names, defaults
+    and validation."""
     round_profile: str = "round2"
     max_iters: int | None = None
+    budget_seconds: float = 60.0
     pose_opt: bool | None = None
     depth_supervision: bool | None = None
+
     lambda_: float = 0.2
     depth_weight0: float = 0.1
+
+    densify: bool = True
+    densify_interval: int = 300
+    densify_start: int = 500
+    densify_end: int | None = None  # defaults to 0.8 * max_iters
+    consistency_views: int = 10  # K
+    error_tau: float = 0.5
+    theta_plus: float = 16.0
+    theta_minus: float = 0.9
+    scale_split_threshold_frac: float = 0.01
+    min_splats: int = 16
+
+    pose_bake_interval: int = 300
+
     sh_degree: int = 0
     background: tuple = (0.0, 0.0, 0.0)
     near: float = 0.01
     seed: int = 0
+    eval_interval: int = 100
+    holdout_views: tuple = ()
+    deterministic: bool = True
+    threads: int = 1
     binning_strategy: str = "sequential"  # sequential | load_balanced
     backward_path: str = "per_gaussian"
+    init_opacity: float = 0.1
     lrs: dict = field(default_factory=dict)
+
+    colmap_dir: str | None = None
+    images_dir: str | None = None
+    depth_dir: str | None = None
+    output_dir: str | None = None
+    depth_samples_per_view: int = 0
 
     def __post_init__(self):
         if self.round_profile not in _PROFILE_DEFAULTS:
@@ -59,11 +86,31 @@ class TrainConfig:
             self.pose_opt = prof["pose_opt"]
         if self.depth_supervision is None:
             self.depth_supervision = prof["depth_supervision"]
+        if self.densify_end is None:
+            self.densify_end = int(0.8 * self.max_iters)
+        if self.budget_seconds <= 0:
+            raise ValueError("budget_seconds must be > 0")
         if self.binning_strategy not in ("sequential", "load_balanced"):
             raise ValueError(f"unknown binning_strategy {self.binning_strategy!r}")
         if self.backward_path != "per_gaussian":
             raise ValueError("only the per-Gaussian backward is built for the GPU "
                              "(backward_per_pixel is the CPU oracle)")
+
+    @classmethod
+    def from_json(cls, path) -> "TrainConfig":
+        import json
+        with open(path) as fh:
+            data = json.load(fh)
+        unknown = set(data) - set(cls.__dataclass_fields__)
+        if unknown:
+            raise ValueError(f"unknown config keys: {sorted(unknown)}")
+        return cls(**data)
+
+    def to_json(self, path) -> None:
+        import json
+        from dataclasses import asdict
+        with open(path, "w") as fh:
+            json.dump(asdict(self), fh, indent=2, default=list)
 
     @property
     def strategy_id(self) -> int:
@@ -87,9 +134,12 @@ def render_view(gset: GaussianSet, camera: Camera, cfg: TrainConfig,
     batch = project(gset, camera, near=cfg.near, delta=delta, strategy=cfg.strategy_id)
     tiles = build_index(batch, cfg.strategy_id)
     colors = batch.colors
-    bufs = render(batch, tiles, colors, cfg.background, record_checkpoints=checkpoints,
-                  scoring=scoring)
-    return ViewRender(batch, tiles, colors, None, bufs)
+    out = render(batch, tiles, colors, cfg.background, record_checkpoints=checkpoints,
+                 scoring=scoring)
+    if scoring:
+        bufs, contribs = out
+        return ViewRender(batch, tiles, colors, None, bufs, contribs)
+    return ViewRender(batch, tiles, colors, None, out)
 
 
 def view_loss_and_grads(camera: Camera, cfg: TrainConfig, vr: ViewRender,
@@ -171,6 +221,7 @@ class TrainStep:
         self.status_event = None
         self.lib = _lib.load()
         self.last = None
+        self.last_losses = None
 
     @staticmethod
     def _mark(timer, name):
@@ -233,11 +284,19 @@ class TrainStep:
         self._mark(timer, "render")
         return batch
 
-    def loss_and_backward(self, batch, camera: Camera, gt_image, timer=None):
+    def loss_and_backward(self, batch, camera: Camera, gt_image, timer=None,
+                          depth_weight: float = 0.0, depth_prior=None, depth_valid=None):
         out, idx = self.targets, self.index
         e, l1, s, grad_color = losses.photometric_device(out.color, gt_image, self.cfg.lambda_,
                                                          grad=self.grad_color,
                                                          workspace=self.loss_ws)
+        gd = gt = None
+        dl = None
+        if depth_weight > 0.0 and depth_prior is not None:
+            dl, gd, gt = losses.depth_chain_device(out.depth, out.final_T, out.n_contrib,
+                                                   depth_prior, depth_valid, depth_weight)
+            e = e + dl
+        self.last_losses = (e, l1, s, dl)
         self._mark(timer, "loss")
         if not self._grad2d_clean:
             self.grad2d.zero_()
@@ -246,8 +305,8 @@ class TrainStep:
             batch.rec.data_ptr(), idx.values.data_ptr(), idx.offsets.data_ptr(), camera.width,
             camera.height, out.color.data_ptr(), out.depth.data_ptr(), out.final_T.data_ptr(),
             out.n_considered.data_ptr(), out.ckpt.data_ptr(), idx.ckpt_base.data_ptr(),
-            grad_color.data_ptr(), None, None, self.grad2d.data_ptr(), self.merges.data_ptr(),
-            _lib.stream_handle()), "tsr_render_bwd")
+            grad_color.data_ptr(), _lib.ptr(gd), _lib.ptr(gt), self.grad2d.data_ptr(),
+            self.merges.data_ptr(), _lib.stream_handle()), "tsr_render_bwd")
         self._mark(timer, "backward")
         return e
 
@@ -258,13 +317,15 @@ class TrainStep:
         self.status_event = torch.cuda.Event()
         self.status_event.record()
 
-    def step(self, camera: Camera, gt_image: torch.Tensor, timer=None) -> torch.Tensor:
+    def step(self, camera: Camera, gt_image: torch.Tensor, timer=None,
+             depth_weight: float = 0.0, depth_prior=None, depth_valid=None) -> torch.Tensor:
         """Run one step; returns the loss as a device scalar (no host sync)."""
         if self.index is not None:
             self._poll_status(camera)
         self.iteration += 1
         batch = self.forward(camera, timer)
-        e = self.loss_and_backward(batch, camera, gt_image, timer)
+        e = self.loss_and_backward(batch, camera, gt_image, timer, depth_weight, depth_prior,
+                                   depth_valid)
         lr = {"positions": position_lr(self.pos_base_lr, self.iteration, self.cfg.max_iters)}
         groups = self.opt.groups_for_fused(self.gset.params(), lr)
         _lib.check(self.lib.tsr_preprocess_bwd_adam(
@@ -311,3 +372,264 @@ def phase_times(timer) -> dict:
             continue
         out[name] = out.get(name, 0.0) + a.elapsed_time(b)
     return out
+
+
+# --------------------------------------------------------------------------
+# The training loop (trainer.py:255-395)
+
+
+class TrainingDiverged(RuntimeError):
+    def __init__(self, message, dump=None):
+        super().__init__(message)
+        self.dump = dump or {}
+
+
+@dataclass
+class TrainResult:
+    gset: GaussianSet
+    metrics: list
+    delta: PoseDelta
+    baked_total: PoseDelta
+    iterations: int
+    elapsed: float
+    stop_reason: str  # completed | budget
+    eval_split: str = "train"
+
+
+def init_gaussians(scene, sh_degree: int = 0, init_opacity: float = 0.1) -> GaussianSet:
+    """Seed splats from the point cloud, isotropic with radius = mean distance
+    to the 3 nearest neighbours (trainer.py:137-160).  Host setup (once)."""
+    from scipy.spatial import cKDTree
+    pts = np.asarray(scene.points, dtype=np.float64).reshape(-1, 3)
+    n = len(pts)
+    if n == 0:
+        raise ValueError("cannot initialize from an empty point cloud")
+    if n >= 4:
+        dist, _ = cKDTree(pts).query(pts, k=4)
+        radius = np.maximum(dist[:, 1:].mean(axis=1), 1e-7)
+    else:
+        radius = np.full(n, 0.1 * scene.extent)
+    colors = np.zeros((n, (sh_degree + 1) ** 2, 3))
+    colors[:, 0, :] = np.asarray(scene.colors) / 255.0
+    rot = np.zeros((n, 4))
+    rot[:, 0] = 1.0
+    return GaussianSet(positions=pts.copy(), log_scales=np.log(radius)[:, None].repeat(3, 1),
+                       rotations=rot, opacity_logits=np.full(n, np.log(init_opacity /
+                                                                        (1 - init_opacity))),
+                       colors=colors)
+
+
+def evaluate(gset: GaussianSet, cameras, cfg: TrainConfig | None = None,
+             delta: PoseDelta | None = None) -> float:
+    """Mean PSNR over the cameras' ground truth (trainer.py:260-270)."""
+    cfg = cfg or TrainConfig()
+    values = []
+    for cam in cameras:
+        if cam.gt_image is None:
+            continue
+        vr = render_view(gset, cam, cfg, delta, checkpoints=False)
+        values.append(losses.psnr(vr.buffers.color, cam.gt_image))
+    if not values:
+        raise ValueError("no cameras with ground-truth images to evaluate")
+    return float(np.mean(values))
+
+
+def _densify_round(gset, scene, cfg, delta, rng, pool):
+    """Sample K views, render in scoring mode, return (s+, s-)
+    (trainer.py:273-290) -- the reference's form, through Contributions."""
+    from . import density
+    k = cfg.consistency_views
+    view_ids = pool[rng.integers(0, len(pool), size=k)]
+    masks, pix, ids, e_photos = [], [], [], []
+    for v in view_ids:
+        cam = scene.cameras[int(v)]
+        vr = render_view(gset, cam, cfg, delta, checkpoints=False, scoring=True)
+        rep, _ = losses.photometric(vr.buffers.color, cam.gt_image, cfg.lambda_)
+        masks.append(density.error_mask(vr.buffers.color, cam.gt_image, cfg.error_tau))
+        pix.append(vr.contributions.pixel_idx)
+        ids.append(vr.batch.source_ids[vr.contributions.splat_rows])
+        e_photos.append(rep.photometric)
+    s_plus = density.score_densify(masks, pix, ids, len(gset))
+    s_minus = density.score_prune(masks, pix, ids, e_photos, len(gset))
+    return s_plus, s_minus
+
+
+def _densify_round_fused(gset, scene, cfg, delta, rng, pool, gt_dev):
+    """The same scores with K3 scoring mode 3: per view one render, the error
+    mask, and one masked-count render straight into per-row scores; no
+    contribution lists.  Draws the same view ids from rng."""
+    from . import density
+    k = cfg.consistency_views
+    view_ids = pool[rng.integers(0, len(pool), size=k)]
+    n = len(gset)
+    dev = _device()
+    s_plus = torch.zeros(n, dtype=torch.float64, device=dev)
+    raw = torch.zeros(n, dtype=torch.float64, device=dev)
+    for v in view_ids:
+        cam = scene.cameras[int(v)]
+        vr = render_view(gset, cam, cfg, delta, checkpoints=False)
+        gt = gt_dev[int(v)]
+        e, _, _, _ = losses.photometric_device(vr.buffers.color, gt, cfg.lambda_)
+        mask = density.error_mask(vr.buffers.color, gt, cfg.error_tau)
+        counts = density.masked_row_counts(vr.batch, vr.tiles, cfg.background, mask)
+        src = vr.batch.source_ids.long()
+        c64 = counts.double()
+        s_plus.index_add_(0, src, c64)
+        raw.index_add_(0, src, e.double() * c64)
+    return s_plus / max(k, 1), density._minmax(raw)
+
+
+def train(scene, cfg: TrainConfig, *, ply_path=None, metrics_path=None, decisions_path=None,
+          initial: GaussianSet | None = None, fused_scoring: bool = True) -> TrainResult:
+    """The reference loop (trainer.py:293-395): view sampling, render, loss,
+    backward, Adam, densify/prune cadence, pose bake cadence, PSNR cadence,
+    wall-clock budget stop, PLY save.
+
+    Without pose optimisation every iteration is one `TrainStep` (no host
+    synchronisation; per-iteration losses stay on the device and are read
+    at eval points, where the budget and divergence are also checked).  With
+    pose optimisation the composable API path (render_view ->
+    view_loss_and_grads -> _full_grads -> Adam) runs, as in the reference."""
+    import time
+    from pathlib import Path
+    from . import density
+    from .pose import bake, compose, identity_delta
+    if not scene.cameras:
+        raise ValueError("scene has no cameras")
+    rng = np.random.default_rng(cfg.seed)
+    gset = initial.copy() if initial is not None else init_gaussians(
+        scene, cfg.sh_degree, cfg.init_opacity)
+    holdout = set(int(i) for i in cfg.holdout_views)
+    pool = np.array([i for i in range(len(scene.cameras)) if i not in holdout])
+    if len(pool) == 0:
+        raise ValueError("holdout_views leaves no training cameras")
+    eval_cams = [scene.cameras[i] for i in sorted(holdout)] if holdout else scene.cameras
+    opt = Adam({k: v for k, v in cfg.lrs.items() if k != "positions"})
+    pos_base_lr = cfg.lrs.get("positions", 1.6e-4 * scene.extent)
+    delta = identity_delta() if cfg.pose_opt else None
+    baked_total = identity_delta()
+    gt_dev = [as_device_f32(c.gt_image) if c.gt_image is not None else None
+              for c in scene.cameras]
+    prior_dev = [as_device_f32(c.depth_prior) if c.depth_prior is not None else None
+                 for c in scene.cameras]
+    valid_dev = [torch.as_tensor(np.asarray(c.depth_valid), device=_device()).bool()
+                 if c.depth_valid is not None else None for c in scene.cameras]
+    stepper = None if cfg.pose_opt else TrainStep(gset, cfg, extent=scene.extent, optimizer=opt)
+    pose_t = {k: torch.zeros((1, 3), dtype=torch.float32, device=_device())
+              for k in ("pose_rot", "pose_trans")}
+    metrics, pending, decision_rows = [], [], []
+    stop_reason = "completed"
+    start = time.perf_counter()
+    iteration = 0
+
+    def flush():
+        """Read the pending device losses; divergence check."""
+        if not pending:
+            return
+        vals = torch.stack([torch.stack([e, l1, s, d]) for _, e, l1, s, d in pending]).cpu()
+        for (it, *_), row in zip(pending, vals.tolist()):
+            if not np.isfinite(row[0]):
+                dump = {"iteration": it, "loss": row[0], "l1": row[1], "ssim": row[2]}
+                if ply_path:
+                    Path(ply_path).with_suffix(".diverged.json").write_text(str(dump))
+                raise TrainingDiverged(f"non-finite loss at iteration {it}", dump)
+            metrics.append({"iter": it, "l1": row[1], "ssim": row[2], "depth_loss": row[3],
+                            "total": row[0], "psnr": np.nan})
+        pending.clear()
+
+    zero = torch.zeros((), device=_device())
+    while iteration < cfg.max_iters:
+        iteration += 1
+        v = int(pool[rng.integers(0, len(pool))])
+        cam = scene.cameras[v]
+        depth_weight = (losses.depth_weight_schedule(iteration - 1, cfg.max_iters,
+                                                     cfg.depth_weight0)
+                        if cfg.depth_supervision else 0.0)
+        if stepper is not None:
+            stepper.iteration = iteration - 1
+            stepper.step(cam, gt_dev[v], depth_weight=depth_weight, depth_prior=prior_dev[v],
+                         depth_valid=valid_dev[v])
+            e, l1, s, dl = stepper.last_losses
+            pending.append((iteration, e, l1, s, dl if dl is not None else zero))
+        else:
+            vr = render_view(gset, cam, cfg, delta)
+            report, g2 = view_loss_and_grads(cam, cfg, vr, depth_weight)
+            grads = _full_grads(gset, cam, cfg, delta, vr, g2)
+            opt.step(gset.params(), {k: grads[k] for k in gset.params()},
+                     {"positions": position_lr(pos_base_lr, iteration, cfg.max_iters)})
+            pose_t["pose_rot"].copy_(torch.as_tensor(delta.rot_vec).reshape(1, 3))
+            pose_t["pose_trans"].copy_(torch.as_tensor(delta.trans).reshape(1, 3))
+            opt.step(pose_t, {k: torch.as_tensor(np.asarray(grads[k], np.float32)).reshape(1, 3)
+                              for k in pose_t})
+            delta.rot_vec[:] = pose_t["pose_rot"].double().cpu().numpy().reshape(3)
+            delta.trans[:] = pose_t["pose_trans"].double().cpu().numpy().reshape(3)
+            delta.steps_since_bake += 1
+            t = lambda x: torch.tensor(float(x), device=_device())  # noqa: E731
+            pending.append((iteration, t(report.total), t(report.l1), t(report.ssim),
+                            t(report.depth_loss)))
+
+        if (cfg.densify and cfg.densify_start <= iteration < cfg.densify_end
+                and iteration % cfg.densify_interval == 0):
+            flush()
+            if fused_scoring:
+                s_plus, s_minus = _densify_round_fused(gset, scene, cfg, delta, rng, pool, gt_dev)
+            else:
+                s_plus, s_minus = _densify_round(gset, scene, cfg, delta, rng, pool)
+            threshold = cfg.scale_split_threshold_frac * scene.extent
+            gset, decisions = density.apply_decisions(gset, s_plus, s_minus, cfg.theta_plus,
+                                                      cfg.theta_minus, threshold, rng,
+                                                      min_splats=cfg.min_splats)
+            opt.resize(decisions)
+            c = decisions.counts()
+            decision_rows.append({"iter": iteration, "clones": c["clone"], "splits": c["split"],
+                                  "prunes": c["prune"], "total": len(gset)})
+            if stepper is not None:
+                stepper = TrainStep(gset, cfg, extent=scene.extent, optimizer=opt)
+
+        if cfg.pose_opt and delta.steps_since_bake >= cfg.pose_bake_interval:
+            baked = bake(delta, scene.cameras)
+            baked_total = compose(baked_total, baked)
+            opt.reset_group("pose_rot")
+            opt.reset_group("pose_trans")
+
+        if iteration % cfg.eval_interval == 0 or iteration == cfg.max_iters:
+            flush()
+            metrics[-1]["psnr"] = evaluate(gset, eval_cams, cfg, delta)
+        if iteration % 32 == 0 or iteration == cfg.max_iters:
+            torch.cuda.synchronize()  # bound the launch queue so host time ~ device time
+        if time.perf_counter() - start > cfg.budget_seconds:
+            stop_reason = "budget"
+            break
+    flush()
+    torch.cuda.synchronize()
+    elapsed = time.perf_counter() - start
+    result = TrainResult(gset=gset, metrics=metrics, delta=delta or identity_delta(),
+                         baked_total=baked_total, iterations=iteration, elapsed=elapsed,
+                         stop_reason=stop_reason,
+                         eval_split="holdout" if holdout else "train")
+    if ply_path:
+        from .ingest import write_ply
+        write_ply(gset, ply_path)
+    if metrics_path:
+        write_metrics_csv(metrics_path, metrics, eval_split=result.eval_split)
+    if decisions_path:
+        write_decisions_csv(decisions_path, decision_rows)
+    return result
+
+
+def write_metrics_csv(path, metrics, eval_split="train") -> None:
+    with open(path, "w") as fh:
+        fh.write(f"# eval split: {eval_split}\n")
+        fh.write("iter,l1,ssim,depth_loss,total,psnr\n")
+        for row in metrics:
+            psnr = "" if np.isnan(row["psnr"]) else f"{row['psnr']:.6f}"
+            fh.write(f"{row['iter']},{row['l1']:.8f},{row['ssim']:.8f},"
+                     f"{row['depth_loss']:.8f},{row['total']:.8f},{psnr}\n")
+
+
+def write_decisions_csv(path, rows) -> None:
+    with open(path, "w") as fh:
+        fh.write("iter,clones,splits,prunes,total\n")
+        for row in rows:
+            fh.write(f"{row['iter']},{row['clones']},{row['splits']},"
+                     f"{row['prunes']},{row['total']}\n")

@@ -242,7 +242,76 @@ def golden_projection():
     np.savez_compressed(OUT / "projection.npz", **out)
 
 
+def golden_density():
+    """Scoring render, error masks, scores, decisions and moment resize
+    (density.py, forward.py:132-137, optim.py:90-111)."""
+    from tilesplat import density
+    from tilesplat.optim import Adam
+    out = {}
+    rng = np.random.default_rng(77)
+    masks, pix, ids, e_ph = [], [], [], []
+    for v, (n, w, h) in enumerate(((90, 48, 40), (90, 48, 40))):
+        b, colors = raster_scene(rng, n, w, h, (0.1, 0.85), (2.0, 7.0))
+        tiles = binning.bin_sequential(b)
+        bufs, con = render(b, tiles, colors, np.zeros(3), scoring=True)
+        gt = f32(rng.uniform(0, 1, (h, w, 3)))
+        rep, _ = losses.photometric(bufs.color, gt, 0.2)
+        m = density.error_mask(bufs.color, gt, 0.5)
+        out.update(batch_arrays(b, f"v{v}_"))
+        out[f"v{v}_colors"] = colors
+        out[f"v{v}_gt"] = gt
+        out[f"v{v}_color"] = bufs.color
+        out[f"v{v}_pix"] = con.pixel_idx
+        out[f"v{v}_rows"] = con.splat_rows
+        out[f"v{v}_mask"] = m.mask
+        out[f"v{v}_e"] = m.e
+        out[f"v{v}_ephoto"] = np.array(rep.photometric)
+        masks.append(m)
+        pix.append(con.pixel_idx)
+        ids.append(b.source_ids[con.splat_rows])
+        e_ph.append(rep.photometric)
+    out["s_plus"] = density.score_densify(masks, pix, ids, 90)
+    out["s_minus"] = density.score_prune(masks, pix, ids, e_ph, 90)
+    # decisions on a small 3D set with chosen scores (all four actions + floor guard)
+    params, _, _ = make_scene(200, 64, 48, seed=9)
+    gset = GaussianSet(**params)
+    sp = f32(rng.uniform(0, 30, 200))
+    sm = f32(rng.uniform(0, 1, 200))
+    for name, min_splats in (("dec", 16), ("floor", 190)):
+        new, dec = density.apply_decisions(gset, sp, sm, 16.0, 0.9, 0.01,
+                                           np.random.default_rng(5), min_splats=min_splats)
+        for k in ("positions", "log_scales", "rotations", "opacity_logits", "colors"):
+            out[f"{name}_new_{k}"] = getattr(new, k)
+        out[f"{name}_actions"] = np.array(
+            [["keep", "clone", "split", "prune"].index(d.action) for d in dec])
+        if name == "dec":
+            opt = Adam()
+            p = {k: getattr(gset, k).copy() for k in ("positions", "log_scales", "rotations",
+                                                         "opacity_logits", "colors")}
+            g = {k: f32(rng.normal(0, 1, v.shape)) for k, v in p.items()}
+            opt.step(p, g)
+            out["adam_m_before"] = opt.moments("positions")[0].copy()
+            opt.resize(dec)
+            out["adam_m_after"] = opt.moments("positions")[0].copy()
+            out["adam_v_after"] = opt.moments("log_scales")[1].copy()
+            out["adam_g_pos"] = g["positions"]
+            out["adam_g_ls"] = g["log_scales"]
+    out.update({f"set_{k}": v for k, v in params.items()})
+    out["dec_sp"], out["dec_sm"] = sp, sm
+    np.savez_compressed(OUT / "density.npz", **out)
+
+
+def golden_ply():
+    """A reference-written PLY (SH degree 1) for the drop-in file-format test."""
+    from tilesplat.ingest import write_ply
+    params, _, _ = make_scene(37, 64, 48, seed=4, sh_degree=1)
+    write_ply(GaussianSet(**params), OUT / "ref_sh1.ply")
+    np.savez_compressed(OUT / "ply.npz", **params)
+
+
 if __name__ == "__main__":
+    golden_density()
+    golden_ply()
     golden_binning()
     golden_raster()
     golden_scene()
