@@ -3,6 +3,7 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c1]
     python bench.py --impl reference ...        # CPU reference arm
+    python bench.py --config c5 [--budget S]    # the 1-minute training loop
 
 A step is one training step over one camera view per GPU: K1 preprocess ->
 K2 keys/sort/ranges -> K3 render -> photometric loss -> K4 per-Gaussian
@@ -49,7 +50,9 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c5"])
+    ap.add_argument("--budget", type=float, default=60.0, help="c5 wall-clock budget (s)")
+    ap.add_argument("--c5-views", type=int, default=200)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -474,9 +477,65 @@ def gpu_arm(args):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------------------- C5 ---
+def c5_arm(args):
+    """BASELINE.json configs[4]: the 1-minute loop on a synthetic 200-view
+    1080p scene with multi-view-consistency splitting/pruning (SURVEY.md
+    §8(d) C5).  GT = the canonical 1M-splat scene rendered by the B200
+    renderer into a camera ring (with exact depth priors, round2); the init
+    keeps a random half of the GT splats, perturbed as in the reference's
+    ablation setup (test_acceptance.py:427-440); densify on; the loop runs
+    `train()` until the wall-clock budget.  Reports training iterations/s
+    (densify rounds, PSNR evals and the budget checks included) and the
+    held-out PSNR before and after."""
+    import torch
+    import paper_2601_19489_b200 as ts
+    from paper_2601_19489_b200.synthetic import make_scene, synthetic_scene
+    torch.cuda.set_device(_env_int("LOCAL_RANK", 0))
+    t0 = time.perf_counter()
+    params, cam, _ = make_scene(1_000_000, 1920, 1080, seed=0)
+    gt_set = ts.GaussianSet(**params)
+    scene, _ = synthetic_scene(n_views=args.c5_views, width=1920, height=1080, fx=cam["fx"],
+                               gt_set=gt_set)
+    rng = np.random.default_rng(22)
+    n = len(gt_set)
+    keep = np.sort(rng.choice(n, size=n // 2, replace=False))
+    init = {k: v[keep].copy() for k, v in params.items()}
+    m = len(keep)
+    init["positions"] = init["positions"] * (1.0 + rng.normal(0, 0.02, (m, 1))) + \
+        rng.normal(0, 0.005, (m, 3))
+    init["log_scales"] += rng.normal(0, 0.15, (m, 3)) + 0.15
+    init["colors"] += rng.normal(0, 0.05, init["colors"].shape)
+    init = ts.GaussianSet(**init)
+    holdout = tuple(range(0, args.c5_views, max(args.c5_views // 4, 1)))
+    cfg = ts.TrainConfig(round_profile="round2", max_iters=200_000,
+                         budget_seconds=args.budget, eval_interval=10**9, seed=0,
+                         densify_start=500, densify_interval=300, densify_end=10**9,
+                         holdout_views=holdout)
+    eval_cams = [scene.cameras[i] for i in holdout]
+    psnr0 = ts.evaluate(init, eval_cams, cfg)
+    setup_s = time.perf_counter() - t0
+    res = ts.train(scene, cfg, initial=init)
+    psnr1 = ts.evaluate(res.gset, eval_cams, cfg)
+    line = {"metric": "C5 training iterations/s (1-minute loop, densify on)",
+            "value": res.iterations / res.elapsed, "unit": "iterations/s", "n_gpus": 1,
+            "higher_is_better": True, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"c5: 1M-splat GT rendered into {args.c5_views} 1920x1080 "
+                                   f"ring views (+depth priors); init = 500k perturbed; round2; "
+                                   f"densify every 300 its (K=10); budget {args.budget:g} s",
+                       "holdout_views": list(holdout)},
+            "iterations": res.iterations, "elapsed_s": res.elapsed,
+            "stop_reason": res.stop_reason, "splats_final": len(res.gset),
+            "psnr_holdout_before": psnr0, "psnr_holdout_after": psnr1,
+            "setup_s": setup_s}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.config == "c5":
+        c5_arm(args)
+    elif args.impl == "reference":
         reference_arm(args)
     else:
         gpu_arm(args)

@@ -91,10 +91,11 @@ def synthetic_scene(n_splats: int = 10, n_views: int = 5, width: int = 48, heigh
     for cam in cams:
         vr = render_view(gt_set, cam, cfg, checkpoints=False)
         b = vr.buffers
-        cam.gt_image = torch.clamp(b.color, 0.0, 1.0).cpu().numpy().astype(np.float64)
+        # ground truth stays resident on the device (FP32), like every image
+        cam.gt_image = torch.clamp(b.color, 0.0, 1.0).clone()
         if with_depth:
-            cam.depth_prior = b.normalized_depth().cpu().numpy().astype(np.float64)
-            cam.depth_valid = ((b.n_contrib > 0).cpu().numpy()) & (cam.depth_prior > 0)
+            cam.depth_prior = b.normalized_depth().clone()
+            cam.depth_valid = (b.n_contrib > 0) & (cam.depth_prior > 0)
     h = gt_set.to_numpy()
     scene = Scene(cameras=cams, points=h["positions"].copy(),
                   colors=(np.clip(h["colors"][:, 0, :], 0, 1) * 255).astype(np.uint8),

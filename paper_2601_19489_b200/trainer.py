@@ -512,7 +512,8 @@ def train(scene, cfg: TrainConfig, *, ply_path=None, metrics_path=None, decision
               for c in scene.cameras]
     prior_dev = [as_device_f32(c.depth_prior) if c.depth_prior is not None else None
                  for c in scene.cameras]
-    valid_dev = [torch.as_tensor(np.asarray(c.depth_valid), device=_device()).bool()
+    valid_dev = [(c.depth_valid.to(_device()).bool() if isinstance(c.depth_valid, torch.Tensor)
+                  else torch.as_tensor(np.asarray(c.depth_valid), device=_device()).bool())
                  if c.depth_valid is not None else None for c in scene.cameras]
     stepper = None if cfg.pose_opt else TrainStep(gset, cfg, extent=scene.extent, optimizer=opt)
     pose_t = {k: torch.zeros((1, 3), dtype=torch.float32, device=_device())
