@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
                    r2 = __ldg(rec + 3 * row0 + 2);
       mxn.x = -r0.x; myn.x = -r0.y;
       ca.x = __fmul_rn(r0.z, kQScale);
-      cb.x = __fmul_rn(r0.w, kQScale);
+      cb.x = __fmul_rn(r0.w, 2.0f * kQScale);
       cc.x = __fmul_rn(r1.x, kQScale);
       op.x = r1.y; dep.x = r1.z;
       cr.x = r2.x; cg.x = r2.y; cbl.x = r2.z;
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
                    r2 = __ldg(rec + 3 * row1 + 2);
       mxn.y = -r0.x; myn.y = -r0.y;
       ca.y = __fmul_rn(r0.z, kQScale);
-      cb.y = __fmul_rn(r0.w, kQScale);
+      cb.y = __fmul_rn(r0.w, 2.0f * kQScale);
       cc.y = __fmul_rn(r1.x, kQScale);
       op.y = r1.y; dep.y = r1.z;
       cr.y = r2.x; cg.y = r2.y; cbl.y = r2.z;
@@ -223,9 +223,8 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
         // alpha of both splats at this pixel (eval_alpha, packed)
         const float2 dx = __fadd2_rn(bc(pa.x), mxn);
         const float2 dy = __fadd2_rn(bc(pa.y), myn);
-        const float2 u = __ffma2_rn(ca, dx, __fmul2_rn(cb, dy));
-        const float2 v = __ffma2_rn(cb, dx, __fmul2_rn(cc, dy));
-        const float2 qs = __ffma2_rn(dx, u, __fmul2_rn(dy, v));
+        const float2 dxx = __fmul2_rn(dx, dx), dxy = __fmul2_rn(dx, dy), dyy = __fmul2_rn(dy, dy);
+        const float2 qs = __ffma2_rn(ca, dxx, __ffma2_rn(cb, dxy, __fmul2_rn(cc, dyy)));
         const float2 gauss = f2(fast_exp2(qs.x), fast_exp2(qs.y));
         const float2 raw = __fmul2_rn(op, gauss);
         const float2 alpha = f2(fminf(kAlphaCap, raw.x), fminf(kAlphaCap, raw.y));
@@ -248,12 +247,11 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
         const float2 ld = f2(part0 && !(raw.x > alpha.x) ? dLda.x : 0.f,
                              part1 && !(raw.y > alpha.y) ? dLda.y : 0.f);
         const float2 gq = __fmul2_rn(ld, alpha);
-        const float2 gqdx = __fmul2_rn(gq, dx), gqdy = __fmul2_rn(gq, dy);
-        acc_a = __ffma2_rn(gqdx, dx, acc_a);
-        acc_b = __ffma2_rn(gqdx, dy, acc_b);
-        acc_c = __ffma2_rn(gqdy, dy, acc_c);
-        acc_mx = __ffma2_rn(gq, u, acc_mx);
-        acc_my = __ffma2_rn(gq, v, acc_my);
+        acc_a = __ffma2_rn(gq, dxx, acc_a);
+        acc_b = __ffma2_rn(gq, dxy, acc_b);
+        acc_c = __ffma2_rn(gq, dyy, acc_c);
+        acc_mx = __ffma2_rn(gq, dx, acc_mx);  // sum gq dx; times the conic at the merge
+        acc_my = __ffma2_rn(gq, dy, acc_my);
         acc_o = __ffma2_rn(ld, gauss, acc_o);
         const float2 w = f2(w0, w1);
         acc_r = __ffma2_rn(w, bc(pb.x), acc_r);
@@ -267,6 +265,14 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
       if (lane == 0) next = atomicAdd(&s_next, 1);
       G = __shfl_sync(0xffffffffu, next, 0);
       const float ms = 2.0f / kQScale;  // d/dmean of the prescaled quadratic, x(-1/2)
+      // sum gq u = a' sum gq dx + b' sum gq dy (b' = b2' / 2), likewise v
+      {
+        const float2 hb = __fmul2_rn(cb, bc(0.5f));
+        const float2 u = __ffma2_rn(ca, acc_mx, __fmul2_rn(hb, acc_my));
+        const float2 v = __ffma2_rn(hb, acc_mx, __fmul2_rn(cc, acc_my));
+        acc_mx = u;
+        acc_my = v;
+      }
       if (row0 >= 0 && ((acc_o.x != 0.f) | (acc_r.x != 0.f) | (acc_g.x != 0.f) |
                         (acc_bl.x != 0.f) | (acc_d.x != 0.f) | (acc_a.x != 0.f))) {
         float* dst = grad2d + (long long)row0 * TSR_GRAD2D_FLOATS;

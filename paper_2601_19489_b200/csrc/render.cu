@@ -85,9 +85,10 @@ __device__ __forceinline__ void blend_pair(const float4 g, const float4 c, const
                                            float pxf, float2 pyf, int pos, PixPair& s) {
   const float dx = __fsub_rn(pxf, g.x);
   const float2 dy = __fadd2_rn(pyf, bc2(-g.y));
-  const float2 u = __ffma2_rn(bc2(c.x), bc2(dx), __fmul2_rn(bc2(c.y), dy));
-  const float2 v = __ffma2_rn(bc2(c.y), bc2(dx), __fmul2_rn(bc2(c.z), dy));
-  const float2 qs = __ffma2_rn(bc2(dx), u, __fmul2_rn(dy, v));
+  const float dxx = __fmul_rn(dx, dx);
+  const float2 dxy = __fmul2_rn(bc2(dx), dy), dyy = __fmul2_rn(dy, dy);
+  const float2 qs = __ffma2_rn(bc2(c.x), bc2(dxx),
+                               __ffma2_rn(bc2(c.y), dxy, __fmul2_rn(bc2(c.z), dyy)));
   const float2 raw = __fmul2_rn(bc2(g.z), make_float2(fast_exp2(qs.x), fast_exp2(qs.y)));
   const float2 alpha = make_float2(fminf(kAlphaCap, raw.x), fminf(kAlphaCap, raw.y));
   const bool b0 = s.alive0 && (alpha.x >= kMinAlpha);
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
     int32_t* __restrict__ out_ncons, float* __restrict__ ckpt,
     const int64_t* __restrict__ ckpt_base, ScoreArgs sc) {
   __shared__ float4 s_geo[kBatch];  // mx, my, opacity, depth
-  __shared__ float4 s_con[kBatch];  // prescaled conic a', b', c'
+  __shared__ float4 s_con[kBatch];  // prescaled conic a', 2b', c'
   __shared__ float4 s_col[kBatch];  // r, g, b, depth
   __shared__ float4 s_raw[kBatch];  // a, b, c (unscaled), level t
   __shared__ int s_row[kScore ? kBatch : 1];
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
         const float4 r0 = __ldg(rec + 3 * row), r1 = __ldg(rec + 3 * row + 1),
                      r2 = __ldg(rec + 3 * row + 2);
         s_geo[i] = make_float4(r0.x, r0.y, r1.y, r1.z);
-        s_con[i] = make_float4(__fmul_rn(r0.z, kQScale), __fmul_rn(r0.w, kQScale),
+        s_con[i] = make_float4(__fmul_rn(r0.z, kQScale), __fmul_rn(r0.w, 2.0f * kQScale),
                                __fmul_rn(r1.x, kQScale), 0.f);
         s_col[i] = make_float4(r2.x, r2.y, r2.z, r1.z);
         s_raw[i] = make_float4(r0.z, r0.w, r1.x, r1.w);

@@ -25,7 +25,7 @@ constexpr float kMinAlpha = 1.0f / 255.0f;         // forward.py:26
 constexpr float kTTerminate = 1e-4f;               // forward.py:27
 constexpr float kCovDilation = 0.3f;               // projection.py:26
 constexpr float kMinOpacity = 1.0f / 255.0f;       // projection.py:27
-// conic prescale: exp(-q/2) == exp2(q * kQScale)
+// conic prescale: exp(-q/2) == exp2(q * kQScale) (the cross term carries 2b)
 constexpr float kQScale = -0.72134752044448170368f;  // -0.5 * log2(e)
 
 // ------------------------------------------------------------------ FP64 --
@@ -173,10 +173,14 @@ __device__ __forceinline__ double min_q_box(const SplatF64& s, double rx0, doubl
 
 // ------------------------------------------------------------------ FP32 --
 // Alpha of one (pixel, splat) evaluation (splat_alpha, forward.py:71-84) on
-// the prescaled conic (a', b', c') = kQScale * (a, b, c):
-//   u = a'dx + b'dy, v = b'dx + c'dy, q' = dx u + dy v = kQScale * q
+// the prescaled conic (a', b2', c') = kQScale * (a, 2b, c) (b2' = 2 b' is
+// exact):
+//   dxx = dx dx, dxy = dx dy, dyy = dy dy,
+//   q' = a' dxx + (b2' dxy + c' dyy) = kQScale * q,
 //   gauss = 2^q' = exp(-q/2), raw = o * gauss, alpha = min(0.99, raw).
-// Every op is an explicit intrinsic so forward and backward agree bitwise.
+// K3 and K4 run exactly this sequence (packed FP32x2 instructions round each
+// half like the scalar ones), so their alphas agree bit for bit; K4 reuses
+// dxx, dxy, dyy for the conic gradient.
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -184,17 +188,17 @@ __device__ __forceinline__ float fast_exp2(float x) {
 }
 
 struct AlphaEval {
-  float dx, dy, u, v, gauss, raw, alpha;
+  float dx, dy, gauss, raw, alpha;
 };
 
 __device__ __forceinline__ AlphaEval eval_alpha(float px, float py, float mx, float my,
-                                                float a, float b, float c, float o) {
+                                                float a, float b2, float c, float o) {
   AlphaEval e;
   e.dx = __fsub_rn(px, mx);
   e.dy = __fsub_rn(py, my);
-  e.u = __fmaf_rn(a, e.dx, __fmul_rn(b, e.dy));
-  e.v = __fmaf_rn(b, e.dx, __fmul_rn(c, e.dy));
-  float qs = __fmaf_rn(e.dx, e.u, __fmul_rn(e.dy, e.v));
+  const float qs = __fmaf_rn(a, __fmul_rn(e.dx, e.dx),
+                             __fmaf_rn(b2, __fmul_rn(e.dx, e.dy),
+                                       __fmul_rn(c, __fmul_rn(e.dy, e.dy))));
   e.gauss = fast_exp2(qs);
   e.raw = __fmul_rn(o, e.gauss);
   e.alpha = fminf(kAlphaCap, e.raw);
