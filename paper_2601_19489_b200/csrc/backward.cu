@@ -199,19 +199,8 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
       const unsigned short* my_list = list + kListPad - lane;
       const int steps = n_act + 31;
       const float2 one = bc(1.f);
-      // software pipeline: the next step's pixel record is loaded while this
-      // step computes
-      float4 pa_n, pb_n;
-      pa_n = *reinterpret_cast<const float4*>(pa_base + my_list[0]);
-      pb_n = *reinterpret_cast<const float4*>(pb_base + my_list[0]);
-      for (int t = 0; t < steps; ++t) {
-        const float4 pa = pa_n;
-        const float4 pb = pb_n;
-        {
-          const unsigned off = my_list[t + 1];
-          pa_n = *reinterpret_cast<const float4*>(pa_base + off);
-          pb_n = *reinterpret_cast<const float4*>(pb_base + off);
-        }
+      // one systolic step of this lane's splat pair on pixel record (pa, pb)
+      auto step = [&](const float4& pa, const float4& pb, int t) {
         float T_in = __shfl_up_sync(0xffffffffu, T_out, 1);
         float R_in = __shfl_up_sync(0xffffffffu, R_out, 1);
         if (lane == 0) {
@@ -228,8 +217,9 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
         const float2 gauss = f2(fast_exp2(qs.x), fast_exp2(qs.y));
         const float2 raw = __fmul2_rn(op, gauss);
         const float2 alpha = f2(fminf(kAlphaCap, raw.x), fminf(kAlphaCap, raw.y));
-        const bool part0 = (p < nc) && (alpha.x >= kMinAlpha);
-        const bool part1 = (p + 1 < nc) && (alpha.y >= kMinAlpha);
+        const bool in0 = p < nc, in1 = p + 1 < nc;
+        const bool part0 = in0 && (alpha.x >= kMinAlpha);
+        const bool part1 = in1 && (alpha.y >= kMinAlpha);
         const float2 om = __fadd2_rn(one, f2(-alpha.x, -alpha.y));
         float2 gc = __ffma2_rn(bc(pb.x), cr, __ffma2_rn(bc(pb.y), cg, __fmul2_rn(bc(pb.z), cbl)));
         if (kDepth) gc = __ffma2_rn(bc(pa.z), dep, gc);
@@ -242,10 +232,12 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
         const float num1 = fmaf(-w1, gc.y, num0);
         R_out = num1;
         const float2 rcp = f2(fast_rcp(om.x), fast_rcp(om.y));
-        const float2 dLda = __ffma2_rn(f2(-num0, -num1), rcp, __fmul2_rn(f2(T_in, T1), gc));
-        // uncapped participants only (backward.py:64,72); x(-1/2) folded into the merge
-        const float2 ld = f2(part0 && !(raw.x > alpha.x) ? dLda.x : 0.f,
-                             part1 && !(raw.y > alpha.y) ? dLda.y : 0.f);
+        const float2 dLda = f2(fmaf(-num0, rcp.x, T_in * gc.x), fmaf(-num1, rcp.y, T1 * gc.y));
+        // uncapped participants only (backward.py:64,72): 1/255 <= raw <= 0.99
+        // (then alpha == raw); x(-1/2) folded into the merge
+        const bool l0 = in0 && raw.x >= kMinAlpha && raw.x <= kAlphaCap;
+        const bool l1 = in1 && raw.y >= kMinAlpha && raw.y <= kAlphaCap;
+        const float2 ld = f2(l0 ? dLda.x : 0.f, l1 ? dLda.y : 0.f);
         const float2 gq = __fmul2_rn(ld, alpha);
         acc_a = __ffma2_rn(gq, dxx, acc_a);
         acc_b = __ffma2_rn(gq, dxy, acc_b);
@@ -258,6 +250,27 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
         acc_g = __ffma2_rn(w, bc(pb.y), acc_g);
         acc_bl = __ffma2_rn(w, bc(pb.z), acc_bl);
         if (kDepth) acc_d = __ffma2_rn(w, bc(pa.z), acc_d);
+      };
+      // software pipeline, unrolled by two with ping-pong registers: the
+      // next step's pixel record is loaded while this step computes (the
+      // padded list makes the loads past the end read sentinels)
+      float4 pa0 = *reinterpret_cast<const float4*>(pa_base + my_list[0]);
+      float4 pb0 = *reinterpret_cast<const float4*>(pb_base + my_list[0]);
+      float4 pa1, pb1;
+      for (int t = 0; t < steps; t += 2) {
+        {
+          const unsigned off = my_list[t + 1];
+          pa1 = *reinterpret_cast<const float4*>(pa_base + off);
+          pb1 = *reinterpret_cast<const float4*>(pb_base + off);
+        }
+        step(pa0, pb0, t);
+        if (t + 1 >= steps) break;
+        {
+          const unsigned off = my_list[t + 2];
+          pa0 = *reinterpret_cast<const float4*>(pa_base + off);
+          pb0 = *reinterpret_cast<const float4*>(pb_base + off);
+        }
+        step(pa1, pb1, t + 1);
       }
       __syncwarp();
       // next supergroup: dynamic, so the warps of a tile finish together
