@@ -22,14 +22,14 @@
 //      so the tiles' record ranges never overlap and the total is <= P / 32).
 //
 // B200 shape: the whole index build is ONE persistent cooperative kernel (all
-// CTAs co-resident, 2 per SM) whose phases are separated by grid barriers.
+// CTAs co-resident, 3 per SM) whose phases are separated by grid barriers.
 // At C2 sizes (1M rows, 4.4M pairs) every phase is latency-bound, so the
 // multi-kernel form (3 launches per radix pass) or a decoupled look-back
 // over ~1000 CTAs costs far more than the bytes.  A radix pass here is:
 //   count   each CTA histograms its contiguous slice (warp-aggregated smem
 //           atomics) -> cnt[cta][digit];                      grid barrier
 //   scan    CTA d scans digit column d over the CTAs -> colscan; grid barrier
-//   scatter each CTA re-reads its slice (L2-resident) in 4096-item sub-tiles,
+//   scatter each CTA re-reads its slice (L2-resident) in 2048-item sub-tiles,
 //           ranks them stably with a ballot multi-split, stages them digit-sorted
 //           in shared memory and stores each digit run coalesced at
 //           digit_start + colscan + running offset;           grid barrier
@@ -43,8 +43,8 @@ namespace tsr {
 
 constexpr int kSB = 256;                 // threads per CTA
 constexpr int kBins = 256;               // 8-bit digits
-constexpr int kItems = 16;               // items per thread per sub-tile
-constexpr int kSub = kSB * kItems;       // 4096-item sub-tiles
+constexpr int kItems = 8;                // items per thread per sub-tile
+constexpr int kSub = kSB * kItems;       // 2048-item sub-tiles
 constexpr int kEmitPer = 2;              // ranks per thread per emission block
 constexpr int kEmitRanks = kSB * kEmitPer;
 constexpr int kStage = 4096;             // staged pairs per emission window
@@ -483,7 +483,7 @@ __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, lon
 }
 
 // ---- the persistent index kernel
-__global__ void __launch_bounds__(kSB, 2) build_index_kernel(IndexArgs a) {
+__global__ void __launch_bounds__(kSB, 3) build_index_kernel(IndexArgs a) {
   __shared__ SortSmem sm;
   extern __shared__ __align__(16) unsigned char dyn[];
   const int G = gridDim.x, bid = blockIdx.x, tid = threadIdx.x;
@@ -742,7 +742,7 @@ extern "C" int tsr_build_index(const float* rec, const uint32_t* depth_bits, con
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, build_index_kernel, kSB,
                                                     kDynSmem) != cudaSuccess)
     return TSR_E_CUDA;
-  int grid = sms * (per_sm < 2 ? per_sm : 2);
+  int grid = sms * (per_sm < 3 ? per_sm : 3);
   if (grid > kMaxGrid) grid = kMaxGrid;
   if (grid < 1) return TSR_E_CUDA;
   if (cudaMemsetAsync(w + pl.ctl_off, 0, pl.ctl_bytes, s) != cudaSuccess) return TSR_E_CUDA;
