@@ -1,7 +1,7 @@
 // Fused photometric loss: E = (1 - lam) mean|r - g| + lam (1 - SSIM) and
 // dE/dr (losses.py:44-91) -- SURVEY.md §8(f) next #1.
 //
-// Two tile kernels over 32x32 output tiles (separable 11-tap Gaussian,
+// Two tile kernels over 32x32 output tiles, one CTA per (tile, channel) (separable 11-tap Gaussian,
 // sigma 1.5, zero padding, window passed as a kernel parameter):
 //   ssim_fwd: per channel, stage r, g (tile + 5-pixel halo) in shared memory,
 //             filter the 5 moments (mu1, mu2, E[r^2], E[g^2], E[rg]), form the
@@ -62,10 +62,13 @@ __global__ void __launch_bounds__(256, 4) ssim_fwd_kernel(const float* __restric
   __shared__ float s_h[5][kLIn][kLT + 1];
   __shared__ double s_red[2][8];
   const int tid = threadIdx.x;
-  const int tx0 = blockIdx.x * kLT, ty0 = blockIdx.y * kLT;
+  // one CTA per (tile, channel); the 3 channel CTAs of a tile are adjacent
+  // in launch order, so the interleaved image sectors are shared in L2
+  const int c = blockIdx.x % 3;
+  const int tx0 = (blockIdx.x / 3) * kLT, ty0 = blockIdx.y * kLT;
   const long long HW = (long long)H * W;
   double acc_ssim = 0.0, acc_l1 = 0.0;
-  for (int c = 0; c < 3; ++c) {
+  {
     load_halo(r, c, H, W, ty0, tx0, s_r);
     load_halo(g, c, H, W, ty0, tx0, s_g);
     __syncthreads();
@@ -180,9 +183,10 @@ __global__ void __launch_bounds__(256, 4) ssim_bwd_kernel(const float* __restric
   __shared__ __align__(16) float s_q[3][kLIn * kLS];
   __shared__ float s_h[3][kLIn][kLT + 1];
   const int tid = threadIdx.x;
-  const int tx0 = blockIdx.x * kLT, ty0 = blockIdx.y * kLT;
+  const int c = blockIdx.x % 3;
+  const int tx0 = (blockIdx.x / 3) * kLT, ty0 = blockIdx.y * kLT;
   const long long HW = (long long)H * W;
-  for (int c = 0; c < 3; ++c) {
+  {
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
       float v[kHaloIters];
@@ -315,7 +319,7 @@ static size_t q_bytes(int32_t height, int32_t width) {
 
 extern "C" size_t tsr_photometric_workspace(int32_t height, int32_t width) {
   const size_t tiles = (size_t)((width + kLT - 1) / kLT) * ((height + kLT - 1) / kLT);
-  return q_bytes(height, width) + tiles * 2 * sizeof(double) + 256;
+  return q_bytes(height, width) + 3 * tiles * 2 * sizeof(double) + 256;
 }
 
 extern "C" int tsr_photometric(const float* rendered, const float* gt, int32_t height,
@@ -326,7 +330,7 @@ extern "C" int tsr_photometric(const float* rendered, const float* gt, int32_t h
   if (workspace_bytes < tsr_photometric_workspace(height, width)) return TSR_E_WORKSPACE;
   const Win win = make_window();
   cudaStream_t s = (cudaStream_t)stream;
-  dim3 grid((width + kLT - 1) / kLT, (height + kLT - 1) / kLT);
+  dim3 grid(3 * ((width + kLT - 1) / kLT), (height + kLT - 1) / kLT);
   const int n_blocks = grid.x * grid.y;
   float* Q = (float*)workspace;
   double* partials = (double*)((char*)workspace + q_bytes(height, width));
