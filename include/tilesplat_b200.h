@@ -78,7 +78,8 @@ typedef struct {
  * row_of_source (-1 if culled), counts[M] (pairs per row), depth_bits[M]
  * (f32 depth bits, binning.py:137-139), spans[M] (16-byte compact column
  * walk, see sort.cu), totals[0] = M, totals[1] = P (device).
- * strategy: 0 = bin_sequential column walk, 1 = bin_load_balanced min-q test
+ * strategy: 0 = bin_sequential column walk, 1 = bin_load_balanced min-q test,
+ *           2 = bin_aabb radius rectangle (binning.py:301-325, the bench-tiling baseline)
  * (both yield the same pair multiset). */
 size_t tsr_preprocess_workspace(int64_t n);
 int tsr_preprocess_fwd(const tsr_gaussians_t* g, const tsr_camera_t* cam, int32_t strategy,

@@ -180,6 +180,12 @@ def bin_load_balanced(batch: SplatBatch, group_size: int = 32) -> TileIndex:
     return build_index(batch, 1)
 
 
+def bin_aabb(batch: SplatBatch) -> TileIndex:
+    """Radius-rectangle baseline (binning.py:301-325): every tile of the square
+    of half-side sqrt(t / lambda_min) around the mean, no intersection test."""
+    return build_index(batch, 2)
+
+
 def lane_test_counts(batch: SplatBatch, splat_row: int, group_size: int = 32):
     """Candidates tested per lane for one splat (binning.py:289-298)."""
     if batch.tile_rect is None:

@@ -93,6 +93,24 @@ __device__ __forceinline__ long long count_pairs_of(const float* rp, int strateg
     span.y = 1u << 31;
     return count_load_balanced(s, tiles_x, tiles_y);
   }
+  if (strategy == 2) {  // bin_aabb: the whole rectangle, one span code per column
+    long long tx0, tx1, ty0, ty1;
+    aabb_rect(s, tiles_x, tiles_y, tx0, tx1, ty0, ty1);
+    if (tx0 > tx1 || ty0 > ty1) return 0;
+    const long long ncols = tx1 - tx0 + 1, nrows = ty1 - ty0 + 1;
+    span.x = (uint32_t)(tx0 & 0xffff) | ((uint32_t)(ncols < 255 ? ncols : 255) << 16);
+    span.y = (uint32_t)(ty0 & 0xffff);
+    if (ncols <= 8 && nrows <= 15) {
+      for (long long c = 0; c < ncols; ++c) {
+        const uint32_t code = (uint32_t)nrows << 4;
+        if (c < 4) span.z |= code << (8 * c);
+        else span.w |= code << (8 * (c - 4));
+      }
+    } else {
+      span.y |= 1u << 31;
+    }
+    return ncols * nrows;
+  }
   SnugRect r = snugbox(s, tiles_x, tiles_y);
   if (r.tx0 > r.tx1 || r.ty0 > r.ty1) return 0;
   const long long ncols = r.tx1 - r.tx0 + 1;

@@ -450,6 +450,17 @@ __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, lon
       const unsigned long long depk = dep[k];
       long long out = O + off[k];
       SplatF64 s = load_splat_f64(a.rec + (long long)row[k] * 12);
+      if (strategy == 2) {  // bin_aabb rectangle, column-major
+        long long tx0, tx1, ty0, ty1;
+        aabb_rect(s, tiles_x, tiles_y, tx0, tx1, ty0, ty1);
+        for (long long tx = tx0; tx <= tx1; ++tx)
+          for (long long ty = ty0; ty <= ty1; ++ty, ++out)
+            if (out < p_cap) {
+              pairs[out] = ((unsigned long long)(ty * tiles_x + tx) << 32) | depk;
+              pair_rows[out] = row[k];
+            }
+        continue;
+      }
       SnugRect box = snugbox(s, tiles_x, tiles_y);
       if (box.tx0 > box.tx1 || box.ty0 > box.ty1) continue;
       for (long long tx = box.tx0; tx <= box.tx1; ++tx) {
@@ -566,7 +577,7 @@ __global__ void __launch_bounds__(kSB, 3) build_index_kernel(IndexArgs a) {
       for (int j = 0; j < 4; ++j) {
         const long long r = r0 + j * kSB;
         if (r >= rhi) continue;
-        if (a.strategy != 0) sp[j].y |= 1u << 31;
+        if (a.strategy == 1) sp[j].y |= 1u << 31;
         uint32_t c;
         if (sp[j].y >> 31) {
           c = (uint32_t)a.counts[row[j]];

@@ -131,6 +131,20 @@ __device__ __forceinline__ int column_rows(const SplatF64& s, const SnugRect& r,
   return n > 0 ? (int)n : 0;
 }
 
+// bin_aabb's rectangle (binning.py:301-325): the square of half-side
+// sqrt(t / lambda_min(conic)) around the mean, in the reference's NumPy
+// operation order; every tile of the rectangle is emitted (column-major).
+__device__ __forceinline__ void aabb_rect(const SplatF64& s, int tiles_x, int tiles_y,
+                                          long long& tx0, long long& tx1, long long& ty0,
+                                          long long& ty1) {
+  const double half_sum = dmul(dadd(s.a, s.c), 0.5);   // (a + c) / 2.0 (exact halving)
+  const double half_diff = dmul(dsub(s.a, s.c), 0.5);  // (a - c) / 2.0
+  const double lam_min = dsub(half_sum, dsqrt(dadd(dmul(half_diff, half_diff), dmul(s.b, s.b))));
+  const double radius = dsqrt(ddiv(s.t, lam_min));
+  tile_span(dsub(s.mx, radius), dadd(s.mx, radius), tiles_x, tx0, tx1);
+  tile_span(dsub(s.my, radius), dadd(s.my, radius), tiles_y, ty0, ty1);
+}
+
 // Total pairs of one splat under bin_sequential.
 __device__ __forceinline__ long long count_sequential(const SplatF64& s, int tiles_x,
                                                       int tiles_y) {

@@ -129,3 +129,26 @@ def make_scene(n, width, height, seed=0, clustered=False, sh_degree=0):
                   opacity_logits=f32(logits), colors=f32(colors))
     cam = look_at((0.0, 0.0, -4.0), (0.0, 0.0, 0.0), fx, width, height)
     return params, cam, f32(gt)
+
+
+def random_splat_batch(n_splats: int, anisotropy: float = 1.0, seed: int = 0, width: int = 640,
+                       height: int = 480, sigma_range=(0.8, 4.0)):
+    """Random PD conics at a given anisotropy (synthetic.py:16-43), drawn on
+    the host in float64 exactly as the reference draws them, then stored as
+    the device batch (FP32)."""
+    from .projection import SplatBatch
+    rng = np.random.default_rng(seed)
+    means = np.stack([rng.uniform(0, width, n_splats), rng.uniform(0, height, n_splats)], axis=1)
+    minor = rng.uniform(*sigma_range, n_splats)
+    major = minor * anisotropy
+    theta = rng.uniform(0.0, np.pi, n_splats)
+    ct, st = np.cos(theta), np.sin(theta)
+    inv1, inv2 = 1.0 / major ** 2, 1.0 / minor ** 2
+    a = ct * ct * inv1 + st * st * inv2
+    c = st * st * inv1 + ct * ct * inv2
+    b = ct * st * (inv1 - inv2)
+    opacities = rng.uniform(0.05, 0.98, n_splats)
+    return SplatBatch(means, np.stack([a, b, c], axis=1),
+                      np.maximum(0.0, 2.0 * np.log(255.0 * opacities)),
+                      rng.uniform(0.1, 20.0, n_splats), opacities,
+                      np.arange(n_splats, dtype=np.int64), width, height)

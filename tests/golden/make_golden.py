@@ -309,7 +309,31 @@ def golden_ply():
     np.savez_compressed(OUT / "ply.npz", **params)
 
 
+def golden_benchtiling():
+    """The reference's bench-tiling harness (cli.py:170-183): pairs and
+    checksums per strategy for a few (n, anisotropy, seed)."""
+    from tilesplat.cli import run_bench_tiling
+    out = {}
+    for i, (n, an, seed, w, h) in enumerate(((20000, 8.0, 0, 640, 480), (5000, 1.0, 3, 640, 480),
+                                             (30000, 15.0, 7, 1280, 720))):
+        res = run_bench_tiling(n, an, seed, w, h)
+        out[f"c{i}_args"] = np.array([n, an, seed, w, h], dtype=np.float64)
+        for r in res:
+            out[f"c{i}_{r.strategy}_pairs"] = np.array(r.pairs)
+            out[f"c{i}_{r.strategy}_checksum"] = np.array(r.checksum)
+        # the same harness on the FP32-rounded batch (what the device stores)
+        b = f32_batch(synthetic.random_splat_batch(n, an, seed, width=w, height=h))
+        binning.compute_snugboxes(b)
+        for name, fn in (("aabb", binning.bin_aabb), ("snug_seq", binning.bin_sequential),
+                         ("snug_lb", binning.bin_load_balanced)):
+            idx = fn(b)
+            out[f"c{i}_f32_{name}_pairs"] = np.array(idx.n_pairs)
+            out[f"c{i}_f32_{name}_checksum"] = np.array(idx.checksum())
+    np.savez_compressed(OUT / "benchtiling.npz", **out)
+
+
 if __name__ == "__main__":
+    golden_benchtiling()
     golden_density()
     golden_ply()
     golden_binning()

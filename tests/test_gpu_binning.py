@@ -162,3 +162,23 @@ def test_pair_capacity_overflow_is_flagged():
     assert int(ok.overflow.item()) == 0
     assert_index_equal(ts.TileIndex(ok.keys[:p], ok.values[:p], ok.offsets, 40, 30),
                        O.bin_sequential(b))
+
+
+@pytest.mark.parametrize("case", [0, 1, 2])
+def test_bench_tiling_harness_matches_reference(case):
+    """The reference's bench-tiling (cli.py:170-202): the same three
+    strategies on the same random batch.  On the FP32-rounded batch (what the
+    device stores) pairs and checksums are identical to the reference run on
+    that batch; against the reference's float64 batch the pair counts agree
+    to within FP32 input rounding."""
+    from paper_2601_19489_b200.benchtiling import bench_tiling_csv, run_bench_tiling
+    g = golden("benchtiling")
+    n, an, seed, w, h = g[f"c{case}_args"]
+    res = run_bench_tiling(int(n), float(an), int(seed), int(w), int(h), repeats=1)
+    for r in res:
+        assert r.pairs == int(g[f"c{case}_f32_{r.strategy}_pairs"]), r.strategy
+        assert r.checksum == str(g[f"c{case}_f32_{r.strategy}_checksum"]), r.strategy
+        ref = int(g[f"c{case}_{r.strategy}_pairs"])
+        assert abs(r.pairs - ref) <= max(2, 1e-5 * ref)
+        assert r.millis > 0
+    assert bench_tiling_csv(res).startswith("strategy,splats,pairs,millis\naabb,")
