@@ -264,9 +264,10 @@ __device__ __forceinline__ bool project_one(const tsr_gaussians_t& g, const tsr_
   return true;
 }
 
-// (a) cull + compaction: row_of_source, source_ids and M.  8 consecutive
-// Gaussians per thread keep the look-back chain short (N / 2048 blocks).
-constexpr int kCullItems = 8;
+// (a) cull + compaction: row_of_source, source_ids and M.  4 consecutive
+// Gaussians per thread (N / 1024 blocks: more CTAs in flight beat a shorter
+// look-back chain here, measured).
+constexpr int kCullItems = 4;
 __global__ void __launch_bounds__(kScanBlock) cull_compact_kernel(
     tsr_gaussians_t g, tsr_camera_t cam, int32_t* __restrict__ source_ids,
     int32_t* __restrict__ row_of_source, int64_t* __restrict__ totals,
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(kScanBlock) cull_compact_kernel(
 }
 
 // (b) projection + colour + exact pair count into the compacted rows.
-__global__ void __launch_bounds__(kScanBlock) preprocess_kernel(
+__global__ void __launch_bounds__(kScanBlock, 4) preprocess_kernel(
     tsr_gaussians_t g, tsr_camera_t cam, int strategy, float4* __restrict__ rec_out,
     const int32_t* __restrict__ row_of_source, int32_t* __restrict__ counts,
     uint32_t* __restrict__ depth_bits, uint4* __restrict__ spans,
