@@ -206,6 +206,18 @@ int tsr_preprocess_bwd_adam(const tsr_gaussians_t* g, const tsr_camera_t* cam,
                             float* pose_sums, unsigned long long* skipped,
                             void* stream);
 
+/* Same, with the per-step scalars read from DEVICE memory when group_scalars
+ * is not NULL: [lr, bias_correction1, bias_correction2] for each of the 5
+ * groups (the descriptors' own lr / bias corrections are then ignored).  A
+ * CUDA graph that captures this launch replays with the scalars the host
+ * writes each step (pinned-memory copy node), since kernel arguments are
+ * frozen at capture. */
+int tsr_preprocess_bwd_adam_dev(const tsr_gaussians_t* g, const tsr_camera_t* cam,
+                                const float* rec, const int32_t* row_of_source,
+                                const float* grad2d, const tsr_adam_group_t* groups_host,
+                                const float* group_scalars, float* pose_sums,
+                                unsigned long long* skipped, void* stream);
+
 /* --------------------------------------------------------------- loss ----
  * Fused photometric objective (losses.py:44-91): E = (1-lam) mean|r-g| +
  * lam (1 - SSIM), 11-tap sigma=1.5 Gaussian window, zero padding.  rendered,

@@ -291,7 +291,8 @@ struct AdamGroups {
 // element) and the step uses a fast divide: the update differs from the
 // reference's float64 m_hat / (sqrt(v_hat) + eps) by a few FP32 ulp.
 template <typename GradFn>
-__device__ __forceinline__ int adam_row(const tsr_adam_group_t& G, long long r, GradFn grad) {
+__device__ __forceinline__ int adam_row(const tsr_adam_group_t& G, long long r, GradFn grad,
+                                        const float* scal = nullptr, int gk = 0) {
   const int w = G.width;
   bool finite = true;
   for (int k = 0; k < w; ++k) finite &= isfinite(grad(k));
@@ -299,7 +300,9 @@ __device__ __forceinline__ int adam_row(const tsr_adam_group_t& G, long long r, 
   float* p = G.param + r * w;
   float* m = G.exp_avg + r * w;
   float* v = G.exp_avg_sq + r * w;
-  const float ibc1 = 1.0f / G.bias_correction1, ibc2 = 1.0f / G.bias_correction2;
+  const float lr = scal ? scal[3 * gk] : G.lr;
+  const float ibc1 = 1.0f / (scal ? scal[3 * gk + 1] : G.bias_correction1),
+              ibc2 = 1.0f / (scal ? scal[3 * gk + 2] : G.bias_correction2);
   float nrm = 0.f;
   for (int k = 0; k < w; ++k) {
     const float gk = grad(k);
@@ -307,7 +310,7 @@ __device__ __forceinline__ int adam_row(const tsr_adam_group_t& G, long long r, 
     const float vk = kBeta2 * v[k] + kOneMinusBeta2 * gk * gk;
     m[k] = mk;
     v[k] = vk;
-    const float pk = p[k] - __fdividef(G.lr * (mk * ibc1), sqrtf(vk * ibc2) + kEps);
+    const float pk = p[k] - __fdividef(lr * (mk * ibc1), sqrtf(vk * ibc2) + kEps);
     p[k] = pk;
     nrm += pk * pk;
   }
@@ -342,7 +345,8 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamGroups groups,
 __global__ void __launch_bounds__(256) preprocess_bwd_adam_kernel(
     tsr_gaussians_t G, tsr_camera_t cam, const float4* __restrict__ rec,
     const int32_t* __restrict__ row_of_source, const float* __restrict__ grad2d,
-    AdamGroups groups, float* __restrict__ pose_sums, unsigned long long* __restrict__ skipped) {
+    AdamGroups groups, float* __restrict__ pose_sums, unsigned long long* __restrict__ skipped,
+    const float* __restrict__ scal) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   Vjp v;
   bool vis = false;
@@ -352,13 +356,13 @@ __global__ void __launch_bounds__(256) preprocess_bwd_adam_kernel(
     const int C = G.sh_coeffs;
     float basis[16];
     if (vis && C > 1) sh_basis(sh_degree_of(C), v.dir[0], v.dir[1], v.dir[2], basis);
-    local += adam_row(groups.g[0], i, [&](int k) { return vis ? v.gp[k] : 0.f; });
-    local += adam_row(groups.g[1], i, [&](int k) { return vis ? v.gls[k] : 0.f; });
-    local += adam_row(groups.g[2], i, [&](int k) { return vis ? v.gq[k] : 0.f; });
-    local += adam_row(groups.g[3], i, [&](int k) { return vis ? v.go : 0.f; });
+    local += adam_row(groups.g[0], i, [&](int k) { return vis ? v.gp[k] : 0.f; }, scal, 0);
+    local += adam_row(groups.g[1], i, [&](int k) { return vis ? v.gls[k] : 0.f; }, scal, 1);
+    local += adam_row(groups.g[2], i, [&](int k) { return vis ? v.gq[k] : 0.f; }, scal, 2);
+    local += adam_row(groups.g[3], i, [&](int k) { return vis ? v.go : 0.f; }, scal, 3);
     local += adam_row(groups.g[4], i, [&](int k) {
       return vis ? color_grad(v, basis, C, k / 3, k % 3) : 0.f;
-    });
+    }, scal, 4);
   }
   if (pose_sums) {
     float pv[12];
@@ -372,20 +376,32 @@ __global__ void __launch_bounds__(256) preprocess_bwd_adam_kernel(
 
 // Adam update of one row held in registers (optim.py:74-88); returns 1 when
 // the row is skipped (non-finite gradient: moments and params untouched).
+// Per-step scalars of one group: from the descriptor (by value), or from a
+// device array [lr, bias_correction1, bias_correction2] x 5 that the host
+// rewrites every step (CUDA-graph replay, where kernel arguments are frozen).
+struct AdamScal {
+  float lr, ibc1, ibc2;
+};
+
+__device__ __forceinline__ AdamScal adam_scal(const tsr_adam_group_t& G, const float* dev, int k) {
+  if (dev) return {dev[3 * k], 1.0f / dev[3 * k + 1], 1.0f / dev[3 * k + 2]};
+  return {G.lr, 1.0f / G.bias_correction1, 1.0f / G.bias_correction2};
+}
+
 template <int W>
-__device__ __forceinline__ int adam_regs(const tsr_adam_group_t& G, const float* g, float* p,
-                                         float* m, float* v) {
+__device__ __forceinline__ int adam_regs(const tsr_adam_group_t& G, const AdamScal& S,
+                                         const float* g, float* p, float* m, float* v) {
   bool finite = true;
 #pragma unroll
   for (int k = 0; k < W; ++k) finite &= isfinite(g[k]);
   if (!finite) return 1;
-  const float ibc1 = 1.0f / G.bias_correction1, ibc2 = 1.0f / G.bias_correction2;
+  const float ibc1 = S.ibc1, ibc2 = S.ibc2;
   float nrm = 0.f;
 #pragma unroll
   for (int k = 0; k < W; ++k) {
     m[k] = kBeta1 * m[k] + kOneMinusBeta1 * g[k];
     v[k] = kBeta2 * v[k] + kOneMinusBeta2 * g[k] * g[k];
-    p[k] = p[k] - __fdividef(G.lr * (m[k] * ibc1), sqrtf(v[k] * ibc2) + kEps);
+    p[k] = p[k] - __fdividef(S.lr * (m[k] * ibc1), sqrtf(v[k] * ibc2) + kEps);
     nrm += p[k] * p[k];
   }
   if (G.renormalize) {
@@ -417,7 +433,8 @@ __device__ __forceinline__ void store_row(float* base, long long i, const float*
 __global__ void __launch_bounds__(256) vjp_adam_sh0_kernel(
     tsr_camera_t cam, long long n, const float4* __restrict__ rec,
     const int32_t* __restrict__ row_of_source, float* __restrict__ grad2d, AdamGroups groups,
-    float* __restrict__ pose_sums, unsigned long long* __restrict__ skipped) {
+    float* __restrict__ pose_sums, unsigned long long* __restrict__ skipped,
+    const float* __restrict__ scal) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   Vjp vj;
   bool vis = false;
@@ -434,6 +451,9 @@ __global__ void __launch_bounds__(256) vjp_adam_sh0_kernel(
     load_row<1>(G3.param, i, po); load_row<1>(G3.exp_avg, i, mo); load_row<1>(G3.exp_avg_sq, i, vo);
     load_row<3>(G4.param, i, pc); load_row<3>(G4.exp_avg, i, mc); load_row<3>(G4.exp_avg_sq, i, vc);
     const int row = row_of_source[i];
+    const AdamScal S0 = adam_scal(G0, scal, 0), S1 = adam_scal(G1, scal, 1),
+                   S2 = adam_scal(G2, scal, 2), S3 = adam_scal(G3, scal, 3),
+                   S4 = adam_scal(G4, scal, 4);
     float gp[3] = {0.f, 0.f, 0.f}, gl[3] = {0.f, 0.f, 0.f}, gq[4] = {0.f, 0.f, 0.f, 0.f};
     float go[1] = {0.f}, gc[3] = {0.f, 0.f, 0.f};
     if (row >= 0) {
@@ -455,11 +475,11 @@ __global__ void __launch_bounds__(256) vjp_adam_sh0_kernel(
       for (int k = 0; k < 4; ++k) gq[k] = vj.gq[k];
       go[0] = vj.go;
     }
-    local += adam_regs<3>(G0, gp, pp, mp, vp);
-    local += adam_regs<3>(G1, gl, pl, ml, vl);
-    local += adam_regs<4>(G2, gq, pq, mq, vq);
-    local += adam_regs<1>(G3, go, po, mo, vo);
-    local += adam_regs<3>(G4, gc, pc, mc, vc);
+    local += adam_regs<3>(G0, S0, gp, pp, mp, vp);
+    local += adam_regs<3>(G1, S1, gl, pl, ml, vl);
+    local += adam_regs<4>(G2, S2, gq, pq, mq, vq);
+    local += adam_regs<1>(G3, S3, go, po, mo, vo);
+    local += adam_regs<3>(G4, S4, gc, pc, mc, vc);
     store_row<3>(G0.param, i, pp); store_row<3>(G0.exp_avg, i, mp); store_row<3>(G0.exp_avg_sq, i, vp);
     store_row<3>(G1.param, i, pl); store_row<3>(G1.exp_avg, i, ml); store_row<3>(G1.exp_avg_sq, i, vl);
     store_row<4>(G2.param, i, pq); store_row<4>(G2.exp_avg, i, mq); store_row<4>(G2.exp_avg_sq, i, vq);
@@ -528,6 +548,16 @@ extern "C" int tsr_preprocess_bwd_adam(const tsr_gaussians_t* g, const tsr_camer
                                        const float* grad2d,
                                        const tsr_adam_group_t* groups_host, float* pose_sums,
                                        unsigned long long* skipped, void* stream) {
+  return tsr_preprocess_bwd_adam_dev(g, cam, rec, row_of_source, grad2d, groups_host, nullptr,
+                                     pose_sums, skipped, stream);
+}
+
+extern "C" int tsr_preprocess_bwd_adam_dev(const tsr_gaussians_t* g, const tsr_camera_t* cam,
+                                           const float* rec, const int32_t* row_of_source,
+                                           const float* grad2d,
+                                           const tsr_adam_group_t* groups_host,
+                                           const float* group_scalars, float* pose_sums,
+                                           unsigned long long* skipped, void* stream) {
   AdamGroups gs;
   if (!g || !cam || !fill_groups(groups_host, 5, gs) || !skipped) return TSR_E_INVALID;
   for (int k = 0; k < 5; ++k)
@@ -540,10 +570,12 @@ extern "C" int tsr_preprocess_bwd_adam(const tsr_gaussians_t* g, const tsr_camer
   if (g->sh_coeffs == 1) {
     // fast path; also zeroes the consumed Grad2D rows for the next step
     vjp_adam_sh0_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
-        *cam, g->n, (const float4*)rec, row_of_source, (float*)grad2d, gs, pose_sums, skipped);
+        *cam, g->n, (const float4*)rec, row_of_source, (float*)grad2d, gs, pose_sums, skipped,
+        group_scalars);
   } else {
     preprocess_bwd_adam_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
-        *g, *cam, (const float4*)rec, row_of_source, grad2d, gs, pose_sums, skipped);
+        *g, *cam, (const float4*)rec, row_of_source, grad2d, gs, pose_sums, skipped,
+        group_scalars);
   }
   TSR_CHECK_LAUNCH();
   return TSR_OK;

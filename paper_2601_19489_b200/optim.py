@@ -123,9 +123,15 @@ class Adam:
         self.skipped_rows += skipped
         return skipped
 
-    def groups_for_fused(self, params: dict, lr_overrides=None):
-        """Descriptors for the fused K4b+K5 kernel (grads come from registers)."""
+    def groups_for_fused(self, params: dict, lr_overrides=None, advance: bool = True):
+        """Descriptors for the fused K4b+K5 kernel (grads come from registers).
+        advance=False builds them without counting a step (CUDA-graph capture,
+        where lr / bias corrections come from device memory instead)."""
+        if not advance:
+            steps = dict(self._steps)
         descs = [self._group(name, params[name], None, lr_overrides) for name in SPLAT_GROUPS]
+        if not advance:
+            self._steps.update(steps)
         return (_lib.AdamGroup_t * 5)(*descs)
 
     def resize(self, decisions) -> None:

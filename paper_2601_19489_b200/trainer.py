@@ -196,9 +196,20 @@ class TrainStep:
     is reached."""
 
     def __init__(self, gset: GaussianSet, cfg: TrainConfig, extent: float = 4.0,
-                 optimizer: Adam | None = None, p_headroom: float = 1.5):
+                 optimizer: Adam | None = None, p_headroom: float = 1.5, graphs: bool = False):
         self.gset = gset
         self.cfg = cfg
+        # CUDA-graph replay of the whole step (after the first, eager, step
+        # has sized the capacities): one graph per (camera, GT buffer, depth
+        # inputs), each with its own private memory pool.  Per-step scalars
+        # (Adam lr and bias corrections, the depth weight) reach the kernels
+        # through pinned-memory copy nodes.
+        self.graphs = graphs
+        self._graph_cache = {}
+        self._scal_host = torch.zeros(15, dtype=torch.float32).pin_memory()
+        self._scal_dev = torch.zeros(15, dtype=torch.float32, device=_device())
+        self._dw_host = torch.zeros(1, dtype=torch.float32).pin_memory()
+        self._dw_dev = torch.zeros(1, dtype=torch.float32, device=_device())
         self.opt = optimizer or Adam({k: v for k, v in cfg.lrs.items() if k != "positions"})
         self.pos_base_lr = cfg.lrs.get("positions", 1.6e-4 * extent)
         self.iteration = 0
@@ -292,7 +303,9 @@ class TrainStep:
                                                          workspace=self.loss_ws)
         gd = gt = None
         dl = None
-        if depth_weight > 0.0 and depth_prior is not None:
+        # (a tensor weight comes from graph capture: no host read of it)
+        if depth_prior is not None and (isinstance(depth_weight, torch.Tensor)
+                                        or depth_weight > 0.0):
             dl, gd, gt = losses.depth_chain_device(out.depth, out.final_T, out.n_contrib,
                                                    depth_prior, depth_valid, depth_weight)
             e = e + dl
@@ -317,9 +330,65 @@ class TrainStep:
         self.status_event = torch.cuda.Event()
         self.status_event.record()
 
+    def _graph_key(self, camera: Camera, gt_image, depth_on: bool, depth_prior, depth_valid):
+        return (camera.fx, camera.fy, camera.cx, camera.cy, camera.width, camera.height,
+                camera.rotation.tobytes(), camera.translation.tobytes(), gt_image.data_ptr(),
+                depth_on, _lib.ptr(depth_prior) if depth_on else 0,
+                _lib.ptr(depth_valid) if depth_on else 0)
+
+    def _graph_body(self, camera: Camera, gt_image, depth_on: bool, depth_prior, depth_valid):
+        """The captured step: scalar uploads, K1-K5, status publish."""
+        self._scal_dev.copy_(self._scal_host, non_blocking=True)
+        self._dw_dev.copy_(self._dw_host, non_blocking=True)
+        batch = self.forward(camera, None)
+        e = self.loss_and_backward(batch, camera, gt_image, None,
+                                   self._dw_dev[0] if depth_on else 0.0,
+                                   depth_prior if depth_on else None, depth_valid)
+        groups = self.opt.groups_for_fused(self.gset.params(), None, advance=False)
+        _lib.check(self.lib.tsr_preprocess_bwd_adam_dev(
+            gaussians_struct(self.gset), camera_struct(camera, None, self.cfg.near),
+            batch.rec.data_ptr(), batch.row_of_source.data_ptr(), self.grad2d.data_ptr(), groups,
+            self._scal_dev.data_ptr(), None, self.skipped.data_ptr(), _lib.stream_handle()),
+            "tsr_preprocess_bwd_adam_dev")
+        self.status_dev[0:1].copy_(self.index.overflow)
+        self.status_dev[1:3].copy_(self.scratch.totals.flip(0))
+        self.status_host.copy_(self.status_dev, non_blocking=True)
+        return e
+
+    def _graph_step(self, camera: Camera, gt_image, depth_weight, depth_prior, depth_valid):
+        cap = self.index.p_cap
+        self._poll_status(camera)
+        if self.index.p_cap != cap:  # capacity grew: the buffers moved
+            self._graph_cache.clear()
+        self.iteration += 1
+        lr = {"positions": position_lr(self.pos_base_lr, self.iteration, self.cfg.max_iters)}
+        descs = self.opt.groups_for_fused(self.gset.params(), lr)  # advances the step counts
+        for k, d in enumerate(descs):
+            self._scal_host[3 * k] = d.lr
+            self._scal_host[3 * k + 1] = d.bias_correction1
+            self._scal_host[3 * k + 2] = d.bias_correction2
+        depth_on = depth_weight > 0.0 and depth_prior is not None
+        self._dw_host[0] = float(depth_weight)
+        key = self._graph_key(camera, gt_image, depth_on, depth_prior, depth_valid)
+        entry = self._graph_cache.get(key)
+        if entry is None:
+            torch.cuda.current_stream().synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                e = self._graph_body(camera, gt_image, depth_on, depth_prior, depth_valid)
+            entry = self._graph_cache[key] = (g, e)
+        entry[0].replay()
+        self._grad2d_clean = self.gset.colors.shape[1] == 1
+        self.status_event = torch.cuda.Event()
+        self.status_event.record()
+        self.last_camera = camera
+        return entry[1]
+
     def step(self, camera: Camera, gt_image: torch.Tensor, timer=None,
              depth_weight: float = 0.0, depth_prior=None, depth_valid=None) -> torch.Tensor:
         """Run one step; returns the loss as a device scalar (no host sync)."""
+        if self.graphs and timer is None and self.index is not None and self._grad2d_clean:
+            return self._graph_step(camera, gt_image, depth_weight, depth_prior, depth_valid)
         if self.index is not None:
             self._poll_status(camera)
         self.iteration += 1
