@@ -128,6 +128,15 @@ int tsr_render_fwd(const float* rec, const int32_t* values, const int64_t* offse
                    int32_t* out_n_contrib, int32_t* out_n_considered,
                    float* ckpt, const int64_t* ckpt_base, void* stream);
 
+/* Same with ckpt_stride 1 (every record, as above) or 2 (only the odd
+ * records r = 1, 3, 5, ...: the supergroup starts tsr_render_bwd reads, half
+ * the checkpoint traffic; the training step uses this). */
+int tsr_render_fwd_ex(const float* rec, const int32_t* values, const int64_t* offsets,
+                      int32_t width, int32_t height, const float* background_host,
+                      float* out_color, float* out_depth, float* out_final_T,
+                      int32_t* out_n_contrib, int32_t* out_n_considered, float* ckpt,
+                      const int64_t* ckpt_base, int32_t ckpt_stride, void* stream);
+
 /* K3 scoring mode (forward.py:132-137; density.py:36-76).  Re-renders the
  * view (same outputs as tsr_render_fwd, no checkpoints) and handles every
  * strong contribution (blend with w = T alpha >= 1/255):

@@ -63,6 +63,8 @@ _SIGNATURES = {
                                  c_vp, c_vp, c_vp]),
     "tsr_render_fwd": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, ctypes.POINTER(c_f32), c_vp, c_vp,
                                c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "tsr_render_fwd_ex": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, ctypes.POINTER(c_f32), c_vp,
+                                  c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "tsr_render_bwd": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
                                c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tsr_preprocess_bwd": (c_i32, [ctypes.POINTER(Gaussians_t), ctypes.POINTER(Camera_t), c_vp,

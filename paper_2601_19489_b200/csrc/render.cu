@@ -116,7 +116,10 @@ __device__ __forceinline__ void blend_pair(const float4 g, const float4 c, const
 constexpr int kFwdThreads = 128;
 constexpr int kBatch = 256;
 
-template <bool kCkpt, int kScore>
+// kCkpt: 0 no checkpoints, 1 every record (the reference's checkpoints), 2
+// only the odd records -- the ones K4 reads (supergroup starts, 64 positions
+// apart): half the checkpoint traffic in the training step.
+template <int kCkpt, int kScore>
 __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
     const float4* __restrict__ rec, const int32_t* __restrict__ values,
     const int64_t* __restrict__ offsets, int width, int height, int tiles_x, float bg_r,
@@ -224,7 +227,7 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
           }
         }
       }
-      if (kCkpt && cend == kGroup) {
+      if (kCkpt && cend == kGroup && (kCkpt == 1 || ((pos0 >> 5) & 1))) {
         // state after list position pos0+31 -> record (pos0+32)/32 - 1, for
         // each pixel that consumed that position (still alive, or died there)
         float* dst = ck0 + (long long)(pos0 >> 5) * (5 * kTilePixels);
@@ -277,30 +280,36 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
 
 using namespace tsr;
 
+extern "C" int tsr_render_fwd_ex(const float* rec, const int32_t* values, const int64_t* offsets,
+                                  int32_t width, int32_t height, const float* background_host,
+                                  float* out_color, float* out_depth, float* out_final_T,
+                                  int32_t* out_n_contrib, int32_t* out_n_considered, float* ckpt,
+                                  const int64_t* ckpt_base, int32_t ckpt_stride, void* stream) {
+  if (width <= 0 || height <= 0 || !background_host) return TSR_E_INVALID;
+  if (ckpt && !ckpt_base) return TSR_E_INVALID;
+  if (ckpt && ckpt_stride != 1 && ckpt_stride != 2) return TSR_E_INVALID;
+  const int tx = tiles_of(width), ty = tiles_of(height);
+  const int n_tiles = tx * ty;
+  cudaStream_t s = (cudaStream_t)stream;
+  const ScoreArgs none{};
+  auto* k = !ckpt ? render_fwd_kernel<0, 0>
+            : ckpt_stride == 2 ? render_fwd_kernel<2, 0> : render_fwd_kernel<1, 0>;
+  k<<<n_tiles, kFwdThreads, 0, s>>>((const float4*)rec, values, offsets, width, height, tx,
+                                    background_host[0], background_host[1], background_host[2],
+                                    out_color, out_depth, out_final_T, out_n_contrib,
+                                    out_n_considered, ckpt, ckpt_base, none);
+  TSR_CHECK_LAUNCH();
+  return TSR_OK;
+}
+
 extern "C" int tsr_render_fwd(const float* rec, const int32_t* values, const int64_t* offsets,
                               int32_t width, int32_t height, const float* background_host,
                               float* out_color, float* out_depth, float* out_final_T,
                               int32_t* out_n_contrib, int32_t* out_n_considered, float* ckpt,
                               const int64_t* ckpt_base, void* stream) {
-  if (width <= 0 || height <= 0 || !background_host) return TSR_E_INVALID;
-  if (ckpt && !ckpt_base) return TSR_E_INVALID;
-  const int tx = tiles_of(width), ty = tiles_of(height);
-  const int n_tiles = tx * ty;
-  cudaStream_t s = (cudaStream_t)stream;
-  const ScoreArgs none{};
-  if (ckpt) {
-    render_fwd_kernel<true, 0><<<n_tiles, kFwdThreads, 0, s>>>(
-        (const float4*)rec, values, offsets, width, height, tx, background_host[0],
-        background_host[1], background_host[2], out_color, out_depth, out_final_T,
-        out_n_contrib, out_n_considered, ckpt, ckpt_base, none);
-  } else {
-    render_fwd_kernel<false, 0><<<n_tiles, kFwdThreads, 0, s>>>(
-        (const float4*)rec, values, offsets, width, height, tx, background_host[0],
-        background_host[1], background_host[2], out_color, out_depth, out_final_T,
-        out_n_contrib, out_n_considered, nullptr, nullptr, none);
-  }
-  TSR_CHECK_LAUNCH();
-  return TSR_OK;
+  return tsr_render_fwd_ex(rec, values, offsets, width, height, background_host, out_color,
+                           out_depth, out_final_T, out_n_contrib, out_n_considered, ckpt,
+                           ckpt_base, 1, stream);
 }
 
 extern "C" int tsr_render_score(const float* rec, const int32_t* values, const int64_t* offsets,
@@ -321,8 +330,8 @@ extern "C" int tsr_render_score(const float* rec, const int32_t* values, const i
   cudaStream_t s = (cudaStream_t)stream;
   ScoreArgs sc{mask, weight, row_score, (long long*)warp_counts, (const long long*)warp_base,
                (long long*)out_pixel, (long long*)out_row};
-  auto* k = mode == 1 ? render_fwd_kernel<false, 1>
-            : mode == 2 ? render_fwd_kernel<false, 2> : render_fwd_kernel<false, 3>;
+  auto* k = mode == 1 ? render_fwd_kernel<0, 1>
+            : mode == 2 ? render_fwd_kernel<0, 2> : render_fwd_kernel<0, 3>;
   k<<<n_tiles, kFwdThreads, 0, s>>>((const float4*)rec, values, offsets, width, height, tx,
                                     background_host[0], background_host[1], background_host[2],
                                     out_color, out_depth, out_final_T, out_n_contrib,

@@ -140,17 +140,18 @@ def render_score_raw(rec, values, offsets, width: int, height: int, background, 
 
 
 def render_raw(rec, values, offsets, ckpt_base, width: int, height: int, background,
-               out: RenderTargets) -> None:
-    """Launch K3 into preallocated targets (no host synchronisation)."""
+               out: RenderTargets, ckpt_stride: int = 1) -> None:
+    """Launch K3 into preallocated targets (no host synchronisation).
+    ckpt_stride 2 writes only the checkpoint records K4 reads (training step)."""
     lib = _lib.load()
     bg = np.asarray(background, dtype=np.float64).reshape(3)
     bg_host = (_lib.c_f32 * 3)(*[float(v) for v in bg])
-    _lib.check(lib.tsr_render_fwd(
+    _lib.check(lib.tsr_render_fwd_ex(
         rec.data_ptr(), _lib.ptr(values), offsets.data_ptr(), width, height, bg_host,
         out.color.data_ptr(), out.depth.data_ptr(), out.final_T.data_ptr(),
         out.n_contrib.data_ptr(), out.n_considered.data_ptr(), _lib.ptr(out.ckpt),
-        _lib.ptr(ckpt_base) if out.ckpt is not None else None, _lib.stream_handle()),
-        "tsr_render_fwd")
+        _lib.ptr(ckpt_base) if out.ckpt is not None else None, int(ckpt_stride),
+        _lib.stream_handle()), "tsr_render_fwd_ex")
 
 
 def render(batch: SplatBatch, tiles: TileIndex, colors, background, *,
