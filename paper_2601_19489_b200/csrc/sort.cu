@@ -754,6 +754,10 @@ extern "C" int tsr_build_index(const float* rec, const uint32_t* depth_bits, con
                                                     kDynSmem) != cudaSuccess)
     return TSR_E_CUDA;
   int grid = sms * (per_sm < 3 ? per_sm : 3);
+  // small problems: fewer CTAs (each grid barrier costs ~ one arrival per
+  // CTA, and a slice of a few hundred items cannot use a whole CTA)
+  const long long work = (p_cap > m_cap ? p_cap : m_cap) / 4096 + 8;
+  if (work < grid) grid = (int)work;
   if (grid > kMaxGrid) grid = kMaxGrid;
   if (grid < 1) return TSR_E_CUDA;
   if (cudaMemsetAsync(w + pl.ctl_off, 0, pl.ctl_bytes, s) != cudaSuccess) return TSR_E_CUDA;
