@@ -167,6 +167,24 @@ int tsr_render_bwd(const float* rec, const int32_t* values, const int64_t* offse
                    const float* grad_depth, const float* grad_final_T,
                    float* grad2d, unsigned long long* merges, void* stream);
 
+/* Deterministic merge (bitwise run-to-run reproducible): K4 writes each
+ * processed (splat, tile) pair's 10 scaled sums to slots[pair] (P x 10
+ * floats, no atomics; processed[t] = list positions tile t processed), then
+ * one thread per batch row sums its slots in emission order into grad2d
+ * (overwritten: no zeroing needed).  spans / depth_bits are K1's outputs for
+ * the same batch and strategy; keys / values / offsets its TileIndex.  The
+ * row count is m, or *m_dev when m_dev is not NULL and smaller (capacity
+ * launches without a host read). */
+int tsr_render_bwd_det(const float* rec, const int32_t* values, const int64_t* offsets,
+                       int32_t width, int32_t height, const float* color, const float* depth,
+                       const float* final_T, const int32_t* n_considered, const float* ckpt,
+                       const int64_t* ckpt_base, const float* grad_color,
+                       const float* grad_depth, const float* grad_final_T,
+                       unsigned long long* merges, float* slots, int32_t* processed,
+                       const void* spans, const uint32_t* depth_bits, const int64_t* keys,
+                       int64_t m, const int64_t* m_dev, int32_t strategy, float* grad2d,
+                       void* stream);
+
 /* --------------------------------------------------------------- K4b ----
  * project_vjp + SH/colour chain (projection.py:139-241, trainer.py:231-257,
  * scene.py:279-291).  Writes (not accumulates) per-Gaussian gradients for

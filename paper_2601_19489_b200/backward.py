@@ -88,10 +88,32 @@ def backward_per_gaussian_raw(buffers: RenderBuffers, batch: SplatBatch, tiles: 
     return out, merges
 
 
+def backward_det_raw(buffers: RenderBuffers, batch: SplatBatch, tiles: TileIndex, grad_color,
+                     grad_depth, grad_final_T, out: torch.Tensor, merges: torch.Tensor,
+                     slots: torch.Tensor, processed: torch.Tensor, m_dev=None) -> None:
+    """K4 with the deterministic merge (slots + per-row emission-order sum)."""
+    lib = _lib.load()
+    gc = as_device_f32(grad_color)
+    gd = as_device_f32(grad_depth) if grad_depth is not None else None
+    gt = as_device_f32(grad_final_T) if grad_final_T is not None else None
+    _lib.check(lib.tsr_render_bwd_det(
+        batch.rec.data_ptr(), _lib.ptr(tiles.values) if tiles.n_pairs else None,
+        tiles.offsets.data_ptr(), batch.width, batch.height, buffers.color.data_ptr(),
+        buffers.depth.data_ptr(), buffers.final_T.data_ptr(), buffers.n_considered.data_ptr(),
+        _lib.ptr(buffers.ckpt), _lib.ptr(buffers.ckpt_base), gc.data_ptr(), _lib.ptr(gd),
+        _lib.ptr(gt), merges.data_ptr(), slots.data_ptr(), processed.data_ptr(),
+        batch.spans.data_ptr(), batch.depth_bits.data_ptr(), tiles.keys.data_ptr(),
+        out.shape[0], _lib.ptr(m_dev), int(batch.strategy), out.data_ptr(),
+        _lib.stream_handle()), "tsr_render_bwd_det")
+
+
 def backward_per_gaussian(buffers: RenderBuffers, batch: SplatBatch, tiles: TileIndex,
                           colors, grad_color, grad_depth=None, grad_final_T=None,
-                          group_size: int = CHECKPOINT_INTERVAL) -> Grad2D:
-    """K4 (backward.py:137-223)."""
+                          group_size: int = CHECKPOINT_INTERVAL,
+                          deterministic: bool = False) -> Grad2D:
+    """K4 (backward.py:137-223).  deterministic=True merges through per-pair
+    slots summed per row in emission order: bitwise reproducible run to run
+    (the default atomic merge agrees within FP32 rounding)."""
     if group_size != CHECKPOINT_INTERVAL:
         raise ValueError("groups are one 32-lane warp (CHECKPOINT_INTERVAL)")
     if not buffers.has_checkpoints and tiles.n_pairs > group_size:
@@ -103,6 +125,18 @@ def backward_per_gaussian(buffers: RenderBuffers, batch: SplatBatch, tiles: Tile
                 f"tile {tile} has {worst} splats but no stored checkpoints; "
                 "rerun the forward pass with checkpointing enabled")
     _ensure_colors(batch, colors)
+    if deterministic:
+        from .binning import _ensure_counts
+        _ensure_counts(batch, batch.strategy if batch.strategy is not None else 0)
+        dev = _device()
+        packed = torch.empty((len(batch), _lib.GRAD2D_FLOATS), dtype=torch.float32, device=dev)
+        merges = torch.zeros(1, dtype=torch.int64, device=dev)
+        slots = torch.empty((max(tiles.n_pairs, 1), _lib.GRAD2D_FLOATS), dtype=torch.float32,
+                            device=dev)
+        processed = torch.zeros(tiles.n_tiles, dtype=torch.int32, device=dev)
+        backward_det_raw(buffers, batch, tiles, grad_color, grad_depth, grad_final_T, packed,
+                         merges, slots, processed)
+        return Grad2D(packed, int(merges.item()))
     packed, merges = backward_per_gaussian_raw(buffers, batch, tiles, grad_color, grad_depth,
                                                grad_final_T)
     return Grad2D(packed, int(merges.item()))

@@ -56,7 +56,12 @@ constexpr int kListPad = 32;
 //   a = pixel centre x, y, g_depth, n_considered (int bits)
 //   b = g_r, g_g, g_b, Ktot + g_T T_final
 
-template <bool kDepth>
+// kDet: deterministic merge -- instead of atomics into grad2d, every pair of
+// a processed supergroup writes its 10 scaled sums to slot[pair] (plain
+// stores, one writer per pair) and the tile records how many list positions
+// it processed; grad_reduce_kernel then sums each row's slots in emission
+// order, so results are bitwise reproducible.
+template <bool kDepth, bool kDet>
 __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
     const float4* __restrict__ rec, const int32_t* __restrict__ values,
     const int64_t* __restrict__ offsets, int width, int height, int tiles_x,
@@ -65,7 +70,8 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
     const float* __restrict__ ckpt, const int64_t* __restrict__ ckpt_base,
     const float* __restrict__ grad_color, const float* __restrict__ grad_depth,
     const float* __restrict__ grad_final_T, float* __restrict__ grad2d,
-    unsigned long long* __restrict__ merges) {
+    unsigned long long* __restrict__ merges, float* __restrict__ slots,
+    int32_t* __restrict__ processed) {
   __shared__ float4 s_pa[kPixSlots];
   __shared__ float4 s_pb[kPixSlots];
   __shared__ unsigned short s_list[kBwdWarps][kTilePixels + 2 * kListPad];  // byte offsets
@@ -109,11 +115,15 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
     s_pb[px] = make_float4(gr, gg, gb, k);
   }
   // tile skipped when its upstream is all zero (backward.py:156-158)
-  if (!__syncthreads_or(nz)) return;
+  if (!__syncthreads_or(nz)) {
+    if (kDet && tid == 0) processed[tile] = 0;
+    return;
+  }
   atomicMax(&s_maxnc, my_max);
   if (tid == 0) atomicAdd(merges, (unsigned long long)n);
   __syncthreads();
   const int n_super = (s_maxnc + kSuper - 1) / kSuper;
+  if (kDet && tid == 0) processed[tile] = n_super * kSuper;
   const int lane = tid & 31, warp = tid >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   long long rbase = 0;
@@ -286,6 +296,23 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
         acc_mx = u;
         acc_my = v;
       }
+      if (kDet) {
+        if (row0 >= 0) {
+          float* dst = slots + (start + p) * TSR_GRAD2D_FLOATS;
+          dst[0] = ms * 0.5f * acc_mx.x; dst[1] = ms * 0.5f * acc_my.x;
+          dst[2] = -0.5f * acc_a.x; dst[3] = -acc_b.x; dst[4] = -0.5f * acc_c.x;
+          dst[5] = acc_o.x; dst[6] = acc_r.x; dst[7] = acc_g.x; dst[8] = acc_bl.x;
+          dst[9] = kDepth ? acc_d.x : 0.f;
+        }
+        if (row1 >= 0) {
+          float* dst = slots + (start + p + 1) * TSR_GRAD2D_FLOATS;
+          dst[0] = ms * 0.5f * acc_mx.y; dst[1] = ms * 0.5f * acc_my.y;
+          dst[2] = -0.5f * acc_a.y; dst[3] = -acc_b.y; dst[4] = -0.5f * acc_c.y;
+          dst[5] = acc_o.y; dst[6] = acc_r.y; dst[7] = acc_g.y; dst[8] = acc_bl.y;
+          dst[9] = kDepth ? acc_d.y : 0.f;
+        }
+        continue;
+      }
       if (row0 >= 0 && ((acc_o.x != 0.f) | (acc_r.x != 0.f) | (acc_g.x != 0.f) |
                         (acc_bl.x != 0.f) | (acc_d.x != 0.f) | (acc_a.x != 0.f))) {
         float* dst = grad2d + (long long)row0 * TSR_GRAD2D_FLOATS;
@@ -318,6 +345,81 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
   }
 }
 
+// Deterministic merge, second half: one thread per batch row sums the row's
+// slots in emission order (binning.py:217-221: column-major over its tiles).
+// Each (tile, row) pair is located by a binary search of the tile's
+// depth-sorted keys for tile << 32 | depth bits (then the row among equal
+// keys); slots of positions the tile did not process count as zero.
+__global__ void __launch_bounds__(256) grad_reduce_kernel(
+    const float* __restrict__ rec, const uint4* __restrict__ spans,
+    const uint32_t* __restrict__ depth_bits, const int64_t* __restrict__ keys,
+    const int32_t* __restrict__ values, const int64_t* __restrict__ offsets,
+    const int32_t* __restrict__ processed, const float* __restrict__ slots, long long m,
+    const int64_t* __restrict__ m_dev, int tiles_x, int tiles_y, int strategy,
+    float* __restrict__ grad2d) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m_dev && *m_dev < m) m = *m_dev;  // rows on the device (capacity launch)
+  if (r >= m) return;
+  float acc[TSR_GRAD2D_FLOATS];
+#pragma unroll
+  for (int j = 0; j < TSR_GRAD2D_FLOATS; ++j) acc[j] = 0.f;
+  const uint32_t db = depth_bits[r];
+  auto add_tile = [&](long long t) {
+    const long long lo0 = offsets[t], hi = offsets[t + 1];
+    const long long target = (t << 32) | (long long)db;
+    long long lo = lo0, h = hi;
+    while (lo < h) {  // first key >= target
+      const long long mid = (lo + h) >> 1;
+      if (keys[mid] < target) lo = mid + 1;
+      else h = mid;
+    }
+    while (lo < hi && keys[lo] == target && values[lo] != (int32_t)r) ++lo;  // depth ties
+    if (lo < hi && keys[lo] == target && lo - lo0 < processed[t]) {
+      const float* sl = slots + lo * TSR_GRAD2D_FLOATS;
+#pragma unroll
+      for (int j = 0; j < TSR_GRAD2D_FLOATS; ++j) acc[j] += sl[j];
+    }
+  };
+  const uint4 sp = spans[r];
+  if (strategy == 0 && !(sp.y >> 31)) {
+    const long long tx0 = sp.x & 0xffffu, ncols = sp.x >> 16, ty_base = sp.y & 0xffffu;
+    for (long long c = 0; c < ncols; ++c) {
+      const uint32_t code = ((c < 4 ? sp.z : sp.w) >> (8 * (c & 3))) & 0xffu;
+      for (long long q = 0; q < (code >> 4); ++q)
+        add_tile((ty_base + (code & 15u) + q) * tiles_x + tx0 + c);
+    }
+  } else {
+    SplatF64 s = load_splat_f64(rec + r * 12);
+    if (strategy == 2) {
+      long long tx0, tx1, ty0, ty1;
+      aabb_rect(s, tiles_x, tiles_y, tx0, tx1, ty0, ty1);
+      for (long long tx = tx0; tx <= tx1; ++tx)
+        for (long long ty = ty0; ty <= ty1; ++ty) add_tile(ty * tiles_x + tx);
+    } else {
+      SnugRect box = snugbox(s, tiles_x, tiles_y);
+      if (box.tx0 <= box.tx1 && box.ty0 <= box.ty1) {
+        for (long long tx = box.tx0; tx <= box.tx1; ++tx) {
+          if (strategy == 1) {
+            const double rx0 = dsub((double)(16 * tx), s.mx);
+            for (long long ty = box.ty0; ty <= box.ty1; ++ty) {
+              const double ry0 = dsub((double)(16 * ty), s.my);
+              if (min_q_box(s, rx0, dadd(rx0, 16.0), ry0, dadd(ry0, 16.0)) <= s.t)
+                add_tile(ty * tiles_x + tx);
+            }
+          } else {
+            long long ty0, ty1;
+            const int nr = column_rows(s, box, tx, tiles_y, ty0, ty1);
+            for (int q = 0; q < nr; ++q) add_tile((ty0 + q) * tiles_x + tx);
+          }
+        }
+      }
+    }
+  }
+  float* dst = grad2d + r * TSR_GRAD2D_FLOATS;
+#pragma unroll
+  for (int j = 0; j < TSR_GRAD2D_FLOATS; ++j) dst[j] = acc[j];
+}
+
 }  // namespace tsr
 
 using namespace tsr;
@@ -332,10 +434,42 @@ extern "C" int tsr_render_bwd(const float* rec, const int32_t* values, const int
   if (width <= 0 || height <= 0 || !grad_color || !merges) return TSR_E_INVALID;
   if (ckpt && !ckpt_base) return TSR_E_INVALID;
   const int tx = tiles_of(width), ty = tiles_of(height);
-  auto* k = grad_depth ? render_bwd_kernel<true> : render_bwd_kernel<false>;
+  auto* k = grad_depth ? render_bwd_kernel<true, false> : render_bwd_kernel<false, false>;
   k<<<tx * ty, kBwdThreads, 0, (cudaStream_t)stream>>>(
       (const float4*)rec, values, offsets, width, height, tx, color, depth, final_T,
-      n_considered, ckpt, ckpt_base, grad_color, grad_depth, grad_final_T, grad2d, merges);
+      n_considered, ckpt, ckpt_base, grad_color, grad_depth, grad_final_T, grad2d, merges,
+      nullptr, nullptr);
   TSR_CHECK_LAUNCH();
+  return TSR_OK;
+}
+
+extern "C" int tsr_render_bwd_det(const float* rec, const int32_t* values, const int64_t* offsets,
+                                  int32_t width, int32_t height, const float* color,
+                                  const float* depth, const float* final_T,
+                                  const int32_t* n_considered, const float* ckpt,
+                                  const int64_t* ckpt_base, const float* grad_color,
+                                  const float* grad_depth, const float* grad_final_T,
+                                  unsigned long long* merges, float* slots, int32_t* processed,
+                                  const void* spans, const uint32_t* depth_bits,
+                                  const int64_t* keys, int64_t m, const int64_t* m_dev,
+                                  int32_t strategy, float* grad2d, void* stream) {
+  if (width <= 0 || height <= 0 || !grad_color || !merges || !slots || !processed || !spans ||
+      !depth_bits || !keys || m < 0 || !grad2d)
+    return TSR_E_INVALID;
+  if (ckpt && !ckpt_base) return TSR_E_INVALID;
+  const int tx = tiles_of(width), ty = tiles_of(height);
+  cudaStream_t s = (cudaStream_t)stream;
+  auto* k = grad_depth ? render_bwd_kernel<true, true> : render_bwd_kernel<false, true>;
+  k<<<tx * ty, kBwdThreads, 0, s>>>((const float4*)rec, values, offsets, width, height, tx,
+                                    color, depth, final_T, n_considered, ckpt, ckpt_base,
+                                    grad_color, grad_depth, grad_final_T, nullptr, merges, slots,
+                                    processed);
+  TSR_CHECK_LAUNCH();
+  if (m > 0) {
+    grad_reduce_kernel<<<(int)((m + 255) / 256), 256, 0, s>>>(
+        rec, (const uint4*)spans, depth_bits, keys, values, offsets, processed, slots, m, m_dev,
+        tx, ty, strategy, grad2d);
+    TSR_CHECK_LAUNCH();
+  }
   return TSR_OK;
 }

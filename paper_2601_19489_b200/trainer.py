@@ -196,9 +196,16 @@ class TrainStep:
     is reached."""
 
     def __init__(self, gset: GaussianSet, cfg: TrainConfig, extent: float = 4.0,
-                 optimizer: Adam | None = None, p_headroom: float = 1.5, graphs: bool = False):
+                 optimizer: Adam | None = None, p_headroom: float = 1.5, graphs: bool = False,
+                 deterministic: bool | None = None):
         self.gset = gset
         self.cfg = cfg
+        # deterministic merge in K4: bitwise run-to-run reproducible (opt-in;
+        # the default atomic merge agrees within FP32 rounding).  The
+        # reference's cfg.deterministic concerns its CPU worker pool.
+        self.deterministic = bool(deterministic)
+        self.slots = None
+        self.processed = None
         # CUDA-graph replay of the whole step (after the first, eager, step
         # has sized the capacities): one graph per (camera, GT buffer, depth
         # inputs), each with its own private memory pool.  Per-step scalars
@@ -206,10 +213,14 @@ class TrainStep:
         # through pinned-memory copy nodes.
         self.graphs = graphs
         self._graph_cache = {}
-        self._scal_host = torch.zeros(15, dtype=torch.float32).pin_memory()
-        self._scal_dev = torch.zeros(15, dtype=torch.float32, device=_device())
-        self._dw_host = torch.zeros(1, dtype=torch.float32).pin_memory()
-        self._dw_dev = torch.zeros(1, dtype=torch.float32, device=_device())
+        # device copy the graph reads: [lr, bc1, bc2] x 5 groups, depth weight
+        self._scal_dev = torch.zeros(16, dtype=torch.float32, device=_device())
+        # host staging ring: slot k is copied (stream-ordered, before the
+        # replay) into _scal_dev and not rewritten until its copy completed,
+        # so the host may run ahead of the device by up to kRing steps
+        self._ring = [torch.zeros(16, dtype=torch.float32).pin_memory() for _ in range(8)]
+        self._ring_ev = [None] * 8
+        self._ring_k = 0
         self.opt = optimizer or Adam({k: v for k, v in cfg.lrs.items() if k != "positions"})
         self.pos_base_lr = cfg.lrs.get("positions", 1.6e-4 * extent)
         self.iteration = 0
@@ -260,6 +271,10 @@ class TrainStep:
         self.hw = (camera.height, camera.width)
         self.grad_color = torch.empty((camera.height, camera.width, 3), dtype=torch.float32,
                                       device=self.grad2d.device)
+        if self.deterministic:
+            self.slots = torch.empty((max(p_cap, 1), _lib.GRAD2D_FLOATS), dtype=torch.float32,
+                                     device=self.grad2d.device)
+            self.processed = torch.zeros(tiles, dtype=torch.int32, device=self.grad2d.device)
 
     def _poll_status(self, camera: Camera) -> None:
         """Non-blocking check of an earlier step's overflow flag and P."""
@@ -311,6 +326,19 @@ class TrainStep:
             e = e + dl
         self.last_losses = (e, l1, s, dl)
         self._mark(timer, "loss")
+        if self.deterministic:  # slots + emission-order row sums overwrite grad2d
+            _lib.check(self.lib.tsr_render_bwd_det(
+                batch.rec.data_ptr(), idx.values.data_ptr(), idx.offsets.data_ptr(),
+                camera.width, camera.height, out.color.data_ptr(), out.depth.data_ptr(),
+                out.final_T.data_ptr(), out.n_considered.data_ptr(), out.ckpt.data_ptr(),
+                idx.ckpt_base.data_ptr(), grad_color.data_ptr(), _lib.ptr(gd), _lib.ptr(gt),
+                self.merges.data_ptr(), self.slots.data_ptr(), self.processed.data_ptr(),
+                batch.spans.data_ptr(), batch.depth_bits.data_ptr(), idx.keys.data_ptr(),
+                self.grad2d.shape[0], self.scratch.totals.data_ptr(), self.cfg.strategy_id,
+                self.grad2d.data_ptr(), _lib.stream_handle()), "tsr_render_bwd_det")
+            self._grad2d_clean = False
+            self._mark(timer, "backward")
+            return e
         if not self._grad2d_clean:
             self.grad2d.zero_()
         self._grad2d_clean = False
@@ -337,12 +365,11 @@ class TrainStep:
                 _lib.ptr(depth_valid) if depth_on else 0)
 
     def _graph_body(self, camera: Camera, gt_image, depth_on: bool, depth_prior, depth_valid):
-        """The captured step: scalar uploads, K1-K5, status publish."""
-        self._scal_dev.copy_(self._scal_host, non_blocking=True)
-        self._dw_dev.copy_(self._dw_host, non_blocking=True)
+        """The captured step: K1-K5 and the status publish; the per-step
+        scalars are read from _scal_dev."""
         batch = self.forward(camera, None)
         e = self.loss_and_backward(batch, camera, gt_image, None,
-                                   self._dw_dev[0] if depth_on else 0.0,
+                                   self._scal_dev[15] if depth_on else 0.0,
                                    depth_prior if depth_on else None, depth_valid)
         groups = self.opt.groups_for_fused(self.gset.params(), None, advance=False)
         _lib.check(self.lib.tsr_preprocess_bwd_adam_dev(
@@ -363,12 +390,21 @@ class TrainStep:
         self.iteration += 1
         lr = {"positions": position_lr(self.pos_base_lr, self.iteration, self.cfg.max_iters)}
         descs = self.opt.groups_for_fused(self.gset.params(), lr)  # advances the step counts
-        for k, d in enumerate(descs):
-            self._scal_host[3 * k] = d.lr
-            self._scal_host[3 * k + 1] = d.bias_correction1
-            self._scal_host[3 * k + 2] = d.bias_correction2
+        k = self._ring_k
+        self._ring_k = (k + 1) % len(self._ring)
+        if self._ring_ev[k] is not None:
+            self._ring_ev[k].synchronize()  # that slot's copy has been consumed
+        host = self._ring[k]
+        for j, d in enumerate(descs):
+            host[3 * j] = d.lr
+            host[3 * j + 1] = d.bias_correction1
+            host[3 * j + 2] = d.bias_correction2
+        host[15] = float(depth_weight)
+        self._scal_dev.copy_(host, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._ring_ev[k] = ev
         depth_on = depth_weight > 0.0 and depth_prior is not None
-        self._dw_host[0] = float(depth_weight)
         key = self._graph_key(camera, gt_image, depth_on, depth_prior, depth_valid)
         entry = self._graph_cache.get(key)
         if entry is None:

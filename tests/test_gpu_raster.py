@@ -133,3 +133,26 @@ def test_early_termination_consideration_point():
     k = int(bufs.n_considered[16, 16])
     assert k < n and float(bufs.final_T[16, 16]) < 1e-4
     assert abs(k - np.ceil(np.log(1e-4) / np.log(0.1))) <= 1
+
+
+@pytest.mark.parametrize("name", ["r60", "r128", "deep"])
+def test_deterministic_merge_is_bitwise_reproducible(graster, name):
+    """The deterministic merge (per-pair slots summed per row in emission
+    order) reproduces itself bit for bit and matches the reference like the
+    atomic merge does."""
+    import paper_2601_19489_b200 as ts
+    from conftest import rel_err
+    g = graster
+    b = batch_from(g, name + "_")
+    db = dev_batch(b)
+    tiles = ts.bin_sequential(db)
+    bufs = ts.render(db, tiles, g[name + "_colors"], g[name + "_bg"])
+    args = (bufs, db, tiles, g[name + "_colors"], g[name + "_gc"], g[name + "_gd"],
+            g[name + "_gt"])
+    a = ts.backward_per_gaussian(*args, deterministic=True)
+    c = ts.backward_per_gaussian(*args, deterministic=True)
+    for k in ("d_means2d", "d_conics", "d_opacities", "d_colors", "d_depths"):
+        x, y = getattr(a, k).cpu().numpy(), getattr(c, k).cpu().numpy()
+        assert np.array_equal(x, y), k
+        assert rel_err(x, g[f"{name}_pg_{k}"]) < 1e-4, k
+    assert a.merges == int(g[name + "_merges"])

@@ -206,3 +206,26 @@ def test_graph_replayed_train_step_matches_eager():
         de = np.abs(a - out["eager2"][k]).reshape(len(a), -1).max(axis=1)
         assert dg.max() <= 12 * lrs[k], k
         assert (dg > tol).mean() <= 2.0 * (de > tol).mean() + 0.005, k
+
+
+def test_deterministic_train_step_is_bitwise_reproducible():
+    """TrainStep(deterministic=True): two runs from the same state give
+    bitwise-identical parameters (the reference's determinism contract,
+    test_trainer.py:74-82), eager and graph-replayed alike."""
+    import torch
+    import paper_2601_19489_b200 as ts
+    from oracle.raster import make_scene
+    params, cam, gt = make_scene(20_000, 320, 240, seed=9)
+    camera = ts.Camera(cam["fx"], cam["fy"], cam["cx"], cam["cy"], 320, 240, cam["R"], cam["t"])
+    g_dev = torch.as_tensor(np.asarray(gt, np.float32), device="cuda")
+    runs = []
+    for graphs in (False, False, True):
+        g = ts.GaussianSet(**params)
+        st = ts.TrainStep(g, ts.TrainConfig(max_iters=100), deterministic=True, graphs=graphs)
+        for _ in range(5):
+            st.step(camera, g_dev)
+        torch.cuda.synchronize()
+        runs.append(g.to_numpy())
+    for k in runs[0]:
+        assert np.array_equal(runs[0][k], runs[1][k]), k
+        assert np.array_equal(runs[0][k], runs[2][k]), k
