@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="K4 deterministic merge (bitwise reproducible)")
     return ap.parse_args()
 
 
@@ -321,7 +323,8 @@ def gpu_arm(args):
     cfg = ts.TrainConfig(max_iters=30_000)
     if world == 1:
         # the step replays as one CUDA graph (captured during warm-up)
-        stepper = ts.TrainStep(gset, cfg, extent=4.0, graphs=True)
+        stepper = ts.TrainStep(gset, cfg, extent=4.0, graphs=True,
+                               deterministic=args.deterministic)
         run = lambda timer=None: stepper.step(camera, gt_dev, timer)  # noqa: E731
     else:
         stepper = ViewParallelStep(gset, cfg, extent=4.0)
@@ -492,6 +495,8 @@ def gpu_arm(args):
         "config": {"workload": f"{args.config}: " + _workload(args.config, world),
                    "views_per_step": world, "parallelism": f"view-parallel dp{world}",
                    "launch": "one CUDA graph replay per step" if world == 1 else "eager launches",
+                   "merge": "deterministic (slots + emission-order row sums)"
+                            if args.deterministic else "float atomics (FP32-tolerance)",
                    "l2": "inputs larger than L2 (Gaussian state + Adam moments 168 MB, "
                          "per-step buffers ~1 GB)"},
         "roofline": {"kernel": "render_bwd_kernel (K4)", "bound": "fp32",

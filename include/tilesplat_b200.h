@@ -111,6 +111,16 @@ int tsr_snugboxes(const float* rec, int64_t m, int32_t width, int32_t height,
  * *overflow (sticky, device int32) is set to 1: the caller re-runs with a
  * larger capacity. */
 size_t tsr_index_workspace(int64_t m_cap, int64_t p_cap);
+/* tsr_build_index plus what the deterministic merge needs: inv_perm[e] =
+ * sorted position of emission index e (P_cap), and per depth rank the batch
+ * row, pair count and emission offset (M_cap each). */
+int tsr_build_index_det(const float* rec, const uint32_t* depth_bits, const void* spans,
+                        const int32_t* counts, const int64_t* totals, int64_t m_cap,
+                        int64_t p_cap, int32_t width, int32_t height, int32_t strategy,
+                        int64_t* keys, int32_t* values, int64_t* offsets, int64_t* ckpt_base,
+                        int32_t* overflow, void* workspace, size_t workspace_bytes,
+                        uint32_t* inv_perm, uint32_t* rank_row, uint32_t* rank_count,
+                        uint32_t* rank_off, void* stream);
 int tsr_build_index(const float* rec, const uint32_t* depth_bits, const void* spans,
                     const int32_t* counts, const int64_t* totals, int64_t m_cap, int64_t p_cap,
                     int32_t width, int32_t height, int32_t strategy, int64_t* keys,
@@ -170,19 +180,19 @@ int tsr_render_bwd(const float* rec, const int32_t* values, const int64_t* offse
 /* Deterministic merge (bitwise run-to-run reproducible): K4 writes each
  * processed (splat, tile) pair's 10 scaled sums to slots[pair] (P x 10
  * floats, no atomics; processed[t] = list positions tile t processed), then
- * one thread per batch row sums its slots in emission order into grad2d
- * (overwritten: no zeroing needed).  spans / depth_bits are K1's outputs for
- * the same batch and strategy; keys / values / offsets its TileIndex.  The
- * row count is m, or *m_dev when m_dev is not NULL and smaller (capacity
- * launches without a host read). */
+ * one thread per depth rank sums its row's slots in emission order into
+ * grad2d (overwritten: no zeroing needed), using tsr_build_index_det's
+ * outputs.  The row count is m, or *m_dev when m_dev is not NULL and smaller
+ * (capacity launches without a host read). */
 int tsr_render_bwd_det(const float* rec, const int32_t* values, const int64_t* offsets,
                        int32_t width, int32_t height, const float* color, const float* depth,
                        const float* final_T, const int32_t* n_considered, const float* ckpt,
                        const int64_t* ckpt_base, const float* grad_color,
                        const float* grad_depth, const float* grad_final_T,
                        unsigned long long* merges, float* slots, int32_t* processed,
-                       const void* spans, const uint32_t* depth_bits, const int64_t* keys,
-                       int64_t m, const int64_t* m_dev, int32_t strategy, float* grad2d,
+                       const uint32_t* inv_perm, const uint32_t* rank_row,
+                       const uint32_t* rank_count, const uint32_t* rank_off,
+                       const int64_t* keys, int64_t m, const int64_t* m_dev, float* grad2d,
                        void* stream);
 
 /* --------------------------------------------------------------- K4b ----

@@ -69,7 +69,10 @@ _SIGNATURES = {
                                c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tsr_render_bwd_det": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
                                    c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
-                                   c_i64, c_vp, c_i32, c_vp, c_vp]),
+                                   c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "tsr_build_index_det": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_i32,
+                                    c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp, c_vp,
+                                    c_vp, c_vp, c_vp]),
     "tsr_preprocess_bwd": (c_i32, [ctypes.POINTER(Gaussians_t), ctypes.POINTER(Camera_t), c_vp,
                                    c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "tsr_adam_step": (c_i32, [ctypes.POINTER(AdamGroup_t), c_i32, c_vp, c_vp]),

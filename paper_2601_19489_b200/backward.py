@@ -91,19 +91,24 @@ def backward_per_gaussian_raw(buffers: RenderBuffers, batch: SplatBatch, tiles: 
 def backward_det_raw(buffers: RenderBuffers, batch: SplatBatch, tiles: TileIndex, grad_color,
                      grad_depth, grad_final_T, out: torch.Tensor, merges: torch.Tensor,
                      slots: torch.Tensor, processed: torch.Tensor, m_dev=None) -> None:
-    """K4 with the deterministic merge (slots + per-row emission-order sum)."""
+    """K4 with the deterministic merge (per-pair slots, per-row emission-order
+    sums through K2's inverse permutation)."""
     lib = _lib.load()
+    if tiles.det is None:
+        raise ValueError("the deterministic merge needs a TileIndex built with its "
+                         "permutation outputs (IndexBuffers(det=True))")
     gc = as_device_f32(grad_color)
     gd = as_device_f32(grad_depth) if grad_depth is not None else None
     gt = as_device_f32(grad_final_T) if grad_final_T is not None else None
+    inv_perm, rank_row, rank_count, rank_off = tiles.det
     _lib.check(lib.tsr_render_bwd_det(
         batch.rec.data_ptr(), _lib.ptr(tiles.values) if tiles.n_pairs else None,
         tiles.offsets.data_ptr(), batch.width, batch.height, buffers.color.data_ptr(),
         buffers.depth.data_ptr(), buffers.final_T.data_ptr(), buffers.n_considered.data_ptr(),
         _lib.ptr(buffers.ckpt), _lib.ptr(buffers.ckpt_base), gc.data_ptr(), _lib.ptr(gd),
         _lib.ptr(gt), merges.data_ptr(), slots.data_ptr(), processed.data_ptr(),
-        batch.spans.data_ptr(), batch.depth_bits.data_ptr(), tiles.keys.data_ptr(),
-        out.shape[0], _lib.ptr(m_dev), int(batch.strategy), out.data_ptr(),
+        inv_perm.data_ptr(), rank_row.data_ptr(), rank_count.data_ptr(), rank_off.data_ptr(),
+        tiles.keys.data_ptr(), out.shape[0], _lib.ptr(m_dev), out.data_ptr(),
         _lib.stream_handle()), "tsr_render_bwd_det")
 
 
@@ -126,8 +131,6 @@ def backward_per_gaussian(buffers: RenderBuffers, batch: SplatBatch, tiles: Tile
                 "rerun the forward pass with checkpointing enabled")
     _ensure_colors(batch, colors)
     if deterministic:
-        from .binning import _ensure_counts
-        _ensure_counts(batch, batch.strategy if batch.strategy is not None else 0)
         dev = _device()
         packed = torch.empty((len(batch), _lib.GRAD2D_FLOATS), dtype=torch.float32, device=dev)
         merges = torch.zeros(1, dtype=torch.int64, device=dev)

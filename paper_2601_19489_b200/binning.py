@@ -37,13 +37,15 @@ class SnugBox:
 class TileIndex:
     """Depth-sorted (tile, splat) pairs with per-tile ranges (binning.py:37-71)."""
 
-    def __init__(self, keys, values, offsets, tiles_x, tiles_y, ckpt_base=None):
+    def __init__(self, keys, values, offsets, tiles_x, tiles_y, ckpt_base=None, det=None):
         self.keys = keys
         self.values = values
         self.offsets = offsets
         self.tiles_x = int(tiles_x)
         self.tiles_y = int(tiles_y)
         self.ckpt_base = ckpt_base
+        # (inv_perm, rank_row, rank_count, rank_off) for the deterministic merge
+        self.det = det
 
     @property
     def n_pairs(self) -> int:
@@ -129,10 +131,17 @@ def _ensure_counts(batch: SplatBatch, strategy: int) -> None:
 class IndexBuffers:
     """Capacity buffers for K2 (reused across steps by the trainer)."""
 
-    def __init__(self, m_cap: int, p_cap: int, n_tiles: int):
+    def __init__(self, m_cap: int, p_cap: int, n_tiles: int, det: bool = False):
         dev = _device()
         lib = _lib.load()
         self.m_cap, self.p_cap, self.n_tiles = m_cap, p_cap, n_tiles
+        self.det = None
+        if det:  # K2's outputs for the deterministic merge
+            u32 = torch.int32
+            self.det = (torch.empty(max(p_cap, 1), dtype=u32, device=dev),
+                        torch.empty(max(m_cap, 1), dtype=u32, device=dev),
+                        torch.empty(max(m_cap, 1), dtype=u32, device=dev),
+                        torch.empty(max(m_cap, 1), dtype=u32, device=dev))
         self.keys = torch.empty(max(p_cap, 1), dtype=torch.int64, device=dev)
         self.values = torch.empty(max(p_cap, 1), dtype=torch.int32, device=dev)
         self.offsets = torch.empty(n_tiles + 1, dtype=torch.int64, device=dev)
@@ -148,12 +157,16 @@ class IndexBuffers:
 def build_index_raw(batch: SplatBatch, strategy: int, bufs: IndexBuffers) -> None:
     """Launch K2 into capacity buffers; sizes come from batch.totals on the device."""
     lib = _lib.load()
-    _lib.check(lib.tsr_build_index(
-        batch.rec.data_ptr(), batch.depth_bits.data_ptr(), batch.spans.data_ptr(),
-        batch.counts.data_ptr(), batch.totals.data_ptr(), bufs.m_cap, bufs.p_cap, batch.width,
-        batch.height, strategy, bufs.keys.data_ptr(), bufs.values.data_ptr(),
-        bufs.offsets.data_ptr(), bufs.ckpt_base.data_ptr(), bufs.overflow.data_ptr(),
-        bufs.workspace.data_ptr(), bufs.ws_bytes, _lib.stream_handle()), "tsr_build_index")
+    args = (batch.rec.data_ptr(), batch.depth_bits.data_ptr(), batch.spans.data_ptr(),
+            batch.counts.data_ptr(), batch.totals.data_ptr(), bufs.m_cap, bufs.p_cap,
+            batch.width, batch.height, strategy, bufs.keys.data_ptr(), bufs.values.data_ptr(),
+            bufs.offsets.data_ptr(), bufs.ckpt_base.data_ptr(), bufs.overflow.data_ptr(),
+            bufs.workspace.data_ptr(), bufs.ws_bytes)
+    if bufs.det is not None:
+        _lib.check(lib.tsr_build_index_det(*args, *(t.data_ptr() for t in bufs.det),
+                                           _lib.stream_handle()), "tsr_build_index_det")
+    else:
+        _lib.check(lib.tsr_build_index(*args, _lib.stream_handle()), "tsr_build_index")
 
 
 def build_index(batch: SplatBatch, strategy: int, bufs: IndexBuffers | None = None) -> TileIndex:
@@ -162,10 +175,10 @@ def build_index(batch: SplatBatch, strategy: int, bufs: IndexBuffers | None = No
     tiles_x, tiles_y = _tiles(batch)
     m, p = len(batch), int(batch.n_pairs)
     if bufs is None or not bufs.fits(m, p, tiles_x * tiles_y):
-        bufs = IndexBuffers(m, p, tiles_x * tiles_y)
+        bufs = IndexBuffers(m, p, tiles_x * tiles_y, det=True)
     build_index_raw(batch, strategy, bufs)
     return TileIndex(bufs.keys[:p], bufs.values[:p], bufs.offsets, tiles_x, tiles_y,
-                     bufs.ckpt_base)
+                     bufs.ckpt_base, bufs.det)
 
 
 def bin_sequential(batch: SplatBatch) -> TileIndex:

@@ -345,77 +345,50 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
   }
 }
 
-// Deterministic merge, second half: one thread per batch row sums the row's
-// slots in emission order (binning.py:217-221: column-major over its tiles).
-// Each (tile, row) pair is located by a binary search of the tile's
-// depth-sorted keys for tile << 32 | depth bits (then the row among equal
-// keys); slots of positions the tile did not process count as zero.
+// Deterministic merge, second half: one thread per depth rank sums its
+// row's slots in emission order (binning.py:217-221: the row's pairs are a
+// contiguous emission range [rank_off, rank_off + rank_count), and K2's
+// inverse permutation gives each pair's sorted position); a slot counts only
+// if its tile processed that list position.  No searches, no atomics.
 __global__ void __launch_bounds__(256) grad_reduce_kernel(
-    const float* __restrict__ rec, const uint4* __restrict__ spans,
-    const uint32_t* __restrict__ depth_bits, const int64_t* __restrict__ keys,
-    const int32_t* __restrict__ values, const int64_t* __restrict__ offsets,
+    const uint32_t* __restrict__ rank_row, const uint32_t* __restrict__ rank_count,
+    const uint32_t* __restrict__ rank_off, const uint32_t* __restrict__ inv_perm,
+    const int64_t* __restrict__ keys, const int64_t* __restrict__ offsets,
     const int32_t* __restrict__ processed, const float* __restrict__ slots, long long m,
-    const int64_t* __restrict__ m_dev, int tiles_x, int tiles_y, int strategy,
-    float* __restrict__ grad2d) {
-  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t* __restrict__ m_dev, float* __restrict__ grad2d) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (m_dev && *m_dev < m) m = *m_dev;  // rows on the device (capacity launch)
-  if (r >= m) return;
+  if (q >= m) return;
   float acc[TSR_GRAD2D_FLOATS];
 #pragma unroll
   for (int j = 0; j < TSR_GRAD2D_FLOATS; ++j) acc[j] = 0.f;
-  const uint32_t db = depth_bits[r];
-  auto add_tile = [&](long long t) {
-    const long long lo0 = offsets[t], hi = offsets[t + 1];
-    const long long target = (t << 32) | (long long)db;
-    long long lo = lo0, h = hi;
-    while (lo < h) {  // first key >= target
-      const long long mid = (lo + h) >> 1;
-      if (keys[mid] < target) lo = mid + 1;
-      else h = mid;
-    }
-    while (lo < hi && keys[lo] == target && values[lo] != (int32_t)r) ++lo;  // depth ties
-    if (lo < hi && keys[lo] == target && lo - lo0 < processed[t]) {
-      const float* sl = slots + lo * TSR_GRAD2D_FLOATS;
+  const uint32_t e0 = rank_off[q], c = rank_count[q];
+  const int* khi = reinterpret_cast<const int*>(keys) + 1;  // tile = high word
+  // 4 pairs in flight per round (independent gathers), summed in order
+  for (uint32_t e = e0; e < e0 + c; e += 4) {
+    uint32_t k[4];
+    int t[4];
+    bool ok[4];
 #pragma unroll
-      for (int j = 0; j < TSR_GRAD2D_FLOATS; ++j) acc[j] += sl[j];
-    }
-  };
-  const uint4 sp = spans[r];
-  if (strategy == 0 && !(sp.y >> 31)) {
-    const long long tx0 = sp.x & 0xffffu, ncols = sp.x >> 16, ty_base = sp.y & 0xffffu;
-    for (long long c = 0; c < ncols; ++c) {
-      const uint32_t code = ((c < 4 ? sp.z : sp.w) >> (8 * (c & 3))) & 0xffu;
-      for (long long q = 0; q < (code >> 4); ++q)
-        add_tile((ty_base + (code & 15u) + q) * tiles_x + tx0 + c);
-    }
-  } else {
-    SplatF64 s = load_splat_f64(rec + r * 12);
-    if (strategy == 2) {
-      long long tx0, tx1, ty0, ty1;
-      aabb_rect(s, tiles_x, tiles_y, tx0, tx1, ty0, ty1);
-      for (long long tx = tx0; tx <= tx1; ++tx)
-        for (long long ty = ty0; ty <= ty1; ++ty) add_tile(ty * tiles_x + tx);
-    } else {
-      SnugRect box = snugbox(s, tiles_x, tiles_y);
-      if (box.tx0 <= box.tx1 && box.ty0 <= box.ty1) {
-        for (long long tx = box.tx0; tx <= box.tx1; ++tx) {
-          if (strategy == 1) {
-            const double rx0 = dsub((double)(16 * tx), s.mx);
-            for (long long ty = box.ty0; ty <= box.ty1; ++ty) {
-              const double ry0 = dsub((double)(16 * ty), s.my);
-              if (min_q_box(s, rx0, dadd(rx0, 16.0), ry0, dadd(ry0, 16.0)) <= s.t)
-                add_tile(ty * tiles_x + tx);
-            }
-          } else {
-            long long ty0, ty1;
-            const int nr = column_rows(s, box, tx, tiles_y, ty0, ty1);
-            for (int q = 0; q < nr; ++q) add_tile((ty0 + q) * tiles_x + tx);
-          }
-        }
+    for (int u = 0; u < 4; ++u) k[u] = e + u < e0 + c ? inv_perm[e + u] : 0u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) t[u] = e + u < e0 + c ? khi[2 * (long long)k[u]] : 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      ok[u] = e + u < e0 + c && (long long)k[u] - offsets[t[u]] < processed[t[u]];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (!ok[u]) continue;
+      const float2* sl = reinterpret_cast<const float2*>(slots + (long long)k[u] * TSR_GRAD2D_FLOATS);
+#pragma unroll
+      for (int j = 0; j < TSR_GRAD2D_FLOATS / 2; ++j) {
+        const float2 v = sl[j];
+        acc[2 * j] += v.x;
+        acc[2 * j + 1] += v.y;
       }
     }
   }
-  float* dst = grad2d + r * TSR_GRAD2D_FLOATS;
+  float* dst = grad2d + (long long)rank_row[q] * TSR_GRAD2D_FLOATS;
 #pragma unroll
   for (int j = 0; j < TSR_GRAD2D_FLOATS; ++j) dst[j] = acc[j];
 }
@@ -450,11 +423,12 @@ extern "C" int tsr_render_bwd_det(const float* rec, const int32_t* values, const
                                   const int64_t* ckpt_base, const float* grad_color,
                                   const float* grad_depth, const float* grad_final_T,
                                   unsigned long long* merges, float* slots, int32_t* processed,
-                                  const void* spans, const uint32_t* depth_bits,
+                                  const uint32_t* inv_perm, const uint32_t* rank_row,
+                                  const uint32_t* rank_count, const uint32_t* rank_off,
                                   const int64_t* keys, int64_t m, const int64_t* m_dev,
-                                  int32_t strategy, float* grad2d, void* stream) {
-  if (width <= 0 || height <= 0 || !grad_color || !merges || !slots || !processed || !spans ||
-      !depth_bits || !keys || m < 0 || !grad2d)
+                                  float* grad2d, void* stream) {
+  if (width <= 0 || height <= 0 || !grad_color || !merges || !slots || !processed ||
+      !inv_perm || !rank_row || !rank_count || !rank_off || !keys || m < 0 || !grad2d)
     return TSR_E_INVALID;
   if (ckpt && !ckpt_base) return TSR_E_INVALID;
   const int tx = tiles_of(width), ty = tiles_of(height);
@@ -467,8 +441,8 @@ extern "C" int tsr_render_bwd_det(const float* rec, const int32_t* values, const
   TSR_CHECK_LAUNCH();
   if (m > 0) {
     grad_reduce_kernel<<<(int)((m + 255) / 256), 256, 0, s>>>(
-        rec, (const uint4*)spans, depth_bits, keys, values, offsets, processed, slots, m, m_dev,
-        tx, ty, strategy, grad2d);
+        rank_row, rank_count, rank_off, inv_perm, keys, offsets, processed, slots, m, m_dev,
+        grad2d);
     TSR_CHECK_LAUNCH();
   }
   return TSR_OK;

@@ -76,6 +76,11 @@ struct IndexArgs {
   unsigned long long* ptot;          // kMaxGrid emitted pairs per CTA
   uint32_t* rank_cnt;                // M_cap pair count per rank
   uint4* rank_span;                  // M_cap column-span record per rank
+  // deterministic-merge outputs (nullable; see tsr_build_index_det):
+  uint32_t* inv_perm;                // P_cap: sorted position of each emission index
+  uint32_t* out_rank_row;            // M_cap: batch row of each depth rank
+  uint32_t* out_rank_count;          // M_cap: pairs of each rank
+  uint32_t* out_rank_off;            // M_cap: emission offset of each rank
   // zeroed by the per-call memset:
   uint32_t* hist4;                   // 4 x 256 depth-byte histogram
   unsigned int* bar;                 // kMaxBarriers arrival counters
@@ -255,7 +260,8 @@ __device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restr
                               long long hi, int shift, int bits,
                               const uint32_t* __restrict__ colscan_row,
                               const uint32_t* __restrict__ dtotal, SortSmem& sm,
-                              unsigned char* dyn) {
+                              unsigned char* dyn, const uint32_t* __restrict__ gather = nullptr,
+                              uint32_t* __restrict__ inv = nullptr) {
   constexpr bool kVals = true;
   K* s_keys = reinterpret_cast<K*>(dyn);
   uint32_t* s_vals = reinterpret_cast<uint32_t*>(dyn + kSub * sizeof(K));
@@ -321,7 +327,13 @@ __device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restr
       const uint32_t d = digit_of(k, shift, mask);
       const uint32_t g = sm.run[d] + (uint32_t)i - sm.lbase[d];
       kout[g] = k;
-      vout[g] = s_vals[i];
+      const uint32_t v = s_vals[i];
+      if (gather) {  // values carry emission indices: rows + inverse permutation
+        vout[g] = gather[v];
+        inv[v] = g;
+      } else {
+        vout[g] = v;
+      }
     }
     __syncthreads();
     sm.run[tid] += tot;
@@ -332,7 +344,8 @@ __device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restr
 template <typename K>
 __device__ void radix_pass(const IndexArgs& a, int& nb, const K* kin, const uint32_t* vin,
                            K* kout, uint32_t* vout, long long n, int shift, int bits,
-                           SortSmem& sm, unsigned char* dyn) {
+                           SortSmem& sm, unsigned char* dyn,
+                           const uint32_t* gather = nullptr, uint32_t* inv = nullptr) {
   const int G = gridDim.x, bid = blockIdx.x;
   long long lo, hi;
   slice(n, bid, G, lo, hi);
@@ -341,7 +354,7 @@ __device__ void radix_pass(const IndexArgs& a, int& nb, const K* kin, const uint
   colscan_phase(a.cnt, a.colscan, a.dtotal, G, sm);
   grid_barrier(a.bar + nb++, G);
   scatter_phase<K>(kin, vin, kout, vout, lo, hi, shift, bits, a.colscan + (long long)bid * kBins,
-                   a.dtotal, sm, dyn);
+                   a.dtotal, sm, dyn, gather, inv);
   grid_barrier(a.bar + nb++, G);
 }
 
@@ -387,6 +400,17 @@ __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, lon
     for (int k = 0; k < kEmitPer; ++k) {
       off[k] = run;
       run += cnt[k];
+    }
+    if (a.out_rank_row) {
+#pragma unroll
+      for (int k = 0; k < kEmitPer; ++k) {
+        const long long r = r0 + kEmitPer * tid + k;
+        if (r < rhi) {
+          a.out_rank_row[r] = rank_row(row_by_rank, r);
+          a.out_rank_count[r] = cnt[k];
+          a.out_rank_off[r] = (uint32_t)(O + off[k]);
+        }
+      }
     }
     for (uint32_t w0 = 0; w0 < total; w0 += kStage) {
       const uint32_t w1 = min(total, w0 + (uint32_t)kStage);
@@ -618,14 +642,20 @@ __global__ void __launch_bounds__(kSB, 3) build_index_kernel(IndexArgs a) {
   const long long np = clamp_ll(P, a.p_cap);
   unsigned long long* keys_out = reinterpret_cast<unsigned long long*>(a.keys);
   uint32_t* vals_out = reinterpret_cast<uint32_t*>(a.values);
+  // deterministic-merge mode: the passes carry emission indices (vin ==
+  // nullptr: value = input index) and the last one gathers the rows and
+  // writes the inverse permutation
+  const bool det = a.inv_perm != nullptr;
+  const uint32_t* v0 = det ? nullptr : a.pv0;
+  const uint32_t* gat = det ? a.pv0 : nullptr;
   if (a.tile_bits > 8) {  // two passes of ~half the tile bits each
     const int b1 = (a.tile_bits + 1) / 2, b2 = a.tile_bits - b1;
-    radix_pass<unsigned long long>(a, nb, a.pk0, a.pv0, a.pk1, a.pv1, np, 32, b1, sm, dyn);
+    radix_pass<unsigned long long>(a, nb, a.pk0, v0, a.pk1, a.pv1, np, 32, b1, sm, dyn);
     radix_pass<unsigned long long>(a, nb, a.pk1, a.pv1, keys_out, vals_out, np, 32 + b1, b2, sm,
-                                   dyn);
+                                   dyn, gat, a.inv_perm);
   } else {
-    radix_pass<unsigned long long>(a, nb, a.pk0, a.pv0, keys_out, vals_out, np, 32, a.tile_bits,
-                                   sm, dyn);
+    radix_pass<unsigned long long>(a, nb, a.pk0, v0, keys_out, vals_out, np, 32, a.tile_bits,
+                                   sm, dyn, gat, a.inv_perm);
   }
 
   // ---- 4. per-tile ranges (binning.py:156-157) + checkpoint bases
@@ -695,12 +725,13 @@ extern "C" size_t tsr_index_workspace(int64_t m_cap, int64_t p_cap) {
   return plan(m_cap, p_cap).bytes;
 }
 
-extern "C" int tsr_build_index(const float* rec, const uint32_t* depth_bits, const void* spans,
-                               const int32_t* counts, const int64_t* totals, int64_t m_cap,
-                               int64_t p_cap, int32_t width, int32_t height, int32_t strategy,
-                               int64_t* keys, int32_t* values, int64_t* offsets,
-                               int64_t* ckpt_base, int32_t* overflow, void* workspace,
-                               size_t workspace_bytes, void* stream) {
+static int build_index_impl(const float* rec, const uint32_t* depth_bits, const void* spans,
+                            const int32_t* counts, const int64_t* totals, int64_t m_cap,
+                            int64_t p_cap, int32_t width, int32_t height, int32_t strategy,
+                            int64_t* keys, int32_t* values, int64_t* offsets,
+                            int64_t* ckpt_base, int32_t* overflow, void* workspace,
+                            size_t workspace_bytes, uint32_t* inv_perm, uint32_t* rank_row_out,
+                            uint32_t* rank_count_out, uint32_t* rank_off_out, void* stream) {
   if (m_cap < 0 || p_cap < 0 || width <= 0 || height <= 0 || !totals || !offsets)
     return TSR_E_INVALID;
   if (p_cap >= (1ll << 32) || m_cap >= (1ll << 32)) return TSR_E_INVALID;  // u32 offsets
@@ -741,6 +772,10 @@ extern "C" int tsr_build_index(const float* rec, const uint32_t* depth_bits, con
   a.dtotal = (uint32_t*)(w + pl.dtotal);
   a.ptot = (unsigned long long*)(w + pl.ptot);
   a.rank_cnt = (uint32_t*)(w + pl.rank_cnt);
+  a.inv_perm = inv_perm;
+  a.out_rank_row = rank_row_out;
+  a.out_rank_count = rank_count_out;
+  a.out_rank_off = rank_off_out;
   a.rank_span = (uint4*)(w + pl.rank_span);
   a.hist4 = (uint32_t*)(w + pl.hist4);
   a.bar = (unsigned int*)(w + pl.bar);
@@ -766,4 +801,30 @@ extern "C" int tsr_build_index(const float* rec, const uint32_t* depth_bits, con
                                   kDynSmem, s) != cudaSuccess)
     return TSR_E_CUDA;
   return TSR_OK;
+}
+
+extern "C" int tsr_build_index(const float* rec, const uint32_t* depth_bits, const void* spans,
+                               const int32_t* counts, const int64_t* totals, int64_t m_cap,
+                               int64_t p_cap, int32_t width, int32_t height, int32_t strategy,
+                               int64_t* keys, int32_t* values, int64_t* offsets,
+                               int64_t* ckpt_base, int32_t* overflow, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  return build_index_impl(rec, depth_bits, spans, counts, totals, m_cap, p_cap, width, height,
+                          strategy, keys, values, offsets, ckpt_base, overflow, workspace,
+                          workspace_bytes, nullptr, nullptr, nullptr, nullptr, stream);
+}
+
+extern "C" int tsr_build_index_det(const float* rec, const uint32_t* depth_bits,
+                                   const void* spans, const int32_t* counts,
+                                   const int64_t* totals, int64_t m_cap, int64_t p_cap,
+                                   int32_t width, int32_t height, int32_t strategy,
+                                   int64_t* keys, int32_t* values, int64_t* offsets,
+                                   int64_t* ckpt_base, int32_t* overflow, void* workspace,
+                                   size_t workspace_bytes, uint32_t* inv_perm,
+                                   uint32_t* rank_row, uint32_t* rank_count, uint32_t* rank_off,
+                                   void* stream) {
+  if (!inv_perm || !rank_row || !rank_count || !rank_off) return TSR_E_INVALID;
+  return build_index_impl(rec, depth_bits, spans, counts, totals, m_cap, p_cap, width, height,
+                          strategy, keys, values, offsets, ckpt_base, overflow, workspace,
+                          workspace_bytes, inv_perm, rank_row, rank_count, rank_off, stream);
 }

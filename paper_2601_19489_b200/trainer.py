@@ -266,7 +266,7 @@ class TrainStep:
         from .binning import IndexBuffers
         from .forward import RenderTargets
         tiles = camera.tiles_x * camera.tiles_y
-        self.index = IndexBuffers(len(self.gset), p_cap, tiles)
+        self.index = IndexBuffers(len(self.gset), p_cap, tiles, det=self.deterministic)
         self.targets = RenderTargets(camera.height, camera.width, p_cap // 32 + tiles + 1)
         self.hw = (camera.height, camera.width)
         self.grad_color = torch.empty((camera.height, camera.width, 3), dtype=torch.float32,
@@ -333,9 +333,9 @@ class TrainStep:
                 out.final_T.data_ptr(), out.n_considered.data_ptr(), out.ckpt.data_ptr(),
                 idx.ckpt_base.data_ptr(), grad_color.data_ptr(), _lib.ptr(gd), _lib.ptr(gt),
                 self.merges.data_ptr(), self.slots.data_ptr(), self.processed.data_ptr(),
-                batch.spans.data_ptr(), batch.depth_bits.data_ptr(), idx.keys.data_ptr(),
-                self.grad2d.shape[0], self.scratch.totals.data_ptr(), self.cfg.strategy_id,
-                self.grad2d.data_ptr(), _lib.stream_handle()), "tsr_render_bwd_det")
+                *(t.data_ptr() for t in idx.det), idx.keys.data_ptr(), self.grad2d.shape[0],
+                self.scratch.totals.data_ptr(), self.grad2d.data_ptr(), _lib.stream_handle()),
+                "tsr_render_bwd_det")
             self._grad2d_clean = False
             self._mark(timer, "backward")
             return e

@@ -182,3 +182,29 @@ def test_bench_tiling_harness_matches_reference(case):
         assert abs(r.pairs - ref) <= max(2, 1e-5 * ref)
         assert r.millis > 0
     assert bench_tiling_csv(res).startswith("strategy,splats,pairs,millis\naabb,")
+
+
+def test_deterministic_index_outputs_are_consistent():
+    """tsr_build_index_det: the same keys/values/offsets as the plain build,
+    and a consistent emission permutation + per-rank (row, count, offset)."""
+    import torch
+    from paper_2601_19489_b200.binning import IndexBuffers, _ensure_counts, build_index_raw
+    b = random_splats(40_000, 6, 1280, 720)
+    db = dev_batch(b)
+    _ensure_counts(db, 0)
+    p, m = int(db.n_pairs), len(db)
+    plain = IndexBuffers(m, p, 80 * 45)
+    det = IndexBuffers(m, p, 80 * 45, det=True)
+    build_index_raw(db, 0, plain)
+    build_index_raw(db, 0, det)
+    assert torch.equal(plain.keys[:p], det.keys[:p])
+    assert torch.equal(plain.values[:p], det.values[:p])
+    assert torch.equal(plain.offsets, det.offsets)
+    inv, rrow, rcnt, roff = (t.cpu().numpy().astype(np.int64) for t in det.det)
+    inv, rrow, rcnt, roff = inv[:p], rrow[:m], rcnt[:m], roff[:m]
+    assert np.array_equal(np.sort(inv), np.arange(p))  # a permutation
+    assert rcnt.sum() == p and np.array_equal(np.sort(rrow), np.arange(m))
+    assert np.array_equal(roff, np.concatenate([[0], np.cumsum(rcnt)[:-1]]))
+    vals = det.values[:p].cpu().numpy()
+    owner = np.repeat(rrow, rcnt)  # emission index -> row
+    assert np.array_equal(vals[inv], owner)
