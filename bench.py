@@ -307,9 +307,16 @@ def gpu_arm(args):
 
     rank, world = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1)
     local = _env_int("LOCAL_RANK", 0)
+    # TSR_BENCH_BACKEND=gloo + more ranks than GPUs: a functional check of the
+    # N>1 path on a one-GPU box (ranks share devices); timings are not valid
+    backend = os.environ.get("TSR_BENCH_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     c = CONFIGS[args.config]
     params, cam, gt = make_scene(c["n"], c["width"], c["height"], seed=0,
                                  clustered=c["clustered"])
