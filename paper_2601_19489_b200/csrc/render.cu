@@ -93,16 +93,17 @@ __device__ __forceinline__ void blend_pair(const float4 g, const float4 c, const
   const float2 alpha = make_float2(fminf(kAlphaCap, raw.x), fminf(kAlphaCap, raw.y));
   const bool b0 = s.alive0 && (alpha.x >= kMinAlpha);
   const bool b1 = s.alive1 && (alpha.y >= kMinAlpha);
-  const float2 wt = __fmul2_rn(s.T, alpha);
-  s.strong0 = b0 && (wt.x >= kMinAlpha);
-  s.strong1 = b1 && (wt.y >= kMinAlpha);
-  const float2 w = make_float2(b0 ? wt.x : 0.f, b1 ? wt.y : 0.f);
+  // the non-blending pixel of a pair gets a = 0: w = T * 0 = 0 and
+  // T * (1 - 0) = T exactly, so no selects on w and T are needed
+  const float2 a = make_float2(b0 ? alpha.x : 0.f, b1 ? alpha.y : 0.f);
+  const float2 w = __fmul2_rn(s.T, a);
+  s.strong0 = b0 && (w.x >= kMinAlpha);
+  s.strong1 = b1 && (w.y >= kMinAlpha);
   s.Cr = __ffma2_rn(w, bc2(col.x), s.Cr);
   s.Cg = __ffma2_rn(w, bc2(col.y), s.Cg);
   s.Cb = __ffma2_rn(w, bc2(col.z), s.Cb);
   s.D = __ffma2_rn(w, bc2(col.w), s.D);
-  const float2 Tn = __fmul2_rn(s.T, __fadd2_rn(bc2(1.f), make_float2(-alpha.x, -alpha.y)));
-  s.T = make_float2(b0 ? Tn.x : s.T.x, b1 ? Tn.y : s.T.y);
+  s.T = __fmul2_rn(s.T, __fadd2_rn(bc2(1.f), make_float2(-a.x, -a.y)));
   s.nc0 += b0 ? 1 : 0;
   s.nc1 += b1 ? 1 : 0;
   s.ncons0 = s.alive0 ? pos + 1 : s.ncons0;
