@@ -230,14 +230,17 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
         const bool in0 = p < nc, in1 = p + 1 < nc;
         const bool part0 = in0 && (alpha.x >= kMinAlpha);
         const bool part1 = in1 && (alpha.y >= kMinAlpha);
-        const float2 om = __fadd2_rn(one, f2(-alpha.x, -alpha.y));
+        // non-participants get a = 0: w = T * 0 = 0 and T * (1 - 0) = T
+        // exactly (no selects on the chain; their 1/(1 - a) is unused)
+        const float2 a = f2(part0 ? alpha.x : 0.f, part1 ? alpha.y : 0.f);
+        const float2 om = __fadd2_rn(one, f2(-a.x, -a.y));
         float2 gc = __ffma2_rn(bc(pb.x), cr, __ffma2_rn(bc(pb.y), cg, __fmul2_rn(bc(pb.z), cbl)));
         if (kDepth) gc = __ffma2_rn(bc(pa.z), dep, gc);
         // scalar chain through the pair
-        const float w0 = part0 ? T_in * alpha.x : 0.f;
-        const float T1 = part0 ? T_in * om.x : T_in;
-        const float w1 = part1 ? T1 * alpha.y : 0.f;
-        T_out = part1 ? T1 * om.y : T1;
+        const float w0 = T_in * a.x;
+        const float T1 = T_in * om.x;
+        const float w1 = T1 * a.y;
+        T_out = T1 * om.y;
         const float num0 = fmaf(-w0, gc.x, R_in);
         const float num1 = fmaf(-w1, gc.y, num0);
         R_out = num1;
