@@ -33,6 +33,9 @@ CONFIGS = {
     "c1": dict(n=10_000, width=256, height=256, clustered=False),
     "c2": dict(n=1_000_000, width=1920, height=1080, clustered=False),
     "c3": dict(n=3_000_000, width=1920, height=1080, clustered=True),
+    # BASELINE configs[3]: a batch of 8 ring views per optimizer step, split
+    # across the GPUs (strong scaling), one gradient allreduce per step
+    "c4": dict(n=1_000_000, width=1920, height=1080, clustered=False, views=8),
 }
 METRIC = "train steps/sec (fwd+bwd+Adam) at 1M Gaussians 1080p"
 # FP32 lane-op counts per unit of work
@@ -290,8 +293,10 @@ def reference_arm(args):
 
 def _workload(name, n_gpus):
     c = CONFIGS[name]
+    views = (f"a batch of {c['views']} ring views per step split over the GPUs, one "
+             f"gradient allreduce" if c.get("views") else "one view per GPU per step")
     return (f"{c['n']:,} Gaussians{' (clustered depth)' if c['clustered'] else ''}, "
-            f"{c['width']}x{c['height']}, SH0, one view per GPU per step, "
+            f"{c['width']}x{c['height']}, SH0, {views}, "
             f"fwd+loss+bwd+Adam, {n_gpus} GPU(s)")
 
 
@@ -321,14 +326,23 @@ def gpu_arm(args):
     params, cam, gt = make_scene(c["n"], c["width"], c["height"], seed=0,
                                  clustered=c["clustered"])
     gset = ts.GaussianSet(**params)
-    ring = ring_poses(max(world, 1), 4.0, cam["fx"], c["width"], c["height"])
-    rc = ring[rank]
+    batch_views = c.get("views", 0)
+    ring = ring_poses(batch_views or max(world, 1), 4.0, cam["fx"], c["width"], c["height"])
+    rc = ring[rank % len(ring)]
     camera = ts.Camera(rc["fx"], rc["fy"], rc["cx"], rc["cy"], c["width"], c["height"],
                        rc["R"], rc["t"])
     gt_host = torch.from_numpy(np.asarray(gt, np.float32)).pin_memory()
     gt_dev = gt_host.to("cuda")
     cfg = ts.TrainConfig(max_iters=30_000)
-    if world == 1:
+    if batch_views:
+        from paper_2601_19489_b200.parallel import shard_views
+        mine = shard_views(batch_views, world, rank)
+        cams = [ts.Camera(ring[v]["fx"], ring[v]["fy"], ring[v]["cx"], ring[v]["cy"],
+                          c["width"], c["height"], ring[v]["R"], ring[v]["t"]) for v in mine]
+        stepper = ViewParallelStep(gset, cfg, extent=4.0)
+        run = lambda timer=None: stepper.step_views(cams, [gt_dev] * len(cams), timer)  # noqa
+        args.no_e2e = True
+    elif world == 1:
         # the step replays as one CUDA graph (captured during warm-up)
         stepper = ts.TrainStep(gset, cfg, extent=4.0, graphs=True,
                                deterministic=args.deterministic)
@@ -367,7 +381,7 @@ def gpu_arm(args):
         stepper.iteration = snap_it
         torch.cuda.synchronize()
 
-    graphs = world == 1
+    graphs = world == 1 and not batch_views
     clocks = ClockSampler(local)
     clocks.start()
     timer = {}
@@ -396,7 +410,7 @@ def gpu_arm(args):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = world * 1e3 / ms
+    value = (batch_views or world) * 1e3 / ms
 
     # work counters of the last timed step (for the roofline), outside the timed region
     batch, tiles, bufs = stepper.last_view()
@@ -497,10 +511,12 @@ def gpu_arm(args):
     line = {
         "metric": METRIC, "value": value, "unit": "view-steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong" if batch_views else "weak",
+        "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (canonical generator, SURVEY.md §8(d), seed 0)",
         "config": {"workload": f"{args.config}: " + _workload(args.config, world),
-                   "views_per_step": world, "parallelism": f"view-parallel dp{world}",
+                   "views_per_step": batch_views or world,
+                   "parallelism": f"view-parallel dp{world}",
                    "launch": "one CUDA graph replay per step" if world == 1 else "eager launches",
                    "merge": "deterministic (slots + emission-order row sums)"
                             if args.deterministic else "float atomics (FP32-tolerance)",

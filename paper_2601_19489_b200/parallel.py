@@ -42,7 +42,10 @@ def grad_numel(gset) -> int:
 
 
 def allreduce_grads(flat: torch.Tensor, group=None, deterministic: bool = False) -> torch.Tensor:
-    """Sum the flat gradient buffer over ranks (in place)."""
+    """Sum the flat gradient buffer over ranks (in place); a no-op without a
+    process group (one GPU)."""
+    if not dist.is_available() or not dist.is_initialized():
+        return flat
     world = dist.get_world_size(group)
     if world == 1:
         return flat
