@@ -13,7 +13,8 @@
 //   ssim_bwd: filter Q (the filter is symmetric, so its transpose is itself)
 //             and combine grad = (1-lam) sign(r-g)/N
 //                              - lam (F g_mu1 + 2 r F g_v1 + g F g_v12).
-//   finalize: one block reduces the partials to (E, l1, ssim).
+//   finalize: the first CTA of ssim_bwd reduces the forward's block partials
+//             (complete when it starts) to (E, l1, ssim) -- no third launch.
 #include <cuda_runtime.h>
 
 #include "tsr_common.cuh"
@@ -30,36 +31,46 @@ struct Win {
   float w[11];
 };
 
-// Load a (kLIn x kLIn) halo tile of one channel of an interleaved (H,W,3)
-// image (zero outside) into s[row][col] (row stride kLS).
-// All (up to 7) loads of a thread are issued before any shared store.
+__device__ __forceinline__ float2 bc2(float x) { return make_float2(x, x); }
+
+// Load a (kLIn x kLIn) halo tile of one channel of the interleaved (H,W,3)
+// images r and g (zero outside) into s[row][col] = (r, g) (row stride kLS).
+// All loads of a thread are issued before any shared store.
 constexpr int kHaloIters = (kLIn * kLIn + 255) / 256;
-__device__ __forceinline__ void load_halo(const float* __restrict__ img, int c, int H, int W,
-                                          int ty0, int tx0, float* s) {
-  float v[kHaloIters];
+__device__ __forceinline__ void load_halo2(const float* __restrict__ r, const float* __restrict__ g,
+                                           int c, int H, int W, int ty0, int tx0, float2* s) {
+  float2 v[kHaloIters];
   int dst[kHaloIters];
 #pragma unroll
   for (int k = 0; k < kHaloIters; ++k) {
     const int i = threadIdx.x + 256 * k;
     const int yy = i / kLIn, xx = i - yy * kLIn;
     const int y = ty0 - kLR + yy, x = tx0 - kLR + xx;
-    v[k] = 0.f;
+    v[k] = make_float2(0.f, 0.f);
     dst[k] = i < kLIn * kLIn ? yy * kLS + xx : -1;
-    if (i < kLIn * kLIn && y >= 0 && y < H && x >= 0 && x < W)
-      v[k] = __ldg(img + ((long long)y * W + x) * 3 + c);
+    if (i < kLIn * kLIn && y >= 0 && y < H && x >= 0 && x < W) {
+      const long long o = ((long long)y * W + x) * 3 + c;
+      v[k] = make_float2(__ldg(r + o), __ldg(g + o));
+    }
   }
 #pragma unroll
   for (int k = 0; k < kHaloIters; ++k)
     if (dst[k] >= 0) s[dst[k]] = v[k];
 }
 
+// The two images (and in the backward the first two SSIM sources) travel as
+// one packed FP32x2 pair through both filter passes: each tap is one FFMA2
+// for (mu1, mu2), one for (E[r^2], E[g^2]) and one scalar FFMA for E[rg]
+// (5 FFMA before); every lane of a packed op is an IEEE FMA, so the sums are
+// bit-identical to the scalar form.
 __global__ void __launch_bounds__(256, 4) ssim_fwd_kernel(const float* __restrict__ r,
                                                        const float* __restrict__ g, int H, int W,
-                                                       float inv_n, float* __restrict__ Q,
+                                                       float inv_n, float2* __restrict__ Q01,
+                                                       float* __restrict__ Q2,
                                                        double* __restrict__ partials, Win win) {
-  __shared__ __align__(16) float s_r[kLIn * kLS];
-  __shared__ __align__(16) float s_g[kLIn * kLS];
-  __shared__ float s_h[5][kLIn][kLT + 1];
+  __shared__ __align__(16) float2 s_rg[kLIn * kLS];
+  __shared__ __align__(16) float2 s_h2[2][kLIn][kLT + 1];  // (mu1, mu2), (E11, E22)
+  __shared__ float s_h1[kLIn][kLT + 1];                    // E12
   __shared__ double s_red[2][8];
   const int tid = threadIdx.x;
   // one CTA per (tile, channel); the 3 channel CTAs of a tile are adjacent
@@ -69,67 +80,68 @@ __global__ void __launch_bounds__(256, 4) ssim_fwd_kernel(const float* __restric
   const long long HW = (long long)H * W;
   double acc_ssim = 0.0, acc_l1 = 0.0;
   {
-    load_halo(r, c, H, W, ty0, tx0, s_r);
-    load_halo(g, c, H, W, ty0, tx0, s_g);
+    load_halo2(r, g, c, H, W, ty0, tx0, s_rg);
     __syncthreads();
     // horizontal: item = (row, 2 consecutive output cols); 42 x 16 items
     for (int it = tid; it < kLIn * (kLT / 2); it += 256) {
       const int row = it >> 4, c0 = (it & 15) * 2;
-      float a[12], b[12];
+      float2 ab[12];
       {
-        const float2* pr = reinterpret_cast<const float2*>(s_r + row * kLS + c0);
-        const float2* pg = reinterpret_cast<const float2*>(s_g + row * kLS + c0);
+        const float4* pr = reinterpret_cast<const float4*>(s_rg + row * kLS + c0);
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
-          const float2 x = pr[k], y = pg[k];
-          a[2 * k] = x.x; a[2 * k + 1] = x.y;
-          b[2 * k] = y.x; b[2 * k + 1] = y.y;
+          const float4 x = pr[k];
+          ab[2 * k] = make_float2(x.x, x.y);
+          ab[2 * k + 1] = make_float2(x.z, x.w);
         }
       }
-      float m1[2] = {0, 0}, m2[2] = {0, 0}, q11[2] = {0, 0}, q22[2] = {0, 0}, q12[2] = {0, 0};
+      float2 m[2] = {bc2(0.f), bc2(0.f)}, q[2] = {bc2(0.f), bc2(0.f)};
+      float q12[2] = {0.f, 0.f};
 #pragma unroll
       for (int k = 0; k < 12; ++k) {
-        const float ak = a[k], bk = b[k], aa = ak * ak, bb = bk * bk, ab = ak * bk;
+        const float2 sq = __fmul2_rn(ab[k], ab[k]);
+        const float p = __fmul_rn(ab[k].x, ab[k].y);
 #pragma unroll
         for (int o = 0; o < 2; ++o) {
           const int tap = k - o;
           if (tap >= 0 && tap < 11) {
             const float w = win.w[tap];
-            m1[o] = fmaf(w, ak, m1[o]);
-            m2[o] = fmaf(w, bk, m2[o]);
-            q11[o] = fmaf(w, aa, q11[o]);
-            q22[o] = fmaf(w, bb, q22[o]);
-            q12[o] = fmaf(w, ab, q12[o]);
+            m[o] = __ffma2_rn(bc2(w), ab[k], m[o]);
+            q[o] = __ffma2_rn(bc2(w), sq, q[o]);
+            q12[o] = fmaf(w, p, q12[o]);
           }
         }
       }
 #pragma unroll
       for (int o = 0; o < 2; ++o) {
-        s_h[0][row][c0 + o] = m1[o];
-        s_h[1][row][c0 + o] = m2[o];
-        s_h[2][row][c0 + o] = q11[o];
-        s_h[3][row][c0 + o] = q22[o];
-        s_h[4][row][c0 + o] = q12[o];
+        s_h2[0][row][c0 + o] = m[o];
+        s_h2[1][row][c0 + o] = q[o];
+        s_h1[row][c0 + o] = q12[o];
       }
     }
     __syncthreads();
     // vertical: item = (col, 4 consecutive output rows); 32 x 8 items = 256
     {
       const int col = tid & 31, r0 = (tid >> 5) * 4;
-      float v[5][4];
+      float2 vm[4], vq[4];
+      float v12[4];
 #pragma unroll
-      for (int q = 0; q < 5; ++q)
-#pragma unroll
-        for (int o = 0; o < 4; ++o) v[q][o] = 0.f;
+      for (int o = 0; o < 4; ++o) {
+        vm[o] = vq[o] = bc2(0.f);
+        v12[o] = 0.f;
+      }
 #pragma unroll
       for (int k = 0; k < 14; ++k) {
+        const float2 hm = s_h2[0][r0 + k][col], hq = s_h2[1][r0 + k][col];
+        const float h12 = s_h1[r0 + k][col];
 #pragma unroll
-        for (int q = 0; q < 5; ++q) {
-          const float h = s_h[q][r0 + k][col];
-#pragma unroll
-          for (int o = 0; o < 4; ++o) {
-            const int tap = k - o;
-            if (tap >= 0 && tap < 11) v[q][o] = fmaf(win.w[tap], h, v[q][o]);
+        for (int o = 0; o < 4; ++o) {
+          const int tap = k - o;
+          if (tap >= 0 && tap < 11) {
+            const float w = win.w[tap];
+            vm[o] = __ffma2_rn(bc2(w), hm, vm[o]);
+            vq[o] = __ffma2_rn(bc2(w), hq, vq[o]);
+            v12[o] = fmaf(w, h12, v12[o]);
           }
         }
       }
@@ -138,8 +150,8 @@ __global__ void __launch_bounds__(256, 4) ssim_fwd_kernel(const float* __restric
       for (int o = 0; o < 4; ++o) {
         const int y = ty0 + r0 + o, x = tx0 + col;
         if (y >= H || x >= W) continue;
-        const float mu1 = v[0][o], mu2 = v[1][o];
-        const float s1 = v[2][o] - mu1 * mu1, s2 = v[3][o] - mu2 * mu2, s12 = v[4][o] - mu1 * mu2;
+        const float mu1 = vm[o].x, mu2 = vm[o].y;
+        const float s1 = vq[o].x - mu1 * mu1, s2 = vq[o].y - mu2 * mu2, s12 = v12[o] - mu1 * mu2;
         const float A1 = 2.f * mu1 * mu2 + C1, A2 = 2.f * s12 + C2;
         const float B1 = mu1 * mu1 + mu2 * mu2 + C1, B2 = s1 + s2 + C2;
         const float inv_b = 1.0f / (B1 * B2);
@@ -147,12 +159,11 @@ __global__ void __launch_bounds__(256, 4) ssim_fwd_kernel(const float* __restric
         const float dA1 = inv_n * A2 * inv_b, dA2 = inv_n * A1 * inv_b;
         const float dB1 = -inv_n * map * (B2 * inv_b), dB2 = -inv_n * map * (B1 * inv_b);
         const long long pix = (long long)y * W + x;
-        Q[(c * 3 + 0) * HW + pix] = 2.f * mu2 * (dA1 - dA2) + 2.f * mu1 * (dB1 - dB2);
-        Q[(c * 3 + 1) * HW + pix] = dB2;
-        Q[(c * 3 + 2) * HW + pix] = 2.f * dA2;
+        Q01[c * HW + pix] = make_float2(2.f * mu2 * (dA1 - dA2) + 2.f * mu1 * (dB1 - dB2), dB2);
+        Q2[c * HW + pix] = 2.f * dA2;
         acc_ssim += (double)map;
-        const int yy = r0 + o + kLR, xx = col + kLR;
-        acc_l1 += (double)fabsf(s_r[yy * kLS + xx] - s_g[yy * kLS + xx]);
+        const float2 rg = s_rg[(r0 + o + kLR) * kLS + col + kLR];
+        acc_l1 += (double)fabsf(rg.x - rg.y);
       }
     }
     __syncthreads();
@@ -175,103 +186,25 @@ __global__ void __launch_bounds__(256, 4) ssim_fwd_kernel(const float* __restric
   }
 }
 
-__global__ void __launch_bounds__(256, 4) ssim_bwd_kernel(const float* __restrict__ r,
-                                                       const float* __restrict__ g, int H, int W,
-                                                       float lam, float inv_n,
-                                                       const float* __restrict__ Q,
-                                                       float* __restrict__ grad, Win win) {
-  __shared__ __align__(16) float s_q[3][kLIn * kLS];
-  __shared__ float s_h[3][kLIn][kLT + 1];
-  const int tid = threadIdx.x;
-  const int c = blockIdx.x % 3;
-  const int tx0 = (blockIdx.x / 3) * kLT, ty0 = blockIdx.y * kLT;
-  const long long HW = (long long)H * W;
-  {
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      float v[kHaloIters];
-      int dst[kHaloIters];
-#pragma unroll
-      for (int k = 0; k < kHaloIters; ++k) {
-        const int i = tid + 256 * k;
-        const int yy = i / kLIn, xx = i - yy * kLIn;
-        const int y = ty0 - kLR + yy, x = tx0 - kLR + xx;
-        v[k] = 0.f;
-        dst[k] = i < kLIn * kLIn ? yy * kLS + xx : -1;
-        if (i < kLIn * kLIn && y >= 0 && y < H && x >= 0 && x < W)
-          v[k] = __ldg(Q + (c * 3 + q) * HW + (long long)y * W + x);
-      }
-#pragma unroll
-      for (int k = 0; k < kHaloIters; ++k)
-        if (dst[k] >= 0) s_q[q][dst[k]] = v[k];
-    }
-    __syncthreads();
-    for (int it = tid; it < kLIn * (kLT / 2); it += 256) {
-      const int row = it >> 4, c0 = (it & 15) * 2;
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        float a[12];
-        const float2* pq = reinterpret_cast<const float2*>(s_q[q] + row * kLS + c0);
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          const float2 x = pq[k];
-          a[2 * k] = x.x; a[2 * k + 1] = x.y;
-        }
-        float h[2] = {0, 0};
-#pragma unroll
-        for (int k = 0; k < 12; ++k)
-#pragma unroll
-          for (int o = 0; o < 2; ++o) {
-            const int tap = k - o;
-            if (tap >= 0 && tap < 11) h[o] = fmaf(win.w[tap], a[k], h[o]);
-          }
-#pragma unroll
-        for (int o = 0; o < 2; ++o) s_h[q][row][c0 + o] = h[o];
-      }
-    }
-    __syncthreads();
-    {
-      const int col = tid & 31, r0 = (tid >> 5) * 4;
-      float v[3][4];
-#pragma unroll
-      for (int q = 0; q < 3; ++q)
-#pragma unroll
-        for (int o = 0; o < 4; ++o) v[q][o] = 0.f;
-#pragma unroll
-      for (int k = 0; k < 14; ++k)
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          const float h = s_h[q][r0 + k][col];
-#pragma unroll
-          for (int o = 0; o < 4; ++o) {
-            const int tap = k - o;
-            if (tap >= 0 && tap < 11) v[q][o] = fmaf(win.w[tap], h, v[q][o]);
-          }
-        }
-#pragma unroll
-      for (int o = 0; o < 4; ++o) {
-        const int y = ty0 + r0 + o, x = tx0 + col;
-        if (y >= H || x >= W) continue;
-        const long long p = ((long long)y * W + x) * 3 + c;
-        const float rv = r[p], gv = g[p];
-        const float d = rv - gv;
-        const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
-        const float gs = v[0][o] + v[1][o] * 2.f * rv + v[2][o] * gv;
-        grad[p] = (1.f - lam) * sgn * inv_n - lam * gs;
-      }
-    }
-    __syncthreads();
-  }
-}
-
-__global__ void __launch_bounds__(256) loss_finalize_kernel(const double* __restrict__ partials,
-                                                            int n_blocks, double inv_n,
-                                                            float lam, float* __restrict__ out) {
+// (E, l1, ssim) from the forward's block partials, in a fixed order (the
+// first CTA of ssim_bwd runs it: the partials are complete when it starts).
+__device__ void loss_finalize(const double* __restrict__ partials, int n_blocks, double inv_n,
+                              float lam, float* __restrict__ out) {
   __shared__ double s[2][8];
   double a = 0.0, b = 0.0;
-  for (int i = threadIdx.x; i < n_blocks; i += 256) {
-    a += partials[2 * i];
-    b += partials[2 * i + 1];
+  constexpr int kU = 8;
+  for (int i0 = threadIdx.x; i0 < n_blocks; i0 += 256 * kU) {
+    double2 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + 256 * u;
+      v[u] = i < n_blocks ? reinterpret_cast<const double2*>(partials)[i] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      a += v[u].x;
+      b += v[u].y;
+    }
   }
   for (int d = 16; d > 0; d >>= 1) {
     a += __shfl_xor_sync(0xffffffffu, a, d);
@@ -293,6 +226,119 @@ __global__ void __launch_bounds__(256) loss_finalize_kernel(const double* __rest
     out[0] = (float)((1.0 - lam) * l1 + lam * (1.0 - ss));
     out[1] = (float)l1;
     out[2] = (float)ss;
+  }
+}
+
+__global__ void __launch_bounds__(256, 4) ssim_bwd_kernel(
+    const float* __restrict__ r, const float* __restrict__ g, int H, int W, float lam,
+    float inv_n, const float2* __restrict__ Q01, const float* __restrict__ Q2,
+    float* __restrict__ grad, Win win, const double* __restrict__ partials, int n_blocks,
+    double inv_n_d, float* __restrict__ out3) {
+  __shared__ __align__(16) float2 s_q2[kLIn * kLS];
+  __shared__ __align__(16) float s_q1[kLIn * kLS];
+  __shared__ float2 s_h2[kLIn][kLT + 1];
+  __shared__ float s_h1[kLIn][kLT + 1];
+  const int tid = threadIdx.x;
+  const int c = blockIdx.x % 3;
+  const int tx0 = (blockIdx.x / 3) * kLT, ty0 = blockIdx.y * kLT;
+  const long long HW = (long long)H * W;
+  if (blockIdx.x == 0 && blockIdx.y == 0)
+    loss_finalize(partials, n_blocks, inv_n_d, lam, out3);
+  {
+    float2 v2[kHaloIters];
+    float v1[kHaloIters];
+    int dst[kHaloIters];
+#pragma unroll
+    for (int k = 0; k < kHaloIters; ++k) {
+      const int i = tid + 256 * k;
+      const int yy = i / kLIn, xx = i - yy * kLIn;
+      const int y = ty0 - kLR + yy, x = tx0 - kLR + xx;
+      v2[k] = bc2(0.f);
+      v1[k] = 0.f;
+      dst[k] = i < kLIn * kLIn ? yy * kLS + xx : -1;
+      if (i < kLIn * kLIn && y >= 0 && y < H && x >= 0 && x < W) {
+        const long long o = c * HW + (long long)y * W + x;
+        v2[k] = __ldg(Q01 + o);
+        v1[k] = __ldg(Q2 + o);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kHaloIters; ++k)
+      if (dst[k] >= 0) {
+        s_q2[dst[k]] = v2[k];
+        s_q1[dst[k]] = v1[k];
+      }
+    __syncthreads();
+    for (int it = tid; it < kLIn * (kLT / 2); it += 256) {
+      const int row = it >> 4, c0 = (it & 15) * 2;
+      float2 a2[12];
+      float a1[12];
+      {
+        const float4* p2 = reinterpret_cast<const float4*>(s_q2 + row * kLS + c0);
+        const float2* p1 = reinterpret_cast<const float2*>(s_q1 + row * kLS + c0);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          const float4 x = p2[k];
+          const float2 y = p1[k];
+          a2[2 * k] = make_float2(x.x, x.y);
+          a2[2 * k + 1] = make_float2(x.z, x.w);
+          a1[2 * k] = y.x;
+          a1[2 * k + 1] = y.y;
+        }
+      }
+      float2 h2[2] = {bc2(0.f), bc2(0.f)};
+      float h1[2] = {0.f, 0.f};
+#pragma unroll
+      for (int k = 0; k < 12; ++k)
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          const int tap = k - o;
+          if (tap >= 0 && tap < 11) {
+            h2[o] = __ffma2_rn(bc2(win.w[tap]), a2[k], h2[o]);
+            h1[o] = fmaf(win.w[tap], a1[k], h1[o]);
+          }
+        }
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        s_h2[row][c0 + o] = h2[o];
+        s_h1[row][c0 + o] = h1[o];
+      }
+    }
+    __syncthreads();
+    {
+      const int col = tid & 31, r0 = (tid >> 5) * 4;
+      float2 v2o[4];
+      float v1o[4];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        v2o[o] = bc2(0.f);
+        v1o[o] = 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 14; ++k) {
+        const float2 h2 = s_h2[r0 + k][col];
+        const float h1 = s_h1[r0 + k][col];
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+          const int tap = k - o;
+          if (tap >= 0 && tap < 11) {
+            v2o[o] = __ffma2_rn(bc2(win.w[tap]), h2, v2o[o]);
+            v1o[o] = fmaf(win.w[tap], h1, v1o[o]);
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        const int y = ty0 + r0 + o, x = tx0 + col;
+        if (y >= H || x >= W) continue;
+        const long long p = ((long long)y * W + x) * 3 + c;
+        const float rv = r[p], gv = g[p];
+        const float d = rv - gv;
+        const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+        const float gs = v2o[o].x + v2o[o].y * 2.f * rv + v1o[o] * gv;
+        grad[p] = (1.f - lam) * sgn * inv_n - lam * gs;
+      }
+    }
   }
 }
 
@@ -332,16 +378,16 @@ extern "C" int tsr_photometric(const float* rendered, const float* gt, int32_t h
   cudaStream_t s = (cudaStream_t)stream;
   dim3 grid(3 * ((width + kLT - 1) / kLT), (height + kLT - 1) / kLT);
   const int n_blocks = grid.x * grid.y;
-  float* Q = (float*)workspace;
+  float* Q = (float*)workspace;  // planar (Q0, Q1) pairs [3][H][W] + Q2 [3][H][W]
+  float2* Q01 = reinterpret_cast<float2*>(Q);
+  float* Q2 = Q + 6 * (size_t)height * width;
   double* partials = (double*)((char*)workspace + q_bytes(height, width));
   const double n = 3.0 * (double)height * width;
-  ssim_fwd_kernel<<<grid, 256, 0, s>>>(rendered, gt, height, width, (float)(1.0 / n), Q,
+  ssim_fwd_kernel<<<grid, 256, 0, s>>>(rendered, gt, height, width, (float)(1.0 / n), Q01, Q2,
                                        partials, win);
   TSR_CHECK_LAUNCH();
-  ssim_bwd_kernel<<<grid, 256, 0, s>>>(rendered, gt, height, width, lam, (float)(1.0 / n), Q,
-                                       grad, win);
-  TSR_CHECK_LAUNCH();
-  loss_finalize_kernel<<<1, 256, 0, s>>>(partials, n_blocks, 1.0 / n, lam, out3);
+  ssim_bwd_kernel<<<grid, 256, 0, s>>>(rendered, gt, height, width, lam, (float)(1.0 / n), Q01,
+                                       Q2, grad, win, partials, n_blocks, 1.0 / n, out3);
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }

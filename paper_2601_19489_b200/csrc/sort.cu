@@ -322,17 +322,29 @@ __device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restr
     }
     __syncthreads();
     const int n_here = (int)(hi - base < kSub ? hi - base : kSub);
-    for (int i = tid; i < n_here; i += kSB) {
-      const K k = s_keys[i];
-      const uint32_t d = digit_of(k, shift, mask);
-      const uint32_t g = sm.run[d] + (uint32_t)i - sm.lbase[d];
-      kout[g] = k;
-      const uint32_t v = s_vals[i];
-      if (gather) {  // values carry emission indices: rows + inverse permutation
-        vout[g] = gather[v];
-        inv[v] = g;
-      } else {
-        vout[g] = v;
+    {
+      // all kItems items of the thread in flight at once (the det-mode
+      // gathers are random loads)
+      K k[kItems];
+      uint32_t v[kItems], g[kItems];
+#pragma unroll
+      for (int r = 0; r < kItems; ++r) {
+        const int i = tid + r * kSB;
+        k[r] = i < n_here ? s_keys[i] : (K)0;
+        v[r] = i < n_here ? s_vals[i] : 0u;
+        const uint32_t d = digit_of(k[r], shift, mask);
+        g[r] = sm.run[d] + (uint32_t)i - sm.lbase[d];
+      }
+      uint32_t gv[kItems];
+#pragma unroll
+      for (int r = 0; r < kItems; ++r)
+        gv[r] = (gather && tid + r * kSB < n_here) ? gather[v[r]] : v[r];
+#pragma unroll
+      for (int r = 0; r < kItems; ++r) {
+        if (tid + r * kSB >= n_here) continue;
+        kout[g[r]] = k[r];
+        vout[g[r]] = gv[r];
+        if (gather) inv[v[r]] = g[r];  // values carry emission indices: inverse permutation
       }
     }
     __syncthreads();
@@ -659,15 +671,28 @@ __global__ void __launch_bounds__(kSB, 3) build_index_kernel(IndexArgs a) {
   }
 
   // ---- 4. per-tile ranges (binning.py:156-157) + checkpoint bases
+  // 8 boundary tests per thread in flight per round (independent loads)
   const int* khi = reinterpret_cast<const int*>(a.keys) + 1;  // tile = high word
-  for (long long i = (long long)bid * kSB + tid; i <= np; i += (long long)G * kSB) {
-    const long long cur = i < np ? khi[2 * i] : (long long)a.n_tiles;
-    const long long prev = i == 0 ? -1 : khi[2 * (i - 1)];
-    for (long long t = prev + 1; t <= cur; ++t) {
-      a.offsets[t] = i;
-      if (a.ckpt_base) a.ckpt_base[t] = i >> 5;
+  constexpr int kR = 8;
+  for (long long i0 = (long long)bid * kSB * kR + tid; i0 <= np; i0 += (long long)G * kSB * kR) {
+    int cur[kR], prev[kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      const long long i = i0 + (long long)r * kSB;
+      cur[r] = i < np ? khi[2 * i] : a.n_tiles;
+      prev[r] = (i == 0 || i > np) ? -1 : khi[2 * (i - 1)];
+    }
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      const long long i = i0 + (long long)r * kSB;
+      if (i > np) continue;
+      for (long long t = (long long)prev[r] + 1; t <= cur[r]; ++t) {
+        a.offsets[t] = i;
+        if (a.ckpt_base) a.ckpt_base[t] = i >> 5;
+      }
     }
   }
+  TSR_TRACE_AT(47);
 }
 
 // -------------------------------------------------------------- planning --

@@ -445,8 +445,9 @@ class TrainStep:
 
     def kernels_per_step(self) -> int:
         """Our kernel launches per step: K1a, K1b; K2 (one persistent
-        cooperative kernel); K3; loss (fwd, bwd, finalize); K4; fused K4b+K5."""
-        return 2 + 1 + 1 + 3 + 1 + 1
+        cooperative kernel); K3; loss (fwd, bwd + finalize); K4; fused K4b+K5
+        (+ the row reduction in deterministic mode)."""
+        return 2 + 1 + 1 + 2 + 1 + 1 + (1 if self.deterministic else 0)
 
     def last_view(self):
         """(batch, TileIndex, RenderBuffers) views of the last step (synchronises)."""

@@ -208,3 +208,22 @@ def test_deterministic_index_outputs_are_consistent():
     vals = det.values[:p].cpu().numpy()
     owner = np.repeat(rrow, rcnt)  # emission index -> row
     assert np.array_equal(vals[inv], owner)
+
+
+@pytest.mark.parametrize("distinct_depths", [0, 5])
+def test_crowded_tiles_and_depth_ties(distinct_depths):
+    """Crowded tiles (> 8k pairs) with continuous depths and with only a few
+    distinct depths (ties resolved by row: the reference's stable order)."""
+    import paper_2601_19489_b200 as ts
+    b = random_splats(60_000, 9, 256, 192, minor=(0.5, 2.0), anisotropy=(1.0, 3.0))
+    rng = np.random.default_rng(1)
+    b["means2d"][:40_000] = np.asarray(rng.normal((100.0, 90.0), (9.0, 7.0), (40_000, 2)),
+                                       np.float32).astype(np.float64)
+    if distinct_depths:
+        b["depths"] = np.asarray(np.round(b["depths"] / 10 * distinct_depths) + 1.0,
+                                 np.float32).astype(np.float64)
+    ref = O.bin_sequential(b)
+    counts = np.diff(ref["offsets"])
+    assert counts.max() > 8192
+    for fn in (ts.bin_sequential, ts.bin_load_balanced):
+        assert_index_equal(fn(dev_batch(b)), ref)

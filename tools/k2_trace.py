@@ -29,6 +29,6 @@ for _ in range(5):
     t = np.array(buf[:33], dtype=np.int64)
     n = int(np.count_nonzero(t[1:]))
     print("K2 phase ends (us from start):", [round((x - t[0]) / 1e3, 1) for x in t[1:1 + n]])
-    e = np.array(buf[40:47], dtype=np.int64)
-    print("   emission CTA0 (gathers, scan, window-expand..., rewalk, end, expand, copy):",
+    e = np.array(buf[40:48], dtype=np.int64)
+    print("   emission CTA0 (gathers, scan, window-expand..., rewalk, end, expand, copy, kernel end):",
           [round((x - t[0]) / 1e3, 1) for x in e])
