@@ -244,6 +244,17 @@ __global__ void __launch_bounds__(256, 4) ssim_bwd_kernel(
   const long long HW = (long long)H * W;
   if (blockIdx.x == 0 && blockIdx.y == 0)
     loss_finalize(partials, n_blocks, inv_n_d, lam, out3);
+  // the epilogue's r, g values: loads issued now, consumed after the filters
+  const int col = tid & 31, r0 = (tid >> 5) * 4;
+  float rv[4], gv[4];
+#pragma unroll
+  for (int o = 0; o < 4; ++o) {
+    const int y = ty0 + r0 + o, x = tx0 + col;
+    const bool in = y < H && x < W;
+    const long long p = ((long long)y * W + x) * 3 + c;
+    rv[o] = in ? __ldg(r + p) : 0.f;
+    gv[o] = in ? __ldg(g + p) : 0.f;
+  }
   {
     float2 v2[kHaloIters];
     float v1[kHaloIters];
@@ -306,7 +317,6 @@ __global__ void __launch_bounds__(256, 4) ssim_bwd_kernel(
     }
     __syncthreads();
     {
-      const int col = tid & 31, r0 = (tid >> 5) * 4;
       float2 v2o[4];
       float v1o[4];
 #pragma unroll
@@ -332,10 +342,9 @@ __global__ void __launch_bounds__(256, 4) ssim_bwd_kernel(
         const int y = ty0 + r0 + o, x = tx0 + col;
         if (y >= H || x >= W) continue;
         const long long p = ((long long)y * W + x) * 3 + c;
-        const float rv = r[p], gv = g[p];
-        const float d = rv - gv;
+        const float d = rv[o] - gv[o];
         const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
-        const float gs = v2o[o].x + v2o[o].y * 2.f * rv + v1o[o] * gv;
+        const float gs = v2o[o].x + v2o[o].y * 2.f * rv[o] + v1o[o] * gv[o];
         grad[p] = (1.f - lam) * sgn * inv_n - lam * gs;
       }
     }
