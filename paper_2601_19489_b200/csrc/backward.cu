@@ -225,11 +225,16 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
         const float2 dxx = __fmul2_rn(dx, dx), dxy = __fmul2_rn(dx, dy), dyy = __fmul2_rn(dy, dy);
         const float2 qs = __ffma2_rn(ca, dxx, __ffma2_rn(cb, dxy, __fmul2_rn(cc, dyy)));
         const float2 gauss = f2(fast_exp2(qs.x), fast_exp2(qs.y));
-        const float2 raw = __fmul2_rn(op, gauss);
+        // two scalar multiplies (bitwise the packed product): the opacity
+        // pair does not live in an aligned register pair, and a packed
+        // multiply would copy it every step
+        const float2 raw = f2(__fmul_rn(op.x, gauss.x), __fmul_rn(op.y, gauss.y));
         const float2 alpha = f2(fminf(kAlphaCap, raw.x), fminf(kAlphaCap, raw.y));
+        // predicates chained so each costs one compare (alpha >= 1/255 <=>
+        // raw >= 1/255 since the cap is above it)
         const bool in0 = p < nc, in1 = p + 1 < nc;
-        const bool part0 = in0 && (alpha.x >= kMinAlpha);
-        const bool part1 = in1 && (alpha.y >= kMinAlpha);
+        const bool part0 = in0 & (alpha.x >= kMinAlpha);
+        const bool part1 = in1 & (alpha.y >= kMinAlpha);
         // non-participants get a = 0: w = T * 0 = 0 and T * (1 - 0) = T
         // exactly (no selects on the chain; their 1/(1 - a) is unused)
         const float2 a = f2(part0 ? alpha.x : 0.f, part1 ? alpha.y : 0.f);
@@ -248,8 +253,8 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
         const float2 dLda = f2(fmaf(-num0, rcp.x, T_in * gc.x), fmaf(-num1, rcp.y, T1 * gc.y));
         // uncapped participants only (backward.py:64,72): 1/255 <= raw <= 0.99
         // (then alpha == raw); x(-1/2) folded into the merge
-        const bool l0 = in0 && raw.x >= kMinAlpha && raw.x <= kAlphaCap;
-        const bool l1 = in1 && raw.y >= kMinAlpha && raw.y <= kAlphaCap;
+        const bool l0 = part0 & (raw.x <= kAlphaCap);
+        const bool l1 = part1 & (raw.y <= kAlphaCap);
         const float2 ld = f2(l0 ? dLda.x : 0.f, l1 ? dLda.y : 0.f);
         const float2 gq = __fmul2_rn(ld, alpha);
         acc_a = __ffma2_rn(gq, dxx, acc_a);
