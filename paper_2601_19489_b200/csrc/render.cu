@@ -64,11 +64,18 @@ __device__ __forceinline__ float2 bc2(float x) { return make_float2(x, x); }
 // lane, branch-free (predicated): the warp executes it in lockstep.  dx is
 // shared; every other per-pixel operation is one packed FP32x2 instruction.
 // The alpha sequence is eval_alpha's, so K4 reproduces these alphas bitwise.
+// Liveness is T itself: a pixel is alive iff T >= 1e-4.  T starts at 1 and
+// only changes by blending, blending needs a live pixel, and the pixel dies
+// at the first blend that takes T below 1e-4 (forward.py:138), after which T
+// is frozen below the threshold -- so (T >= 1e-4) is exactly the reference's
+// alive flag.  Pixels outside the image start at T = 0 (never written).
 struct PixPair {
   float2 T, Cr, Cg, Cb, D;
-  int nc0, nc1, ncons0, ncons1;
-  bool alive0, alive1;
+  float2 nc;  // blends so far (exact small integers; one packed add per entry)
+  int ncons0, ncons1;
   bool strong0, strong1;  // last blend was a strong contribution (w >= 1/255)
+  __device__ __forceinline__ bool alive0() const { return T.x >= kTTerminate; }
+  __device__ __forceinline__ bool alive1() const { return T.y >= kTTerminate; }
 };
 
 struct ScoreArgs {
@@ -91,8 +98,9 @@ __device__ __forceinline__ void blend_pair(const float4 g, const float4 c, const
                                __ffma2_rn(bc2(c.y), dxy, __fmul2_rn(bc2(c.z), dyy)));
   const float2 raw = __fmul2_rn(bc2(g.z), make_float2(fast_exp2(qs.x), fast_exp2(qs.y)));
   const float2 alpha = make_float2(fminf(kAlphaCap, raw.x), fminf(kAlphaCap, raw.y));
-  const bool b0 = s.alive0 && (alpha.x >= kMinAlpha);
-  const bool b1 = s.alive1 && (alpha.y >= kMinAlpha);
+  const bool live0 = s.alive0(), live1 = s.alive1();
+  const bool b0 = live0 & (alpha.x >= kMinAlpha);
+  const bool b1 = live1 & (alpha.y >= kMinAlpha);
   // the non-blending pixel of a pair gets a = 0: w = T * 0 = 0 and
   // T * (1 - 0) = T exactly, so no selects on w and T are needed
   const float2 a = make_float2(b0 ? alpha.x : 0.f, b1 ? alpha.y : 0.f);
@@ -104,12 +112,9 @@ __device__ __forceinline__ void blend_pair(const float4 g, const float4 c, const
   s.Cb = __ffma2_rn(w, bc2(col.z), s.Cb);
   s.D = __ffma2_rn(w, bc2(col.w), s.D);
   s.T = __fmul2_rn(s.T, __fadd2_rn(bc2(1.f), make_float2(-a.x, -a.y)));
-  s.nc0 += b0 ? 1 : 0;
-  s.nc1 += b1 ? 1 : 0;
-  s.ncons0 = s.alive0 ? pos + 1 : s.ncons0;
-  s.ncons1 = s.alive1 ? pos + 1 : s.ncons1;
-  s.alive0 = s.alive0 && (s.T.x >= kTTerminate);
-  s.alive1 = s.alive1 && (s.T.y >= kTTerminate);
+  s.nc = __fadd2_rn(s.nc, make_float2(b0 ? 1.f : 0.f, b1 ? 1.f : 0.f));
+  s.ncons0 = live0 ? pos + 1 : s.ncons0;
+  s.ncons1 = live1 ? pos + 1 : s.ncons1;
 }
 
 // 4 warps; warp w owns the 8x8 block (bx, by) = (w & 1, w >> 1) of the tile;
@@ -128,9 +133,9 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
     float* __restrict__ out_T, int32_t* __restrict__ out_ncontrib,
     int32_t* __restrict__ out_ncons, float* __restrict__ ckpt,
     const int64_t* __restrict__ ckpt_base, ScoreArgs sc) {
-  __shared__ float4 s_geo[kBatch];  // mx, my, opacity, depth
-  __shared__ float4 s_con[kBatch];  // prescaled conic a', 2b', c'
-  __shared__ float4 s_col[kBatch];  // r, g, b, depth
+  // per staged splat: [0] mx, my, opacity, depth  [1] prescaled conic a',
+  // 2b', c'  [2] r, g, b, depth -- one base address per list entry
+  __shared__ float4 s_spl[kBatch][3];
   __shared__ float4 s_raw[kBatch];  // a, b, c (unscaled), level t
   __shared__ int s_row[kScore ? kBatch : 1];
 
@@ -152,11 +157,10 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
   if (kCkpt) ck0 = ckpt + ckpt_base[tile] * (5 * kTilePixels) + ly0 * kTile + lx;
 
   PixPair s;
-  s.T = bc2(1.f);
+  s.T = make_float2(in0 ? 1.f : 0.f, in1 ? 1.f : 0.f);
   s.Cr = s.Cg = s.Cb = s.D = bc2(0.f);
-  s.nc0 = s.nc1 = s.ncons0 = s.ncons1 = 0;
-  s.alive0 = in0;
-  s.alive1 = in1;
+  s.nc = bc2(0.f);
+  s.ncons0 = s.ncons1 = 0;
   s.strong0 = s.strong1 = false;
   const unsigned lt_mask = (1u << lane) - 1u;
   long long sc_cursor = 0;  // kScore 1/2: this warp's contributions so far
@@ -169,7 +173,7 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
   }
 
   for (int b0 = 0; b0 < n; b0 += kBatch) {
-    if (!__syncthreads_or(s.alive0 || s.alive1)) break;
+    if (!__syncthreads_or(s.alive0() || s.alive1())) break;
 #pragma unroll
     for (int h = 0; h < kBatch / kFwdThreads; ++h) {
       const int i = tid + h * kFwdThreads;
@@ -178,10 +182,10 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
         const int row = values[start + k];
         const float4 r0 = __ldg(rec + 3 * row), r1 = __ldg(rec + 3 * row + 1),
                      r2 = __ldg(rec + 3 * row + 2);
-        s_geo[i] = make_float4(r0.x, r0.y, r1.y, r1.z);
-        s_con[i] = make_float4(__fmul_rn(r0.z, kQScale), __fmul_rn(r0.w, 2.0f * kQScale),
-                               __fmul_rn(r1.x, kQScale), 0.f);
-        s_col[i] = make_float4(r2.x, r2.y, r2.z, r1.z);
+        s_spl[i][0] = make_float4(r0.x, r0.y, r1.y, r1.z);
+        s_spl[i][1] = make_float4(__fmul_rn(r0.z, kQScale), __fmul_rn(r0.w, 2.0f * kQScale),
+                                  __fmul_rn(r1.x, kQScale), 0.f);
+        s_spl[i][2] = make_float4(r2.x, r2.y, r2.z, r1.z);
         s_raw[i] = make_float4(r0.z, r0.w, r1.x, r1.w);
         if (kScore) s_row[i] = row;
       }
@@ -190,20 +194,21 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
     const int cnt = min(kBatch, n - b0);
     // chunks of 32 list positions == one checkpoint interval
     for (int c0 = 0; c0 < cnt; c0 += kGroup) {
-      if (!__any_sync(0xffffffffu, s.alive0 || s.alive1)) break;  // warp-level early exit
+      if (!__any_sync(0xffffffffu, s.alive0() || s.alive1())) break;  // warp-level early exit
       const int cend = min(kGroup, cnt - c0);
       const int pos0 = b0 + c0;
       // lane j tests splat c0 + j against this warp's 8x8 block
       bool hit = false;
       if (lane < cend) {
-        const float4 g = s_geo[c0 + lane], rw = s_raw[c0 + lane];
+        const float4 g = s_spl[c0 + lane][0], rw = s_raw[c0 + lane];
         hit = strip_hit(g.x, g.y, rw.x, rw.y, rw.z, rw.w, sx0, sx0 + 7.f, sy0, sy0 + 7.f);
       }
       unsigned mask = __ballot_sync(0xffffffffu, hit);
       while (mask) {
         const int j = __ffs(mask) - 1;
         mask &= mask - 1u;
-        blend_pair(s_geo[c0 + j], s_con[c0 + j], s_col[c0 + j], pxf, pyf, pos0 + j, s);
+        const float4* sp = s_spl[c0 + j];
+        blend_pair(sp[0], sp[1], sp[2], pxf, pyf, pos0 + j, s);
         if (kScore) {
           const unsigned q0 = __ballot_sync(0xffffffffu, kScore == 3 ? s.strong0 && m0 : s.strong0);
           const unsigned q1 = __ballot_sync(0xffffffffu, kScore == 3 ? s.strong1 && m1 : s.strong1);
@@ -232,14 +237,14 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
         // state after list position pos0+31 -> record (pos0+32)/32 - 1, for
         // each pixel that consumed that position (still alive, or died there)
         float* dst = ck0 + (long long)(pos0 >> 5) * (5 * kTilePixels);
-        if (s.alive0 || s.ncons0 == pos0 + kGroup) {
+        if (s.alive0() || s.ncons0 == pos0 + kGroup) {
           dst[0] = s.T.x;
           dst[kTilePixels] = s.Cr.x;
           dst[2 * kTilePixels] = s.Cg.x;
           dst[3 * kTilePixels] = s.Cb.x;
           dst[4 * kTilePixels] = s.D.x;
         }
-        if (s.alive1 || s.ncons1 == pos0 + kGroup) {
+        if (s.alive1() || s.ncons1 == pos0 + kGroup) {
           dst += 4 * kTile;
           dst[0] = s.T.y;
           dst[kTilePixels] = s.Cr.y;
@@ -253,8 +258,8 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
   if (kScore == 1 && lane == 0) sc.warp_counts[tile * 4 + warp] = sc_cursor;
   // a pixel that never terminated considered the whole list (skipped
   // entries included); a terminated one stopped at its death position
-  if (s.alive0) s.ncons0 = n;
-  if (s.alive1) s.ncons1 = n;
+  if (s.alive0()) s.ncons0 = n;
+  if (s.alive1()) s.ncons1 = n;
   if (in0) {
     const long long pix = (long long)y0 * width + x;
     out_color[3 * pix] = fmaf(s.T.x, bg_r, s.Cr.x);
@@ -262,7 +267,7 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
     out_color[3 * pix + 2] = fmaf(s.T.x, bg_b, s.Cb.x);
     out_depth[pix] = s.D.x;
     out_T[pix] = s.T.x;
-    out_ncontrib[pix] = s.nc0;
+    out_ncontrib[pix] = (int)s.nc.x;
     out_ncons[pix] = s.ncons0;
   }
   if (in1) {
@@ -272,7 +277,7 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
     out_color[3 * pix + 2] = fmaf(s.T.y, bg_b, s.Cb.y);
     out_depth[pix] = s.D.y;
     out_T[pix] = s.T.y;
-    out_ncontrib[pix] = s.nc1;
+    out_ncontrib[pix] = (int)s.nc.y;
     out_ncons[pix] = s.ncons1;
   }
 }
