@@ -74,8 +74,10 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
     int32_t* __restrict__ processed) {
   __shared__ float4 s_pa[kPixSlots];
   __shared__ float4 s_pb[kPixSlots];
-  __shared__ unsigned short s_list[kBwdWarps][kTilePixels + 2 * kListPad];  // byte offsets
-  __shared__ float2 s_tr[kBwdWarps][kTilePixels + kListPad];  // (T_ckpt, R_ckpt)
+  // byte offsets; the step count is rounded up to a multiple of 4, hence
+  // kListPad + 3 trailing sentinels
+  __shared__ unsigned short s_list[kBwdWarps][kTilePixels + 2 * kListPad + 4];
+  __shared__ float2 s_tr[kBwdWarps][kTilePixels + kListPad + 4];  // (T_ckpt, R_ckpt)
   __shared__ int s_maxnc;
   __shared__ int s_next;
 
@@ -200,14 +202,21 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
         }
         n_act += __popc(bal);
       }
-      list[kListPad + n_act + lane] = kSentinel;  // trailing sentinels
+      // trailing sentinels; their (T, R) entries are finite zeros so the
+      // sentinel steps contribute exact zeros (w = T * 0)
+      list[kListPad + n_act + lane] = kSentinel;
+      tr[n_act + lane] = make_float2(0.f, 0.f);
+      if (lane < 3) {
+        list[kListPad + n_act + 32 + lane] = kSentinel;
+        tr[n_act + 32 + lane] = make_float2(0.f, 0.f);
+      }
       __syncwarp();
 
       float2 acc_a = bc(0.f), acc_b = bc(0.f), acc_c = bc(0.f), acc_mx = bc(0.f), acc_my = bc(0.f);
       float2 acc_o = bc(0.f), acc_r = bc(0.f), acc_g = bc(0.f), acc_bl = bc(0.f), acc_d = bc(0.f);
       float T_out = 1.f, R_out = 0.f;
       const unsigned short* my_list = list + kListPad - lane;
-      const int steps = n_act + 31;
+      const int steps = (n_act + 31 + 3) & ~3;  // sentinel steps pad to a multiple of 4
       const float2 one = bc(1.f);
       // one systolic step of this lane's splat pair on pixel record (pa, pb)
       auto step = [&](const float4& pa, const float4& pb, int t) {
@@ -269,26 +278,26 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
         acc_bl = __ffma2_rn(w, bc(pb.z), acc_bl);
         if (kDepth) acc_d = __ffma2_rn(w, bc(pa.z), acc_d);
       };
-      // software pipeline, unrolled by two with ping-pong registers: the
+      // software pipeline, unrolled by four with ping-pong registers: the
       // next step's pixel record is loaded while this step computes (the
       // padded list makes the loads past the end read sentinels)
       float4 pa0 = *reinterpret_cast<const float4*>(pa_base + my_list[0]);
       float4 pb0 = *reinterpret_cast<const float4*>(pb_base + my_list[0]);
       float4 pa1, pb1;
-      for (int t = 0; t < steps; t += 2) {
-        {
-          const unsigned off = my_list[t + 1];
-          pa1 = *reinterpret_cast<const float4*>(pa_base + off);
-          pb1 = *reinterpret_cast<const float4*>(pb_base + off);
-        }
+      auto load = [&](float4& a, float4& b, int t) {
+        const unsigned off = my_list[t];
+        a = *reinterpret_cast<const float4*>(pa_base + off);
+        b = *reinterpret_cast<const float4*>(pb_base + off);
+      };
+      for (int t = 0; t < steps; t += 4) {
+        load(pa1, pb1, t + 1);
         step(pa0, pb0, t);
-        if (t + 1 >= steps) break;
-        {
-          const unsigned off = my_list[t + 2];
-          pa0 = *reinterpret_cast<const float4*>(pa_base + off);
-          pb0 = *reinterpret_cast<const float4*>(pb_base + off);
-        }
+        load(pa0, pb0, t + 2);
         step(pa1, pb1, t + 1);
+        load(pa1, pb1, t + 3);
+        step(pa0, pb0, t + 2);
+        load(pa0, pb0, t + 4);
+        step(pa1, pb1, t + 3);
       }
       __syncwarp();
       // next supergroup: dynamic, so the warps of a tile finish together
