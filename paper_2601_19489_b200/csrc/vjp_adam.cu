@@ -430,7 +430,7 @@ __device__ __forceinline__ void store_row(float* base, long long i, const float*
 // up front (42 independent loads in flight), the VJP runs on the registers,
 // the consumed Grad2D row is zeroed for the next step, and the five Adam
 // groups are updated and stored.
-__global__ void __launch_bounds__(256) vjp_adam_sh0_kernel(
+__global__ void __launch_bounds__(256, 3) vjp_adam_sh0_kernel(
     tsr_camera_t cam, long long n, const float4* __restrict__ rec,
     const int32_t* __restrict__ row_of_source, float* __restrict__ grad2d, AdamGroups groups,
     float* __restrict__ pose_sums, unsigned long long* __restrict__ skipped,
@@ -440,20 +440,15 @@ __global__ void __launch_bounds__(256) vjp_adam_sh0_kernel(
   bool vis = false;
   unsigned long long local = 0;
   if (i < n) {
-    float pp[3], pl[3], pq[4], po[1], pc[3];
-    float mp[3], ml[3], mq[4], mo[1], mc[3];
-    float vp[3], vl[3], vq[4], vo[1], vc[3];
+    // two load phases (VJP inputs, then the moments) keep fewer registers
+    // live than loading all 42 values up front, so 3 CTAs (24 warps) fit
     const tsr_adam_group_t &G0 = groups.g[0], &G1 = groups.g[1], &G2 = groups.g[2],
                            &G3 = groups.g[3], &G4 = groups.g[4];
-    load_row<3>(G0.param, i, pp); load_row<3>(G0.exp_avg, i, mp); load_row<3>(G0.exp_avg_sq, i, vp);
-    load_row<3>(G1.param, i, pl); load_row<3>(G1.exp_avg, i, ml); load_row<3>(G1.exp_avg_sq, i, vl);
-    load_row<4>(G2.param, i, pq); load_row<4>(G2.exp_avg, i, mq); load_row<4>(G2.exp_avg_sq, i, vq);
-    load_row<1>(G3.param, i, po); load_row<1>(G3.exp_avg, i, mo); load_row<1>(G3.exp_avg_sq, i, vo);
-    load_row<3>(G4.param, i, pc); load_row<3>(G4.exp_avg, i, mc); load_row<3>(G4.exp_avg_sq, i, vc);
+    float pp[3], pl[3], pq[4], po[1], pc[3];
+    load_row<3>(G0.param, i, pp);
+    load_row<3>(G1.param, i, pl);
+    load_row<4>(G2.param, i, pq);
     const int row = row_of_source[i];
-    const AdamScal S0 = adam_scal(G0, scal, 0), S1 = adam_scal(G1, scal, 1),
-                   S2 = adam_scal(G2, scal, 2), S3 = adam_scal(G3, scal, 3),
-                   S4 = adam_scal(G4, scal, 4);
     float gp[3] = {0.f, 0.f, 0.f}, gl[3] = {0.f, 0.f, 0.f}, gq[4] = {0.f, 0.f, 0.f, 0.f};
     float go[1] = {0.f}, gc[3] = {0.f, 0.f, 0.f};
     if (row >= 0) {
@@ -475,6 +470,16 @@ __global__ void __launch_bounds__(256) vjp_adam_sh0_kernel(
       for (int k = 0; k < 4; ++k) gq[k] = vj.gq[k];
       go[0] = vj.go;
     }
+    float mp[3], ml[3], mq[4], mo[1], mc[3];
+    float vp[3], vl[3], vq[4], vo[1], vc[3];
+    load_row<3>(G0.exp_avg, i, mp); load_row<3>(G0.exp_avg_sq, i, vp);
+    load_row<3>(G1.exp_avg, i, ml); load_row<3>(G1.exp_avg_sq, i, vl);
+    load_row<4>(G2.exp_avg, i, mq); load_row<4>(G2.exp_avg_sq, i, vq);
+    load_row<1>(G3.param, i, po); load_row<1>(G3.exp_avg, i, mo); load_row<1>(G3.exp_avg_sq, i, vo);
+    load_row<3>(G4.param, i, pc); load_row<3>(G4.exp_avg, i, mc); load_row<3>(G4.exp_avg_sq, i, vc);
+    const AdamScal S0 = adam_scal(G0, scal, 0), S1 = adam_scal(G1, scal, 1),
+                   S2 = adam_scal(G2, scal, 2), S3 = adam_scal(G3, scal, 3),
+                   S4 = adam_scal(G4, scal, 4);
     local += adam_regs<3>(G0, S0, gp, pp, mp, vp);
     local += adam_regs<3>(G1, S1, gl, pl, ml, vl);
     local += adam_regs<4>(G2, S2, gq, pq, mq, vq);
