@@ -430,7 +430,7 @@ __device__ __forceinline__ void store_row(float* base, long long i, const float*
 // up front (42 independent loads in flight), the VJP runs on the registers,
 // the consumed Grad2D row is zeroed for the next step, and the five Adam
 // groups are updated and stored.
-__global__ void __launch_bounds__(256, 3) vjp_adam_sh0_kernel(
+__global__ void __launch_bounds__(128, 7) vjp_adam_sh0_kernel(
     tsr_camera_t cam, long long n, const float4* __restrict__ rec,
     const int32_t* __restrict__ row_of_source, float* __restrict__ grad2d, AdamGroups groups,
     float* __restrict__ pose_sums, unsigned long long* __restrict__ skipped,
@@ -574,7 +574,7 @@ extern "C" int tsr_preprocess_bwd_adam_dev(const tsr_gaussians_t* g, const tsr_c
   int blocks = (int)((g->n + 255) / 256);
   if (g->sh_coeffs == 1) {
     // fast path; also zeroes the consumed Grad2D rows for the next step
-    vjp_adam_sh0_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+    vjp_adam_sh0_kernel<<<(int)((g->n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
         *cam, g->n, (const float4*)rec, row_of_source, (float*)grad2d, gs, pose_sums, skipped,
         group_scalars);
   } else {
