@@ -6,7 +6,15 @@ with ONE allreduce per step, and every rank applies the identical Adam update
 (K5), so replicas stay bit-identical.  `deterministic=True` replaces the
 NCCL sum by an all-gather + fixed rank-order sum, making the result
 independent of the reduction tree (bitwise-equal params for any N with the
-same view set)."""
+same view set).
+
+`sharded=True` is the ZeRO-1 form of the same step (the
+B200 variant): per group, a reduce-scatter gives rank r the summed
+gradient of its row shard [r R, (r + 1) R) (R = ceil(N / G)), K5 updates
+only that shard with shard-sized moments (Adam's work and its m, v memory
+drop G-fold), and an all-gather of the updated rows makes the parameters
+whole again on every rank.  Same bytes on the wire as the allreduce; the
+result is bitwise the replicated step's (Adam is row-local)."""
 
 from __future__ import annotations
 
@@ -14,7 +22,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
-from .optim import Adam, SPLAT_GROUPS, position_lr
+from .optim import BETA1, BETA2, Adam, SPLAT_GROUPS, position_lr
 from .projection import camera_struct, gaussians_struct
 from .trainer import TrainConfig, TrainStep
 
@@ -61,16 +69,125 @@ def allreduce_grads(flat: torch.Tensor, group=None, deterministic: bool = False)
     return flat
 
 
+def shard_rows(n: int, world: int, rank: int) -> tuple[int, int, int]:
+    """This rank's optimizer row shard [s, e) and the padded shard size R
+    (every group splits its rows the same way; the last shard may be short)."""
+    r = -(-n // world) if n else 0
+    s = min(rank * r, n)
+    return s, min(s + r, n), r
+
+
+def padded_grad_views(flat: torch.Tensor, gset, rows: int) -> dict:
+    """Per-group (rows, ...) views into one flat buffer, rows >= N (the
+    padding rows stay zero), in optimizer group order."""
+    out, off = {}, 0
+    for name, p in gset.params().items():
+        shape = (rows,) + tuple(p.shape[1:])
+        n = rows * (p.numel() // max(p.shape[0], 1))
+        out[name] = flat[off: off + n].view(shape)
+        off += n
+    return out
+
+
+def _world_rank(group):
+    if not dist.is_available() or not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+def reduce_scatter_rows(full: torch.Tensor, out: torch.Tensor, group=None,
+                        deterministic: bool = False) -> torch.Tensor:
+    """out (R, ...) = sum over ranks of rows [rank R, (rank + 1) R) of full
+    (G R, ...).  NCCL: one reduce_scatter_tensor; gloo (no reduce-scatter)
+    and deterministic mode: the allreduce forms above, then this rank's rows."""
+    world, rank = _world_rank(group)
+    r = out.shape[0]
+    if world == 1:
+        return out.copy_(full[:r])
+    if not deterministic and dist.get_backend(group) == "nccl":
+        dist.reduce_scatter_tensor(out, full, group=group)
+        return out
+    summed = allreduce_grads(full.clone(), group, deterministic)
+    return out.copy_(summed[rank * r:(rank + 1) * r])
+
+
+def all_gather_rows(shard: torch.Tensor, full: torch.Tensor, group=None) -> torch.Tensor:
+    """full (G R, ...) = the ranks' (R, ...) shards in rank order."""
+    world, _ = _world_rank(group)
+    if world == 1:
+        return full[:shard.shape[0]].copy_(shard)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(full, shard, group=group)
+    else:
+        dist.all_gather(list(full.chunk(world)), shard, group=group)
+    return full
+
+
+class ZeroAdam:
+    """ZeRO-1 Adam over a row shard (optim.py:60-88 semantics per row): this
+    rank owns the moments of rows [s, e) of every group; lr, bias
+    corrections and the per-group step counts follow Adam exactly."""
+
+    def __init__(self, gset, world: int, rank: int, lrs: dict | None = None):
+        self.adam = Adam(lrs)
+        self.s, self.e, self.rows = shard_rows(len(gset), world, rank)
+        self.m = {k: torch.zeros((self.rows,) + tuple(p.shape[1:]), dtype=torch.float32,
+                                 device="cuda") for k, p in gset.params().items()}
+        self.v = {k: torch.zeros_like(t) for k, t in self.m.items()}
+        self.steps = {k: 0 for k in self.m}
+
+    def step_async(self, params: dict, grad_shards: dict, lr_overrides=None) -> torch.Tensor:
+        lib = _lib.load()
+        descs = []
+        n = self.e - self.s
+        for name, p in params.items():
+            self.steps[name] += 1
+            t = self.steps[name]
+            width = p.numel() // max(p.shape[0], 1)
+            d = _lib.AdamGroup_t()
+            d.param = p.data_ptr() + 4 * self.s * width
+            d.grad = grad_shards[name].data_ptr()
+            d.exp_avg = self.m[name].data_ptr()
+            d.exp_avg_sq = self.v[name].data_ptr()
+            d.rows = n
+            d.width = width
+            d.renormalize = 1 if name == "rotations" else 0
+            d.lr = (lr_overrides or {}).get(name, self.adam.lrs.get(name, 1e-3))
+            d.bias_correction1 = 1.0 - BETA1 ** t
+            d.bias_correction2 = 1.0 - BETA2 ** t
+            descs.append(d)
+        counter = self.adam._counter()
+        if n > 0:
+            arr = (_lib.AdamGroup_t * len(descs))(*descs)
+            _lib.check(lib.tsr_adam_step(arr, len(descs), counter.data_ptr(),
+                                         _lib.stream_handle()), "tsr_adam_step")
+        return counter
+
+
 class ViewParallelStep(TrainStep):
-    """One optimizer step over this rank's views + an allreduce."""
+    """One optimizer step over this rank's views + an allreduce (or, with
+    sharded=True, reduce-scatter -> K5 on the row shard -> all-gather)."""
 
     def __init__(self, gset, cfg: TrainConfig, extent: float = 4.0, group=None,
-                 deterministic: bool = False):
+                 deterministic: bool = False, sharded: bool = False):
         super().__init__(gset, cfg, extent)
         self.group = group
         self.deterministic = deterministic
-        self.flat = torch.zeros(grad_numel(gset), dtype=torch.float32, device="cuda")
-        self.grads = flat_grad_views(self.flat, gset)
+        self.sharded = sharded
+        if sharded:
+            world, rank = _world_rank(group)
+            self.zero = ZeroAdam(gset, world, rank, self.opt.lrs)
+            rows = self.zero.rows * world
+            self.flat = torch.zeros(rows * sum(p.numel() // max(p.shape[0], 1)
+                                               for p in gset.params().values()),
+                                    dtype=torch.float32, device="cuda")
+            self.grads = padded_grad_views(self.flat, gset, rows)
+            self.grad_shards = {k: torch.zeros_like(t) for k, t in self.zero.m.items()}
+            self.param_shards = {k: torch.zeros_like(t) for k, t in self.zero.m.items()}
+            self.param_full = {k: torch.zeros_like(g) for k, g in self.grads.items()}
+        else:
+            self.flat = torch.zeros(grad_numel(gset), dtype=torch.float32, device="cuda")
+            self.grads = flat_grad_views(self.flat, gset)
 
     def kernels_per_step(self, views: int = 1) -> int:
         """Per view: K1-K4 + K4b; then one K5 (the NCCL allreduce is not ours)."""
@@ -97,9 +214,28 @@ class ViewParallelStep(TrainStep):
         if not cameras:
             self.flat.zero_()
         self._mark(timer, "vjp")
+        lr = {"positions": position_lr(self.pos_base_lr, self.iteration, self.cfg.max_iters)}
+        if self.sharded:
+            return self._sharded_update(lr, timer, total)
         allreduce_grads(self.flat, self.group, self.deterministic)
         self._mark(timer, "allreduce")
-        lr = {"positions": position_lr(self.pos_base_lr, self.iteration, self.cfg.max_iters)}
         self.opt.step_async(self.gset.params(), self.grads, lr)
         self._mark(timer, "adam")
+        return total
+
+    def _sharded_update(self, lr, timer, total):
+        params = self.gset.params()
+        for name in params:
+            reduce_scatter_rows(self.grads[name], self.grad_shards[name], self.group,
+                                self.deterministic)
+        self._mark(timer, "allreduce")
+        self.zero.step_async(params, self.grad_shards, lr)
+        self._mark(timer, "adam")
+        s, e = self.zero.s, self.zero.e
+        for name, p in params.items():
+            shard = self.param_shards[name]
+            shard[:e - s].copy_(p[s:e])
+            all_gather_rows(shard, self.param_full[name], self.group)
+            p.copy_(self.param_full[name][:p.shape[0]])
+        self._mark(timer, "allgather")
         return total

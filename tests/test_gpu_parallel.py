@@ -97,3 +97,49 @@ def test_two_rank_view_parallel_step_matches_single_process(tmp_path, determinis
         got = flat_grad_views(torch.as_tensor(r0["flat0"]), ts.GaussianSet(**params))[k]
         err = float((got - ref).abs().max() / ref.abs().max().clamp(min=1e-12))
         assert err < 1e-5, (k, err)
+
+
+def _params_worker(rank, world, port, sharded, out_dir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2601_19489_b200 as ts
+    from paper_2601_19489_b200.parallel import ViewParallelStep, shard_views
+    params, ring, gt = _scene()
+    cams, gts = _cams(ring, gt)
+    step = ViewParallelStep(ts.GaussianSet(**params), ts.TrainConfig(max_iters=100),
+                            deterministic=True, sharded=sharded)
+    mine = shard_views(len(cams), world, rank)
+    for _ in range(3):
+        step.step_views([cams[v] for v in mine], [gts[v] for v in mine])
+    torch.cuda.synchronize()
+    np.savez(os.path.join(out_dir, f"{'zero' if sharded else 'rep'}{rank}.npz"),
+             **step.gset.to_numpy())
+    dist.destroy_process_group()
+
+
+def test_zero1_sharded_step_equals_replicated_step(tmp_path):
+    """ZeRO-1 (reduce-scatter -> K5 on a row shard with shard-sized moments ->
+    all-gather) gives bitwise the replicated step's parameters on every rank
+    (deterministic reduction; Adam is row-local)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    for k, sharded in enumerate((False, True)):
+        port = 29900 + os.getpid() % 50 + 60 * k
+        procs = [ctx.Process(target=_params_worker, args=(r, 2, port, sharded, str(tmp_path)))
+                 for r in range(2)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(timeout=600)
+            assert p.exitcode == 0
+    rep = dict(np.load(tmp_path / "rep0.npz"))
+    for name in ("zero0", "zero1", "rep1"):
+        got = dict(np.load(tmp_path / f"{name}.npz"))
+        for k in rep:
+            assert np.array_equal(rep[k], got[k]), (name, k)

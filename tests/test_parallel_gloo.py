@@ -60,3 +60,70 @@ def test_allreduce_sum_of_views_gloo(world):
     for rank, err, exact in res:
         assert err < 1e-5
         assert exact  # deterministic mode is bitwise the fixed-order sum
+
+
+def test_shard_rows_cover_every_row_once():
+    from paper_2601_19489_b200.parallel import shard_rows
+    for n in (0, 1, 9, 10, 1000):
+        for world in (1, 2, 3, 8):
+            spans = [shard_rows(n, world, r) for r in range(world)]
+            rows = [i for s, e, _ in spans for i in range(s, e)]
+            assert rows == list(range(n))
+            assert all(e - s <= r for s, e, r in spans)
+
+
+def _adam_rows(p, g, m, v, lr, t):
+    """optim.py:60-88 per row (torch, for the choreography check)."""
+    m = 0.9 * m + 0.1 * g
+    v = 0.999 * v + 0.001 * g * g
+    return p - lr * (m / (1 - 0.9 ** t)) / ((v / (1 - 0.999 ** t)).sqrt() + 1e-15), m, v
+
+
+def _zero_worker(rank, world, port, q):
+    from paper_2601_19489_b200.parallel import all_gather_rows, reduce_scatter_rows, shard_rows
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n, w = 9, 3
+    params = torch.tensor(np.random.default_rng(100).normal(0, 1, (n, w)), dtype=torch.float32)
+    grads = [torch.tensor(np.random.default_rng(r).normal(0, 1, (n, w)), dtype=torch.float32)
+             for r in range(world)]
+    s, e, r = shard_rows(n, world, rank)
+    full = torch.zeros(r * world, w)
+    full[:n] = grads[rank]
+    out = torch.zeros(r, w)
+    ok = []
+    for det in (False, True):
+        reduce_scatter_rows(full, out, deterministic=det)
+        summed = torch.zeros(n, w)
+        for g in grads:  # fixed rank order (the deterministic reduction)
+            summed += g
+        ok.append(bool(torch.allclose(out[:e - s], summed[s:e], atol=1e-6)))
+    # K5 on the shard (torch stand-in), then the all-gather: whole parameters
+    zeros = torch.zeros(e - s, w)
+    upd, _, _ = _adam_rows(params[s:e], out[:e - s], zeros, zeros, 1e-2, 1)
+    shard = torch.zeros(r, w)
+    shard[:e - s] = upd
+    whole = torch.zeros(r * world, w)
+    all_gather_rows(shard, whole)
+    ref, _, _ = _adam_rows(params, summed, torch.zeros(n, w), torch.zeros(n, w), 1e-2, 1)
+    ok.append(bool(torch.allclose(whole[:n], ref, atol=1e-6)))
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+def test_zero1_reduce_scatter_adam_all_gather_gloo():
+    """ZeRO-1 choreography of the sharded step: the reduce-scatter hands each
+    rank the summed gradient of its row shard (both reduction modes), and
+    the all-gather of the per-shard updates equals the replicated update."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29650 + os.getpid() % 300
+    procs = [ctx.Process(target=_zero_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok in res:
+        assert all(ok), (rank, ok)
