@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--peer", action="store_true",
+                    help="N>1 / c4: ZeRO-1 fused into one kernel over peer memory (CUDA IPC)")
     ap.add_argument("--zero1", action="store_true",
                     help="N>1 / c4: ZeRO-1 update (reduce-scatter, K5 on the row shard, all-gather)")
     ap.add_argument("--deterministic", action="store_true",
@@ -341,7 +343,7 @@ def gpu_arm(args):
         mine = shard_views(batch_views, world, rank)
         cams = [ts.Camera(ring[v]["fx"], ring[v]["fy"], ring[v]["cx"], ring[v]["cy"],
                           c["width"], c["height"], ring[v]["R"], ring[v]["t"]) for v in mine]
-        stepper = ViewParallelStep(gset, cfg, extent=4.0, sharded=args.zero1)
+        stepper = ViewParallelStep(gset, cfg, extent=4.0, sharded=args.zero1, peer=args.peer)
         run = lambda timer=None: stepper.step_views(cams, [gt_dev] * len(cams), timer)  # noqa
         args.no_e2e = True
     elif world == 1:
@@ -350,7 +352,7 @@ def gpu_arm(args):
                                deterministic=args.deterministic)
         run = lambda timer=None: stepper.step(camera, gt_dev, timer)  # noqa: E731
     else:
-        stepper = ViewParallelStep(gset, cfg, extent=4.0, sharded=args.zero1)
+        stepper = ViewParallelStep(gset, cfg, extent=4.0, sharded=args.zero1, peer=args.peer)
         run = lambda timer=None: stepper.step_views([camera], [gt_dev], timer)  # noqa: E731
 
     def barrier():
@@ -519,7 +521,9 @@ def gpu_arm(args):
         "config": {"workload": f"{args.config}: " + _workload(args.config, world),
                    "views_per_step": batch_views or world,
                    "parallelism": f"view-parallel dp{world}"
-                                  + (" zero1 (reduce-scatter + sharded Adam + all-gather)"
+                                  + (" zero1 fused over peer memory (one kernel: peer gradient "
+                                     "reads, sharded Adam, peer parameter stores)" if args.peer
+                                     else " zero1 (reduce-scatter + sharded Adam + all-gather)"
                                      if args.zero1 else ""),
                    "launch": "one CUDA graph replay per step" if world == 1 else "eager launches",
                    "merge": "deterministic (slots + emission-order row sums)"

@@ -231,6 +231,23 @@ typedef struct {
 int tsr_adam_step(const tsr_adam_group_t* groups_host, int32_t n_groups,
                   unsigned long long* skipped, void* stream);
 
+/* Fused ZeRO-1 update over peer memory (SURVEY §8(e), B200 variant;
+ * replaces the reference's single-process Adam.step, optim.py:60-88, in a
+ * G-rank view-parallel step).  For the shard rows [row_begin, row_end) of
+ * every group k: g = sum over ranks q = 0..world-1, in rank order, of
+ * peer_grads[q * n_groups + k] (full-size (N, width) gradient buffers, device
+ * pointers valid in this process: CUDA IPC / peer mappings); Adam on
+ * groups[k].param (full-size, local) with groups[k].exp_avg / exp_avg_sq
+ * holding ONLY the shard's moments (row 0 = row_begin); the updated row is
+ * stored into every peer_params[q * n_groups + k].  groups[k].grad and
+ * .rows are ignored.  world <= 8, width <= 48.  The caller orders the ranks:
+ * every rank's gradients complete before any launch, every launch complete
+ * before the parameters are read again. */
+int tsr_zero1_peer_adam(const tsr_adam_group_t* groups_host, int32_t n_groups, int32_t world,
+                        const float* const* peer_grads, float* const* peer_params,
+                        int64_t row_begin, int64_t row_end, unsigned long long* skipped,
+                        void* stream);
+
 /* K4b fused with K5 for the single-view training step: the per-Gaussian
  * gradient never leaves registers.  groups_host[0..4] = positions,
  * log_scales, rotations, opacity_logits, colors (grad pointers ignored).

@@ -501,6 +501,78 @@ __global__ void __launch_bounds__(128, 7) vjp_adam_sh0_kernel(
   if ((threadIdx.x & 31) == 0 && local) atomicAdd(skipped, local);
 }
 
+// ---- fused ZeRO-1 update over peer memory (the B200 variant)
+// One thread per (group, shard row): the gradient row is the sum of the
+// ranks' rows read through peer pointers in rank order (bitwise the
+// deterministic fixed-order reduction), Adam runs on the local parameter
+// row with this rank's shard moments, and the updated row is stored into
+// every rank's parameter buffer -- reduce-scatter + K5 + all-gather as one
+// kernel, no collective library.
+constexpr int kPeerMaxWorld = 8;
+constexpr int kPeerMaxWidth = 48;  // colors at SH degree 3
+struct PeerPtrs {
+  const float* g[kPeerMaxWorld * TSR_MAX_ADAM_GROUPS];  // [rank * n_groups + group]
+  float* p[kPeerMaxWorld * TSR_MAX_ADAM_GROUPS];
+};
+
+__global__ void __launch_bounds__(256) zero1_peer_adam_kernel(AdamGroups groups, PeerPtrs pp,
+                                                              int world, long long row_begin,
+                                                              unsigned long long* __restrict__ skipped) {
+  const long long total = groups.row_start[groups.n];
+  const int ng = groups.n;
+  unsigned long long local = 0;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    int gi = 0;
+    while (t >= groups.row_start[gi + 1]) ++gi;
+    const tsr_adam_group_t& G = groups.g[gi];
+    const long long r = t - groups.row_start[gi];  // shard row (moments)
+    const long long row = row_begin + r;           // parameter row
+    const int w = G.width;
+    float gsum[kPeerMaxWidth];
+    bool finite = true;
+    for (int k = 0; k < w; ++k) {
+      float acc = pp.g[gi][row * w + k];
+      for (int q = 1; q < world; ++q) acc += pp.g[q * ng + gi][row * w + k];
+      gsum[k] = acc;
+      finite &= isfinite(acc);
+    }
+    if (!finite) {
+      ++local;
+      continue;
+    }
+    float* p = G.param + row * w;
+    float* m = G.exp_avg + r * w;
+    float* v = G.exp_avg_sq + r * w;
+    const float ibc1 = 1.0f / G.bias_correction1, ibc2 = 1.0f / G.bias_correction2;
+    float nrm = 0.f;
+    for (int k = 0; k < w; ++k) {
+      const float gk = gsum[k];
+      const float mk = kBeta1 * m[k] + kOneMinusBeta1 * gk;
+      const float vk = kBeta2 * v[k] + kOneMinusBeta2 * gk * gk;
+      m[k] = mk;
+      v[k] = vk;
+      const float pk = p[k] - __fdividef(G.lr * (mk * ibc1), sqrtf(vk * ibc2) + kEps);
+      p[k] = pk;
+      nrm += pk * pk;
+    }
+    if (G.renormalize) {
+      nrm = sqrtf(nrm);
+      if (nrm > 0.f) {
+        const float inv = 1.0f / nrm;
+        for (int k = 0; k < w; ++k) p[k] = p[k] * inv;
+      }
+    }
+    for (int q = 0; q < world; ++q) {  // all-gather by direct peer stores
+      float* dst = pp.p[q * ng + gi] + row * w;
+      if (dst == p) continue;
+      for (int k = 0; k < w; ++k) dst[k] = p[k];
+    }
+  }
+  for (int d = 16; d > 0; d >>= 1) local += __shfl_xor_sync(0xffffffffu, local, d);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(skipped, local);
+}
+
 static bool fill_groups(const tsr_adam_group_t* gh, int n, AdamGroups& out) {
   if (n <= 0 || n > TSR_MAX_ADAM_GROUPS) return false;
   out.n = n;
@@ -544,6 +616,38 @@ extern "C" int tsr_adam_step(const tsr_adam_group_t* groups_host, int32_t n_grou
   long long blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   adam_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(gs, skipped);
+  TSR_CHECK_LAUNCH();
+  return TSR_OK;
+}
+
+extern "C" int tsr_zero1_peer_adam(const tsr_adam_group_t* groups_host, int32_t n_groups,
+                                   int32_t world, const float* const* peer_grads,
+                                   float* const* peer_params, int64_t row_begin,
+                                   int64_t row_end, unsigned long long* skipped, void* stream) {
+  if (!groups_host || !peer_grads || !peer_params || !skipped) return TSR_E_INVALID;
+  if (world < 1 || world > kPeerMaxWorld || n_groups < 1 || n_groups > TSR_MAX_ADAM_GROUPS)
+    return TSR_E_INVALID;
+  if (row_begin < 0 || row_end < row_begin) return TSR_E_INVALID;
+  AdamGroups gs;
+  if (!fill_groups(groups_host, n_groups, gs)) return TSR_E_INVALID;
+  PeerPtrs pp;
+  for (int q = 0; q < world; ++q)
+    for (int k = 0; k < n_groups; ++k) {
+      if (gs.g[k].width > kPeerMaxWidth || !gs.g[k].exp_avg || !gs.g[k].exp_avg_sq)
+        return TSR_E_INVALID;
+      pp.g[q * n_groups + k] = peer_grads[q * n_groups + k];
+      pp.p[q * n_groups + k] = peer_params[q * n_groups + k];
+      if (!pp.g[q * n_groups + k] || !pp.p[q * n_groups + k]) return TSR_E_INVALID;
+    }
+  // every group covers the shard rows [row_begin, row_end)
+  gs.row_start[0] = 0;
+  for (int k = 0; k < n_groups; ++k) gs.row_start[k + 1] = gs.row_start[k] + (row_end - row_begin);
+  const long long total = gs.row_start[n_groups];
+  if (total == 0) return TSR_OK;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  zero1_peer_adam_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(gs, pp, world, row_begin,
+                                                                          skipped);
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }

@@ -18,6 +18,8 @@ result is bitwise the replicated step's (Adam is row-local)."""
 
 from __future__ import annotations
 
+import ctypes
+
 import torch
 import torch.distributed as dist
 
@@ -164,17 +166,102 @@ class ZeroAdam:
         return counter
 
 
+def share_peer_tensors(tensors: list, group=None) -> list:
+    """Every rank's `tensors`, opened in this process: CUDA IPC handles
+    (torch.multiprocessing's rebuild path) exchanged with one all_gather_object.
+    Returns [rank][i] tensors aliasing the peers' device memory (this rank's
+    own entries are the originals)."""
+    from torch.multiprocessing.reductions import reduce_tensor
+    world, rank = _world_rank(group)
+    if world == 1:
+        return [list(tensors)]
+    mine = [reduce_tensor(t) for t in tensors]
+    everyone = [None] * world
+    dist.all_gather_object(everyone, mine, group=group)
+    out = []
+    for q, items in enumerate(everyone):
+        if q == rank:
+            out.append(list(tensors))
+        else:
+            out.append([fn(*args) for fn, args in items])
+    return out
+
+
+class PeerZeroUpdate:
+    """ZeRO-1 fused over peer memory (tsr_zero1_peer_adam): one kernel per
+    rank reads every rank's gradient rows of its shard through CUDA IPC
+    mappings, sums them in rank order, runs Adam with shard moments and
+    stores the updated rows into every rank's parameters.  Two host barriers
+    order it: all gradients complete before any rank reads them; all
+    updates complete before the parameters (or gradient buffers) are
+    touched again.  Fixed N (no densification in this mode)."""
+
+    def __init__(self, gset, grads: dict, zero: ZeroAdam, world: int, group=None):
+        self.world, self.group, self.zero = world, group, zero
+        names = list(gset.params())
+        self.names = names
+        local = [grads[n] for n in names] + [gset.params()[n] for n in names]
+        peers = share_peer_tensors(local, group)
+        self._peers = peers  # keep the mappings alive
+        ng = len(names)
+        ptr_g = [peers[q][k].data_ptr() for q in range(world) for k in range(ng)]
+        ptr_p = [peers[q][ng + k].data_ptr() for q in range(world) for k in range(ng)]
+        self.peer_grads = (ctypes.c_void_p * len(ptr_g))(*ptr_g)
+        self.peer_params = (ctypes.c_void_p * len(ptr_p))(*ptr_p)
+
+    def step(self, params: dict, lr_overrides=None) -> None:
+        lib = _lib.load()
+        z = self.zero
+        descs = []
+        for name in self.names:
+            p = params[name]
+            z.steps[name] += 1
+            t = z.steps[name]
+            d = _lib.AdamGroup_t()
+            d.param = p.data_ptr()
+            d.grad = None
+            d.exp_avg = z.m[name].data_ptr()
+            d.exp_avg_sq = z.v[name].data_ptr()
+            d.rows = p.shape[0]
+            d.width = p.numel() // max(p.shape[0], 1)
+            d.renormalize = 1 if name == "rotations" else 0
+            d.lr = (lr_overrides or {}).get(name, z.adam.lrs.get(name, 1e-3))
+            d.bias_correction1 = 1.0 - BETA1 ** t
+            d.bias_correction2 = 1.0 - BETA2 ** t
+            descs.append(d)
+        arr = (_lib.AdamGroup_t * len(descs))(*descs)
+        _barrier(self.group)  # every rank's gradients are complete
+        _lib.check(lib.tsr_zero1_peer_adam(arr, len(descs), self.world, self.peer_grads,
+                                           self.peer_params, z.s, z.e,
+                                           z.adam._counter().data_ptr(), _lib.stream_handle()),
+                   "tsr_zero1_peer_adam")
+        _barrier(self.group)  # every rank's rows are stored everywhere
+
+
+def _barrier(group):
+    torch.cuda.current_stream().synchronize()
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.barrier(group=group)
+
+
 class ViewParallelStep(TrainStep):
     """One optimizer step over this rank's views + an allreduce (or, with
     sharded=True, reduce-scatter -> K5 on the row shard -> all-gather)."""
 
     def __init__(self, gset, cfg: TrainConfig, extent: float = 4.0, group=None,
-                 deterministic: bool = False, sharded: bool = False):
+                 deterministic: bool = False, sharded: bool = False, peer: bool = False):
         super().__init__(gset, cfg, extent)
         self.group = group
         self.deterministic = deterministic
-        self.sharded = sharded
-        if sharded:
+        self.sharded = sharded or peer
+        self.peer = None
+        if peer:  # fused ZeRO-1 over peer memory (tsr_zero1_peer_adam)
+            world, rank = _world_rank(group)
+            self.zero = ZeroAdam(gset, world, rank, self.opt.lrs)
+            self.flat = torch.zeros(grad_numel(gset), dtype=torch.float32, device="cuda")
+            self.grads = flat_grad_views(self.flat, gset)
+            self.peer = PeerZeroUpdate(gset, self.grads, self.zero, world, group)
+        elif sharded:
             world, rank = _world_rank(group)
             self.zero = ZeroAdam(gset, world, rank, self.opt.lrs)
             rows = self.zero.rows * world
@@ -215,6 +302,10 @@ class ViewParallelStep(TrainStep):
             self.flat.zero_()
         self._mark(timer, "vjp")
         lr = {"positions": position_lr(self.pos_base_lr, self.iteration, self.cfg.max_iters)}
+        if self.peer is not None:
+            self.peer.step(self.gset.params(), lr)
+            self._mark(timer, "adam")
+            return total
         if self.sharded:
             return self._sharded_update(lr, timer, total)
         allreduce_grads(self.flat, self.group, self.deterministic)

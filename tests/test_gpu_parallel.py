@@ -99,7 +99,7 @@ def test_two_rank_view_parallel_step_matches_single_process(tmp_path, determinis
         assert err < 1e-5, (k, err)
 
 
-def _params_worker(rank, world, port, sharded, out_dir):
+def _params_worker(rank, world, port, mode, out_dir):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import torch
@@ -113,33 +113,34 @@ def _params_worker(rank, world, port, sharded, out_dir):
     params, ring, gt = _scene()
     cams, gts = _cams(ring, gt)
     step = ViewParallelStep(ts.GaussianSet(**params), ts.TrainConfig(max_iters=100),
-                            deterministic=True, sharded=sharded)
+                            deterministic=True, sharded=mode == "zero", peer=mode == "peer")
     mine = shard_views(len(cams), world, rank)
     for _ in range(3):
         step.step_views([cams[v] for v in mine], [gts[v] for v in mine])
     torch.cuda.synchronize()
-    np.savez(os.path.join(out_dir, f"{'zero' if sharded else 'rep'}{rank}.npz"),
-             **step.gset.to_numpy())
+    np.savez(os.path.join(out_dir, f"{mode}{rank}.npz"), **step.gset.to_numpy())
     dist.destroy_process_group()
 
 
-def test_zero1_sharded_step_equals_replicated_step(tmp_path):
-    """ZeRO-1 (reduce-scatter -> K5 on a row shard with shard-sized moments ->
-    all-gather) gives bitwise the replicated step's parameters on every rank
-    (deterministic reduction; Adam is row-local)."""
+def test_zero1_sharded_and_peer_fused_steps_equal_replicated_step(tmp_path):
+    """ZeRO-1 with collectives (reduce-scatter -> K5 on a row shard with
+    shard-sized moments -> all-gather) and fused over peer memory (one
+    kernel reads every rank's gradient rows through CUDA IPC mappings, sums
+    them in rank order, updates, stores into every rank's parameters) both
+    give bitwise the replicated step's parameters on every rank."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
-    for k, sharded in enumerate((False, True)):
+    for k, mode in enumerate(("rep", "zero", "peer")):
         port = 29900 + os.getpid() % 50 + 60 * k
-        procs = [ctx.Process(target=_params_worker, args=(r, 2, port, sharded, str(tmp_path)))
+        procs = [ctx.Process(target=_params_worker, args=(r, 2, port, mode, str(tmp_path)))
                  for r in range(2)]
         for p in procs:
             p.start()
         for p in procs:
             p.join(timeout=600)
-            assert p.exitcode == 0
+            assert p.exitcode == 0, mode
     rep = dict(np.load(tmp_path / "rep0.npz"))
-    for name in ("zero0", "zero1", "rep1"):
+    for name in ("zero0", "zero1", "peer0", "peer1", "rep1"):
         got = dict(np.load(tmp_path / f"{name}.npz"))
         for k in rep:
             assert np.array_equal(rep[k], got[k]), (name, k)
