@@ -238,8 +238,10 @@ class TrainStep:
         self.loss_ws = losses.PhotometricWorkspace()
         self._grad2d_clean = True  # the SH-0 fused kernel re-zeroes consumed rows
         self.grad_color = None
-        self.status_host = torch.zeros(3, dtype=torch.int64).pin_memory()
-        self.status_dev = torch.zeros(3, dtype=torch.int64, device=dev)
+        # step status read back without kernels: two D2H copy nodes into
+        # pinned memory (overflow flag; totals = (M, P))
+        self.status_ovf_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self.status_tot_host = torch.zeros(2, dtype=torch.int64).pin_memory()
         self.status_event = None
         self.lib = _lib.load()
         self.last = None
@@ -280,7 +282,7 @@ class TrainStep:
         """Non-blocking check of an earlier step's overflow flag and P."""
         if self.status_event is None or not self.status_event.query():
             return
-        overflow, p = int(self.status_host[0]), int(self.status_host[1])
+        overflow, p = int(self.status_ovf_host[0]), int(self.status_tot_host[1])
         self.status_event = None
         if overflow:
             raise RuntimeError(f"pair capacity {self.index.p_cap} overflowed (P = {p}); "
@@ -352,9 +354,8 @@ class TrainStep:
         return e
 
     def _publish_status(self) -> None:
-        self.status_dev[0:1].copy_(self.index.overflow)
-        self.status_dev[1:3].copy_(self.scratch.totals.flip(0))
-        self.status_host.copy_(self.status_dev, non_blocking=True)
+        self.status_ovf_host.copy_(self.index.overflow, non_blocking=True)
+        self.status_tot_host.copy_(self.scratch.totals, non_blocking=True)
         self.status_event = torch.cuda.Event()
         self.status_event.record()
 
@@ -377,9 +378,8 @@ class TrainStep:
             batch.rec.data_ptr(), batch.row_of_source.data_ptr(), self.grad2d.data_ptr(), groups,
             self._scal_dev.data_ptr(), None, self.skipped.data_ptr(), _lib.stream_handle()),
             "tsr_preprocess_bwd_adam_dev")
-        self.status_dev[0:1].copy_(self.index.overflow)
-        self.status_dev[1:3].copy_(self.scratch.totals.flip(0))
-        self.status_host.copy_(self.status_dev, non_blocking=True)
+        self.status_ovf_host.copy_(self.index.overflow, non_blocking=True)
+        self.status_tot_host.copy_(self.scratch.totals, non_blocking=True)
         return e
 
     def _graph_step(self, camera: Camera, gt_image, depth_weight, depth_prior, depth_valid):
