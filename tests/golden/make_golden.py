@@ -332,7 +332,73 @@ def golden_benchtiling():
     np.savez_compressed(OUT / "benchtiling.npz", **out)
 
 
+def golden_e2e():
+    """Acceptance criterion 5 (test_acceptance.py:161-247): the 5-splat 32x32
+    scene with a pose delta, photometric + disparity loss; the reference's
+    analytic gradients of every parameter class (incl. the pose) and their
+    float64 central finite differences (h = 1e-4), on FP32-rounded inputs."""
+    from tilesplat import pose as rpose
+    from tilesplat.scene import inverse_sigmoid
+    from tilesplat.trainer import TrainConfig as RefConfig
+    from tilesplat.trainer import _full_grads, render_view, view_loss_and_grads
+    rng = np.random.default_rng(3)
+    n = 5
+    params = dict(positions=f32(rng.normal(0, 0.3, (n, 3)) + [0, 0, 3.0]),
+                  log_scales=f32(np.log(rng.uniform(0.8, 1.4, (n, 3)))),
+                  rotations=f32(rng.normal(0, 1, (n, 4))),
+                  opacity_logits=f32(inverse_sigmoid(rng.uniform(0.3, 0.6, n))),
+                  colors=f32(rng.uniform(0.2, 0.8, (n, 1, 3))))
+    R = f32(rpose.rodrigues([0.05, -0.1, 0.02]))
+    t = f32([0.02, -0.03, 0.1])
+    gt = f32(rng.uniform(0, 1, (32, 32, 3)))
+    prior = f32(np.full((32, 32), 3.0))
+    rot, trans = f32([0.01, -0.02, 0.015]), f32([0.005, 0.01, -0.02])
+    bg = f32([0.1, 0.2, 0.3])
+    cfg = RefConfig(round_profile="round2", near=0.1, background=tuple(bg))
+
+    def loss_and_grads(ps, rv, tv, want_grads):
+        gset = GaussianSet(**{k: v.copy() for k, v in ps.items()})
+        cam = Camera(fx=30.0, fy=32.0, cx=16.0, cy=16.0, width=32, height=32, rotation=R,
+                     translation=t, gt_image=gt, depth_prior=prior)
+        delta = rpose.PoseDelta(rv.copy(), tv.copy())
+        vr = render_view(gset, cam, cfg, delta)
+        rep, g2 = view_loss_and_grads(cam, cfg, vr, 0.1)
+        if not want_grads:
+            return rep.total
+        return rep.total, _full_grads(gset, cam, cfg, delta, vr, g2)
+
+    total, grads = loss_and_grads(params, rot, trans, True)
+    h = 1e-4
+    out = {f"p_{k}": v for k, v in params.items()}
+    out.update(cam_R=R, cam_t=t, gt=gt, prior=prior, pose_rot=rot, pose_trans=trans, bg=bg,
+               total=np.array(total))
+    for k, v in grads.items():
+        out[f"g_{k}"] = np.asarray(v)
+
+    def fd(get, put):
+        base = get().copy()
+        g = np.zeros_like(base)
+        for i in range(base.size):
+            x = base.copy().reshape(-1)
+            x[i] += h
+            put(x.reshape(base.shape))
+            fp = loss_and_grads(params, rot, trans, False)
+            x[i] -= 2 * h
+            put(x.reshape(base.shape))
+            fm = loss_and_grads(params, rot, trans, False)
+            put(base)
+            g.reshape(-1)[i] = (fp - fm) / (2 * h)
+        return g
+
+    for k in list(params):
+        out[f"fd_{k}"] = fd(lambda k=k: params[k], lambda x, k=k: params.__setitem__(k, x))
+    out["fd_pose_rot"] = fd(lambda: rot, lambda x: rot.__setitem__(slice(None), x))
+    out["fd_pose_trans"] = fd(lambda: trans, lambda x: trans.__setitem__(slice(None), x))
+    np.savez_compressed(OUT / "e2e.npz", **out)
+
+
 if __name__ == "__main__":
+    golden_e2e()
     golden_benchtiling()
     golden_density()
     golden_ply()
