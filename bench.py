@@ -587,7 +587,7 @@ def c5_arm(args):
     cfg = ts.TrainConfig(round_profile="round2", max_iters=200_000,
                          budget_seconds=args.budget, eval_interval=10**9, seed=0,
                          densify_start=500, densify_interval=300, densify_end=10**9,
-                         holdout_views=holdout)
+                         holdout_views=holdout, deterministic=args.deterministic)
     eval_cams = [scene.cameras[i] for i in holdout]
     psnr0 = ts.evaluate(init, eval_cams, cfg)
     setup_s = time.perf_counter() - t0
@@ -599,7 +599,9 @@ def c5_arm(args):
             "config": {"workload": f"c5: 1M-splat GT rendered into {args.c5_views} 1920x1080 "
                                    f"ring views (+depth priors); init = 500k perturbed; round2; "
                                    f"densify every 300 its (K=10); budget {args.budget:g} s",
-                       "holdout_views": list(holdout)},
+                       "holdout_views": list(holdout),
+                       "merge": "deterministic (slots + emission-order row sums)"
+                                if args.deterministic else "float atomics (FP32-tolerance)"},
             "iterations": res.iterations, "elapsed_s": res.elapsed,
             "stop_reason": res.stop_reason, "splats_final": len(res.gset),
             "psnr_holdout_before": psnr0, "psnr_holdout_after": psnr1,

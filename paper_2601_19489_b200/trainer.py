@@ -621,7 +621,10 @@ def train(scene, cfg: TrainConfig, *, ply_path=None, metrics_path=None, decision
     valid_dev = [(c.depth_valid.to(_device()).bool() if isinstance(c.depth_valid, torch.Tensor)
                   else torch.as_tensor(np.asarray(c.depth_valid), device=_device()).bool())
                  if c.depth_valid is not None else None for c in scene.cameras]
-    stepper = None if cfg.pose_opt else TrainStep(gset, cfg, extent=scene.extent, optimizer=opt)
+    # cfg.deterministic (default True, like the reference) selects K4's
+    # deterministic merge: the same seed gives bitwise-identical metrics
+    stepper = None if cfg.pose_opt else TrainStep(gset, cfg, extent=scene.extent, optimizer=opt,
+                                                  deterministic=cfg.deterministic)
     pose_t = {k: torch.zeros((1, 3), dtype=torch.float32, device=_device())
               for k in ("pose_rot", "pose_trans")}
     metrics, pending, decision_rows = [], [], []
@@ -691,7 +694,8 @@ def train(scene, cfg: TrainConfig, *, ply_path=None, metrics_path=None, decision
             decision_rows.append({"iter": iteration, "clones": c["clone"], "splits": c["split"],
                                   "prunes": c["prune"], "total": len(gset)})
             if stepper is not None:
-                stepper = TrainStep(gset, cfg, extent=scene.extent, optimizer=opt)
+                stepper = TrainStep(gset, cfg, extent=scene.extent, optimizer=opt,
+                                    deterministic=cfg.deterministic)
 
         if cfg.pose_opt and delta.steps_since_bake >= cfg.pose_bake_interval:
             baked = bake(delta, scene.cameras)
