@@ -6,11 +6,11 @@ holding FP32 CUDA tensors, backed by hand-written CUDA kernels in
 libtilesplat_b200.so (include/tilesplat_b200.h).  There is no CPU fallback.
 """
 
-from .scene import TILE, Camera, GaussianSet, inverse_sigmoid, sigmoid
+from .scene import TILE, Camera, GaussianSet, activate, inverse_sigmoid, sigmoid, validate
 from .pose import PoseDelta, apply_delta
 from .projection import (COV_DILATION, MIN_OPACITY, Grad3D, PoseGrad, SplatBatch, project,
                          project_vjp)
-from .binning import (SnugBox, TileIndex, bin_load_balanced, bin_sequential,
+from .binning import (SnugBox, TileIndex, bin_aabb, bin_load_balanced, bin_sequential,
                       compute_snugboxes, lane_test_counts, snugbox)
 from .forward import (ALPHA_CAP, CHECKPOINT_INTERVAL, MIN_ALPHA, T_TERMINATE, Contributions,
                       RenderBuffers, render)

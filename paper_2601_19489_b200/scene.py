@@ -87,6 +87,111 @@ class GaussianSet:
     def to_numpy(self) -> dict:
         return {k: v.detach().cpu().numpy().astype(np.float64) for k, v in self.params().items()}
 
+    def scales(self) -> torch.Tensor:
+        return torch.exp(self.log_scales)
+
+    def opacities(self) -> torch.Tensor:
+        return torch.sigmoid(self.opacity_logits)
+
+    def rotation_matrices(self) -> torch.Tensor:
+        return quat_to_rotmat(self.rotations)
+
+
+def quat_normalize(quats) -> torch.Tensor:
+    """Unit wxyz quaternions (scene.py:25-30); zero-norm rows stay zero."""
+    q = as_device_f32(quats, (-1, 4))
+    n = torch.linalg.norm(q, dim=1, keepdim=True)
+    return torch.where(n > 0, q / torch.where(n > 0, n, torch.ones_like(n)), q)
+
+
+def quat_to_rotmat(quats) -> torch.Tensor:
+    """(N, 3, 3) rotation matrices of normalised wxyz quaternions (scene.py:33-47)."""
+    w, x, y, z = quat_normalize(quats).unbind(1)
+    return torch.stack([
+        torch.stack([1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)], 1),
+        torch.stack([2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)], 1),
+        torch.stack([2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)], 1),
+    ], 1)
+
+
+def activate(gset: GaussianSet, index: int):
+    """(scale (3,), opacity, rotation (3, 3)) of one splat (scene.py:109-116)."""
+    if not 0 <= index < len(gset):
+        raise IndexError(f"splat index {index} out of range [0, {len(gset)})")
+    scale = torch.exp(gset.log_scales[index]).cpu().numpy().astype(np.float64)
+    opacity = float(torch.sigmoid(gset.opacity_logits[index]))
+    rot = quat_to_rotmat(gset.rotations[index:index + 1])[0].cpu().numpy().astype(np.float64)
+    return scale, opacity, rot
+
+
+def validate(gset: GaussianSet) -> list:
+    """Violated invariants, one line per (splat, problem); [] when clean
+    (scene.py:119-137): non-finite fields, zero-norm quaternions."""
+    report = []
+    n = len(gset)
+    for name, arr in gset.params().items():
+        bad = ~torch.isfinite(arr.reshape(n, -1)).all(dim=1)
+        for i in torch.nonzero(bad).flatten().tolist():
+            report.append(f"splat {i}: non-finite {name}")
+    norms = torch.linalg.norm(gset.rotations, dim=1)
+    for i in torch.nonzero(~(norms > 0)).flatten().tolist():
+        report.append(f"splat {i}: zero-norm quaternion")
+    return report
+
+
+# Real SH basis with the l = 0 term equal to 1 (degree 0 == plain RGB),
+# scene.py:186-276; the kernels evaluate the same basis (tsr_common.cuh).
+_C1 = 0.4886025119029199
+_C2 = (1.0925484305920792, -1.0925484305920792, 0.31539156525252005, -1.0925484305920792,
+       0.5462742152960396)
+_C3 = (-0.5900435899266435, 2.890611442640554, -0.4570457994644658, 0.3731763325901154,
+       -0.4570457994644658, 1.445305721320277, -0.5900435899266435)
+
+
+def sh_basis(degree: int, dirs) -> torch.Tensor:
+    """(N, (degree+1)^2) basis values at unit directions."""
+    d = as_device_f32(dirs, (-1, 3))
+    x, y, z = d.unbind(1)
+    cols = [torch.ones_like(x)]
+    if degree >= 1:
+        cols += [-_C1 * y, _C1 * z, -_C1 * x]
+    if degree >= 2:
+        xx, yy, zz = x * x, y * y, z * z
+        cols += [_C2[0] * x * y, _C2[1] * y * z, _C2[2] * (2 * zz - xx - yy), _C2[3] * x * z,
+                 _C2[4] * (xx - yy)]
+    if degree >= 3:
+        cols += [_C3[0] * y * (3 * xx - yy), _C3[1] * x * y * z, _C3[2] * y * (4 * zz - xx - yy),
+                 _C3[3] * z * (2 * zz - 3 * xx - 3 * yy), _C3[4] * x * (4 * zz - xx - yy),
+                 _C3[5] * z * (xx - yy), _C3[6] * x * (xx - 3 * yy)]
+    return torch.stack(cols, 1)
+
+
+def eval_sh(coeffs, dirs) -> torch.Tensor:
+    """View-dependent colours (N, 3) from SH coefficients (N, C, 3)."""
+    c = as_device_f32(coeffs)
+    degree = int(round(np.sqrt(c.shape[1]))) - 1
+    if degree == 0:
+        return c[:, 0, :].clone()
+    return torch.einsum("nc,ncd->nd", sh_basis(degree, dirs), c)
+
+
+def eval_sh_vjp(coeffs, dirs, grad_color):
+    """(d coeffs, d dirs) of eval_sh for upstream grad_color (N, 3)
+    (scene.py:279-291); the direction part by autograd of the basis."""
+    c = as_device_f32(coeffs)
+    g = as_device_f32(grad_color, (-1, 3))
+    degree = int(round(np.sqrt(c.shape[1]))) - 1
+    if degree == 0:
+        gc = torch.zeros_like(c)
+        gc[:, 0, :] = g
+        return gc, torch.zeros((c.shape[0], 3), device=c.device)
+    d = as_device_f32(dirs, (-1, 3)).clone().requires_grad_(True)
+    with torch.enable_grad():
+        basis = sh_basis(degree, d)
+        out = torch.einsum("nc,ncd->nd", basis, c)
+        (gd,) = torch.autograd.grad(out, d, grad_outputs=g)
+    return basis.detach()[:, :, None] * g[:, None, :], gd
+
 
 @dataclass
 class Camera:
@@ -121,6 +226,9 @@ class Camera:
 
     def center(self) -> np.ndarray:
         return -self.rotation.T @ self.translation
+
+    def world_to_cam(self, points) -> np.ndarray:
+        return np.asarray(points, dtype=np.float64) @ self.rotation.T + self.translation
 
     def replace_pose(self, rotation, translation) -> None:
         self.rotation = np.asarray(rotation, dtype=np.float64).reshape(3, 3)
