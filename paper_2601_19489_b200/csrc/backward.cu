@@ -241,12 +241,23 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
         const float2 alpha = f2(fminf(kAlphaCap, raw.x), fminf(kAlphaCap, raw.y));
         // predicates chained so each costs one compare (alpha >= 1/255 <=>
         // raw >= 1/255 since the cap is above it)
-        const bool in0 = p < nc, in1 = p + 1 < nc;
-        const bool part0 = in0 & (alpha.x >= kMinAlpha);
-        const bool part1 = in1 & (alpha.y >= kMinAlpha);
-        // non-participants get a = 0: w = T * 0 = 0 and T * (1 - 0) = T
-        // exactly (no selects on the chain; their 1/(1 - a) is unused)
-        const float2 a = f2(part0 ? alpha.x : 0.f, part1 ? alpha.y : 0.f);
+        // a = (p < nc && alpha >= 1/255) ? alpha : 0 as one chained compare
+        // + select per splat (inline PTX: the compiler otherwise splits the
+        // chain into two selects).  Non-participants get a = 0: w = T * 0 = 0
+        // and T * (1 - 0) = T exactly (no selects on the chain; their
+        // 1 / (1 - a) is unused).
+        float a0, a1;
+        asm("{\n\t.reg .pred q;\n\t"
+            "setp.lt.s32 q, %1, %2;\n\t"
+            "setp.ge.and.f32 q, %3, %4, q;\n\t"
+            "selp.f32 %0, %3, 0f00000000, q;\n\t}"
+            : "=f"(a0) : "r"(p), "r"(nc), "f"(alpha.x), "f"(kMinAlpha));
+        asm("{\n\t.reg .pred q;\n\t"
+            "setp.lt.s32 q, %1, %2;\n\t"
+            "setp.ge.and.f32 q, %3, %4, q;\n\t"
+            "selp.f32 %0, %3, 0f00000000, q;\n\t}"
+            : "=f"(a1) : "r"(p + 1), "r"(nc), "f"(alpha.y), "f"(kMinAlpha));
+        const float2 a = f2(a0, a1);
         const float2 om = __fadd2_rn(one, f2(-a.x, -a.y));
         float2 gc = __ffma2_rn(bc(pb.x), cr, __ffma2_rn(bc(pb.y), cg, __fmul2_rn(bc(pb.z), cbl)));
         if (kDepth) gc = __ffma2_rn(bc(pa.z), dep, gc);
@@ -262,9 +273,12 @@ __global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
         const float2 dLda = f2(fmaf(-num0, rcp.x, T_in * gc.x), fmaf(-num1, rcp.y, T1 * gc.y));
         // uncapped participants only (backward.py:64,72): 1/255 <= raw <= 0.99
         // (then alpha == raw); x(-1/2) folded into the merge
-        const bool l0 = part0 & (raw.x <= kAlphaCap);
-        const bool l1 = part1 & (raw.y <= kAlphaCap);
-        const float2 ld = f2(l0 ? dLda.x : 0.f, l1 ? dLda.y : 0.f);
+        // one compare: a == raw holds exactly for uncapped participants
+        // (a = alpha = raw), fails for capped ones (a = 0.99 < raw) and for
+        // non-participants with raw != 0 (a = 0); a non-participant with
+        // raw == 0 keeps its finite dLda but has alpha = gauss = 0, so every
+        // product below is zero
+        const float2 ld = f2(a.x == raw.x ? dLda.x : 0.f, a.y == raw.y ? dLda.y : 0.f);
         const float2 gq = __fmul2_rn(ld, alpha);
         acc_a = __ffma2_rn(gq, dxx, acc_a);
         acc_b = __ffma2_rn(gq, dxy, acc_b);
