@@ -62,7 +62,7 @@ constexpr int kListPad = 32;
 // it processed; grad_reduce_kernel then sums each row's slots in emission
 // order, so results are bitwise reproducible.
 template <bool kDepth, bool kDet>
-__global__ void __launch_bounds__(kBwdThreads, 6) render_bwd_kernel(
+__global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
     const float4* __restrict__ rec, const int32_t* __restrict__ values,
     const int64_t* __restrict__ offsets, int width, int height, int tiles_x,
     const float* __restrict__ color, const float* __restrict__ depth,
