@@ -156,3 +156,30 @@ def test_deterministic_merge_is_bitwise_reproducible(graster, name):
         assert np.array_equal(x, y), k
         assert rel_err(x, g[f"{name}_pg_{k}"]) < 1e-4, k
     assert a.merges == int(g[name + "_merges"])
+
+
+def test_blend_weights_plus_final_T_is_one():
+    """test_forward.py:59-69: white splats on black, colour = sum of weights."""
+    import paper_2601_19489_b200 as ts
+    rng = np.random.default_rng(0)
+    n = 25
+    b = dict(means2d=np.stack([rng.uniform(0, 64, n), rng.uniform(0, 64, n)], 1),
+             conics=np.array([[0.02, 0.005, 0.03]] * n),
+             level_t=np.full(n, 2 * np.log(255 * 0.7)), depths=rng.uniform(1, 5, n),
+             opacities=np.full(n, 0.7), source_ids=np.arange(n), width=64, height=64)
+    db = dev_batch(b)
+    bufs = ts.render(db, ts.bin_sequential(db), np.ones((n, 3)), np.zeros(3))
+    assert np.abs(np64(bufs.color[:, :, 0]) + np64(bufs.final_T) - 1.0).max() < 1e-6
+
+
+def test_single_splat_color_gradient_closed_form():
+    """test_backward.py:53-63: with one splat and unit upstream gradient,
+    dL/dc = sum over pixels of its weight = sum (1 - final_T)."""
+    import paper_2601_19489_b200 as ts
+    b = dev_batch(_centered(1, [0.8], [2.0], sigma=5.0))
+    colors = np.array([[0.3, 0.6, 0.9]])
+    tiles = ts.bin_sequential(b)
+    bufs = ts.render(b, tiles, colors, np.zeros(3))
+    g = ts.backward_per_gaussian(bufs, b, tiles, colors, np.ones((32, 32, 3)))
+    expected = float((1.0 - np64(bufs.final_T)).sum())
+    assert np.allclose(np64(g.d_colors)[0], expected, rtol=1e-5)
