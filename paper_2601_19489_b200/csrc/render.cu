@@ -50,7 +50,9 @@ __device__ __forceinline__ bool strip_hit(float mx, float my, float a, float b, 
   float qmin = 0.f;
   if (!(rx0 <= 0.f && rx1 >= 0.f && ry0 <= 0.f && ry1 >= 0.f)) {
     auto q = [&](float dx, float dy) { return fmaf(a * dx, dx, fmaf(2.f * b * dx, dy, c * dy * dy)); };
-    const float bc = -b / c, ba = -b / a;
+    // approximate divides: a slightly-off edge argmin only raises the
+    // candidate q by a second-order amount, far inside the margin below
+    const float bc = __fdividef(-b, c), ba = __fdividef(-b, a);
     const float yx0 = fminf(fmaxf(bc * rx0, ry0), ry1), yx1 = fminf(fmaxf(bc * rx1, ry0), ry1);
     const float xy0 = fminf(fmaxf(ba * ry0, rx0), rx1), xy1 = fminf(fmaxf(ba * ry1, rx0), rx1);
     qmin = fminf(fminf(q(rx0, yx0), q(rx1, yx1)), fminf(q(xy0, ry0), q(xy1, ry1)));
