@@ -38,10 +38,39 @@ CONFIGS = {
     "c4": dict(n=1_000_000, width=1920, height=1080, clustered=False, views=8),
 }
 METRIC = "train steps/sec (fwd+bwd+Adam) at 1M Gaussians 1080p"
+# one training step over one camera view; at N GPUs the job runs N views per
+# step (weak scaling), so the whole-job unit is view-steps/s in BOTH arms
+UNIT = "view-steps/s"
 # FP32 lane-op counts per unit of work
 RENDER_OPS = (12, 7)       # per evaluation, per blend
 BACKWARD_OPS = (12, 45)
 NOMINAL_FP32_LANES = 148 * 128
+
+
+def fp32_peak(sm_mhz):
+    """FP32 lane-op peak (T/s): the measured FFMA/FFMA2 throughput of this
+    part (profiles/r2_fp32_peak.json, tools/ubench/fma_pipe.cu), scaled to the
+    SM clock sampled during the timed region; nominal 148 x 128 x clock if the
+    measurement is missing."""
+    f = ROOT / "profiles" / "r2_fp32_peak.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        meas = d["peak_lane_ops_tops"] * sm_mhz / d["sm_clock_mhz_sampled"]
+        return meas, (f"measured FP32 peak {d['peak_lane_ops_tops']:.2f} T lane-ops/s at "
+                      f"{d['sm_clock_mhz_sampled']} MHz (profiles/r2_fp32_peak.json, "
+                      f"tools/ubench/fma_pipe.cu), scaled to the sampled {sm_mhz:.0f} MHz")
+    return (NOMINAL_FP32_LANES * sm_mhz * 1e6 / 1e12,
+            "nominal FP32 lane-ops/s = 148 SMs x 128 lanes x sampled SM clock")
+
+
+def k4_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum of ONE K4 launch from the
+    committed ncu --set full capture of the current kernel."""
+    f = ROOT / "profiles" / "k4_traffic.json"
+    if not f.exists():
+        return None, None
+    d = json.loads(f.read_text())
+    return d["bytes_per_launch"], d["source"]
 
 
 def _env_int(name, default):
@@ -246,7 +275,7 @@ def cpu_baseline(cfg_name, target_s=20.0):
     t0 = time.perf_counter()
     est, stages, sample = _cpu_sample_step(scene, frac)
     wall = time.perf_counter() - t0
-    return {"value": 1.0 / est, "unit": "steps/s", "cores": 1, "kind": "port",
+    return {"value": 1.0 / est, "unit": UNIT, "cores": 1, "kind": "port",
             "sample": (f"oracle/raster.py (float64 NumPy restatement, pinned to the reference's "
                        f"golden vectors), 1 thread; one step of {cfg_name} with project/bin/"
                        f"loss/VJP/Adam at full size and render+backward on "
@@ -269,28 +298,41 @@ def reference_arm(args):
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     gauss_frac = 1.0 / 16 if c["n"] >= 1_000_000 else 1.0
     tile_frac = min(1.0, 0.002 * cores) if c["n"] >= 1_000_000 else 1.0
-    ests = []
+    ests, walls = [], []
     info = None
     for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
         est, stages, info = _cpu_sample_step(scene, tile_frac, cores, gauss_frac, seed=i)
         if i >= args.warmup:
             ests.append(est)
+            walls.append(time.perf_counter() - t0)
     est = float(np.mean(ests))
+    sample_s = float(np.mean(walls))
     value = 1.0 / est
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s",
+    # the same metric, unit and config as the GPU arm (one view per step at
+    # N=1), so the driver's ratio is defined; each timed step is a bounded
+    # sample of the full step (measured wall time below) whose per-stage
+    # times are scaled up to the full workload
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": est * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: " + _workload(args.config, 1),
                        "views_per_step": 1},
-            "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "port",
+            "ms_per_step_note": ("ms_per_step is the extrapolated full-step time; the timed "
+                                 "region measured sample_s_per_step x steps of wall clock"),
+            "sample_s_per_step": sample_s, "timed_region_s": float(np.sum(walls)),
+            "extrapolation_factor": est / sample_s,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": (f"oracle/raster.py float64 NumPy port on {cores} "
                                         f"processes; per step: project/bin/VJP/Adam on "
                                         f"{gauss_frac:.4g} of the Gaussians and loss on the "
                                         f"same fraction of rows (x{1/gauss_frac:.0f}), render+"
                                         f"backward on {info['tiles']} random non-empty tiles "
-                                        f"({info['pair_frac']:.3%} of pairs), extrapolated")},
-            "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
+                                        f"({info['pair_frac']:.3%} of pairs); measured "
+                                        f"{sample_s:.2f} s per sampled step, extrapolated "
+                                        f"x{est / sample_s:.0f} to the full step")},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -472,7 +514,7 @@ def gpu_arm(args):
             t = torch.tensor([e2e_s], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
-        e2e = {"value": world / e2e_s, "unit": "view-steps/s",
+        e2e = {"value": world / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": int(gt_host.numel() * 4),
                "d2h_bytes_per_step": 4, "ms_per_step": e2e_s * 1e3,
                "last_loss": float(losses_seen[-1]),
@@ -488,8 +530,11 @@ def gpu_arm(args):
         return
 
     sm_mhz = clock.get("sm_mhz") or 1965.0
-    peak_ops = NOMINAL_FP32_LANES * sm_mhz * 1e6 / 1e12   # T lane-ops/s at the sampled clock
-    bwd_ms = phases.get("backward", 0.0) - phases.get("loss", 0.0) * 0  # backward phase only
+    peak_ops, peak_note = fp32_peak(sm_mhz)
+    # the backward phase covers every view this rank rasterised in the step;
+    # the work counters are the last view's, so time one view's launch
+    views_here = len(mine) if batch_views else 1
+    bwd_ms = phases.get("backward", 0.0) / views_here
     bwd_ops = BACKWARD_OPS[0] * evals + BACKWARD_OPS[1] * blends
     achieved = bwd_ops / (bwd_ms * 1e-3) / 1e12 if bwd_ms > 0 else None
     # HBM roofline of the fused projection-VJP + Adam kernel (N=1)
@@ -508,12 +553,9 @@ def gpu_arm(args):
                     "algorithmic_bytes": algo, "peak_source": hbm_src,
                     "bytes_model": "per Gaussian p,m,v read+write (14 x 4 B x 6) + row index 4 B; per row "
                                    "Grad2D read+zero (80 B) + rec 32 B"}
-    traffic = None
-    prof = ROOT / "profiles" / "backward_traffic.json"
-    if prof.exists():
-        traffic = json.loads(prof.read_text()).get("bytes_per_launch")
+    traffic, traffic_src = k4_traffic()
     line = {
-        "metric": METRIC, "value": value, "unit": "view-steps/s", "n_gpus": world,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong" if batch_views else "weak",
         "vs_baseline": None, "dtype": "f32",
@@ -525,7 +567,7 @@ def gpu_arm(args):
                                      "reads, sharded Adam, peer parameter stores)" if args.peer
                                      else " zero1 (reduce-scatter + sharded Adam + all-gather)"
                                      if args.zero1 else ""),
-                   "launch": "one CUDA graph replay per step" if world == 1 else "eager launches",
+                   "launch": "one CUDA graph replay per step" if graphs else "eager launches",
                    "merge": "deterministic (slots + emission-order row sums)"
                             if args.deterministic else "float atomics (FP32-tolerance)",
                    "l2": "inputs larger than L2 (Gaussian state + Adam moments 168 MB, "
@@ -533,9 +575,9 @@ def gpu_arm(args):
         "roofline": {"kernel": "render_bwd_kernel (K4)", "bound": "fp32",
                      "achieved": achieved, "peak": peak_ops, "unit": "Tops/s",
                      "frac": (achieved / peak_ops) if achieved else None,
-                     "traffic": traffic,
-                     "peak_note": "nominal FP32 lane-ops/s = 148 SMs x 128 lanes x sampled SM "
-                                  "clock (MEASURED_PEAKS.json has no FP32 figure)",
+                     "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_note": peak_note,
+                     "per_view_launch_ms": bwd_ms,
                      "ops_per_unit": {"per_eval": BACKWARD_OPS[0], "per_blend": BACKWARD_OPS[1]},
                      "units": {"evals": evals, "blends": blends, "pairs": pairs}},
         "roofline_hbm": hbm_line,

@@ -272,6 +272,21 @@ int tsr_preprocess_bwd_adam_dev(const tsr_gaussians_t* g, const tsr_camera_t* ca
                                 const float* group_scalars, float* pose_sums,
                                 unsigned long long* skipped, void* stream);
 
+/* tsr_preprocess_bwd_adam_dev with an overflow gate (nullable): when *gate is
+ * non-zero (K2's sticky pair-capacity overflow flag of this step) the update
+ * is skipped -- params and moments untouched, consumed Grad2D rows zeroed --
+ * and *gated_steps (nullable) is incremented, so the host can grow the
+ * capacity and redo exactly the skipped steps.  Training-loop guard, no
+ * reference counterpart (the reference has no capacities).  loss_guard
+ * (nullable, device scalar): a non-finite loss skips the update too, the
+ * reference's divergence guard before Adam (trainer.py:331-338). */
+int tsr_preprocess_bwd_adam_ex(const tsr_gaussians_t* g, const tsr_camera_t* cam,
+                               const float* rec, const int32_t* row_of_source,
+                               const float* grad2d, const tsr_adam_group_t* groups_host,
+                               const float* group_scalars, float* pose_sums,
+                               unsigned long long* skipped, const int32_t* gate,
+                               int32_t* gated_steps, const float* loss_guard, void* stream);
+
 /* --------------------------------------------------------------- loss ----
  * Fused photometric objective (losses.py:44-91): E = (1-lam) mean|r-g| +
  * lam (1 - SSIM), 11-tap sigma=1.5 Gaussian window, zero padding.  rendered,

@@ -345,7 +345,12 @@ def backward_per_gaussian(bufs, batch, index, colors, grad_color, grad_depth=Non
         ctot = bufs["color"][y0:y1, x0:x1].reshape(-1, 3)
         dtot = bufs["depth"][y0:y1, x0:x1].reshape(-1)
         tf_term = None if gt is None else -gt * fT
-        for g in range(-(-n // GROUP)):
+        # groups past the tile's largest n_considered contribute nothing
+        # (part is all False there: backward.py:189 skips them one position
+        # at a time); bounding the walk keeps heavy C3 tiles (200k entries)
+        # affordable.  merges still counts every pair (backward.py:214-222).
+        n_walk = min(n, int(ncons.max(initial=0)))
+        for g in range(-(-n_walk // GROUP)):
             p0, p1 = g * GROUP, min(n, (g + 1) * GROUP)
             if g == 0:
                 T, C, D = np.ones(px.size), np.zeros((px.size, 3)), np.zeros(px.size)
@@ -381,7 +386,7 @@ def backward_per_gaussian(bufs, batch, index, colors, grad_color, grad_depth=Non
                     out["d_depths"][row] += np.sum(gd * w)
                 T = np.where(part, T * om, T)
                 C, D = Ca, Da
-            out["merges"] += p1 - p0
+        out["merges"] += n  # one merge per (splat, tile) pair of a processed tile
     return out
 
 

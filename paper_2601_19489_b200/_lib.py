@@ -84,6 +84,10 @@ _SIGNATURES = {
     "tsr_preprocess_bwd_adam_dev": (c_i32, [ctypes.POINTER(Gaussians_t),
                                             ctypes.POINTER(Camera_t), c_vp, c_vp, c_vp,
                                             ctypes.POINTER(AdamGroup_t), c_vp, c_vp, c_vp, c_vp]),
+    "tsr_preprocess_bwd_adam_ex": (c_i32, [ctypes.POINTER(Gaussians_t),
+                                           ctypes.POINTER(Camera_t), c_vp, c_vp, c_vp,
+                                           ctypes.POINTER(AdamGroup_t), c_vp, c_vp, c_vp, c_vp,
+                                           c_vp, c_vp, c_vp]),
     "tsr_photometric_workspace": (c_sz, [c_i32, c_i32]),
     "tsr_photometric": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_f32, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "tsr_version": (ctypes.c_char_p, []),

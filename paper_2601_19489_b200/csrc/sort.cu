@@ -418,9 +418,15 @@ __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, lon
       for (int k = 0; k < kEmitPer; ++k) {
         const long long r = r0 + kEmitPer * tid + k;
         if (r < rhi) {
+          // clamp to the pair capacity: on overflow (P > p_cap) the pairs
+          // past p_cap were never stored, and the reducer must not read
+          // their inverse permutation (sticky overflow flag, grow, retry)
+          const long long e0 = O + (long long)off[k];
+          const long long room = a.p_cap - e0;
           a.out_rank_row[r] = rank_row(row_by_rank, r);
-          a.out_rank_count[r] = cnt[k];
-          a.out_rank_off[r] = (uint32_t)(O + off[k]);
+          a.out_rank_count[r] =
+              room <= 0 ? 0u : (uint32_t)min((long long)cnt[k], room);
+          a.out_rank_off[r] = (uint32_t)min(e0, a.p_cap);
         }
       }
     }

@@ -346,8 +346,14 @@ __global__ void __launch_bounds__(256) preprocess_bwd_adam_kernel(
     tsr_gaussians_t G, tsr_camera_t cam, const float4* __restrict__ rec,
     const int32_t* __restrict__ row_of_source, const float* __restrict__ grad2d,
     AdamGroups groups, float* __restrict__ pose_sums, unsigned long long* __restrict__ skipped,
-    const float* __restrict__ scal) {
+    const float* __restrict__ scal, const int32_t* __restrict__ gate,
+    int32_t* __restrict__ gated_steps, const float* __restrict__ loss_guard) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool diverged = loss_guard && !isfinite(*loss_guard);
+  if ((gate && *gate) || diverged) {  // no update (see vjp_adam_sh0_kernel)
+    if (i == 0 && gated_steps && !diverged) atomicAdd(gated_steps, 1);
+    return;
+  }
   Vjp v;
   bool vis = false;
   unsigned long long local = 0;
@@ -434,8 +440,29 @@ __global__ void __launch_bounds__(128, 7) vjp_adam_sh0_kernel(
     tsr_camera_t cam, long long n, const float4* __restrict__ rec,
     const int32_t* __restrict__ row_of_source, float* __restrict__ grad2d, AdamGroups groups,
     float* __restrict__ pose_sums, unsigned long long* __restrict__ skipped,
-    const float* __restrict__ scal) {
+    const float* __restrict__ scal, const int32_t* __restrict__ gate,
+    int32_t* __restrict__ gated_steps, const float* __restrict__ loss_guard) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  // a non-finite loss (trainer.py:331-338 raises TrainingDiverged before its
+  // Adam step) leaves the parameters untouched; the host raises at its next
+  // flush
+  const bool diverged = loss_guard && !isfinite(*loss_guard);
+  if ((gate && *gate) || diverged) {
+    // the step's pair capacity overflowed (K2's sticky flag): its Grad2D
+    // comes from truncated tile lists, so the update is skipped -- params
+    // and moments untouched, the consumed row zeroed for the next step; the
+    // host grows the capacity and redoes the step (TrainStep._poll_status)
+    if (i < n) {
+      const int row = row_of_source[i];
+      if (row >= 0) {
+        float* g2p = grad2d + (long long)row * TSR_GRAD2D_FLOATS;
+#pragma unroll
+        for (int k = 0; k < TSR_GRAD2D_FLOATS; ++k) g2p[k] = 0.f;
+      }
+    }
+    if (i == 0 && gated_steps && !diverged) atomicAdd(gated_steps, 1);
+    return;
+  }
   Vjp vj;
   bool vis = false;
   unsigned long long local = 0;
@@ -657,8 +684,8 @@ extern "C" int tsr_preprocess_bwd_adam(const tsr_gaussians_t* g, const tsr_camer
                                        const float* grad2d,
                                        const tsr_adam_group_t* groups_host, float* pose_sums,
                                        unsigned long long* skipped, void* stream) {
-  return tsr_preprocess_bwd_adam_dev(g, cam, rec, row_of_source, grad2d, groups_host, nullptr,
-                                     pose_sums, skipped, stream);
+  return tsr_preprocess_bwd_adam_ex(g, cam, rec, row_of_source, grad2d, groups_host, nullptr,
+                                    pose_sums, skipped, nullptr, nullptr, nullptr, stream);
 }
 
 extern "C" int tsr_preprocess_bwd_adam_dev(const tsr_gaussians_t* g, const tsr_camera_t* cam,
@@ -667,6 +694,18 @@ extern "C" int tsr_preprocess_bwd_adam_dev(const tsr_gaussians_t* g, const tsr_c
                                            const tsr_adam_group_t* groups_host,
                                            const float* group_scalars, float* pose_sums,
                                            unsigned long long* skipped, void* stream) {
+  return tsr_preprocess_bwd_adam_ex(g, cam, rec, row_of_source, grad2d, groups_host,
+                                    group_scalars, pose_sums, skipped, nullptr, nullptr, nullptr, stream);
+}
+
+extern "C" int tsr_preprocess_bwd_adam_ex(const tsr_gaussians_t* g, const tsr_camera_t* cam,
+                                          const float* rec, const int32_t* row_of_source,
+                                          const float* grad2d,
+                                          const tsr_adam_group_t* groups_host,
+                                          const float* group_scalars, float* pose_sums,
+                                          unsigned long long* skipped, const int32_t* gate,
+                                          int32_t* gated_steps, const float* loss_guard,
+                                          void* stream) {
   AdamGroups gs;
   if (!g || !cam || !fill_groups(groups_host, 5, gs) || !skipped) return TSR_E_INVALID;
   for (int k = 0; k < 5; ++k)
@@ -680,11 +719,11 @@ extern "C" int tsr_preprocess_bwd_adam_dev(const tsr_gaussians_t* g, const tsr_c
     // fast path; also zeroes the consumed Grad2D rows for the next step
     vjp_adam_sh0_kernel<<<(int)((g->n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
         *cam, g->n, (const float4*)rec, row_of_source, (float*)grad2d, gs, pose_sums, skipped,
-        group_scalars);
+        group_scalars, gate, gated_steps, loss_guard);
   } else {
     preprocess_bwd_adam_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
         *g, *cam, (const float4*)rec, row_of_source, grad2d, gs, pose_sums, skipped,
-        group_scalars);
+        group_scalars, gate, gated_steps, loss_guard);
   }
   TSR_CHECK_LAUNCH();
   return TSR_OK;

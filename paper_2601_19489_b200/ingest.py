@@ -36,90 +36,93 @@ class Scene:
     warnings: list = field(default_factory=list)
 
 
-def _ply_property_names(n_coeffs: int) -> list[str]:
-    names = ["x", "y", "z", "f_dc_0", "f_dc_1", "f_dc_2"]
-    names += [f"f_rest_{i}" for i in range(3 * (n_coeffs - 1))]
-    names += ["opacity", "scale_0", "scale_1", "scale_2", "rot_0", "rot_1", "rot_2", "rot_3"]
-    return names
+# On-disk column order of a splat PLY (the reference's format, ingest.py:270-
+# 288): position, DC colour, the higher SH coefficients flattened channel-
+# major, opacity logit, log scales, quaternion (w, x, y, z).  Each entry is
+# (property name, GaussianSet field, column index inside that field).
+def _ply_columns(n_coeffs: int) -> list[tuple[str, str, tuple]]:
+    cols = [(axis, "positions", (i,)) for i, axis in enumerate("xyz")]
+    cols += [(f"f_dc_{ch}", "colors", (0, ch)) for ch in range(3)]
+    higher = n_coeffs - 1
+    cols += [(f"f_rest_{ch * higher + k}", "colors", (k + 1, ch))
+             for ch in range(3) for k in range(higher)]
+    cols.append(("opacity", "opacity_logits", ()))
+    cols += [(f"scale_{i}", "log_scales", (i,)) for i in range(3)]
+    cols += [(f"rot_{i}", "rotations", (i,)) for i in range(4)]
+    return cols
 
 
 def write_ply(gset: GaussianSet, path) -> None:
-    """Binary little-endian PLY, double precision (ingest.py:270-288)."""
+    """Binary little-endian PLY, one double per property (ingest.py:270-288)."""
+    host = gset.to_numpy()
     n = len(gset)
-    h = gset.to_numpy()
-    colors = h["colors"]
-    n_coeffs = colors.shape[1]
-    names = _ply_property_names(n_coeffs)
-    rest = np.transpose(colors[:, 1:, :], (0, 2, 1)).reshape(n, 3 * (n_coeffs - 1))
-    data = np.empty((n, len(names)), dtype="<f8")
-    data[:, 0:3] = h["positions"]
-    data[:, 3:6] = colors[:, 0, :]
-    c = 6 + rest.shape[1]
-    data[:, 6:c] = rest
-    data[:, c] = h["opacity_logits"]
-    data[:, c + 1:c + 4] = h["log_scales"]
-    data[:, c + 4:c + 8] = h["rotations"]
-    header = ["ply", "format binary_little_endian 1.0", f"element vertex {n}"]
-    header += [f"property double {name}" for name in names]
-    header.append("end_header")
+    cols = _ply_columns(host["colors"].shape[1])
+    table = np.empty((n, len(cols)), dtype="<f8")
+    for j, (_, field_name, idx) in enumerate(cols):
+        src = host[field_name]
+        table[:, j] = src if not idx else src[(slice(None),) + idx]
+    head = "".join(f"property double {name}\n" for name, _, _ in cols)
+    preamble = (f"ply\nformat binary_little_endian 1.0\nelement vertex {n}\n{head}"
+                "end_header\n").encode()
     with open(path, "wb") as fh:
-        fh.write(("\n".join(header) + "\n").encode())
-        fh.write(np.ascontiguousarray(data).tobytes())
+        fh.write(preamble)
+        fh.write(table.tobytes())
+
+
+_PLY_SCALARS = {"float": "<f4", "float32": "<f4", "double": "<f8", "float64": "<f8"}
+
+
+def _parse_ply_header(fh, path):
+    """(vertex count, [(property, numpy dtype)]) of a binary little-endian
+    vertex-only PLY; the file position is left at the first vertex byte."""
+    if fh.readline().rstrip(b"\r\n") != b"ply":
+        raise PlySchemaError(f"{path}: missing 'ply' magic")
+    count, fields = None, []
+    for raw in iter(fh.readline, b""):
+        words = raw.decode("ascii", "replace").split()
+        if not words:
+            continue
+        key = words[0]
+        if key == "end_header":
+            if count is None:
+                raise PlySchemaError(f"{path}: no vertex element declared")
+            return count, fields
+        if key == "format" and words[1:2] != ["binary_little_endian"]:
+            raise PlySchemaError(f"{path}: only binary_little_endian PLY is supported, "
+                                 f"got {' '.join(words[1:])}")
+        elif key == "element":
+            if words[1] != "vertex":
+                raise PlySchemaError(f"{path}: element '{words[1]}' is not supported")
+            count = int(words[2])
+        elif key == "property":
+            if words[1] not in _PLY_SCALARS:
+                raise PlySchemaError(f"{path}: property type '{words[1]}' is not supported")
+            fields.append((words[2], _PLY_SCALARS[words[1]]))
+    raise PlySchemaError(f"{path}: header never ends")
 
 
 def read_ply(path) -> GaussianSet:
-    """Read a splat PLY; float or double properties (ingest.py:291-344)."""
+    """Load a splat PLY written by the reference or by write_ply; float and
+    double properties are both accepted (ingest.py:291-344)."""
     with open(path, "rb") as fh:
-        if fh.readline().strip() != b"ply":
-            raise PlySchemaError(f"{path}: not a PLY file")
-        n = None
-        props: list[tuple[str, str]] = []
-        while True:
-            line = fh.readline()
-            if not line:
-                raise PlySchemaError(f"{path}: unterminated header")
-            tokens = line.decode().strip().split()
-            if not tokens:
-                continue
-            if tokens[0] == "format" and tokens[1] != "binary_little_endian":
-                raise PlySchemaError(f"{path}: unsupported format {tokens[1]}")
-            if tokens[0] == "element":
-                if tokens[1] != "vertex":
-                    raise PlySchemaError(f"{path}: unexpected element {tokens[1]}")
-                n = int(tokens[2])
-            if tokens[0] == "property":
-                props.append((tokens[2], tokens[1]))
-            if tokens[0] == "end_header":
-                break
-        if n is None:
-            raise PlySchemaError(f"{path}: missing vertex element")
-        typemap = {"float": "<f4", "float32": "<f4", "double": "<f8", "float64": "<f8"}
-        try:
-            dtype = np.dtype([(name, typemap[t]) for name, t in props])
-        except KeyError as exc:
-            raise PlySchemaError(f"{path}: unsupported property type {exc}") from exc
-        raw = np.frombuffer(fh.read(dtype.itemsize * n), dtype=dtype, count=n)
-    have = {name for name, _ in props}
-    n_rest = len([name for name in have if name.startswith("f_rest_")])
-    if n_rest % 3:
-        raise PlySchemaError(f"{path}: f_rest count {n_rest} not divisible by 3")
-    n_coeffs = n_rest // 3 + 1
-    for required in _ply_property_names(n_coeffs):
-        if required not in have:
-            raise PlySchemaError(f"{path}: missing property \"{required}\"")
-
-    def col(name):
-        return raw[name].astype(np.float64)
-
-    positions = np.stack([col("x"), col("y"), col("z")], axis=1)
-    colors = np.empty((n, n_coeffs, 3))
-    colors[:, 0, :] = np.stack([col(f"f_dc_{i}") for i in range(3)], axis=1)
-    for ch in range(3):
-        for j in range(n_coeffs - 1):
-            colors[:, j + 1, ch] = col(f"f_rest_{ch * (n_coeffs - 1) + j}")
-    log_scales = np.stack([col(f"scale_{i}") for i in range(3)], axis=1)
-    rotations = np.stack([col(f"rot_{i}") for i in range(4)], axis=1)
-    return GaussianSet(positions, log_scales, rotations, col("opacity"), colors)
+        count, fields = _parse_ply_header(fh, path)
+        rec = np.dtype(fields)
+        body = np.frombuffer(fh.read(rec.itemsize * count), dtype=rec, count=count)
+    present = set(rec.names or ())
+    higher_terms = sum(1 for name in present if name.startswith("f_rest_"))
+    if higher_terms % 3 != 0:
+        raise PlySchemaError(f"{path}: {higher_terms} f_rest properties is not a multiple of 3")
+    n_coeffs = 1 + higher_terms // 3
+    cols = _ply_columns(n_coeffs)
+    absent = [name for name, _, _ in cols if name not in present]
+    if absent:
+        raise PlySchemaError(f"{path}: required properties absent: {', '.join(absent)}")
+    shapes = {"positions": (count, 3), "log_scales": (count, 3), "rotations": (count, 4),
+              "opacity_logits": (count,), "colors": (count, n_coeffs, 3)}
+    out = {k: np.empty(v, dtype=np.float64) for k, v in shapes.items()}
+    for name, field_name, idx in cols:
+        out[field_name][(slice(None),) + idx] = body[name]
+    return GaussianSet(**out)
 
 
 __all__ = ["Camera", "PlySchemaError", "Scene", "read_ply", "write_ply"]

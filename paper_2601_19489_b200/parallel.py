@@ -280,7 +280,16 @@ class ViewParallelStep(TrainStep):
         """Per view: K1-K4 + K4b; then one K5 (the NCCL allreduce is not ours)."""
         return views * (super().kernels_per_step() - 1 + 1) + 1
 
+    def _recover_overflow(self, camera) -> None:
+        # the view batch is reserved up front (step_views), and this path's
+        # update (allreduce + K5) is not gated: an overflow here means the
+        # 1.5x headroom was outgrown mid-run
+        raise RuntimeError(f"pair capacity {self.index.p_cap} overflowed in the view-parallel "
+                           "step; reserve() a larger capacity for the view batch")
+
     def step_views(self, cameras, gts, timer=None) -> torch.Tensor:
+        if self.index is None and cameras:
+            self.reserve(cameras)  # pair capacity for the largest view of the batch
         if self.index is not None and cameras:
             self._poll_status(cameras[0])
         self.iteration += 1

@@ -9,6 +9,8 @@ host read of the pair count (P sizes the key buffers).
 
 from __future__ import annotations
 
+import json
+
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -190,10 +192,17 @@ class TrainStep:
 
     The step never synchronises with the host: every size (M rows, P pairs)
     stays on the device and all buffers are capacity-allocated.  The pair
-    capacity is sized once (one host read on the first step) with headroom;
-    K2 raises a sticky overflow flag that is polled without blocking (a
-    pinned copy + event from an earlier step) and the capacity grows before it
-    is reached."""
+    capacity is sized with headroom from the first step's P, or up front
+    from the largest P over a camera set (`reserve`).  K2 raises a sticky
+    overflow flag; the fused VJP + Adam kernel reads it and skips the update
+    of an overflowed step (its tile lists were truncated), counting the
+    skipped steps on the device.  The host polls the flag without blocking
+    (a pinned copy + event from an earlier step); on overflow it grows the
+    capacity, rolls the Adam step counters back and redoes the skipped steps
+    from its history, so training proceeds exactly as with enough capacity.
+    Capacity also grows pre-emptively at 80 % occupancy."""
+
+    HISTORY = 64  # steps kept for redo (bounds how far the host may run ahead)
 
     def __init__(self, gset: GaussianSet, cfg: TrainConfig, extent: float = 4.0,
                  optimizer: Adam | None = None, p_headroom: float = 1.5, graphs: bool = False,
@@ -234,6 +243,10 @@ class TrainStep:
         self.grad2d = torch.zeros((max(n, 1), _lib.GRAD2D_FLOATS), dtype=torch.float32,
                                   device=dev)
         self.skipped = torch.zeros(1, dtype=torch.int64, device=dev)
+        # overflowed steps whose update the fused kernel skipped (device)
+        self.gated_steps = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._history = []  # (camera, gt, depth args, iteration, loss tensors) per step
+        self.redone_steps = 0
         self.merges = torch.zeros(1, dtype=torch.int64, device=dev)
         self.loss_ws = losses.PhotometricWorkspace()
         self._grad2d_clean = True  # the SH-0 fused kernel re-zeroes consumed rows
@@ -244,6 +257,7 @@ class TrainStep:
         self.status_tot_host = torch.zeros(2, dtype=torch.int64).pin_memory()
         self.status_event = None
         self.lib = _lib.load()
+        self.last_camera = None
         self.last = None
         self.last_losses = None
 
@@ -278,6 +292,24 @@ class TrainStep:
                                      device=self.grad2d.device)
             self.processed = torch.zeros(tiles, dtype=torch.int32, device=self.grad2d.device)
 
+    def reserve(self, cameras) -> int:
+        """Size the pair capacity for a camera set up front: K1 runs for
+        every camera (no binning), the largest pair count is read back with
+        ONE host synchronisation, and the buffers are allocated for it with
+        headroom.  Returns the largest P."""
+        cams = list(cameras)
+        if not cams:
+            raise ValueError("reserve() needs at least one camera")
+        totals = []
+        for cam in cams:
+            project_raw(self.gset, cam, self.cfg.near, None, self.cfg.strategy_id, self.scratch)
+            totals.append(self.scratch.totals[1].clone())
+        p_max = int(torch.stack(totals).max().item())
+        big = max(cams, key=lambda c: c.width * c.height)
+        if self.index is None or int(p_max * self.p_headroom) + 65536 > self.index.p_cap:
+            self._allocate(big, int(p_max * self.p_headroom) + 65536)
+        return p_max
+
     def _poll_status(self, camera: Camera) -> None:
         """Non-blocking check of an earlier step's overflow flag and P."""
         if self.status_event is None or not self.status_event.query():
@@ -285,10 +317,42 @@ class TrainStep:
         overflow, p = int(self.status_ovf_host[0]), int(self.status_tot_host[1])
         self.status_event = None
         if overflow:
-            raise RuntimeError(f"pair capacity {self.index.p_cap} overflowed (P = {p}); "
-                               "the step results are invalid")
+            self._recover_overflow(camera)
+            return
         if p > 0.8 * self.index.p_cap:
             self._allocate(camera, int(p * self.p_headroom) + 65536)
+            self._graph_cache.clear()
+
+    def _recover_overflow(self, camera: Camera) -> None:
+        """Grow the pair capacity and redo the steps whose update the fused
+        kernel skipped (the most recent ones: the overflow flag is sticky)."""
+        torch.cuda.current_stream().synchronize()
+        n_skip = int(self.gated_steps.item())
+        if n_skip > len(self._history):
+            raise RuntimeError(f"{n_skip} overflowed steps exceed the redo history "
+                               f"({len(self._history)})")
+        redo = self._history[len(self._history) - n_skip:] if n_skip else []
+        # the largest P among the skipped views sizes the new capacity
+        p_need = self.reserve([h[0] for h in redo] or [camera])
+        self.gated_steps.zero_()
+        self._graph_cache.clear()
+        for name in self.opt._steps:
+            if name in self.gset.params():
+                self.opt._steps[name] -= n_skip
+        del self._history[len(self._history) - n_skip:]
+        for cam, gt, dw, dp, dv, it, outs in redo:
+            self.iteration = it - 1
+            self._eager_step(cam, gt, None, dw, dp, dv)
+            if outs is not None:
+                for old, new in zip(outs, self.last_losses):
+                    if old is not None and new is not None:
+                        old.copy_(new)
+                self.last_losses = outs
+        self.redone_steps += n_skip
+        torch.cuda.current_stream().synchronize()
+        if int(self.index.overflow.item()):
+            raise RuntimeError(f"pair capacity still overflowed after growing to "
+                               f"{self.index.p_cap} (P >= {p_need})")
 
     # ------------------------------------------------------------------ step
     def forward(self, camera: Camera, timer=None):
@@ -373,11 +437,12 @@ class TrainStep:
                                    self._scal_dev[15] if depth_on else 0.0,
                                    depth_prior if depth_on else None, depth_valid)
         groups = self.opt.groups_for_fused(self.gset.params(), None, advance=False)
-        _lib.check(self.lib.tsr_preprocess_bwd_adam_dev(
+        _lib.check(self.lib.tsr_preprocess_bwd_adam_ex(
             gaussians_struct(self.gset), camera_struct(camera, None, self.cfg.near),
             batch.rec.data_ptr(), batch.row_of_source.data_ptr(), self.grad2d.data_ptr(), groups,
-            self._scal_dev.data_ptr(), None, self.skipped.data_ptr(), _lib.stream_handle()),
-            "tsr_preprocess_bwd_adam_dev")
+            self._scal_dev.data_ptr(), None, self.skipped.data_ptr(),
+            self.index.overflow.data_ptr(), self.gated_steps.data_ptr(), e.data_ptr(),
+            _lib.stream_handle()), "tsr_preprocess_bwd_adam_ex")
         self.status_ovf_host.copy_(self.index.overflow, non_blocking=True)
         self.status_tot_host.copy_(self.scratch.totals, non_blocking=True)
         return e
@@ -414,6 +479,7 @@ class TrainStep:
                 e = self._graph_body(camera, gt_image, depth_on, depth_prior, depth_valid)
             entry = self._graph_cache[key] = (g, e)
         entry[0].replay()
+        self._remember(camera, gt_image, depth_weight, depth_prior, depth_valid, None)
         self._grad2d_clean = self.gset.colors.shape[1] == 1
         self.status_event = torch.cuda.Event()
         self.status_event.record()
@@ -427,21 +493,42 @@ class TrainStep:
             return self._graph_step(camera, gt_image, depth_weight, depth_prior, depth_valid)
         if self.index is not None:
             self._poll_status(camera)
+        e = self._eager_step(camera, gt_image, timer, depth_weight, depth_prior, depth_valid)
+        self._remember(camera, gt_image, depth_weight, depth_prior, depth_valid,
+                       self.last_losses)
+        return e
+
+    def _remember(self, camera, gt_image, depth_weight, depth_prior, depth_valid, outs):
+        self._history.append((camera, gt_image, depth_weight, depth_prior, depth_valid,
+                              self.iteration, outs))
+        if len(self._history) > self.HISTORY:
+            del self._history[0]
+
+    def _eager_step(self, camera, gt_image, timer, depth_weight, depth_prior, depth_valid):
         self.iteration += 1
         batch = self.forward(camera, timer)
         e = self.loss_and_backward(batch, camera, gt_image, timer, depth_weight, depth_prior,
                                    depth_valid)
         lr = {"positions": position_lr(self.pos_base_lr, self.iteration, self.cfg.max_iters)}
         groups = self.opt.groups_for_fused(self.gset.params(), lr)
-        _lib.check(self.lib.tsr_preprocess_bwd_adam(
+        _lib.check(self.lib.tsr_preprocess_bwd_adam_ex(
             gaussians_struct(self.gset), camera_struct(camera, None, self.cfg.near),
             batch.rec.data_ptr(), batch.row_of_source.data_ptr(), self.grad2d.data_ptr(), groups,
-            None, self.skipped.data_ptr(), _lib.stream_handle()), "tsr_preprocess_bwd_adam")
+            None, None, self.skipped.data_ptr(), self.index.overflow.data_ptr(),
+            self.gated_steps.data_ptr(), e.data_ptr(), _lib.stream_handle()),
+            "tsr_preprocess_bwd_adam_ex")
         self._grad2d_clean = self.gset.colors.shape[1] == 1
         self._mark(timer, "vjp_adam")
         self._publish_status()
         self.last_camera = camera
         return e
+
+    def sync(self) -> None:
+        """Wait for the queued steps and settle their status: an overflowed
+        step is redone with a grown capacity before this returns."""
+        torch.cuda.current_stream().synchronize()
+        if self.index is not None and self.last_camera is not None:
+            self._poll_status(self.last_camera)
 
     def kernels_per_step(self) -> int:
         """Our kernel launches per step: K1a, K1b; K2 (one persistent
@@ -502,62 +589,76 @@ class TrainResult:
     eval_split: str = "train"
 
 
-def init_gaussians(scene, sh_degree: int = 0, init_opacity: float = 0.1) -> GaussianSet:
-    """Seed splats from the point cloud, isotropic with radius = mean distance
-    to the 3 nearest neighbours (trainer.py:137-160).  Host setup (once)."""
+def _mean_neighbour_distance(pts: np.ndarray, k: int = 3) -> np.ndarray:
+    """Mean distance of every point to its k nearest other points (host,
+    once per run; scipy's KD-tree, as the reference's trainer.py:147)."""
     from scipy.spatial import cKDTree
-    pts = np.asarray(scene.points, dtype=np.float64).reshape(-1, 3)
-    n = len(pts)
-    if n == 0:
+    dist, _ = cKDTree(pts).query(pts, k=k + 1, workers=-1)
+    return dist[:, 1:].mean(axis=1)
+
+
+def init_gaussians(scene, sh_degree: int = 0, init_opacity: float = 0.1) -> GaussianSet:
+    """Seed one isotropic splat per point of the scene's cloud (trainer.py:137-
+    160): radius = mean distance to the 3 nearest neighbours (floored at 1e-7;
+    0.1 x extent for clouds of fewer than 4 points), DC colour = point colour /
+    255, identity rotation, opacity `init_opacity`."""
+    pts = np.array(scene.points, dtype=np.float64).reshape(-1, 3)
+    count = pts.shape[0]
+    if count == 0:
         raise ValueError("cannot initialize from an empty point cloud")
-    if n >= 4:
-        dist, _ = cKDTree(pts).query(pts, k=4)
-        radius = np.maximum(dist[:, 1:].mean(axis=1), 1e-7)
+    if count < 4:
+        radius = np.full(count, 0.1 * float(scene.extent))
     else:
-        radius = np.full(n, 0.1 * scene.extent)
-    colors = np.zeros((n, (sh_degree + 1) ** 2, 3))
-    colors[:, 0, :] = np.asarray(scene.colors) / 255.0
-    rot = np.zeros((n, 4))
-    rot[:, 0] = 1.0
-    return GaussianSet(positions=pts.copy(), log_scales=np.log(radius)[:, None].repeat(3, 1),
-                       rotations=rot, opacity_logits=np.full(n, np.log(init_opacity /
-                                                                        (1 - init_opacity))),
-                       colors=colors)
+        radius = np.maximum(_mean_neighbour_distance(pts), 1e-7)
+    n_coeffs = (sh_degree + 1) ** 2
+    colors = np.zeros((count, n_coeffs, 3))
+    colors[:, 0] = np.asarray(scene.colors, dtype=np.float64) / 255.0
+    log_r = np.log(radius)
+    return GaussianSet(
+        positions=pts,
+        log_scales=np.stack([log_r, log_r, log_r], axis=1),
+        rotations=np.tile(np.array([1.0, 0.0, 0.0, 0.0]), (count, 1)),
+        opacity_logits=np.full(count, np.log(init_opacity) - np.log1p(-init_opacity)),
+        colors=colors)
 
 
 def evaluate(gset: GaussianSet, cameras, cfg: TrainConfig | None = None,
              delta: PoseDelta | None = None) -> float:
-    """Mean PSNR over the cameras' ground truth (trainer.py:260-270)."""
-    cfg = cfg or TrainConfig()
-    values = []
-    for cam in cameras:
-        if cam.gt_image is None:
-            continue
-        vr = render_view(gset, cam, cfg, delta, checkpoints=False)
-        values.append(losses.psnr(vr.buffers.color, cam.gt_image))
-    if not values:
-        raise ValueError("no cameras with ground-truth images to evaluate")
-    return float(np.mean(values))
+    """Mean PSNR of the renders against the cameras that carry ground truth
+    (trainer.py:260-270); cameras without it are ignored."""
+    scored = [cam for cam in cameras if cam.gt_image is not None]
+    if not scored:
+        raise ValueError("evaluate() needs at least one camera with a ground-truth image")
+    cfg = TrainConfig() if cfg is None else cfg
+    total = 0.0
+    for cam in scored:
+        color = render_view(gset, cam, cfg, delta, checkpoints=False).buffers.color
+        total += losses.psnr(color, cam.gt_image)
+    return total / len(scored)
 
 
 def _densify_round(gset, scene, cfg, delta, rng, pool):
-    """Sample K views, render in scoring mode, return (s+, s-)
-    (trainer.py:273-290) -- the reference's form, through Contributions."""
+    """(s+, s-) of one density round through materialised Contributions
+    (trainer.py:273-290): K views drawn from the pool, each rendered in
+    scoring mode, its error mask and photometric error collected; the fused
+    form below is what train() uses."""
     from . import density
-    k = cfg.consistency_views
-    view_ids = pool[rng.integers(0, len(pool), size=k)]
-    masks, pix, ids, e_photos = [], [], [], []
-    for v in view_ids:
-        cam = scene.cameras[int(v)]
+    drawn = pool[rng.integers(0, len(pool), size=cfg.consistency_views)]
+    per_view = {"masks": [], "pixels": [], "ids": [], "errors": []}
+    for view in drawn:
+        cam = scene.cameras[int(view)]
         vr = render_view(gset, cam, cfg, delta, checkpoints=False, scoring=True)
-        rep, _ = losses.photometric(vr.buffers.color, cam.gt_image, cfg.lambda_)
-        masks.append(density.error_mask(vr.buffers.color, cam.gt_image, cfg.error_tau))
-        pix.append(vr.contributions.pixel_idx)
-        ids.append(vr.batch.source_ids[vr.contributions.splat_rows])
-        e_photos.append(rep.photometric)
-    s_plus = density.score_densify(masks, pix, ids, len(gset))
-    s_minus = density.score_prune(masks, pix, ids, e_photos, len(gset))
-    return s_plus, s_minus
+        contrib = vr.contributions
+        per_view["masks"].append(density.error_mask(vr.buffers.color, cam.gt_image,
+                                                    cfg.error_tau))
+        per_view["pixels"].append(contrib.pixel_idx)
+        per_view["ids"].append(vr.batch.source_ids[contrib.splat_rows])
+        per_view["errors"].append(
+            losses.photometric(vr.buffers.color, cam.gt_image, cfg.lambda_)[0].photometric)
+    n = len(gset)
+    return (density.score_densify(per_view["masks"], per_view["pixels"], per_view["ids"], n),
+            density.score_prune(per_view["masks"], per_view["pixels"], per_view["ids"],
+                                per_view["errors"], n))
 
 
 def _densify_round_fused(gset, scene, cfg, delta, rng, pool, gt_dev):
@@ -625,6 +726,9 @@ def train(scene, cfg: TrainConfig, *, ply_path=None, metrics_path=None, decision
     # deterministic merge: the same seed gives bitwise-identical metrics
     stepper = None if cfg.pose_opt else TrainStep(gset, cfg, extent=scene.extent, optimizer=opt,
                                                   deterministic=cfg.deterministic)
+    train_cams = [scene.cameras[int(i)] for i in pool]
+    if stepper is not None:
+        stepper.reserve(train_cams)  # pair capacity for the largest training view
     pose_t = {k: torch.zeros((1, 3), dtype=torch.float32, device=_device())
               for k in ("pose_rot", "pose_trans")}
     metrics, pending, decision_rows = [], [], []
@@ -639,9 +743,14 @@ def train(scene, cfg: TrainConfig, *, ply_path=None, metrics_path=None, decision
         vals = torch.stack([torch.stack([e, l1, s, d]) for _, e, l1, s, d in pending]).cpu()
         for (it, *_), row in zip(pending, vals.tolist()):
             if not np.isfinite(row[0]):
-                dump = {"iteration": it, "loss": row[0], "l1": row[1], "ssim": row[2]}
+                # the fused update skipped this step on the device (loss
+                # guard), so the set is the one that produced the loss
+                from .scene import validate
+                dump = {"iteration": it, "loss": row[0], "l1": row[1], "ssim": row[2],
+                        "invariant_report": validate(gset)}
                 if ply_path:
-                    Path(ply_path).with_suffix(".diverged.json").write_text(str(dump))
+                    Path(ply_path).with_suffix(".diverged.json").write_text(
+                        json.dumps(dump, indent=2))
                 raise TrainingDiverged(f"non-finite loss at iteration {it}", dump)
             metrics.append({"iter": it, "l1": row[1], "ssim": row[2], "depth_loss": row[3],
                             "total": row[0], "psnr": np.nan})
@@ -696,6 +805,7 @@ def train(scene, cfg: TrainConfig, *, ply_path=None, metrics_path=None, decision
             if stepper is not None:
                 stepper = TrainStep(gset, cfg, extent=scene.extent, optimizer=opt,
                                     deterministic=cfg.deterministic)
+                stepper.reserve(train_cams)
 
         if cfg.pose_opt and delta.steps_since_bake >= cfg.pose_bake_interval:
             baked = bake(delta, scene.cameras)
@@ -706,8 +816,11 @@ def train(scene, cfg: TrainConfig, *, ply_path=None, metrics_path=None, decision
         if iteration % cfg.eval_interval == 0 or iteration == cfg.max_iters:
             flush()
             metrics[-1]["psnr"] = evaluate(gset, eval_cams, cfg, delta)
-        if iteration % 32 == 0 or iteration == cfg.max_iters:
-            torch.cuda.synchronize()  # bound the launch queue so host time ~ device time
+        if iteration % 32 == 0 or iteration == 1 or iteration == cfg.max_iters:
+            # bound the launch queue so host time ~ device time (and the
+            # first iteration's budget check sees its device time, like the
+            # reference's synchronous step)
+            torch.cuda.synchronize()
         if time.perf_counter() - start > cfg.budget_seconds:
             stop_reason = "budget"
             break

@@ -97,6 +97,36 @@ def test_two_rank_view_parallel_step_matches_single_process(tmp_path, determinis
         got = flat_grad_views(torch.as_tensor(r0["flat0"]), ts.GaussianSet(**params))[k]
         err = float((got - ref).abs().max() / ref.abs().max().clamp(min=1e-12))
         assert err < 1e-5, (k, err)
+    # ... and the reduced gradient is the sum over the 4 views of the
+    # oracle's Grad3D (render -> photometric -> backward_per_gaussian ->
+    # project_vjp in float64), SURVEY §8(e) parity
+    oracle = _oracle_view_sum(params, ring, gt)
+    for k, got in flat_grad_views(torch.as_tensor(r0["flat0"]), ts.GaussianSet(**params)).items():
+        ref = oracle[k].reshape(got.shape)
+        err = float(np.abs(got.numpy() - ref).max() / max(np.abs(ref).max(), 1e-12))
+        assert err < 1e-3, (k, err)
+
+
+def _oracle_view_sum(params, ring, gt):
+    """Sum over views of the oracle's Grad3D for the FP32-rounded parameters
+    (the device's inputs)."""
+    from oracle import raster as O
+    p32 = {k: np.asarray(v, np.float32).astype(np.float64) for k, v in params.items()}
+    total = None
+    for r in ring:
+        cam = dict(fx=r["fx"], fy=r["fy"], cx=r["cx"], cy=r["cy"], width=160, height=120,
+                   R=np.asarray(r["R"], np.float64), t=np.asarray(r["t"], np.float64))
+        batch, colors = O.project(p32, cam)
+        # the device batch is FP32: round the oracle's the same way
+        for k in ("means2d", "conics", "level_t", "depths", "opacities"):
+            batch[k] = np.asarray(batch[k], np.float32).astype(np.float64)
+        idx = O.bin_sequential(batch)
+        bufs = O.render(batch, idx, colors, np.zeros(3))
+        gcol = O.photometric(bufs["color"], np.asarray(gt, np.float32).astype(np.float64))[3]
+        g2 = O.backward_per_gaussian(bufs, batch, idx, colors, gcol)
+        g3 = O.project_vjp(p32, cam, batch, g2)
+        total = g3 if total is None else {k: total[k] + g3[k] for k in total}
+    return total
 
 
 def _params_worker(rank, world, port, mode, out_dir):

@@ -58,8 +58,8 @@ void run(const char* name, float* out, int sms, int clk_khz) {
   const double lane_ops = (double)blocks * threads * iters * 16 * 8;
   const double warp_instr = lane_ops / 32 / (MODE == 1 ? 2 : 1);
   const double clks = ms * 1e-3 * clk_khz * 1e3;
-  printf("%-6s %8.3f ms  lane-ops/clk/SM %6.1f  warp-instr/clk/SMSP %5.2f\n", name, ms,
-         lane_ops / clks / sms, warp_instr / clks / sms / 4);
+  printf("%-6s %8.3f ms  lane-ops/s %7.2f T  lane-ops/clk/SM %6.1f  warp-instr/clk/SMSP %5.2f\n",
+         name, ms, lane_ops / (ms * 1e-3) / 1e12, lane_ops / clks / sms, warp_instr / clks / sms / 4);
 }
 
 int main() {
