@@ -164,11 +164,31 @@ int tsr_render_score(const float* rec, const int32_t* values, const int64_t* off
                      int32_t* out_n_contrib, int32_t* out_n_considered, void* stream);
 
 /* ---------------------------------------------------------------- K4 ----
- * backward_per_gaussian (backward.py:137-223): lane-per-splat groups of 32
- * restarting from checkpoints, warp scans for T and the weighted colour
- * suffix, one merged atomic write per (splat, tile).  grad2d must be zeroed
- * by the caller.  grad_depth / grad_final_T are nullable.  merges (device,
- * u64) counts (splat, tile) merges with the reference's semantics. */
+ * backward_per_gaussian (backward.py:137-223): a warp owns a supergroup of
+ * 64 list positions (two checkpoint groups, lane j the splat pair 2j, 2j+1)
+ * and runs a systolic pipeline over the pixels that entered it, restarting
+ * from the checkpoint record: lane j takes (T, R) from lane j-1 by one
+ * shuffle per step; one merged atomic write per (splat pair, supergroup).
+ * grad2d must be zeroed by the caller.  grad_depth / grad_final_T are
+ * nullable.  merges (device, u64) counts (splat, tile) merges with the
+ * reference's semantics.
+ *
+ * tsr_render_bwd: one CTA (4 warps) per tile, the warps taking the tile's
+ * supergroups.  tsr_render_bwd_ws (the product path): the (tile,
+ * supergroup) work units of the whole frame go to a global queue that every
+ * warp of a persistent grid drains, each warp compacting its unit's active
+ * pixels with their checkpoint state into its own shared-memory records --
+ * heavy tiles spread over the whole GPU and no warp idles at a tile's end.
+ * It needs a workspace of tsr_render_bwd_workspace(width, height, p_bound)
+ * bytes, p_bound >= the pair count (a capacity is fine). */
+size_t tsr_render_bwd_workspace(int32_t width, int32_t height, int64_t p_bound);
+int tsr_render_bwd_ws(const float* rec, const int32_t* values, const int64_t* offsets,
+                      int32_t width, int32_t height, const float* color, const float* depth,
+                      const float* final_T, const int32_t* n_considered, const float* ckpt,
+                      const int64_t* ckpt_base, const float* grad_color,
+                      const float* grad_depth, const float* grad_final_T, float* grad2d,
+                      unsigned long long* merges, int64_t p_bound, void* workspace,
+                      size_t workspace_bytes, void* stream);
 int tsr_render_bwd(const float* rec, const int32_t* values, const int64_t* offsets,
                    int32_t width, int32_t height, const float* color,
                    const float* depth, const float* final_T,
@@ -194,6 +214,19 @@ int tsr_render_bwd_det(const float* rec, const int32_t* values, const int64_t* o
                        const uint32_t* rank_count, const uint32_t* rank_off,
                        const int64_t* keys, int64_t m, const int64_t* m_dev, float* grad2d,
                        void* stream);
+/* the deterministic merge on the work-unit K4 (same slots/processed contract;
+ * processed[] is written by the call) */
+int tsr_render_bwd_ws_det(const float* rec, const int32_t* values, const int64_t* offsets,
+                          int32_t width, int32_t height, const float* color, const float* depth,
+                          const float* final_T, const int32_t* n_considered, const float* ckpt,
+                          const int64_t* ckpt_base, const float* grad_color,
+                          const float* grad_depth, const float* grad_final_T,
+                          unsigned long long* merges, float* slots, int32_t* processed,
+                          const uint32_t* inv_perm, const uint32_t* rank_row,
+                          const uint32_t* rank_count, const uint32_t* rank_off,
+                          const int64_t* keys, int64_t m, const int64_t* m_dev, float* grad2d,
+                          int64_t p_bound, void* workspace, size_t workspace_bytes,
+                          void* stream);
 
 /* --------------------------------------------------------------- K4b ----
  * project_vjp + SH/colour chain (projection.py:139-241, trainer.py:231-257,

@@ -70,6 +70,13 @@ _SIGNATURES = {
     "tsr_render_bwd_det": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
                                    c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                    c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "tsr_render_bwd_workspace": (c_sz, [c_i32, c_i32, c_i64]),
+    "tsr_render_bwd_ws": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                  c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_sz, c_vp]),
+    "tsr_render_bwd_ws_det": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp,
+                                      c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                      c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_sz,
+                                      c_vp]),
     "tsr_build_index_det": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_i32,
                                     c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp, c_vp,
                                     c_vp, c_vp, c_vp]),

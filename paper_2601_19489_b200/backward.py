@@ -10,6 +10,8 @@ gradient is not all zero (backward.py:214-222).
 
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import _lib
@@ -64,11 +66,42 @@ class Grad2D:
         return self.packed[:, 9]
 
 
+# K4 schedule.  "tiles" (default): one CTA per tile, its 4 warps taking the
+# tile's supergroups (tsr_render_bwd).  "units": the (tile, supergroup) work
+# units of the frame drained by the warps of a persistent grid
+# (tsr_render_bwd_ws) -- heavy tiles spread over the GPU and no warp idles at
+# a tile's end (warp slots busy 75 % -> ~94 %), but at C2 it measured 4 %
+# slower: K4 is FP32-pipe bound (math-pipe throttle is the top stall and
+# grows with the extra warps) and each unit re-gathers its pixel records
+# (DESIGN.md §8).  TSR_K4=units selects it.
+K4_FORM = os.environ.get("TSR_K4", "tiles")
+
+
+class BackwardWorkspace:
+    """Device scratch of the work-unit K4 (unit plan + queue), sized for a
+    pair bound; reused across calls of the same shape."""
+
+    def __init__(self):
+        self.buf = None
+        self.key = None
+
+    def get(self, width: int, height: int, p_bound: int) -> torch.Tensor:
+        if self.buf is None or self.key[0] != (width, height) or self.key[1] < p_bound:
+            n = int(_lib.load().tsr_render_bwd_workspace(width, height, p_bound))
+            self.buf = torch.empty(n, dtype=torch.uint8, device=_device())
+            self.key = ((width, height), p_bound)
+        return self.buf
+
+
 def backward_per_gaussian_raw(buffers: RenderBuffers, batch: SplatBatch, tiles: TileIndex,
                               grad_color, grad_depth=None, grad_final_T=None,
                               out: torch.Tensor | None = None,
-                              merges: torch.Tensor | None = None) -> tuple:
-    """Launch K4 without host synchronisation; returns (packed grads, merges)."""
+                              merges: torch.Tensor | None = None,
+                              workspace: BackwardWorkspace | None = None,
+                              p_bound: int | None = None) -> tuple:
+    """Launch K4 without host synchronisation; returns (packed grads, merges).
+    p_bound (>= the pair count; a capacity is fine) sizes the work-unit
+    plan; default tiles.n_pairs."""
     lib = _lib.load()
     dev = _device()
     if out is None:
@@ -78,19 +111,27 @@ def backward_per_gaussian_raw(buffers: RenderBuffers, batch: SplatBatch, tiles: 
     gc = as_device_f32(grad_color)
     gd = as_device_f32(grad_depth) if grad_depth is not None else None
     gt = as_device_f32(grad_final_T) if grad_final_T is not None else None
-    _lib.check(lib.tsr_render_bwd(
-        batch.rec.data_ptr(), _lib.ptr(tiles.values) if tiles.n_pairs else None,
-        tiles.offsets.data_ptr(), batch.width, batch.height, buffers.color.data_ptr(),
-        buffers.depth.data_ptr(), buffers.final_T.data_ptr(), buffers.n_considered.data_ptr(),
-        _lib.ptr(buffers.ckpt), _lib.ptr(buffers.ckpt_base), gc.data_ptr(), _lib.ptr(gd),
-        _lib.ptr(gt), out.data_ptr(), merges.data_ptr(), _lib.stream_handle()),
-        "tsr_render_bwd")
+    common = (batch.rec.data_ptr(), _lib.ptr(tiles.values) if tiles.n_pairs else None,
+              tiles.offsets.data_ptr(), batch.width, batch.height, buffers.color.data_ptr(),
+              buffers.depth.data_ptr(), buffers.final_T.data_ptr(),
+              buffers.n_considered.data_ptr(), _lib.ptr(buffers.ckpt),
+              _lib.ptr(buffers.ckpt_base), gc.data_ptr(), _lib.ptr(gd), _lib.ptr(gt),
+              out.data_ptr(), merges.data_ptr())
+    if K4_FORM == "tiles":
+        _lib.check(lib.tsr_render_bwd(*common, _lib.stream_handle()), "tsr_render_bwd")
+        return out, merges
+    p_bound = tiles.n_pairs if p_bound is None else p_bound
+    ws = (workspace or BackwardWorkspace()).get(batch.width, batch.height, p_bound)
+    _lib.check(lib.tsr_render_bwd_ws(*common, int(p_bound), ws.data_ptr(), ws.numel(),
+                                     _lib.stream_handle()), "tsr_render_bwd_ws")
     return out, merges
 
 
 def backward_det_raw(buffers: RenderBuffers, batch: SplatBatch, tiles: TileIndex, grad_color,
                      grad_depth, grad_final_T, out: torch.Tensor, merges: torch.Tensor,
-                     slots: torch.Tensor, processed: torch.Tensor, m_dev=None) -> None:
+                     slots: torch.Tensor, processed: torch.Tensor, m_dev=None,
+                     workspace: BackwardWorkspace | None = None,
+                     p_bound: int | None = None) -> None:
     """K4 with the deterministic merge (per-pair slots, per-row emission-order
     sums through K2's inverse permutation)."""
     lib = _lib.load()
@@ -101,15 +142,21 @@ def backward_det_raw(buffers: RenderBuffers, batch: SplatBatch, tiles: TileIndex
     gd = as_device_f32(grad_depth) if grad_depth is not None else None
     gt = as_device_f32(grad_final_T) if grad_final_T is not None else None
     inv_perm, rank_row, rank_count, rank_off = tiles.det
-    _lib.check(lib.tsr_render_bwd_det(
-        batch.rec.data_ptr(), _lib.ptr(tiles.values) if tiles.n_pairs else None,
-        tiles.offsets.data_ptr(), batch.width, batch.height, buffers.color.data_ptr(),
-        buffers.depth.data_ptr(), buffers.final_T.data_ptr(), buffers.n_considered.data_ptr(),
-        _lib.ptr(buffers.ckpt), _lib.ptr(buffers.ckpt_base), gc.data_ptr(), _lib.ptr(gd),
-        _lib.ptr(gt), merges.data_ptr(), slots.data_ptr(), processed.data_ptr(),
-        inv_perm.data_ptr(), rank_row.data_ptr(), rank_count.data_ptr(), rank_off.data_ptr(),
-        tiles.keys.data_ptr(), out.shape[0], _lib.ptr(m_dev), out.data_ptr(),
-        _lib.stream_handle()), "tsr_render_bwd_det")
+    common = (batch.rec.data_ptr(), _lib.ptr(tiles.values) if tiles.n_pairs else None,
+              tiles.offsets.data_ptr(), batch.width, batch.height, buffers.color.data_ptr(),
+              buffers.depth.data_ptr(), buffers.final_T.data_ptr(),
+              buffers.n_considered.data_ptr(), _lib.ptr(buffers.ckpt),
+              _lib.ptr(buffers.ckpt_base), gc.data_ptr(), _lib.ptr(gd), _lib.ptr(gt),
+              merges.data_ptr(), slots.data_ptr(), processed.data_ptr(), inv_perm.data_ptr(),
+              rank_row.data_ptr(), rank_count.data_ptr(), rank_off.data_ptr(),
+              tiles.keys.data_ptr(), out.shape[0], _lib.ptr(m_dev), out.data_ptr())
+    if K4_FORM == "tiles":
+        _lib.check(lib.tsr_render_bwd_det(*common, _lib.stream_handle()), "tsr_render_bwd_det")
+        return
+    p_bound = tiles.n_pairs if p_bound is None else p_bound
+    ws = (workspace or BackwardWorkspace()).get(batch.width, batch.height, p_bound)
+    _lib.check(lib.tsr_render_bwd_ws_det(*common, int(p_bound), ws.data_ptr(), ws.numel(),
+                                         _lib.stream_handle()), "tsr_render_bwd_ws_det")
 
 
 def backward_per_gaussian(buffers: RenderBuffers, batch: SplatBatch, tiles: TileIndex,

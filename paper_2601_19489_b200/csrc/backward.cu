@@ -376,6 +376,363 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
   }
 }
 
+// ---- K4, work-unit form ---------------------------------------------------
+// The same systolic supergroup step, scheduled per WARP instead of per tile.
+// A work unit is one (tile, supergroup G) pair; the units of all tiles are
+// laid out in raster order (unit_plan_kernel) and every warp of a persistent
+// grid grabs the next unit from a global counter.  So a heavy tile's
+// supergroups spread over as many warps as the GPU has free (the paper's
+// work redistribution across heavy tiles), and no warp of
+// a CTA idles while a sibling finishes a tile (the per-tile CTA form leaves
+// ~20 % of the warp slots empty: 4 warps share 3-9 supergroups).
+//
+// Each warp compacts the unit's active pixels (n_considered > 64 G) into its
+// own shared-memory records, with the supergroup's entry state folded in:
+//   a = (x + 1/2, y + 1/2, T0, n_considered)   b = (g_r, g_g, g_b, R0)
+// (T0, R0) = checkpoint record 2G - 1 (T, Ktot + g_T T_f - <g, C> - g_d D),
+// or (1, Ktot + g_T T_f) for G = 0.  The records sit at [32, 32 + n_act)
+// between sentinel records (x = -65536: alpha 0; T0 = R0 = 0), so lane j at
+// step t reads record 32 + t - j at a lane-constant base + 16 t: no list
+// indirection, and lane 0 takes (T0, R0) from the record it loads anyway.
+constexpr int kRecPad = 32;
+constexpr int kRecSlots = kRecPad + kTilePixels + kListPad + 4;
+
+// unit plan, part 1: supergroups per tile = ceil(max n_considered / 64) (one
+// warp per tile).  Later positions contribute exactly zero.
+__global__ void __launch_bounds__(256) unit_count_kernel(const int64_t* __restrict__ offsets,
+                                                         const int32_t* __restrict__ n_considered,
+                                                         int width, int height, int tiles_x,
+                                                         int n_tiles, int32_t* __restrict__ nsup) {
+  const int tile = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (tile >= n_tiles) return;
+  const int tyi = tile / tiles_x, txi = tile - tyi * tiles_x;
+  int mx = 0;
+#pragma unroll
+  for (int s = 0; s < kTilePixels / 32; ++s) {
+    const int px = 32 * s + lane;
+    const int x = txi * kTile + (px & 15), y = tyi * kTile + (px >> 4);
+    if (x < width && y < height) mx = max(mx, n_considered[(long long)y * width + x]);
+  }
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (lane == 0) {
+    const long long n = offsets[tile + 1] - offsets[tile];
+    const long long m = min((long long)mx, n);
+    nsup[tile] = (int32_t)((m + kSuper - 1) / kSuper);
+  }
+}
+
+// unit plan, part 2 (one CTA): exclusive scan of the per-tile counts ->
+// units[U_t + g] = tile << 16 | g; the unit count; the grab counter reset;
+// and, for the deterministic merge, processed[t] = 64 x supergroups.
+constexpr int kPlanThreads = 1024;
+__global__ void __launch_bounds__(kPlanThreads) unit_plan_kernel(
+    const int32_t* __restrict__ nsup, int n_tiles, uint32_t* __restrict__ units,
+    long long units_cap, int32_t* __restrict__ n_units, int32_t* __restrict__ counter,
+    int32_t* __restrict__ processed) {
+  __shared__ int s_w[kPlanThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (n_tiles + kPlanThreads - 1) / kPlanThreads;
+  const int t0 = tid * per, t1 = min(n_tiles, t0 + per);
+  int sum = 0;
+  for (int t = t0; t < t1; ++t) sum += nsup[t];
+  int incl = sum;
+#pragma unroll
+  for (int k = 1; k < 32; k <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, k);
+    if (lane >= k) incl += v;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int w = s_w[lane], wi = w;
+#pragma unroll
+    for (int k = 1; k < 32; k <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, wi, k);
+      if (lane >= k) wi += v;
+    }
+    s_w[lane] = wi - w;  // exclusive prefix of the warps
+  }
+  __syncthreads();
+  long long u = (long long)s_w[warp] + incl - sum;
+  for (int t = t0; t < t1; ++t) {
+    const int k = nsup[t];
+    if (processed) processed[t] = k * kSuper;
+    for (int g = 0; g < k; ++g, ++u)
+      if (u < units_cap) units[u] = ((uint32_t)t << 16) | (uint32_t)g;
+  }
+  if (tid == kPlanThreads - 1) {
+    *n_units = (int32_t)min(u, units_cap);
+    *counter = 0;
+  }
+}
+
+template <bool kDepth, bool kDet>
+__global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_units_kernel(
+    const float4* __restrict__ rec, const int32_t* __restrict__ values,
+    const int64_t* __restrict__ offsets, int width, int height, int tiles_x,
+    const float* __restrict__ color, const float* __restrict__ depth,
+    const float* __restrict__ final_T, const int32_t* __restrict__ n_considered,
+    const float* __restrict__ ckpt, const int64_t* __restrict__ ckpt_base,
+    const float* __restrict__ grad_color, const float* __restrict__ grad_depth,
+    const float* __restrict__ grad_final_T, float* __restrict__ grad2d,
+    unsigned long long* __restrict__ merges, float* __restrict__ slots,
+    const uint32_t* __restrict__ units, const int32_t* __restrict__ n_units_dev,
+    int32_t* __restrict__ counter, int32_t* __restrict__ processed) {
+  __shared__ float4 s_pa[kBwdWarps][kRecSlots];
+  __shared__ float4 s_pb[kBwdWarps][kRecSlots];
+  __shared__ float s_gd[kDepth ? kBwdWarps : 1][kDepth ? kRecSlots : 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  float4* pa = s_pa[warp];
+  float4* pb = s_pb[warp];
+  float* gdv = kDepth ? s_gd[warp] : nullptr;
+  const float4 sent_a = make_float4(-65536.f, -65536.f, 0.f, __int_as_float(0));
+  const float4 sent_b = make_float4(0.f, 0.f, 0.f, 0.f);
+  pa[lane] = sent_a;  // leading sentinels (records start at kRecPad)
+  pb[lane] = sent_b;
+  if (kDepth) gdv[lane] = 0.f;
+  const int n_units = *n_units_dev;
+  for (;;) {
+    int u = 0;
+    if (lane == 0) u = atomicAdd(counter, 1);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= n_units) break;
+    const uint32_t code = units[u];
+    const int tile = (int)(code >> 16), G = (int)(code & 0xffffu);
+    const long long start = offsets[tile], end = offsets[tile + 1];
+    const int n = (int)(end - start);
+    const int tyi = tile / tiles_x, txi = tile - tyi * tiles_x;
+    const int P0 = G * kSuper;
+    const int p = P0 + 2 * lane;  // this lane's first position; second is p + 1
+    int row0 = -1, row1 = -1;
+    if (p < n) row0 = values[start + p];
+    if (p + 1 < n) row1 = values[start + p + 1];
+    // ---- compact the unit's active pixels with their entry state
+    const float* src0 = G > 0 ? ckpt + (ckpt_base[tile] + 2 * G - 1) * (5 * kTilePixels) : nullptr;
+    int nc[kTilePixels / 32];
+    long long pix[kTilePixels / 32];
+#pragma unroll
+    for (int s = 0; s < kTilePixels / 32; ++s) {
+      const int px = 32 * s + lane;
+      const int x = txi * kTile + (px & 15), y = tyi * kTile + (px >> 4);
+      const bool inside = x < width && y < height;
+      pix[s] = (long long)y * width + x;
+      nc[s] = inside ? n_considered[pix[s]] : 0;
+    }
+    bool nz = false;
+    int n_act = 0;
+#pragma unroll
+    for (int s = 0; s < kTilePixels / 32; ++s) {
+      const bool act = nc[s] > P0;
+      const unsigned bal = __ballot_sync(0xffffffffu, act);
+      if (act) {
+        const int px = 32 * s + lane;
+        const long long q = pix[s];
+        const float gr = grad_color[3 * q], gg = grad_color[3 * q + 1], gb = grad_color[3 * q + 2];
+        const float gd = (kDepth && grad_depth) ? grad_depth[q] : 0.f;
+        const float gt = grad_final_T ? grad_final_T[q] : 0.f;
+        float k = gr * color[3 * q] + gg * color[3 * q + 1] + gb * color[3 * q + 2] + gt * final_T[q];
+        if (kDepth) k += gd * depth[q];
+        float T0 = 1.f, K0 = 0.f;
+        if (src0) {
+          T0 = src0[px];
+          K0 = gr * src0[kTilePixels + px] + gg * src0[2 * kTilePixels + px] +
+               gb * src0[3 * kTilePixels + px];
+          if (kDepth) K0 += gd * src0[4 * kTilePixels + px];
+        }
+        nz |= (gr != 0.f) || (gg != 0.f) || (gb != 0.f) || (gd != 0.f) || (gt != 0.f);
+        const int kk = kRecPad + n_act + __popc(bal & lt_mask);
+        pa[kk] = make_float4((float)(txi * kTile + (px & 15)) + 0.5f,
+                             (float)(tyi * kTile + (px >> 4)) + 0.5f, T0, __int_as_float(nc[s]));
+        pb[kk] = make_float4(gr, gg, gb, k - K0);
+        if (kDepth) gdv[kk] = gd;
+      }
+      n_act += __popc(bal);
+    }
+    // tile skipped when its upstream is all zero (backward.py:156-158): the
+    // G = 0 unit sees every in-image pixel; a later unit whose active pixels
+    // carry no upstream contributes exact zeros
+    if (!__any_sync(0xffffffffu, nz)) {
+      if (kDet) {  // the reducer reads slots below processed[tile]
+        if (G == 0) {
+          if (lane == 0) processed[tile] = 0;  // skipped tile
+        } else {
+#pragma unroll
+          for (int j = 0; j < TSR_GRAD2D_FLOATS; ++j) {
+            if (row0 >= 0) slots[(start + p) * TSR_GRAD2D_FLOATS + j] = 0.f;
+            if (row1 >= 0) slots[(start + p + 1) * TSR_GRAD2D_FLOATS + j] = 0.f;
+          }
+        }
+      }
+      continue;
+    }
+    if (G == 0 && lane == 0) atomicAdd(merges, (unsigned long long)n);
+    // trailing sentinels (finite zero T0, R0: the sentinel steps add zeros)
+    pa[kRecPad + n_act + lane] = sent_a;
+    pb[kRecPad + n_act + lane] = sent_b;
+    if (kDepth) gdv[kRecPad + n_act + lane] = 0.f;
+    if (lane < 4) {
+      pa[kRecPad + n_act + 32 + lane] = sent_a;
+      pb[kRecPad + n_act + 32 + lane] = sent_b;
+      if (kDepth) gdv[kRecPad + n_act + 32 + lane] = 0.f;
+    }
+    float2 mxn = bc(0.f), myn = bc(0.f), ca = bc(0.f), cb = bc(0.f), cc = bc(0.f), op = bc(0.f);
+    float2 cr = bc(0.f), cg = bc(0.f), cbl = bc(0.f), dep = bc(0.f);
+    if (row0 >= 0) {
+      const float4 r0 = __ldg(rec + 3 * row0), r1 = __ldg(rec + 3 * row0 + 1),
+                   r2 = __ldg(rec + 3 * row0 + 2);
+      mxn.x = -r0.x; myn.x = -r0.y;
+      ca.x = __fmul_rn(r0.z, kQScale);
+      cb.x = __fmul_rn(r0.w, 2.0f * kQScale);
+      cc.x = __fmul_rn(r1.x, kQScale);
+      op.x = r1.y; dep.x = r1.z;
+      cr.x = r2.x; cg.x = r2.y; cbl.x = r2.z;
+    }
+    if (row1 >= 0) {
+      const float4 r0 = __ldg(rec + 3 * row1), r1 = __ldg(rec + 3 * row1 + 1),
+                   r2 = __ldg(rec + 3 * row1 + 2);
+      mxn.y = -r0.x; myn.y = -r0.y;
+      ca.y = __fmul_rn(r0.z, kQScale);
+      cb.y = __fmul_rn(r0.w, 2.0f * kQScale);
+      cc.y = __fmul_rn(r1.x, kQScale);
+      op.y = r1.y; dep.y = r1.z;
+      cr.y = r2.x; cg.y = r2.y; cbl.y = r2.z;
+    }
+    __syncwarp();
+
+    float2 acc_a = bc(0.f), acc_b = bc(0.f), acc_c = bc(0.f), acc_mx = bc(0.f), acc_my = bc(0.f);
+    float2 acc_o = bc(0.f), acc_r = bc(0.f), acc_g = bc(0.f), acc_bl = bc(0.f), acc_d = bc(0.f);
+    float T_out = 1.f, R_out = 0.f;
+    const char* a_base = reinterpret_cast<const char*>(pa + kRecPad - lane);
+    const char* b_base = reinterpret_cast<const char*>(pb + kRecPad - lane);
+    const float* g_base = kDepth ? gdv + kRecPad - lane : nullptr;
+    const int steps = (n_act + 31 + 3) & ~3;  // sentinel steps pad to a multiple of 4
+    const float2 one = bc(1.f);
+    auto step = [&](const float4& ra, const float4& rb, float gdp) {
+      float T_in = __shfl_up_sync(0xffffffffu, T_out, 1);
+      float R_in = __shfl_up_sync(0xffffffffu, R_out, 1);
+      if (lane == 0) {
+        T_in = ra.z;
+        R_in = rb.w;
+      }
+      const int ncp = __float_as_int(ra.w);
+      const float2 dx = __fadd2_rn(bc(ra.x), mxn);
+      const float2 dy = __fadd2_rn(bc(ra.y), myn);
+      const float2 dxx = __fmul2_rn(dx, dx), dxy = __fmul2_rn(dx, dy), dyy = __fmul2_rn(dy, dy);
+      const float2 qs = __ffma2_rn(ca, dxx, __ffma2_rn(cb, dxy, __fmul2_rn(cc, dyy)));
+      const float2 gauss = f2(fast_exp2(qs.x), fast_exp2(qs.y));
+      const float2 raw = f2(__fmul_rn(op.x, gauss.x), __fmul_rn(op.y, gauss.y));
+      const float2 alpha = f2(fminf(kAlphaCap, raw.x), fminf(kAlphaCap, raw.y));
+      float a0, a1;
+      asm("{\n\t.reg .pred q;\n\t"
+          "setp.lt.s32 q, %1, %2;\n\t"
+          "setp.ge.and.f32 q, %3, %4, q;\n\t"
+          "selp.f32 %0, %3, 0f00000000, q;\n\t}"
+          : "=f"(a0) : "r"(p), "r"(ncp), "f"(alpha.x), "f"(kMinAlpha));
+      asm("{\n\t.reg .pred q;\n\t"
+          "setp.lt.s32 q, %1, %2;\n\t"
+          "setp.ge.and.f32 q, %3, %4, q;\n\t"
+          "selp.f32 %0, %3, 0f00000000, q;\n\t}"
+          : "=f"(a1) : "r"(p + 1), "r"(ncp), "f"(alpha.y), "f"(kMinAlpha));
+      const float2 a = f2(a0, a1);
+      const float2 om = __fadd2_rn(one, f2(-a.x, -a.y));
+      float2 gc = __ffma2_rn(bc(rb.x), cr, __ffma2_rn(bc(rb.y), cg, __fmul2_rn(bc(rb.z), cbl)));
+      if (kDepth) gc = __ffma2_rn(bc(gdp), dep, gc);
+      const float w0 = T_in * a.x;
+      const float T1 = T_in * om.x;
+      const float w1 = T1 * a.y;
+      T_out = T1 * om.y;
+      const float num0 = fmaf(-w0, gc.x, R_in);
+      const float num1 = fmaf(-w1, gc.y, num0);
+      R_out = num1;
+      const float2 rcp = f2(fast_rcp(om.x), fast_rcp(om.y));
+      const float2 dLda = f2(fmaf(-num0, rcp.x, T_in * gc.x), fmaf(-num1, rcp.y, T1 * gc.y));
+      const float2 ld = f2(a.x == raw.x ? dLda.x : 0.f, a.y == raw.y ? dLda.y : 0.f);
+      const float2 gq = __fmul2_rn(ld, alpha);
+      acc_a = __ffma2_rn(gq, dxx, acc_a);
+      acc_b = __ffma2_rn(gq, dxy, acc_b);
+      acc_c = __ffma2_rn(gq, dyy, acc_c);
+      acc_mx = __ffma2_rn(gq, dx, acc_mx);
+      acc_my = __ffma2_rn(gq, dy, acc_my);
+      acc_o = __ffma2_rn(ld, gauss, acc_o);
+      const float2 w = f2(w0, w1);
+      acc_r = __ffma2_rn(w, bc(rb.x), acc_r);
+      acc_g = __ffma2_rn(w, bc(rb.y), acc_g);
+      acc_bl = __ffma2_rn(w, bc(rb.z), acc_bl);
+      if (kDepth) acc_d = __ffma2_rn(w, bc(gdp), acc_d);
+    };
+    auto ld_a = [&](int t) { return *reinterpret_cast<const float4*>(a_base + 16 * t); };
+    auto ld_b = [&](int t) { return *reinterpret_cast<const float4*>(b_base + 16 * t); };
+    auto ld_g = [&](int t) { return kDepth ? g_base[t] : 0.f; };
+    float4 a0r = ld_a(0), b0r = ld_b(0), a1r, b1r;
+    float g0r = ld_g(0), g1r;
+    for (int t = 0; t < steps; t += 4) {
+      a1r = ld_a(t + 1); b1r = ld_b(t + 1); g1r = ld_g(t + 1);
+      step(a0r, b0r, g0r);
+      a0r = ld_a(t + 2); b0r = ld_b(t + 2); g0r = ld_g(t + 2);
+      step(a1r, b1r, g1r);
+      a1r = ld_a(t + 3); b1r = ld_b(t + 3); g1r = ld_g(t + 3);
+      step(a0r, b0r, g0r);
+      a0r = ld_a(t + 4); b0r = ld_b(t + 4); g0r = ld_g(t + 4);
+      step(a1r, b1r, g1r);
+    }
+    __syncwarp();  // records are rewritten by the next unit
+    const float ms = 2.0f / kQScale;
+    {
+      const float2 hb = __fmul2_rn(cb, bc(0.5f));
+      const float2 uu = __ffma2_rn(ca, acc_mx, __fmul2_rn(hb, acc_my));
+      const float2 vv = __ffma2_rn(hb, acc_mx, __fmul2_rn(cc, acc_my));
+      acc_mx = uu;
+      acc_my = vv;
+    }
+    if (kDet) {
+      if (row0 >= 0) {
+        float* dst = slots + (start + p) * TSR_GRAD2D_FLOATS;
+        dst[0] = ms * 0.5f * acc_mx.x; dst[1] = ms * 0.5f * acc_my.x;
+        dst[2] = -0.5f * acc_a.x; dst[3] = -acc_b.x; dst[4] = -0.5f * acc_c.x;
+        dst[5] = acc_o.x; dst[6] = acc_r.x; dst[7] = acc_g.x; dst[8] = acc_bl.x;
+        dst[9] = kDepth ? acc_d.x : 0.f;
+      }
+      if (row1 >= 0) {
+        float* dst = slots + (start + p + 1) * TSR_GRAD2D_FLOATS;
+        dst[0] = ms * 0.5f * acc_mx.y; dst[1] = ms * 0.5f * acc_my.y;
+        dst[2] = -0.5f * acc_a.y; dst[3] = -acc_b.y; dst[4] = -0.5f * acc_c.y;
+        dst[5] = acc_o.y; dst[6] = acc_r.y; dst[7] = acc_g.y; dst[8] = acc_bl.y;
+        dst[9] = kDepth ? acc_d.y : 0.f;
+      }
+      continue;
+    }
+    if (row0 >= 0 && ((acc_o.x != 0.f) | (acc_r.x != 0.f) | (acc_g.x != 0.f) |
+                      (acc_bl.x != 0.f) | (acc_d.x != 0.f) | (acc_a.x != 0.f))) {
+      float* dst = grad2d + (long long)row0 * TSR_GRAD2D_FLOATS;
+      atomicAdd(dst + 0, ms * 0.5f * acc_mx.x);
+      atomicAdd(dst + 1, ms * 0.5f * acc_my.x);
+      atomicAdd(dst + 2, -0.5f * acc_a.x);
+      atomicAdd(dst + 3, -acc_b.x);
+      atomicAdd(dst + 4, -0.5f * acc_c.x);
+      atomicAdd(dst + 5, acc_o.x);
+      atomicAdd(dst + 6, acc_r.x);
+      atomicAdd(dst + 7, acc_g.x);
+      atomicAdd(dst + 8, acc_bl.x);
+      if (kDepth) atomicAdd(dst + 9, acc_d.x);
+    }
+    if (row1 >= 0 && ((acc_o.y != 0.f) | (acc_r.y != 0.f) | (acc_g.y != 0.f) |
+                      (acc_bl.y != 0.f) | (acc_d.y != 0.f) | (acc_a.y != 0.f))) {
+      float* dst = grad2d + (long long)row1 * TSR_GRAD2D_FLOATS;
+      atomicAdd(dst + 0, ms * 0.5f * acc_mx.y);
+      atomicAdd(dst + 1, ms * 0.5f * acc_my.y);
+      atomicAdd(dst + 2, -0.5f * acc_a.y);
+      atomicAdd(dst + 3, -acc_b.y);
+      atomicAdd(dst + 4, -0.5f * acc_c.y);
+      atomicAdd(dst + 5, acc_o.y);
+      atomicAdd(dst + 6, acc_r.y);
+      atomicAdd(dst + 7, acc_g.y);
+      atomicAdd(dst + 8, acc_bl.y);
+      if (kDepth) atomicAdd(dst + 9, acc_d.y);
+    }
+  }
+}
+
 // Deterministic merge, second half: one thread per depth rank sums its
 // row's slots in emission order (binning.py:217-221: the row's pairs are a
 // contiguous emission range [rank_off, rank_off + rank_count), and K2's
@@ -470,6 +827,141 @@ extern "C" int tsr_render_bwd_det(const float* rec, const int32_t* values, const
                                     grad_color, grad_depth, grad_final_T, nullptr, merges, slots,
                                     processed);
   TSR_CHECK_LAUNCH();
+  if (m > 0) {
+    grad_reduce_kernel<<<(int)((m + 255) / 256), 256, 0, s>>>(
+        rank_row, rank_count, rank_off, inv_perm, keys, offsets, processed, slots, m, m_dev,
+        grad2d);
+    TSR_CHECK_LAUNCH();
+  }
+  return TSR_OK;
+}
+
+// ---- work-unit K4 entry points ---------------------------------------------
+namespace {
+struct UnitWs {
+  int32_t* nsup;
+  int32_t* n_units;
+  int32_t* counter;
+  uint32_t* units;
+  long long cap;
+};
+
+size_t units_cap(int n_tiles, int64_t p_bound) {
+  // units = sum_t ceil(min(max n_cons, n_t) / 64) <= P / 64 + n_tiles
+  return (size_t)(p_bound > 0 ? p_bound : 0) / kSuper + (size_t)n_tiles + 1;
+}
+
+size_t units_ws_bytes(int n_tiles, int64_t p_bound) {
+  return ((size_t)n_tiles * 4 + 255) / 256 * 256 + 256 + units_cap(n_tiles, p_bound) * 4;
+}
+
+UnitWs carve(void* ws, int n_tiles, int64_t p_bound) {
+  UnitWs u;
+  char* b = (char*)ws;
+  u.nsup = (int32_t*)b;
+  b += ((size_t)n_tiles * 4 + 255) / 256 * 256;
+  u.n_units = (int32_t*)b;
+  u.counter = (int32_t*)(b + 4);
+  b += 256;
+  u.units = (uint32_t*)b;
+  u.cap = (long long)units_cap(n_tiles, p_bound);
+  return u;
+}
+
+template <bool kDepth, bool kDet>
+int launch_units(const float* rec, const int32_t* values, const int64_t* offsets, int width,
+                 int height, const float* color, const float* depth, const float* final_T,
+                 const int32_t* n_considered, const float* ckpt, const int64_t* ckpt_base,
+                 const float* grad_color, const float* grad_depth, const float* grad_final_T,
+                 float* grad2d, unsigned long long* merges, float* slots, int32_t* processed,
+                 const UnitWs& u, cudaStream_t s) {
+  const int tx = tiles_of(width), ty = tiles_of(height), n_tiles = tx * ty;
+  unit_count_kernel<<<(n_tiles + 7) / 8, 256, 0, s>>>(offsets, n_considered, width, height, tx,
+                                                      n_tiles, u.nsup);
+  TSR_CHECK_LAUNCH();
+  unit_plan_kernel<<<1, kPlanThreads, 0, s>>>(u.nsup, n_tiles, u.units, u.cap, u.n_units,
+                                              u.counter, processed);
+  TSR_CHECK_LAUNCH();
+  auto* k = render_bwd_units_kernel<kDepth, kDet>;
+  static int per_sm = 0, sms = 0;  // occupancy of this instantiation (host-side constant)
+  if (per_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBwdThreads, 0);
+    if (per_sm < 1) per_sm = 1;
+  }
+  k<<<sms * per_sm, kBwdThreads, 0, s>>>((const float4*)rec, values, offsets, width, height, tx,
+                                         color, depth, final_T, n_considered, ckpt, ckpt_base,
+                                         grad_color, grad_depth, grad_final_T, grad2d, merges,
+                                         slots, u.units, u.n_units, u.counter, processed);
+  TSR_CHECK_LAUNCH();
+  return TSR_OK;
+}
+}  // namespace
+
+extern "C" size_t tsr_render_bwd_workspace(int32_t width, int32_t height, int64_t p_bound) {
+  if (width <= 0 || height <= 0) return 0;
+  return units_ws_bytes(tiles_of(width) * tiles_of(height), p_bound);
+}
+
+extern "C" int tsr_render_bwd_ws(const float* rec, const int32_t* values, const int64_t* offsets,
+                                 int32_t width, int32_t height, const float* color,
+                                 const float* depth, const float* final_T,
+                                 const int32_t* n_considered, const float* ckpt,
+                                 const int64_t* ckpt_base, const float* grad_color,
+                                 const float* grad_depth, const float* grad_final_T,
+                                 float* grad2d, unsigned long long* merges, int64_t p_bound,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
+  if (width <= 0 || height <= 0 || !grad_color || !merges || !grad2d || !workspace)
+    return TSR_E_INVALID;
+  if (ckpt && !ckpt_base) return TSR_E_INVALID;
+  const int n_tiles = tiles_of(width) * tiles_of(height);
+  if (n_tiles >= (1 << 16)) return TSR_E_INVALID;
+  if (workspace_bytes < units_ws_bytes(n_tiles, p_bound)) return TSR_E_WORKSPACE;
+  const UnitWs u = carve(workspace, n_tiles, p_bound);
+  cudaStream_t s = (cudaStream_t)stream;
+  return grad_depth
+             ? launch_units<true, false>(rec, values, offsets, width, height, color, depth, final_T,
+                                         n_considered, ckpt, ckpt_base, grad_color, grad_depth,
+                                         grad_final_T, grad2d, merges, nullptr, nullptr, u, s)
+             : launch_units<false, false>(rec, values, offsets, width, height, color, depth,
+                                          final_T, n_considered, ckpt, ckpt_base, grad_color,
+                                          grad_depth, grad_final_T, grad2d, merges, nullptr,
+                                          nullptr, u, s);
+}
+
+extern "C" int tsr_render_bwd_ws_det(const float* rec, const int32_t* values,
+                                     const int64_t* offsets, int32_t width, int32_t height,
+                                     const float* color, const float* depth, const float* final_T,
+                                     const int32_t* n_considered, const float* ckpt,
+                                     const int64_t* ckpt_base, const float* grad_color,
+                                     const float* grad_depth, const float* grad_final_T,
+                                     unsigned long long* merges, float* slots, int32_t* processed,
+                                     const uint32_t* inv_perm, const uint32_t* rank_row,
+                                     const uint32_t* rank_count, const uint32_t* rank_off,
+                                     const int64_t* keys, int64_t m, const int64_t* m_dev,
+                                     float* grad2d, int64_t p_bound, void* workspace,
+                                     size_t workspace_bytes, void* stream) {
+  if (width <= 0 || height <= 0 || !grad_color || !merges || !slots || !processed ||
+      !inv_perm || !rank_row || !rank_count || !rank_off || !keys || m < 0 || !grad2d ||
+      !workspace)
+    return TSR_E_INVALID;
+  if (ckpt && !ckpt_base) return TSR_E_INVALID;
+  const int n_tiles = tiles_of(width) * tiles_of(height);
+  if (n_tiles >= (1 << 16)) return TSR_E_INVALID;
+  if (workspace_bytes < units_ws_bytes(n_tiles, p_bound)) return TSR_E_WORKSPACE;
+  const UnitWs u = carve(workspace, n_tiles, p_bound);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int rc =
+      grad_depth
+          ? launch_units<true, true>(rec, values, offsets, width, height, color, depth, final_T,
+                                     n_considered, ckpt, ckpt_base, grad_color, grad_depth,
+                                     grad_final_T, nullptr, merges, slots, processed, u, s)
+          : launch_units<false, true>(rec, values, offsets, width, height, color, depth, final_T,
+                                      n_considered, ckpt, ckpt_base, grad_color, grad_depth,
+                                      grad_final_T, nullptr, merges, slots, processed, u, s);
+  if (rc != TSR_OK) return rc;
   if (m > 0) {
     grad_reduce_kernel<<<(int)((m + 255) / 256), 256, 0, s>>>(
         rank_row, rank_count, rank_off, inv_perm, keys, offsets, processed, slots, m, m_dev,

@@ -249,6 +249,8 @@ class TrainStep:
         self.redone_steps = 0
         self.merges = torch.zeros(1, dtype=torch.int64, device=dev)
         self.loss_ws = losses.PhotometricWorkspace()
+        from .backward import BackwardWorkspace
+        self.bwd_ws = BackwardWorkspace()
         self._grad2d_clean = True  # the SH-0 fused kernel re-zeroes consumed rows
         self.grad_color = None
         # step status read back without kernels: two D2H copy nodes into
@@ -392,28 +394,37 @@ class TrainStep:
             e = e + dl
         self.last_losses = (e, l1, s, dl)
         self._mark(timer, "loss")
+        from .backward import K4_FORM
+        common = (batch.rec.data_ptr(), idx.values.data_ptr(), idx.offsets.data_ptr(),
+                  camera.width, camera.height, out.color.data_ptr(), out.depth.data_ptr(),
+                  out.final_T.data_ptr(), out.n_considered.data_ptr(), out.ckpt.data_ptr(),
+                  idx.ckpt_base.data_ptr(), grad_color.data_ptr(), _lib.ptr(gd), _lib.ptr(gt))
+        ws = self.bwd_ws.get(camera.width, camera.height, idx.p_cap)
         if self.deterministic:  # slots + emission-order row sums overwrite grad2d
-            _lib.check(self.lib.tsr_render_bwd_det(
-                batch.rec.data_ptr(), idx.values.data_ptr(), idx.offsets.data_ptr(),
-                camera.width, camera.height, out.color.data_ptr(), out.depth.data_ptr(),
-                out.final_T.data_ptr(), out.n_considered.data_ptr(), out.ckpt.data_ptr(),
-                idx.ckpt_base.data_ptr(), grad_color.data_ptr(), _lib.ptr(gd), _lib.ptr(gt),
-                self.merges.data_ptr(), self.slots.data_ptr(), self.processed.data_ptr(),
-                *(t.data_ptr() for t in idx.det), idx.keys.data_ptr(), self.grad2d.shape[0],
-                self.scratch.totals.data_ptr(), self.grad2d.data_ptr(), _lib.stream_handle()),
-                "tsr_render_bwd_det")
+            det = (self.merges.data_ptr(), self.slots.data_ptr(), self.processed.data_ptr(),
+                   *(t.data_ptr() for t in idx.det), idx.keys.data_ptr(), self.grad2d.shape[0],
+                   self.scratch.totals.data_ptr(), self.grad2d.data_ptr())
+            if K4_FORM == "tiles":
+                _lib.check(self.lib.tsr_render_bwd_det(*common, *det, _lib.stream_handle()),
+                           "tsr_render_bwd_det")
+            else:
+                _lib.check(self.lib.tsr_render_bwd_ws_det(
+                    *common, *det, idx.p_cap, ws.data_ptr(), ws.numel(), _lib.stream_handle()),
+                    "tsr_render_bwd_ws_det")
             self._grad2d_clean = False
             self._mark(timer, "backward")
             return e
         if not self._grad2d_clean:
             self.grad2d.zero_()
         self._grad2d_clean = False
-        _lib.check(self.lib.tsr_render_bwd(
-            batch.rec.data_ptr(), idx.values.data_ptr(), idx.offsets.data_ptr(), camera.width,
-            camera.height, out.color.data_ptr(), out.depth.data_ptr(), out.final_T.data_ptr(),
-            out.n_considered.data_ptr(), out.ckpt.data_ptr(), idx.ckpt_base.data_ptr(),
-            grad_color.data_ptr(), _lib.ptr(gd), _lib.ptr(gt), self.grad2d.data_ptr(),
-            self.merges.data_ptr(), _lib.stream_handle()), "tsr_render_bwd")
+        if K4_FORM == "tiles":
+            _lib.check(self.lib.tsr_render_bwd(*common, self.grad2d.data_ptr(),
+                                               self.merges.data_ptr(), _lib.stream_handle()),
+                       "tsr_render_bwd")
+        else:
+            _lib.check(self.lib.tsr_render_bwd_ws(
+                *common, self.grad2d.data_ptr(), self.merges.data_ptr(), idx.p_cap,
+                ws.data_ptr(), ws.numel(), _lib.stream_handle()), "tsr_render_bwd_ws")
         self._mark(timer, "backward")
         return e
 
@@ -532,9 +543,12 @@ class TrainStep:
 
     def kernels_per_step(self) -> int:
         """Our kernel launches per step: K1a, K1b; K2 (one persistent
-        cooperative kernel); K3; loss (fwd, bwd + finalize); K4; fused K4b+K5
-        (+ the row reduction in deterministic mode)."""
-        return 2 + 1 + 1 + 2 + 1 + 1 + (1 if self.deterministic else 0)
+        cooperative kernel); K3; loss (fwd, bwd + finalize); K4 (+ its two
+        work-unit plan kernels); fused K4b+K5 (+ the row reduction in
+        deterministic mode)."""
+        from .backward import K4_FORM
+        return (2 + 1 + 1 + 2 + 1 + (2 if K4_FORM == "units" else 0) + 1
+                + (1 if self.deterministic else 0))
 
     def last_view(self):
         """(batch, TileIndex, RenderBuffers) views of the last step (synchronises)."""
@@ -727,13 +741,15 @@ def train(scene, cfg: TrainConfig, *, ply_path=None, metrics_path=None, decision
     stepper = None if cfg.pose_opt else TrainStep(gset, cfg, extent=scene.extent, optimizer=opt,
                                                   deterministic=cfg.deterministic)
     train_cams = [scene.cameras[int(i)] for i in pool]
-    if stepper is not None:
-        stepper.reserve(train_cams)  # pair capacity for the largest training view
     pose_t = {k: torch.zeros((1, 3), dtype=torch.float32, device=_device())
               for k in ("pose_rot", "pose_trans")}
     metrics, pending, decision_rows = [], [], []
     stop_reason = "completed"
     start = time.perf_counter()
+    if stepper is not None:
+        # pair capacity for the largest training view (one host read; on the
+        # budget clock, like the reference's first-iteration setup)
+        stepper.reserve(train_cams)
     iteration = 0
 
     def flush():
