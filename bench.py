@@ -33,6 +33,11 @@ CONFIGS = {
     "c1": dict(n=10_000, width=256, height=256, clustered=False),
     "c2": dict(n=1_000_000, width=1920, height=1080, clustered=False),
     "c3": dict(n=3_000_000, width=1920, height=1080, clustered=True),
+    # C3 with a low-opacity cluster (U(0.005, 0.03)): the
+    # cluster tiles need thousands of blends per pixel before terminating,
+    # the heavy-tile stress case for K3/K4 load balance
+    "c3lo": dict(n=3_000_000, width=1920, height=1080, clustered=True,
+                 cluster_opacity=(0.005, 0.03)),
     # BASELINE configs[3]: a batch of 8 ring views per optimizer step, split
     # across the GPUs (strong scaling), one gradient allreduce per step
     "c4": dict(n=1_000_000, width=1920, height=1080, clustered=False, views=8),
@@ -270,7 +275,8 @@ def cpu_baseline(cfg_name, target_s=20.0):
     """Single-core oracle, bounded sample (~10-30 s of CPU work)."""
     from paper_2601_19489_b200.synthetic import make_scene
     c = CONFIGS[cfg_name]
-    scene = make_scene(c["n"], c["width"], c["height"], seed=0, clustered=c["clustered"])
+    scene = make_scene(c["n"], c["width"], c["height"], seed=0, clustered=c["clustered"],
+                       cluster_opacity=c.get("cluster_opacity"))
     frac = 0.01 if c["n"] >= 1_000_000 else 0.25
     t0 = time.perf_counter()
     est, stages, sample = _cpu_sample_step(scene, frac)
@@ -293,7 +299,8 @@ def reference_arm(args):
         return
     from paper_2601_19489_b200.synthetic import make_scene
     c = CONFIGS[args.config]
-    scene = make_scene(c["n"], c["width"], c["height"], seed=0, clustered=c["clustered"])
+    scene = make_scene(c["n"], c["width"], c["height"], seed=0, clustered=c["clustered"],
+                       cluster_opacity=c.get("cluster_opacity"))
     cores = len(os.sched_getaffinity(0))
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     gauss_frac = 1.0 / 16 if c["n"] >= 1_000_000 else 1.0
@@ -341,7 +348,8 @@ def _workload(name, n_gpus):
     c = CONFIGS[name]
     views = (f"a batch of {c['views']} ring views per step split over the GPUs, one "
              f"gradient allreduce" if c.get("views") else "one view per GPU per step")
-    return (f"{c['n']:,} Gaussians{' (clustered depth)' if c['clustered'] else ''}, "
+    lo = " low-opacity" if c.get("cluster_opacity") else ""
+    return (f"{c['n']:,} Gaussians{f' ({lo} clustered depth)'.replace('( ', '(') if c['clustered'] else ''}, "
             f"{c['width']}x{c['height']}, SH0, {views}, "
             f"fwd+loss+bwd+Adam, {n_gpus} GPU(s)")
 
@@ -370,7 +378,8 @@ def gpu_arm(args):
             dist.init_process_group(backend)
     c = CONFIGS[args.config]
     params, cam, gt = make_scene(c["n"], c["width"], c["height"], seed=0,
-                                 clustered=c["clustered"])
+                                 clustered=c["clustered"],
+                                 cluster_opacity=c.get("cluster_opacity"))
     gset = ts.GaussianSet(**params)
     batch_views = c.get("views", 0)
     ring = ring_poses(batch_views or max(world, 1), 4.0, cam["fx"], c["width"], c["height"])

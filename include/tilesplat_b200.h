@@ -320,6 +320,22 @@ int tsr_preprocess_bwd_adam_ex(const tsr_gaussians_t* g, const tsr_camera_t* cam
                                unsigned long long* skipped, const int32_t* gate,
                                int32_t* gated_steps, const float* loss_guard, void* stream);
 
+/* ---------------------------------------------------------- depth chain ----
+ * Disparity loss on the normalised render depth and its chain to the raster
+ * outputs (losses.py:94-112 + trainer.py:201-214): mask = n_contrib > 0
+ * [& valid (u8, nullable)], d = depth / (1 - final_T), L = w mean_mask
+ * |1/max(d,eps) - 1/max(prior,eps)|, grad_depth / grad_final_T written for
+ * every pixel (zero outside the mask).  The weight is *weight_dev when not
+ * NULL (graph replay), else `weight`.  loss_out / total_out (nullable, device
+ * scalars): L and *e_photo + L.  workspace: tsr_depth_chain_workspace()
+ * bytes, zero-filled once before the first call (it re-arms itself). */
+size_t tsr_depth_chain_workspace(void);
+int tsr_depth_chain(const float* depth, const float* final_T, const int32_t* n_contrib,
+                    const float* prior, const uint8_t* valid, int32_t height, int32_t width,
+                    float weight, const float* weight_dev, const float* e_photo, float* loss_out,
+                    float* total_out, float* grad_depth, float* grad_final_T, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
 /* --------------------------------------------------------------- loss ----
  * Fused photometric objective (losses.py:44-91): E = (1-lam) mean|r-g| +
  * lam (1 - SSIM), 11-tap sigma=1.5 Gaussian window, zero padding.  rendered,

@@ -95,6 +95,9 @@ _SIGNATURES = {
                                            ctypes.POINTER(Camera_t), c_vp, c_vp, c_vp,
                                            ctypes.POINTER(AdamGroup_t), c_vp, c_vp, c_vp, c_vp,
                                            c_vp, c_vp, c_vp]),
+    "tsr_depth_chain_workspace": (c_sz, []),
+    "tsr_depth_chain": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_f32, c_vp, c_vp,
+                                c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "tsr_photometric_workspace": (c_sz, [c_i32, c_i32]),
     "tsr_photometric": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_f32, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "tsr_version": (ctypes.c_char_p, []),

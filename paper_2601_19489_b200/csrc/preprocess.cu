@@ -300,17 +300,35 @@ __global__ void __launch_bounds__(kScanBlock) cull_compact_kernel(
 }
 
 // (b) projection + colour + exact pair count into the compacted rows.
-__global__ void __launch_bounds__(kScanBlock, 4) preprocess_kernel(
+template <bool kLB>
+__global__ void __launch_bounds__(kScanBlock, kLB ? 3 : 4) preprocess_kernel(
     tsr_gaussians_t g, tsr_camera_t cam, int strategy, float4* __restrict__ rec_out,
     const int32_t* __restrict__ row_of_source, int32_t* __restrict__ counts,
     uint32_t* __restrict__ depth_bits, uint4* __restrict__ spans,
     unsigned long long* __restrict__ total_pairs) {
   __shared__ unsigned long long s_sum[kScanBlock / 32];
+  __shared__ LbWarp s_lb[kLB ? kScanBlock / 32 : 1];
   const long long i = (long long)blockIdx.x * kScanBlock + threadIdx.x;
   const int tiles_x = tiles_of(cam.width), tiles_y = tiles_of(cam.height);
   long long cnt = 0;
   const int row = i < g.n ? row_of_source[i] : -1;
-  if (row >= 0) {
+  if (kLB) {
+    float rec[12] = {};
+    uint4 span;
+    if (row >= 0) project_one(g, cam, i, rec);
+    // warp-cooperative: every lane of the warp takes part
+    cnt = warp_count_lb(load_splat_f64(rec), row >= 0, tiles_x, tiles_y, span,
+                        s_lb[threadIdx.x >> 5]);
+    if (row >= 0) {
+      float4* dst = rec_out + (long long)row * 3;
+      dst[0] = make_float4(rec[0], rec[1], rec[2], rec[3]);
+      dst[1] = make_float4(rec[4], rec[5], rec[6], rec[7]);
+      dst[2] = make_float4(rec[8], rec[9], rec[10], rec[11]);
+      counts[row] = (int32_t)cnt;
+      depth_bits[row] = __float_as_uint(rec[6]);
+      spans[row] = span;
+    }
+  } else if (row >= 0) {
     float rec[12];
     project_one(g, cam, i, rec);
     uint4 span;
@@ -341,11 +359,19 @@ __global__ void __launch_bounds__(kScanBlock) count_kernel(
     int32_t* __restrict__ counts, uint32_t* __restrict__ depth_bits, uint4* __restrict__ spans,
     unsigned long long* __restrict__ total_pairs) {
   __shared__ unsigned long long s_sum[kScanBlock / 32];
+  __shared__ LbWarp s_lb[kScanBlock / 32];
   const long long i = (long long)blockIdx.x * kScanBlock + threadIdx.x;
   long long cnt = 0;
+  uint4 span;
+  if (strategy == 1) {
+    SplatF64 sf{};
+    if (i < m) sf = load_splat_f64(rec + i * 12);
+    cnt = warp_count_lb(sf, i < m, tiles_of(width), tiles_of(height), span,
+                        s_lb[threadIdx.x >> 5]);
+  }
   if (i < m) {
-    uint4 span;
-    cnt = count_pairs_of(rec + i * 12, strategy, tiles_of(width), tiles_of(height), span);
+    if (strategy != 1)
+      cnt = count_pairs_of(rec + i * 12, strategy, tiles_of(width), tiles_of(height), span);
     counts[i] = (int32_t)cnt;
     depth_bits[i] = __float_as_uint(rec[i * 12 + 6]);
     spans[i] = span;
@@ -409,7 +435,8 @@ extern "C" int tsr_preprocess_fwd(const tsr_gaussians_t* g, const tsr_camera_t* 
   cull_compact_kernel<<<cull_blocks, kScanBlock, 0, s>>>(*g, *cam, source_ids, row_of_source,
                                                          totals, status, ticket, cull_blocks);
   TSR_CHECK_LAUNCH();
-  preprocess_kernel<<<blocks, kScanBlock, 0, s>>>(*g, *cam, strategy, (float4*)rec,
+  auto* pk = strategy == 1 ? preprocess_kernel<true> : preprocess_kernel<false>;
+  pk<<<blocks, kScanBlock, 0, s>>>(*g, *cam, strategy, (float4*)rec,
                                                   row_of_source, counts, depth_bits,
                                                   (uint4*)spans,
                                                   (unsigned long long*)(totals + 1));

@@ -9,8 +9,9 @@
 //      exponent byte -- is skipped) -> depth rank of every row; rank order
 //      == (depth bits, row) order, exactly the reference's tie rule;
 //   2. rank-major emission of (key = tile << 32 | depth bits, value = row)
-//      pairs from K1's compact column spans (rows whose span did not fit the
-//      16-byte record, and the load-balanced strategy, re-walk in FP64),
+//      pairs from K1's compact column spans (written by both SnugBox
+//      strategies; rows whose span did not fit the 16-byte record re-walk
+//      in FP64),
 //      staged in shared memory so every CTA stores its contiguous output
 //      range coalesced;
 //   3. stable LSD radix sort of the pairs by the tile bits only (1-2 passes
@@ -49,6 +50,7 @@ constexpr int kEmitPer = 2;              // ranks per thread per emission block
 constexpr int kEmitRanks = kSB * kEmitPer;
 constexpr int kStage = 4096;             // staged pairs per emission window
 constexpr int kDynSmem = 49152;          // staging: 4096 x (u64 key, u32 row)
+static_assert((kSB / 32) * sizeof(LbWarp) <= kDynSmem, "LB re-walk scratch in the staging area");
 constexpr int kMaxGrid = 2048;
 constexpr int kMaxBarriers = 32;
 constexpr int kMaxTiles = 1 << 16;
@@ -485,10 +487,25 @@ __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, lon
       if (r0 == rlo && w0 == 0) TSR_TRACE_AT(46);
     }
     if (r0 == rlo) TSR_TRACE_AT(42);
-    // exact FP64 re-walk (span overflow, or the load-balanced min-q test)
+    // exact FP64 re-walk of the rows whose span record overflowed
+    if (strategy == 1) {
+      // load-balanced strategy: the warp-cooperative round-robin min-q walk
+      // (bin_load_balanced, binning.py:262-298), writing each splat's passing
+      // tiles at its emission offset; the staging area is free here
+      LbWarp* lbw = reinterpret_cast<LbWarp*>(dyn) + (threadIdx.x >> 5);
+#pragma unroll
+      for (int k = 0; k < kEmitPer; ++k) {
+        const long long r = r0 + kEmitPer * tid + k;
+        const bool v = r < rhi && (sp[k].y >> 31) && cnt[k] != 0;
+        SplatF64 s{};
+        if (v) s = load_splat_f64(a.rec + (long long)row[k] * 12);
+        warp_emit_lb(s, v, tiles_x, tiles_y, dep[k], row[k], O + off[k], p_cap, pairs,
+                     pair_rows, *lbw);
+      }
+    }
 #pragma unroll
     for (int k = 0; k < kEmitPer; ++k) {
-      if (!(sp[k].y >> 31) || cnt[k] == 0) continue;
+      if (strategy == 1 || !(sp[k].y >> 31) || cnt[k] == 0) continue;
       const unsigned long long depk = dep[k];
       long long out = O + off[k];
       SplatF64 s = load_splat_f64(a.rec + (long long)row[k] * 12);
@@ -619,7 +636,6 @@ __global__ void __launch_bounds__(kSB, 3) build_index_kernel(IndexArgs a) {
       for (int j = 0; j < 4; ++j) {
         const long long r = r0 + j * kSB;
         if (r >= rhi) continue;
-        if (a.strategy == 1) sp[j].y |= 1u << 31;
         uint32_t c;
         if (sp[j].y >> 31) {
           c = (uint32_t)a.counts[row[j]];

@@ -185,6 +185,256 @@ __device__ __forceinline__ double min_q_box(const SplatF64& s, double rx0, doubl
                npmin(q(x_at_y0, ry0), q(x_at_y1, ry1)));
 }
 
+// ---- load-balanced writing, warp-cooperative (bin_load_balanced,
+// binning.py:262-298; lane_test_counts :289-298) ------------
+// The 32 lanes of a warp each own one splat.  The candidate tiles of the 32
+// SnugBox rectangles (column-major) are flattened into one list and the
+// lanes test it round-robin, 32 candidates per round, each with the FP64
+// min-q box test (min_q_box <= t).  So a warp spends rounds in proportion to
+// its splats' total candidate count, not to the largest rectangle (the
+// per-thread loop's divergence).  Per (splat, column) the passing rows are a
+// run (the level set is convex); the owner gets its exact count plus the
+// same compact span record the sequential walk writes, so the emission in
+// sort.cu needs no FP64 re-walk for this strategy either (a span that does
+// not fit, or a non-contiguous column, keeps the overflow bit: re-walk).
+struct LbSplat {
+  double mx, my, a, b, c, t, bc, ba;  // bc = -(b / c), ba = -(b / a): per-splat constants
+  int tx0, ty0, ncols, nrows;
+  float inv_rows;  // 1 / nrows (FP32)
+};
+
+// column-major candidate j of a rectangle with nrows rows -> (column, row).
+// (j + 1/2) / nrows is at least 1 / (2 nrows) from an integer; the FP32
+// product's error is below 2.4e-7 x column, so truncation equals j / nrows
+// whenever ncols x nrows <= 2^16 (every rectangle: there are < 2^16 tiles).
+__device__ __forceinline__ void lb_cell(const LbSplat& S, int j, int& c, int& rr) {
+  c = __float2int_rz(((float)j + 0.5f) * S.inv_rows);
+  rr = j - c * S.nrows;
+}
+
+// min_q_box (binning.py:241-259) with the splat's two divides and 2 b hoisted
+// (the same FP64 values the per-box form computes -- 2.0 * b is exact -- so
+// decisions are identical).  The batch is finite here (projected splats), so
+// the clips use plain min/max (NumPy's NaN propagation never triggers).
+__device__ __forceinline__ double min_q_box_lb(const LbSplat& S, double rx0, double rx1,
+                                               double ry0, double ry1) {
+  if ((rx0 <= 0.0) && (0.0 <= rx1) && (ry0 <= 0.0) && (0.0 <= ry1)) return 0.0;
+  const double b2 = dmul(2.0, S.b);
+  auto q = [&](double dx, double dy) {
+    const double t0 = dmul(dmul(S.a, dx), dx);
+    const double t1 = dmul(dmul(b2, dx), dy);
+    const double t2 = dmul(dmul(S.c, dy), dy);
+    return dadd(dadd(t0, t1), t2);
+  };
+  auto clip = [](double v, double lo, double hi) { return fmin(fmax(v, lo), hi); };
+  const double y0 = clip(dmul(S.bc, rx0), ry0, ry1), y1 = clip(dmul(S.bc, rx1), ry0, ry1);
+  const double x0 = clip(dmul(S.ba, ry0), rx0, rx1), x1 = clip(dmul(S.ba, ry1), rx0, rx1);
+  return fmin(fmin(q(rx0, y0), q(rx1, y1)), fmin(q(x0, ry0), q(x1, ry1)));
+}
+struct LbWarp {
+  LbSplat sp[32];
+  unsigned cnt[32];
+  unsigned char ccnt[32][8];    // passing rows per (splat, column < 8)
+  unsigned char cstart[32][8];  // first passing row (255: none yet)
+  unsigned bad;                 // splats whose span cannot be encoded
+};
+
+__device__ __forceinline__ long long warp_count_lb(const SplatF64& s, bool valid, int tiles_x,
+                                                   int tiles_y, uint4& span, LbWarp& w) {
+  const int lane = threadIdx.x & 31;
+  SnugRect r;
+  int ncols = 0, nrows = 0;
+  if (valid) {
+    r = snugbox(s, tiles_x, tiles_y);
+    if (r.tx0 <= r.tx1 && r.ty0 <= r.ty1) {
+      ncols = (int)(r.tx1 - r.tx0 + 1);
+      nrows = (int)(r.ty1 - r.ty0 + 1);
+    }
+  }
+  w.sp[lane] = LbSplat{s.mx, s.my, s.a, s.b, s.c, s.t,
+                       ncols ? -ddiv(s.b, s.c) : 0.0, ncols ? -ddiv(s.b, s.a) : 0.0,
+                       ncols ? (int)r.tx0 : 0, ncols ? (int)r.ty0 : 0, ncols, nrows,
+                       nrows ? 1.0f / (float)nrows : 0.f};
+  w.cnt[lane] = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    w.ccnt[lane][c] = 0;
+    w.cstart[lane][c] = 255;
+  }
+  if (lane == 0) w.bad = 0;
+  const int area = ncols * nrows;
+  int incl = area;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  const int offs = incl - area;
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  __syncwarp();
+  bool carry = false;  // pass of the previous candidate (last lane of the last round)
+  for (int base = 0; base < total; base += 32) {
+    const int k = base + lane;
+    const bool active = k < total;
+    // owner = the last lane whose offset is <= k (offsets are non-decreasing)
+    int o = 0;
+#pragma unroll
+    for (int st = 16; st > 0; st >>= 1) {
+      const int v = __shfl_sync(0xffffffffu, offs, (o + st) & 31);
+      if (o + st < 32 && v <= k) o += st;
+    }
+    const int ob = __shfl_sync(0xffffffffu, offs, o);
+    bool pass = false;
+    int c = 0, rr = 0;
+    if (active) {
+      const LbSplat& S = w.sp[o];
+      const int j = k - ob;
+      lb_cell(S, j, c, rr);
+      const double rx0 = dsub((double)(16 * (S.tx0 + c)), S.mx);
+      const double ry0 = dsub((double)(16 * (S.ty0 + rr)), S.my);
+      pass = min_q_box_lb(S, rx0, dadd(rx0, 16.0), ry0, dadd(ry0, 16.0)) <= S.t;
+    }
+    bool prev = __shfl_up_sync(0xffffffffu, pass, 1);
+    if (lane == 0) prev = carry;
+    const bool start = pass && (rr == 0 || !prev);
+    const bool head = active && (lane == 0 || rr == 0);  // a new (splat, column) run
+    const unsigned pb = __ballot_sync(0xffffffffu, pass);
+    const unsigned sb = __ballot_sync(0xffffffffu, start);
+    const unsigned hb = __ballot_sync(0xffffffffu, head);
+    carry = __shfl_sync(0xffffffffu, pass, 31);
+    if (head) {
+      const unsigned above = hb & ~((2u << lane) - 1u);  // (2 << 31) wraps to 0: all bits
+      const int next = lane == 31 ? 32 : (above ? __ffs(above) - 1 : 32);
+      const unsigned seg = (next == 32 ? 0xffffffffu : ((1u << next) - 1u)) & ~((1u << lane) - 1u);
+      const unsigned np = __popc(pb & seg), ns = __popc(sb & seg);
+      atomicAdd(&w.cnt[o], np);  // one head per (splat, column): several per splat
+      if (c < 8) {
+        w.ccnt[o][c] += (unsigned char)np;
+        if (ns) {
+          if (ns > 1 || w.cstart[o][c] != 255) {
+            atomicOr(&w.bad, 1u << o);
+          } else {
+            w.cstart[o][c] = (unsigned char)(rr + (__ffs(sb & seg) - 1 - lane));
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  const long long count = w.cnt[lane];
+  span = make_uint4(0u, 0u, 0u, 0u);
+  if (ncols) {
+    span.x = (uint32_t)(r.tx0 & 0xffff) | ((uint32_t)(ncols < 255 ? ncols : 255) << 16);
+    span.y = (uint32_t)(r.ty0 & 0xffff);
+    bool fits = ncols <= 8 && !((w.bad >> lane) & 1u);
+    for (int c = 0; fits && c < ncols; ++c) {
+      const unsigned nr = w.ccnt[lane][c];
+      const unsigned off = nr ? w.cstart[lane][c] : 0u;
+      if (nr > 15 || off > 15) {
+        fits = false;
+        break;
+      }
+      const uint32_t code = (off & 15u) | (nr << 4);
+      if (c < 4) span.z |= code << (8 * c);
+      else span.w |= code << (8 * (c - 4));
+    }
+    if (!fits) span = make_uint4(span.x, span.y | (1u << 31), 0u, 0u);
+  }
+  __syncwarp();  // w is reused by the next call
+  return count;
+}
+
+
+// The same round-robin walk, emitting: every passing candidate of splat o is
+// written as (tile << 32 | key_lo[o], row[o]) at out_base[o] + (passing
+// candidates of o before it, column-major) -- the rank-major emission's
+// FP64 re-walk for rows whose span record overflowed (sort.cu).  All 32
+// lanes call; `valid` lanes own a splat.
+__device__ __forceinline__ void warp_emit_lb(const SplatF64& s, bool valid, int tiles_x,
+                                             int tiles_y, unsigned long long key_lo,
+                                             uint32_t row, long long out_base, long long p_cap,
+                                             unsigned long long* __restrict__ pairs,
+                                             uint32_t* __restrict__ pair_rows, LbWarp& w) {
+  const int lane = threadIdx.x & 31;
+  SnugRect r;
+  int ncols = 0, nrows = 0;
+  if (valid) {
+    r = snugbox(s, tiles_x, tiles_y);
+    if (r.tx0 <= r.tx1 && r.ty0 <= r.ty1) {
+      ncols = (int)(r.tx1 - r.tx0 + 1);
+      nrows = (int)(r.ty1 - r.ty0 + 1);
+    }
+  }
+  w.sp[lane] = LbSplat{s.mx, s.my, s.a, s.b, s.c, s.t,
+                       ncols ? -ddiv(s.b, s.c) : 0.0, ncols ? -ddiv(s.b, s.a) : 0.0,
+                       ncols ? (int)r.tx0 : 0, ncols ? (int)r.ty0 : 0, ncols, nrows,
+                       nrows ? 1.0f / (float)nrows : 0.f};
+  w.cnt[lane] = 0;  // passing candidates written so far
+  const int area = ncols * nrows;
+  int incl = area;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  const int offs = incl - area;
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  __syncwarp();
+  for (int base = 0; base < total; base += 32) {
+    const int k = base + lane;
+    const bool active = k < total;
+    int o = 0;
+#pragma unroll
+    for (int st = 16; st > 0; st >>= 1) {
+      const int v = __shfl_sync(0xffffffffu, offs, (o + st) & 31);
+      if (o + st < 32 && v <= k) o += st;
+    }
+    const int ob = __shfl_sync(0xffffffffu, offs, o);
+    const long long ob_out = __shfl_sync(0xffffffffu, out_base, o);
+    const unsigned long long ok = __shfl_sync(0xffffffffu, key_lo, o);
+    const uint32_t orow = __shfl_sync(0xffffffffu, row, o);
+    bool pass = false;
+    int tile = 0;
+    if (active) {
+      const LbSplat& S = w.sp[o];
+      const int j = k - ob;
+      int c, rr;
+      lb_cell(S, j, c, rr);
+      const double rx0 = dsub((double)(16 * (S.tx0 + c)), S.mx);
+      const double ry0 = dsub((double)(16 * (S.ty0 + rr)), S.my);
+      pass = min_q_box_lb(S, rx0, dadd(rx0, 16.0), ry0, dadd(ry0, 16.0)) <= S.t;
+      tile = (S.ty0 + rr) * tiles_x + S.tx0 + c;
+    }
+    const unsigned pb = __ballot_sync(0xffffffffu, pass);
+    // lanes of o's segment in this round: [max(ob - base, 0), lane)
+    const int seg0 = ob - base > 0 ? ob - base : 0;
+    const unsigned below = ((1u << lane) - 1u) & ~((1u << seg0) - 1u);
+    if (pass) {
+      const long long g = ob_out + w.cnt[o] + __popc(pb & below);
+      if (g < p_cap) {
+        pairs[g] = ((unsigned long long)(uint32_t)tile << 32) | ok;
+        pair_rows[g] = orow;
+      }
+    }
+    __syncwarp();
+    // per-splat running counts: every passing lane's owner gains one; the
+    // lowest lane of each owner segment adds its segment's total
+    {
+      const bool first = active && (lane == 0 || k == ob);
+      const unsigned fb = __ballot_sync(0xffffffffu, first);
+      if (first) {
+        const unsigned above = fb & ~((2u << lane) - 1u);
+        const int next = lane == 31 ? 32 : (above ? __ffs(above) - 1 : 32);
+        const unsigned seg = (next == 32 ? 0xffffffffu : ((1u << next) - 1u)) &
+                             ~((1u << lane) - 1u);
+        w.cnt[o] += __popc(pb & seg);
+      }
+    }
+    __syncwarp();
+  }
+  __syncwarp();  // w is reused by the next call
+}
+
 // ------------------------------------------------------------------ FP32 --
 // Alpha of one (pixel, splat) evaluation (splat_alpha, forward.py:71-84) on
 // the prescaled conic (a', b2', c') = kQScale * (a, 2b, c) (b2' = 2 b' is

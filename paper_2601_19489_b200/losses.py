@@ -107,27 +107,51 @@ def disparity_loss(rendered_depth, prior_depth, valid_mask, weight: float):
     return loss, grad
 
 
-def depth_chain_device(depth, final_T, n_contrib, prior, valid, weight: float):
-    """Sync-free disparity loss + its chain through d_norm = D / (1 - T_f)
-    (losses.py:94-112, trainer.py:201-214) for the fused training step:
-    returns (loss 0-d tensor, grad_depth, grad_final_T), all on the device."""
-    mask = n_contrib > 0
+class DepthChainWorkspace:
+    """Scratch of the depth-chain kernels (block partials + a self-resetting
+    ticket); zero-filled once."""
+
+    def __init__(self):
+        self.buf = None
+
+    def get(self, device) -> torch.Tensor:
+        if self.buf is None or self.buf.device != device:
+            n = int(_lib.load().tsr_depth_chain_workspace())
+            self.buf = torch.zeros(n, dtype=torch.uint8, device=device)
+        return self.buf
+
+
+_default_dc_ws = DepthChainWorkspace()
+
+
+def depth_chain_device(depth, final_T, n_contrib, prior, valid, weight, e_photo=None,
+                       workspace: DepthChainWorkspace | None = None):
+    """Disparity loss + its chain through d_norm = D / (1 - T_f) (losses.py:
+    94-112, trainer.py:201-214) in two sync-free kernels (csrc/depth.cu).
+    weight: a float or a device scalar tensor (graph replay).  Returns
+    (loss, grad_depth, grad_final_T) as device tensors; with e_photo (device
+    scalar) the fourth value is e_photo + loss (the step's total), else None."""
+    lib = _lib.load()
+    d = as_device_f32(depth)
+    h, w = int(d.shape[0]), int(d.shape[1])
+    t = as_device_f32(final_T)
+    nb = n_contrib.to(torch.int32).contiguous()
+    p = as_device_f32(prior)
+    v = None
     if valid is not None:
-        mask = mask & valid
-    denom = 1.0 - final_T
-    one = torch.ones_like(denom)
-    d = torch.where(mask, depth / torch.where(mask, denom, one), torch.zeros_like(depth))
-    n_valid = mask.sum().clamp(min=1).to(torch.float32)
-    d_r = torch.clamp(d, min=DISPARITY_EPS)
-    d_p = torch.clamp(prior, min=DISPARITY_EPS)
-    diff = 1.0 / d_r - 1.0 / d_p
-    loss = weight * torch.where(mask, diff.abs(), torch.zeros_like(diff)).sum() / n_valid
-    g = weight * torch.sign(diff) * (-1.0 / (d_r * d_r)) / n_valid
-    g = torch.where(mask & (d >= DISPARITY_EPS), g, torch.zeros_like(g))
-    grad_depth = torch.where(mask, g / torch.where(mask, denom, one), torch.zeros_like(g))
-    grad_final_T = torch.where(mask, g * depth / torch.where(mask, denom * denom, one),
-                               torch.zeros_like(g))
-    return loss, grad_depth, grad_final_T
+        v = valid if isinstance(valid, torch.Tensor) else torch.as_tensor(np.asarray(valid))
+        v = v.to(d.device).bool().contiguous()
+    w_dev = weight if isinstance(weight, torch.Tensor) else None
+    out = torch.empty(2, dtype=torch.float32, device=d.device)
+    gd = torch.empty_like(d)
+    gt = torch.empty_like(d)
+    ws = (workspace or _default_dc_ws).get(d.device)
+    _lib.check(lib.tsr_depth_chain(
+        d.data_ptr(), t.data_ptr(), nb.data_ptr(), p.data_ptr(), _lib.ptr(v), h, w,
+        0.0 if w_dev is not None else float(weight), _lib.ptr(w_dev),
+        _lib.ptr(e_photo), out[0].data_ptr(), out[1].data_ptr(), gd.data_ptr(), gt.data_ptr(),
+        ws.data_ptr(), ws.numel(), _lib.stream_handle()), "tsr_depth_chain")
+    return out[0], gd, gt, (out[1] if e_photo is not None else None)
 
 
 def depth_weight_schedule(iteration: int, max_iter: int, w0: float = 0.1) -> float:

@@ -103,10 +103,13 @@ def synthetic_scene(n_splats: int = 10, n_views: int = 5, width: int = 48, heigh
     return scene, gt_set
 
 
-def make_scene(n, width, height, seed=0, clustered=False, sh_degree=0):
+def make_scene(n, width, height, seed=0, clustered=False, sh_degree=0, cluster_opacity=None):
     """Canonical synthetic scene of SURVEY.md §8(d).  Every parameter is made
     FP32-representable so the CPU oracle and the FP32 device see identical
-    inputs."""
+    inputs.  cluster_opacity=(lo, hi) redraws the clustered half's opacities
+    from U(lo, hi) -- the low-opacity "C3-lo" stress case of SURVEY §7.3 #4,
+    whose cluster tiles need thousands of blends per pixel to terminate (drawn
+    after everything else, so the other parameters equal C3's)."""
     rng = np.random.default_rng(seed)
     fx = 1600.0 * width / 1920.0
     pos = rng.uniform(-1.0, 1.0, (n, 3)) * np.array([1.5, 1.5 * height / width, 1.0])
@@ -124,6 +127,10 @@ def make_scene(n, width, height, seed=0, clustered=False, sh_degree=0):
     if C > 1:
         colors[:, 1:, :] = rng.normal(0.0, 0.05, (n, C - 1, 3))
     gt = rng.uniform(0.0, 1.0, (height, width, 3))
+    if clustered and cluster_opacity is not None:
+        lo, hi = cluster_opacity
+        oc = rng.uniform(lo, hi, n - n // 2)
+        logits[n // 2:] = np.log(oc / (1.0 - oc))
     f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)  # noqa: E731
     params = dict(positions=f32(pos), log_scales=f32(log_scales), rotations=f32(q),
                   opacity_logits=f32(logits), colors=f32(colors))

@@ -152,18 +152,11 @@ def view_loss_and_grads(camera: Camera, cfg: TrainConfig, vr: ViewRender,
     grad_depth = grad_final_T = None
     depth_loss = 0.0
     if depth_weight > 0.0 and camera.depth_prior is not None:
-        mask = bufs.n_contrib > 0
-        if camera.depth_valid is not None:
-            mask &= torch.as_tensor(camera.depth_valid, device=mask.device).bool()
-        d_norm = bufs.normalized_depth()
-        depth_loss, g_dnorm = losses.disparity_loss(d_norm, camera.depth_prior, mask,
-                                                    depth_weight)
-        denom = 1.0 - bufs.final_T
-        one = torch.ones_like(denom)
-        grad_depth = torch.where(mask, g_dnorm / torch.where(mask, denom, one),
-                                 torch.zeros_like(denom))
-        grad_final_T = torch.where(mask, g_dnorm * bufs.depth / torch.where(mask, denom ** 2, one),
-                                   torch.zeros_like(denom))
+        # fused disparity loss + chain through d_norm = D / (1 - T_f)
+        dl, grad_depth, grad_final_T, _ = losses.depth_chain_device(
+            bufs.depth, bufs.final_T, bufs.n_contrib, camera.depth_prior, camera.depth_valid,
+            depth_weight)
+        depth_loss = float(dl.item())
     g2 = backward_per_gaussian(bufs, vr.batch, vr.tiles, vr.colors, grad_color, grad_depth,
                                grad_final_T)
     report = losses.LossReport(l1=report.l1, ssim=report.ssim, photometric=report.photometric,
@@ -251,6 +244,7 @@ class TrainStep:
         self.loss_ws = losses.PhotometricWorkspace()
         from .backward import BackwardWorkspace
         self.bwd_ws = BackwardWorkspace()
+        self.dc_ws = losses.DepthChainWorkspace()
         self._grad2d_clean = True  # the SH-0 fused kernel re-zeroes consumed rows
         self.grad_color = None
         # step status read back without kernels: two D2H copy nodes into
@@ -389,9 +383,9 @@ class TrainStep:
         # (a tensor weight comes from graph capture: no host read of it)
         if depth_prior is not None and (isinstance(depth_weight, torch.Tensor)
                                         or depth_weight > 0.0):
-            dl, gd, gt = losses.depth_chain_device(out.depth, out.final_T, out.n_contrib,
-                                                   depth_prior, depth_valid, depth_weight)
-            e = e + dl
+            dl, gd, gt, e = losses.depth_chain_device(out.depth, out.final_T, out.n_contrib,
+                                                      depth_prior, depth_valid, depth_weight,
+                                                      e_photo=e, workspace=self.dc_ws)
         self.last_losses = (e, l1, s, dl)
         self._mark(timer, "loss")
         from .backward import K4_FORM

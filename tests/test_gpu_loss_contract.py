@@ -91,3 +91,49 @@ def test_psnr_values():
     assert psnr(np.zeros((10, 10, 3)), np.full((10, 10, 3), 0.1)) == pytest.approx(20.0, abs=1e-5)
     assert psnr(np.full((8, 8, 3), 0.5), np.zeros((8, 8, 3))) == pytest.approx(
         -10 * np.log10(0.25), abs=1e-5)
+
+
+@pytest.mark.parametrize("with_valid", [False, True])
+def test_fused_depth_chain_matches_reference_formula(with_valid):
+    """csrc/depth.cu (disparity loss on D / (1 - T_f) + its chain,
+    trainer.py:201-214) against the reference's float64 formula on random
+    buffers with masked, empty (n_contrib = 0) and d < eps pixels."""
+    import torch
+    from paper_2601_19489_b200 import losses
+    rng = np.random.default_rng(3)
+    H, W = 67, 91
+    depth = rng.uniform(0.0, 5.0, (H, W))
+    final_T = rng.uniform(0.0, 0.95, (H, W))
+    depth[:3] = 1e-7  # d < eps: zero gradient
+    n_contrib = rng.integers(0, 4, (H, W))
+    prior = rng.uniform(0.5, 8.0, (H, W))
+    valid = rng.uniform(size=(H, W)) > 0.3 if with_valid else None
+    w = 0.37
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)  # noqa: E731
+    depth, final_T, prior = f32(depth), f32(final_T), f32(prior)
+    mask = n_contrib > 0
+    if valid is not None:
+        mask &= valid
+    d = np.where(mask, depth / (1.0 - final_T), 0.0)
+    dr, dp = np.maximum(d, 1e-4), np.maximum(prior, 1e-4)
+    diff = 1.0 / dr - 1.0 / dp
+    n = mask.sum()
+    ref_loss = w * np.abs(diff)[mask].mean()
+    g = w * np.sign(diff) * (-1.0 / (dr * dr)) / n
+    g = np.where(mask & (d >= 1e-4), g, 0.0)
+    ref_gd = np.where(mask, g / (1.0 - final_T), 0.0)
+    ref_gt = np.where(mask, g * depth / (1.0 - final_T) ** 2, 0.0)
+    dev = lambda a, t=torch.float32: torch.as_tensor(a, dtype=t, device="cuda")  # noqa: E731
+    e = dev(np.array(0.25))
+    loss, gd, gt, total = losses.depth_chain_device(
+        dev(depth), dev(final_T), dev(n_contrib, torch.int32), dev(prior),
+        None if valid is None else dev(valid, torch.bool), w, e_photo=e)
+    assert abs(float(loss) - ref_loss) <= 1e-5 * ref_loss
+    assert abs(float(total) - (0.25 + ref_loss)) <= 1e-5
+    for got, ref in ((gd, ref_gd), (gt, ref_gt)):
+        got = got.cpu().numpy().astype(np.float64)
+        assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max()
+    # device weight (graph replay) and an empty mask
+    loss2, *_ = losses.depth_chain_device(dev(depth), dev(final_T), dev(n_contrib * 0, torch.int32),
+                                          dev(prior), None, dev(np.array(w)))
+    assert float(loss2) == 0.0
