@@ -163,6 +163,19 @@ int tsr_render_score(const float* rec, const int32_t* values, const int64_t* off
                      float* out_color, float* out_depth, float* out_final_T,
                      int32_t* out_n_contrib, int32_t* out_n_considered, void* stream);
 
+/* Launch order for the per-tile kernels: heavy tiles (list longer than 4x
+ * the mean) first in raster order, then the rest in raster order (one CTA;
+ * order is (n_tiles,) int32).  tsr_render_fwd_ordered / tsr_render_bwd_ordered
+ * take it (NULL: raster order) -- the same outputs, the heavy tiles no longer
+ * finish last (C3-lo). */
+int tsr_tile_order(const int64_t* offsets, int32_t n_tiles, int32_t* order, void* stream);
+int tsr_render_fwd_ordered(const float* rec, const int32_t* values, const int64_t* offsets,
+                           int32_t width, int32_t height, const float* background_host,
+                           float* out_color, float* out_depth, float* out_final_T,
+                           int32_t* out_n_contrib, int32_t* out_n_considered, float* ckpt,
+                           const int64_t* ckpt_base, int32_t ckpt_stride,
+                           const int32_t* tile_order, void* stream);
+
 /* ---------------------------------------------------------------- K4 ----
  * backward_per_gaussian (backward.py:137-223): a warp owns a supergroup of
  * 64 list positions (two checkpoint groups, lane j the splat pair 2j, 2j+1)
@@ -181,6 +194,12 @@ int tsr_render_score(const float* rec, const int32_t* values, const int64_t* off
  * heavy tiles spread over the whole GPU and no warp idles at a tile's end.
  * It needs a workspace of tsr_render_bwd_workspace(width, height, p_bound)
  * bytes, p_bound >= the pair count (a capacity is fine). */
+int tsr_render_bwd_ordered(const float* rec, const int32_t* values, const int64_t* offsets,
+                           int32_t width, int32_t height, const float* color, const float* depth,
+                           const float* final_T, const int32_t* n_considered, const float* ckpt,
+                           const int64_t* ckpt_base, const float* grad_color,
+                           const float* grad_depth, const float* grad_final_T, float* grad2d,
+                           unsigned long long* merges, const int32_t* tile_order, void* stream);
 size_t tsr_render_bwd_workspace(int32_t width, int32_t height, int64_t p_bound);
 int tsr_render_bwd_ws(const float* rec, const int32_t* values, const int64_t* offsets,
                       int32_t width, int32_t height, const float* color, const float* depth,

@@ -70,6 +70,12 @@ _SIGNATURES = {
     "tsr_render_bwd_det": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
                                    c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                    c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "tsr_tile_order": (c_i32, [c_vp, c_i32, c_vp, c_vp]),
+    "tsr_render_fwd_ordered": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, ctypes.POINTER(c_f32),
+                                       c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp,
+                                       c_vp]),
+    "tsr_render_bwd_ordered": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp,
+                                       c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tsr_render_bwd_workspace": (c_sz, [c_i32, c_i32, c_i64]),
     "tsr_render_bwd_ws": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
                                   c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_sz, c_vp]),

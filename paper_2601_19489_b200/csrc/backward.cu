@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
     const float* __restrict__ grad_color, const float* __restrict__ grad_depth,
     const float* __restrict__ grad_final_T, float* __restrict__ grad2d,
     unsigned long long* __restrict__ merges, float* __restrict__ slots,
-    int32_t* __restrict__ processed) {
+    int32_t* __restrict__ processed, const int32_t* __restrict__ order) {
   __shared__ float4 s_pa[kPixSlots];
   __shared__ float4 s_pb[kPixSlots];
   // byte offsets; the step count is rounded up to a multiple of 4, hence
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
   __shared__ int s_maxnc;
   __shared__ int s_next;
 
-  const int tile = blockIdx.x;
+  const int tile = order ? order[blockIdx.x] : (int)blockIdx.x;  // heavy tiles first
   const long long start = offsets[tile], end = offsets[tile + 1];
   const int n = (int)(end - start);
   if (n == 0) return;
@@ -799,7 +799,28 @@ extern "C" int tsr_render_bwd(const float* rec, const int32_t* values, const int
   k<<<tx * ty, kBwdThreads, 0, (cudaStream_t)stream>>>(
       (const float4*)rec, values, offsets, width, height, tx, color, depth, final_T,
       n_considered, ckpt, ckpt_base, grad_color, grad_depth, grad_final_T, grad2d, merges,
-      nullptr, nullptr);
+      nullptr, nullptr, nullptr);
+  TSR_CHECK_LAUNCH();
+  return TSR_OK;
+}
+
+extern "C" int tsr_render_bwd_ordered(const float* rec, const int32_t* values,
+                                      const int64_t* offsets, int32_t width, int32_t height,
+                                      const float* color, const float* depth,
+                                      const float* final_T, const int32_t* n_considered,
+                                      const float* ckpt, const int64_t* ckpt_base,
+                                      const float* grad_color, const float* grad_depth,
+                                      const float* grad_final_T, float* grad2d,
+                                      unsigned long long* merges, const int32_t* tile_order,
+                                      void* stream) {
+  if (width <= 0 || height <= 0 || !grad_color || !merges) return TSR_E_INVALID;
+  if (ckpt && !ckpt_base) return TSR_E_INVALID;
+  const int tx = tiles_of(width), ty = tiles_of(height);
+  auto* k = grad_depth ? render_bwd_kernel<true, false> : render_bwd_kernel<false, false>;
+  k<<<tx * ty, kBwdThreads, 0, (cudaStream_t)stream>>>(
+      (const float4*)rec, values, offsets, width, height, tx, color, depth, final_T,
+      n_considered, ckpt, ckpt_base, grad_color, grad_depth, grad_final_T, grad2d, merges,
+      nullptr, nullptr, tile_order);
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }
@@ -825,7 +846,7 @@ extern "C" int tsr_render_bwd_det(const float* rec, const int32_t* values, const
   k<<<tx * ty, kBwdThreads, 0, s>>>((const float4*)rec, values, offsets, width, height, tx,
                                     color, depth, final_T, n_considered, ckpt, ckpt_base,
                                     grad_color, grad_depth, grad_final_T, nullptr, merges, slots,
-                                    processed);
+                                    processed, nullptr);
   TSR_CHECK_LAUNCH();
   if (m > 0) {
     grad_reduce_kernel<<<(int)((m + 255) / 256), 256, 0, s>>>(

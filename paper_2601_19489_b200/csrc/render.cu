@@ -134,14 +134,15 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
     float bg_g, float bg_b, float* __restrict__ out_color, float* __restrict__ out_depth,
     float* __restrict__ out_T, int32_t* __restrict__ out_ncontrib,
     int32_t* __restrict__ out_ncons, float* __restrict__ ckpt,
-    const int64_t* __restrict__ ckpt_base, ScoreArgs sc) {
+    const int64_t* __restrict__ ckpt_base, ScoreArgs sc, const int32_t* __restrict__ order) {
   // per staged splat: [0] mx, my, opacity, depth  [1] prescaled conic a',
   // 2b', c'  [2] r, g, b, depth -- one base address per list entry
   __shared__ float4 s_spl[kBatch][3];
   __shared__ float4 s_raw[kBatch];  // a, b, c (unscaled), level t
   __shared__ int s_row[kScore ? kBatch : 1];
 
-  const int tile = blockIdx.x;
+  // heavy tiles first when an order is given (tile_order_kernel)
+  const int tile = order ? order[blockIdx.x] : (int)blockIdx.x;
   const int tyi = tile / tiles_x, txi = tile - tyi * tiles_x;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -284,9 +285,104 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
   }
 }
 
+// Launch order of the per-tile kernels (K3, K4): the heavy tiles (list longer
+// than 4x the mean) first, in raster order, then the others in raster order.
+// Raster order keeps neighbouring tiles -- which share splats -- close in
+// time (L2 reuse of the splat records); a heavy tile launched in the middle
+// of the frame would finish last and set the tail (the low-opacity cluster
+// of C3-lo: thousands of blends per pixel).  One CTA.
+constexpr int kOrderThreads = 1024;
+constexpr int kOrderMaxTiles = 11264;  // 44 KB of list lengths in shared memory
+__global__ void __launch_bounds__(kOrderThreads) tile_order_kernel(const int64_t* __restrict__ offsets,
+                                                                   int n_tiles,
+                                                                   int32_t* __restrict__ order) {
+  __shared__ int s_len[kOrderMaxTiles];
+  __shared__ int s_w[kOrderThreads / 32];
+  __shared__ int s_tot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool staged = n_tiles <= kOrderMaxTiles;
+  // coalesced: every load of a thread in flight at once
+  if (staged) {
+    for (int t = tid; t < n_tiles; t += kOrderThreads)
+      s_len[t] = (int)(offsets[t + 1] - offsets[t]);
+  }
+  const long long P = offsets[n_tiles] - offsets[0];
+  const long long thr = max(4 * P / max(n_tiles, 1), 64ll);
+  __syncthreads();
+  auto len = [&](int t) -> long long {
+    return staged ? (long long)s_len[t] : offsets[t + 1] - offsets[t];
+  };
+  const int per = (n_tiles + kOrderThreads - 1) / kOrderThreads;
+  const int t0 = tid * per, t1 = min(n_tiles, t0 + per);
+  int heavy = 0;
+  for (int t = t0; t < t1; ++t) heavy += len(t) > thr;
+  int incl = heavy;
+#pragma unroll
+  for (int k = 1; k < 32; k <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, k);
+    if (lane >= k) incl += v;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int w = s_w[lane];
+    int wi = w;
+#pragma unroll
+    for (int k = 1; k < 32; k <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, wi, k);
+      if (lane >= k) wi += v;
+    }
+    s_w[lane] = wi - w;
+    if (lane == 31) s_tot = wi;
+  }
+  __syncthreads();
+  if (s_tot == 0) {  // no heavy tile: raster order, written coalesced
+    for (int t = tid; t < n_tiles; t += kOrderThreads) order[t] = t;
+    return;
+  }
+  int h = s_w[warp] + incl - heavy;  // heavy tiles before this thread's range
+  int l = s_tot + (t0 - h);          // light tiles before it, after all heavy ones
+  for (int t = t0; t < t1; ++t) {
+    if (len(t) > thr) order[h++] = t;
+    else order[l++] = t;
+  }
+}
+
 }  // namespace tsr
 
 using namespace tsr;
+
+extern "C" int tsr_tile_order(const int64_t* offsets, int32_t n_tiles, int32_t* order,
+                              void* stream) {
+  if (!offsets || !order || n_tiles <= 0) return TSR_E_INVALID;
+  tile_order_kernel<<<1, kOrderThreads, 0, (cudaStream_t)stream>>>(offsets, n_tiles, order);
+  TSR_CHECK_LAUNCH();
+  return TSR_OK;
+}
+
+extern "C" int tsr_render_fwd_ordered(const float* rec, const int32_t* values,
+                                      const int64_t* offsets, int32_t width, int32_t height,
+                                      const float* background_host, float* out_color,
+                                      float* out_depth, float* out_final_T,
+                                      int32_t* out_n_contrib, int32_t* out_n_considered,
+                                      float* ckpt, const int64_t* ckpt_base, int32_t ckpt_stride,
+                                      const int32_t* tile_order, void* stream) {
+  if (width <= 0 || height <= 0 || !background_host) return TSR_E_INVALID;
+  if (ckpt && !ckpt_base) return TSR_E_INVALID;
+  if (ckpt && ckpt_stride != 1 && ckpt_stride != 2) return TSR_E_INVALID;
+  const int tx = tiles_of(width), ty = tiles_of(height);
+  const int n_tiles = tx * ty;
+  cudaStream_t s = (cudaStream_t)stream;
+  const ScoreArgs none{};
+  auto* k = !ckpt ? render_fwd_kernel<0, 0>
+            : ckpt_stride == 2 ? render_fwd_kernel<2, 0> : render_fwd_kernel<1, 0>;
+  k<<<n_tiles, kFwdThreads, 0, s>>>((const float4*)rec, values, offsets, width, height, tx,
+                                    background_host[0], background_host[1], background_host[2],
+                                    out_color, out_depth, out_final_T, out_n_contrib,
+                                    out_n_considered, ckpt, ckpt_base, none, tile_order);
+  TSR_CHECK_LAUNCH();
+  return TSR_OK;
+}
 
 extern "C" int tsr_render_fwd_ex(const float* rec, const int32_t* values, const int64_t* offsets,
                                   int32_t width, int32_t height, const float* background_host,
@@ -305,7 +401,7 @@ extern "C" int tsr_render_fwd_ex(const float* rec, const int32_t* values, const 
   k<<<n_tiles, kFwdThreads, 0, s>>>((const float4*)rec, values, offsets, width, height, tx,
                                     background_host[0], background_host[1], background_host[2],
                                     out_color, out_depth, out_final_T, out_n_contrib,
-                                    out_n_considered, ckpt, ckpt_base, none);
+                                    out_n_considered, ckpt, ckpt_base, none, nullptr);
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }
@@ -343,7 +439,7 @@ extern "C" int tsr_render_score(const float* rec, const int32_t* values, const i
   k<<<n_tiles, kFwdThreads, 0, s>>>((const float4*)rec, values, offsets, width, height, tx,
                                     background_host[0], background_host[1], background_host[2],
                                     out_color, out_depth, out_final_T, out_n_contrib,
-                                    out_n_considered, nullptr, nullptr, sc);
+                                    out_n_considered, nullptr, nullptr, sc, nullptr);
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }

@@ -12,6 +12,8 @@ n_considered > 32 g); `checkpoints_dict()` materialises the reference's
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -140,18 +142,24 @@ def render_score_raw(rec, values, offsets, width: int, height: int, background, 
 
 
 def render_raw(rec, values, offsets, ckpt_base, width: int, height: int, background,
-               out: RenderTargets, ckpt_stride: int = 1) -> None:
+               out: RenderTargets, ckpt_stride: int = 1, tile_order=None) -> None:
     """Launch K3 into preallocated targets (no host synchronisation).
-    ckpt_stride 2 writes only the checkpoint records K4 reads (training step)."""
+    ckpt_stride 2 writes only the checkpoint records K4 reads (training step);
+    tile_order (device int32, tsr_tile_order) launches heavy tiles first."""
     lib = _lib.load()
     bg = np.asarray(background, dtype=np.float64).reshape(3)
     bg_host = (_lib.c_f32 * 3)(*[float(v) for v in bg])
-    _lib.check(lib.tsr_render_fwd_ex(
+    _lib.check(lib.tsr_render_fwd_ordered(
         rec.data_ptr(), _lib.ptr(values), offsets.data_ptr(), width, height, bg_host,
         out.color.data_ptr(), out.depth.data_ptr(), out.final_T.data_ptr(),
         out.n_contrib.data_ptr(), out.n_considered.data_ptr(), _lib.ptr(out.ckpt),
         _lib.ptr(ckpt_base) if out.ckpt is not None else None, int(ckpt_stride),
-        _lib.stream_handle()), "tsr_render_fwd_ex")
+        _lib.ptr(tile_order), _lib.stream_handle()), "tsr_render_fwd_ordered")
+
+
+# per-tile kernel launch order in the training step: "heavy" (heavy tiles
+# first, tsr_tile_order) or "raster"
+TILE_ORDER = os.environ.get("TSR_TILE_ORDER", "heavy")
 
 
 def render(batch: SplatBatch, tiles: TileIndex, colors, background, *,

@@ -244,6 +244,8 @@ class TrainStep:
         self.loss_ws = losses.PhotometricWorkspace()
         from .backward import BackwardWorkspace
         self.bwd_ws = BackwardWorkspace()
+        self._order_buf = None
+        self.tile_order = None
         self.dc_ws = losses.DepthChainWorkspace()
         self._grad2d_clean = True  # the SH-0 fused kernel re-zeroes consumed rows
         self.grad_color = None
@@ -365,10 +367,21 @@ class TrainStep:
         from .binning import build_index_raw
         from .forward import render_raw
         build_index_raw(batch, self.cfg.strategy_id, self.index)
-        self._mark(timer, "binning")
         idx, out = self.index, self.targets
+        from .forward import TILE_ORDER
+        self.tile_order = None
+        if TILE_ORDER == "heavy":  # heavy tiles first in K3 and K4
+            n_tiles = camera.tiles_x * camera.tiles_y
+            if self._order_buf is None or self._order_buf.numel() != n_tiles:
+                self._order_buf = torch.empty(n_tiles, dtype=torch.int32, device=s.rec.device)
+            self.tile_order = self._order_buf
+            _lib.check(self.lib.tsr_tile_order(idx.offsets.data_ptr(), n_tiles,
+                                               self.tile_order.data_ptr(), _lib.stream_handle()),
+                       "tsr_tile_order")
+        self._mark(timer, "binning")
         render_raw(s.rec, idx.values, idx.offsets, idx.ckpt_base, camera.width, camera.height,
-                   self.cfg.background, out, ckpt_stride=2)  # only the records K4 reads
+                   self.cfg.background, out, ckpt_stride=2,  # only the records K4 reads
+                   tile_order=self.tile_order)
         self._mark(timer, "render")
         return batch
 
@@ -412,9 +425,9 @@ class TrainStep:
             self.grad2d.zero_()
         self._grad2d_clean = False
         if K4_FORM == "tiles":
-            _lib.check(self.lib.tsr_render_bwd(*common, self.grad2d.data_ptr(),
-                                               self.merges.data_ptr(), _lib.stream_handle()),
-                       "tsr_render_bwd")
+            _lib.check(self.lib.tsr_render_bwd_ordered(
+                *common, self.grad2d.data_ptr(), self.merges.data_ptr(),
+                _lib.ptr(self.tile_order), _lib.stream_handle()), "tsr_render_bwd_ordered")
         else:
             _lib.check(self.lib.tsr_render_bwd_ws(
                 *common, self.grad2d.data_ptr(), self.merges.data_ptr(), idx.p_cap,
@@ -541,8 +554,9 @@ class TrainStep:
         work-unit plan kernels); fused K4b+K5 (+ the row reduction in
         deterministic mode)."""
         from .backward import K4_FORM
-        return (2 + 1 + 1 + 2 + 1 + (2 if K4_FORM == "units" else 0) + 1
-                + (1 if self.deterministic else 0))
+        from .forward import TILE_ORDER
+        return (2 + 1 + (1 if TILE_ORDER == "heavy" else 0) + 1 + 2 + 1
+                + (2 if K4_FORM == "units" else 0) + 1 + (1 if self.deterministic else 0))
 
     def last_view(self):
         """(batch, TileIndex, RenderBuffers) views of the last step (synchronises)."""
