@@ -99,6 +99,9 @@ def parse():
                     help="N>1 / c4: ZeRO-1 update (reduce-scatter, K5 on the row shard, all-gather)")
     ap.add_argument("--deterministic", action="store_true",
                     help="K4 deterministic merge (bitwise reproducible)")
+    ap.add_argument("--vp", action="store_true",
+                    help="N=1: run the view-parallel (N>1) step, with its NCCL collectives "
+                         "on a world-size-1 communicator")
     return ap.parse_args()
 
 
@@ -371,7 +374,11 @@ def gpu_arm(args):
     backend = os.environ.get("TSR_BENCH_BACKEND", "nccl")
     local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.vp:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29611")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -397,13 +404,15 @@ def gpu_arm(args):
         stepper = ViewParallelStep(gset, cfg, extent=4.0, sharded=args.zero1, peer=args.peer)
         run = lambda timer=None: stepper.step_views(cams, [gt_dev] * len(cams), timer)  # noqa
         args.no_e2e = True
-    elif world == 1:
+    elif world == 1 and not args.vp:
         # the step replays as one CUDA graph (captured during warm-up)
         stepper = ts.TrainStep(gset, cfg, extent=4.0, graphs=True,
                                deterministic=args.deterministic)
         run = lambda timer=None: stepper.step(camera, gt_dev, timer)  # noqa: E731
     else:
-        stepper = ViewParallelStep(gset, cfg, extent=4.0, sharded=args.zero1, peer=args.peer)
+        stepper = ViewParallelStep(gset, cfg, extent=4.0, sharded=args.zero1, peer=args.peer,
+                                   force_collectives=args.vp,
+                                   chunks=4 if args.vp else None)
         run = lambda timer=None: stepper.step_views([camera], [gt_dev], timer)  # noqa: E731
 
     def barrier():
@@ -436,7 +445,7 @@ def gpu_arm(args):
         stepper.iteration = snap_it
         torch.cuda.synchronize()
 
-    graphs = world == 1 and not batch_views
+    graphs = world == 1 and not batch_views and not args.vp
     clocks = ClockSampler(local)
     clocks.start()
     timer = {}
@@ -505,7 +514,7 @@ def gpu_arm(args):
                 with torch.cuda.stream(copy_stream):
                     bufs[nxt].copy_(gt_host, non_blocking=True)
                     copied[nxt].record(copy_stream)
-            if world == 1:
+            if world == 1 and not args.vp:
                 loss = stepper.step(camera, bufs[cur])
             else:
                 loss = stepper.step_views([camera], [bufs[cur]])
@@ -534,7 +543,7 @@ def gpu_arm(args):
                        "async into pinned memory every step"}
 
     if rank != 0:
-        if world > 1:
+        if dist.is_available() and dist.is_initialized():
             dist.destroy_process_group()
         return
 
@@ -590,6 +599,12 @@ def gpu_arm(args):
                      "ops_per_unit": {"per_eval": BACKWARD_OPS[0], "per_blend": BACKWARD_OPS[1]},
                      "units": {"evals": evals, "blends": blends, "pairs": pairs}},
         "roofline_hbm": hbm_line,
+        "collective": ({"backend": dist.get_backend(), "world": dist.get_world_size(),
+                        "chunks": getattr(stepper, "chunks", 1),
+                        "exchange": "per-row-chunk allreduce + Adam on a communication stream, "
+                                    "overlapping K4b of the next chunk"
+                        if getattr(stepper, "chunks", 1) > 1 else "one flat-buffer allreduce"}
+                       if dist.is_available() and dist.is_initialized() else None),
         "phases_ms": {k: round(v, 4) for k, v in phases.items()},
         "host_launch_ms_per_step": host_ms,
         "gpu_launches": stepper.kernels_per_step() * args.steps,
@@ -600,7 +615,7 @@ def gpu_arm(args):
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config)
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_available() and dist.is_initialized():
         dist.destroy_process_group()
 
 

@@ -19,6 +19,7 @@ result is bitwise the replicated step's (Adam is row-local)."""
 from __future__ import annotations
 
 import ctypes
+import os
 
 import torch
 import torch.distributed as dist
@@ -244,17 +245,77 @@ def _barrier(group):
         dist.barrier(group=group)
 
 
+class ChunkedGrads:
+    """Chunk-major flat gradient buffer for the overlapped exchange: the
+    Gaussian rows are split into `chunks` ranges and each range's five group
+    gradients are contiguous, so one collective moves one chunk.  K4b writes
+    a chunk through row-offset views of the set (no kernel change), Adam
+    updates it through row-offset descriptors (Adam is row-local)."""
+
+    def __init__(self, gset, chunks: int):
+        n = len(gset)
+        self.bounds = [n * c // chunks for c in range(chunks + 1)]
+        widths = [p.numel() // max(p.shape[0], 1) for p in gset.params().values()]
+        self.names = list(gset.params())
+        self.widths = dict(zip(self.names, widths))
+        self.row_floats = sum(widths)
+        self.flat = torch.zeros(n * self.row_floats, dtype=torch.float32, device="cuda")
+        # chunk c starts at row_floats * bounds[c]; inside it group g starts at
+        # rows_c * (sum of the widths before g)
+        self.seg = []
+        for c in range(chunks):
+            r0, r1 = self.bounds[c], self.bounds[c + 1]
+            base, off, seg = self.row_floats * r0, 0, {}
+            for name, w in zip(self.names, widths):
+                seg[name] = base + off
+                off += (r1 - r0) * w
+            self.seg.append(seg)
+
+    def chunk(self, c: int) -> torch.Tensor:
+        r0, r1 = self.bounds[c], self.bounds[c + 1]
+        return self.flat[self.row_floats * r0: self.row_floats * r1]
+
+    def ptr(self, c: int, name: str) -> int:
+        return self.flat.data_ptr() + 4 * self.seg[c][name]
+
+    def group_views(self) -> dict:
+        """Per-group (N, ...) gradients gathered from the chunks (tests)."""
+        out = {}
+        for name in self.names:
+            w = self.widths[name]
+            parts = [self.flat[self.seg[c][name]: self.seg[c][name] +
+                               (self.bounds[c + 1] - self.bounds[c]) * w]
+                     for c in range(len(self.seg))]
+            out[name] = torch.cat(parts).view(-1, w)
+        return out
+
+
 class ViewParallelStep(TrainStep):
     """One optimizer step over this rank's views + an allreduce (or, with
-    sharded=True, reduce-scatter -> K5 on the row shard -> all-gather)."""
+    sharded=True, reduce-scatter -> K5 on the row shard -> all-gather).
+
+    With `chunks` > 1 (default 4 at N > 1 in the replicated mode) the last
+    view's K4b runs per Gaussian-row chunk and each chunk's gradient is
+    summed (one NCCL allreduce) and Adam-updated on a communication stream
+    while K4b computes the next chunk, so the exchange overlaps the tail of
+    the step."""
 
     def __init__(self, gset, cfg: TrainConfig, extent: float = 4.0, group=None,
-                 deterministic: bool = False, sharded: bool = False, peer: bool = False):
+                 deterministic: bool = False, sharded: bool = False, peer: bool = False,
+                 chunks: int | None = None, force_collectives: bool = False):
         super().__init__(gset, cfg, extent)
         self.group = group
         self.deterministic = deterministic
         self.sharded = sharded or peer
         self.peer = None
+        # collectives also at world size 1 (exercises the NCCL path on one GPU)
+        self.force_collectives = force_collectives
+        world, _ = _world_rank(group)
+        if chunks is None:
+            chunks = int(os.environ.get("TSR_VP_CHUNKS", 4 if world > 1 else 1))
+        self.chunks = 1 if self.sharded else max(1, chunks)
+        self.cgrads = None
+        self.comm_stream = None
         if peer:  # fused ZeRO-1 over peer memory (tsr_zero1_peer_adam)
             world, rank = _world_rank(group)
             self.zero = ZeroAdam(gset, world, rank, self.opt.lrs)
@@ -272,13 +333,122 @@ class ViewParallelStep(TrainStep):
             self.grad_shards = {k: torch.zeros_like(t) for k, t in self.zero.m.items()}
             self.param_shards = {k: torch.zeros_like(t) for k, t in self.zero.m.items()}
             self.param_full = {k: torch.zeros_like(g) for k, g in self.grads.items()}
+        elif self.chunks > 1:
+            self.cgrads = ChunkedGrads(gset, self.chunks)
+            self.flat = self.cgrads.flat
+            self.grads = None
+            self.comm_stream = torch.cuda.Stream()
+            self._chunk_ev = [torch.cuda.Event() for _ in range(self.chunks)]
         else:
             self.flat = torch.zeros(grad_numel(gset), dtype=torch.float32, device="cuda")
             self.grads = flat_grad_views(self.flat, gset)
 
+    # -------------------------------------------------- chunked exchange ---
+    def _chunk_struct(self, c: int):
+        """The set's rows [r0, r1) as a K4b input (row-offset pointers)."""
+        r0, r1 = self.cgrads.bounds[c], self.cgrads.bounds[c + 1]
+        g = gaussians_struct(self.gset)
+        for name in ("positions", "log_scales", "rotations", "opacity_logits", "colors"):
+            setattr(g, name, getattr(g, name) + 4 * r0 * self.cgrads.widths[name])
+        g.n = r1 - r0
+        return g
+
+    def _vjp_chunk(self, camera, batch, c: int, accumulate: bool) -> None:
+        r0 = self.cgrads.bounds[c]
+        cg = self.cgrads
+        _lib.check(self.lib.tsr_preprocess_bwd(
+            self._chunk_struct(c), camera_struct(camera, None, self.cfg.near),
+            batch.rec.data_ptr(), batch.row_of_source.data_ptr() + 4 * r0,
+            self.grad2d.data_ptr(), cg.ptr(c, "positions"), cg.ptr(c, "log_scales"),
+            cg.ptr(c, "rotations"), cg.ptr(c, "opacity_logits"), cg.ptr(c, "colors"), None,
+            1 if accumulate else 0, _lib.stream_handle()), "tsr_preprocess_bwd")
+
+    def _adam_chunk(self, c: int, descs: dict, stream) -> None:
+        """K5 on rows [r0, r1) of every group (the step's lr / bias
+        corrections, gradient from chunk c)."""
+        r0, r1 = self.cgrads.bounds[c], self.cgrads.bounds[c + 1]
+        arr = (_lib.AdamGroup_t * len(descs))()
+        for j, (name, d) in enumerate(descs.items()):
+            w = self.cgrads.widths[name]
+            e = arr[j]
+            e.param = d.param + 4 * r0 * w
+            e.grad = self.cgrads.ptr(c, name)
+            e.exp_avg = d.exp_avg + 4 * r0 * w
+            e.exp_avg_sq = d.exp_avg_sq + 4 * r0 * w
+            e.rows = r1 - r0
+            e.width = w
+            e.renormalize = d.renormalize
+            e.lr = d.lr
+            e.bias_correction1 = d.bias_correction1
+            e.bias_correction2 = d.bias_correction2
+        _lib.check(self.lib.tsr_adam_step(arr, len(descs), self.opt._counter().data_ptr(),
+                                          ctypes.c_void_p(stream.cuda_stream)), "tsr_adam_step")
+
+    def _reduce_chunk(self, c: int) -> None:
+        """Sum chunk c over ranks: one NCCL allreduce, or (deterministic) an
+        all-gather + rank-order sum, bitwise independent of the tree."""
+        if not self._collective():
+            return
+        chunk = self.cgrads.chunk(c)
+        if self.deterministic:
+            world, _ = _world_rank(self.group)
+            parts = [torch.empty_like(chunk) for _ in range(world)]
+            dist.all_gather(parts, chunk, group=self.group)
+            acc = parts[0].clone()
+            for q in parts[1:]:
+                acc += q
+            chunk.copy_(acc)
+        else:
+            dist.all_reduce(chunk, op=dist.ReduceOp.SUM, group=self.group)
+
+    def _collective(self) -> bool:
+        world, _ = _world_rank(self.group)
+        return world > 1 or (self.force_collectives and dist.is_available()
+                             and dist.is_initialized())
+
+    def _step_views_chunked(self, cameras, gts, timer) -> torch.Tensor:
+        total = None
+        main = torch.cuda.current_stream()
+        lr = {"positions": position_lr(self.pos_base_lr, self.iteration, self.cfg.max_iters)}
+        params = self.gset.params()
+        # the step's descriptors (advance the group step counts once)
+        descs = {name: self.opt._group(name, p, None, lr) for name, p in params.items()}
+        if not cameras:
+            self.flat.zero_()
+        last = len(cameras) - 1
+        for k, (camera, gt) in enumerate(zip(cameras, gts)):
+            batch = self.forward(camera, timer)
+            e = self.loss_and_backward(batch, camera, gt, timer)
+            total = e if total is None else total + e
+            self._publish_status()
+            self.last_camera = camera
+            for c in range(self.chunks):
+                self._vjp_chunk(camera, batch, c, accumulate=k > 0)
+                if k == last:  # exchange + update chunk c while K4b runs chunk c + 1
+                    self._chunk_ev[c].record(main)
+                    with torch.cuda.stream(self.comm_stream):
+                        self.comm_stream.wait_event(self._chunk_ev[c])
+                        self._reduce_chunk(c)
+                        self._adam_chunk(c, descs, self.comm_stream)
+        if cameras:
+            done = torch.cuda.Event()
+            done.record(self.comm_stream)
+            main.wait_event(done)
+        else:
+            for c in range(self.chunks):
+                with torch.cuda.stream(self.comm_stream):
+                    self._reduce_chunk(c)
+                    self._adam_chunk(c, descs, self.comm_stream)
+            done = torch.cuda.Event()
+            done.record(self.comm_stream)
+            main.wait_event(done)
+        self._mark(timer, "vjp_allreduce_adam")
+        return total
+
     def kernels_per_step(self, views: int = 1) -> int:
-        """Per view: K1-K4 + K4b; then one K5 (the NCCL allreduce is not ours)."""
-        return views * (super().kernels_per_step() - 1 + 1) + 1
+        """Per view: K1-K4 + K4b (one per row chunk); then K5 (one per row
+        chunk).  The NCCL collectives are not ours."""
+        return views * (super().kernels_per_step() - 1 + self.chunks) + self.chunks
 
     def _recover_overflow(self, camera) -> None:
         # the view batch is reserved up front (step_views), and this path's
@@ -293,6 +463,8 @@ class ViewParallelStep(TrainStep):
         if self.index is not None and cameras:
             self._poll_status(cameras[0])
         self.iteration += 1
+        if self.cgrads is not None:
+            return self._step_views_chunked(cameras, gts, timer)
         total = None
         for k, (camera, gt) in enumerate(zip(cameras, gts)):
             batch = self.forward(camera, timer)
@@ -317,7 +489,10 @@ class ViewParallelStep(TrainStep):
             return total
         if self.sharded:
             return self._sharded_update(lr, timer, total)
-        allreduce_grads(self.flat, self.group, self.deterministic)
+        if self.force_collectives and _world_rank(self.group)[0] == 1 and dist.is_initialized():
+            dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=self.group)
+        else:
+            allreduce_grads(self.flat, self.group, self.deterministic)
         self._mark(timer, "allreduce")
         self.opt.step_async(self.gset.params(), self.grads, lr)
         self._mark(timer, "adam")

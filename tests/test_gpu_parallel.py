@@ -48,7 +48,9 @@ def _worker(rank, world, port, deterministic, out_dir):
     grads = []
     for _ in range(3):
         step.step_views([cams[v] for v in mine], [gts[v] for v in mine])
-        grads.append(step.flat.cpu().numpy().copy())  # the reduced gradient
+        flat = step.flat if step.cgrads is None else torch.cat(  # chunk-major -> group order
+            [v.reshape(-1) for v in step.cgrads.group_views().values()])
+        grads.append(flat.cpu().numpy().copy())  # the reduced gradient
     torch.cuda.synchronize()
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), flat0=grads[0], **step.gset.to_numpy())
     dist.destroy_process_group()
@@ -143,7 +145,8 @@ def _params_worker(rank, world, port, mode, out_dir):
     params, ring, gt = _scene()
     cams, gts = _cams(ring, gt)
     step = ViewParallelStep(ts.GaussianSet(**params), ts.TrainConfig(max_iters=100),
-                            deterministic=True, sharded=mode == "zero", peer=mode == "peer")
+                            deterministic=True, sharded=mode == "zero", peer=mode == "peer",
+                            chunks=4 if mode == "chunk" else 1)
     mine = shard_views(len(cams), world, rank)
     for _ in range(3):
         step.step_views([cams[v] for v in mine], [gts[v] for v in mine])
@@ -154,13 +157,15 @@ def _params_worker(rank, world, port, mode, out_dir):
 
 def test_zero1_sharded_and_peer_fused_steps_equal_replicated_step(tmp_path):
     """ZeRO-1 with collectives (reduce-scatter -> K5 on a row shard with
-    shard-sized moments -> all-gather) and fused over peer memory (one
-    kernel reads every rank's gradient rows through CUDA IPC mappings, sums
-    them in rank order, updates, stores into every rank's parameters) both
-    give bitwise the replicated step's parameters on every rank."""
+    shard-sized moments -> all-gather), fused over peer memory (one kernel
+    reads every rank's gradient rows through CUDA IPC mappings, sums them in
+    rank order, updates, stores into every rank's parameters) and the
+    chunked overlapped exchange (per-row-chunk reduction + Adam on a
+    communication stream) all give bitwise the replicated step's parameters
+    on every rank."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
-    for k, mode in enumerate(("rep", "zero", "peer")):
+    for k, mode in enumerate(("rep", "zero", "peer", "chunk")):
         port = 29900 + os.getpid() % 50 + 60 * k
         procs = [ctx.Process(target=_params_worker, args=(r, 2, port, mode, str(tmp_path)))
                  for r in range(2)]
@@ -170,7 +175,42 @@ def test_zero1_sharded_and_peer_fused_steps_equal_replicated_step(tmp_path):
             p.join(timeout=600)
             assert p.exitcode == 0, mode
     rep = dict(np.load(tmp_path / "rep0.npz"))
-    for name in ("zero0", "zero1", "peer0", "peer1", "rep1"):
+    for name in ("zero0", "zero1", "peer0", "peer1", "rep1", "chunk0", "chunk1"):
         got = dict(np.load(tmp_path / f"{name}.npz"))
         for k in rep:
             assert np.array_equal(rep[k], got[k]), (name, k)
+
+
+def test_nccl_single_rank_chunked_exchange_matches_unchunked():
+    """The NCCL code path on the box's one GPU: a world-size-1 NCCL process
+    group with the collectives forced on.  The chunked step (K4b per
+    Gaussian-row chunk, each chunk's allreduce + Adam on a communication
+    stream overlapping the next chunk's K4b) gives bitwise the parameters of
+    the unchunked step (one allreduce of the flat buffer, one K5)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2601_19489_b200 as ts
+    from paper_2601_19489_b200.parallel import ViewParallelStep
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(31000 + os.getpid() % 500)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        assert dist.get_backend() == "nccl"
+        params, ring, gt = _scene()
+        cams, gts = _cams(ring, gt)
+        out = {}
+        for chunks in (1, 4):
+            # deterministic: K4's merge and the reduction are bitwise reproducible
+            step = ViewParallelStep(ts.GaussianSet(**params), ts.TrainConfig(max_iters=100),
+                                    deterministic=True, chunks=chunks, force_collectives=True)
+            for _ in range(3):
+                step.step_views(cams[:2], gts[:2])
+            torch.cuda.synchronize()
+            out[chunks] = step.gset.to_numpy()
+            if chunks == 4:
+                assert step.cgrads is not None and step.comm_stream is not None
+        for k in out[1]:
+            assert np.array_equal(out[1][k], out[4][k]), k
+    finally:
+        dist.destroy_process_group()
