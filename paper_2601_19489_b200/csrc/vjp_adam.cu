@@ -436,7 +436,13 @@ __device__ __forceinline__ void store_row(float* base, long long i, const float*
 // up front (42 independent loads in flight), the VJP runs on the registers,
 // the consumed Grad2D row is zeroed for the next step, and the five Adam
 // groups are updated and stored.
-__global__ void __launch_bounds__(128, 7) vjp_adam_sh0_kernel(
+#ifndef TSR_VJP_MINB
+#define TSR_VJP_MINB 6  // 80 registers: measured 97 us vs 101 us at 7 CTAs/SM (72 registers, more spills)
+#endif
+// kPose: accumulate the pose sums (pose optimisation); without it the
+// twelve per-Gaussian pose terms are dead code (registers for the Adam part)
+template <bool kPose>
+__global__ void __launch_bounds__(128, TSR_VJP_MINB) vjp_adam_sh0_kernel(
     tsr_camera_t cam, long long n, const float4* __restrict__ rec,
     const int32_t* __restrict__ row_of_source, float* __restrict__ grad2d, AdamGroups groups,
     float* __restrict__ pose_sums, unsigned long long* __restrict__ skipped,
@@ -518,7 +524,7 @@ __global__ void __launch_bounds__(128, 7) vjp_adam_sh0_kernel(
     store_row<1>(G3.param, i, po); store_row<1>(G3.exp_avg, i, mo); store_row<1>(G3.exp_avg_sq, i, vo);
     store_row<3>(G4.param, i, pc); store_row<3>(G4.exp_avg, i, mc); store_row<3>(G4.exp_avg_sq, i, vc);
   }
-  if (pose_sums) {
+  if (kPose) {
     float pv[12];
 #pragma unroll
     for (int k = 0; k < 12; ++k) pv[k] = vis ? vj.pose[k] : 0.f;
@@ -717,7 +723,8 @@ extern "C" int tsr_preprocess_bwd_adam_ex(const tsr_gaussians_t* g, const tsr_ca
   int blocks = (int)((g->n + 255) / 256);
   if (g->sh_coeffs == 1) {
     // fast path; also zeroes the consumed Grad2D rows for the next step
-    vjp_adam_sh0_kernel<<<(int)((g->n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+    auto* k = pose_sums ? vjp_adam_sh0_kernel<true> : vjp_adam_sh0_kernel<false>;
+    k<<<(int)((g->n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
         *cam, g->n, (const float4*)rec, row_of_source, (float*)grad2d, gs, pose_sums, skipped,
         group_scalars, gate, gated_steps, loss_guard);
   } else {

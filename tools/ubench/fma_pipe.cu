@@ -30,6 +30,24 @@ __global__ void kern(float* out, float s, int iters) {
         asm("mov.b64 {%0,%1}, %2;" : "=f"(a2), "=f"(a3) : "l"(x1));
         asm("mov.b64 {%0,%1}, %2;" : "=f"(a4), "=f"(a5) : "l"(x2));
         asm("mov.b64 {%0,%1}, %2;" : "=f"(a6), "=f"(a7) : "l"(x3));
+      } else if (MODE == 4 || MODE == 5) {
+        // mixed: packed chains (a0..a3 as 2 pairs) and scalar chains (a4..a7);
+        // MODE 4: 1 FFMA2 : 1 FFMA per pair of chains, MODE 5: 1 FFMA2 : 2 FFMA
+        unsigned long long x0, x1, bb, cc;
+        asm("mov.b64 %0, {%1,%2};" : "=l"(x0) : "f"(a0), "f"(a1));
+        asm("mov.b64 %0, {%1,%2};" : "=l"(x1) : "f"(a2), "f"(a3));
+        asm("mov.b64 %0, {%1,%2};" : "=l"(bb) : "f"(b), "f"(b));
+        asm("mov.b64 %0, {%1,%2};" : "=l"(cc) : "f"(c), "f"(c));
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x0) : "l"(bb), "l"(cc));
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x1) : "l"(bb), "l"(cc));
+        asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(a4) : "f"(b), "f"(c));
+        asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(a5) : "f"(b), "f"(c));
+        if (MODE == 5) {
+          asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(a6) : "f"(b), "f"(c));
+          asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(a7) : "f"(b), "f"(c));
+        }
+        asm("mov.b64 {%0,%1}, %2;" : "=f"(a0), "=f"(a1) : "l"(x0));
+        asm("mov.b64 {%0,%1}, %2;" : "=f"(a2), "=f"(a3) : "l"(x1));
       } else if (MODE == 2) {  // FMUL
         a0 = a0 * b; a1 = a1 * b; a2 = a2 * b; a3 = a3 * b;
         a4 = a4 * b; a5 = a5 * b; a6 = a6 * b; a7 = a7 * b;
@@ -55,8 +73,12 @@ void run(const char* name, float* out, int sms, int clk_khz) {
   cudaEventSynchronize(e1);
   float ms;
   cudaEventElapsedTime(&ms, e0, e1);
-  const double lane_ops = (double)blocks * threads * iters * 16 * 8;
-  const double warp_instr = lane_ops / 32 / (MODE == 1 ? 2 : 1);
+  // lane-ops per inner step: 8 chains (modes 0-3), 4 packed + 2 scalar
+  // (mode 4), 4 packed + 4 scalar (mode 5)
+  const double per = MODE == 4 ? 6.0 : 8.0;
+  const double lane_ops = (double)blocks * threads * iters * 16 * per;
+  const double warp_instr = (double)blocks * threads * iters * 16 / 32 *
+                            (MODE == 1 ? 4.0 : MODE == 4 ? 4.0 : MODE == 5 ? 6.0 : 8.0);
   const double clks = ms * 1e-3 * clk_khz * 1e3;
   printf("%-6s %8.3f ms  lane-ops/s %7.2f T  lane-ops/clk/SM %6.1f  warp-instr/clk/SMSP %5.2f\n",
          name, ms, lane_ops / (ms * 1e-3) / 1e12, lane_ops / clks / sms, warp_instr / clks / sms / 4);
@@ -74,5 +96,7 @@ int main() {
   run<1>("FFMA2", out, p.multiProcessorCount, clk);
   run<2>("FMUL", out, p.multiProcessorCount, clk);
   run<3>("FADD", out, p.multiProcessorCount, clk);
+  run<4>("MIX11", out, p.multiProcessorCount, clk);
+  run<5>("MIX12", out, p.multiProcessorCount, clk);
   return 0;
 }
