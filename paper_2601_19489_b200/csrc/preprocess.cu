@@ -85,8 +85,10 @@ __device__ __forceinline__ long long count_load_balanced(const SplatF64& s, int 
 //   x = tx0 | ncols << 16, y = ty_base | overflow << 31,
 //   z, w = columns 0..7 as (row offset 4 bits | nrows 4 bits) bytes.
 // overflow is set when the span does not fit (the emission then re-walks).
+template <int kStrategy = -1>  // -1: runtime `strategy`; 0 / 2: that strategy only
 __device__ __forceinline__ long long count_pairs_of(const float* rp, int strategy, int tiles_x,
                                                     int tiles_y, uint4& span) {
+  if (kStrategy >= 0) strategy = kStrategy;
   SplatF64 s = load_splat_f64(rp);
   span = make_uint4(0u, 0u, 0u, 0u);
   if (strategy == 1) {
@@ -300,13 +302,20 @@ __global__ void __launch_bounds__(kScanBlock) cull_compact_kernel(
 }
 
 // (b) projection + colour + exact pair count into the compacted rows.
-template <bool kLB>
-__global__ void __launch_bounds__(kScanBlock, kLB ? 3 : 4) preprocess_kernel(
+// kS: the binning strategy (0 sequential walk, 1 warp-cooperative
+// load-balanced, 2 AABB), a template parameter so each instantiation holds
+// only its own count code (registers)
+#ifndef TSR_K1_MINB
+#define TSR_K1_MINB 4
+#endif
+template <int kS>
+__global__ void __launch_bounds__(kScanBlock, kS == 1 ? 3 : TSR_K1_MINB) preprocess_kernel(
     tsr_gaussians_t g, tsr_camera_t cam, int strategy, float4* __restrict__ rec_out,
     const int32_t* __restrict__ row_of_source, int32_t* __restrict__ counts,
     uint32_t* __restrict__ depth_bits, uint4* __restrict__ spans,
     unsigned long long* __restrict__ total_pairs) {
   __shared__ unsigned long long s_sum[kScanBlock / 32];
+  constexpr bool kLB = kS == 1;
   __shared__ LbWarp s_lb[kLB ? kScanBlock / 32 : 1];
   const long long i = (long long)blockIdx.x * kScanBlock + threadIdx.x;
   const int tiles_x = tiles_of(cam.width), tiles_y = tiles_of(cam.height);
@@ -332,7 +341,7 @@ __global__ void __launch_bounds__(kScanBlock, kLB ? 3 : 4) preprocess_kernel(
     float rec[12];
     project_one(g, cam, i, rec);
     uint4 span;
-    cnt = count_pairs_of(rec, strategy, tiles_x, tiles_y, span);
+    cnt = count_pairs_of<kS>(rec, strategy, tiles_x, tiles_y, span);
     float4* dst = rec_out + (long long)row * 3;
     dst[0] = make_float4(rec[0], rec[1], rec[2], rec[3]);
     dst[1] = make_float4(rec[4], rec[5], rec[6], rec[7]);
@@ -435,7 +444,9 @@ extern "C" int tsr_preprocess_fwd(const tsr_gaussians_t* g, const tsr_camera_t* 
   cull_compact_kernel<<<cull_blocks, kScanBlock, 0, s>>>(*g, *cam, source_ids, row_of_source,
                                                          totals, status, ticket, cull_blocks);
   TSR_CHECK_LAUNCH();
-  auto* pk = strategy == 1 ? preprocess_kernel<true> : preprocess_kernel<false>;
+  auto* pk = strategy == 1   ? preprocess_kernel<1>
+             : strategy == 2 ? preprocess_kernel<2>
+                             : preprocess_kernel<0>;
   pk<<<blocks, kScanBlock, 0, s>>>(*g, *cam, strategy, (float4*)rec,
                                                   row_of_source, counts, depth_bits,
                                                   (uint4*)spans,
