@@ -412,7 +412,8 @@ def gpu_arm(args):
     else:
         stepper = ViewParallelStep(gset, cfg, extent=4.0, sharded=args.zero1, peer=args.peer,
                                    force_collectives=args.vp,
-                                   chunks=4 if args.vp else None)
+                                   chunks=4 if args.vp else None,
+                                   graphs=os.environ.get("TSR_VP_GRAPHS", "1") == "1")
         run = lambda timer=None: stepper.step_views([camera], [gt_dev], timer)  # noqa: E731
 
     def barrier():
@@ -445,7 +446,7 @@ def gpu_arm(args):
         stepper.iteration = snap_it
         torch.cuda.synchronize()
 
-    graphs = world == 1 and not batch_views and not args.vp
+    graphs = (world == 1 and not batch_views and not args.vp) or getattr(stepper, "graphs", False)
     clocks = ClockSampler(local)
     clocks.start()
     timer = {}
@@ -493,7 +494,10 @@ def gpu_arm(args):
         if graphs:  # capture the graphs of both GT buffers before timing
             for b in bufs:
                 b.copy_(gt_host)
-                stepper.step(camera, b)
+                if world == 1 and not args.vp:
+                    stepper.step(camera, b)
+                else:
+                    stepper.step_views([camera], [b])
         restore()  # same training segment as the timed loop (outside both timed regions)
         copied = [torch.cuda.Event() for _ in range(2)]
         consumed = [torch.cuda.Event() for _ in range(2)]

@@ -282,6 +282,12 @@ typedef struct {
 #define TSR_MAX_ADAM_GROUPS 8
 int tsr_adam_step(const tsr_adam_group_t* groups_host, int32_t n_groups,
                   unsigned long long* skipped, void* stream);
+/* tsr_adam_step with the per-step scalars from device memory: group k uses
+ * group_scalars[3 (k % scal_period) + {0, 1, 2}] = {lr, bias_correction1,
+ * bias_correction2} (CUDA-graph replay of the view-parallel step). */
+int tsr_adam_step_dev(const tsr_adam_group_t* groups_host, int32_t n_groups,
+                      const float* group_scalars, int32_t scal_period,
+                      unsigned long long* skipped, void* stream);
 
 /* Fused ZeRO-1 update over peer memory (SURVEY §8(e), B200 variant;
  * replaces the reference's single-process Adam.step, optim.py:60-88, in a

@@ -89,6 +89,7 @@ _SIGNATURES = {
     "tsr_preprocess_bwd": (c_i32, [ctypes.POINTER(Gaussians_t), ctypes.POINTER(Camera_t), c_vp,
                                    c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "tsr_adam_step": (c_i32, [ctypes.POINTER(AdamGroup_t), c_i32, c_vp, c_vp]),
+    "tsr_adam_step_dev": (c_i32, [ctypes.POINTER(AdamGroup_t), c_i32, c_vp, c_i32, c_vp, c_vp]),
     "tsr_zero1_peer_adam": (c_i32, [ctypes.POINTER(AdamGroup_t), c_i32, c_i32, c_vp, c_vp,
                                     c_i64, c_i64, c_vp, c_vp]),
     "tsr_preprocess_bwd_adam": (c_i32, [ctypes.POINTER(Gaussians_t), ctypes.POINTER(Camera_t),

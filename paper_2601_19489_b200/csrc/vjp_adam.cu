@@ -324,8 +324,13 @@ __device__ __forceinline__ int adam_row(const tsr_adam_group_t& G, long long r, 
   return 0;
 }
 
+// scal (nullable): per-step [lr, bias_correction1, bias_correction2] of group
+// (gi % scal_period) from device memory -- CUDA-graph replay, where the
+// descriptors' by-value scalars are frozen at capture
 __global__ void __launch_bounds__(256) adam_kernel(AdamGroups groups,
-                                                   unsigned long long* __restrict__ skipped) {
+                                                   unsigned long long* __restrict__ skipped,
+                                                   const float* __restrict__ scal,
+                                                   int scal_period) {
   const long long total = groups.row_start[groups.n];
   unsigned long long local = 0;
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
@@ -335,7 +340,7 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamGroups groups,
     const tsr_adam_group_t& G = groups.g[gi];
     const long long r = t - groups.row_start[gi];
     const float* g = G.grad + r * G.width;
-    local += adam_row(G, r, [&](int k) { return g[k]; });
+    local += adam_row(G, r, [&](int k) { return g[k]; }, scal, scal ? gi % scal_period : 0);
   }
   // warp-aggregated skip counter
   for (int d = 16; d > 0; d >>= 1) local += __shfl_xor_sync(0xffffffffu, local, d);
@@ -648,7 +653,25 @@ extern "C" int tsr_adam_step(const tsr_adam_group_t* groups_host, int32_t n_grou
   if (total == 0) return TSR_OK;
   long long blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  adam_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(gs, skipped);
+  adam_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(gs, skipped, nullptr, 1);
+  TSR_CHECK_LAUNCH();
+  return TSR_OK;
+}
+
+extern "C" int tsr_adam_step_dev(const tsr_adam_group_t* groups_host, int32_t n_groups,
+                                 const float* group_scalars, int32_t scal_period,
+                                 unsigned long long* skipped, void* stream) {
+  AdamGroups gs;
+  if (!fill_groups(groups_host, n_groups, gs) || !skipped || !group_scalars || scal_period < 1)
+    return TSR_E_INVALID;
+  for (int k = 0; k < n_groups; ++k)
+    if (!gs.g[k].grad || !gs.g[k].exp_avg || !gs.g[k].exp_avg_sq) return TSR_E_INVALID;
+  const long long total = gs.row_start[n_groups];
+  if (total == 0) return TSR_OK;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  adam_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(gs, skipped, group_scalars,
+                                                             scal_period);
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }

@@ -302,8 +302,12 @@ class ViewParallelStep(TrainStep):
 
     def __init__(self, gset, cfg: TrainConfig, extent: float = 4.0, group=None,
                  deterministic: bool = False, sharded: bool = False, peer: bool = False,
-                 chunks: int | None = None, force_collectives: bool = False):
+                 chunks: int | None = None, force_collectives: bool = False,
+                 graphs: bool = False):
         super().__init__(gset, cfg, extent)
+        # CUDA-graph replay of the chunked step (after one eager step)
+        self.graphs = graphs
+        self._warm = False
         self.group = group
         self.deterministic = deterministic
         self.sharded = sharded or peer
@@ -363,9 +367,10 @@ class ViewParallelStep(TrainStep):
             cg.ptr(c, "rotations"), cg.ptr(c, "opacity_logits"), cg.ptr(c, "colors"), None,
             1 if accumulate else 0, _lib.stream_handle()), "tsr_preprocess_bwd")
 
-    def _adam_chunk(self, c: int, descs: dict, stream) -> None:
+    def _adam_chunk(self, c: int, descs: dict, stream, scal_dev=None) -> None:
         """K5 on rows [r0, r1) of every group (the step's lr / bias
-        corrections, gradient from chunk c)."""
+        corrections -- by value, or from `scal_dev` under graph replay --
+        gradient from chunk c)."""
         r0, r1 = self.cgrads.bounds[c], self.cgrads.bounds[c + 1]
         arr = (_lib.AdamGroup_t * len(descs))()
         for j, (name, d) in enumerate(descs.items()):
@@ -381,8 +386,14 @@ class ViewParallelStep(TrainStep):
             e.lr = d.lr
             e.bias_correction1 = d.bias_correction1
             e.bias_correction2 = d.bias_correction2
-        _lib.check(self.lib.tsr_adam_step(arr, len(descs), self.opt._counter().data_ptr(),
-                                          ctypes.c_void_p(stream.cuda_stream)), "tsr_adam_step")
+        if scal_dev is not None:
+            _lib.check(self.lib.tsr_adam_step_dev(
+                arr, len(descs), scal_dev.data_ptr(), len(descs), self.opt._counter().data_ptr(),
+                ctypes.c_void_p(stream.cuda_stream)), "tsr_adam_step_dev")
+        else:
+            _lib.check(self.lib.tsr_adam_step(arr, len(descs), self.opt._counter().data_ptr(),
+                                              ctypes.c_void_p(stream.cuda_stream)),
+                       "tsr_adam_step")
 
     def _reduce_chunk(self, c: int) -> None:
         """Sum chunk c over ranks: one NCCL allreduce, or (deterministic) an
@@ -406,13 +417,14 @@ class ViewParallelStep(TrainStep):
         return world > 1 or (self.force_collectives and dist.is_available()
                              and dist.is_initialized())
 
-    def _step_views_chunked(self, cameras, gts, timer) -> torch.Tensor:
+    def _step_views_chunked(self, cameras, gts, timer, descs=None, scal_dev=None) -> torch.Tensor:
         total = None
         main = torch.cuda.current_stream()
-        lr = {"positions": position_lr(self.pos_base_lr, self.iteration, self.cfg.max_iters)}
-        params = self.gset.params()
-        # the step's descriptors (advance the group step counts once)
-        descs = {name: self.opt._group(name, p, None, lr) for name, p in params.items()}
+        if descs is None:
+            lr = {"positions": position_lr(self.pos_base_lr, self.iteration, self.cfg.max_iters)}
+            # the step's descriptors (advance the group step counts once)
+            descs = {name: self.opt._group(name, p, None, lr)
+                     for name, p in self.gset.params().items()}
         if not cameras:
             self.flat.zero_()
         last = len(cameras) - 1
@@ -420,7 +432,11 @@ class ViewParallelStep(TrainStep):
             batch = self.forward(camera, timer)
             e = self.loss_and_backward(batch, camera, gt, timer)
             total = e if total is None else total + e
-            self._publish_status()
+            if torch.cuda.is_current_stream_capturing():  # copy nodes only
+                self.status_ovf_host.copy_(self.index.overflow, non_blocking=True)
+                self.status_tot_host.copy_(self.scratch.totals, non_blocking=True)
+            else:
+                self._publish_status()
             self.last_camera = camera
             for c in range(self.chunks):
                 self._vjp_chunk(camera, batch, c, accumulate=k > 0)
@@ -429,7 +445,7 @@ class ViewParallelStep(TrainStep):
                     with torch.cuda.stream(self.comm_stream):
                         self.comm_stream.wait_event(self._chunk_ev[c])
                         self._reduce_chunk(c)
-                        self._adam_chunk(c, descs, self.comm_stream)
+                        self._adam_chunk(c, descs, self.comm_stream, scal_dev)
         if cameras:
             done = torch.cuda.Event()
             done.record(self.comm_stream)
@@ -438,7 +454,7 @@ class ViewParallelStep(TrainStep):
             for c in range(self.chunks):
                 with torch.cuda.stream(self.comm_stream):
                     self._reduce_chunk(c)
-                    self._adam_chunk(c, descs, self.comm_stream)
+                    self._adam_chunk(c, descs, self.comm_stream, scal_dev)
             done = torch.cuda.Event()
             done.record(self.comm_stream)
             main.wait_event(done)
@@ -457,14 +473,60 @@ class ViewParallelStep(TrainStep):
         raise RuntimeError(f"pair capacity {self.index.p_cap} overflowed in the view-parallel "
                            "step; reserve() a larger capacity for the view batch")
 
+    def _graph_step_views(self, cameras, gts) -> torch.Tensor:
+        """The chunked step replayed as ONE CUDA graph: every view's K1-K4b,
+        the per-chunk NCCL allreduces and Adam updates on the communication
+        stream (forked from and joined back into the capture stream), and
+        the status copies.  The step's Adam scalars reach the captured K5
+        launches from device memory (pinned ring + copy, as TrainStep)."""
+        cap = self.index.p_cap
+        self._poll_status(cameras[0])
+        if self.index.p_cap != cap:
+            self._graph_cache.clear()
+        self.iteration += 1
+        lr = {"positions": position_lr(self.pos_base_lr, self.iteration, self.cfg.max_iters)}
+        descs = {name: self.opt._group(name, p, None, lr)
+                 for name, p in self.gset.params().items()}
+        k = self._ring_k
+        self._ring_k = (k + 1) % len(self._ring)
+        if self._ring_ev[k] is not None:
+            self._ring_ev[k].synchronize()
+        host = self._ring[k]
+        for j, d in enumerate(descs.values()):
+            host[3 * j], host[3 * j + 1], host[3 * j + 2] = (d.lr, d.bias_correction1,
+                                                             d.bias_correction2)
+        self._scal_dev.copy_(host, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._ring_ev[k] = ev
+        key = tuple(self._graph_key(c, g, False, None, None) for c, g in zip(cameras, gts))
+        entry = self._graph_cache.get(key)
+        if entry is None:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                e = self._step_views_chunked(cameras, gts, None, descs=descs,
+                                             scal_dev=self._scal_dev)
+            entry = self._graph_cache[key] = (g, e)
+        entry[0].replay()
+        self.status_event = torch.cuda.Event()
+        self.status_event.record()
+        self.last_camera = cameras[-1]
+        return entry[1]
+
     def step_views(self, cameras, gts, timer=None) -> torch.Tensor:
         if self.index is None and cameras:
             self.reserve(cameras)  # pair capacity for the largest view of the batch
+        if (self.graphs and timer is None and self.cgrads is not None and cameras
+                and self._warm):
+            return self._graph_step_views(cameras, gts)
         if self.index is not None and cameras:
             self._poll_status(cameras[0])
         self.iteration += 1
         if self.cgrads is not None:
-            return self._step_views_chunked(cameras, gts, timer)
+            out = self._step_views_chunked(cameras, gts, timer)
+            self._warm = True  # the collectives ran once eagerly (NCCL warm-up)
+            return out
         total = None
         for k, (camera, gt) in enumerate(zip(cameras, gts)):
             batch = self.forward(camera, timer)

@@ -214,3 +214,35 @@ def test_nccl_single_rank_chunked_exchange_matches_unchunked():
             assert np.array_equal(out[1][k], out[4][k]), k
     finally:
         dist.destroy_process_group()
+
+
+def test_nccl_single_rank_graph_replayed_chunked_step_matches_eager():
+    """The chunked N>1 step captured as one CUDA graph (views, per-chunk NCCL
+    allreduce + Adam on the communication stream, Adam scalars from device
+    memory) gives bitwise the eager chunked step's parameters."""
+    import torch
+    import torch.distributed as dist
+    import paper_2601_19489_b200 as ts
+    from paper_2601_19489_b200.parallel import ViewParallelStep
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(31600 + os.getpid() % 300)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        params, ring, gt = _scene()
+        cams, gts = _cams(ring, gt)
+        out = {}
+        for graphs in (False, True):
+            step = ViewParallelStep(ts.GaussianSet(**params), ts.TrainConfig(max_iters=100),
+                                    deterministic=True, chunks=4, force_collectives=True,
+                                    graphs=graphs)
+            losses = [float(step.step_views(cams[:2], gts[:2])) for _ in range(4)]
+            torch.cuda.synchronize()
+            out[graphs] = (step.gset.to_numpy(), losses)
+            if graphs:
+                assert len(step._graph_cache) == 1
+        for k in out[False][0]:
+            assert np.array_equal(out[False][0][k], out[True][0][k]), k
+        assert out[False][1] == out[True][1]
+    finally:
+        dist.destroy_process_group()
