@@ -401,7 +401,10 @@ def gpu_arm(args):
         mine = shard_views(batch_views, world, rank)
         cams = [ts.Camera(ring[v]["fx"], ring[v]["fy"], ring[v]["cx"], ring[v]["cy"],
                           c["width"], c["height"], ring[v]["R"], ring[v]["t"]) for v in mine]
-        stepper = ViewParallelStep(gset, cfg, extent=4.0, sharded=args.zero1, peer=args.peer)
+        plain = not (args.zero1 or args.peer)
+        stepper = ViewParallelStep(gset, cfg, extent=4.0, sharded=args.zero1, peer=args.peer,
+                                   chunks=4 if plain else None,
+                                   graphs=plain and os.environ.get("TSR_VP_GRAPHS", "1") == "1")
         run = lambda timer=None: stepper.step_views(cams, [gt_dev] * len(cams), timer)  # noqa
         args.no_e2e = True
     elif world == 1 and not args.vp:
@@ -593,7 +596,10 @@ def gpu_arm(args):
                    "merge": "deterministic (slots + emission-order row sums)"
                             if args.deterministic else "float atomics (FP32-tolerance)",
                    "l2": "inputs larger than L2 (Gaussian state + Adam moments 168 MB, "
-                         "per-step buffers ~1 GB)"},
+                         "per-step buffers ~1 GB)",
+                   "window": f"training steps {args.warmup + 1}-{args.warmup + args.steps} from "
+                             "the seeded init (the scene trains during the run; the e2e loop "
+                             "replays the same segment from a post-warm-up snapshot)"},
         "roofline": {"kernel": "render_bwd_kernel (K4)", "bound": "fp32",
                      "achieved": achieved, "peak": peak_ops, "unit": "Tops/s",
                      "frac": (achieved / peak_ops) if achieved else None,
