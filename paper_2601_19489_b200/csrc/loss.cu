@@ -36,26 +36,38 @@ __device__ __forceinline__ float2 bc2(float x) { return make_float2(x, x); }
 // Load a (kLIn x kLIn) halo tile of one channel of the interleaved (H,W,3)
 // images r and g (zero outside) into s[row][col] = (r, g) (row stride kLS).
 // All loads of a thread are issued before any shared store.
-constexpr int kHaloIters = (kLIn * kLIn + 255) / 256;
+// Row-wise halo loads: warp w stages rows w, w + 8, ... of the 42-row halo;
+// lane l loads column l and lanes 0-9 also column 32 + l.  A row's validity
+// is warp-uniform and its base address is formed once (no per-element
+// division or 64-bit index arithmetic); all loads of a thread are issued
+// before any shared store.
+constexpr int kHaloRows = (kLIn + 7) / 8;  // rows per warp (6; warps 2-7 load 5)
 __device__ __forceinline__ void load_halo2(const float* __restrict__ r, const float* __restrict__ g,
                                            int c, int H, int W, int ty0, int tx0, float2* s) {
-  float2 v[kHaloIters];
-  int dst[kHaloIters];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int x0 = tx0 - kLR + lane, x1 = x0 + 32;
+  const bool in0 = x0 >= 0 && x0 < W, in1 = lane < kLIn - 32 && x1 >= 0 && x1 < W;
+  float2 v0[kHaloRows], v1[kHaloRows];
 #pragma unroll
-  for (int k = 0; k < kHaloIters; ++k) {
-    const int i = threadIdx.x + 256 * k;
-    const int yy = i / kLIn, xx = i - yy * kLIn;
-    const int y = ty0 - kLR + yy, x = tx0 - kLR + xx;
-    v[k] = make_float2(0.f, 0.f);
-    dst[k] = i < kLIn * kLIn ? yy * kLS + xx : -1;
-    if (i < kLIn * kLIn && y >= 0 && y < H && x >= 0 && x < W) {
-      const long long o = ((long long)y * W + x) * 3 + c;
-      v[k] = make_float2(__ldg(r + o), __ldg(g + o));
+  for (int k = 0; k < kHaloRows; ++k) {
+    const int row = warp + 8 * k;
+    const int y = ty0 - kLR + row;
+    v0[k] = v1[k] = make_float2(0.f, 0.f);
+    if (row < kLIn && y >= 0 && y < H) {
+      const float* rr = r + ((long long)y * W) * 3 + c;
+      const float* gg = g + ((long long)y * W) * 3 + c;
+      if (in0) v0[k] = make_float2(__ldg(rr + 3 * x0), __ldg(gg + 3 * x0));
+      if (in1) v1[k] = make_float2(__ldg(rr + 3 * x1), __ldg(gg + 3 * x1));
     }
   }
 #pragma unroll
-  for (int k = 0; k < kHaloIters; ++k)
-    if (dst[k] >= 0) s[dst[k]] = v[k];
+  for (int k = 0; k < kHaloRows; ++k) {
+    const int row = warp + 8 * k;
+    if (row < kLIn) {
+      s[row * kLS + lane] = v0[k];
+      if (lane < kLIn - 32) s[row * kLS + 32 + lane] = v1[k];
+    }
+  }
 }
 
 // The two images (and in the backward the first two SSIM sources) travel as
@@ -256,29 +268,44 @@ __global__ void __launch_bounds__(256, 4) ssim_bwd_kernel(
     gv[o] = in ? __ldg(g + p) : 0.f;
   }
   {
-    float2 v2[kHaloIters];
-    float v1[kHaloIters];
-    int dst[kHaloIters];
+    // row-wise halo of the planar SSIM sources (see load_halo2)
+    {
+      const int lane = tid & 31, warp = tid >> 5;
+      const int x0 = tx0 - kLR + lane, x1 = x0 + 32;
+      const bool in0 = x0 >= 0 && x0 < W, in1 = lane < kLIn - 32 && x1 >= 0 && x1 < W;
+      float2 v2a[kHaloRows], v2b[kHaloRows];
+      float v1a[kHaloRows], v1b[kHaloRows];
 #pragma unroll
-    for (int k = 0; k < kHaloIters; ++k) {
-      const int i = tid + 256 * k;
-      const int yy = i / kLIn, xx = i - yy * kLIn;
-      const int y = ty0 - kLR + yy, x = tx0 - kLR + xx;
-      v2[k] = bc2(0.f);
-      v1[k] = 0.f;
-      dst[k] = i < kLIn * kLIn ? yy * kLS + xx : -1;
-      if (i < kLIn * kLIn && y >= 0 && y < H && x >= 0 && x < W) {
-        const long long o = c * HW + (long long)y * W + x;
-        v2[k] = __ldg(Q01 + o);
-        v1[k] = __ldg(Q2 + o);
+      for (int k = 0; k < kHaloRows; ++k) {
+        const int row = warp + 8 * k;
+        const int y = ty0 - kLR + row;
+        v2a[k] = v2b[k] = bc2(0.f);
+        v1a[k] = v1b[k] = 0.f;
+        if (row < kLIn && y >= 0 && y < H) {
+          const long long o = c * HW + (long long)y * W;
+          if (in0) {
+            v2a[k] = __ldg(Q01 + o + x0);
+            v1a[k] = __ldg(Q2 + o + x0);
+          }
+          if (in1) {
+            v2b[k] = __ldg(Q01 + o + x1);
+            v1b[k] = __ldg(Q2 + o + x1);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kHaloRows; ++k) {
+        const int row = warp + 8 * k;
+        if (row < kLIn) {
+          s_q2[row * kLS + lane] = v2a[k];
+          s_q1[row * kLS + lane] = v1a[k];
+          if (lane < kLIn - 32) {
+            s_q2[row * kLS + 32 + lane] = v2b[k];
+            s_q1[row * kLS + 32 + lane] = v1b[k];
+          }
+        }
       }
     }
-#pragma unroll
-    for (int k = 0; k < kHaloIters; ++k)
-      if (dst[k] >= 0) {
-        s_q2[dst[k]] = v2[k];
-        s_q1[dst[k]] = v1[k];
-      }
     __syncthreads();
     for (int it = tid; it < kLIn * (kLT / 2); it += 256) {
       const int row = it >> 4, c0 = (it & 15) * 2;
