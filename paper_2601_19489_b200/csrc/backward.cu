@@ -425,16 +425,23 @@ __global__ void __launch_bounds__(256) unit_count_kernel(const int64_t* __restri
 // units[U_t + g] = tile << 16 | g; the unit count; the grab counter reset;
 // and, for the deterministic merge, processed[t] = 64 x supergroups.
 constexpr int kPlanThreads = 1024;
+constexpr int kPlanMaxTiles = 12288;  // staged counts (48 KB); larger frames read global
 __global__ void __launch_bounds__(kPlanThreads) unit_plan_kernel(
     const int32_t* __restrict__ nsup, int n_tiles, uint32_t* __restrict__ units,
     long long units_cap, int32_t* __restrict__ n_units, int32_t* __restrict__ counter,
     int32_t* __restrict__ processed) {
+  extern __shared__ int s_n[];  // per-tile supergroup counts (coalesced stage)
   __shared__ int s_w[kPlanThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool staged = n_tiles <= kPlanMaxTiles;
+  if (staged)
+    for (int t = tid; t < n_tiles; t += kPlanThreads) s_n[t] = nsup[t];
+  __syncthreads();
+  auto cnt = [&](int t) { return staged ? s_n[t] : nsup[t]; };
   const int per = (n_tiles + kPlanThreads - 1) / kPlanThreads;
   const int t0 = tid * per, t1 = min(n_tiles, t0 + per);
   int sum = 0;
-  for (int t = t0; t < t1; ++t) sum += nsup[t];
+  for (int t = t0; t < t1; ++t) sum += cnt(t);
   int incl = sum;
 #pragma unroll
   for (int k = 1; k < 32; k <<= 1) {
@@ -455,7 +462,7 @@ __global__ void __launch_bounds__(kPlanThreads) unit_plan_kernel(
   __syncthreads();
   long long u = (long long)s_w[warp] + incl - sum;
   for (int t = t0; t < t1; ++t) {
-    const int k = nsup[t];
+    const int k = cnt(t);
     if (processed) processed[t] = k * kSuper;
     for (int g = 0; g < k; ++g, ++u)
       if (u < units_cap) units[u] = ((uint32_t)t << 16) | (uint32_t)g;
@@ -900,8 +907,15 @@ int launch_units(const float* rec, const int32_t* values, const int64_t* offsets
   unit_count_kernel<<<(n_tiles + 7) / 8, 256, 0, s>>>(offsets, n_considered, width, height, tx,
                                                       n_tiles, u.nsup);
   TSR_CHECK_LAUNCH();
-  unit_plan_kernel<<<1, kPlanThreads, 0, s>>>(u.nsup, n_tiles, u.units, u.cap, u.n_units,
-                                              u.counter, processed);
+  const size_t plan_smem = n_tiles <= kPlanMaxTiles ? (size_t)n_tiles * sizeof(int) : 0;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(unit_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kPlanMaxTiles * (int)sizeof(int));
+    attr_set = true;
+  }
+  unit_plan_kernel<<<1, kPlanThreads, plan_smem, s>>>(u.nsup, n_tiles, u.units, u.cap,
+                                                      u.n_units, u.counter, processed);
   TSR_CHECK_LAUNCH();
   auto* k = render_bwd_units_kernel<kDepth, kDet>;
   static int per_sm = 0, sms = 0;  // occupancy of this instantiation (host-side constant)
