@@ -11,7 +11,7 @@ LIB := paper_2601_19489_b200/libtilesplat_b200.so
 
 all: $(LIB)
 
-build/%.o: $(SRC_DIR)/%.cu $(SRC_DIR)/tsr_common.cuh include/tilesplat_b200.h
+build/%.o: $(SRC_DIR)/%.cu $(SRC_DIR)/tsr_common.cuh $(SRC_DIR)/tsr_vjp_adam.cuh include/tilesplat_b200.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 

@@ -345,6 +345,28 @@ int tsr_preprocess_bwd_adam_ex(const tsr_gaussians_t* g, const tsr_camera_t* cam
                                unsigned long long* skipped, const int32_t* gate,
                                int32_t* gated_steps, const float* loss_guard, void* stream);
 
+/* K4 with the projection VJP + Adam fused into its tail (SH 0 training step;
+ * replaces tsr_render_bwd_ordered + tsr_preprocess_bwd_adam_ex).  Each tile
+ * CTA, after its merges, counts its pairs into row_done[row]; the CTA that
+ * brings a row to counts[row] (K1's pair count) runs that Gaussian's VJP and
+ * Adam update (source_ids maps rows to Gaussians) and zeroes its Grad2D row.
+ * A second kernel updates the Gaussians without pairs (culled, or no tile)
+ * and re-arms row_done (zero-filled once by the caller).  Adam scalars from
+ * group_scalars (device, [lr, bc1, bc2] x 5) when not NULL; gate /
+ * gated_steps / loss_guard as in tsr_preprocess_bwd_adam_ex. */
+int tsr_render_bwd_adam(const float* rec, const int32_t* values, const int64_t* offsets,
+                        int32_t width, int32_t height, const float* color, const float* depth,
+                        const float* final_T, const int32_t* n_considered, const float* ckpt,
+                        const int64_t* ckpt_base, const float* grad_color,
+                        const float* grad_depth, const float* grad_final_T, float* grad2d,
+                        unsigned long long* merges, const int32_t* tile_order,
+                        const tsr_gaussians_t* g, const tsr_camera_t* cam,
+                        const tsr_adam_group_t* groups_host, const float* group_scalars,
+                        const int32_t* source_ids, const int32_t* row_of_source,
+                        const int32_t* counts, int32_t* row_done, unsigned long long* skipped,
+                        const int32_t* gate, int32_t* gated_steps, const float* loss_guard,
+                        void* stream);
+
 /* ---------------------------------------------------------- depth chain ----
  * Disparity loss on the normalised render depth and its chain to the raster
  * outputs (losses.py:94-112 + trainer.py:201-214): mask = n_contrib > 0

@@ -76,6 +76,11 @@ _SIGNATURES = {
                                        c_vp]),
     "tsr_render_bwd_ordered": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp,
                                        c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "tsr_render_bwd_adam": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp,
+                                    c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                    ctypes.POINTER(Gaussians_t), ctypes.POINTER(Camera_t),
+                                    ctypes.POINTER(AdamGroup_t), c_vp, c_vp, c_vp, c_vp, c_vp,
+                                    c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tsr_render_bwd_workspace": (c_sz, [c_i32, c_i32, c_i64]),
     "tsr_render_bwd_ws": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
                                   c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_sz, c_vp]),

@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include "tsr_common.cuh"
+#include "tsr_vjp_adam.cuh"
 
 namespace tsr {
 
@@ -56,12 +57,67 @@ constexpr int kListPad = 32;
 //   a = pixel centre x, y, g_depth, n_considered (int bits)
 //   b = g_r, g_g, g_b, Ktot + g_T T_final
 
+// K4 with the projection VJP and Adam fused into its tail (SH 0 training
+// step).  Every CTA, after its merges, counts its list's pairs into a per-row
+// counter; the CTA that completes a row (count == K1's pair count of the row:
+// every tile holding the row has merged) runs that Gaussian's VJP + Adam, from
+// a shared-memory queue so the work is convergent.  The HBM-bound update
+// (~450 B per Gaussian) thus runs inside the FP32-bound backward instead of
+// as a separate 90 us kernel after it; vjp_adam_rest_kernel updates the
+// Gaussians without any pair and re-arms the counters.
+struct FusedAdamArgs {
+  tsr_camera_t cam;
+  AdamGroups groups;
+  const int32_t* source_ids;  // row -> Gaussian
+  const int32_t* counts;      // K1: pairs of each row
+  int32_t* row_done;          // merged (tile, row) pairs so far (zero between steps)
+  const float* scal;          // per-step [lr, bc1, bc2] x 5 (device), or null: by value
+  const int32_t* gate;        // K2's overflow flag (skip the update)
+  const float* loss_guard;    // the step's loss (non-finite: skip the update)
+  unsigned long long* skipped;
+};
+
+constexpr int kRowQueue = 1024;
+
+__device__ __forceinline__ void fused_row_epilogue(const FusedAdamArgs& fa,
+                                                   const int32_t* __restrict__ values,
+                                                   long long start, int n,
+                                                   const float4* __restrict__ rec,
+                                                   float* __restrict__ grad2d, int* s_q,
+                                                   int* s_qn) {
+  __syncthreads();  // every warp of the CTA has issued its merges ...
+  __threadfence();  // ... and they are visible before its counts
+  const bool update = !((fa.gate && *fa.gate) || (fa.loss_guard && !isfinite(*fa.loss_guard)));
+  unsigned long long skipped = 0;
+  for (int base = 0; base < n; base += kRowQueue) {
+    if (threadIdx.x == 0) *s_qn = 0;
+    __syncthreads();
+    for (int j = threadIdx.x; j < kRowQueue && base + j < n; j += kBwdThreads) {
+      const int row = values[start + base + j];
+      if (atomicAdd(fa.row_done + row, 1) == fa.counts[row] - 1) s_q[atomicAdd(s_qn, 1)] = row;
+    }
+    __syncthreads();
+    const int qn = *s_qn;
+    if (qn) __threadfence();  // the other tiles' merges of the completed rows
+    for (int q = threadIdx.x; q < qn; q += kBwdThreads) {
+      const int row = s_q[q];
+      bool vis;
+      float pose[12];
+      skipped += vjp_adam_row_sh0<false, true>(fa.cam, fa.groups, fa.source_ids[row], row, rec,
+                                               grad2d, fa.scal, update, pose, vis);
+    }
+    __syncthreads();
+  }
+  for (int d = 16; d > 0; d >>= 1) skipped += __shfl_xor_sync(0xffffffffu, skipped, d);
+  if ((threadIdx.x & 31) == 0 && skipped) atomicAdd(fa.skipped, skipped);
+}
+
 // kDet: deterministic merge -- instead of atomics into grad2d, every pair of
 // a processed supergroup writes its 10 scaled sums to slot[pair] (plain
 // stores, one writer per pair) and the tile records how many list positions
 // it processed; grad_reduce_kernel then sums each row's slots in emission
 // order, so results are bitwise reproducible.
-template <bool kDepth, bool kDet>
+template <bool kDepth, bool kDet, bool kFused = false>
 __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
     const float4* __restrict__ rec, const int32_t* __restrict__ values,
     const int64_t* __restrict__ offsets, int width, int height, int tiles_x,
@@ -71,8 +127,11 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
     const float* __restrict__ grad_color, const float* __restrict__ grad_depth,
     const float* __restrict__ grad_final_T, float* __restrict__ grad2d,
     unsigned long long* __restrict__ merges, float* __restrict__ slots,
-    int32_t* __restrict__ processed, const int32_t* __restrict__ order) {
+    int32_t* __restrict__ processed, const int32_t* __restrict__ order,
+    FusedAdamArgs fa = FusedAdamArgs{}) {
   __shared__ float4 s_pa[kPixSlots];
+  __shared__ int s_q[kFused ? kRowQueue : 1];
+  __shared__ int s_qn;
   __shared__ float4 s_pb[kPixSlots];
   // byte offsets; the step count is rounded up to a multiple of 4, hence
   // kListPad + 3 trailing sentinels
@@ -116,9 +175,11 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
     s_pa[px] = make_float4((float)x + 0.5f, (float)y + 0.5f, gd, __int_as_float(nc));
     s_pb[px] = make_float4(gr, gg, gb, k);
   }
-  // tile skipped when its upstream is all zero (backward.py:156-158)
+  // tile skipped when its upstream is all zero (backward.py:156-158); the
+  // fused form still counts its pairs (their rows' updates wait on them)
   if (!__syncthreads_or(nz)) {
     if (kDet && tid == 0) processed[tile] = 0;
+    if (kFused) fused_row_epilogue(fa, values, start, n, rec, grad2d, s_q, &s_qn);
     return;
   }
   atomicMax(&s_maxnc, my_max);
@@ -374,6 +435,7 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
       }
     }
   }
+  if (kFused) fused_row_epilogue(fa, values, start, n, rec, grad2d, s_q, &s_qn);
 }
 
 // ---- K4, work-unit form ---------------------------------------------------
@@ -806,7 +868,7 @@ extern "C" int tsr_render_bwd(const float* rec, const int32_t* values, const int
   k<<<tx * ty, kBwdThreads, 0, (cudaStream_t)stream>>>(
       (const float4*)rec, values, offsets, width, height, tx, color, depth, final_T,
       n_considered, ckpt, ckpt_base, grad_color, grad_depth, grad_final_T, grad2d, merges,
-      nullptr, nullptr, nullptr);
+      nullptr, nullptr, nullptr, FusedAdamArgs{});
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }
@@ -827,7 +889,7 @@ extern "C" int tsr_render_bwd_ordered(const float* rec, const int32_t* values,
   k<<<tx * ty, kBwdThreads, 0, (cudaStream_t)stream>>>(
       (const float4*)rec, values, offsets, width, height, tx, color, depth, final_T,
       n_considered, ckpt, ckpt_base, grad_color, grad_depth, grad_final_T, grad2d, merges,
-      nullptr, nullptr, tile_order);
+      nullptr, nullptr, tile_order, FusedAdamArgs{});
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }
@@ -853,7 +915,7 @@ extern "C" int tsr_render_bwd_det(const float* rec, const int32_t* values, const
   k<<<tx * ty, kBwdThreads, 0, s>>>((const float4*)rec, values, offsets, width, height, tx,
                                     color, depth, final_T, n_considered, ckpt, ckpt_base,
                                     grad_color, grad_depth, grad_final_T, nullptr, merges, slots,
-                                    processed, nullptr);
+                                    processed, nullptr, FusedAdamArgs{});
   TSR_CHECK_LAUNCH();
   if (m > 0) {
     grad_reduce_kernel<<<(int)((m + 255) / 256), 256, 0, s>>>(
@@ -1004,4 +1066,48 @@ extern "C" int tsr_render_bwd_ws_det(const float* rec, const int32_t* values,
     TSR_CHECK_LAUNCH();
   }
   return TSR_OK;
+}
+
+extern "C" int tsr_render_bwd_adam(
+    const float* rec, const int32_t* values, const int64_t* offsets, int32_t width,
+    int32_t height, const float* color, const float* depth, const float* final_T,
+    const int32_t* n_considered, const float* ckpt, const int64_t* ckpt_base,
+    const float* grad_color, const float* grad_depth, const float* grad_final_T, float* grad2d,
+    unsigned long long* merges, const int32_t* tile_order, const tsr_gaussians_t* g,
+    const tsr_camera_t* cam, const tsr_adam_group_t* groups_host, const float* group_scalars,
+    const int32_t* source_ids, const int32_t* row_of_source, const int32_t* counts,
+    int32_t* row_done, unsigned long long* skipped, const int32_t* gate, int32_t* gated_steps,
+    const float* loss_guard, void* stream) {
+  if (width <= 0 || height <= 0 || !grad_color || !merges || !grad2d || !g || !cam ||
+      !source_ids || !row_of_source || !counts || !row_done || !skipped)
+    return TSR_E_INVALID;
+  if (ckpt && !ckpt_base) return TSR_E_INVALID;
+  if (g->sh_coeffs != 1) return TSR_E_INVALID;  // the SH-0 fast path only
+  FusedAdamArgs fa{};
+  if (!fill_adam_groups(groups_host, 5, fa.groups)) return TSR_E_INVALID;
+  for (int k = 0; k < 5; ++k)
+    if (fa.groups.g[k].rows != g->n || !fa.groups.g[k].exp_avg || !fa.groups.g[k].exp_avg_sq)
+      return TSR_E_INVALID;
+  if (fa.groups.g[0].width != 3 || fa.groups.g[1].width != 3 || fa.groups.g[2].width != 4 ||
+      fa.groups.g[3].width != 1 || fa.groups.g[4].width != 3)
+    return TSR_E_INVALID;
+  fa.cam = *cam;
+  fa.source_ids = source_ids;
+  fa.counts = counts;
+  fa.row_done = row_done;
+  fa.scal = group_scalars;
+  fa.gate = gate;
+  fa.loss_guard = loss_guard;
+  fa.skipped = skipped;
+  const int tx = tiles_of(width), ty = tiles_of(height);
+  cudaStream_t s = (cudaStream_t)stream;
+  auto* k = grad_depth ? render_bwd_kernel<true, false, true> : render_bwd_kernel<false, false, true>;
+  k<<<tx * ty, kBwdThreads, 0, s>>>((const float4*)rec, values, offsets, width, height, tx, color,
+                                    depth, final_T, n_considered, ckpt, ckpt_base, grad_color,
+                                    grad_depth, grad_final_T, grad2d, merges, nullptr, nullptr,
+                                    tile_order, fa);
+  TSR_CHECK_LAUNCH();
+  return tsr_launch_vjp_adam_rest(*cam, g->n, rec, row_of_source, counts, row_done, grad2d,
+                                  fa.groups, skipped, group_scalars, gate, gated_steps,
+                                  loss_guard, s);
 }

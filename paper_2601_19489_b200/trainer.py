@@ -10,6 +10,7 @@ host read of the pair count (P sizes the key buffers).
 from __future__ import annotations
 
 import json
+import os
 
 from dataclasses import dataclass, field
 
@@ -176,6 +177,15 @@ def _full_grads(gset: GaussianSet, camera: Camera, cfg: TrainConfig, delta, vr: 
             "colors": gcol, "pose_rot": gpose.rot_vec, "pose_trans": gpose.trans}
 
 
+# TSR_FUSED_ADAM=1: the SH-0 step runs the projection VJP + Adam fused into
+# K4's tail (tsr_render_bwd_adam: per-row merge counters, the CTA completing a
+# row updates it).  Measured slower at C2 (K4 575 -> 1177 us, + 55 us for the
+# rows without pairs, against 86 us for the separate K4b+K5 kernel): each
+# tile CTA's counting atomics and its HBM-latency-bound updates hold the SM
+# slot the FP32-bound backward needs, so it is opt-in.
+FUSED_ADAM = os.environ.get("TSR_FUSED_ADAM", "0") == "1"
+
+
 class TrainStep:
     """One-view training step on the device (fwd + loss + bwd + Adam).
 
@@ -238,6 +248,9 @@ class TrainStep:
         self.skipped = torch.zeros(1, dtype=torch.int64, device=dev)
         # overflowed steps whose update the fused kernel skipped (device)
         self.gated_steps = torch.zeros(1, dtype=torch.int32, device=dev)
+        # per-row merge counters of the fused K4 + update (zero between steps)
+        self.row_done = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+        self._updated = False
         self._history = []  # (camera, gt, depth args, iteration, loss tensors) per step
         self.redone_steps = 0
         self.merges = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -385,8 +398,19 @@ class TrainStep:
         self._mark(timer, "render")
         return batch
 
+    def _can_fuse_update(self) -> bool:
+        from .backward import K4_FORM
+        return (FUSED_ADAM and K4_FORM == "tiles" and not self.deterministic
+                and self.gset.colors.shape[1] == 1)
+
     def loss_and_backward(self, batch, camera: Camera, gt_image, timer=None,
-                          depth_weight: float = 0.0, depth_prior=None, depth_valid=None):
+                          depth_weight: float = 0.0, depth_prior=None, depth_valid=None,
+                          update=None):
+        """Loss + K4.  update = (Adam group descriptors, device scalars or
+        None): with the SH-0 per-tile K4, the projection VJP and Adam run
+        fused into K4's tail (tsr_render_bwd_adam) and self._updated is set;
+        otherwise the caller launches the fused K4b+K5 kernel."""
+        self._updated = False
         out, idx = self.targets, self.index
         e, l1, s, grad_color = losses.photometric_device(out.color, gt_image, self.cfg.lambda_,
                                                          grad=self.grad_color,
@@ -424,7 +448,19 @@ class TrainStep:
         if not self._grad2d_clean:
             self.grad2d.zero_()
         self._grad2d_clean = False
-        if K4_FORM == "tiles":
+        if update is not None and self._can_fuse_update():
+            groups, scal = update
+            s_ = self.scratch
+            _lib.check(self.lib.tsr_render_bwd_adam(
+                *common, self.grad2d.data_ptr(), self.merges.data_ptr(),
+                _lib.ptr(self.tile_order), gaussians_struct(self.gset),
+                camera_struct(camera, None, self.cfg.near), groups, _lib.ptr(scal),
+                s_.source_ids.data_ptr(), s_.row_of_source.data_ptr(), s_.counts.data_ptr(),
+                self.row_done.data_ptr(), self.skipped.data_ptr(), idx.overflow.data_ptr(),
+                self.gated_steps.data_ptr(), e.data_ptr(), _lib.stream_handle()),
+                "tsr_render_bwd_adam")
+            self._updated = True
+        elif K4_FORM == "tiles":
             _lib.check(self.lib.tsr_render_bwd_ordered(
                 *common, self.grad2d.data_ptr(), self.merges.data_ptr(),
                 _lib.ptr(self.tile_order), _lib.stream_handle()), "tsr_render_bwd_ordered")
@@ -448,19 +484,21 @@ class TrainStep:
                 _lib.ptr(depth_valid) if depth_on else 0)
 
     def _graph_body(self, camera: Camera, gt_image, depth_on: bool, depth_prior, depth_valid):
-        """The captured step: K1-K5 and the status publish; the per-step
-        scalars are read from _scal_dev."""
+        """The captured step: K1-K5 (K4b+K5 fused into K4 for SH 0) and the
+        status publish; the per-step scalars are read from _scal_dev."""
         batch = self.forward(camera, None)
+        groups = self.opt.groups_for_fused(self.gset.params(), None, advance=False)
         e = self.loss_and_backward(batch, camera, gt_image, None,
                                    self._scal_dev[15] if depth_on else 0.0,
-                                   depth_prior if depth_on else None, depth_valid)
-        groups = self.opt.groups_for_fused(self.gset.params(), None, advance=False)
-        _lib.check(self.lib.tsr_preprocess_bwd_adam_ex(
-            gaussians_struct(self.gset), camera_struct(camera, None, self.cfg.near),
-            batch.rec.data_ptr(), batch.row_of_source.data_ptr(), self.grad2d.data_ptr(), groups,
-            self._scal_dev.data_ptr(), None, self.skipped.data_ptr(),
-            self.index.overflow.data_ptr(), self.gated_steps.data_ptr(), e.data_ptr(),
-            _lib.stream_handle()), "tsr_preprocess_bwd_adam_ex")
+                                   depth_prior if depth_on else None, depth_valid,
+                                   update=(groups, self._scal_dev))
+        if not self._updated:
+            _lib.check(self.lib.tsr_preprocess_bwd_adam_ex(
+                gaussians_struct(self.gset), camera_struct(camera, None, self.cfg.near),
+                batch.rec.data_ptr(), batch.row_of_source.data_ptr(), self.grad2d.data_ptr(),
+                groups, self._scal_dev.data_ptr(), None, self.skipped.data_ptr(),
+                self.index.overflow.data_ptr(), self.gated_steps.data_ptr(), e.data_ptr(),
+                _lib.stream_handle()), "tsr_preprocess_bwd_adam_ex")
         self.status_ovf_host.copy_(self.index.overflow, non_blocking=True)
         self.status_tot_host.copy_(self.scratch.totals, non_blocking=True)
         return e
@@ -525,16 +563,17 @@ class TrainStep:
     def _eager_step(self, camera, gt_image, timer, depth_weight, depth_prior, depth_valid):
         self.iteration += 1
         batch = self.forward(camera, timer)
-        e = self.loss_and_backward(batch, camera, gt_image, timer, depth_weight, depth_prior,
-                                   depth_valid)
         lr = {"positions": position_lr(self.pos_base_lr, self.iteration, self.cfg.max_iters)}
         groups = self.opt.groups_for_fused(self.gset.params(), lr)
-        _lib.check(self.lib.tsr_preprocess_bwd_adam_ex(
-            gaussians_struct(self.gset), camera_struct(camera, None, self.cfg.near),
-            batch.rec.data_ptr(), batch.row_of_source.data_ptr(), self.grad2d.data_ptr(), groups,
-            None, None, self.skipped.data_ptr(), self.index.overflow.data_ptr(),
-            self.gated_steps.data_ptr(), e.data_ptr(), _lib.stream_handle()),
-            "tsr_preprocess_bwd_adam_ex")
+        e = self.loss_and_backward(batch, camera, gt_image, timer, depth_weight, depth_prior,
+                                   depth_valid, update=(groups, None))
+        if not self._updated:
+            _lib.check(self.lib.tsr_preprocess_bwd_adam_ex(
+                gaussians_struct(self.gset), camera_struct(camera, None, self.cfg.near),
+                batch.rec.data_ptr(), batch.row_of_source.data_ptr(), self.grad2d.data_ptr(),
+                groups, None, None, self.skipped.data_ptr(), self.index.overflow.data_ptr(),
+                self.gated_steps.data_ptr(), e.data_ptr(), _lib.stream_handle()),
+                "tsr_preprocess_bwd_adam_ex")
         self._grad2d_clean = self.gset.colors.shape[1] == 1
         self._mark(timer, "vjp_adam")
         self._publish_status()
