@@ -201,7 +201,54 @@ struct LbSplat {
   double mx, my, a, b, c, t, bc, ba;  // bc = -(b / c), ba = -(b / a): per-splat constants
   int tx0, ty0, ncols, nrows;
   float inv_rows;  // 1 / nrows (FP32)
+  float fmx, fmy, fa, fb2, fc, ft, fbc, fba;  // FP32 copies for the filter below
 };
+
+__device__ __forceinline__ LbSplat make_lb_splat(const SplatF64& s, const SnugRect& r, int ncols,
+                                                 int nrows) {
+  LbSplat L;
+  L.mx = s.mx; L.my = s.my; L.a = s.a; L.b = s.b; L.c = s.c; L.t = s.t;
+  L.bc = ncols ? -ddiv(s.b, s.c) : 0.0;
+  L.ba = ncols ? -ddiv(s.b, s.a) : 0.0;
+  L.tx0 = ncols ? (int)r.tx0 : 0;
+  L.ty0 = ncols ? (int)r.ty0 : 0;
+  L.ncols = ncols;
+  L.nrows = nrows;
+  L.inv_rows = nrows ? 1.0f / (float)nrows : 0.f;
+  L.fmx = (float)s.mx; L.fmy = (float)s.my; L.fa = (float)s.a; L.fb2 = (float)(2.0 * s.b);
+  L.fc = (float)s.c; L.ft = (float)s.t; L.fbc = (float)L.bc; L.fba = (float)L.ba;
+  return L;
+}
+
+// FP32 pre-decision of min_q_box <= t for tile (tx, ty): +1 certainly
+// passes, -1 certainly fails, 0 too close to call (then the exact FP64 test
+// decides).  The batch values, t and the tile edges are FP32-exact, so the
+// FP32 evaluation differs from the FP64 one only by rounding: a few units of
+// 2^-24 relative on the box coordinates, the hoisted divides and every
+// product, i.e. |q32 - q64| <= ~10 eps Q with Q = |a| X^2 + 2|b| X Y + |c| Y^2
+// over the box (X, Y its largest |coordinates|; the clipped candidates move
+// continuously with their inputs).  The band is 64 eps Q: most candidates
+// are decided in FP32 and the decisions are exactly the FP64 ones.
+__device__ __forceinline__ int min_q_box_lb32(const LbSplat& S, int tx, int ty) {
+  const float rx0 = (float)(16 * tx) - S.fmx, rx1 = rx0 + 16.f;
+  const float ry0 = (float)(16 * ty) - S.fmy, ry1 = ry0 + 16.f;
+  float qm = 0.f;
+  if (!((rx0 <= 0.f) && (0.f <= rx1) && (ry0 <= 0.f) && (0.f <= ry1))) {
+    auto q = [&](float dx, float dy) {
+      return fmaf(S.fa * dx, dx, fmaf(S.fb2 * dx, dy, S.fc * dy * dy));
+    };
+    auto clip = [](float v, float lo, float hi) { return fminf(fmaxf(v, lo), hi); };
+    const float y0 = clip(S.fbc * rx0, ry0, ry1), y1 = clip(S.fbc * rx1, ry0, ry1);
+    const float x0 = clip(S.fba * ry0, rx0, rx1), x1 = clip(S.fba * ry1, rx0, rx1);
+    qm = fminf(fminf(q(rx0, y0), q(rx1, y1)), fminf(q(x0, ry0), q(x1, ry1)));
+  }
+  const float X = fmaxf(fabsf(rx0), fabsf(rx1)), Y = fmaxf(fabsf(ry0), fabsf(ry1));
+  const float Q = fabsf(S.fa) * X * X + fabsf(S.fb2) * X * Y + fabsf(S.fc) * Y * Y;
+  const float band = 64.f * 5.9604645e-8f * Q + 1e-30f;
+  if (qm + band < S.ft) return 1;
+  if (qm - band > S.ft) return -1;
+  return 0;
+}
 
 // column-major candidate j of a rectangle with nrows rows -> (column, row).
 // (j + 1/2) / nrows is at least 1 / (2 nrows) from an integer; the FP32
@@ -251,10 +298,7 @@ __device__ __forceinline__ long long warp_count_lb(const SplatF64& s, bool valid
       nrows = (int)(r.ty1 - r.ty0 + 1);
     }
   }
-  w.sp[lane] = LbSplat{s.mx, s.my, s.a, s.b, s.c, s.t,
-                       ncols ? -ddiv(s.b, s.c) : 0.0, ncols ? -ddiv(s.b, s.a) : 0.0,
-                       ncols ? (int)r.tx0 : 0, ncols ? (int)r.ty0 : 0, ncols, nrows,
-                       nrows ? 1.0f / (float)nrows : 0.f};
+  w.sp[lane] = make_lb_splat(s, r, ncols, nrows);
   w.cnt[lane] = 0;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
@@ -290,9 +334,14 @@ __device__ __forceinline__ long long warp_count_lb(const SplatF64& s, bool valid
       const LbSplat& S = w.sp[o];
       const int j = k - ob;
       lb_cell(S, j, c, rr);
-      const double rx0 = dsub((double)(16 * (S.tx0 + c)), S.mx);
-      const double ry0 = dsub((double)(16 * (S.ty0 + rr)), S.my);
-      pass = min_q_box_lb(S, rx0, dadd(rx0, 16.0), ry0, dadd(ry0, 16.0)) <= S.t;
+      const int d = min_q_box_lb32(S, S.tx0 + c, S.ty0 + rr);
+      if (d == 0) {  // within the FP32 error band: the exact FP64 test
+        const double rx0 = dsub((double)(16 * (S.tx0 + c)), S.mx);
+        const double ry0 = dsub((double)(16 * (S.ty0 + rr)), S.my);
+        pass = min_q_box_lb(S, rx0, dadd(rx0, 16.0), ry0, dadd(ry0, 16.0)) <= S.t;
+      } else {
+        pass = d > 0;
+      }
     }
     bool prev = __shfl_up_sync(0xffffffffu, pass, 1);
     if (lane == 0) prev = carry;
@@ -365,10 +414,7 @@ __device__ __forceinline__ void warp_emit_lb(const SplatF64& s, bool valid, int 
       nrows = (int)(r.ty1 - r.ty0 + 1);
     }
   }
-  w.sp[lane] = LbSplat{s.mx, s.my, s.a, s.b, s.c, s.t,
-                       ncols ? -ddiv(s.b, s.c) : 0.0, ncols ? -ddiv(s.b, s.a) : 0.0,
-                       ncols ? (int)r.tx0 : 0, ncols ? (int)r.ty0 : 0, ncols, nrows,
-                       nrows ? 1.0f / (float)nrows : 0.f};
+  w.sp[lane] = make_lb_splat(s, r, ncols, nrows);
   w.cnt[lane] = 0;  // passing candidates written so far
   const int area = ncols * nrows;
   int incl = area;
@@ -400,9 +446,14 @@ __device__ __forceinline__ void warp_emit_lb(const SplatF64& s, bool valid, int 
       const int j = k - ob;
       int c, rr;
       lb_cell(S, j, c, rr);
-      const double rx0 = dsub((double)(16 * (S.tx0 + c)), S.mx);
-      const double ry0 = dsub((double)(16 * (S.ty0 + rr)), S.my);
-      pass = min_q_box_lb(S, rx0, dadd(rx0, 16.0), ry0, dadd(ry0, 16.0)) <= S.t;
+      const int d = min_q_box_lb32(S, S.tx0 + c, S.ty0 + rr);
+      if (d == 0) {  // within the FP32 error band: the exact FP64 test
+        const double rx0 = dsub((double)(16 * (S.tx0 + c)), S.mx);
+        const double ry0 = dsub((double)(16 * (S.ty0 + rr)), S.my);
+        pass = min_q_box_lb(S, rx0, dadd(rx0, 16.0), ry0, dadd(ry0, 16.0)) <= S.t;
+      } else {
+        pass = d > 0;
+      }
       tile = (S.ty0 + rr) * tiles_x + S.tx0 + c;
     }
     const unsigned pb = __ballot_sync(0xffffffffu, pass);
