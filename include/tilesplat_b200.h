@@ -165,7 +165,8 @@ int tsr_render_score(const float* rec, const int32_t* values, const int64_t* off
 
 /* Launch order for the per-tile kernels: heavy tiles (list longer than 4x
  * the mean) first in raster order, then the rest in raster order (one CTA;
- * order is (n_tiles,) int32).  tsr_render_fwd_ordered / tsr_render_bwd_ordered
+ * order is (n_tiles + 1,) int32, order[n_tiles] = 0 when there is no heavy
+ * tile -- raster order, nothing else written).  tsr_render_fwd_ordered / tsr_render_bwd_ordered
  * take it (NULL: raster order) -- the same outputs, the heavy tiles no longer
  * finish last (C3-lo). */
 int tsr_tile_order(const int64_t* offsets, int32_t n_tiles, int32_t* order, void* stream);

@@ -140,7 +140,8 @@ __global__ void __launch_bounds__(kBwdThreads, 5) render_bwd_kernel(
   __shared__ int s_maxnc;
   __shared__ int s_next;
 
-  const int tile = order ? order[blockIdx.x] : (int)blockIdx.x;  // heavy tiles first
+  const int tile = (order && order[gridDim.x]) ? order[blockIdx.x]  // heavy tiles first
+                                                : (int)blockIdx.x;
   const long long start = offsets[tile], end = offsets[tile + 1];
   const int n = (int)(end - start);
   if (n == 0) return;

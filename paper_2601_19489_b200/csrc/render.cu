@@ -141,8 +141,9 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
   __shared__ float4 s_raw[kBatch];  // a, b, c (unscaled), level t
   __shared__ int s_row[kScore ? kBatch : 1];
 
-  // heavy tiles first when an order is given (tile_order_kernel)
-  const int tile = order ? order[blockIdx.x] : (int)blockIdx.x;
+  // heavy tiles first when an order is given (tile_order_kernel; its last
+  // entry flags whether it differs from raster order)
+  const int tile = (order && order[gridDim.x]) ? order[blockIdx.x] : (int)blockIdx.x;
   const int tyi = tile / tiles_x, txi = tile - tyi * tiles_x;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -287,6 +288,8 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
 
 // Launch order of the per-tile kernels (K3, K4): the heavy tiles (list longer
 // than 4x the mean) first, in raster order, then the others in raster order.
+// order has n_tiles + 1 entries; order[n_tiles] = 0 when there is no heavy
+// tile (raster order: the kernel then writes nothing else).
 // Raster order keeps neighbouring tiles -- which share splats -- close in
 // time (L2 reuse of the splat records); a heavy tile launched in the middle
 // of the frame would finish last and set the tail (the low-opacity cluster
@@ -336,10 +339,11 @@ __global__ void __launch_bounds__(kOrderThreads) tile_order_kernel(const int64_t
     if (lane == 31) s_tot = wi;
   }
   __syncthreads();
-  if (s_tot == 0) {  // no heavy tile: raster order, written coalesced
-    for (int t = tid; t < n_tiles; t += kOrderThreads) order[t] = t;
+  if (s_tot == 0) {  // no heavy tile: raster order (order[n_tiles] = 0 says so)
+    if (tid == 0) order[n_tiles] = 0;
     return;
   }
+  if (tid == 0) order[n_tiles] = 1;
   int h = s_w[warp] + incl - heavy;  // heavy tiles before this thread's range
   int l = s_tot + (t0 - h);          // light tiles before it, after all heavy ones
   for (int t = t0; t < t1; ++t) {

@@ -385,8 +385,9 @@ class TrainStep:
         self.tile_order = None
         if TILE_ORDER == "heavy":  # heavy tiles first in K3 and K4
             n_tiles = camera.tiles_x * camera.tiles_y
-            if self._order_buf is None or self._order_buf.numel() != n_tiles:
-                self._order_buf = torch.empty(n_tiles, dtype=torch.int32, device=s.rec.device)
+            if self._order_buf is None or self._order_buf.numel() != n_tiles + 1:
+                self._order_buf = torch.empty(n_tiles + 1, dtype=torch.int32,
+                                              device=s.rec.device)
             self.tile_order = self._order_buf
             _lib.check(self.lib.tsr_tile_order(idx.offsets.data_ptr(), n_tiles,
                                                self.tile_order.data_ptr(), _lib.stream_handle()),
