@@ -468,10 +468,11 @@ def gpu_arm(args):
         # per-phase device times: the same segment again, eagerly with events
         # between the phases (outside the timed region)
         restore()
+        prev_graphs = stepper.graphs
         stepper.graphs = False
         for _ in range(args.steps):
             run(timer)
-        stepper.graphs = True
+        stepper.graphs = prev_graphs
         barrier()
     phases = {k: v / args.steps for k, v in phase_times(timer).items()}
     if world > 1:
@@ -592,7 +593,10 @@ def gpu_arm(args):
                                      "reads, sharded Adam, peer parameter stores)" if args.peer
                                      else " zero1 (reduce-scatter + sharded Adam + all-gather)"
                                      if args.zero1 else ""),
-                   "launch": "one CUDA graph replay per step" if graphs else "eager launches",
+                   "launch": ("one CUDA graph replay per step" if graphs and
+                              getattr(stepper, "graphs", True) else "eager launches"
+                              + (f" (graph capture failed: {stepper.graph_error})"
+                                 if getattr(stepper, "graph_error", None) else "")),
                    "merge": "deterministic (slots + emission-order row sums)"
                             if args.deterministic else "float atomics (FP32-tolerance)",
                    "l2": "inputs larger than L2 (Gaussian state + Adam moments 168 MB, "

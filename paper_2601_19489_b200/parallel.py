@@ -307,6 +307,7 @@ class ViewParallelStep(TrainStep):
         super().__init__(gset, cfg, extent)
         # CUDA-graph replay of the chunked step (after one eager step)
         self.graphs = graphs
+        self.graph_error = None
         self._warm = False
         self.group = group
         self.deterministic = deterministic
@@ -504,9 +505,21 @@ class ViewParallelStep(TrainStep):
         if entry is None:
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                e = self._step_views_chunked(cameras, gts, None, descs=descs,
-                                             scal_dev=self._scal_dev)
+            try:
+                with torch.cuda.graph(g):
+                    e = self._step_views_chunked(cameras, gts, None, descs=descs,
+                                                 scal_dev=self._scal_dev)
+            except RuntimeError as exc:
+                # a communicator that cannot be captured: run this (and every
+                # later) step eagerly instead -- same kernels, same result
+                import sys
+                print(f"[tilesplat_b200] CUDA-graph capture of the view-parallel step failed "
+                      f"({exc}); continuing with eager launches", file=sys.stderr)
+                self.graphs = False
+                self.graph_error = str(exc)[:200]
+                torch.cuda.synchronize()
+                return self._step_views_chunked(cameras, gts, None, descs=descs,
+                                                scal_dev=self._scal_dev)
             entry = self._graph_cache[key] = (g, e)
         entry[0].replay()
         self.status_event = torch.cuda.Event()
