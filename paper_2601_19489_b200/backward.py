@@ -66,7 +66,11 @@ class Grad2D:
         return self.packed[:, 9]
 
 
-# K4 schedule.  "tiles" (default): one CTA per tile, its 4 warps taking the
+# K4 schedule.  "regions" (default for the training step): the region-culled
+# K4 (tsr_render_bwd_regions, csrc/backward_regions.cu) fed by K3's region
+# lists; the public backward_per_gaussian, whose buffers carry the
+# reference's checkpoints but no region lists, then runs the per-tile form.
+# "tiles": one CTA per tile, its 4 warps taking the
 # tile's supergroups (tsr_render_bwd).  "units": the (tile, supergroup) work
 # units of the frame drained by the warps of a persistent grid
 # (tsr_render_bwd_ws) -- heavy tiles spread over the GPU and no warp idles at
@@ -74,7 +78,39 @@ class Grad2D:
 # slower: K4 is FP32-pipe bound (math-pipe throttle is the top stall and
 # grows with the extra warps) and each unit re-gathers its pixel records
 # (DESIGN.md §8).  TSR_K4=units selects it.
-K4_FORM = os.environ.get("TSR_K4", "tiles")
+K4_FORM = os.environ.get("TSR_K4", "regions")
+
+
+class RegionWorkspace:
+    """Device scratch of the region-culled K4 (unit plan + queue)."""
+
+    def __init__(self):
+        self.buf = None
+        self.key = None
+
+    def get(self, width: int, height: int, p_bound: int) -> torch.Tensor:
+        if self.buf is None or self.key[0] != (width, height) or self.key[1] < p_bound:
+            n = int(_lib.load().tsr_render_bwd_regions_workspace(width, height, p_bound))
+            self.buf = torch.empty(n, dtype=torch.uint8, device=_device())
+            self.key = ((width, height), p_bound)
+        return self.buf
+
+
+def backward_regions_raw(rec, values, offsets, width: int, height: int, targets, ckpt_base,
+                         regions, grad_color, grad_depth, grad_final_T, out: torch.Tensor,
+                         merges: torch.Tensor, workspace: RegionWorkspace,
+                         p_bound: int) -> None:
+    """Region-culled K4 (backward.py:137-223) over K3's region lists
+    (render_regions_raw); merges into `out` (zeroed by the caller)."""
+    lib = _lib.load()
+    ws = workspace.get(width, height, p_bound)
+    _lib.check(lib.tsr_render_bwd_regions(
+        rec.data_ptr(), _lib.ptr(values), offsets.data_ptr(), width, height,
+        targets.color.data_ptr(), targets.depth.data_ptr(), targets.final_T.data_ptr(),
+        targets.n_considered.data_ptr(), targets.ckpt.data_ptr(), ckpt_base.data_ptr(),
+        regions.list.data_ptr(), regions.seg.data_ptr(), grad_color.data_ptr(),
+        _lib.ptr(grad_depth), _lib.ptr(grad_final_T), out.data_ptr(), merges.data_ptr(),
+        int(p_bound), ws.data_ptr(), ws.numel(), _lib.stream_handle()), "tsr_render_bwd_regions")
 
 
 class BackwardWorkspace:
@@ -117,7 +153,7 @@ def backward_per_gaussian_raw(buffers: RenderBuffers, batch: SplatBatch, tiles: 
               buffers.n_considered.data_ptr(), _lib.ptr(buffers.ckpt),
               _lib.ptr(buffers.ckpt_base), gc.data_ptr(), _lib.ptr(gd), _lib.ptr(gt),
               out.data_ptr(), merges.data_ptr())
-    if K4_FORM == "tiles":
+    if K4_FORM in ("tiles", "regions"):
         _lib.check(lib.tsr_render_bwd(*common, _lib.stream_handle()), "tsr_render_bwd")
         return out, merges
     p_bound = tiles.n_pairs if p_bound is None else p_bound
@@ -150,7 +186,7 @@ def backward_det_raw(buffers: RenderBuffers, batch: SplatBatch, tiles: TileIndex
               merges.data_ptr(), slots.data_ptr(), processed.data_ptr(), inv_perm.data_ptr(),
               rank_row.data_ptr(), rank_count.data_ptr(), rank_off.data_ptr(),
               tiles.keys.data_ptr(), out.shape[0], _lib.ptr(m_dev), out.data_ptr())
-    if K4_FORM == "tiles":
+    if K4_FORM in ("tiles", "regions"):
         _lib.check(lib.tsr_render_bwd_det(*common, _lib.stream_handle()), "tsr_render_bwd_det")
         return
     p_bound = tiles.n_pairs if p_bound is None else p_bound

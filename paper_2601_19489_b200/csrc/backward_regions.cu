@@ -1,0 +1,564 @@
+// K4r: region-culled per-Gaussian raster backward (backward_per_gaussian,
+// backward.py:137-223) -- the training step's backward.
+//
+// Same arithmetic as K4 (backward.cu): per pixel and list position p, with
+// gc_p = <g_color, c_p> + g_depth d_p,
+//   T_p = T_seg * prod_{i<p, part_i} (1 - alpha_i)
+//   R_p = Ktot + g_T T_f - K_seg - sum_{i<=p} w_i gc_i
+//   dL/dalpha_p = T_p gc_p - R_p / (1 - alpha_p)
+// and per splat the ten Grad2D sums (backward.py:195-222), merged into
+// grad2d with atomics.  Alphas are K3's bit for bit (same operation
+// sequence), so participation (p < n_considered, alpha >= 1/255) agrees.
+//
+// What differs is the schedule.  K4 keeps splats in lanes and streams every
+// active pixel of the tile past them, so each (pixel, splat) pair of the
+// tile's list costs a full evaluation.  K4r keeps PIXELS in lanes and
+// streams the splats past them, and only the splats that can reach
+// alpha >= 1/255 somewhere in the lanes' 8x8 region: K3 already decides that
+// per (8x8 block, list position) for its own culling and writes the passing
+// positions as the region's list (render.cu, RegionArgs).  A splat that
+// fails the test contributes exact zeros to every pixel of the region, so
+// skipping it changes nothing; at C2 the region lists hold ~55 % of the
+// tile-list evaluations.
+//
+// Layout.  A warp is one work unit (tile, row pair rp, segment): its two
+// 16-lane halves run the regions (bx, rp), bx = 0, 1; lane j of a half owns
+// the four pixels (x0, y0), (x0, y1), (x0 + 4, y0), (x0 + 4, y1) with
+// x0 = 8 bx + (j & 3), y0 = 8 rp + (j >> 2), y1 = y0 + 4 -- two vertical pairs
+// sharing dy, so the alpha and chain arithmetic is packed FP32x2.  Each half
+// is a 16-stage systolic pipeline: at step t lane j processes the region
+// list entry e = t - j for its four pixels; the ten per-splat partial sums
+// flow lane to lane (one shuffle each), so lane 15 holds entry t - 15's
+// complete region sums.  The pixel state (T, R) never leaves its lane.
+// Splat records are staged per half in a shared-memory ring of 64 entries
+// (cp.async straight from rec, one block of 16 entries a round ahead; the
+// list position and row are loaded two rounds ahead); finished sums go to a
+// 32-entry buffer and are merged 16 at a time, one lane per entry.
+//
+// Segments.  A unit covers the list positions [1024 s, 1024 (s + 1)) of its
+// tile (K3 writes a checkpoint record at every segment start and the region
+// list offsets at every segment boundary), so a heavy tile's work spreads
+// over many warps (the paper's redistribution across heavy tiles,
+// PAPER.md:121/145); units are drawn from a global queue, long tiles first.
+#include <climits>
+
+#include <cuda_runtime.h>
+
+#include "tsr_common.cuh"
+
+namespace tsr {
+namespace {
+
+constexpr int kRWarps = 4;
+constexpr int kRThreads = 32 * kRWarps;
+constexpr int kRing = 64;    // staged region-list entries per half-warp (4 blocks of 16)
+constexpr int kOut = 32;     // finished-entry sums per half-warp (2 blocks of 16)
+constexpr int kHeavyN = 768; // units of tiles with longer lists are queued first
+
+__device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
+__device__ __forceinline__ float2 bc(float x) { return make_float2(x, x); }
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// a = (p < nc && alpha >= 1/255) ? alpha : 0 as one chained compare + select
+__device__ __forceinline__ float participate(int p, int nc, float alpha) {
+  float a;
+  asm("{\n\t.reg .pred q;\n\t"
+      "setp.lt.s32 q, %1, %2;\n\t"
+      "setp.ge.and.f32 q, %3, %4, q;\n\t"
+      "selp.f32 %0, %3, 0f00000000, q;\n\t}"
+      : "=f"(a)
+      : "r"(p), "r"(nc), "f"(alpha), "f"(kMinAlpha));
+  return a;
+}
+
+// Unit plan (one CTA): per tile ceil(n / kSeg) segments x 2 row pairs; the
+// units of tiles with n > kHeavyN first, then the rest, each in raster order.
+// unit = tile << 16 | segment << 1 | row pair.  Also resets the grab counter.
+constexpr int kPlanThreads = 1024;
+__global__ void __launch_bounds__(kPlanThreads) region_plan_kernel(
+    const int64_t* __restrict__ offsets, int n_tiles, uint32_t* __restrict__ units,
+    long long cap, int32_t* __restrict__ n_units, int32_t* __restrict__ counter) {
+  __shared__ int s_w[2][kPlanThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (n_tiles + kPlanThreads - 1) / kPlanThreads;
+  const int t0 = tid * per, t1 = min(n_tiles, t0 + per);
+  int cnt[2] = {0, 0};  // units of heavy / light tiles in this thread's range
+  for (int t = t0; t < t1; ++t) {
+    const long long n = offsets[t + 1] - offsets[t];
+    cnt[n > kHeavyN ? 0 : 1] += 2 * (int)((n + kSeg - 1) >> kSegShift);
+  }
+  int incl[2], excl[2];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    incl[c] = cnt[c];
+#pragma unroll
+    for (int k = 1; k < 32; k <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl[c], k);
+      if (lane >= k) incl[c] += v;
+    }
+    if (lane == 31) s_w[c][warp] = incl[c];
+  }
+  __syncthreads();
+  if (warp < 2) {
+    const int w = s_w[warp][lane];
+    int wi = w;
+#pragma unroll
+    for (int k = 1; k < 32; k <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, wi, k);
+      if (lane >= k) wi += v;
+    }
+    s_w[warp][lane] = wi - w;  // exclusive prefix of the warps
+  }
+  __syncthreads();
+  // totals: the last thread's inclusive prefix
+  __shared__ int s_tot;
+  if (tid == kPlanThreads - 1) s_tot = s_w[0][warp] + incl[0];
+  __syncthreads();
+  excl[0] = s_w[0][warp] + incl[0] - cnt[0];
+  excl[1] = s_tot + s_w[1][warp] + incl[1] - cnt[1];
+  long long u[2] = {excl[0], excl[1]};
+  for (int t = t0; t < t1; ++t) {
+    const long long n = offsets[t + 1] - offsets[t];
+    const int c = n > kHeavyN ? 0 : 1;
+    const int nseg = (int)((n + kSeg - 1) >> kSegShift);
+    for (int s = 0; s < nseg; ++s)
+      for (int rp = 0; rp < 2; ++rp, ++u[c])
+        if (u[c] < cap) units[u[c]] = ((uint32_t)t << 16) | ((uint32_t)s << 1) | (uint32_t)rp;
+  }
+  if (tid == kPlanThreads - 1) {
+    *n_units = (int32_t)min(u[1], cap);
+    *counter = 0;
+  }
+}
+
+// upstream of four pixels (x0 / x1, y0 / y1) is not all zero
+__device__ __forceinline__ bool quad_nz(const float* __restrict__ grad_color,
+                                        const float* __restrict__ grad_depth,
+                                        const float* __restrict__ grad_final_T, int width,
+                                        int height, int X0, int Y0) {
+  bool nz = false;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int x = X0 + (q >> 1) * 4, y = Y0 + (q & 1) * 4;
+    if (x < width && y < height) {
+      const long long pix = (long long)y * width + x;
+      nz |= grad_color[3 * pix] != 0.f || grad_color[3 * pix + 1] != 0.f ||
+            grad_color[3 * pix + 2] != 0.f || (grad_depth && grad_depth[pix] != 0.f) ||
+            (grad_final_T && grad_final_T[pix] != 0.f);
+    }
+  }
+  return nz;
+}
+
+template <bool kDepth>
+__global__ void __launch_bounds__(kRThreads, 4) render_bwd_regions_kernel(
+    const float4* __restrict__ rec, const int32_t* __restrict__ values,
+    const int64_t* __restrict__ offsets, int width, int height, int tiles_x,
+    const float* __restrict__ color, const float* __restrict__ depth,
+    const float* __restrict__ final_T, const int32_t* __restrict__ n_considered,
+    const float* __restrict__ ckpt, const int64_t* __restrict__ ckpt_base,
+    const uint32_t* __restrict__ rlist, const int32_t* __restrict__ rseg,
+    const float* __restrict__ grad_color, const float* __restrict__ grad_depth,
+    const float* __restrict__ grad_final_T, float* __restrict__ grad2d,
+    unsigned long long* __restrict__ merges, const uint32_t* __restrict__ units,
+    const int32_t* __restrict__ n_units_dev, int32_t* __restrict__ counter) {
+  // one half-warp's ring: a slot's four records share one address register
+  struct HalfRing {
+    float4 a[kRing];   // mx, my, a, b
+    float4 b[kRing];   // c, opacity, depth, level t
+    float4 c[kRing];   // r, g, b, -
+    int4 pr[kRing];    // list position, row
+  };
+  __shared__ HalfRing s_ring[kRWarps][2];
+  __shared__ float4 s_oa[kRWarps][2][kOut];   // sums: gq dx, gq dy, gq dxx, gq dxy
+  __shared__ float4 s_ob[kRWarps][2][kOut];   //       gq dyy, ld gauss, w g_r, w g_g
+  __shared__ float2 s_oc[kRWarps][2][kOut];   //       w g_b, w g_d
+  __shared__ int s_pos[kRWarps][2][kRing];    // list positions, staged 3 rounds ahead
+  __shared__ int s_row[kRWarps][2][kRing];    // their rows, staged 2 rounds ahead
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, h = lane >> 4, j = lane & 15;
+  float4* ra = s_ring[warp][h].a;
+  float4* rb = s_ring[warp][h].b;
+  float4* rc = s_ring[warp][h].c;
+  int4* pr = s_ring[warp][h].pr;
+  float4* oa = s_oa[warp][h];
+  float4* ob = s_ob[warp][h];
+  float2* oc = s_oc[warp][h];
+  int* spos = s_pos[warp][h];
+  int* srow = s_row[warp][h];
+  // sentinel splat: alpha = gauss = 0 at every pixel, finite products
+  const float4 sent_a = make_float4(-65536.f, -65536.f, 1.f, 0.f);
+  const float4 sent_b = make_float4(1.f, 1.f, 0.f, 0.f);
+  const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float keep = j != 0 ? 1.f : 0.f;  // lane 0 of a half starts each entry's sums
+  const int n_units = *n_units_dev;
+
+  for (;;) {
+    int u = 0;
+    if (lane == 0) u = atomicAdd(counter, 1);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= n_units) break;
+    const uint32_t code = units[u];
+    const int tile = (int)(code >> 16), seg = (int)((code >> 1) & 0x7fffu), rp = (int)(code & 1u);
+    const long long start = offsets[tile];
+    const int n = (int)(offsets[tile + 1] - start);
+    const int r = 2 * rp + h;  // K3's warp index of this 8x8 block
+    const long long sb = 4 * ((start >> kSegShift) + tile) + r;
+    const int e0 = seg > 0 ? rseg[sb + 4 * (seg - 1)] : 0;
+    const int L = rseg[sb + 4 * seg] - e0;
+    const int Lmax = max(L, __shfl_xor_sync(0xffffffffu, L, 16));
+    const int tyi = tile / tiles_x, txi = tile - tyi * tiles_x;
+    const int X0 = txi * kTile + 8 * h + (j & 3), Y0 = tyi * kTile + 8 * rp + (j >> 2);
+    const int p0 = seg << kSegShift;
+
+    // ---- pixel state: q = 0 (X0, Y0), 1 (X0, Y0 + 4) [pair A], 2, 3 [pair B, x + 4]
+    float T[4], R[4], g_r[4], g_g[4], g_b[4], g_d[4];
+    int nc[4];
+    bool nzl = false;
+    const float* ck = seg > 0 ? ckpt + (ckpt_base[tile] + ((long long)seg << (kSegShift - 5)) - 1) *
+                                           (5 * kTilePixels)
+                              : nullptr;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int x = X0 + (q >> 1) * 4, y = Y0 + (q & 1) * 4;
+      T[q] = 0.f;
+      R[q] = 0.f;
+      g_r[q] = g_g[q] = g_b[q] = g_d[q] = 0.f;
+      nc[q] = 0;
+      if (x < width && y < height) {
+        const long long pix = (long long)y * width + x;
+        g_r[q] = grad_color[3 * pix];
+        g_g[q] = grad_color[3 * pix + 1];
+        g_b[q] = grad_color[3 * pix + 2];
+        if (kDepth && grad_depth) g_d[q] = grad_depth[pix];
+        const float gt = grad_final_T ? grad_final_T[pix] : 0.f;
+        nzl |= (g_r[q] != 0.f) || (g_g[q] != 0.f) || (g_b[q] != 0.f) || (g_d[q] != 0.f) ||
+               (gt != 0.f);
+        nc[q] = n_considered[pix];
+        if (nc[q] > p0) {  // active in this segment
+          float k = g_r[q] * color[3 * pix] + g_g[q] * color[3 * pix + 1] +
+                    g_b[q] * color[3 * pix + 2] + gt * final_T[pix];
+          if (kDepth) k += g_d[q] * depth[pix];
+          float T0 = 1.f, K0 = 0.f;
+          if (ck) {
+            const int lp = (y - tyi * kTile) * kTile + (x - txi * kTile);
+            T0 = ck[lp];
+            K0 = g_r[q] * ck[kTilePixels + lp] + g_g[q] * ck[2 * kTilePixels + lp] +
+                 g_b[q] * ck[3 * kTilePixels + lp];
+            if (kDepth) K0 += g_d[q] * ck[4 * kTilePixels + lp];
+          }
+          T[q] = T0;
+          R[q] = k - K0;
+        }
+      }
+    }
+    const bool nz = __any_sync(0xffffffffu, nzl);
+    // merges follow the reference's count: every pair of a tile whose
+    // upstream is not all zero (backward.py:156-158, 214-222)
+    if (seg == 0 && rp == 0) {
+      const bool other = quad_nz(grad_color, kDepth ? grad_depth : nullptr, grad_final_T, width,
+                                 height, X0, Y0 + 8);
+      if (__any_sync(0xffffffffu, nzl || other) && lane == 0)
+        atomicAdd(merges, (unsigned long long)n);
+    }
+    if (!nz || Lmax == 0) continue;  // exact zeros
+
+    const uint32_t* lst = rlist + 4 * start + (long long)r * n + e0;
+    const int32_t* vals = values + start;
+    // Every list access is asynchronous (cp.async into shared memory, waited
+    // once per round), three stages per entry e of this lane's half:
+    //   position  lst[e]          -> spos  (3 rounds ahead)
+    //   row       values[pos]     -> srow  (2 rounds ahead)
+    //   record    rec[row] x 3    -> ring  (1 round ahead), (pos, row) -> pr
+    auto fetch_pos = [&](int e) {
+      if (e < L) cp_async4(&spos[e & (kRing - 1)], lst + e);
+      else spos[e & (kRing - 1)] = INT_MAX;
+    };
+    auto fetch_row = [&](int e) {
+      const int pos = spos[e & (kRing - 1)];
+      if (pos != INT_MAX) cp_async4(&srow[e & (kRing - 1)], vals + pos);
+      else srow[e & (kRing - 1)] = -1;
+    };
+    auto stage = [&](int e) {
+      const int slot = e & (kRing - 1);
+      const int pos = spos[slot], row = srow[slot];
+      if (row >= 0) {
+        cp_async16(&ra[slot], rec + 3 * (long long)row);
+        cp_async16(&rb[slot], rec + 3 * (long long)row + 1);
+        cp_async16(&rc[slot], rec + 3 * (long long)row + 2);
+      } else {
+        ra[slot] = sent_a;
+        rb[slot] = sent_b;
+        rc[slot] = zero4;
+      }
+      pr[slot] = make_int4(pos, row, 0, 0);
+    };
+    __syncwarp();  // the previous unit's flush has read the ring
+    // block -1 (the pipeline fill reads entries -16..-1): sentinels
+    ra[kRing - 16 + j] = sent_a;
+    rb[kRing - 16 + j] = sent_b;
+    rc[kRing - 16 + j] = zero4;
+    pr[kRing - 16 + j] = make_int4(INT_MAX, -1, 0, 0);
+    fetch_pos(j);
+    fetch_pos(16 + j);
+    fetch_pos(32 + j);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncwarp();
+    fetch_row(j);
+    fetch_row(16 + j);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncwarp();
+    stage(j);
+    cp_async_commit();
+
+    const float xa = (float)X0 + 0.5f, xb = (float)(X0 + 4) + 0.5f;
+    const float2 yp = f2((float)Y0 + 0.5f, (float)(Y0 + 4) + 0.5f);
+    float2 TA = f2(T[0], T[1]), TB = f2(T[2], T[3]);
+    float2 RA = f2(R[0], R[1]), RB = f2(R[2], R[3]);
+    const float2 grA = f2(g_r[0], g_r[1]), grB = f2(g_r[2], g_r[3]);
+    const float2 ggA = f2(g_g[0], g_g[1]), ggB = f2(g_g[2], g_g[3]);
+    const float2 gbA = f2(g_b[0], g_b[1]), gbB = f2(g_b[2], g_b[3]);
+    const float2 gdA = f2(g_d[0], g_d[1]), gdB = f2(g_d[2], g_d[3]);
+    const int nc0 = nc[0], nc1 = nc[1], nc2 = nc[2], nc3 = nc[3];
+    float s_mx = 0.f, s_my = 0.f, s_a = 0.f, s_b = 0.f, s_c = 0.f, s_o = 0.f, s_r = 0.f,
+          s_g = 0.f, s_bl = 0.f, s_d = 0.f;
+    const float2 one = bc(1.f);
+
+    // one systolic step: entry t - j of this half for the lane's four pixels
+    // (A, B, pos) of a step are loaded one step ahead (ping-pong registers);
+    // the colour record C in the step (first used after the alpha chain)
+    auto step = [&](const float4& A, const float4& B, int pos, int t) {
+      const float4 C = rc[(t - j) & (kRing - 1)];
+      float i_mx = __shfl_up_sync(0xffffffffu, s_mx, 1, 16);
+      float i_my = __shfl_up_sync(0xffffffffu, s_my, 1, 16);
+      float i_a = __shfl_up_sync(0xffffffffu, s_a, 1, 16);
+      float i_b = __shfl_up_sync(0xffffffffu, s_b, 1, 16);
+      float i_c = __shfl_up_sync(0xffffffffu, s_c, 1, 16);
+      float i_o = __shfl_up_sync(0xffffffffu, s_o, 1, 16);
+      float i_r = __shfl_up_sync(0xffffffffu, s_r, 1, 16);
+      float i_g = __shfl_up_sync(0xffffffffu, s_g, 1, 16);
+      float i_bl = __shfl_up_sync(0xffffffffu, s_bl, 1, 16);
+      float i_d = kDepth ? __shfl_up_sync(0xffffffffu, s_d, 1, 16) : 0.f;
+      // alpha of the four pixels: K3's operation sequence (eval_alpha)
+      const float ca = __fmul_rn(A.z, kQScale), cb = __fmul_rn(A.w, 2.0f * kQScale),
+                  cc = __fmul_rn(B.x, kQScale);
+      const float dx0 = __fsub_rn(xa, A.x), dx1 = __fsub_rn(xb, A.x);
+      const float2 dy = __fadd2_rn(yp, bc(-A.y));
+      const float dxx0 = __fmul_rn(dx0, dx0), dxx1 = __fmul_rn(dx1, dx1);
+      const float2 dyy = __fmul2_rn(dy, dy);
+      const float2 dxyA = __fmul2_rn(bc(dx0), dy), dxyB = __fmul2_rn(bc(dx1), dy);
+      const float2 cyy = __fmul2_rn(bc(cc), dyy);
+      const float2 qA = __ffma2_rn(bc(ca), bc(dxx0), __ffma2_rn(bc(cb), dxyA, cyy));
+      const float2 qB = __ffma2_rn(bc(ca), bc(dxx1), __ffma2_rn(bc(cb), dxyB, cyy));
+      const float2 gaA = f2(fast_exp2(qA.x), fast_exp2(qA.y));
+      const float2 gaB = f2(fast_exp2(qB.x), fast_exp2(qB.y));
+      const float2 rawA = __fmul2_rn(bc(B.y), gaA), rawB = __fmul2_rn(bc(B.y), gaB);
+      const float2 alA = f2(fminf(kAlphaCap, rawA.x), fminf(kAlphaCap, rawA.y));
+      const float2 alB = f2(fminf(kAlphaCap, rawB.x), fminf(kAlphaCap, rawB.y));
+      // non-participants get a = 0: w = 0, T and R unchanged exactly
+      const float2 aA = f2(participate(pos, nc0, alA.x), participate(pos, nc1, alA.y));
+      const float2 aB = f2(participate(pos, nc2, alB.x), participate(pos, nc3, alB.y));
+      const float2 omA = __fadd2_rn(one, f2(-aA.x, -aA.y));
+      const float2 omB = __fadd2_rn(one, f2(-aB.x, -aB.y));
+      float2 gcA = __ffma2_rn(grA, bc(C.x), __ffma2_rn(ggA, bc(C.y), __fmul2_rn(gbA, bc(C.z))));
+      float2 gcB = __ffma2_rn(grB, bc(C.x), __ffma2_rn(ggB, bc(C.y), __fmul2_rn(gbB, bc(C.z))));
+      if (kDepth) {
+        gcA = __ffma2_rn(gdA, bc(B.z), gcA);
+        gcB = __ffma2_rn(gdB, bc(B.z), gcB);
+      }
+      const float2 wA = __fmul2_rn(TA, aA), wB = __fmul2_rn(TB, aB);
+      const float2 numA = __ffma2_rn(f2(-wA.x, -wA.y), gcA, RA);
+      const float2 numB = __ffma2_rn(f2(-wB.x, -wB.y), gcB, RB);
+      const float2 rcA = f2(rcp_approx(omA.x), rcp_approx(omA.y));
+      const float2 rcB = f2(rcp_approx(omB.x), rcp_approx(omB.y));
+      const float2 dLA = __ffma2_rn(f2(-numA.x, -numA.y), rcA, __fmul2_rn(TA, gcA));
+      const float2 dLB = __ffma2_rn(f2(-numB.x, -numB.y), rcB, __fmul2_rn(TB, gcB));
+      TA = __fmul2_rn(TA, omA);
+      TB = __fmul2_rn(TB, omB);
+      RA = numA;
+      RB = numB;
+      // uncapped participants only (backward.py:64,72): a == raw exactly
+      // for them; a non-participant with raw == 0 has gauss == 0
+      const float2 ldA = f2(aA.x == rawA.x ? dLA.x : 0.f, aA.y == rawA.y ? dLA.y : 0.f);
+      const float2 ldB = f2(aB.x == rawB.x ? dLB.x : 0.f, aB.y == rawB.y ? dLB.y : 0.f);
+      const float2 gqA = __fmul2_rn(ldA, alA), gqB = __fmul2_rn(ldB, alB);
+      // region sums of this lane's four pixels, added to the incoming sums
+      const float2 hx = __ffma2_rn(gqB, bc(dx1), __fmul2_rn(gqA, bc(dx0)));  // per row: gq dx
+      const float2 gs = __fadd2_rn(gqA, gqB);                                // per row: gq
+      const float2 go = __ffma2_rn(ldB, gaB, __fmul2_rn(ldA, gaA));
+      const float2 wr = __ffma2_rn(wB, grB, __fmul2_rn(wA, grA));
+      const float2 wg = __ffma2_rn(wB, ggB, __fmul2_rn(wA, ggA));
+      const float2 wbl = __ffma2_rn(wB, gbB, __fmul2_rn(wA, gbA));
+      s_mx = fmaf(i_mx, keep, hx.x + hx.y);
+      s_b = fmaf(hx.x, dy.x, fmaf(hx.y, dy.y, i_b * keep));
+      s_my = fmaf(gs.x, dy.x, fmaf(gs.y, dy.y, i_my * keep));
+      s_c = fmaf(gs.x, dyy.x, fmaf(gs.y, dyy.y, i_c * keep));
+      s_a = fmaf(dxx0, gqA.x + gqA.y, fmaf(dxx1, gqB.x + gqB.y, i_a * keep));
+      s_o = fmaf(i_o, keep, go.x + go.y);
+      s_r = fmaf(i_r, keep, wr.x + wr.y);
+      s_g = fmaf(i_g, keep, wg.x + wg.y);
+      s_bl = fmaf(i_bl, keep, wbl.x + wbl.y);
+      if (kDepth) {
+        const float2 wd = __ffma2_rn(wB, gdB, __fmul2_rn(wA, gdA));
+        s_d = fmaf(i_d, keep, wd.x + wd.y);
+      }
+      if (j == 15) {  // entry t - 15 is complete: park its sums
+        const int o = (t - 15) & (kOut - 1);
+        oa[o] = make_float4(s_mx, s_my, s_a, s_b);
+        ob[o] = make_float4(s_c, s_o, s_r, s_g);
+        oc[o] = make_float2(s_bl, s_d);
+      }
+    };
+    // merge entry e's region sums (one lane per entry; backward.py:214-222)
+    const float ms = 2.0f / kQScale;
+    auto flush = [&](int e) {
+      if (e < 0 || e >= L) return;
+      const float4 A = oa[e & (kOut - 1)], B = ob[e & (kOut - 1)];
+      const float2 Cc = oc[e & (kOut - 1)];
+      if (!((B.y != 0.f) | (B.z != 0.f) | (B.w != 0.f) | (Cc.x != 0.f) | (Cc.y != 0.f) |
+            (A.z != 0.f)))
+        return;
+      const int slot = e & (kRing - 1);
+      const float4 sa = ra[slot];
+      const float cc = __fmul_rn(rb[slot].x, kQScale);
+      const float ca = __fmul_rn(sa.z, kQScale), hb = __fmul_rn(sa.w, kQScale);  // (2b') / 2
+      const int row = pr[slot].y;
+      // sum gq u = a' sum gq dx + b' sum gq dy, likewise v (the conic's rows)
+      const float uu = fmaf(ca, A.x, hb * A.y), vv = fmaf(hb, A.x, cc * A.y);
+      float* dst = grad2d + (long long)row * TSR_GRAD2D_FLOATS;
+      atomicAdd(dst + 0, ms * 0.5f * uu);
+      atomicAdd(dst + 1, ms * 0.5f * vv);
+      atomicAdd(dst + 2, -0.5f * A.z);
+      atomicAdd(dst + 3, -A.w);
+      atomicAdd(dst + 4, -0.5f * B.x);
+      atomicAdd(dst + 5, B.y);
+      atomicAdd(dst + 6, B.z);
+      atomicAdd(dst + 7, B.w);
+      atomicAdd(dst + 8, Cc.x);
+      if (kDepth) atomicAdd(dst + 9, Cc.y);
+    };
+
+    auto load = [&](float4& A, float4& B, int& pos, int t) {
+      const int slot = (t - j) & (kRing - 1);
+      A = ra[slot];
+      B = rb[slot];
+      pos = pr[slot].x;
+    };
+    const int rounds = (Lmax + 15 + 15) >> 4;
+    cp_async_wait_all();
+    __syncwarp();  // block 0 staged
+    float4 A0, B0, A1, B1;
+    int q0, q1;
+    load(A0, B0, q0, 0);
+    for (int k = 0; k < rounds; ++k) {
+      // block k's records, k + 1's rows, k + 2's positions landed (waited
+      // at the previous round's step 14)
+      stage(16 * (k + 1) + j);
+      fetch_row(16 * (k + 2) + j);
+      fetch_pos(16 * (k + 3) + j);
+      cp_async_commit();
+#pragma unroll 1
+      for (int i = 0; i < 16; i += 2) {
+        const int t = 16 * k + i;
+        if (i == 14) {  // block k + 1 (the next step's lane 0 entry) has landed
+          cp_async_wait_all();
+          __syncwarp();
+        }
+        load(A1, B1, q1, t + 1);
+        step(A0, B0, q0, t);
+        load(A0, B0, q0, t + 2);
+        step(A1, B1, q1, t + 1);
+      }
+      __syncwarp();
+      flush(16 * k - 15 + j);
+    }
+    cp_async_wait_all();  // the last staged block lands before the ring is reused
+  }
+}
+
+// ---- workspace: unit list + count + grab counter
+size_t regions_units_cap(int n_tiles, int64_t p_bound) {
+  return 2 * ((size_t)(p_bound > 0 ? p_bound : 0) / kSeg + (size_t)n_tiles + 1);
+}
+
+}  // namespace
+}  // namespace tsr
+
+using namespace tsr;
+
+extern "C" size_t tsr_render_bwd_regions_workspace(int32_t width, int32_t height, int64_t p_bound) {
+  if (width <= 0 || height <= 0) return 0;
+  return 256 + regions_units_cap(tiles_of(width) * tiles_of(height), p_bound) * 4;
+}
+
+extern "C" size_t tsr_region_list_entries(int32_t width, int32_t height, int64_t p_bound) {
+  (void)width;
+  (void)height;
+  return 4 * (size_t)(p_bound > 0 ? p_bound : 0) + 1;
+}
+
+extern "C" size_t tsr_region_seg_entries(int32_t width, int32_t height, int64_t p_bound) {
+  if (width <= 0 || height <= 0) return 0;
+  return 4 * ((size_t)(p_bound > 0 ? p_bound : 0) / kSeg + (size_t)tiles_of(width) * tiles_of(height) + 1);
+}
+
+extern "C" int tsr_render_bwd_regions(const float* rec, const int32_t* values,
+                                      const int64_t* offsets, int32_t width, int32_t height,
+                                      const float* color, const float* depth,
+                                      const float* final_T, const int32_t* n_considered,
+                                      const float* ckpt, const int64_t* ckpt_base,
+                                      const uint32_t* region_list, const int32_t* region_seg,
+                                      const float* grad_color, const float* grad_depth,
+                                      const float* grad_final_T, float* grad2d,
+                                      unsigned long long* merges, int64_t p_bound, void* workspace,
+                                      size_t workspace_bytes, void* stream) {
+  if (width <= 0 || height <= 0 || !grad_color || !merges || !grad2d || !workspace || !ckpt ||
+      !ckpt_base || !region_list || !region_seg || !offsets)
+    return TSR_E_INVALID;
+  const int tx = tiles_of(width), ty = tiles_of(height), n_tiles = tx * ty;
+  if (n_tiles >= (1 << 16)) return TSR_E_INVALID;
+  if (workspace_bytes < tsr_render_bwd_regions_workspace(width, height, p_bound))
+    return TSR_E_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  char* w = (char*)workspace;
+  int32_t* n_units = (int32_t*)w;
+  int32_t* counter = (int32_t*)(w + 4);
+  uint32_t* units = (uint32_t*)(w + 256);
+  region_plan_kernel<<<1, kPlanThreads, 0, s>>>(offsets, n_tiles, units,
+                                                (long long)regions_units_cap(n_tiles, p_bound),
+                                                n_units, counter);
+  TSR_CHECK_LAUNCH();
+  auto* k = grad_depth ? render_bwd_regions_kernel<true> : render_bwd_regions_kernel<false>;
+  static int per_sm[2] = {0, 0}, sms = 0;
+  int& ps = per_sm[grad_depth ? 1 : 0];
+  if (ps == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k, kRThreads, 0);
+    if (ps < 1) ps = 1;
+  }
+  k<<<sms * ps, kRThreads, 0, s>>>((const float4*)rec, values, offsets, width, height, tx, color,
+                                   depth, final_T, n_considered, ckpt, ckpt_base, region_list,
+                                   region_seg, grad_color, grad_depth, grad_final_T, grad2d, merges,
+                                   units, n_units, counter);
+  TSR_CHECK_LAUNCH();
+  return TSR_OK;
+}

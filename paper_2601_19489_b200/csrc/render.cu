@@ -119,6 +119,20 @@ __device__ __forceinline__ void blend_pair(const float4 g, const float4 c, const
   s.ncons1 = live1 ? pos + 1 : s.ncons1;
 }
 
+// Region lists for the region-culled backward (kCkpt 3, backward_regions.cu):
+// warp w's 8x8 block is region w of the tile; every list position whose splat
+// passes the block test is appended to the region's list (in list order, so
+// the list is a superset of the positions that blend in the block, cut at the
+// chunk where the block's last pixel died).  Region r of tile t stores its
+// positions at list[4 start_t + r n_t ...]; seg[4 (segbase_t + s - 1) + r]
+// holds the number of entries with position < kSeg s for s = 1..ceil(n/kSeg)
+// (segbase_t = (start_t >> 10) + t: floor((O + n) / kSeg) - floor(O / kSeg)
+// + 1 >= ceil(n / kSeg), so the tiles' segment slots never overlap).
+struct RegionArgs {
+  uint32_t* list;
+  int32_t* seg;
+};
+
 // 4 warps; warp w owns the 8x8 block (bx, by) = (w & 1, w >> 1) of the tile;
 // lane l owns pixels (8 bx + (l & 7), 8 by + (l >> 3)) and the one 4 rows below.
 constexpr int kFwdThreads = 128;
@@ -126,7 +140,9 @@ constexpr int kBatch = 256;
 
 // kCkpt: 0 no checkpoints, 1 every record (the reference's checkpoints), 2
 // only the odd records -- the ones K4 reads (supergroup starts, 64 positions
-// apart): half the checkpoint traffic in the training step.
+// apart): half the checkpoint traffic in the training step; 3 only the
+// records at segment starts (every kSeg positions) plus the region lists the
+// region-culled backward reads.
 template <int kCkpt, int kScore>
 __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
     const float4* __restrict__ rec, const int32_t* __restrict__ values,
@@ -134,7 +150,8 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
     float bg_g, float bg_b, float* __restrict__ out_color, float* __restrict__ out_depth,
     float* __restrict__ out_T, int32_t* __restrict__ out_ncontrib,
     int32_t* __restrict__ out_ncons, float* __restrict__ ckpt,
-    const int64_t* __restrict__ ckpt_base, ScoreArgs sc, const int32_t* __restrict__ order) {
+    const int64_t* __restrict__ ckpt_base, ScoreArgs sc, const int32_t* __restrict__ order,
+    RegionArgs rg = RegionArgs{}) {
   // per staged splat: [0] mx, my, opacity, depth  [1] prescaled conic a',
   // 2b', c'  [2] r, g, b, depth -- one base address per list entry
   __shared__ float4 s_spl[kBatch][3];
@@ -170,6 +187,10 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
   long long sc_cursor = 0;  // kScore 1/2: this warp's contributions so far
   if (kScore == 2) sc_cursor = sc.warp_base[tile * 4 + warp];
   const long long pix0 = (long long)y0 * width + x, pix1 = (long long)y1 * width + x;
+  uint32_t* rl = nullptr;
+  int r_count = 0, s_next = 1;
+  const long long segbase = (start >> kSegShift) + tile;
+  if (kCkpt == 3) rl = rg.list + 4 * start + (long long)warp * n;
   bool m0 = false, m1 = false;
   if (kScore == 3) {
     m0 = in0 && sc.mask[pix0];
@@ -201,6 +222,10 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
       if (!__any_sync(0xffffffffu, s.alive0() || s.alive1())) break;  // warp-level early exit
       const int cend = min(kGroup, cnt - c0);
       const int pos0 = b0 + c0;
+      if (kCkpt == 3 && pos0 > 0 && (pos0 & (kSeg - 1)) == 0) {  // segment boundary
+        if (lane == 0) rg.seg[4 * (segbase + s_next - 1) + warp] = r_count;
+        ++s_next;
+      }
       // lane j tests splat c0 + j against this warp's 8x8 block
       bool hit = false;
       if (lane < cend) {
@@ -208,6 +233,10 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
         hit = strip_hit(g.x, g.y, rw.x, rw.y, rw.z, rw.w, sx0, sx0 + 7.f, sy0, sy0 + 7.f);
       }
       unsigned mask = __ballot_sync(0xffffffffu, hit);
+      if (kCkpt == 3) {
+        if (hit) rl[r_count + __popc(mask & lt_mask)] = (uint32_t)(pos0 + lane);
+        r_count += __popc(mask);
+      }
       while (mask) {
         const int j = __ffs(mask) - 1;
         mask &= mask - 1u;
@@ -237,7 +266,9 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
           }
         }
       }
-      if (kCkpt && cend == kGroup && (kCkpt == 1 || ((pos0 >> 5) & 1))) {
+      if (kCkpt && cend == kGroup &&
+          (kCkpt == 1 || (kCkpt == 2 && ((pos0 >> 5) & 1)) ||
+           (kCkpt == 3 && ((pos0 + kGroup) & (kSeg - 1)) == 0))) {
         // state after list position pos0+31 -> record (pos0+32)/32 - 1, for
         // each pixel that consumed that position (still alive, or died there)
         float* dst = ck0 + (long long)(pos0 >> 5) * (5 * kTilePixels);
@@ -260,6 +291,9 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
     }
   }
   if (kScore == 1 && lane == 0) sc.warp_counts[tile * 4 + warp] = sc_cursor;
+  if (kCkpt == 3 && lane == 0)  // the remaining segment ends (after an early exit)
+    for (const int nseg = (n + kSeg - 1) >> kSegShift; s_next <= nseg; ++s_next)
+      rg.seg[4 * (segbase + s_next - 1) + warp] = r_count;
   // a pixel that never terminated considered the whole list (skipped
   // entries included); a terminated one stopped at its death position
   if (s.alive0()) s.ncons0 = n;
@@ -383,7 +417,34 @@ extern "C" int tsr_render_fwd_ordered(const float* rec, const int32_t* values,
   k<<<n_tiles, kFwdThreads, 0, s>>>((const float4*)rec, values, offsets, width, height, tx,
                                     background_host[0], background_host[1], background_host[2],
                                     out_color, out_depth, out_final_T, out_n_contrib,
-                                    out_n_considered, ckpt, ckpt_base, none, tile_order);
+                                    out_n_considered, ckpt, ckpt_base, none, tile_order, RegionArgs{});
+  TSR_CHECK_LAUNCH();
+  return TSR_OK;
+}
+
+// K3 for the region-culled backward: checkpoint records at segment starts
+// only, plus the per-(tile, 8x8 region) lists of list positions that pass the
+// region's block test (RegionArgs above).  region_list holds 4 x P entries,
+// region_seg 4 x (P / kSeg + n_tiles + 1).
+extern "C" int tsr_render_fwd_regions(const float* rec, const int32_t* values,
+                                      const int64_t* offsets, int32_t width, int32_t height,
+                                      const float* background_host, float* out_color,
+                                      float* out_depth, float* out_final_T,
+                                      int32_t* out_n_contrib, int32_t* out_n_considered,
+                                      float* ckpt, const int64_t* ckpt_base,
+                                      uint32_t* region_list, int32_t* region_seg,
+                                      const int32_t* tile_order, void* stream) {
+  if (width <= 0 || height <= 0 || !background_host || !ckpt || !ckpt_base || !region_list ||
+      !region_seg)
+    return TSR_E_INVALID;
+  const int tx = tiles_of(width), ty = tiles_of(height);
+  const int n_tiles = tx * ty;
+  cudaStream_t s = (cudaStream_t)stream;
+  const ScoreArgs none{};
+  render_fwd_kernel<3, 0><<<n_tiles, kFwdThreads, 0, s>>>(
+      (const float4*)rec, values, offsets, width, height, tx, background_host[0],
+      background_host[1], background_host[2], out_color, out_depth, out_final_T, out_n_contrib,
+      out_n_considered, ckpt, ckpt_base, none, tile_order, RegionArgs{region_list, region_seg});
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }
@@ -405,7 +466,7 @@ extern "C" int tsr_render_fwd_ex(const float* rec, const int32_t* values, const 
   k<<<n_tiles, kFwdThreads, 0, s>>>((const float4*)rec, values, offsets, width, height, tx,
                                     background_host[0], background_host[1], background_host[2],
                                     out_color, out_depth, out_final_T, out_n_contrib,
-                                    out_n_considered, ckpt, ckpt_base, none, nullptr);
+                                    out_n_considered, ckpt, ckpt_base, none, nullptr, RegionArgs{});
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }
@@ -443,7 +504,7 @@ extern "C" int tsr_render_score(const float* rec, const int32_t* values, const i
   k<<<n_tiles, kFwdThreads, 0, s>>>((const float4*)rec, values, offsets, width, height, tx,
                                     background_host[0], background_host[1], background_host[2],
                                     out_color, out_depth, out_final_T, out_n_contrib,
-                                    out_n_considered, nullptr, nullptr, sc, nullptr);
+                                    out_n_considered, nullptr, nullptr, sc, nullptr, RegionArgs{});
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }

@@ -20,6 +20,10 @@ namespace tsr {
 constexpr int kTile = 16;
 constexpr int kTilePixels = kTile * kTile;
 constexpr int kGroup = 32;  // CHECKPOINT_INTERVAL (forward.py:28)
+// region-culled backward segments: list positions per work unit (a multiple
+// of 2 kGroup; K3 writes a checkpoint record at every segment start)
+constexpr int kSegShift = 10;
+constexpr int kSeg = 1 << kSegShift;
 constexpr float kAlphaCap = 0.99f;                 // forward.py:25
 constexpr float kMinAlpha = 1.0f / 255.0f;         // forward.py:26
 constexpr float kTTerminate = 1e-4f;               // forward.py:27

@@ -157,6 +157,36 @@ def render_raw(rec, values, offsets, ckpt_base, width: int, height: int, backgro
         _lib.ptr(tile_order), _lib.stream_handle()), "tsr_render_fwd_ordered")
 
 
+class RegionLists:
+    """Per-(tile, 8x8 region) list positions K3 writes for the region-culled
+    K4 (tsr_render_fwd_regions): 4 x p_bound uint32 entries plus the
+    segment-boundary offsets; sized for a pair bound, reused across steps."""
+
+    def __init__(self, width: int, height: int, p_bound: int):
+        lib = _lib.load()
+        dev = _device()
+        self.list = torch.empty(int(lib.tsr_region_list_entries(width, height, p_bound)),
+                                dtype=torch.int32, device=dev)
+        self.seg = torch.empty(int(lib.tsr_region_seg_entries(width, height, p_bound)),
+                               dtype=torch.int32, device=dev)
+        self.shape = (width, height, p_bound)
+
+
+def render_regions_raw(rec, values, offsets, ckpt_base, width: int, height: int, background,
+                       out: RenderTargets, regions: RegionLists, tile_order=None) -> None:
+    """K3 for the region-culled backward: checkpoint records at segment
+    starts only plus the region lists (no host synchronisation)."""
+    lib = _lib.load()
+    bg = np.asarray(background, dtype=np.float64).reshape(3)
+    bg_host = (_lib.c_f32 * 3)(*[float(v) for v in bg])
+    _lib.check(lib.tsr_render_fwd_regions(
+        rec.data_ptr(), _lib.ptr(values), offsets.data_ptr(), width, height, bg_host,
+        out.color.data_ptr(), out.depth.data_ptr(), out.final_T.data_ptr(),
+        out.n_contrib.data_ptr(), out.n_considered.data_ptr(), out.ckpt.data_ptr(),
+        ckpt_base.data_ptr(), regions.list.data_ptr(), regions.seg.data_ptr(),
+        _lib.ptr(tile_order), _lib.stream_handle()), "tsr_render_fwd_regions")
+
+
 # per-tile kernel launch order in the training step: "heavy" (heavy tiles
 # first, tsr_tile_order) or "raster"
 TILE_ORDER = os.environ.get("TSR_TILE_ORDER", "heavy")

@@ -257,6 +257,9 @@ class TrainStep:
         self.loss_ws = losses.PhotometricWorkspace()
         from .backward import BackwardWorkspace
         self.bwd_ws = BackwardWorkspace()
+        from .backward import RegionWorkspace
+        self.reg_ws = RegionWorkspace()
+        self.regions = None
         self._order_buf = None
         self.tile_order = None
         self.dc_ws = losses.DepthChainWorkspace()
@@ -295,6 +298,10 @@ class TrainStep:
         tiles = camera.tiles_x * camera.tiles_y
         self.index = IndexBuffers(len(self.gset), p_cap, tiles, det=self.deterministic)
         self.targets = RenderTargets(camera.height, camera.width, p_cap // 32 + tiles + 1)
+        self.regions = None
+        if self._regions_on():  # K3's region lists for the region-culled K4
+            from .forward import RegionLists
+            self.regions = RegionLists(camera.width, camera.height, p_cap)
         self.hw = (camera.height, camera.width)
         self.grad_color = torch.empty((camera.height, camera.width, 3), dtype=torch.float32,
                                       device=self.grad2d.device)
@@ -393,11 +400,24 @@ class TrainStep:
                                                self.tile_order.data_ptr(), _lib.stream_handle()),
                        "tsr_tile_order")
         self._mark(timer, "binning")
-        render_raw(s.rec, idx.values, idx.offsets, idx.ckpt_base, camera.width, camera.height,
-                   self.cfg.background, out, ckpt_stride=2,  # only the records K4 reads
-                   tile_order=self.tile_order)
+        if self.regions is not None:
+            from .forward import render_regions_raw
+            render_regions_raw(s.rec, idx.values, idx.offsets, idx.ckpt_base, camera.width,
+                               camera.height, self.cfg.background, out, self.regions,
+                               tile_order=self.tile_order)
+        else:
+            render_raw(s.rec, idx.values, idx.offsets, idx.ckpt_base, camera.width,
+                       camera.height, self.cfg.background, out,
+                       ckpt_stride=2,  # only the records K4 reads
+                       tile_order=self.tile_order)
         self._mark(timer, "render")
         return batch
+
+    def _regions_on(self) -> bool:
+        """The training step runs the region-culled K3/K4 pair (the
+        deterministic merge keeps the per-tile K4 and its per-pair slots)."""
+        from .backward import K4_FORM
+        return K4_FORM == "regions" and not self.deterministic and not self._can_fuse_update()
 
     def _can_fuse_update(self) -> bool:
         from .backward import K4_FORM
@@ -436,7 +456,7 @@ class TrainStep:
             det = (self.merges.data_ptr(), self.slots.data_ptr(), self.processed.data_ptr(),
                    *(t.data_ptr() for t in idx.det), idx.keys.data_ptr(), self.grad2d.shape[0],
                    self.scratch.totals.data_ptr(), self.grad2d.data_ptr())
-            if K4_FORM == "tiles":
+            if K4_FORM in ("tiles", "regions"):
                 _lib.check(self.lib.tsr_render_bwd_det(*common, *det, _lib.stream_handle()),
                            "tsr_render_bwd_det")
             else:
@@ -461,7 +481,12 @@ class TrainStep:
                 self.gated_steps.data_ptr(), e.data_ptr(), _lib.stream_handle()),
                 "tsr_render_bwd_adam")
             self._updated = True
-        elif K4_FORM == "tiles":
+        elif self.regions is not None:
+            from .backward import backward_regions_raw
+            backward_regions_raw(batch.rec, idx.values, idx.offsets, camera.width, camera.height,
+                                 out, idx.ckpt_base, self.regions, grad_color, gd, gt,
+                                 self.grad2d, self.merges, self.reg_ws, idx.p_cap)
+        elif K4_FORM in ("tiles", "regions"):
             _lib.check(self.lib.tsr_render_bwd_ordered(
                 *common, self.grad2d.data_ptr(), self.merges.data_ptr(),
                 _lib.ptr(self.tile_order), _lib.stream_handle()), "tsr_render_bwd_ordered")
@@ -596,7 +621,9 @@ class TrainStep:
         from .backward import K4_FORM
         from .forward import TILE_ORDER
         return (2 + 1 + (1 if TILE_ORDER == "heavy" else 0) + 1 + 2 + 1
-                + (2 if K4_FORM == "units" else 0) + 1 + (1 if self.deterministic else 0))
+                + (2 if K4_FORM == "units" else 0)
+                + (1 if self.regions is not None else 0)  # the region unit plan
+                + 1 + (1 if self.deterministic else 0))
 
     def last_view(self):
         """(batch, TileIndex, RenderBuffers) views of the last step (synchronises)."""

@@ -1,0 +1,140 @@
+"""Region-culled K3 + K4 (render.cu kCkpt 3, backward_regions.cu) -- the
+training step's pair -- through the C-ABI, against the oracle
+(backward_per_gaussian, backward.py:137-223) and against the per-tile K4.
+
+Bars: the region render's outputs are the reference-checkpoint render's bit
+for bit (the culling only skips exact zeros); Grad2D max|x - y| / max|y| <=
+1e-4 per field against the oracle (the reference's metric,
+test_backward.py:34-39); merges equal the reference's count.  Scenes cover
+one segment per tile (C1), many segments per tile (a crowded 64x64 frame:
+every tile's list is several 1024-position segments long), the depth and
+final-T channels, and frames whose size is not a multiple of the tile."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import host_batch, host_index, np64, rel_err
+from oracle import raster as O
+
+pytestmark = pytest.mark.gpu
+
+GRAD_RTOL = 1e-4
+FIELDS = ("d_means2d", "d_conics", "d_opacities", "d_colors", "d_depths")
+
+
+def regions_pass(vr, grad_color, grad_depth=None, grad_final_T=None, background=(0.0, 0.0, 0.0)):
+    """K3 (region mode) + K4r on a render_view's batch and index."""
+    import paper_2601_19489_b200 as ts
+    from paper_2601_19489_b200.backward import RegionWorkspace, backward_regions_raw
+    from paper_2601_19489_b200.forward import RegionLists, RenderTargets, render_regions_raw
+    b, t = vr.batch, vr.tiles
+    p = max(t.n_pairs, 1)
+    tgt = RenderTargets(b.height, b.width, p // 32 + t.tiles_x * t.tiles_y + 1)
+    reg = RegionLists(b.width, b.height, p)
+    render_regions_raw(b.rec, t.values if t.n_pairs else None, t.offsets, t.ckpt_base, b.width,
+                       b.height, background, tgt, reg)
+    out = torch.zeros((len(b), 10), dtype=torch.float32, device="cuda")
+    merges = torch.zeros(1, dtype=torch.int64, device="cuda")
+    f32 = lambda a: None if a is None else torch.as_tensor(a, dtype=torch.float32, device="cuda")
+    backward_regions_raw(b.rec, t.values if t.n_pairs else None, t.offsets, b.width, b.height,
+                         tgt, t.ckpt_base, reg, f32(grad_color), f32(grad_depth),
+                         f32(grad_final_T), out, merges, RegionWorkspace(), p)
+    torch.cuda.synchronize()
+    return tgt, reg, ts.Grad2D(out, int(merges.item()))
+
+
+def _scene(n, w, h, seed=0, clustered=False, cluster_opacity=None):
+    import paper_2601_19489_b200 as ts
+    params, cam, gt = O.make_scene(n, w, h, seed=seed, clustered=clustered,
+                                   cluster_opacity=cluster_opacity)
+    gset = ts.GaussianSet(**params)
+    camera = ts.Camera(cam["fx"], cam["fy"], cam["cx"], cam["cy"], w, h, cam["R"], cam["t"])
+    vr = ts.render_view(gset, camera, ts.TrainConfig())
+    return ts, vr, gt
+
+
+def _vs_oracle(vr, gcol, gdep=None, gT=None):
+    hb, hi = host_batch(vr.batch), host_index(vr.tiles)
+    colors = np64(vr.colors)
+    ob = O.render(hb, hi, colors, np.zeros(3))
+    tgt, reg, g2 = regions_pass(vr, gcol, gdep, gT)
+    # the region render is the reference-checkpoint render, bit for bit
+    for k in ("color", "depth", "final_T", "n_contrib", "n_considered"):
+        assert torch.equal(getattr(tgt, k), getattr(vr.buffers, k)), k
+    og = O.backward_per_gaussian(ob, hb, hi, colors, gcol, gdep, gT)
+    errs = {k: rel_err(np64(getattr(g2, k)), og[k]) for k in FIELDS
+            if np.abs(og[k]).max(initial=0.0) > 0}
+    for k, e in errs.items():
+        assert e < GRAD_RTOL, (k, errs)
+    assert g2.merges == og["merges"]
+    return tgt, reg, g2, errs
+
+
+@pytest.mark.parametrize("n,w,h", [(10_000, 256, 256), (3_000, 200, 120), (20_000, 64, 64)])
+def test_regions_backward_vs_oracle(n, w, h):
+    ts, vr, gt = _scene(n, w, h)
+    assert int(torch.diff(vr.tiles.offsets).max()) > 0
+    rng = np.random.default_rng(n)
+    gcol = rng.normal(0, 1e-3, (h, w, 3))
+    _vs_oracle(vr, gcol)
+
+
+def test_regions_many_segments_per_tile():
+    """A low-opacity cluster (C3-lo style): pixels stay alive for thousands
+    of list positions, so their tiles' work spans several segments (units),
+    each starting from K3's segment-start checkpoint."""
+    ts, vr, gt = _scene(30_000, 64, 64, seed=3, clustered=True, cluster_opacity=(0.004, 0.02))
+    assert int(vr.buffers.n_considered.max()) > 3 * 1024, int(vr.buffers.n_considered.max())
+    rng = np.random.default_rng(7)
+    _vs_oracle(vr, rng.normal(0, 1e-3, (64, 64, 3)))
+
+
+def test_regions_depth_and_final_T_channels():
+    ts, vr, gt = _scene(5_000, 160, 96, seed=5)
+    rng = np.random.default_rng(11)
+    _vs_oracle(vr, rng.normal(0, 1e-3, (96, 160, 3)), rng.normal(0, 1e-3, (96, 160)),
+               rng.normal(0, 1e-3, (96, 160)))
+
+
+def test_regions_zero_upstream_half_tile():
+    """Upstream zero outside a band of rows: row pairs with no upstream are
+    skipped (exact zeros) and merges still count every pair of a tile whose
+    upstream is not all zero."""
+    ts, vr, gt = _scene(8_000, 128, 128, seed=2)
+    g = np.zeros((128, 128, 3))
+    g[4:6] = 1e-3  # only the top row pair of the first tile row
+    _vs_oracle(vr, g)
+
+
+def test_region_lists_cover_every_blend():
+    """Each region list is increasing, within [0, n), and holds every list
+    position that blends at a pixel of the region (oracle participation)."""
+    ts, vr, gt = _scene(4_000, 96, 64, seed=9)
+    hb, hi = host_batch(vr.batch), host_index(vr.tiles)
+    tgt, reg, _ = regions_pass(vr, np.zeros((64, 96, 3)))
+    lst, seg = reg.list.cpu().numpy(), reg.seg.cpu().numpy()
+    off = hi["offsets"]
+    for tile in range(hi["tiles_x"] * hi["tiles_y"]):
+        lo, n = int(off[tile]), int(off[tile + 1] - off[tile])
+        if n == 0:
+            continue
+        nseg = -(-n // 1024)
+        ty, tx = divmod(tile, hi["tiles_x"])
+        for r in range(4):
+            total = seg[4 * ((lo >> 10) + tile + nseg - 1) + r]
+            ent = lst[4 * lo + r * n: 4 * lo + r * n + total].astype(np.int64)
+            assert np.all(np.diff(ent) > 0) and (total == 0 or (ent[0] >= 0 and ent[-1] < n))
+            x0, y0 = tx * 16 + 8 * (r & 1), ty * 16 + 8 * (r >> 1)
+            x1, y1 = min(x0 + 8, 96), min(y0 + 8, 64)
+            if x0 >= 96 or y0 >= 64:
+                continue
+            gy, gx = np.mgrid[y0:y1, x0:x1]
+            px, py = gx.reshape(-1) + 0.5, gy.reshape(-1) + 0.5
+            nc = np64(vr.buffers.n_considered)[y0:y1, x0:x1].reshape(-1)
+            need = []
+            for k in range(n):
+                al = O._alpha(hb, hi["values"][lo + k], px, py)[0]
+                if np.any((al >= 1 / 255) & (k < nc)):
+                    need.append(k)
+            assert set(need) <= set(ent.tolist()), (tile, r)

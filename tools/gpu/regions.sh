@@ -1,0 +1,10 @@
+#!/bin/bash
+# region-culled K4: parity tests + C2 bench (+ optional ncu)
+mkdir -p gpurun_out
+make -j8 all > gpurun_out/make.log 2>&1 || { echo make failed; exit 1; }
+timeout 900 python -m pytest tests/test_gpu_regions.py -q -x --timeout=600 > gpurun_out/pytest_regions.log 2>&1; echo pytest=$? > gpurun_out/status_regions.txt
+timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_regions.log 2>&1
+TSR_K4=tiles timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_tiles.log 2>&1
+if [ "$1" = "ncu" ]; then
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:"render_bwd_regions|render_fwd" -s 2 -c 2 -o gpurun_out/regions_full python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_regions.log 2>&1
+fi
