@@ -28,3 +28,8 @@ trace: build/libtilesplat_b200_trace.so
 build/libtilesplat_b200_trace.so: $(SRCS) $(SRC_DIR)/tsr_common.cuh include/tilesplat_b200.h
 	@mkdir -p build
 	$(NVCC) -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC -cudart shared -Iinclude -DTSR_K2_TRACE -shared -o $@ $(SRCS)
+
+# experiment variants: make variant V=name VFLAGS="-DFOO=1" -> build/libtilesplat_b200_<name>.so
+variant:
+	@mkdir -p build
+	$(NVCC) -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC -cudart shared -Iinclude $(VFLAGS) -shared -o build/libtilesplat_b200_$(V).so $(SRCS)

@@ -50,9 +50,18 @@ namespace tsr {
 namespace {
 
 constexpr int kRWarps = 4;
+#ifndef TSR_K4R_CTAS
+#define TSR_K4R_CTAS 4
+#endif
+#ifndef TSR_K4R_PREFETCH
+#define TSR_K4R_PREFETCH 0
+#endif
+#ifndef TSR_K4R_EXIT
+#define TSR_K4R_EXIT 1
+#endif
 constexpr int kRThreads = 32 * kRWarps;
 constexpr int kRing = 64;    // staged region-list entries per half-warp (4 blocks of 16)
-constexpr int kOut = 32;     // finished-entry sums per half-warp (2 blocks of 16)
+constexpr int kOut = 16;     // finished-entry sums per half-warp (one round: flushed at its end)
 constexpr int kHeavyN = 768; // units of tiles with longer lists are queued first
 
 __device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
@@ -167,7 +176,7 @@ __device__ __forceinline__ bool quad_nz(const float* __restrict__ grad_color,
 }
 
 template <bool kDepth>
-__global__ void __launch_bounds__(kRThreads, 4) render_bwd_regions_kernel(
+__global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_kernel(
     const float4* __restrict__ rec, const int32_t* __restrict__ values,
     const int64_t* __restrict__ offsets, int width, int height, int tiles_x,
     const float* __restrict__ color, const float* __restrict__ depth,
@@ -208,12 +217,28 @@ __global__ void __launch_bounds__(kRThreads, 4) render_bwd_regions_kernel(
   const float keep = j != 0 ? 1.f : 0.f;  // lane 0 of a half starts each entry's sums
   const int n_units = *n_units_dev;
 
+  // the next unit is grabbed (and its code loaded) one unit ahead, so its
+  // descriptor loads overlap the current unit's pipeline
+#if TSR_K4R_PREFETCH
+  int u_next = 0;
+  if (lane == 0) u_next = atomicAdd(counter, 1);
+  u_next = __shfl_sync(0xffffffffu, u_next, 0);
+  uint32_t code_next = u_next < n_units ? units[u_next] : 0u;
+  for (;;) {
+    const int u = u_next;
+    if (u >= n_units) break;
+    const uint32_t code = code_next;
+    if (lane == 0) u_next = atomicAdd(counter, 1);
+    u_next = __shfl_sync(0xffffffffu, u_next, 0);
+    code_next = u_next < n_units ? units[u_next] : 0u;
+#else
   for (;;) {
     int u = 0;
     if (lane == 0) u = atomicAdd(counter, 1);
     u = __shfl_sync(0xffffffffu, u, 0);
     if (u >= n_units) break;
     const uint32_t code = units[u];
+#endif
     const int tile = (int)(code >> 16), seg = (int)((code >> 1) & 0x7fffu), rp = (int)(code & 1u);
     const long long start = offsets[tile];
     const int n = (int)(offsets[tile + 1] - start);
@@ -461,7 +486,8 @@ __global__ void __launch_bounds__(kRThreads, 4) render_bwd_regions_kernel(
       B = rb[slot];
       pos = pr[slot].x;
     };
-    const int rounds = (Lmax + 15 + 15) >> 4;
+    const int steps = Lmax + 15;  // entry Lmax - 1 leaves lane 15 at step Lmax + 14
+    const int rounds = (steps + 15) >> 4;
     cp_async_wait_all();
     __syncwarp();  // block 0 staged
     float4 A0, B0, A1, B1;
@@ -477,6 +503,7 @@ __global__ void __launch_bounds__(kRThreads, 4) render_bwd_regions_kernel(
 #pragma unroll 1
       for (int i = 0; i < 16; i += 2) {
         const int t = 16 * k + i;
+        if (TSR_K4R_EXIT && t >= steps) break;  // the last round stops at its last step
         if (i == 14) {  // block k + 1 (the next step's lane 0 entry) has landed
           cp_async_wait_all();
           __syncwarp();
