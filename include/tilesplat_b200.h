@@ -208,31 +208,34 @@ size_t tsr_render_bwd_workspace(int32_t width, int32_t height, int64_t p_bound);
  * backward_per_gaussian, backward.py:137-223).  tsr_render_fwd_regions is K3
  * writing checkpoint records only at segment starts (every 1024 list
  * positions) plus, per (tile, 8x8 region), the list positions whose splat
- * passes the region's conservative alpha >= 1/255 test:
- * region_list holds tsr_region_list_entries(...) uint32 entries,
- * region_seg tsr_region_seg_entries(...) int32 entries.
+ * passes the region's conservative alpha >= 1/255 test, and the work units of
+ * the backward (tile, row pair, segment), queued as the tiles finish:
+ *   region_list   tsr_region_list_entries(...) uint32
+ *   region_seg    tsr_region_seg_entries(...) int32
+ *   region_units  tsr_region_unit_entries(...) uint32
+ *   region_ctl    2 int32 (unit count, grab counter; zeroed by the call).
  * tsr_render_bwd_regions streams each region's list past its pixels (one
- * 16-lane systolic pipeline per region, units of (tile, row pair, segment)
- * from a global queue) and merges the same Grad2D sums with atomics; it needs
- * a workspace of tsr_render_bwd_regions_workspace(...) bytes.  p_bound >= the
- * pair count (a capacity is fine). */
+ * 16-lane systolic pipeline per region, units drawn from the queue) and
+ * merges the same Grad2D sums with atomics.  p_bound >= the pair count (a
+ * capacity is fine). */
 int tsr_render_fwd_regions(const float* rec, const int32_t* values, const int64_t* offsets,
                            int32_t width, int32_t height, const float* background_host,
                            float* out_color, float* out_depth, float* out_final_T,
                            int32_t* out_n_contrib, int32_t* out_n_considered, float* ckpt,
                            const int64_t* ckpt_base, uint32_t* region_list, int32_t* region_seg,
+                           uint32_t* region_units, int32_t* region_ctl,
                            const int32_t* tile_order, void* stream);
 size_t tsr_region_list_entries(int32_t width, int32_t height, int64_t p_bound);
 size_t tsr_region_seg_entries(int32_t width, int32_t height, int64_t p_bound);
-size_t tsr_render_bwd_regions_workspace(int32_t width, int32_t height, int64_t p_bound);
+size_t tsr_region_unit_entries(int32_t width, int32_t height, int64_t p_bound);
 int tsr_render_bwd_regions(const float* rec, const int32_t* values, const int64_t* offsets,
                            int32_t width, int32_t height, const float* color, const float* depth,
                            const float* final_T, const int32_t* n_considered, const float* ckpt,
                            const int64_t* ckpt_base, const uint32_t* region_list,
-                           const int32_t* region_seg, const float* grad_color,
+                           const int32_t* region_seg, const uint32_t* region_units,
+                           int32_t* region_ctl, const float* grad_color,
                            const float* grad_depth, const float* grad_final_T, float* grad2d,
-                           unsigned long long* merges, int64_t p_bound, void* workspace,
-                           size_t workspace_bytes, void* stream);
+                           unsigned long long* merges, void* stream);
 int tsr_render_bwd_ws(const float* rec, const int32_t* values, const int64_t* offsets,
                       int32_t width, int32_t height, const float* color, const float* depth,
                       const float* final_T, const int32_t* n_considered, const float* ckpt,

@@ -81,36 +81,20 @@ class Grad2D:
 K4_FORM = os.environ.get("TSR_K4", "regions")
 
 
-class RegionWorkspace:
-    """Device scratch of the region-culled K4 (unit plan + queue)."""
-
-    def __init__(self):
-        self.buf = None
-        self.key = None
-
-    def get(self, width: int, height: int, p_bound: int) -> torch.Tensor:
-        if self.buf is None or self.key[0] != (width, height) or self.key[1] < p_bound:
-            n = int(_lib.load().tsr_render_bwd_regions_workspace(width, height, p_bound))
-            self.buf = torch.empty(n, dtype=torch.uint8, device=_device())
-            self.key = ((width, height), p_bound)
-        return self.buf
-
-
 def backward_regions_raw(rec, values, offsets, width: int, height: int, targets, ckpt_base,
                          regions, grad_color, grad_depth, grad_final_T, out: torch.Tensor,
-                         merges: torch.Tensor, workspace: RegionWorkspace,
-                         p_bound: int) -> None:
-    """Region-culled K4 (backward.py:137-223) over K3's region lists
-    (render_regions_raw); merges into `out` (zeroed by the caller)."""
+                         merges: torch.Tensor) -> None:
+    """Region-culled K4 (backward.py:137-223) over K3's region lists and
+    work units (render_regions_raw); merges into `out` (zeroed by the caller)."""
     lib = _lib.load()
-    ws = workspace.get(width, height, p_bound)
     _lib.check(lib.tsr_render_bwd_regions(
         rec.data_ptr(), _lib.ptr(values), offsets.data_ptr(), width, height,
         targets.color.data_ptr(), targets.depth.data_ptr(), targets.final_T.data_ptr(),
         targets.n_considered.data_ptr(), targets.ckpt.data_ptr(), ckpt_base.data_ptr(),
-        regions.list.data_ptr(), regions.seg.data_ptr(), grad_color.data_ptr(),
-        _lib.ptr(grad_depth), _lib.ptr(grad_final_T), out.data_ptr(), merges.data_ptr(),
-        int(p_bound), ws.data_ptr(), ws.numel(), _lib.stream_handle()), "tsr_render_bwd_regions")
+        regions.list.data_ptr(), regions.seg.data_ptr(), regions.units.data_ptr(),
+        regions.ctl.data_ptr(), grad_color.data_ptr(), _lib.ptr(grad_depth),
+        _lib.ptr(grad_final_T), out.data_ptr(), merges.data_ptr(), _lib.stream_handle()),
+        "tsr_render_bwd_regions")
 
 
 class BackwardWorkspace:

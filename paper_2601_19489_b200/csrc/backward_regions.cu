@@ -62,7 +62,6 @@ constexpr int kRWarps = 4;
 constexpr int kRThreads = 32 * kRWarps;
 constexpr int kRing = 64;    // staged region-list entries per half-warp (4 blocks of 16)
 constexpr int kOut = 16;     // finished-entry sums per half-warp (one round: flushed at its end)
-constexpr int kHeavyN = 768; // units of tiles with longer lists are queued first
 
 __device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
 __device__ __forceinline__ float2 bc(float x) { return make_float2(x, x); }
@@ -94,66 +93,6 @@ __device__ __forceinline__ float participate(int p, int nc, float alpha) {
       : "=f"(a)
       : "r"(p), "r"(nc), "f"(alpha), "f"(kMinAlpha));
   return a;
-}
-
-// Unit plan (one CTA): per tile ceil(n / kSeg) segments x 2 row pairs; the
-// units of tiles with n > kHeavyN first, then the rest, each in raster order.
-// unit = tile << 16 | segment << 1 | row pair.  Also resets the grab counter.
-constexpr int kPlanThreads = 1024;
-__global__ void __launch_bounds__(kPlanThreads) region_plan_kernel(
-    const int64_t* __restrict__ offsets, int n_tiles, uint32_t* __restrict__ units,
-    long long cap, int32_t* __restrict__ n_units, int32_t* __restrict__ counter) {
-  __shared__ int s_w[2][kPlanThreads / 32];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int per = (n_tiles + kPlanThreads - 1) / kPlanThreads;
-  const int t0 = tid * per, t1 = min(n_tiles, t0 + per);
-  int cnt[2] = {0, 0};  // units of heavy / light tiles in this thread's range
-  for (int t = t0; t < t1; ++t) {
-    const long long n = offsets[t + 1] - offsets[t];
-    cnt[n > kHeavyN ? 0 : 1] += 2 * (int)((n + kSeg - 1) >> kSegShift);
-  }
-  int incl[2], excl[2];
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    incl[c] = cnt[c];
-#pragma unroll
-    for (int k = 1; k < 32; k <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl[c], k);
-      if (lane >= k) incl[c] += v;
-    }
-    if (lane == 31) s_w[c][warp] = incl[c];
-  }
-  __syncthreads();
-  if (warp < 2) {
-    const int w = s_w[warp][lane];
-    int wi = w;
-#pragma unroll
-    for (int k = 1; k < 32; k <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, wi, k);
-      if (lane >= k) wi += v;
-    }
-    s_w[warp][lane] = wi - w;  // exclusive prefix of the warps
-  }
-  __syncthreads();
-  // totals: the last thread's inclusive prefix
-  __shared__ int s_tot;
-  if (tid == kPlanThreads - 1) s_tot = s_w[0][warp] + incl[0];
-  __syncthreads();
-  excl[0] = s_w[0][warp] + incl[0] - cnt[0];
-  excl[1] = s_tot + s_w[1][warp] + incl[1] - cnt[1];
-  long long u[2] = {excl[0], excl[1]};
-  for (int t = t0; t < t1; ++t) {
-    const long long n = offsets[t + 1] - offsets[t];
-    const int c = n > kHeavyN ? 0 : 1;
-    const int nseg = (int)((n + kSeg - 1) >> kSegShift);
-    for (int s = 0; s < nseg; ++s)
-      for (int rp = 0; rp < 2; ++rp, ++u[c])
-        if (u[c] < cap) units[u[c]] = ((uint32_t)t << 16) | ((uint32_t)s << 1) | (uint32_t)rp;
-  }
-  if (tid == kPlanThreads - 1) {
-    *n_units = (int32_t)min(u[1], cap);
-    *counter = 0;
-  }
 }
 
 // upstream of four pixels (x0 / x1, y0 / y1) is not all zero
@@ -427,7 +366,6 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
       // region sums of this lane's four pixels, added to the incoming sums
       const float2 hx = __ffma2_rn(gqB, bc(dx1), __fmul2_rn(gqA, bc(dx0)));  // per row: gq dx
       const float2 gs = __fadd2_rn(gqA, gqB);                                // per row: gq
-      const float2 go = __ffma2_rn(ldB, gaB, __fmul2_rn(ldA, gaA));
       const float2 wr = __ffma2_rn(wB, grB, __fmul2_rn(wA, grA));
       const float2 wg = __ffma2_rn(wB, ggB, __fmul2_rn(wA, ggA));
       const float2 wbl = __ffma2_rn(wB, gbB, __fmul2_rn(wA, gbA));
@@ -436,7 +374,9 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
       s_my = fmaf(gs.x, dy.x, fmaf(gs.y, dy.y, i_my * keep));
       s_c = fmaf(gs.x, dyy.x, fmaf(gs.y, dyy.y, i_c * keep));
       s_a = fmaf(dxx0, gqA.x + gqA.y, fmaf(dxx1, gqB.x + gqB.y, i_a * keep));
-      s_o = fmaf(i_o, keep, go.x + go.y);
+      // sum ld gauss = (sum ld alpha) / o for uncapped participants (alpha =
+      // o gauss): the per-row sums gs already hold it; the merge divides by o
+      s_o = fmaf(i_o, keep, gs.x + gs.y);
       s_r = fmaf(i_r, keep, wr.x + wr.y);
       s_g = fmaf(i_g, keep, wg.x + wg.y);
       s_bl = fmaf(i_bl, keep, wbl.x + wbl.y);
@@ -462,7 +402,8 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
         return;
       const int slot = e & (kRing - 1);
       const float4 sa = ra[slot];
-      const float cc = __fmul_rn(rb[slot].x, kQScale);
+      const float4 sb = rb[slot];
+      const float cc = __fmul_rn(sb.x, kQScale);
       const float ca = __fmul_rn(sa.z, kQScale), hb = __fmul_rn(sa.w, kQScale);  // (2b') / 2
       const int row = pr[slot].y;
       // sum gq u = a' sum gq dx + b' sum gq dy, likewise v (the conic's rows)
@@ -473,7 +414,7 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
       atomicAdd(dst + 2, -0.5f * A.z);
       atomicAdd(dst + 3, -A.w);
       atomicAdd(dst + 4, -0.5f * B.x);
-      atomicAdd(dst + 5, B.y);
+      atomicAdd(dst + 5, __fdiv_rn(B.y, sb.y));  // sum ld gauss (see the step)
       atomicAdd(dst + 6, B.z);
       atomicAdd(dst + 7, B.w);
       atomicAdd(dst + 8, Cc.x);
@@ -520,25 +461,20 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
   }
 }
 
-// ---- workspace: unit list + count + grab counter
-size_t regions_units_cap(int n_tiles, int64_t p_bound) {
-  return 2 * ((size_t)(p_bound > 0 ? p_bound : 0) / kSeg + (size_t)n_tiles + 1);
-}
-
 }  // namespace
 }  // namespace tsr
 
 using namespace tsr;
 
-extern "C" size_t tsr_render_bwd_regions_workspace(int32_t width, int32_t height, int64_t p_bound) {
-  if (width <= 0 || height <= 0) return 0;
-  return 256 + regions_units_cap(tiles_of(width) * tiles_of(height), p_bound) * 4;
-}
-
 extern "C" size_t tsr_region_list_entries(int32_t width, int32_t height, int64_t p_bound) {
   (void)width;
   (void)height;
   return 4 * (size_t)(p_bound > 0 ? p_bound : 0) + 1;
+}
+
+extern "C" size_t tsr_region_unit_entries(int32_t width, int32_t height, int64_t p_bound) {
+  if (width <= 0 || height <= 0) return 0;
+  return 2 * ((size_t)(p_bound > 0 ? p_bound : 0) / kSeg + (size_t)tiles_of(width) * tiles_of(height) + 1);
 }
 
 extern "C" size_t tsr_region_seg_entries(int32_t width, int32_t height, int64_t p_bound) {
@@ -552,26 +488,16 @@ extern "C" int tsr_render_bwd_regions(const float* rec, const int32_t* values,
                                       const float* final_T, const int32_t* n_considered,
                                       const float* ckpt, const int64_t* ckpt_base,
                                       const uint32_t* region_list, const int32_t* region_seg,
+                                      const uint32_t* region_units, int32_t* region_ctl,
                                       const float* grad_color, const float* grad_depth,
                                       const float* grad_final_T, float* grad2d,
-                                      unsigned long long* merges, int64_t p_bound, void* workspace,
-                                      size_t workspace_bytes, void* stream) {
-  if (width <= 0 || height <= 0 || !grad_color || !merges || !grad2d || !workspace || !ckpt ||
-      !ckpt_base || !region_list || !region_seg || !offsets)
+                                      unsigned long long* merges, void* stream) {
+  if (width <= 0 || height <= 0 || !grad_color || !merges || !grad2d || !ckpt || !ckpt_base ||
+      !region_list || !region_seg || !region_units || !region_ctl || !offsets)
     return TSR_E_INVALID;
   const int tx = tiles_of(width), ty = tiles_of(height), n_tiles = tx * ty;
   if (n_tiles >= (1 << 16)) return TSR_E_INVALID;
-  if (workspace_bytes < tsr_render_bwd_regions_workspace(width, height, p_bound))
-    return TSR_E_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
-  char* w = (char*)workspace;
-  int32_t* n_units = (int32_t*)w;
-  int32_t* counter = (int32_t*)(w + 4);
-  uint32_t* units = (uint32_t*)(w + 256);
-  region_plan_kernel<<<1, kPlanThreads, 0, s>>>(offsets, n_tiles, units,
-                                                (long long)regions_units_cap(n_tiles, p_bound),
-                                                n_units, counter);
-  TSR_CHECK_LAUNCH();
   auto* k = grad_depth ? render_bwd_regions_kernel<true> : render_bwd_regions_kernel<false>;
   static int per_sm[2] = {0, 0}, sms = 0;
   int& ps = per_sm[grad_depth ? 1 : 0];
@@ -582,10 +508,11 @@ extern "C" int tsr_render_bwd_regions(const float* rec, const int32_t* values,
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k, kRThreads, 0);
     if (ps < 1) ps = 1;
   }
+  // region_ctl = (n_units written by K3, grab counter zeroed with it)
   k<<<sms * ps, kRThreads, 0, s>>>((const float4*)rec, values, offsets, width, height, tx, color,
                                    depth, final_T, n_considered, ckpt, ckpt_base, region_list,
                                    region_seg, grad_color, grad_depth, grad_final_T, grad2d, merges,
-                                   units, n_units, counter);
+                                   region_units, region_ctl, region_ctl + 1);
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }

@@ -128,9 +128,16 @@ __device__ __forceinline__ void blend_pair(const float4 g, const float4 c, const
 // holds the number of entries with position < kSeg s for s = 1..ceil(n/kSeg)
 // (segbase_t = (start_t >> 10) + t: floor((O + n) / kSeg) - floor(O / kSeg)
 // + 1 >= ceil(n / kSeg), so the tiles' segment slots never overlap).
+// It also enqueues the tile's work units for the region-culled K4: unit =
+// tile << 16 | segment << 1 | row pair, 2 ceil(n / kSeg) per tile, appended
+// at units[atomicAdd(ctl[0])] as the tiles start (so the queue order is the
+// K3 launch order: heavy tiles first); ctl (n_units, grab counter) is zeroed
+// before K3 by the launch.
 struct RegionArgs {
   uint32_t* list;
   int32_t* seg;
+  uint32_t* units;
+  int32_t* ctl;
 };
 
 // 4 warps; warp w owns the 8x8 block (bx, by) = (w & 1, w >> 1) of the tile;
@@ -191,6 +198,12 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
   int r_count = 0, s_next = 1;
   const long long segbase = (start >> kSegShift) + tile;
   if (kCkpt == 3) rl = rg.list + 4 * start + (long long)warp * n;
+  if (kCkpt == 3 && tid == 0 && n > 0) {  // the tile's K4r work units, in K3's launch order
+    const int nu = 2 * ((n + kSeg - 1) >> kSegShift);
+    const int base = atomicAdd(rg.ctl, nu);
+    for (int k = 0; k < nu; ++k)
+      rg.units[base + k] = ((uint32_t)tile << 16) | (uint32_t)k;  // k = segment << 1 | row pair
+  }
   bool m0 = false, m1 = false;
   if (kScore == 3) {
     m0 = in0 && sc.mask[pix0];
@@ -294,6 +307,7 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
   if (kCkpt == 3 && lane == 0)  // the remaining segment ends (after an early exit)
     for (const int nseg = (n + kSeg - 1) >> kSegShift; s_next <= nseg; ++s_next)
       rg.seg[4 * (segbase + s_next - 1) + warp] = r_count;
+
   // a pixel that never terminated considered the whole list (skipped
   // entries included); a terminated one stopped at its death position
   if (s.alive0()) s.ncons0 = n;
@@ -433,18 +447,21 @@ extern "C" int tsr_render_fwd_regions(const float* rec, const int32_t* values,
                                       int32_t* out_n_contrib, int32_t* out_n_considered,
                                       float* ckpt, const int64_t* ckpt_base,
                                       uint32_t* region_list, int32_t* region_seg,
+                                      uint32_t* region_units, int32_t* region_ctl,
                                       const int32_t* tile_order, void* stream) {
   if (width <= 0 || height <= 0 || !background_host || !ckpt || !ckpt_base || !region_list ||
-      !region_seg)
+      !region_seg || !region_units || !region_ctl)
     return TSR_E_INVALID;
   const int tx = tiles_of(width), ty = tiles_of(height);
   const int n_tiles = tx * ty;
   cudaStream_t s = (cudaStream_t)stream;
   const ScoreArgs none{};
+  if (cudaMemsetAsync(region_ctl, 0, 2 * sizeof(int32_t), s) != cudaSuccess) return TSR_E_CUDA;
   render_fwd_kernel<3, 0><<<n_tiles, kFwdThreads, 0, s>>>(
       (const float4*)rec, values, offsets, width, height, tx, background_host[0],
       background_host[1], background_host[2], out_color, out_depth, out_final_T, out_n_contrib,
-      out_n_considered, ckpt, ckpt_base, none, tile_order, RegionArgs{region_list, region_seg});
+      out_n_considered, ckpt, ckpt_base, none, tile_order,
+      RegionArgs{region_list, region_seg, region_units, region_ctl});
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }

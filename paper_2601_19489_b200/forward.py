@@ -159,8 +159,9 @@ def render_raw(rec, values, offsets, ckpt_base, width: int, height: int, backgro
 
 class RegionLists:
     """Per-(tile, 8x8 region) list positions K3 writes for the region-culled
-    K4 (tsr_render_fwd_regions): 4 x p_bound uint32 entries plus the
-    segment-boundary offsets; sized for a pair bound, reused across steps."""
+    K4 (tsr_render_fwd_regions): 4 x p_bound uint32 entries, the
+    segment-boundary offsets and the backward's work-unit queue; sized for a
+    pair bound, reused across steps."""
 
     def __init__(self, width: int, height: int, p_bound: int):
         lib = _lib.load()
@@ -169,6 +170,9 @@ class RegionLists:
                                 dtype=torch.int32, device=dev)
         self.seg = torch.empty(int(lib.tsr_region_seg_entries(width, height, p_bound)),
                                dtype=torch.int32, device=dev)
+        self.units = torch.empty(int(lib.tsr_region_unit_entries(width, height, p_bound)),
+                                 dtype=torch.int32, device=dev)
+        self.ctl = torch.zeros(2, dtype=torch.int32, device=dev)  # unit count, grab counter
         self.shape = (width, height, p_bound)
 
 
@@ -184,7 +188,8 @@ def render_regions_raw(rec, values, offsets, ckpt_base, width: int, height: int,
         out.color.data_ptr(), out.depth.data_ptr(), out.final_T.data_ptr(),
         out.n_contrib.data_ptr(), out.n_considered.data_ptr(), out.ckpt.data_ptr(),
         ckpt_base.data_ptr(), regions.list.data_ptr(), regions.seg.data_ptr(),
-        _lib.ptr(tile_order), _lib.stream_handle()), "tsr_render_fwd_regions")
+        regions.units.data_ptr(), regions.ctl.data_ptr(), _lib.ptr(tile_order),
+        _lib.stream_handle()), "tsr_render_fwd_regions")
 
 
 # per-tile kernel launch order in the training step: "heavy" (heavy tiles

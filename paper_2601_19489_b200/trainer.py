@@ -257,8 +257,6 @@ class TrainStep:
         self.loss_ws = losses.PhotometricWorkspace()
         from .backward import BackwardWorkspace
         self.bwd_ws = BackwardWorkspace()
-        from .backward import RegionWorkspace
-        self.reg_ws = RegionWorkspace()
         self.regions = None
         self._order_buf = None
         self.tile_order = None
@@ -485,7 +483,7 @@ class TrainStep:
             from .backward import backward_regions_raw
             backward_regions_raw(batch.rec, idx.values, idx.offsets, camera.width, camera.height,
                                  out, idx.ckpt_base, self.regions, grad_color, gd, gt,
-                                 self.grad2d, self.merges, self.reg_ws, idx.p_cap)
+                                 self.grad2d, self.merges)
         elif K4_FORM in ("tiles", "regions"):
             _lib.check(self.lib.tsr_render_bwd_ordered(
                 *common, self.grad2d.data_ptr(), self.merges.data_ptr(),
@@ -622,7 +620,6 @@ class TrainStep:
         from .forward import TILE_ORDER
         return (2 + 1 + (1 if TILE_ORDER == "heavy" else 0) + 1 + 2 + 1
                 + (2 if K4_FORM == "units" else 0)
-                + (1 if self.regions is not None else 0)  # the region unit plan
                 + 1 + (1 if self.deterministic else 0))
 
     def last_view(self):

@@ -26,7 +26,7 @@ FIELDS = ("d_means2d", "d_conics", "d_opacities", "d_colors", "d_depths")
 def regions_pass(vr, grad_color, grad_depth=None, grad_final_T=None, background=(0.0, 0.0, 0.0)):
     """K3 (region mode) + K4r on a render_view's batch and index."""
     import paper_2601_19489_b200 as ts
-    from paper_2601_19489_b200.backward import RegionWorkspace, backward_regions_raw
+    from paper_2601_19489_b200.backward import backward_regions_raw
     from paper_2601_19489_b200.forward import RegionLists, RenderTargets, render_regions_raw
     b, t = vr.batch, vr.tiles
     p = max(t.n_pairs, 1)
@@ -39,7 +39,7 @@ def regions_pass(vr, grad_color, grad_depth=None, grad_final_T=None, background=
     f32 = lambda a: None if a is None else torch.as_tensor(a, dtype=torch.float32, device="cuda")
     backward_regions_raw(b.rec, t.values if t.n_pairs else None, t.offsets, b.width, b.height,
                          tgt, t.ckpt_base, reg, f32(grad_color), f32(grad_depth),
-                         f32(grad_final_T), out, merges, RegionWorkspace(), p)
+                         f32(grad_final_T), out, merges)
     torch.cuda.synchronize()
     return tgt, reg, ts.Grad2D(out, int(merges.item()))
 
