@@ -76,8 +76,13 @@ def test_c1_forward_backward_vs_oracle():
         assert rel_err(np64(grads[k]), o3[k]) < VJP_RTOL, k
 
 
-def test_fused_train_step_matches_separate_path():
-    """K4b+K5 fused == project_vjp then Adam.step (same device gradients)."""
+def test_fused_train_step_matches_separate_path(monkeypatch):
+    """K4b+K5 fused == project_vjp then Adam.step (same device gradients).
+    Both paths run the per-tile K4 (the public backward_per_gaussian's), so
+    the Grad2D they feed are the same sums; the region-culled K4 of the
+    default training step has its own parity tests (test_gpu_regions.py)."""
+    from paper_2601_19489_b200 import backward as bw
+    monkeypatch.setattr(bw, "K4_FORM", "tiles")
     ts, params, cam, gt, gset, camera = _setup(20_000, 320, 200, seed=2)
     cfg = ts.TrainConfig(max_iters=100)
     gset_b = gset.copy()
