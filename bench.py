@@ -604,7 +604,11 @@ def gpu_arm(args):
                    "window": f"training steps {args.warmup + 1}-{args.warmup + args.steps} from "
                              "the seeded init (the scene trains during the run; the e2e loop "
                              "replays the same segment from a post-warm-up snapshot)"},
-        "roofline": {"kernel": "render_bwd_kernel (K4)", "bound": "fp32",
+        "roofline": {"kernel": ("render_bwd_regions_kernel (K4r, region-culled: evaluates only "
+                                "the splats of each 8x8 region's K3 list; work counted as the "
+                                "reference's full per-pixel evaluation)"
+                                if getattr(stepper, "regions", None) is not None
+                                else "render_bwd_kernel (K4)"), "bound": "fp32",
                      "achieved": achieved, "peak": peak_ops, "unit": "Tops/s",
                      "frac": (achieved / peak_ops) if achieved else None,
                      "traffic": traffic, "traffic_source": traffic_src,

@@ -16,7 +16,10 @@ Bars (written here, reported in DESIGN.md §2):
                          (FP32 vs FP64 alpha at 1/255 or T at 1e-4) and
                          bounded by 0.1 % of the sampled pixels
   Grad2D                 max|x - y| / max|y| <= 1e-4 per field (the
-                         reference's metric, test_backward.py:34-39)
+                         reference's metric, test_backward.py:34-39), for
+                         the per-tile K4 and for the training step's
+                         region-culled K3 + K4 (whose render must equal
+                         the reference-checkpoint render bit for bit)
 The measured counts are printed and, when TSR_PARITY_LOG is set, appended
 to that file as JSON lines."""
 
@@ -88,18 +91,30 @@ def _check(config, n, clustered, pick_fn):
     og = O.backward_per_gaussian(ob, hb, hi, colors, gcol, tiles=pick)
     errs = {k: rel_err(np64(getattr(g2, k)), og[k])
             for k in ("d_means2d", "d_conics", "d_opacities", "d_colors")}
+    # the training step's region-culled K3 + K4 on the same batch, index and upstream
+    from test_gpu_regions import regions_pass
+    tgt, _, g3 = regions_pass(vr, gcol)
+    same_render = all(torch.equal(getattr(tgt, k), getattr(vr.buffers, k))
+                      for k in ("color", "depth", "final_T", "n_contrib", "n_considered"))
+    errs_r = {k: rel_err(np64(getattr(g3, k)), og[k])
+              for k in ("d_means2d", "d_conics", "d_opacities", "d_colors")}
     rec = {"config": config, "tiles": int(len(pick)), "entries_min": int(counts[pick].min()),
            "entries_max": int(counts[pick].max()), "pixels": int(mask.sum()),
            "flips": int(flip.sum()), "n_considered_flips": int((g_nc != o_nc).sum()),
            "n_contrib_flips": int((g_nb != o_nb).sum()), "color_err": float(col_err),
            "final_T_err": float(t_err), "depth_rel_err": float(d_err),
-           "grad2d_rel_err": errs, "merges": [int(g2.merges), int(og["merges"])]}
+           "grad2d_rel_err": errs, "grad2d_rel_err_regions": errs_r,
+           "regions_render_identical": same_render,
+           "merges": [int(g2.merges), int(g3.merges), int(og["merges"])]}
     _log(rec)
     assert flip.sum() <= FLIP_FRAC * mask.sum(), rec
     assert col_err < ATOL and t_err < ATOL and d_err < ATOL, rec
     for k, e in errs.items():
         assert e < GRAD_RTOL, (k, rec)
-    assert g2.merges == og["merges"] == int(counts[pick].sum())
+    for k, e in errs_r.items():
+        assert e < GRAD_RTOL, (k, "regions", rec)
+    assert same_render, rec
+    assert g2.merges == g3.merges == og["merges"] == int(counts[pick].sum())
 
 
 def test_c2_sampled_tiles_render_and_backward_vs_oracle():
