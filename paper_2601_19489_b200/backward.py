@@ -79,6 +79,8 @@ class Grad2D:
 # grows with the extra warps) and each unit re-gathers its pixel records
 # (DESIGN.md §8).  TSR_K4=units selects it.
 K4_FORM = os.environ.get("TSR_K4", "regions")
+# pair capacity from which the training step takes the region-culled K4
+REGIONS_MIN_PAIRS = int(os.environ.get("TSR_K4_REGIONS_MIN_PAIRS", 1_000_000))
 
 
 def backward_regions_raw(rec, values, offsets, width: int, height: int, targets, ckpt_base,

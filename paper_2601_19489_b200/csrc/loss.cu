@@ -42,22 +42,43 @@ __device__ __forceinline__ float2 bc2(float x) { return make_float2(x, x); }
 // division or 64-bit index arithmetic); all loads of a thread are issued
 // before any shared store.
 constexpr int kHaloRows = (kLIn + 7) / 8;  // rows per warp (6; warps 2-7 load 5)
+// The halo lies inside the image for every tile but the frame's border ring
+// (CTA-uniform): those load unguarded, from one 32-bit offset per row.
+__device__ __forceinline__ bool halo_inside(int H, int W, int ty0, int tx0) {
+  return ty0 >= kLR && tx0 >= kLR && ty0 - kLR + kLIn <= H && tx0 - kLR + kLIn <= W;
+}
 __device__ __forceinline__ void load_halo2(const float* __restrict__ r, const float* __restrict__ g,
                                            int c, int H, int W, int ty0, int tx0, float2* s) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int x0 = tx0 - kLR + lane, x1 = x0 + 32;
-  const bool in0 = x0 >= 0 && x0 < W, in1 = lane < kLIn - 32 && x1 >= 0 && x1 < W;
   float2 v0[kHaloRows], v1[kHaloRows];
+  if (halo_inside(H, W, ty0, tx0)) {
+    const float* rb = r + ((long long)(ty0 - kLR) * W + x0) * 3 + c;
+    const float* gb = g + ((long long)(ty0 - kLR) * W + x0) * 3 + c;
+    const bool two = lane < kLIn - 32;
 #pragma unroll
-  for (int k = 0; k < kHaloRows; ++k) {
-    const int row = warp + 8 * k;
-    const int y = ty0 - kLR + row;
-    v0[k] = v1[k] = make_float2(0.f, 0.f);
-    if (row < kLIn && y >= 0 && y < H) {
-      const float* rr = r + ((long long)y * W) * 3 + c;
-      const float* gg = g + ((long long)y * W) * 3 + c;
-      if (in0) v0[k] = make_float2(__ldg(rr + 3 * x0), __ldg(gg + 3 * x0));
-      if (in1) v1[k] = make_float2(__ldg(rr + 3 * x1), __ldg(gg + 3 * x1));
+    for (int k = 0; k < kHaloRows; ++k) {
+      const int row = warp + 8 * k;
+      const int o = row * 3 * W;  // < 2^31 for frames below ~700 Mpixel
+      v0[k] = v1[k] = make_float2(0.f, 0.f);
+      if (row < kLIn) {
+        v0[k] = make_float2(__ldg(rb + o), __ldg(gb + o));
+        if (two) v1[k] = make_float2(__ldg(rb + o + 96), __ldg(gb + o + 96));
+      }
+    }
+  } else {
+    const bool in0 = x0 >= 0 && x0 < W, in1 = lane < kLIn - 32 && x1 >= 0 && x1 < W;
+#pragma unroll
+    for (int k = 0; k < kHaloRows; ++k) {
+      const int row = warp + 8 * k;
+      const int y = ty0 - kLR + row;
+      v0[k] = v1[k] = make_float2(0.f, 0.f);
+      if (row < kLIn && y >= 0 && y < H) {
+        const float* rr = r + ((long long)y * W) * 3 + c;
+        const float* gg = g + ((long long)y * W) * 3 + c;
+        if (in0) v0[k] = make_float2(__ldg(rr + 3 * x0), __ldg(gg + 3 * x0));
+        if (in1) v1[k] = make_float2(__ldg(rr + 3 * x1), __ldg(gg + 3 * x1));
+      }
     }
   }
 #pragma unroll
@@ -91,6 +112,7 @@ __global__ void __launch_bounds__(256, 4) ssim_fwd_kernel(const float* __restric
   const int tx0 = (blockIdx.x / 3) * kLT, ty0 = blockIdx.y * kLT;
   const long long HW = (long long)H * W;
   double acc_ssim = 0.0, acc_l1 = 0.0;
+  float f_ssim = 0.f, f_l1 = 0.f;  // this thread's 4 pixels, widened once
   {
     load_halo2(r, g, c, H, W, ty0, tx0, s_rg);
     __syncthreads();
@@ -173,10 +195,12 @@ __global__ void __launch_bounds__(256, 4) ssim_fwd_kernel(const float* __restric
         const long long pix = (long long)y * W + x;
         Q01[c * HW + pix] = make_float2(2.f * mu2 * (dA1 - dA2) + 2.f * mu1 * (dB1 - dB2), dB2);
         Q2[c * HW + pix] = 2.f * dA2;
-        acc_ssim += (double)map;
+        f_ssim += map;
         const float2 rg = s_rg[(r0 + o + kLR) * kLS + col + kLR];
-        acc_l1 += (double)fabsf(rg.x - rg.y);
+        f_l1 += fabsf(rg.x - rg.y);
       }
+      acc_ssim = (double)f_ssim;
+      acc_l1 = (double)f_l1;
     }
     __syncthreads();
   }
@@ -272,24 +296,45 @@ __global__ void __launch_bounds__(256, 4) ssim_bwd_kernel(
     {
       const int lane = tid & 31, warp = tid >> 5;
       const int x0 = tx0 - kLR + lane, x1 = x0 + 32;
-      const bool in0 = x0 >= 0 && x0 < W, in1 = lane < kLIn - 32 && x1 >= 0 && x1 < W;
       float2 v2a[kHaloRows], v2b[kHaloRows];
       float v1a[kHaloRows], v1b[kHaloRows];
+      if (halo_inside(H, W, ty0, tx0)) {  // unguarded, one 32-bit offset per row
+        const float2* qa = Q01 + c * HW + (long long)(ty0 - kLR) * W + x0;
+        const float* qb = Q2 + c * HW + (long long)(ty0 - kLR) * W + x0;
+        const bool two = lane < kLIn - 32;
 #pragma unroll
-      for (int k = 0; k < kHaloRows; ++k) {
-        const int row = warp + 8 * k;
-        const int y = ty0 - kLR + row;
-        v2a[k] = v2b[k] = bc2(0.f);
-        v1a[k] = v1b[k] = 0.f;
-        if (row < kLIn && y >= 0 && y < H) {
-          const long long o = c * HW + (long long)y * W;
-          if (in0) {
-            v2a[k] = __ldg(Q01 + o + x0);
-            v1a[k] = __ldg(Q2 + o + x0);
+        for (int k = 0; k < kHaloRows; ++k) {
+          const int row = warp + 8 * k;
+          const int o = row * W;
+          v2a[k] = v2b[k] = bc2(0.f);
+          v1a[k] = v1b[k] = 0.f;
+          if (row < kLIn) {
+            v2a[k] = __ldg(qa + o);
+            v1a[k] = __ldg(qb + o);
+            if (two) {
+              v2b[k] = __ldg(qa + o + 32);
+              v1b[k] = __ldg(qb + o + 32);
+            }
           }
-          if (in1) {
-            v2b[k] = __ldg(Q01 + o + x1);
-            v1b[k] = __ldg(Q2 + o + x1);
+        }
+      } else {
+        const bool in0 = x0 >= 0 && x0 < W, in1 = lane < kLIn - 32 && x1 >= 0 && x1 < W;
+#pragma unroll
+        for (int k = 0; k < kHaloRows; ++k) {
+          const int row = warp + 8 * k;
+          const int y = ty0 - kLR + row;
+          v2a[k] = v2b[k] = bc2(0.f);
+          v1a[k] = v1b[k] = 0.f;
+          if (row < kLIn && y >= 0 && y < H) {
+            const long long o = c * HW + (long long)y * W;
+            if (in0) {
+              v2a[k] = __ldg(Q01 + o + x0);
+              v1a[k] = __ldg(Q2 + o + x0);
+            }
+            if (in1) {
+              v2b[k] = __ldg(Q01 + o + x1);
+              v1b[k] = __ldg(Q2 + o + x1);
+            }
           }
         }
       }

@@ -297,7 +297,7 @@ class TrainStep:
         self.index = IndexBuffers(len(self.gset), p_cap, tiles, det=self.deterministic)
         self.targets = RenderTargets(camera.height, camera.width, p_cap // 32 + tiles + 1)
         self.regions = None
-        if self._regions_on():  # K3's region lists for the region-culled K4
+        if self._regions_on(p_cap):  # K3's region lists for the region-culled K4
             from .forward import RegionLists
             self.regions = RegionLists(camera.width, camera.height, p_cap)
         self.hw = (camera.height, camera.width)
@@ -411,11 +411,15 @@ class TrainStep:
         self._mark(timer, "render")
         return batch
 
-    def _regions_on(self) -> bool:
+    def _regions_on(self, p_cap: int) -> bool:
         """The training step runs the region-culled K3/K4 pair (the
-        deterministic merge keeps the per-tile K4 and its per-pair slots)."""
-        from .backward import K4_FORM
-        return K4_FORM == "regions" and not self.deterministic and not self._can_fuse_update()
+        deterministic merge keeps the per-tile K4 and its per-pair slots).
+        Small frames keep the per-tile K4: the region K4's units (tile, row
+        pair, 1024-position segment) are too few to fill the GPU there (C1:
+        ~500 units for ~2,400 warp slots; measured 101 vs 61 us)."""
+        from .backward import K4_FORM, REGIONS_MIN_PAIRS
+        return (K4_FORM == "regions" and not self.deterministic and not self._can_fuse_update()
+                and p_cap >= REGIONS_MIN_PAIRS)
 
     def _can_fuse_update(self) -> bool:
         from .backward import K4_FORM

@@ -138,3 +138,33 @@ def test_region_lists_cover_every_blend():
                 if np.any((al >= 1 / 255) & (k < nc)):
                     need.append(k)
             assert set(need) <= set(ent.tolist()), (tile, r)
+
+
+def test_train_step_region_k4_matches_tile_k4(monkeypatch):
+    """The training step's K3 + K4 with the region-culled form forced on a
+    small frame equals the per-tile form: same render outputs bit for bit,
+    Grad2D within the FP32 bar (the two merge the same per-(splat, pixel)
+    terms in different orders)."""
+    import paper_2601_19489_b200 as ts
+    from paper_2601_19489_b200 import backward as bw
+    params, cam, gt = O.make_scene(20_000, 320, 200, seed=4)
+    camera = ts.Camera(cam["fx"], cam["fy"], cam["cx"], cam["cy"], 320, 200, cam["R"], cam["t"])
+    gt_t = torch.tensor(gt, dtype=torch.float32, device="cuda")
+    out = {}
+    for form in ("regions", "tiles"):
+        monkeypatch.setattr(bw, "K4_FORM", form)
+        monkeypatch.setattr(bw, "REGIONS_MIN_PAIRS", 0)
+        st = ts.TrainStep(ts.GaussianSet(**params), ts.TrainConfig(max_iters=100), extent=4.0)
+        batch = st.forward(camera)
+        st.loss_and_backward(batch, camera, gt_t)
+        torch.cuda.synchronize()
+        assert (st.regions is not None) == (form == "regions")
+        out[form] = (st.targets.color.clone(), st.targets.n_considered.clone(),
+                     st.grad2d.clone(), int(st.merges.item()))
+    assert torch.equal(out["regions"][0], out["tiles"][0])
+    assert torch.equal(out["regions"][1], out["tiles"][1])
+    g_r, g_t = np64(out["regions"][2]), np64(out["tiles"][2])
+    for f, sl in (("mean", slice(0, 2)), ("conic", slice(2, 5)), ("opacity", slice(5, 6)),
+                  ("color", slice(6, 9))):
+        assert rel_err(g_r[:, sl], g_t[:, sl]) < GRAD_RTOL, f
+    assert out["regions"][3] == out["tiles"][3]
