@@ -21,10 +21,12 @@
 // skipping it changes nothing; at C2 the region lists hold ~55 % of the
 // tile-list evaluations.
 //
-// Layout.  A warp is one work unit (tile, row pair rp, segment): its two
-// 16-lane halves run the regions (bx, rp), bx = 0, 1; lane j of a half owns
+// Layout.  A warp is one work unit (tile, pair p, segment): its two 16-lane
+// halves run two of the tile's four 8x8 regions (bx, by) -- the segment's two
+// longest region lists for p = 0, the other two for p = 1, so the lockstep
+// halves have similar step counts; lane j of a half owns
 // the four pixels (x0, y0), (x0, y1), (x0 + 4, y0), (x0 + 4, y1) with
-// x0 = 8 bx + (j & 3), y0 = 8 rp + (j >> 2), y1 = y0 + 4 -- two vertical pairs
+// x0 = 8 bx + (j & 3), y0 = 8 by + (j >> 2), y1 = y0 + 4 -- two vertical pairs
 // sharing dy, so the alpha and chain arithmetic is packed FP32x2.  Each half
 // is a 16-stage systolic pipeline: at step t lane j processes the region
 // list entry e = t - j for its four pixels; the ten per-splat partial sums
@@ -181,13 +183,42 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
     const int tile = (int)(code >> 16), seg = (int)((code >> 1) & 0x7fffu), rp = (int)(code & 1u);
     const long long start = offsets[tile];
     const int n = (int)(offsets[tile + 1] - start);
-    const int r = 2 * rp + h;  // K3's warp index of this 8x8 block
-    const long long sb = 4 * ((start >> kSegShift) + tile) + r;
-    const int e0 = seg > 0 ? rseg[sb + 4 * (seg - 1)] : 0;
-    const int L = rseg[sb + 4 * seg] - e0;
+    // The segment's four region lists are paired by length (longest two in
+    // unit 0, the others in unit 1): a warp's halves run in lockstep, so the
+    // pair's longer list sets its step count.  Both units of a segment read
+    // the same lengths and make the same choice.
+    const long long sb = 4 * ((start >> kSegShift) + tile);
+    int len[4], beg[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      beg[q] = seg > 0 ? rseg[sb + 4 * (seg - 1) + q] : 0;
+      len[q] = rseg[sb + 4 * seg + q] - beg[q];
+    }
+    // order the regions by (length desc, index asc): rank of region q
+    int rank[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      rank[q] = 0;
+#pragma unroll
+      for (int o = 0; o < 4; ++o)
+        rank[q] += (len[o] > len[q]) || (len[o] == len[q] && o < q);
+    }
+    int r = 0, r_other = 0;  // this half's region, and the other unit's region for this half
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (rank[q] == 2 * rp + h) r = q;
+      if (rank[q] == 2 * (1 - rp) + h) r_other = q;
+    }
+    int e0 = 0, L = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q == r) {
+        e0 = beg[q];
+        L = len[q];
+      }
     const int Lmax = max(L, __shfl_xor_sync(0xffffffffu, L, 16));
     const int tyi = tile / tiles_x, txi = tile - tyi * tiles_x;
-    const int X0 = txi * kTile + 8 * h + (j & 3), Y0 = tyi * kTile + 8 * rp + (j >> 2);
+    const int X0 = txi * kTile + 8 * (r & 1) + (j & 3), Y0 = tyi * kTile + 8 * (r >> 1) + (j >> 2);
     const int p0 = seg << kSegShift;
 
     // ---- pixel state: q = 0 (X0, Y0), 1 (X0, Y0 + 4) [pair A], 2, 3 [pair B, x + 4]
@@ -236,7 +267,8 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
     // upstream is not all zero (backward.py:156-158, 214-222)
     if (seg == 0 && rp == 0) {
       const bool other = quad_nz(grad_color, kDepth ? grad_depth : nullptr, grad_final_T, width,
-                                 height, X0, Y0 + 8);
+                                 height, txi * kTile + 8 * (r_other & 1) + (j & 3),
+                                 tyi * kTile + 8 * (r_other >> 1) + (j >> 2));
       if (__any_sync(0xffffffffu, nzl || other) && lane == 0)
         atomicAdd(merges, (unsigned long long)n);
     }
