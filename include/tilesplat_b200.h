@@ -207,8 +207,10 @@ size_t tsr_render_bwd_workspace(int32_t width, int32_t height, int64_t p_bound);
  * tsr_render_fwd_ordered(ckpt_stride 2) + tsr_render_bwd_ordered pair behind
  * backward_per_gaussian, backward.py:137-223).  tsr_render_fwd_regions is K3
  * writing checkpoint records only at segment starts (every 1024 list
- * positions) plus, per (tile, 8x8 region), the list positions whose splat
- * passes the region's conservative alpha >= 1/255 test, and the work units of
+ * positions) plus, per (tile, region), the list positions whose splat
+ * passes the region's conservative alpha >= 1/255 test (regions of 8 x
+ * region_height pixels, region_height 8 or 4; both calls take the same
+ * value), and the work units of
  * the backward (tile, row pair, segment), queued as the tiles finish:
  *   region_list   tsr_region_list_entries(...) uint32
  *   region_seg    tsr_region_seg_entries(...) int32
@@ -223,7 +225,7 @@ int tsr_render_fwd_regions(const float* rec, const int32_t* values, const int64_
                            float* out_color, float* out_depth, float* out_final_T,
                            int32_t* out_n_contrib, int32_t* out_n_considered, float* ckpt,
                            const int64_t* ckpt_base, uint32_t* region_list, int32_t* region_seg,
-                           uint32_t* region_units, int32_t* region_ctl,
+                           uint32_t* region_units, int32_t* region_ctl, int32_t region_height,
                            const int32_t* tile_order, void* stream);
 size_t tsr_region_list_entries(int32_t width, int32_t height, int64_t p_bound);
 size_t tsr_region_seg_entries(int32_t width, int32_t height, int64_t p_bound);
@@ -235,7 +237,7 @@ int tsr_render_bwd_regions(const float* rec, const int32_t* values, const int64_
                            const int32_t* region_seg, const uint32_t* region_units,
                            int32_t* region_ctl, const float* grad_color,
                            const float* grad_depth, const float* grad_final_T, float* grad2d,
-                           unsigned long long* merges, void* stream);
+                           unsigned long long* merges, int32_t region_height, void* stream);
 int tsr_render_bwd_ws(const float* rec, const int32_t* values, const int64_t* offsets,
                       int32_t width, int32_t height, const float* color, const float* depth,
                       const float* final_T, const int32_t* n_considered, const float* ckpt,

@@ -84,13 +84,13 @@ _SIGNATURES = {
     "tsr_render_bwd_workspace": (c_sz, [c_i32, c_i32, c_i64]),
     "tsr_render_fwd_regions": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, ctypes.POINTER(c_f32),
                                        c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
-                                       c_vp, c_vp, c_vp, c_vp]),
+                                       c_vp, c_vp, c_i32, c_vp, c_vp]),
     "tsr_region_list_entries": (c_sz, [c_i32, c_i32, c_i64]),
     "tsr_region_seg_entries": (c_sz, [c_i32, c_i32, c_i64]),
     "tsr_region_unit_entries": (c_sz, [c_i32, c_i32, c_i64]),
     "tsr_render_bwd_regions": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp,
                                        c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
-                                       c_vp, c_vp, c_vp]),
+                                       c_vp, c_vp, c_i32, c_vp]),
     "tsr_render_bwd_ws": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
                                   c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_sz, c_vp]),
     "tsr_render_bwd_ws_det": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp,

@@ -95,8 +95,8 @@ def backward_regions_raw(rec, values, offsets, width: int, height: int, targets,
         targets.n_considered.data_ptr(), targets.ckpt.data_ptr(), ckpt_base.data_ptr(),
         regions.list.data_ptr(), regions.seg.data_ptr(), regions.units.data_ptr(),
         regions.ctl.data_ptr(), grad_color.data_ptr(), _lib.ptr(grad_depth),
-        _lib.ptr(grad_final_T), out.data_ptr(), merges.data_ptr(), _lib.stream_handle()),
-        "tsr_render_bwd_regions")
+        _lib.ptr(grad_final_T), out.data_ptr(), merges.data_ptr(), regions.height,
+        _lib.stream_handle()), "tsr_render_bwd_regions")
 
 
 class BackwardWorkspace:

@@ -32,7 +32,7 @@
 // list entry e = t - j for its four pixels; the ten per-splat partial sums
 // flow lane to lane (one shuffle each), so lane 15 holds entry t - 15's
 // complete region sums.  The pixel state (T, R) never leaves its lane.
-// Splat records are staged per half in a shared-memory ring of 64 entries
+// Splat records are staged per group in a shared-memory ring of 4 kGL entries
 // (cp.async straight from rec, one block of 16 entries a round ahead; the
 // list position and row are loaded two rounds ahead); finished sums go to a
 // 32-entry buffer and are merged 16 at a time, one lane per entry.
@@ -62,8 +62,6 @@ constexpr int kRWarps = 4;
 #define TSR_K4R_EXIT 1
 #endif
 constexpr int kRThreads = 32 * kRWarps;
-constexpr int kRing = 64;    // staged region-list entries per half-warp (4 blocks of 16)
-constexpr int kOut = 16;     // finished-entry sums per half-warp (one round: flushed at its end)
 
 __device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
 __device__ __forceinline__ float2 bc(float x) { return make_float2(x, x); }
@@ -81,6 +79,11 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+// 8-byte vector atomic add (relaxed, device scope): one L2 request for two fields
+__device__ __forceinline__ void red_add2(float* p, float a, float b) {
+  asm volatile("red.relaxed.gpu.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b)
+               : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
@@ -101,11 +104,11 @@ __device__ __forceinline__ float participate(int p, int nc, float alpha) {
 __device__ __forceinline__ bool quad_nz(const float* __restrict__ grad_color,
                                         const float* __restrict__ grad_depth,
                                         const float* __restrict__ grad_final_T, int width,
-                                        int height, int X0, int Y0) {
+                                        int height, int X0, int Y0, int dy) {
   bool nz = false;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const int x = X0 + (q >> 1) * 4, y = Y0 + (q & 1) * 4;
+    const int x = X0 + (q >> 1) * 4, y = Y0 + (q & 1) * dy;
     if (x < width && y < height) {
       const long long pix = (long long)y * width + x;
       nz |= grad_color[3 * pix] != 0.f || grad_color[3 * pix + 1] != 0.f ||
@@ -116,7 +119,7 @@ __device__ __forceinline__ bool quad_nz(const float* __restrict__ grad_color,
   return nz;
 }
 
-template <bool kDepth>
+template <bool kDepth, int kGL>
 __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_kernel(
     const float4* __restrict__ rec, const int32_t* __restrict__ values,
     const int64_t* __restrict__ offsets, int width, int height, int tiles_x,
@@ -128,34 +131,46 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
     const float* __restrict__ grad_final_T, float* __restrict__ grad2d,
     unsigned long long* __restrict__ merges, const uint32_t* __restrict__ units,
     const int32_t* __restrict__ n_units_dev, int32_t* __restrict__ counter) {
-  // one half-warp's ring: a slot's four records share one address register
-  struct HalfRing {
+  // kGL lanes per region pipeline: 16 (8x8 regions, 4 per tile) or 8 (8x4
+  // regions, 8 per tile); a warp runs 32 / kGL regions
+  constexpr int kGPW = 32 / kGL;   // regions (lane groups) per warp
+  constexpr int kNR = 64 / kGL;    // regions per tile
+  constexpr int kRing = 4 * kGL;   // staged list entries per group (4 blocks of kGL)
+  constexpr int kOut = kGL;        // finished-entry sums per group (one round)
+  constexpr int kDY = kGL / 4;     // row offset of a lane's second pixel row
+  constexpr int kRH = 2 * kDY;     // region height
+  constexpr int kPR = 2 * kRing;  // position / row ring depth (8 blocks: see the lifetimes below)
+  // one group's ring: a slot's three records share one address register
+  struct GroupRing {
     float4 a[kRing];   // mx, my, a, b
     float4 b[kRing];   // c, opacity, depth, level t
     float4 c[kRing];   // r, g, b, -
-    int4 pr[kRing];    // list position, row
   };
-  __shared__ HalfRing s_ring[kRWarps][2];
-  __shared__ float4 s_oa[kRWarps][2][kOut];   // sums: gq dx, gq dy, gq dxx, gq dxy
-  __shared__ float4 s_ob[kRWarps][2][kOut];   //       gq dyy, ld gauss, w g_r, w g_g
-  __shared__ float2 s_oc[kRWarps][2][kOut];   //       w g_b, w g_d
-  __shared__ int s_pos[kRWarps][2][kRing];    // list positions, staged 3 rounds ahead
-  __shared__ int s_row[kRWarps][2][kRing];    // their rows, staged 2 rounds ahead
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, h = lane >> 4, j = lane & 15;
+  __shared__ GroupRing s_ring[kRWarps][kGPW];
+  // finished sums, group-minor so the warp's last-lane stores share a line
+  __shared__ float4 s_oa[kRWarps][kOut][kGPW];   // sums: gq dx, gq dy, gq dxx, gq dxy
+  __shared__ float4 s_ob[kRWarps][kOut][kGPW];   //       gq dyy, ld gauss, w g_r, w g_g
+  __shared__ float2 s_oc[kRWarps][kOut][kGPW];   //       w g_b, w g_d
+  // list positions (staged 3 rounds ahead, read by the steps) and rows (2
+  // rounds ahead, read by the staging and the merge); block b's slots are
+  // reused by block b + 8, whose position is fetched at round b + 5, after
+  // block b's last step (round b + 1) and merge (end of round b + 1)
+  __shared__ int s_pos[kRWarps][kGPW][kPR];
+  __shared__ int s_row[kRWarps][kGPW][kPR];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, h = lane / kGL, j = lane % kGL;
   float4* ra = s_ring[warp][h].a;
   float4* rb = s_ring[warp][h].b;
   float4* rc = s_ring[warp][h].c;
-  int4* pr = s_ring[warp][h].pr;
-  float4* oa = s_oa[warp][h];
-  float4* ob = s_ob[warp][h];
-  float2* oc = s_oc[warp][h];
+  float4(*oa)[kGPW] = s_oa[warp];
+  float4(*ob)[kGPW] = s_ob[warp];
+  float2(*oc)[kGPW] = s_oc[warp];
   int* spos = s_pos[warp][h];
   int* srow = s_row[warp][h];
   // sentinel splat: alpha = gauss = 0 at every pixel, finite products
   const float4 sent_a = make_float4(-65536.f, -65536.f, 1.f, 0.f);
   const float4 sent_b = make_float4(1.f, 1.f, 0.f, 0.f);
   const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  const float keep = j != 0 ? 1.f : 0.f;  // lane 0 of a half starts each entry's sums
+  const float keep = j != 0 ? 1.f : 0.f;  // lane 0 of a group starts each entry's sums
   const int n_units = *n_units_dev;
 
   // the next unit is grabbed (and its code loaded) one unit ahead, so its
@@ -183,45 +198,42 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
     const int tile = (int)(code >> 16), seg = (int)((code >> 1) & 0x7fffu), rp = (int)(code & 1u);
     const long long start = offsets[tile];
     const int n = (int)(offsets[tile + 1] - start);
-    // The segment's four region lists are paired by length (longest two in
-    // unit 0, the others in unit 1): a warp's halves run in lockstep, so the
-    // pair's longer list sets its step count.  Both units of a segment read
-    // the same lengths and make the same choice.
-    const long long sb = 4 * ((start >> kSegShift) + tile);
-    int len[4], beg[4];
+    // The segment's region lists are grouped by length (the longest 32/kGL
+    // in unit 0, the others in unit 1): a warp's groups run in lockstep, so
+    // the group's longest list sets its step count.  Both units of a segment
+    // read the same lengths and make the same choice.
+    const long long sb = kNR * ((start >> kSegShift) + tile);
+    int len[kNR], beg[kNR];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      beg[q] = seg > 0 ? rseg[sb + 4 * (seg - 1) + q] : 0;
-      len[q] = rseg[sb + 4 * seg + q] - beg[q];
+    for (int q = 0; q < kNR; ++q) {
+      beg[q] = seg > 0 ? rseg[sb + kNR * (seg - 1) + q] : 0;
+      len[q] = rseg[sb + kNR * seg + q] - beg[q];
     }
-    // order the regions by (length desc, index asc): rank of region q
-    int rank[4];
+    // order the regions by (length desc, index asc)
+    int r = 0, r_other = 0;  // this group's region, and the other unit's region for this group
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      rank[q] = 0;
+    for (int q = 0; q < kNR; ++q) {
+      int rank = 0;
 #pragma unroll
-      for (int o = 0; o < 4; ++o)
-        rank[q] += (len[o] > len[q]) || (len[o] == len[q] && o < q);
-    }
-    int r = 0, r_other = 0;  // this half's region, and the other unit's region for this half
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (rank[q] == 2 * rp + h) r = q;
-      if (rank[q] == 2 * (1 - rp) + h) r_other = q;
+      for (int o = 0; o < kNR; ++o) rank += (len[o] > len[q]) || (len[o] == len[q] && o < q);
+      if (rank == kGPW * rp + h) r = q;
+      if (rank == kGPW * (1 - rp) + h) r_other = q;
     }
     int e0 = 0, L = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < kNR; ++q)
       if (q == r) {
         e0 = beg[q];
         L = len[q];
       }
-    const int Lmax = max(L, __shfl_xor_sync(0xffffffffu, L, 16));
+    int Lmax = L;
+#pragma unroll
+    for (int m = kGL; m < 32; m <<= 1) Lmax = max(Lmax, __shfl_xor_sync(0xffffffffu, Lmax, m));
     const int tyi = tile / tiles_x, txi = tile - tyi * tiles_x;
-    const int X0 = txi * kTile + 8 * (r & 1) + (j & 3), Y0 = tyi * kTile + 8 * (r >> 1) + (j >> 2);
+    const int X0 = txi * kTile + 8 * (r & 1) + (j & 3), Y0 = tyi * kTile + kRH * (r >> 1) + (j >> 2);
     const int p0 = seg << kSegShift;
 
-    // ---- pixel state: q = 0 (X0, Y0), 1 (X0, Y0 + 4) [pair A], 2, 3 [pair B, x + 4]
+    // ---- pixel state: q = 0 (X0, Y0), 1 (X0, Y0 + kDY) [pair A], 2, 3 [pair B, x + 4]
     float T[4], R[4], g_r[4], g_g[4], g_b[4], g_d[4];
     int nc[4];
     bool nzl = false;
@@ -230,7 +242,7 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
                               : nullptr;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int x = X0 + (q >> 1) * 4, y = Y0 + (q & 1) * 4;
+      const int x = X0 + (q >> 1) * 4, y = Y0 + (q & 1) * kDY;
       T[q] = 0.f;
       R[q] = 0.f;
       g_r[q] = g_g[q] = g_b[q] = g_d[q] = 0.f;
@@ -268,13 +280,13 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
     if (seg == 0 && rp == 0) {
       const bool other = quad_nz(grad_color, kDepth ? grad_depth : nullptr, grad_final_T, width,
                                  height, txi * kTile + 8 * (r_other & 1) + (j & 3),
-                                 tyi * kTile + 8 * (r_other >> 1) + (j >> 2));
+                                 tyi * kTile + kRH * (r_other >> 1) + (j >> 2), kDY);
       if (__any_sync(0xffffffffu, nzl || other) && lane == 0)
         atomicAdd(merges, (unsigned long long)n);
     }
     if (!nz || Lmax == 0) continue;  // exact zeros
 
-    const uint32_t* lst = rlist + 4 * start + (long long)r * n + e0;
+    const uint32_t* lst = rlist + kNR * start + (long long)r * n + e0;
     const int32_t* vals = values + start;
     // Every list access is asynchronous (cp.async into shared memory, waited
     // once per round), three stages per entry e of this lane's half:
@@ -282,17 +294,17 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
     //   row       values[pos]     -> srow  (2 rounds ahead)
     //   record    rec[row] x 3    -> ring  (1 round ahead), (pos, row) -> pr
     auto fetch_pos = [&](int e) {
-      if (e < L) cp_async4(&spos[e & (kRing - 1)], lst + e);
-      else spos[e & (kRing - 1)] = INT_MAX;
+      if (e < L) cp_async4(&spos[e & (kPR - 1)], lst + e);
+      else spos[e & (kPR - 1)] = INT_MAX;
     };
     auto fetch_row = [&](int e) {
-      const int pos = spos[e & (kRing - 1)];
-      if (pos != INT_MAX) cp_async4(&srow[e & (kRing - 1)], vals + pos);
-      else srow[e & (kRing - 1)] = -1;
+      const int pos = spos[e & (kPR - 1)];
+      if (pos != INT_MAX) cp_async4(&srow[e & (kPR - 1)], vals + pos);
+      else srow[e & (kPR - 1)] = -1;
     };
     auto stage = [&](int e) {
       const int slot = e & (kRing - 1);
-      const int pos = spos[slot], row = srow[slot];
+      const int row = srow[e & (kPR - 1)];
       if (row >= 0) {
         cp_async16(&ra[slot], rec + 3 * (long long)row);
         cp_async16(&rb[slot], rec + 3 * (long long)row + 1);
@@ -302,22 +314,21 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
         rb[slot] = sent_b;
         rc[slot] = zero4;
       }
-      pr[slot] = make_int4(pos, row, 0, 0);
     };
     __syncwarp();  // the previous unit's flush has read the ring
-    // block -1 (the pipeline fill reads entries -16..-1): sentinels
-    ra[kRing - 16 + j] = sent_a;
-    rb[kRing - 16 + j] = sent_b;
-    rc[kRing - 16 + j] = zero4;
-    pr[kRing - 16 + j] = make_int4(INT_MAX, -1, 0, 0);
+    // block -1 (the pipeline fill reads entries -kGL..-1): sentinels
+    ra[kRing - kGL + j] = sent_a;
+    rb[kRing - kGL + j] = sent_b;
+    rc[kRing - kGL + j] = zero4;
+    spos[kPR - kGL + j] = INT_MAX;
     fetch_pos(j);
-    fetch_pos(16 + j);
-    fetch_pos(32 + j);
+    fetch_pos(kGL + j);
+    fetch_pos(2 * kGL + j);
     cp_async_commit();
     cp_async_wait_all();
     __syncwarp();
     fetch_row(j);
-    fetch_row(16 + j);
+    fetch_row(kGL + j);
     cp_async_commit();
     cp_async_wait_all();
     __syncwarp();
@@ -325,7 +336,7 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
     cp_async_commit();
 
     const float xa = (float)X0 + 0.5f, xb = (float)(X0 + 4) + 0.5f;
-    const float2 yp = f2((float)Y0 + 0.5f, (float)(Y0 + 4) + 0.5f);
+    const float2 yp = f2((float)Y0 + 0.5f, (float)(Y0 + kDY) + 0.5f);
     float2 TA = f2(T[0], T[1]), TB = f2(T[2], T[3]);
     float2 RA = f2(R[0], R[1]), RB = f2(R[2], R[3]);
     const float2 grA = f2(g_r[0], g_r[1]), grB = f2(g_r[2], g_r[3]);
@@ -337,21 +348,21 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
           s_g = 0.f, s_bl = 0.f, s_d = 0.f;
     const float2 one = bc(1.f);
 
-    // one systolic step: entry t - j of this half for the lane's four pixels
+    // one systolic step: entry t - j of this group for the lane's four pixels
     // (A, B, pos) of a step are loaded one step ahead (ping-pong registers);
     // the colour record C in the step (first used after the alpha chain)
     auto step = [&](const float4& A, const float4& B, int pos, int t) {
       const float4 C = rc[(t - j) & (kRing - 1)];
-      float i_mx = __shfl_up_sync(0xffffffffu, s_mx, 1, 16);
-      float i_my = __shfl_up_sync(0xffffffffu, s_my, 1, 16);
-      float i_a = __shfl_up_sync(0xffffffffu, s_a, 1, 16);
-      float i_b = __shfl_up_sync(0xffffffffu, s_b, 1, 16);
-      float i_c = __shfl_up_sync(0xffffffffu, s_c, 1, 16);
-      float i_o = __shfl_up_sync(0xffffffffu, s_o, 1, 16);
-      float i_r = __shfl_up_sync(0xffffffffu, s_r, 1, 16);
-      float i_g = __shfl_up_sync(0xffffffffu, s_g, 1, 16);
-      float i_bl = __shfl_up_sync(0xffffffffu, s_bl, 1, 16);
-      float i_d = kDepth ? __shfl_up_sync(0xffffffffu, s_d, 1, 16) : 0.f;
+      float i_mx = __shfl_up_sync(0xffffffffu, s_mx, 1, kGL);
+      float i_my = __shfl_up_sync(0xffffffffu, s_my, 1, kGL);
+      float i_a = __shfl_up_sync(0xffffffffu, s_a, 1, kGL);
+      float i_b = __shfl_up_sync(0xffffffffu, s_b, 1, kGL);
+      float i_c = __shfl_up_sync(0xffffffffu, s_c, 1, kGL);
+      float i_o = __shfl_up_sync(0xffffffffu, s_o, 1, kGL);
+      float i_r = __shfl_up_sync(0xffffffffu, s_r, 1, kGL);
+      float i_g = __shfl_up_sync(0xffffffffu, s_g, 1, kGL);
+      float i_bl = __shfl_up_sync(0xffffffffu, s_bl, 1, kGL);
+      float i_d = kDepth ? __shfl_up_sync(0xffffffffu, s_d, 1, kGL) : 0.f;
       // alpha of the four pixels: K3's operation sequence (eval_alpha)
       const float ca = __fmul_rn(A.z, kQScale), cb = __fmul_rn(A.w, 2.0f * kQScale),
                   cc = __fmul_rn(B.x, kQScale);
@@ -416,19 +427,19 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
         const float2 wd = __ffma2_rn(wB, gdB, __fmul2_rn(wA, gdA));
         s_d = fmaf(i_d, keep, wd.x + wd.y);
       }
-      if (j == 15) {  // entry t - 15 is complete: park its sums
-        const int o = (t - 15) & (kOut - 1);
-        oa[o] = make_float4(s_mx, s_my, s_a, s_b);
-        ob[o] = make_float4(s_c, s_o, s_r, s_g);
-        oc[o] = make_float2(s_bl, s_d);
+      if (j == kGL - 1) {  // entry t - (kGL - 1) is complete: park its sums
+        const int o = (t - (kGL - 1)) & (kOut - 1);
+        oa[o][h] = make_float4(s_mx, s_my, s_a, s_b);
+        ob[o][h] = make_float4(s_c, s_o, s_r, s_g);
+        oc[o][h] = make_float2(s_bl, s_d);
       }
     };
     // merge entry e's region sums (one lane per entry; backward.py:214-222)
     const float ms = 2.0f / kQScale;
     auto flush = [&](int e) {
       if (e < 0 || e >= L) return;
-      const float4 A = oa[e & (kOut - 1)], B = ob[e & (kOut - 1)];
-      const float2 Cc = oc[e & (kOut - 1)];
+      const float4 A = oa[e & (kOut - 1)][h], B = ob[e & (kOut - 1)][h];
+      const float2 Cc = oc[e & (kOut - 1)][h];
       if (!((B.y != 0.f) | (B.z != 0.f) | (B.w != 0.f) | (Cc.x != 0.f) | (Cc.y != 0.f) |
             (A.z != 0.f)))
         return;
@@ -437,30 +448,26 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
       const float4 sb = rb[slot];
       const float cc = __fmul_rn(sb.x, kQScale);
       const float ca = __fmul_rn(sa.z, kQScale), hb = __fmul_rn(sa.w, kQScale);  // (2b') / 2
-      const int row = pr[slot].y;
+      const int row = srow[e & (kPR - 1)];
       // sum gq u = a' sum gq dx + b' sum gq dy, likewise v (the conic's rows)
       const float uu = fmaf(ca, A.x, hb * A.y), vv = fmaf(hb, A.x, cc * A.y);
+      // five 8-byte vector atomics per row (rows are 40 B: 8-B aligned)
       float* dst = grad2d + (long long)row * TSR_GRAD2D_FLOATS;
-      atomicAdd(dst + 0, ms * 0.5f * uu);
-      atomicAdd(dst + 1, ms * 0.5f * vv);
-      atomicAdd(dst + 2, -0.5f * A.z);
-      atomicAdd(dst + 3, -A.w);
-      atomicAdd(dst + 4, -0.5f * B.x);
-      atomicAdd(dst + 5, __fdiv_rn(B.y, sb.y));  // sum ld gauss (see the step)
-      atomicAdd(dst + 6, B.z);
-      atomicAdd(dst + 7, B.w);
-      atomicAdd(dst + 8, Cc.x);
-      if (kDepth) atomicAdd(dst + 9, Cc.y);
+      red_add2(dst + 0, ms * 0.5f * uu, ms * 0.5f * vv);
+      red_add2(dst + 2, -0.5f * A.z, -A.w);
+      red_add2(dst + 4, -0.5f * B.x, __fdiv_rn(B.y, sb.y));  // sum ld gauss (see the step)
+      red_add2(dst + 6, B.z, B.w);
+      red_add2(dst + 8, Cc.x, kDepth ? Cc.y : 0.f);
     };
 
     auto load = [&](float4& A, float4& B, int& pos, int t) {
       const int slot = (t - j) & (kRing - 1);
       A = ra[slot];
       B = rb[slot];
-      pos = pr[slot].x;
+      pos = spos[(t - j) & (kPR - 1)];
     };
-    const int steps = Lmax + 15;  // entry Lmax - 1 leaves lane 15 at step Lmax + 14
-    const int rounds = (steps + 15) >> 4;
+    const int steps = Lmax + kGL - 1;  // entry Lmax - 1 leaves the last lane at step Lmax + kGL - 2
+    const int rounds = (steps + kGL - 1) / kGL;
     cp_async_wait_all();
     __syncwarp();  // block 0 staged
     float4 A0, B0, A1, B1;
@@ -468,16 +475,16 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
     load(A0, B0, q0, 0);
     for (int k = 0; k < rounds; ++k) {
       // block k's records, k + 1's rows, k + 2's positions landed (waited
-      // at the previous round's step 14)
-      stage(16 * (k + 1) + j);
-      fetch_row(16 * (k + 2) + j);
-      fetch_pos(16 * (k + 3) + j);
+      // at the previous round's second-to-last step)
+      stage(kGL * (k + 1) + j);
+      fetch_row(kGL * (k + 2) + j);
+      fetch_pos(kGL * (k + 3) + j);
       cp_async_commit();
 #pragma unroll 1
-      for (int i = 0; i < 16; i += 2) {
-        const int t = 16 * k + i;
+      for (int i = 0; i < kGL; i += 2) {
+        const int t = kGL * k + i;
         if (TSR_K4R_EXIT && t >= steps) break;  // the last round stops at its last step
-        if (i == 14) {  // block k + 1 (the next step's lane 0 entry) has landed
+        if (i == kGL - 2) {  // block k + 1 (the next step's lane 0 entry) has landed
           cp_async_wait_all();
           __syncwarp();
         }
@@ -487,7 +494,7 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
         step(A1, B1, q1, t + 1);
       }
       __syncwarp();
-      flush(16 * k - 15 + j);
+      flush(kGL * k - (kGL - 1) + j);
     }
     cp_async_wait_all();  // the last staged block lands before the ring is reused
   }
@@ -501,7 +508,7 @@ using namespace tsr;
 extern "C" size_t tsr_region_list_entries(int32_t width, int32_t height, int64_t p_bound) {
   (void)width;
   (void)height;
-  return 4 * (size_t)(p_bound > 0 ? p_bound : 0) + 1;
+  return 8 * (size_t)(p_bound > 0 ? p_bound : 0) + 1;  // up to 8 regions per tile
 }
 
 extern "C" size_t tsr_region_unit_entries(int32_t width, int32_t height, int64_t p_bound) {
@@ -511,7 +518,7 @@ extern "C" size_t tsr_region_unit_entries(int32_t width, int32_t height, int64_t
 
 extern "C" size_t tsr_region_seg_entries(int32_t width, int32_t height, int64_t p_bound) {
   if (width <= 0 || height <= 0) return 0;
-  return 4 * ((size_t)(p_bound > 0 ? p_bound : 0) / kSeg + (size_t)tiles_of(width) * tiles_of(height) + 1);
+  return 8 * ((size_t)(p_bound > 0 ? p_bound : 0) / kSeg + (size_t)tiles_of(width) * tiles_of(height) + 1);
 }
 
 extern "C" int tsr_render_bwd_regions(const float* rec, const int32_t* values,
@@ -523,16 +530,20 @@ extern "C" int tsr_render_bwd_regions(const float* rec, const int32_t* values,
                                       const uint32_t* region_units, int32_t* region_ctl,
                                       const float* grad_color, const float* grad_depth,
                                       const float* grad_final_T, float* grad2d,
-                                      unsigned long long* merges, void* stream) {
+                                      unsigned long long* merges, int32_t region_height,
+                                      void* stream) {
   if (width <= 0 || height <= 0 || !grad_color || !merges || !grad2d || !ckpt || !ckpt_base ||
-      !region_list || !region_seg || !region_units || !region_ctl || !offsets)
+      !region_list || !region_seg || !region_units || !region_ctl || !offsets ||
+      (region_height != 8 && region_height != 4))
     return TSR_E_INVALID;
   const int tx = tiles_of(width), ty = tiles_of(height), n_tiles = tx * ty;
   if (n_tiles >= (1 << 16)) return TSR_E_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
-  auto* k = grad_depth ? render_bwd_regions_kernel<true> : render_bwd_regions_kernel<false>;
-  static int per_sm[2] = {0, 0}, sms = 0;
-  int& ps = per_sm[grad_depth ? 1 : 0];
+  auto* k = region_height == 8
+                ? (grad_depth ? render_bwd_regions_kernel<true, 16> : render_bwd_regions_kernel<false, 16>)
+                : (grad_depth ? render_bwd_regions_kernel<true, 8> : render_bwd_regions_kernel<false, 8>);
+  static int per_sm[4] = {0, 0, 0, 0}, sms = 0;
+  int& ps = per_sm[(grad_depth ? 1 : 0) + (region_height == 8 ? 2 : 0)];
   if (ps == 0) {
     int dev = 0;
     cudaGetDevice(&dev);

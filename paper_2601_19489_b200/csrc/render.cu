@@ -194,11 +194,19 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
   long long sc_cursor = 0;  // kScore 1/2: this warp's contributions so far
   if (kScore == 2) sc_cursor = sc.warp_base[tile * 4 + warp];
   const long long pix0 = (long long)y0 * width + x, pix1 = (long long)y1 * width + x;
+  // region mode: kCkpt 3 = the warp's 8x8 block is one region (4 per tile);
+  // kCkpt 4 = its top / bottom 8x4 halves (rows of the lanes' first / second
+  // pixels) are two regions, (2 by + half) * 2 + bx (8 per tile)
+  constexpr bool kRegions = kCkpt >= 3;
+  constexpr int kNR = kCkpt == 4 ? 8 : 4;
   uint32_t* rl = nullptr;
-  int r_count = 0, s_next = 1;
+  uint32_t* rl2 = nullptr;
+  int r_count = 0, r_count2 = 0, s_next = 1;
+  const int reg0 = kCkpt == 4 ? (2 * by) * 2 + bx : warp, reg1 = (2 * by + 1) * 2 + bx;
   const long long segbase = (start >> kSegShift) + tile;
-  if (kCkpt == 3) rl = rg.list + 4 * start + (long long)warp * n;
-  if (kCkpt == 3 && tid == 0 && n > 0) {  // the tile's K4r work units, in K3's launch order
+  if (kRegions) rl = rg.list + kNR * start + (long long)reg0 * n;
+  if (kCkpt == 4) rl2 = rg.list + kNR * start + (long long)reg1 * n;
+  if (kRegions && tid == 0 && n > 0) {  // the tile's K4r work units, in K3's launch order
     const int nu = 2 * ((n + kSeg - 1) >> kSegShift);
     const int base = atomicAdd(rg.ctl, nu);
     for (int k = 0; k < nu; ++k)
@@ -235,20 +243,34 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
       if (!__any_sync(0xffffffffu, s.alive0() || s.alive1())) break;  // warp-level early exit
       const int cend = min(kGroup, cnt - c0);
       const int pos0 = b0 + c0;
-      if (kCkpt == 3 && pos0 > 0 && (pos0 & (kSeg - 1)) == 0) {  // segment boundary
-        if (lane == 0) rg.seg[4 * (segbase + s_next - 1) + warp] = r_count;
+      if (kRegions && pos0 > 0 && (pos0 & (kSeg - 1)) == 0) {  // segment boundary
+        if (lane == 0) {
+          rg.seg[kNR * (segbase + s_next - 1) + reg0] = r_count;
+          if (kCkpt == 4) rg.seg[kNR * (segbase + s_next - 1) + reg1] = r_count2;
+        }
         ++s_next;
       }
       // lane j tests splat c0 + j against this warp's 8x8 block
-      bool hit = false;
+      bool hit = false, hit2 = false;
       if (lane < cend) {
         const float4 g = s_spl[c0 + lane][0], rw = s_raw[c0 + lane];
-        hit = strip_hit(g.x, g.y, rw.x, rw.y, rw.z, rw.w, sx0, sx0 + 7.f, sy0, sy0 + 7.f);
+        if (kCkpt == 4) {  // the two 8x4 halves (their union is the 8x8 block)
+          hit = strip_hit(g.x, g.y, rw.x, rw.y, rw.z, rw.w, sx0, sx0 + 7.f, sy0, sy0 + 3.f);
+          hit2 = strip_hit(g.x, g.y, rw.x, rw.y, rw.z, rw.w, sx0, sx0 + 7.f, sy0 + 4.f, sy0 + 7.f);
+        } else {
+          hit = strip_hit(g.x, g.y, rw.x, rw.y, rw.z, rw.w, sx0, sx0 + 7.f, sy0, sy0 + 7.f);
+        }
       }
       unsigned mask = __ballot_sync(0xffffffffu, hit);
-      if (kCkpt == 3) {
+      if (kRegions) {
         if (hit) rl[r_count + __popc(mask & lt_mask)] = (uint32_t)(pos0 + lane);
         r_count += __popc(mask);
+      }
+      if (kCkpt == 4) {
+        const unsigned mask2 = __ballot_sync(0xffffffffu, hit2);
+        if (hit2) rl2[r_count2 + __popc(mask2 & lt_mask)] = (uint32_t)(pos0 + lane);
+        r_count2 += __popc(mask2);
+        mask |= mask2;
       }
       while (mask) {
         const int j = __ffs(mask) - 1;
@@ -281,7 +303,7 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
       }
       if (kCkpt && cend == kGroup &&
           (kCkpt == 1 || (kCkpt == 2 && ((pos0 >> 5) & 1)) ||
-           (kCkpt == 3 && ((pos0 + kGroup) & (kSeg - 1)) == 0))) {
+           (kRegions && ((pos0 + kGroup) & (kSeg - 1)) == 0))) {
         // state after list position pos0+31 -> record (pos0+32)/32 - 1, for
         // each pixel that consumed that position (still alive, or died there)
         float* dst = ck0 + (long long)(pos0 >> 5) * (5 * kTilePixels);
@@ -304,9 +326,11 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
     }
   }
   if (kScore == 1 && lane == 0) sc.warp_counts[tile * 4 + warp] = sc_cursor;
-  if (kCkpt == 3 && lane == 0)  // the remaining segment ends (after an early exit)
-    for (const int nseg = (n + kSeg - 1) >> kSegShift; s_next <= nseg; ++s_next)
-      rg.seg[4 * (segbase + s_next - 1) + warp] = r_count;
+  if (kRegions && lane == 0)  // the remaining segment ends (after an early exit)
+    for (const int nseg = (n + kSeg - 1) >> kSegShift; s_next <= nseg; ++s_next) {
+      rg.seg[kNR * (segbase + s_next - 1) + reg0] = r_count;
+      if (kCkpt == 4) rg.seg[kNR * (segbase + s_next - 1) + reg1] = r_count2;
+    }
 
   // a pixel that never terminated considered the whole list (skipped
   // entries included); a terminated one stopped at its death position
@@ -448,16 +472,18 @@ extern "C" int tsr_render_fwd_regions(const float* rec, const int32_t* values,
                                       float* ckpt, const int64_t* ckpt_base,
                                       uint32_t* region_list, int32_t* region_seg,
                                       uint32_t* region_units, int32_t* region_ctl,
-                                      const int32_t* tile_order, void* stream) {
+                                      int32_t region_height, const int32_t* tile_order,
+                                      void* stream) {
   if (width <= 0 || height <= 0 || !background_host || !ckpt || !ckpt_base || !region_list ||
-      !region_seg || !region_units || !region_ctl)
+      !region_seg || !region_units || !region_ctl || (region_height != 8 && region_height != 4))
     return TSR_E_INVALID;
   const int tx = tiles_of(width), ty = tiles_of(height);
   const int n_tiles = tx * ty;
   cudaStream_t s = (cudaStream_t)stream;
   const ScoreArgs none{};
   if (cudaMemsetAsync(region_ctl, 0, 2 * sizeof(int32_t), s) != cudaSuccess) return TSR_E_CUDA;
-  render_fwd_kernel<3, 0><<<n_tiles, kFwdThreads, 0, s>>>(
+  auto* k = region_height == 8 ? render_fwd_kernel<3, 0> : render_fwd_kernel<4, 0>;
+  k<<<n_tiles, kFwdThreads, 0, s>>>(
       (const float4*)rec, values, offsets, width, height, tx, background_host[0],
       background_host[1], background_host[2], out_color, out_depth, out_final_T, out_n_contrib,
       out_n_considered, ckpt, ckpt_base, none, tile_order,

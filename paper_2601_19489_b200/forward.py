@@ -157,14 +157,19 @@ def render_raw(rec, values, offsets, ckpt_base, width: int, height: int, backgro
         _lib.ptr(tile_order), _lib.stream_handle()), "tsr_render_fwd_ordered")
 
 
+REGION_HEIGHT = int(os.environ.get("TSR_K4R_REGION", 8))
+
+
 class RegionLists:
     """Per-(tile, 8x8 region) list positions K3 writes for the region-culled
     K4 (tsr_render_fwd_regions): 4 x p_bound uint32 entries, the
     segment-boundary offsets and the backward's work-unit queue; sized for a
     pair bound, reused across steps."""
 
-    def __init__(self, width: int, height: int, p_bound: int):
+    def __init__(self, width: int, height: int, p_bound: int, region_height: int | None = None):
         lib = _lib.load()
+        # 8x4 regions (8 per tile, 8-lane backward pipelines) or 8x8 (4 per tile, 16 lanes)
+        self.height = int(region_height or REGION_HEIGHT)
         dev = _device()
         self.list = torch.empty(int(lib.tsr_region_list_entries(width, height, p_bound)),
                                 dtype=torch.int32, device=dev)
@@ -188,7 +193,7 @@ def render_regions_raw(rec, values, offsets, ckpt_base, width: int, height: int,
         out.color.data_ptr(), out.depth.data_ptr(), out.final_T.data_ptr(),
         out.n_contrib.data_ptr(), out.n_considered.data_ptr(), out.ckpt.data_ptr(),
         ckpt_base.data_ptr(), regions.list.data_ptr(), regions.seg.data_ptr(),
-        regions.units.data_ptr(), regions.ctl.data_ptr(), _lib.ptr(tile_order),
+        regions.units.data_ptr(), regions.ctl.data_ptr(), regions.height, _lib.ptr(tile_order),
         _lib.stream_handle()), "tsr_render_fwd_regions")
 
 

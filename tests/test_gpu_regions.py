@@ -6,9 +6,10 @@ Bars: the region render's outputs are the reference-checkpoint render's bit
 for bit (the culling only skips exact zeros); Grad2D max|x - y| / max|y| <=
 1e-4 per field against the oracle (the reference's metric,
 test_backward.py:34-39); merges equal the reference's count.  Scenes cover
-one segment per tile (C1), many segments per tile (a crowded 64x64 frame:
-every tile's list is several 1024-position segments long), the depth and
-final-T channels, and frames whose size is not a multiple of the tile."""
+one segment per tile (C1), many segments per tile (a low-opacity cluster:
+pixels alive over several 1024-position segments), the depth and final-T
+channels, and frames whose size is not a multiple of the tile; both region
+shapes (8x8 regions with 16-lane pipelines, 8x4 with 8-lane ones)."""
 
 import numpy as np
 import pytest
@@ -23,7 +24,8 @@ GRAD_RTOL = 1e-4
 FIELDS = ("d_means2d", "d_conics", "d_opacities", "d_colors", "d_depths")
 
 
-def regions_pass(vr, grad_color, grad_depth=None, grad_final_T=None, background=(0.0, 0.0, 0.0)):
+def regions_pass(vr, grad_color, grad_depth=None, grad_final_T=None, background=(0.0, 0.0, 0.0),
+                 region_height=None):
     """K3 (region mode) + K4r on a render_view's batch and index."""
     import paper_2601_19489_b200 as ts
     from paper_2601_19489_b200.backward import backward_regions_raw
@@ -31,7 +33,7 @@ def regions_pass(vr, grad_color, grad_depth=None, grad_final_T=None, background=
     b, t = vr.batch, vr.tiles
     p = max(t.n_pairs, 1)
     tgt = RenderTargets(b.height, b.width, p // 32 + t.tiles_x * t.tiles_y + 1)
-    reg = RegionLists(b.width, b.height, p)
+    reg = RegionLists(b.width, b.height, p, region_height)
     render_regions_raw(b.rec, t.values if t.n_pairs else None, t.offsets, t.ckpt_base, b.width,
                        b.height, background, tgt, reg)
     out = torch.zeros((len(b), 10), dtype=torch.float32, device="cuda")
@@ -54,11 +56,11 @@ def _scene(n, w, h, seed=0, clustered=False, cluster_opacity=None):
     return ts, vr, gt
 
 
-def _vs_oracle(vr, gcol, gdep=None, gT=None):
+def _vs_oracle(vr, gcol, gdep=None, gT=None, region_height=None):
     hb, hi = host_batch(vr.batch), host_index(vr.tiles)
     colors = np64(vr.colors)
     ob = O.render(hb, hi, colors, np.zeros(3))
-    tgt, reg, g2 = regions_pass(vr, gcol, gdep, gT)
+    tgt, reg, g2 = regions_pass(vr, gcol, gdep, gT, region_height=region_height)
     # the region render is the reference-checkpoint render, bit for bit
     for k in ("color", "depth", "final_T", "n_contrib", "n_considered"):
         assert torch.equal(getattr(tgt, k), getattr(vr.buffers, k)), k
@@ -71,48 +73,54 @@ def _vs_oracle(vr, gcol, gdep=None, gT=None):
     return tgt, reg, g2, errs
 
 
+@pytest.mark.parametrize("region_height", [4, 8])
 @pytest.mark.parametrize("n,w,h", [(10_000, 256, 256), (3_000, 200, 120), (20_000, 64, 64)])
-def test_regions_backward_vs_oracle(n, w, h):
+def test_regions_backward_vs_oracle(n, w, h, region_height):
     ts, vr, gt = _scene(n, w, h)
     assert int(torch.diff(vr.tiles.offsets).max()) > 0
     rng = np.random.default_rng(n)
     gcol = rng.normal(0, 1e-3, (h, w, 3))
-    _vs_oracle(vr, gcol)
+    _vs_oracle(vr, gcol, region_height=region_height)
 
 
-def test_regions_many_segments_per_tile():
+@pytest.mark.parametrize("region_height", [4, 8])
+def test_regions_many_segments_per_tile(region_height):
     """A low-opacity cluster (C3-lo style): pixels stay alive for thousands
     of list positions, so their tiles' work spans several segments (units),
     each starting from K3's segment-start checkpoint."""
     ts, vr, gt = _scene(30_000, 64, 64, seed=3, clustered=True, cluster_opacity=(0.004, 0.02))
     assert int(vr.buffers.n_considered.max()) > 3 * 1024, int(vr.buffers.n_considered.max())
     rng = np.random.default_rng(7)
-    _vs_oracle(vr, rng.normal(0, 1e-3, (64, 64, 3)))
+    _vs_oracle(vr, rng.normal(0, 1e-3, (64, 64, 3)), region_height=region_height)
 
 
-def test_regions_depth_and_final_T_channels():
+@pytest.mark.parametrize("region_height", [4, 8])
+def test_regions_depth_and_final_T_channels(region_height):
     ts, vr, gt = _scene(5_000, 160, 96, seed=5)
     rng = np.random.default_rng(11)
     _vs_oracle(vr, rng.normal(0, 1e-3, (96, 160, 3)), rng.normal(0, 1e-3, (96, 160)),
-               rng.normal(0, 1e-3, (96, 160)))
+               rng.normal(0, 1e-3, (96, 160)), region_height=region_height)
 
 
-def test_regions_zero_upstream_half_tile():
+@pytest.mark.parametrize("region_height", [4, 8])
+def test_regions_zero_upstream_half_tile(region_height):
     """Upstream zero outside a band of rows: row pairs with no upstream are
     skipped (exact zeros) and merges still count every pair of a tile whose
     upstream is not all zero."""
     ts, vr, gt = _scene(8_000, 128, 128, seed=2)
     g = np.zeros((128, 128, 3))
     g[4:6] = 1e-3  # only the top row pair of the first tile row
-    _vs_oracle(vr, g)
+    _vs_oracle(vr, g, region_height=region_height)
 
 
-def test_region_lists_cover_every_blend():
+@pytest.mark.parametrize("region_height", [4, 8])
+def test_region_lists_cover_every_blend(region_height):
     """Each region list is increasing, within [0, n), and holds every list
     position that blends at a pixel of the region (oracle participation)."""
     ts, vr, gt = _scene(4_000, 96, 64, seed=9)
     hb, hi = host_batch(vr.batch), host_index(vr.tiles)
-    tgt, reg, _ = regions_pass(vr, np.zeros((64, 96, 3)))
+    tgt, reg, _ = regions_pass(vr, np.zeros((64, 96, 3)), region_height=region_height)
+    nr = 64 // (2 * region_height)
     lst, seg = reg.list.cpu().numpy(), reg.seg.cpu().numpy()
     off = hi["offsets"]
     for tile in range(hi["tiles_x"] * hi["tiles_y"]):
@@ -121,12 +129,12 @@ def test_region_lists_cover_every_blend():
             continue
         nseg = -(-n // 1024)
         ty, tx = divmod(tile, hi["tiles_x"])
-        for r in range(4):
-            total = seg[4 * ((lo >> 10) + tile + nseg - 1) + r]
-            ent = lst[4 * lo + r * n: 4 * lo + r * n + total].astype(np.int64)
+        for r in range(nr):
+            total = seg[nr * ((lo >> 10) + tile + nseg - 1) + r]
+            ent = lst[nr * lo + r * n: nr * lo + r * n + total].astype(np.int64)
             assert np.all(np.diff(ent) > 0) and (total == 0 or (ent[0] >= 0 and ent[-1] < n))
-            x0, y0 = tx * 16 + 8 * (r & 1), ty * 16 + 8 * (r >> 1)
-            x1, y1 = min(x0 + 8, 96), min(y0 + 8, 64)
+            x0, y0 = tx * 16 + 8 * (r & 1), ty * 16 + region_height * (r >> 1)
+            x1, y1 = min(x0 + 8, 96), min(y0 + region_height, 64)
             if x0 >= 96 or y0 >= 64:
                 continue
             gy, gx = np.mgrid[y0:y1, x0:x1]
