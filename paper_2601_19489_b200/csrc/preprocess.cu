@@ -314,9 +314,18 @@ __global__ void __launch_bounds__(kScanBlock, kS == 1 ? 3 : TSR_K1_MINB) preproc
     const int32_t* __restrict__ row_of_source, int32_t* __restrict__ counts,
     uint32_t* __restrict__ depth_bits, uint4* __restrict__ spans,
     unsigned long long* __restrict__ total_pairs) {
-  __shared__ unsigned long long s_sum[kScanBlock / 32];
+  // the block's pair total: each warp adds its sum when it finishes and the
+  // last warp publishes it (no end-of-block barrier: the per-thread column
+  // walks take very different times, and early warps free their slots)
+  __shared__ unsigned long long s_tot;
+  __shared__ int s_done;
   constexpr bool kLB = kS == 1;
   __shared__ LbWarp s_lb[kLB ? kScanBlock / 32 : 1];
+  if (threadIdx.x == 0) {
+    s_tot = 0;
+    s_done = 0;
+  }
+  __syncthreads();
   const long long i = (long long)blockIdx.x * kScanBlock + threadIdx.x;
   const int tiles_x = tiles_of(cam.width), tiles_y = tiles_of(cam.height);
   long long cnt = 0;
@@ -352,12 +361,13 @@ __global__ void __launch_bounds__(kScanBlock, kS == 1 ? 3 : TSR_K1_MINB) preproc
   }
   unsigned long long v = (unsigned long long)cnt;
   for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-  if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t = 0;
-    for (int w = 0; w < kScanBlock / 32; ++w) t += s_sum[w];
-    if (t) atomicAdd(total_pairs, t);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&s_tot, v);
+    __threadfence_block();
+    if (atomicAdd(&s_done, 1) == kScanBlock / 32 - 1) {
+      const unsigned long long t = atomicAdd(&s_tot, 0ull);
+      if (t) atomicAdd(total_pairs, t);
+    }
   }
 }
 
@@ -367,8 +377,14 @@ __global__ void __launch_bounds__(kScanBlock) count_kernel(
     const float* __restrict__ rec, long long m, int width, int height, int strategy,
     int32_t* __restrict__ counts, uint32_t* __restrict__ depth_bits, uint4* __restrict__ spans,
     unsigned long long* __restrict__ total_pairs) {
-  __shared__ unsigned long long s_sum[kScanBlock / 32];
+  __shared__ unsigned long long s_tot;
+  __shared__ int s_done;
   __shared__ LbWarp s_lb[kScanBlock / 32];
+  if (threadIdx.x == 0) {
+    s_tot = 0;
+    s_done = 0;
+  }
+  __syncthreads();
   const long long i = (long long)blockIdx.x * kScanBlock + threadIdx.x;
   long long cnt = 0;
   uint4 span;
@@ -387,12 +403,13 @@ __global__ void __launch_bounds__(kScanBlock) count_kernel(
   }
   unsigned long long v = (unsigned long long)cnt;
   for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-  if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t = 0;
-    for (int w = 0; w < kScanBlock / 32; ++w) t += s_sum[w];
-    if (t) atomicAdd(total_pairs, t);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&s_tot, v);
+    __threadfence_block();
+    if (atomicAdd(&s_done, 1) == kScanBlock / 32 - 1) {
+      const unsigned long long t = atomicAdd(&s_tot, 0ull);
+      if (t) atomicAdd(total_pairs, t);
+    }
   }
 }
 

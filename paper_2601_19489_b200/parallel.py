@@ -5,8 +5,9 @@ K4b into one flat gradient buffer), the flat buffer is summed across ranks
 with ONE allreduce per step, and every rank applies the identical Adam update
 (K5), so replicas stay bit-identical.  `deterministic=True` replaces the
 NCCL sum by an all-gather + fixed rank-order sum, making the result
-independent of the reduction tree (bitwise-equal params for any N with the
-same view set).
+independent of the reduction tree: bitwise reproducible for a fixed N and
+view assignment (each rank first sums its own views locally, so a different
+N reassociates those sums and agrees to FP32 tolerance, not bitwise).
 
 `sharded=True` is the ZeRO-1 form of the same step (the
 B200 variant): per group, a reduce-scatter gives rank r the summed
