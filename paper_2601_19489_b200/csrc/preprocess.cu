@@ -269,7 +269,10 @@ __device__ __forceinline__ bool project_one(const tsr_gaussians_t& g, const tsr_
 // (a) cull + compaction: row_of_source, source_ids and M.  4 consecutive
 // Gaussians per thread (N / 1024 blocks: more CTAs in flight beat a shorter
 // look-back chain here, measured).
-constexpr int kCullItems = 4;
+#ifndef TSR_CULL_ITEMS
+#define TSR_CULL_ITEMS 4
+#endif
+constexpr int kCullItems = TSR_CULL_ITEMS;
 __global__ void __launch_bounds__(kScanBlock) cull_compact_kernel(
     tsr_gaussians_t g, tsr_camera_t cam, int32_t* __restrict__ source_ids,
     int32_t* __restrict__ row_of_source, int64_t* __restrict__ totals,
@@ -314,18 +317,9 @@ __global__ void __launch_bounds__(kScanBlock, kS == 1 ? 3 : TSR_K1_MINB) preproc
     const int32_t* __restrict__ row_of_source, int32_t* __restrict__ counts,
     uint32_t* __restrict__ depth_bits, uint4* __restrict__ spans,
     unsigned long long* __restrict__ total_pairs) {
-  // the block's pair total: each warp adds its sum when it finishes and the
-  // last warp publishes it (no end-of-block barrier: the per-thread column
-  // walks take very different times, and early warps free their slots)
-  __shared__ unsigned long long s_tot;
-  __shared__ int s_done;
+  __shared__ unsigned long long s_sum[kScanBlock / 32];
   constexpr bool kLB = kS == 1;
   __shared__ LbWarp s_lb[kLB ? kScanBlock / 32 : 1];
-  if (threadIdx.x == 0) {
-    s_tot = 0;
-    s_done = 0;
-  }
-  __syncthreads();
   const long long i = (long long)blockIdx.x * kScanBlock + threadIdx.x;
   const int tiles_x = tiles_of(cam.width), tiles_y = tiles_of(cam.height);
   long long cnt = 0;
@@ -361,13 +355,12 @@ __global__ void __launch_bounds__(kScanBlock, kS == 1 ? 3 : TSR_K1_MINB) preproc
   }
   unsigned long long v = (unsigned long long)cnt;
   for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-  if ((threadIdx.x & 31) == 0) {
-    atomicAdd(&s_tot, v);
-    __threadfence_block();
-    if (atomicAdd(&s_done, 1) == kScanBlock / 32 - 1) {
-      const unsigned long long t = atomicAdd(&s_tot, 0ull);
-      if (t) atomicAdd(total_pairs, t);
-    }
+  if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < kScanBlock / 32; ++w) t += s_sum[w];
+    if (t) atomicAdd(total_pairs, t);
   }
 }
 
@@ -377,14 +370,8 @@ __global__ void __launch_bounds__(kScanBlock) count_kernel(
     const float* __restrict__ rec, long long m, int width, int height, int strategy,
     int32_t* __restrict__ counts, uint32_t* __restrict__ depth_bits, uint4* __restrict__ spans,
     unsigned long long* __restrict__ total_pairs) {
-  __shared__ unsigned long long s_tot;
-  __shared__ int s_done;
+  __shared__ unsigned long long s_sum[kScanBlock / 32];
   __shared__ LbWarp s_lb[kScanBlock / 32];
-  if (threadIdx.x == 0) {
-    s_tot = 0;
-    s_done = 0;
-  }
-  __syncthreads();
   const long long i = (long long)blockIdx.x * kScanBlock + threadIdx.x;
   long long cnt = 0;
   uint4 span;
@@ -403,13 +390,12 @@ __global__ void __launch_bounds__(kScanBlock) count_kernel(
   }
   unsigned long long v = (unsigned long long)cnt;
   for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-  if ((threadIdx.x & 31) == 0) {
-    atomicAdd(&s_tot, v);
-    __threadfence_block();
-    if (atomicAdd(&s_done, 1) == kScanBlock / 32 - 1) {
-      const unsigned long long t = atomicAdd(&s_tot, 0ull);
-      if (t) atomicAdd(total_pairs, t);
-    }
+  if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < kScanBlock / 32; ++w) t += s_sum[w];
+    if (t) atomicAdd(total_pairs, t);
   }
 }
 
