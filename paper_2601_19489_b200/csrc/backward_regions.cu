@@ -43,6 +43,7 @@
 // over many warps (the paper's redistribution across heavy tiles,
 // PAPER.md:121/145); units are drawn from a global queue, long tiles first.
 #include <climits>
+#include <cstdlib>
 
 #include <cuda_runtime.h>
 
@@ -54,12 +55,6 @@ namespace {
 constexpr int kRWarps = 4;
 #ifndef TSR_K4R_CTAS
 #define TSR_K4R_CTAS 4
-#endif
-#ifndef TSR_K4R_PREFETCH
-#define TSR_K4R_PREFETCH 0
-#endif
-#ifndef TSR_K4R_EXIT
-#define TSR_K4R_EXIT 1
 #endif
 constexpr int kRThreads = 32 * kRWarps;
 
@@ -119,7 +114,13 @@ __device__ __forceinline__ bool quad_nz(const float* __restrict__ grad_color,
   return nz;
 }
 
-template <bool kDepth, int kGL>
+// kGL lanes per region pipeline, kPX pixels per lane (two columns x kPX/2
+// rows; rows of a lane are kGL/4 apart): kGL x kPX = the region's pixels.
+//   (16, 4): 8x8 regions, 4 per tile, 2 per warp
+//   ( 8, 4): 8x4 regions, 8 per tile, 4 per warp
+//   ( 8, 8): 8x8 regions, 4 per tile, all 4 in one warp (half the fill and
+//            half the per-step shuffles / loads per pixel)
+template <bool kDepth, int kGL, int kPX>
 __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_kernel(
     const float4* __restrict__ rec, const int32_t* __restrict__ values,
     const int64_t* __restrict__ offsets, int width, int height, int tiles_x,
@@ -131,15 +132,17 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
     const float* __restrict__ grad_final_T, float* __restrict__ grad2d,
     unsigned long long* __restrict__ merges, const uint32_t* __restrict__ units,
     const int32_t* __restrict__ n_units_dev, int32_t* __restrict__ counter) {
-  // kGL lanes per region pipeline: 16 (8x8 regions, 4 per tile) or 8 (8x4
-  // regions, 8 per tile); a warp runs 32 / kGL regions
-  constexpr int kGPW = 32 / kGL;   // regions (lane groups) per warp
-  constexpr int kNR = 64 / kGL;    // regions per tile
-  constexpr int kRing = 4 * kGL;   // staged list entries per group (4 blocks of kGL)
-  constexpr int kOut = kGL;        // finished-entry sums per group (one round)
-  constexpr int kDY = kGL / 4;     // row offset of a lane's second pixel row
-  constexpr int kRH = 2 * kDY;     // region height
-  constexpr int kPR = 2 * kRing;  // position / row ring depth (8 blocks: see the lifetimes below)
+  constexpr int kGPW = 32 / kGL;               // regions (lane groups) per warp
+  constexpr int kRS = kGL / 4;                 // row stride of a lane's pixels
+  constexpr int kRH = kRS * (kPX / 2);         // region height
+  constexpr int kNR = kTilePixels / (kGL * kPX);  // regions per tile
+  constexpr int kUPS = kNR / kGPW;             // units per (tile, segment): 1 or 2
+  constexpr int kNRG = kPX / 4;                // row pairs (packed FP32x2) of a lane
+  constexpr int kNQ = 2 * kNRG;                // pixel pairs of a lane: (column, row pair)
+  constexpr int kRing = 4 * kGL;               // staged list entries per group (4 blocks of kGL)
+  constexpr int kOut = kGL;                    // finished-entry sums per group (one round)
+  constexpr int kPR = 2 * kRing;               // position / row ring depth (8 blocks)
+  static_assert(kNR * kGL * kPX == kTilePixels && kUPS >= 1, "region shape");
   // one group's ring: a slot's three records share one address register
   struct GroupRing {
     float4 a[kRing];   // mx, my, a, b
@@ -149,7 +152,7 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
   __shared__ GroupRing s_ring[kRWarps][kGPW];
   // finished sums, group-minor so the warp's last-lane stores share a line
   __shared__ float4 s_oa[kRWarps][kOut][kGPW];   // sums: gq dx, gq dy, gq dxx, gq dxy
-  __shared__ float4 s_ob[kRWarps][kOut][kGPW];   //       gq dyy, ld gauss, w g_r, w g_g
+  __shared__ float4 s_ob[kRWarps][kOut][kGPW];   //       gq dyy, ld alpha, w g_r, w g_g
   __shared__ float2 s_oc[kRWarps][kOut][kGPW];   //       w g_b, w g_d
   // list positions (staged 3 rounds ahead, read by the steps) and rows (2
   // rounds ahead, read by the staging and the merge); block b's slots are
@@ -173,34 +176,19 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
   const float keep = j != 0 ? 1.f : 0.f;  // lane 0 of a group starts each entry's sums
   const int n_units = *n_units_dev;
 
-  // the next unit is grabbed (and its code loaded) one unit ahead, so its
-  // descriptor loads overlap the current unit's pipeline
-#if TSR_K4R_PREFETCH
-  int u_next = 0;
-  if (lane == 0) u_next = atomicAdd(counter, 1);
-  u_next = __shfl_sync(0xffffffffu, u_next, 0);
-  uint32_t code_next = u_next < n_units ? units[u_next] : 0u;
-  for (;;) {
-    const int u = u_next;
-    if (u >= n_units) break;
-    const uint32_t code = code_next;
-    if (lane == 0) u_next = atomicAdd(counter, 1);
-    u_next = __shfl_sync(0xffffffffu, u_next, 0);
-    code_next = u_next < n_units ? units[u_next] : 0u;
-#else
   for (;;) {
     int u = 0;
     if (lane == 0) u = atomicAdd(counter, 1);
     u = __shfl_sync(0xffffffffu, u, 0);
     if (u >= n_units) break;
     const uint32_t code = units[u];
-#endif
     const int tile = (int)(code >> 16), seg = (int)((code >> 1) & 0x7fffu), rp = (int)(code & 1u);
+    if (rp >= kUPS) continue;  // K3 queues two units per segment; this shape runs one
     const long long start = offsets[tile];
     const int n = (int)(offsets[tile + 1] - start);
-    // The segment's region lists are grouped by length (the longest 32/kGL
-    // in unit 0, the others in unit 1): a warp's groups run in lockstep, so
-    // the group's longest list sets its step count.  Both units of a segment
+    // The segment's region lists are grouped by length (the longest kGPW in
+    // unit 0, the others in unit 1): a warp's groups run in lockstep, so the
+    // group's longest list sets its step count.  Both units of a segment
     // read the same lengths and make the same choice.
     const long long sb = kNR * ((start >> kSegShift) + tile);
     int len[kNR], beg[kNR];
@@ -209,7 +197,6 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
       beg[q] = seg > 0 ? rseg[sb + kNR * (seg - 1) + q] : 0;
       len[q] = rseg[sb + kNR * seg + q] - beg[q];
     }
-    // order the regions by (length desc, index asc)
     int r = 0, r_other = 0;  // this group's region, and the other unit's region for this group
 #pragma unroll
     for (int q = 0; q < kNR; ++q) {
@@ -217,7 +204,7 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
 #pragma unroll
       for (int o = 0; o < kNR; ++o) rank += (len[o] > len[q]) || (len[o] == len[q] && o < q);
       if (rank == kGPW * rp + h) r = q;
-      if (rank == kGPW * (1 - rp) + h) r_other = q;
+      if (kUPS > 1 && rank == kGPW * (1 - rp) + h) r_other = q;
     }
     int e0 = 0, L = 0;
 #pragma unroll
@@ -233,54 +220,66 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
     const int X0 = txi * kTile + 8 * (r & 1) + (j & 3), Y0 = tyi * kTile + kRH * (r >> 1) + (j >> 2);
     const int p0 = seg << kSegShift;
 
-    // ---- pixel state: q = 0 (X0, Y0), 1 (X0, Y0 + kDY) [pair A], 2, 3 [pair B, x + 4]
-    float T[4], R[4], g_r[4], g_g[4], g_b[4], g_d[4];
-    int nc[4];
+    // ---- pixel state: pair q = (column c = q / kNRG, row pair g = q % kNRG):
+    // pixels (X0 + 4c, Y0 + 2g kRS) and (X0 + 4c, Y0 + (2g + 1) kRS)
+    float2 T[kNQ], R[kNQ], gr[kNQ], gg[kNQ], gb[kNQ], gd[kNQ];
+    int nc[kNQ][2];
     bool nzl = false;
     const float* ck = seg > 0 ? ckpt + (ckpt_base[tile] + ((long long)seg << (kSegShift - 5)) - 1) *
                                            (5 * kTilePixels)
                               : nullptr;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int x = X0 + (q >> 1) * 4, y = Y0 + (q & 1) * kDY;
-      T[q] = 0.f;
-      R[q] = 0.f;
-      g_r[q] = g_g[q] = g_b[q] = g_d[q] = 0.f;
-      nc[q] = 0;
-      if (x < width && y < height) {
-        const long long pix = (long long)y * width + x;
-        g_r[q] = grad_color[3 * pix];
-        g_g[q] = grad_color[3 * pix + 1];
-        g_b[q] = grad_color[3 * pix + 2];
-        if (kDepth && grad_depth) g_d[q] = grad_depth[pix];
-        const float gt = grad_final_T ? grad_final_T[pix] : 0.f;
-        nzl |= (g_r[q] != 0.f) || (g_g[q] != 0.f) || (g_b[q] != 0.f) || (g_d[q] != 0.f) ||
-               (gt != 0.f);
-        nc[q] = n_considered[pix];
-        if (nc[q] > p0) {  // active in this segment
-          float k = g_r[q] * color[3 * pix] + g_g[q] * color[3 * pix + 1] +
-                    g_b[q] * color[3 * pix + 2] + gt * final_T[pix];
-          if (kDepth) k += g_d[q] * depth[pix];
-          float T0 = 1.f, K0 = 0.f;
-          if (ck) {
-            const int lp = (y - tyi * kTile) * kTile + (x - txi * kTile);
-            T0 = ck[lp];
-            K0 = g_r[q] * ck[kTilePixels + lp] + g_g[q] * ck[2 * kTilePixels + lp] +
-                 g_b[q] * ck[3 * kTilePixels + lp];
-            if (kDepth) K0 += g_d[q] * ck[4 * kTilePixels + lp];
+    for (int q = 0; q < kNQ; ++q) {
+      float v[2][6];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int x = X0 + 4 * (q / kNRG), y = Y0 + (2 * (q % kNRG) + e) * kRS;
+        float t0 = 0.f, r0 = 0.f, g_r = 0.f, g_g = 0.f, g_b = 0.f, g_d = 0.f;
+        int ncv = 0;
+        if (x < width && y < height) {
+          const long long pix = (long long)y * width + x;
+          g_r = grad_color[3 * pix];
+          g_g = grad_color[3 * pix + 1];
+          g_b = grad_color[3 * pix + 2];
+          if (kDepth && grad_depth) g_d = grad_depth[pix];
+          const float gt = grad_final_T ? grad_final_T[pix] : 0.f;
+          nzl |= (g_r != 0.f) || (g_g != 0.f) || (g_b != 0.f) || (g_d != 0.f) || (gt != 0.f);
+          ncv = n_considered[pix];
+          if (ncv > p0) {  // active in this segment
+            float k = g_r * color[3 * pix] + g_g * color[3 * pix + 1] + g_b * color[3 * pix + 2] +
+                      gt * final_T[pix];
+            if (kDepth) k += g_d * depth[pix];
+            float T0 = 1.f, K0 = 0.f;
+            if (ck) {
+              const int lp = (y - tyi * kTile) * kTile + (x - txi * kTile);
+              T0 = ck[lp];
+              K0 = g_r * ck[kTilePixels + lp] + g_g * ck[2 * kTilePixels + lp] +
+                   g_b * ck[3 * kTilePixels + lp];
+              if (kDepth) K0 += g_d * ck[4 * kTilePixels + lp];
+            }
+            t0 = T0;
+            r0 = k - K0;
           }
-          T[q] = T0;
-          R[q] = k - K0;
         }
+        v[e][0] = t0; v[e][1] = r0; v[e][2] = g_r; v[e][3] = g_g; v[e][4] = g_b; v[e][5] = g_d;
+        nc[q][e] = ncv;
       }
+      T[q] = f2(v[0][0], v[1][0]);
+      R[q] = f2(v[0][1], v[1][1]);
+      gr[q] = f2(v[0][2], v[1][2]);
+      gg[q] = f2(v[0][3], v[1][3]);
+      gb[q] = f2(v[0][4], v[1][4]);
+      gd[q] = f2(v[0][5], v[1][5]);
     }
     const bool nz = __any_sync(0xffffffffu, nzl);
     // merges follow the reference's count: every pair of a tile whose
     // upstream is not all zero (backward.py:156-158, 214-222)
     if (seg == 0 && rp == 0) {
-      const bool other = quad_nz(grad_color, kDepth ? grad_depth : nullptr, grad_final_T, width,
-                                 height, txi * kTile + 8 * (r_other & 1) + (j & 3),
-                                 tyi * kTile + kRH * (r_other >> 1) + (j >> 2), kDY);
+      bool other = false;
+      if (kUPS > 1)
+        other = quad_nz(grad_color, kDepth ? grad_depth : nullptr, grad_final_T, width, height,
+                        txi * kTile + 8 * (r_other & 1) + (j & 3),
+                        tyi * kTile + kRH * (r_other >> 1) + (j >> 2), kRS);
       if (__any_sync(0xffffffffu, nzl || other) && lane == 0)
         atomicAdd(merges, (unsigned long long)n);
     }
@@ -289,10 +288,10 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
     const uint32_t* lst = rlist + kNR * start + (long long)r * n + e0;
     const int32_t* vals = values + start;
     // Every list access is asynchronous (cp.async into shared memory, waited
-    // once per round), three stages per entry e of this lane's half:
+    // once per round), three stages per entry e of this lane's group:
     //   position  lst[e]          -> spos  (3 rounds ahead)
     //   row       values[pos]     -> srow  (2 rounds ahead)
-    //   record    rec[row] x 3    -> ring  (1 round ahead), (pos, row) -> pr
+    //   record    rec[row] x 3    -> ring  (1 round ahead)
     auto fetch_pos = [&](int e) {
       if (e < L) cp_async4(&spos[e & (kPR - 1)], lst + e);
       else spos[e & (kPR - 1)] = INT_MAX;
@@ -315,7 +314,7 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
         rc[slot] = zero4;
       }
     };
-    __syncwarp();  // the previous unit's flush has read the ring
+    __syncwarp();  // the previous unit's merge has read the ring
     // block -1 (the pipeline fill reads entries -kGL..-1): sentinels
     ra[kRing - kGL + j] = sent_a;
     rb[kRing - kGL + j] = sent_b;
@@ -335,22 +334,20 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
     stage(j);
     cp_async_commit();
 
-    const float xa = (float)X0 + 0.5f, xb = (float)(X0 + 4) + 0.5f;
-    const float2 yp = f2((float)Y0 + 0.5f, (float)(Y0 + kDY) + 0.5f);
-    float2 TA = f2(T[0], T[1]), TB = f2(T[2], T[3]);
-    float2 RA = f2(R[0], R[1]), RB = f2(R[2], R[3]);
-    const float2 grA = f2(g_r[0], g_r[1]), grB = f2(g_r[2], g_r[3]);
-    const float2 ggA = f2(g_g[0], g_g[1]), ggB = f2(g_g[2], g_g[3]);
-    const float2 gbA = f2(g_b[0], g_b[1]), gbB = f2(g_b[2], g_b[3]);
-    const float2 gdA = f2(g_d[0], g_d[1]), gdB = f2(g_d[2], g_d[3]);
-    const int nc0 = nc[0], nc1 = nc[1], nc2 = nc[2], nc3 = nc[3];
+    float xf[2];
+    xf[0] = (float)X0 + 0.5f;
+    xf[1] = (float)(X0 + 4) + 0.5f;
+    float2 yf[kNRG];
+#pragma unroll
+    for (int g = 0; g < kNRG; ++g)
+      yf[g] = f2((float)(Y0 + 2 * g * kRS) + 0.5f, (float)(Y0 + (2 * g + 1) * kRS) + 0.5f);
     float s_mx = 0.f, s_my = 0.f, s_a = 0.f, s_b = 0.f, s_c = 0.f, s_o = 0.f, s_r = 0.f,
           s_g = 0.f, s_bl = 0.f, s_d = 0.f;
     const float2 one = bc(1.f);
 
-    // one systolic step: entry t - j of this group for the lane's four pixels
-    // (A, B, pos) of a step are loaded one step ahead (ping-pong registers);
-    // the colour record C in the step (first used after the alpha chain)
+    // one systolic step: entry t - j of this group for the lane's kPX pixels
+    // (A, B, pos of a step are loaded one step ahead; the colour record C in
+    // the step, first used after the alpha chain)
     auto step = [&](const float4& A, const float4& B, int pos, int t) {
       const float4 C = rc[(t - j) & (kRing - 1)];
       float i_mx = __shfl_up_sync(0xffffffffu, s_mx, 1, kGL);
@@ -363,70 +360,83 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
       float i_g = __shfl_up_sync(0xffffffffu, s_g, 1, kGL);
       float i_bl = __shfl_up_sync(0xffffffffu, s_bl, 1, kGL);
       float i_d = kDepth ? __shfl_up_sync(0xffffffffu, s_d, 1, kGL) : 0.f;
-      // alpha of the four pixels: K3's operation sequence (eval_alpha)
+      // alpha: K3's operation sequence (eval_alpha) per pixel
       const float ca = __fmul_rn(A.z, kQScale), cb = __fmul_rn(A.w, 2.0f * kQScale),
                   cc = __fmul_rn(B.x, kQScale);
-      const float dx0 = __fsub_rn(xa, A.x), dx1 = __fsub_rn(xb, A.x);
-      const float2 dy = __fadd2_rn(yp, bc(-A.y));
-      const float dxx0 = __fmul_rn(dx0, dx0), dxx1 = __fmul_rn(dx1, dx1);
-      const float2 dyy = __fmul2_rn(dy, dy);
-      const float2 dxyA = __fmul2_rn(bc(dx0), dy), dxyB = __fmul2_rn(bc(dx1), dy);
-      const float2 cyy = __fmul2_rn(bc(cc), dyy);
-      const float2 qA = __ffma2_rn(bc(ca), bc(dxx0), __ffma2_rn(bc(cb), dxyA, cyy));
-      const float2 qB = __ffma2_rn(bc(ca), bc(dxx1), __ffma2_rn(bc(cb), dxyB, cyy));
-      const float2 gaA = f2(fast_exp2(qA.x), fast_exp2(qA.y));
-      const float2 gaB = f2(fast_exp2(qB.x), fast_exp2(qB.y));
-      const float2 rawA = __fmul2_rn(bc(B.y), gaA), rawB = __fmul2_rn(bc(B.y), gaB);
-      const float2 alA = f2(fminf(kAlphaCap, rawA.x), fminf(kAlphaCap, rawA.y));
-      const float2 alB = f2(fminf(kAlphaCap, rawB.x), fminf(kAlphaCap, rawB.y));
-      // non-participants get a = 0: w = 0, T and R unchanged exactly
-      const float2 aA = f2(participate(pos, nc0, alA.x), participate(pos, nc1, alA.y));
-      const float2 aB = f2(participate(pos, nc2, alB.x), participate(pos, nc3, alB.y));
-      const float2 omA = __fadd2_rn(one, f2(-aA.x, -aA.y));
-      const float2 omB = __fadd2_rn(one, f2(-aB.x, -aB.y));
-      float2 gcA = __ffma2_rn(grA, bc(C.x), __ffma2_rn(ggA, bc(C.y), __fmul2_rn(gbA, bc(C.z))));
-      float2 gcB = __ffma2_rn(grB, bc(C.x), __ffma2_rn(ggB, bc(C.y), __fmul2_rn(gbB, bc(C.z))));
-      if (kDepth) {
-        gcA = __ffma2_rn(gdA, bc(B.z), gcA);
-        gcB = __ffma2_rn(gdB, bc(B.z), gcB);
+      float dx[2], dxx[2];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        dx[c] = __fsub_rn(xf[c], A.x);
+        dxx[c] = __fmul_rn(dx[c], dx[c]);
       }
-      const float2 wA = __fmul2_rn(TA, aA), wB = __fmul2_rn(TB, aB);
-      const float2 numA = __ffma2_rn(f2(-wA.x, -wA.y), gcA, RA);
-      const float2 numB = __ffma2_rn(f2(-wB.x, -wB.y), gcB, RB);
-      const float2 rcA = f2(rcp_approx(omA.x), rcp_approx(omA.y));
-      const float2 rcB = f2(rcp_approx(omB.x), rcp_approx(omB.y));
-      const float2 dLA = __ffma2_rn(f2(-numA.x, -numA.y), rcA, __fmul2_rn(TA, gcA));
-      const float2 dLB = __ffma2_rn(f2(-numB.x, -numB.y), rcB, __fmul2_rn(TB, gcB));
-      TA = __fmul2_rn(TA, omA);
-      TB = __fmul2_rn(TB, omB);
-      RA = numA;
-      RB = numB;
-      // uncapped participants only (backward.py:64,72): a == raw exactly
-      // for them; a non-participant with raw == 0 has gauss == 0
-      const float2 ldA = f2(aA.x == rawA.x ? dLA.x : 0.f, aA.y == rawA.y ? dLA.y : 0.f);
-      const float2 ldB = f2(aB.x == rawB.x ? dLB.x : 0.f, aB.y == rawB.y ? dLB.y : 0.f);
-      const float2 gqA = __fmul2_rn(ldA, alA), gqB = __fmul2_rn(ldB, alB);
-      // region sums of this lane's four pixels, added to the incoming sums
-      const float2 hx = __ffma2_rn(gqB, bc(dx1), __fmul2_rn(gqA, bc(dx0)));  // per row: gq dx
-      const float2 gs = __fadd2_rn(gqA, gqB);                                // per row: gq
-      const float2 wr = __ffma2_rn(wB, grB, __fmul2_rn(wA, grA));
-      const float2 wg = __ffma2_rn(wB, ggB, __fmul2_rn(wA, ggA));
-      const float2 wbl = __ffma2_rn(wB, gbB, __fmul2_rn(wA, gbA));
-      s_mx = fmaf(i_mx, keep, hx.x + hx.y);
-      s_b = fmaf(hx.x, dy.x, fmaf(hx.y, dy.y, i_b * keep));
-      s_my = fmaf(gs.x, dy.x, fmaf(gs.y, dy.y, i_my * keep));
-      s_c = fmaf(gs.x, dyy.x, fmaf(gs.y, dyy.y, i_c * keep));
-      s_a = fmaf(dxx0, gqA.x + gqA.y, fmaf(dxx1, gqB.x + gqB.y, i_a * keep));
+      float2 dy[kNRG], dyy[kNRG], cyy[kNRG];
+#pragma unroll
+      for (int g = 0; g < kNRG; ++g) {
+        dy[g] = __fadd2_rn(yf[g], bc(-A.y));
+        dyy[g] = __fmul2_rn(dy[g], dy[g]);
+        cyy[g] = __fmul2_rn(bc(cc), dyy[g]);
+      }
+      float2 G[kNRG], H[kNRG];  // per row pair: sum gq, sum gq dx (over the two columns)
+      float Sq[2] = {0.f, 0.f};  // per column: sum gq
+      float2 wr = bc(0.f), wg = bc(0.f), wbl = bc(0.f), wd = bc(0.f);
+#pragma unroll
+      for (int g = 0; g < kNRG; ++g) {
+        G[g] = bc(0.f);
+        H[g] = bc(0.f);
+      }
+#pragma unroll
+      for (int q = 0; q < kNQ; ++q) {
+        const int c = q / kNRG, g = q % kNRG;
+        const float2 dxy = __fmul2_rn(bc(dx[c]), dy[g]);
+        const float2 qs = __ffma2_rn(bc(ca), bc(dxx[c]), __ffma2_rn(bc(cb), dxy, cyy[g]));
+        const float2 ga = f2(fast_exp2(qs.x), fast_exp2(qs.y));
+        const float2 raw = __fmul2_rn(bc(B.y), ga);
+        const float2 al = f2(fminf(kAlphaCap, raw.x), fminf(kAlphaCap, raw.y));
+        // non-participants get a = 0: w = 0, T and R unchanged exactly
+        const float2 a = f2(participate(pos, nc[q][0], al.x), participate(pos, nc[q][1], al.y));
+        const float2 om = __fadd2_rn(one, f2(-a.x, -a.y));
+        float2 gc = __ffma2_rn(gr[q], bc(C.x), __ffma2_rn(gg[q], bc(C.y), __fmul2_rn(gb[q], bc(C.z))));
+        if (kDepth) gc = __ffma2_rn(gd[q], bc(B.z), gc);
+        const float2 w = __fmul2_rn(T[q], a);
+        const float2 num = __ffma2_rn(f2(-w.x, -w.y), gc, R[q]);
+        const float2 rcp = f2(rcp_approx(om.x), rcp_approx(om.y));
+        const float2 dL = __ffma2_rn(f2(-num.x, -num.y), rcp, __fmul2_rn(T[q], gc));
+        T[q] = __fmul2_rn(T[q], om);
+        R[q] = num;
+        // uncapped participants only (backward.py:64,72): a == raw exactly
+        // for them; a non-participant with raw == 0 has gauss == 0
+        const float2 ld = f2(a.x == raw.x ? dL.x : 0.f, a.y == raw.y ? dL.y : 0.f);
+        const float2 gq = __fmul2_rn(ld, al);
+        G[g] = __fadd2_rn(G[g], gq);
+        H[g] = __ffma2_rn(gq, bc(dx[c]), H[g]);
+        Sq[c] += gq.x + gq.y;
+        wr = __ffma2_rn(w, gr[q], wr);
+        wg = __ffma2_rn(w, gg[q], wg);
+        wbl = __ffma2_rn(w, gb[q], wbl);
+        if (kDepth) wd = __ffma2_rn(w, gd[q], wd);
+      }
+      // region sums of this lane's pixels, added to the incoming sums
+      float t_mx = 0.f, t_b = 0.f, t_my = 0.f, t_c = 0.f, t_o = 0.f;
+#pragma unroll
+      for (int g = 0; g < kNRG; ++g) {
+        t_mx += H[g].x + H[g].y;
+        t_b = fmaf(H[g].x, dy[g].x, fmaf(H[g].y, dy[g].y, t_b));
+        t_my = fmaf(G[g].x, dy[g].x, fmaf(G[g].y, dy[g].y, t_my));
+        t_c = fmaf(G[g].x, dyy[g].x, fmaf(G[g].y, dyy[g].y, t_c));
+        t_o += G[g].x + G[g].y;
+      }
+      s_mx = fmaf(i_mx, keep, t_mx);
+      s_b = fmaf(i_b, keep, t_b);
+      s_my = fmaf(i_my, keep, t_my);
+      s_c = fmaf(i_c, keep, t_c);
+      s_a = fmaf(dxx[0], Sq[0], fmaf(dxx[1], Sq[1], i_a * keep));
       // sum ld gauss = (sum ld alpha) / o for uncapped participants (alpha =
-      // o gauss): the per-row sums gs already hold it; the merge divides by o
-      s_o = fmaf(i_o, keep, gs.x + gs.y);
+      // o gauss): the sum of gq holds it; the merge divides by o
+      s_o = fmaf(i_o, keep, t_o);
       s_r = fmaf(i_r, keep, wr.x + wr.y);
       s_g = fmaf(i_g, keep, wg.x + wg.y);
       s_bl = fmaf(i_bl, keep, wbl.x + wbl.y);
-      if (kDepth) {
-        const float2 wd = __ffma2_rn(wB, gdB, __fmul2_rn(wA, gdA));
-        s_d = fmaf(i_d, keep, wd.x + wd.y);
-      }
+      if (kDepth) s_d = fmaf(i_d, keep, wd.x + wd.y);
       if (j == kGL - 1) {  // entry t - (kGL - 1) is complete: park its sums
         const int o = (t - (kGL - 1)) & (kOut - 1);
         oa[o][h] = make_float4(s_mx, s_my, s_a, s_b);
@@ -445,8 +455,8 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
         return;
       const int slot = e & (kRing - 1);
       const float4 sa = ra[slot];
-      const float4 sb = rb[slot];
-      const float cc = __fmul_rn(sb.x, kQScale);
+      const float4 sbr = rb[slot];
+      const float cc = __fmul_rn(sbr.x, kQScale);
       const float ca = __fmul_rn(sa.z, kQScale), hb = __fmul_rn(sa.w, kQScale);  // (2b') / 2
       const int row = srow[e & (kPR - 1)];
       // sum gq u = a' sum gq dx + b' sum gq dy, likewise v (the conic's rows)
@@ -455,7 +465,7 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
       float* dst = grad2d + (long long)row * TSR_GRAD2D_FLOATS;
       red_add2(dst + 0, ms * 0.5f * uu, ms * 0.5f * vv);
       red_add2(dst + 2, -0.5f * A.z, -A.w);
-      red_add2(dst + 4, -0.5f * B.x, __fdiv_rn(B.y, sb.y));  // sum ld gauss (see the step)
+      red_add2(dst + 4, -0.5f * B.x, __fdiv_rn(B.y, sbr.y));  // sum ld gauss (see the step)
       red_add2(dst + 6, B.z, B.w);
       red_add2(dst + 8, Cc.x, kDepth ? Cc.y : 0.f);
     };
@@ -483,7 +493,7 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
 #pragma unroll 1
       for (int i = 0; i < kGL; i += 2) {
         const int t = kGL * k + i;
-        if (TSR_K4R_EXIT && t >= steps) break;  // the last round stops at its last step
+        if (t >= steps) break;  // the last round stops at its last step
         if (i == kGL - 2) {  // block k + 1 (the next step's lane 0 entry) has landed
           cp_async_wait_all();
           __syncwarp();
@@ -539,11 +549,18 @@ extern "C" int tsr_render_bwd_regions(const float* rec, const int32_t* values,
   const int tx = tiles_of(width), ty = tiles_of(height), n_tiles = tx * ty;
   if (n_tiles >= (1 << 16)) return TSR_E_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
-  auto* k = region_height == 8
-                ? (grad_depth ? render_bwd_regions_kernel<true, 16> : render_bwd_regions_kernel<false, 16>)
-                : (grad_depth ? render_bwd_regions_kernel<true, 8> : render_bwd_regions_kernel<false, 8>);
-  static int per_sm[4] = {0, 0, 0, 0}, sms = 0;
-  int& ps = per_sm[(grad_depth ? 1 : 0) + (region_height == 8 ? 2 : 0)];
+  // 8x8 regions: 16 lanes x 4 pixels (TSR_K4R_PX=4) or 8 lanes x 8 pixels
+  // (TSR_K4R_PX=8); 8x4 regions: 8 lanes x 4 pixels
+  static const int px = getenv("TSR_K4R_PX") ? atoi(getenv("TSR_K4R_PX")) : 4;
+  const int shape = region_height == 4 ? 2 : (px == 8 ? 1 : 0);
+  using KFn = decltype(&render_bwd_regions_kernel<false, 16, 4>);
+  KFn table[3][2] = {
+      {render_bwd_regions_kernel<false, 16, 4>, render_bwd_regions_kernel<true, 16, 4>},
+      {render_bwd_regions_kernel<false, 8, 8>, render_bwd_regions_kernel<true, 8, 8>},
+      {render_bwd_regions_kernel<false, 8, 4>, render_bwd_regions_kernel<true, 8, 4>}};
+  KFn k = table[shape][grad_depth ? 1 : 0];
+  static int per_sm[6] = {0, 0, 0, 0, 0, 0}, sms = 0;
+  int& ps = per_sm[2 * shape + (grad_depth ? 1 : 0)];
   if (ps == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
