@@ -106,7 +106,7 @@ __device__ __forceinline__ long long clamp_ll(long long n, long long cap) {
 // used once per call (zeroed by the memset), so no sense reversal is needed.
 #ifdef TSR_K2_TRACE
 // instrumented build only (tools/k2_trace.py): CTA 0 stamps every barrier
-__device__ unsigned long long tsr_k2_trace_buf[64];
+__device__ unsigned long long tsr_k2_trace_buf[128];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -116,9 +116,17 @@ __device__ __forceinline__ unsigned long long gtimer() {
   do {                                                                         \
     if (blockIdx.x == 0 && threadIdx.x == 0) tsr_k2_trace_buf[i] = gtimer(); \
   } while (0)
+#define TSR_TRACE_SUB(call, i)                                                     \
+  do {                                                                             \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && base == lo)                          \
+      tsr_k2_trace_buf[64 + 6 * ((call) % 10) + (i)] = gtimer();                   \
+  } while (0)
 #else
 #define TSR_TRACE_AT(i) \
   do {                 \
+  } while (0)
+#define TSR_TRACE_SUB(call, i) \
+  do {                        \
   } while (0)
 #endif
 
@@ -263,7 +271,7 @@ __device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restr
                               const uint32_t* __restrict__ colscan_row,
                               const uint32_t* __restrict__ dtotal, SortSmem& sm,
                               unsigned char* dyn, const uint32_t* __restrict__ gather = nullptr,
-                              uint32_t* __restrict__ inv = nullptr) {
+                              uint32_t* __restrict__ inv = nullptr, int call = 0) {
   constexpr bool kVals = true;
   K* s_keys = reinterpret_cast<K*>(dyn);
   uint32_t* s_vals = reinterpret_cast<uint32_t*>(dyn + kSub * sizeof(K));
@@ -275,19 +283,28 @@ __device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restr
     const uint32_t dstart = block_excl_scan(dtotal[tid], sm.w32, &total);
     sm.run[tid] = dstart + colscan_row[tid];
   }
-  for (long long base = lo; base < hi; base += kSub) {
-#pragma unroll
-    for (int w = 0; w < kSB / 32; ++w) sm.cnt[w][tid] = 0;
-    __syncthreads();
-    const long long wb = base + (long long)warp * (32 * kItems);
-    K key[kItems];
-    uint32_t val[kItems], packed[kItems];
+  // the sub-tile's items are loaded one sub-tile ahead: the next sub-tile's
+  // loads are issued once this one's items are staged in shared memory, so
+  // they overlap the staged read-back and the global stores
+  K key[kItems];
+  uint32_t val[kItems];
+  auto load_items = [&](long long b) {
+    const long long wb = b + (long long)warp * (32 * kItems);
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {  // all loads in flight first
       const long long i = wb + r * 32 + lane;
       key[r] = i < hi ? kin[i] : (K)0;
       if (kVals) val[r] = i < hi ? (vin ? vin[i] : (uint32_t)i) : 0u;
     }
+  };
+  if (lo < hi) load_items(lo);
+  for (long long base = lo; base < hi; base += kSub) {
+#pragma unroll
+    for (int w = 0; w < kSB / 32; ++w) sm.cnt[w][tid] = 0;
+    __syncthreads();
+    const long long wb = base + (long long)warp * (32 * kItems);
+    uint32_t packed[kItems];
+    TSR_TRACE_SUB(call, 0);
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
       const bool valid = wb + r * 32 + lane < hi;
@@ -301,6 +318,7 @@ __device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restr
       __syncwarp();
       packed[r] = valid ? ((d << 16) | (c + before)) : 0xffffffffu;
     }
+    TSR_TRACE_SUB(call, 1);
     __syncthreads();
     // digit tid: exclusive prefix over warps (input order), sub-tile total
     uint32_t tot = 0;
@@ -313,6 +331,7 @@ __device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restr
     uint32_t dummy;
     sm.lbase[tid] = block_excl_scan(tot, sm.w32, &dummy);
     __syncthreads();
+    TSR_TRACE_SUB(call, 2);
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
       if (packed[r] != 0xffffffffu) {
@@ -323,6 +342,8 @@ __device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restr
       }
     }
     __syncthreads();
+    TSR_TRACE_SUB(call, 3);
+    if (base + kSub < hi) load_items(base + kSub);
     const int n_here = (int)(hi - base < kSub ? hi - base : kSub);
     {
       // all kItems items of the thread in flight at once (the det-mode
@@ -350,8 +371,12 @@ __device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restr
       }
     }
     __syncthreads();
+    TSR_TRACE_SUB(call, 4);
     sm.run[tid] += tot;
   }
+#ifdef TSR_K2_TRACE
+  if (blockIdx.x == 0 && threadIdx.x == 0) tsr_k2_trace_buf[64 + 6 * (call % 10) + 5] = gtimer();
+#endif
 }
 
 // ---- one full radix pass (3 phases, 3 grid barriers)
@@ -368,7 +393,7 @@ __device__ void radix_pass(const IndexArgs& a, int& nb, const K* kin, const uint
   colscan_phase(a.cnt, a.colscan, a.dtotal, G, sm);
   grid_barrier(a.bar + nb++, G);
   scatter_phase<K>(kin, vin, kout, vout, lo, hi, shift, bits, a.colscan + (long long)bid * kBins,
-                   a.dtotal, sm, dyn, gather, inv);
+                   a.dtotal, sm, dyn, gather, inv, nb / 3);
   grid_barrier(a.bar + nb++, G);
 }
 

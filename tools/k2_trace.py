@@ -24,7 +24,7 @@ for _ in range(5):
     torch.cuda.synchronize()
     if not hasattr(lib, "tsr_k2_trace_read"):  # plain build (e.g. under ncu)
         continue
-    buf = (ctypes.c_ulonglong * 64)()
+    buf = (ctypes.c_ulonglong * 128)()
     lib.tsr_k2_trace_read(buf, None)
     t = np.array(buf[:33], dtype=np.int64)
     n = int(np.count_nonzero(t[1:]))
@@ -32,3 +32,8 @@ for _ in range(5):
     e = np.array(buf[40:48], dtype=np.int64)
     print("   emission CTA0 (gathers, scan, window-expand..., rewalk, end, expand, copy, kernel end):",
           [round((x - t[0]) / 1e3, 1) for x in e])
+    for c in range(10):
+        sub = np.array(buf[64 + 6 * c:70 + 6 * c], dtype=np.int64)
+        if sub[0]:
+            print(f"   scatter call {c} CTA0 first sub-tile (loads, rank, scan, stage, store, phase end):",
+                  [round((x - t[0]) / 1e3, 1) for x in sub])
