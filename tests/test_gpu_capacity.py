@@ -42,13 +42,17 @@ def _run(ts, params, cams, gt, steps, small_cap=None, deterministic=True):
     return st, gset, losses
 
 
-@pytest.mark.parametrize("deterministic", [True, False])
-def test_overflowed_steps_are_redone_with_grown_capacity(deterministic):
+@pytest.mark.parametrize("deterministic,regions", [(True, False), (False, False), (False, True)])
+def test_overflowed_steps_are_redone_with_grown_capacity(deterministic, regions, monkeypatch):
+    if regions:  # the region-culled K3/K4r pair forced on this small frame
+        from paper_2601_19489_b200 import backward as bw
+        monkeypatch.setattr(bw, "REGIONS_MIN_PAIRS", 0)
     ts, params, cams, gt = _setup()
     a, ga, la = _run(ts, params, cams, gt, 6, deterministic=deterministic)
     b, gb, lb = _run(ts, params, cams, gt, 6, small_cap=0.4, deterministic=deterministic)
     assert a.redone_steps == 0
     assert b.redone_steps >= 1  # the undersized steps were skipped and redone
+    assert (a.regions is not None) == regions and (b.regions is not None) == regions
     assert b.index.p_cap > a.index.p_cap * 0.4
     assert int(b.index.overflow.item()) == 0
     for k in ga.params():

@@ -168,13 +168,19 @@ def test_c3_clustered_heavy_tiles_binning_exact_and_bounded_work():
     assert g2.merges == vr.tiles.n_pairs
 
 
-def test_graph_replayed_train_step_matches_eager():
+@pytest.mark.parametrize("k4", ["auto", "regions"])
+def test_graph_replayed_train_step_matches_eager(k4, monkeypatch):
     """TrainStep(graphs=True) replays one captured CUDA graph per (camera, GT)
     with the per-step Adam scalars and depth weight fed through pinned-memory
     copy nodes; parameters after several steps (alternating two GT buffers,
-    depth supervision on) match the eager step within FP32 tolerance."""
+    depth supervision on) match the eager step within FP32 tolerance.
+    k4="regions" forces the region-culled K3/K4r pair on this small frame
+    (the training step's form at C2 size), incl. its depth channel."""
     import torch
     import paper_2601_19489_b200 as ts
+    if k4 == "regions":
+        from paper_2601_19489_b200 import backward as bw
+        monkeypatch.setattr(bw, "REGIONS_MIN_PAIRS", 0)
     from oracle.raster import make_scene
     params, cam, gt = make_scene(20_000, 320, 240, seed=8)
     camera = ts.Camera(cam["fx"], cam["fy"], cam["cx"], cam["cy"], 320, 240, cam["R"], cam["t"])
@@ -195,6 +201,7 @@ def test_graph_replayed_train_step_matches_eager():
         torch.cuda.synchronize()
         out[run] = g.to_numpy()
         losses[run] = ls
+        assert (st.regions is not None) == (k4 == "regions")
         if graphs:
             assert len(st._graph_cache) >= 2  # two GT buffers (and depth on/off)
     assert np.allclose(losses["eager"], losses["graph"], rtol=1e-5, atol=1e-7)
