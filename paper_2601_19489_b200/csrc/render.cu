@@ -76,6 +76,7 @@ struct PixPair {
   float2 nc;  // blends so far (exact small integers; one packed add per entry)
   int ncons0, ncons1;
   bool strong0, strong1;  // last blend was a strong contribution (w >= 1/255)
+  bool part0, part1;      // last entry blended (the backward's participation)
   __device__ __forceinline__ bool alive0() const { return T.x >= kTTerminate; }
   __device__ __forceinline__ bool alive1() const { return T.y >= kTTerminate; }
 };
@@ -109,6 +110,8 @@ __device__ __forceinline__ void blend_pair(const float4 g, const float4 c, const
   const float2 w = __fmul2_rn(s.T, a);
   s.strong0 = b0 && (w.x >= kMinAlpha);
   s.strong1 = b1 && (w.y >= kMinAlpha);
+  s.part0 = b0;
+  s.part1 = b1;
   s.Cr = __ffma2_rn(w, bc2(col.x), s.Cr);
   s.Cg = __ffma2_rn(w, bc2(col.y), s.Cg);
   s.Cb = __ffma2_rn(w, bc2(col.z), s.Cb);
@@ -119,11 +122,12 @@ __device__ __forceinline__ void blend_pair(const float4 g, const float4 c, const
   s.ncons1 = live1 ? pos + 1 : s.ncons1;
 }
 
-// Region lists for the region-culled backward (kCkpt 3, backward_regions.cu):
-// warp w's 8x8 block is region w of the tile; every list position whose splat
-// passes the block test is appended to the region's list (in list order, so
-// the list is a superset of the positions that blend in the block, cut at the
-// chunk where the block's last pixel died).  Region r of tile t stores its
+// Region lists for the region-culled backward (kCkpt 3/4, backward_regions.cu):
+// warp w's 8x8 block is region w of the tile (or its two 8x4 halves); every
+// list position that blends at >= 1 pixel of the region is appended to the
+// region's list, in list order -- exactly the entries with a participating
+// pixel (p < n_considered, alpha >= 1/255) in the backward; the others
+// contribute exact zeros there.  Region r of tile t stores its
 // positions at list[4 start_t + r n_t ...]; seg[4 (segbase_t + s - 1) + r]
 // holds the number of entries with position < kSeg s for s = 1..ceil(n/kSeg)
 // (segbase_t = (start_t >> 10) + t: floor((O + n) / kSeg) - floor(O / kSeg)
@@ -251,32 +255,27 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
         ++s_next;
       }
       // lane j tests splat c0 + j against this warp's 8x8 block
-      bool hit = false, hit2 = false;
+      bool hit = false;
       if (lane < cend) {
         const float4 g = s_spl[c0 + lane][0], rw = s_raw[c0 + lane];
-        if (kCkpt == 4) {  // the two 8x4 halves (their union is the 8x8 block)
-          hit = strip_hit(g.x, g.y, rw.x, rw.y, rw.z, rw.w, sx0, sx0 + 7.f, sy0, sy0 + 3.f);
-          hit2 = strip_hit(g.x, g.y, rw.x, rw.y, rw.z, rw.w, sx0, sx0 + 7.f, sy0 + 4.f, sy0 + 7.f);
-        } else {
-          hit = strip_hit(g.x, g.y, rw.x, rw.y, rw.z, rw.w, sx0, sx0 + 7.f, sy0, sy0 + 7.f);
-        }
+        hit = strip_hit(g.x, g.y, rw.x, rw.y, rw.z, rw.w, sx0, sx0 + 7.f, sy0, sy0 + 7.f);
       }
       unsigned mask = __ballot_sync(0xffffffffu, hit);
-      if (kRegions) {
-        if (hit) rl[r_count + __popc(mask & lt_mask)] = (uint32_t)(pos0 + lane);
-        r_count += __popc(mask);
-      }
-      if (kCkpt == 4) {
-        const unsigned mask2 = __ballot_sync(0xffffffffu, hit2);
-        if (hit2) rl2[r_count2 + __popc(mask2 & lt_mask)] = (uint32_t)(pos0 + lane);
-        r_count2 += __popc(mask2);
-        mask |= mask2;
-      }
+      // region lists: the chunk's positions that blend at >= 1 pixel of the
+      // region (exactly the backward's participating entries), from the
+      // blends below
+      unsigned pm0 = 0u, pm1 = 0u;
       while (mask) {
         const int j = __ffs(mask) - 1;
         mask &= mask - 1u;
         const float4* sp = s_spl[c0 + j];
         blend_pair(sp[0], sp[1], sp[2], pxf, pyf, pos0 + j, s);
+        if (kCkpt == 4) {  // 8x4 halves: rows of the lanes' first / second pixels
+          if (__any_sync(0xffffffffu, s.part0)) pm0 |= 1u << j;
+          if (__any_sync(0xffffffffu, s.part1)) pm1 |= 1u << j;
+        } else if (kRegions) {
+          if (__any_sync(0xffffffffu, s.part0 || s.part1)) pm0 |= 1u << j;
+        }
         if (kScore) {
           const unsigned q0 = __ballot_sync(0xffffffffu, kScore == 3 ? s.strong0 && m0 : s.strong0);
           const unsigned q1 = __ballot_sync(0xffffffffu, kScore == 3 ? s.strong1 && m1 : s.strong1);
@@ -300,6 +299,14 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
             sc_cursor += nq;
           }
         }
+      }
+      if (kRegions) {
+        if ((pm0 >> lane) & 1u) rl[r_count + __popc(pm0 & lt_mask)] = (uint32_t)(pos0 + lane);
+        r_count += __popc(pm0);
+      }
+      if (kCkpt == 4) {
+        if ((pm1 >> lane) & 1u) rl2[r_count2 + __popc(pm1 & lt_mask)] = (uint32_t)(pos0 + lane);
+        r_count2 += __popc(pm1);
       }
       if (kCkpt && cend == kGroup &&
           (kCkpt == 1 || (kCkpt == 2 && ((pos0 >> 5) & 1)) ||

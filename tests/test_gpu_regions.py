@@ -115,8 +115,10 @@ def test_regions_zero_upstream_half_tile(region_height):
 
 @pytest.mark.parametrize("region_height", [4, 8])
 def test_region_lists_cover_every_blend(region_height):
-    """Each region list is increasing, within [0, n), and holds every list
-    position that blends at a pixel of the region (oracle participation)."""
+    """Each region list is increasing, within [0, n), and holds exactly the
+    list positions that blend at >= 1 pixel of the region (the backward's
+    participation, oracle alphas; positions whose alpha is within 1e-5 of
+    the 1/255 threshold at every such pixel may go either way in FP32)."""
     ts, vr, gt = _scene(4_000, 96, 64, seed=9)
     hb, hi = host_batch(vr.batch), host_index(vr.tiles)
     tgt, reg, _ = regions_pass(vr, np.zeros((64, 96, 3)), region_height=region_height)
@@ -140,12 +142,14 @@ def test_region_lists_cover_every_blend(region_height):
             gy, gx = np.mgrid[y0:y1, x0:x1]
             px, py = gx.reshape(-1) + 0.5, gy.reshape(-1) + 0.5
             nc = np64(vr.buffers.n_considered)[y0:y1, x0:x1].reshape(-1)
-            need = []
+            need, may = [], []
             for k in range(n):
                 al = O._alpha(hb, hi["values"][lo + k], px, py)[0]
-                if np.any((al >= 1 / 255) & (k < nc)):
+                if np.any((al >= (1 / 255) * (1 + 1e-5)) & (k < nc)):
                     need.append(k)
-            assert set(need) <= set(ent.tolist()), (tile, r)
+                if np.any((al >= (1 / 255) * (1 - 1e-5)) & (k < nc)):
+                    may.append(k)
+            assert set(need) <= set(ent.tolist()) <= set(may), (tile, r)
 
 
 def test_train_step_region_k4_matches_tile_k4(monkeypatch):
