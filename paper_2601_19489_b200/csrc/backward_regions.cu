@@ -13,13 +13,13 @@
 // What differs is the schedule.  K4 keeps splats in lanes and streams every
 // active pixel of the tile past them, so each (pixel, splat) pair of the
 // tile's list costs a full evaluation.  K4r keeps PIXELS in lanes and
-// streams the splats past them, and only the splats that can reach
-// alpha >= 1/255 somewhere in the lanes' 8x8 region: K3 already decides that
-// per (8x8 block, list position) for its own culling and writes the passing
-// positions as the region's list (render.cu, RegionArgs).  A splat that
-// fails the test contributes exact zeros to every pixel of the region, so
-// skipping it changes nothing; at C2 the region lists hold ~55 % of the
-// tile-list evaluations.
+// streams the splats past them, and only the splats that blend at >= 1 pixel
+// of the lanes' 8x8 region: K3 sees every blend and writes, per (tile, 8x8
+// block), the list positions with a blending pixel as the region's list
+// (render.cu, RegionArgs) -- exactly the entries with a participating pixel
+// (p < n_considered, alpha >= 1/255) here, since K4r evaluates K3's alphas
+// bit for bit.  Every other entry contributes exact zeros to every pixel of
+// the region, so skipping it changes nothing.
 //
 // Layout.  A warp is one work unit (tile, pair p, segment): its two 16-lane
 // halves run two of the tile's four 8x8 regions (bx, by) -- the segment's two
