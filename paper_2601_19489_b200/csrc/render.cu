@@ -244,7 +244,21 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
     const int cnt = min(kBatch, n - b0);
     // chunks of 32 list positions == one checkpoint interval
     for (int c0 = 0; c0 < cnt; c0 += kGroup) {
-      if (!__any_sync(0xffffffffu, s.alive0() || s.alive1())) break;  // warp-level early exit
+      const unsigned live_lo = __ballot_sync(0xffffffffu, s.alive0()),
+                     live_hi = __ballot_sync(0xffffffffu, s.alive1());
+      if (!(live_lo | live_hi)) break;  // warp-level early exit
+      // the test rectangle: the pixel centres of the block's LIVE pixels (a
+      // dead pixel never blends again, forward.py:125-138), from the two
+      // ballots: lane l holds column l & 7 and rows l >> 3 (live_lo), 4 + (l >> 3) (live_hi)
+      const unsigned mm = live_lo | live_hi;
+      const unsigned cols = (mm | (mm >> 8) | (mm >> 16) | (mm >> 24)) & 0xffu;
+      auto rows_of = [](unsigned m) {
+        return (unsigned)((m & 0xffu) != 0u) | ((unsigned)((m & 0xff00u) != 0u) << 1) |
+               ((unsigned)((m & 0xff0000u) != 0u) << 2) | ((unsigned)((m & 0xff000000u) != 0u) << 3);
+      };
+      const unsigned rows = rows_of(live_lo) | (rows_of(live_hi) << 4);
+      const float bx0 = sx0 + (float)(__ffs(cols) - 1), bx1 = sx0 + (float)(31 - __clz(cols));
+      const float by0 = sy0 + (float)(__ffs(rows) - 1), by1 = sy0 + (float)(31 - __clz(rows));
       const int cend = min(kGroup, cnt - c0);
       const int pos0 = b0 + c0;
       if (kRegions && pos0 > 0 && (pos0 & (kSeg - 1)) == 0) {  // segment boundary
@@ -258,7 +272,7 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
       bool hit = false;
       if (lane < cend) {
         const float4 g = s_spl[c0 + lane][0], rw = s_raw[c0 + lane];
-        hit = strip_hit(g.x, g.y, rw.x, rw.y, rw.z, rw.w, sx0, sx0 + 7.f, sy0, sy0 + 7.f);
+        hit = strip_hit(g.x, g.y, rw.x, rw.y, rw.z, rw.w, bx0, bx1, by0, by1);
       }
       unsigned mask = __ballot_sync(0xffffffffu, hit);
       // region lists: the chunk's positions that blend at >= 1 pixel of the
