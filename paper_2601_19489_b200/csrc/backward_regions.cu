@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
     const int tyi = tile / tiles_x, txi = tile - tyi * tiles_x;
     const int X0 = txi * kTile + 8 * (r & 1) + (j & 3), Y0 = tyi * kTile + kRH * (r >> 1) + (j >> 2);
     const int p0 = seg << kSegShift;
+    if (Lmax == 0 && !(seg == 0 && rp == 0)) continue;  // nothing to stream (no merge count either)
 
     // ---- pixel state: pair q = (column c = q / kNRG, row pair g = q % kNRG):
     // pixels (X0 + 4c, Y0 + 2g kRS) and (X0 + 4c, Y0 + (2g + 1) kRS)
