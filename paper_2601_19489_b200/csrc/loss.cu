@@ -21,6 +21,9 @@
 
 namespace tsr {
 
+#ifndef TSR_SSIM_MINB
+#define TSR_SSIM_MINB 4  // 5 (51 registers) measured slower: 70 / 71 us
+#endif
 constexpr int kLT = 32;              // output tile
 constexpr int kLR = 5;               // filter radius
 constexpr int kLIn = kLT + 2 * kLR;  // 42 rows/cols incl. halo
@@ -96,7 +99,7 @@ __device__ __forceinline__ void load_halo2(const float* __restrict__ r, const fl
 // for (mu1, mu2), one for (E[r^2], E[g^2]) and one scalar FFMA for E[rg]
 // (5 FFMA before); every lane of a packed op is an IEEE FMA, so the sums are
 // bit-identical to the scalar form.
-__global__ void __launch_bounds__(256, 4) ssim_fwd_kernel(const float* __restrict__ r,
+__global__ void __launch_bounds__(256, TSR_SSIM_MINB) ssim_fwd_kernel(const float* __restrict__ r,
                                                        const float* __restrict__ g, int H, int W,
                                                        float inv_n, float2* __restrict__ Q01,
                                                        float* __restrict__ Q2,
@@ -265,7 +268,7 @@ __device__ void loss_finalize(const double* __restrict__ partials, int n_blocks,
   }
 }
 
-__global__ void __launch_bounds__(256, 4) ssim_bwd_kernel(
+__global__ void __launch_bounds__(256, TSR_SSIM_MINB) ssim_bwd_kernel(
     const float* __restrict__ r, const float* __restrict__ g, int H, int W, float lam,
     float inv_n, const float2* __restrict__ Q01, const float* __restrict__ Q2,
     float* __restrict__ grad, Win win, const double* __restrict__ partials, int n_blocks,
