@@ -283,14 +283,19 @@ __global__ void __launch_bounds__(128, TSR_VJP_MINB) vjp_adam_sh0_kernel(
 }
 
 // ---- fused ZeRO-1 update over peer memory (the B200 variant)
-// One thread per (group, shard row): the gradient row is the sum of the
-// ranks' rows read through peer pointers in rank order (bitwise the
-// deterministic fixed-order reduction), Adam runs on the local parameter
-// row with this rank's shard moments, and the updated row is stored into
-// every rank's parameter buffer -- reduce-scatter + K5 + all-gather as one
-// kernel, no collective library.
+// One CTA per (group, 64-row chunk of this rank's shard): the chunk's
+// gradient is the sum of the ranks' rows read through peer pointers in rank
+// order (bitwise the deterministic fixed-order reduction) with consecutive
+// threads on consecutive floats (every peer read is a coalesced 128-byte
+// line over NVLink, not a row-strided scalar), Adam runs element-wise on
+// the local parameters with this rank's shard moments (rows with a
+// non-finite gradient untouched, the quaternion rows renormalised), and the
+// updated chunk is stored into every rank's parameter buffer, again
+// coalesced -- reduce-scatter + K5 + all-gather as one kernel, no collective
+// library.  Rows are staged in shared memory for the row-level parts.
 constexpr int kPeerMaxWorld = 8;
 constexpr int kPeerMaxWidth = 48;  // colors at SH degree 3
+constexpr int kPeerRows = 64;
 struct PeerPtrs {
   const float* g[kPeerMaxWorld * TSR_MAX_ADAM_GROUPS];  // [rank * n_groups + group]
   float* p[kPeerMaxWorld * TSR_MAX_ADAM_GROUPS];
@@ -298,60 +303,65 @@ struct PeerPtrs {
 
 __global__ void __launch_bounds__(256) zero1_peer_adam_kernel(AdamGroups groups, PeerPtrs pp,
                                                               int world, long long row_begin,
+                                                              long long rows,
                                                               unsigned long long* __restrict__ skipped) {
-  const long long total = groups.row_start[groups.n];
-  const int ng = groups.n;
-  unsigned long long local = 0;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    int gi = 0;
-    while (t >= groups.row_start[gi + 1]) ++gi;
-    const tsr_adam_group_t& G = groups.g[gi];
-    const long long r = t - groups.row_start[gi];  // shard row (moments)
-    const long long row = row_begin + r;           // parameter row
-    const int w = G.width;
-    float gsum[kPeerMaxWidth];
-    bool finite = true;
-    for (int k = 0; k < w; ++k) {
-      float acc = pp.g[gi][row * w + k];
-      for (int q = 1; q < world; ++q) acc += pp.g[q * ng + gi][row * w + k];
-      gsum[k] = acc;
-      finite &= isfinite(acc);
+  extern __shared__ float s_peer[];
+  const int gi = blockIdx.y, ng = groups.n, tid = threadIdx.x;
+  const tsr_adam_group_t& G = groups.g[gi];
+  const int w = G.width;
+  const long long r0 = (long long)blockIdx.x * kPeerRows;
+  if (r0 >= rows) return;
+  const int nr = (int)min((long long)kPeerRows, rows - r0), ne = nr * w;
+  float* s_g = s_peer;                                   // summed gradients
+  float* s_p = s_peer + kPeerRows * kPeerMaxWidth;       // updated parameters
+  int* s_ok = reinterpret_cast<int*>(s_peer + 2 * kPeerRows * kPeerMaxWidth);  // finite rows
+  const long long f0 = (row_begin + r0) * w;  // flat offset: parameters / gradients
+  const long long m0 = r0 * w;                // flat offset: the shard's moments
+  if (tid < nr) s_ok[tid] = 1;
+  for (int e = tid; e < ne; e += blockDim.x) {
+    float acc = pp.g[gi][f0 + e];
+    for (int q = 1; q < world; ++q) acc += pp.g[q * ng + gi][f0 + e];
+    s_g[e] = acc;
+  }
+  __syncthreads();
+  for (int e = tid; e < ne; e += blockDim.x)
+    if (!isfinite(s_g[e])) s_ok[e / w] = 0;
+  __syncthreads();
+  const float ibc1 = 1.0f / G.bias_correction1, ibc2 = 1.0f / G.bias_correction2;
+  float* m = G.exp_avg + m0;
+  float* v = G.exp_avg_sq + m0;
+  const float* prm = G.param + f0;
+  for (int e = tid; e < ne; e += blockDim.x) {
+    float pk = prm[e];
+    if (s_ok[e / w]) {
+      const float gk = s_g[e];
+      const float mk = kBeta1 * m[e] + kOneMinusBeta1 * gk;
+      const float vk = kBeta2 * v[e] + kOneMinusBeta2 * gk * gk;
+      m[e] = mk;
+      v[e] = vk;
+      pk = pk - __fdividef(G.lr * (mk * ibc1), sqrtf(vk * ibc2) + kEps);
     }
-    if (!finite) {
-      ++local;
-      continue;
-    }
-    float* p = G.param + row * w;
-    float* m = G.exp_avg + r * w;
-    float* v = G.exp_avg_sq + r * w;
-    const float ibc1 = 1.0f / G.bias_correction1, ibc2 = 1.0f / G.bias_correction2;
+    s_p[e] = pk;
+  }
+  __syncthreads();
+  if (G.renormalize && tid < nr && s_ok[tid]) {  // the row's norm in element order
+    float* row = s_p + tid * w;
     float nrm = 0.f;
-    for (int k = 0; k < w; ++k) {
-      const float gk = gsum[k];
-      const float mk = kBeta1 * m[k] + kOneMinusBeta1 * gk;
-      const float vk = kBeta2 * v[k] + kOneMinusBeta2 * gk * gk;
-      m[k] = mk;
-      v[k] = vk;
-      const float pk = p[k] - __fdividef(G.lr * (mk * ibc1), sqrtf(vk * ibc2) + kEps);
-      p[k] = pk;
-      nrm += pk * pk;
-    }
-    if (G.renormalize) {
-      nrm = sqrtf(nrm);
-      if (nrm > 0.f) {
-        const float inv = 1.0f / nrm;
-        for (int k = 0; k < w; ++k) p[k] = p[k] * inv;
-      }
-    }
-    for (int q = 0; q < world; ++q) {  // all-gather by direct peer stores
-      float* dst = pp.p[q * ng + gi] + row * w;
-      if (dst == p) continue;
-      for (int k = 0; k < w; ++k) dst[k] = p[k];
+    for (int k = 0; k < w; ++k) nrm += row[k] * row[k];
+    nrm = sqrtf(nrm);
+    if (nrm > 0.f) {
+      const float inv = 1.0f / nrm;
+      for (int k = 0; k < w; ++k) row[k] = row[k] * inv;
     }
   }
+  __syncthreads();
+  for (int e = tid; e < ne; e += blockDim.x) {  // all-gather by direct stores, own rank included
+    const float pv = s_p[e];
+    for (int q = 0; q < world; ++q) pp.p[q * ng + gi][f0 + e] = pv;
+  }
+  unsigned long long local = (tid < nr && !s_ok[tid]) ? 1ull : 0ull;
   for (int d = 16; d > 0; d >>= 1) local += __shfl_xor_sync(0xffffffffu, local, d);
-  if ((threadIdx.x & 31) == 0 && local) atomicAdd(skipped, local);
+  if ((tid & 31) == 0 && local) atomicAdd(skipped, local);
 }
 
 // Adam for the Gaussians K4's fused epilogue does not reach (backward.cu,
@@ -471,14 +481,12 @@ extern "C" int tsr_zero1_peer_adam(const tsr_adam_group_t* groups_host, int32_t 
       if (!pp.g[q * n_groups + k] || !pp.p[q * n_groups + k]) return TSR_E_INVALID;
     }
   // every group covers the shard rows [row_begin, row_end)
-  gs.row_start[0] = 0;
-  for (int k = 0; k < n_groups; ++k) gs.row_start[k + 1] = gs.row_start[k] + (row_end - row_begin);
-  const long long total = gs.row_start[n_groups];
-  if (total == 0) return TSR_OK;
-  long long blocks = (total + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  zero1_peer_adam_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(gs, pp, world, row_begin,
-                                                                          skipped);
+  const long long rows = row_end - row_begin;
+  if (rows == 0) return TSR_OK;
+  const size_t smem = (2 * kPeerRows * kPeerMaxWidth + kPeerRows) * sizeof(float);
+  const dim3 grid((unsigned)((rows + kPeerRows - 1) / kPeerRows), (unsigned)n_groups);
+  zero1_peer_adam_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(gs, pp, world, row_begin, rows,
+                                                                    skipped);
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }
