@@ -107,6 +107,7 @@ __device__ __forceinline__ long long clamp_ll(long long n, long long cap) {
 #ifdef TSR_K2_TRACE
 // instrumented build only (tools/k2_trace.py): CTA 0 stamps every barrier
 __device__ unsigned long long tsr_k2_trace_buf[128];
+__device__ unsigned long long tsr_k2_arrive_buf[2048 * 32];  // [cta][barrier] arrival stamps
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -133,6 +134,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int n_ctas) {
   __syncthreads();
   if (threadIdx.x == 0) {
+#ifdef TSR_K2_TRACE
+    tsr_k2_arrive_buf[blockIdx.x * 32 + (((uintptr_t)ctr & 127) >> 2)] = gtimer();
+#endif
     __threadfence();
     atomicAdd(ctr, 1u);
     unsigned int v;
@@ -788,7 +792,8 @@ using namespace tsr;
 
 #ifdef TSR_K2_TRACE
 extern "C" int tsr_k2_trace_read(unsigned long long* host, unsigned int* bar_base) {
-  (void)bar_base;
+  if (bar_base)  // the per-CTA arrival stamps [2048][32]
+    return cudaMemcpyFromSymbol(host, tsr_k2_arrive_buf, sizeof(tsr_k2_arrive_buf)) == cudaSuccess ? 0 : 2;
   return cudaMemcpyFromSymbol(host, tsr_k2_trace_buf, sizeof(tsr_k2_trace_buf)) == cudaSuccess ? 0 : 2;
 }
 #endif

@@ -37,3 +37,16 @@ for _ in range(5):
         if sub[0]:
             print(f"   scatter call {c} CTA0 first sub-tile (loads, rank, scan, stage, store, phase end):",
                   [round((x - t[0]) / 1e3, 1) for x in sub])
+    # per-CTA arrival at each barrier (bar_base != NULL selects that buffer)
+    if _ != 4:
+        continue
+    arr = (ctypes.c_ulonglong * (2048 * 32))()
+    lib.tsr_k2_trace_read(arr, ctypes.c_void_p(1))
+    a = np.array(arr, dtype=np.int64).reshape(2048, 32)
+    g = int(np.count_nonzero(a[:, 0]))
+    a = a[:g, :n]
+    rel = (a - t[0]) / 1e3
+    print(f"   arrivals over {g} CTAs: barrier: min / median / max (us) [slowest CTA]")
+    for b in range(n):
+        print(f"     b{b:2d}: {rel[:, b].min():7.1f} {np.median(rel[:, b]):7.1f} {rel[:, b].max():7.1f}"
+              f" [{int(rel[:, b].argmax())}]")
