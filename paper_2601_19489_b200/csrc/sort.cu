@@ -84,7 +84,7 @@ struct IndexArgs {
   uint32_t* out_rank_count;          // M_cap: pairs of each rank
   uint32_t* out_rank_off;            // M_cap: emission offset of each rank
   // zeroed by the per-call memset:
-  uint32_t* hist4;                   // 4 x 256 depth-byte histogram
+  uint32_t* hist4;                   // [0] OR of the depth keys, [1] OR of their complements
   unsigned int* bar;                 // kMaxBarriers arrival counters
 };
 
@@ -131,23 +131,36 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #endif
 
+// Release-add on arrival (cumulative over the CTA's writes, ordered by the
+// bar.sync before it), relaxed polling, and one acquire load once the count
+// is complete -- no SC fence (MEMBAR.SC) on either side.
 __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int n_ctas) {
   __syncthreads();
   if (threadIdx.x == 0) {
 #ifdef TSR_K2_TRACE
     tsr_k2_arrive_buf[blockIdx.x * 32 + (((uintptr_t)ctr & 127) >> 2)] = gtimer();
 #endif
+#ifdef TSR_K2_SC_BARRIER
     __threadfence();
     atomicAdd(ctr, 1u);
+#else
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+#endif
     unsigned int v;
     // relaxed polling (an acquire load per poll would invalidate L1 under
-    // the co-resident CTA), one fence after
+    // the co-resident CTA)
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
     while (v < n_ctas) {
+#ifndef TSR_K2_SPIN
       __nanosleep(20);
+#endif
       asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
     }
+#ifdef TSR_K2_SC_BARRIER
     __threadfence();
+#else
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+#endif
 #ifdef TSR_K2_TRACE
     if (blockIdx.x == 0) tsr_k2_trace_buf[1 + (((uintptr_t)ctr & 127) >> 2)] = gtimer();  // bar is 256-B aligned
 #endif
@@ -593,40 +606,33 @@ __global__ void __launch_bounds__(kSB, 3) build_index_kernel(IndexArgs a) {
 #endif
 
   // ---- 1. depth ranks
-  // histogram of all four depth bytes (tells which passes are trivial)
-#pragma unroll
-  for (int b = 0; b < 4; ++b) sm.h[b][tid] = 0;
-  __syncthreads();
+  // which depth bytes are the same for every row (those passes are
+  // trivial): OR of the keys and OR of their complements (= ~AND), one
+  // atomic pair per CTA
   {
     long long lo, hi;
     slice(m, bid, G, lo, hi);
-    const int lane = tid & 31, warp = tid >> 5;
-    for (long long base = lo; base < hi; base += kSub) {
-      const long long wb = base + (long long)warp * (32 * kItems);
-      uint32_t k[kItems];
-#pragma unroll
-      for (int r = 0; r < kItems; ++r) {
-        const long long i = wb + r * 32 + lane;
-        k[r] = i < hi ? a.depth_bits[i] : 0u;
-      }
-#pragma unroll
-      for (int r = 0; r < kItems; ++r) {
-        const bool v = wb + r * 32 + lane < hi;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) hist_add(sm.h[b], (k[r] >> (8 * b)) & 255u, v);
-      }
+    uint32_t o = 0u, no = 0u;
+    for (long long i = lo + tid; i < hi; i += kSB) {
+      const uint32_t k = a.depth_bits[i];
+      o |= k;
+      no |= ~k;
+    }
+    for (int d = 16; d > 0; d >>= 1) {
+      o |= __shfl_xor_sync(0xffffffffu, o, d);
+      no |= __shfl_xor_sync(0xffffffffu, no, d);
+    }
+    if ((tid & 31) == 0 && lo < hi) {
+      atomicOr(&a.hist4[0], o);
+      atomicOr(&a.hist4[1], no);
     }
   }
-  __syncthreads();
-#pragma unroll
-  for (int b = 0; b < 4; ++b)
-    if (sm.h[b][tid]) atomicAdd(&a.hist4[b * kBins + tid], sm.h[b][tid]);
   grid_barrier(a.bar + nb++, G);
-  if (tid < 4) sm.skip[tid] = 0;
-  __syncthreads();
-#pragma unroll
-  for (int b = 0; b < 4; ++b)
-    if ((long long)a.hist4[b * kBins + tid] == m) sm.skip[b] = 1;  // one digit for every row
+  if (tid < 4) {
+    // byte q is constant iff no bit of it is 1 in some row and 0 in another
+    const uint32_t var = a.hist4[0] & a.hist4[1];
+    sm.skip[tid] = m == 0 || ((var >> (8 * tid)) & 255u) == 0u;
+  }
   __syncthreads();
   const uint32_t* dkey = a.depth_bits;
   const uint32_t* drow = nullptr;  // identity

@@ -1,0 +1,13 @@
+#!/bin/bash
+# K2 barrier variants: binning parity on the default lib, trace, and C2/C3 benches per variant
+mkdir -p gpurun_out; rm -f gpurun_out/k2bar_status.txt
+make -j16 all > gpurun_out/make.log 2>&1 || { echo make failed; exit 1; }
+timeout 600 python -m pytest tests/test_gpu_binning.py tests/test_gpu_scene.py -q -x > gpurun_out/k2bar_pytest.log 2>&1; echo "pytest=$?" >> gpurun_out/k2bar_status.txt
+TSR_LIB=build/libtilesplat_b200_trace.so timeout 300 python tools/k2_trace.py c2 > gpurun_out/k2trace_c2.txt 2>&1
+for v in base sc spin; do
+  if [ "$v" = "base" ]; then lib=paper_2601_19489_b200/libtilesplat_b200.so; else lib=build/libtilesplat_b200_$v.so; fi
+  for rep in 1 2; do
+    TSR_LIB=$lib timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_${v}_$rep.log 2>&1
+  done
+  TSR_LIB=$lib timeout 300 python bench.py --config c3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_${v}_c3.log 2>&1
+done
