@@ -46,6 +46,10 @@ constexpr int kSB = 256;                 // threads per CTA
 constexpr int kBins = 256;               // 8-bit digits
 constexpr int kItems = 8;                // items per thread per sub-tile
 constexpr int kSub = kSB * kItems;       // 2048-item sub-tiles
+#ifndef TSR_K2_DEPTH_ITEMS
+#define TSR_K2_DEPTH_ITEMS 10
+#endif
+constexpr int kDepthItems = TSR_K2_DEPTH_ITEMS;  // the 4-byte depth passes: 2560-item sub-tiles (8/12/16 measured slower)
 constexpr int kEmitPer = 2;              // ranks per thread per emission block
 constexpr int kEmitRanks = kSB * kEmitPer;
 constexpr int kStage = 4096;             // staged pairs per emission window
@@ -230,22 +234,22 @@ __device__ __forceinline__ uint32_t digit_of(K k, int shift, uint32_t mask) {
 }
 
 // ---- radix pass, phase 1: per-CTA digit histogram of the slice
-template <typename K>
+template <typename K, int kI>
 __device__ void count_phase(const K* __restrict__ kin, long long lo, long long hi, int shift,
                             uint32_t mask, uint32_t* __restrict__ cnt_out, SortSmem& sm) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   sm.h[0][tid] = 0;
   __syncthreads();
-  for (long long base = lo; base < hi; base += kSub) {
-    const long long wb = base + (long long)warp * (32 * kItems);
-    K k[kItems];
+  for (long long base = lo; base < hi; base += (kSB * kI)) {
+    const long long wb = base + (long long)warp * (32 * kI);
+    K k[kI];
 #pragma unroll
-    for (int r = 0; r < kItems; ++r) {
+    for (int r = 0; r < kI; ++r) {
       const long long i = wb + r * 32 + lane;
       k[r] = i < hi ? kin[i] : (K)0;
     }
 #pragma unroll
-    for (int r = 0; r < kItems; ++r)
+    for (int r = 0; r < kI; ++r)
       hist_add(sm.h[0], digit_of(k[r], shift, mask), wb + r * 32 + lane < hi);
   }
   __syncthreads();
@@ -281,7 +285,7 @@ __device__ void colscan_phase(const uint32_t* __restrict__ cnt, uint32_t* __rest
 // ---- radix pass, phase 3: stable scatter of the slice.
 // K = u32 depth bits (values: rows; vin == nullptr -> value = index) or
 // u64 pair keys tile << 32 | depth bits (values: rows).
-template <typename K>
+template <typename K, int kI>
 __device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                               K* __restrict__ kout, uint32_t* __restrict__ vout, long long lo,
                               long long hi, int shift, int bits,
@@ -291,7 +295,7 @@ __device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restr
                               uint32_t* __restrict__ inv = nullptr, int call = 0) {
   constexpr bool kVals = true;
   K* s_keys = reinterpret_cast<K*>(dyn);
-  uint32_t* s_vals = reinterpret_cast<uint32_t*>(dyn + kSub * sizeof(K));
+  uint32_t* s_vals = reinterpret_cast<uint32_t*>(dyn + (kSB * kI) * sizeof(K));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt = (1u << lane) - 1u;
   const uint32_t mask = (1u << bits) - 1u;
@@ -303,27 +307,27 @@ __device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restr
   // the sub-tile's items are loaded one sub-tile ahead: the next sub-tile's
   // loads are issued once this one's items are staged in shared memory, so
   // they overlap the staged read-back and the global stores
-  K key[kItems];
-  uint32_t val[kItems];
+  K key[kI];
+  uint32_t val[kI];
   auto load_items = [&](long long b) {
-    const long long wb = b + (long long)warp * (32 * kItems);
+    const long long wb = b + (long long)warp * (32 * kI);
 #pragma unroll
-    for (int r = 0; r < kItems; ++r) {  // all loads in flight first
+    for (int r = 0; r < kI; ++r) {  // all loads in flight first
       const long long i = wb + r * 32 + lane;
       key[r] = i < hi ? kin[i] : (K)0;
       if (kVals) val[r] = i < hi ? (vin ? vin[i] : (uint32_t)i) : 0u;
     }
   };
   if (lo < hi) load_items(lo);
-  for (long long base = lo; base < hi; base += kSub) {
+  for (long long base = lo; base < hi; base += (kSB * kI)) {
 #pragma unroll
     for (int w = 0; w < kSB / 32; ++w) sm.cnt[w][tid] = 0;
     __syncthreads();
-    const long long wb = base + (long long)warp * (32 * kItems);
-    uint32_t packed[kItems];
+    const long long wb = base + (long long)warp * (32 * kI);
+    uint32_t packed[kI];
     TSR_TRACE_SUB(call, 0);
 #pragma unroll
-    for (int r = 0; r < kItems; ++r) {
+    for (int r = 0; r < kI; ++r) {
       const bool valid = wb + r * 32 + lane < hi;
       const uint32_t d = digit_of(key[r], shift, mask);
       const unsigned peers = digit_peers(d, bits, __ballot_sync(0xffffffffu, valid));
@@ -350,7 +354,7 @@ __device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restr
     __syncthreads();
     TSR_TRACE_SUB(call, 2);
 #pragma unroll
-    for (int r = 0; r < kItems; ++r) {
+    for (int r = 0; r < kI; ++r) {
       if (packed[r] != 0xffffffffu) {
         const uint32_t d = packed[r] >> 16;
         const uint32_t local = sm.lbase[d] + sm.cnt[warp][d] + (packed[r] & 0xffffu);
@@ -360,27 +364,27 @@ __device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restr
     }
     __syncthreads();
     TSR_TRACE_SUB(call, 3);
-    if (base + kSub < hi) load_items(base + kSub);
-    const int n_here = (int)(hi - base < kSub ? hi - base : kSub);
+    if (base + (kSB * kI) < hi) load_items(base + (kSB * kI));
+    const int n_here = (int)(hi - base < (kSB * kI) ? hi - base : (kSB * kI));
     {
-      // all kItems items of the thread in flight at once (the det-mode
+      // all kI items of the thread in flight at once (the det-mode
       // gathers are random loads)
-      K k[kItems];
-      uint32_t v[kItems], g[kItems];
+      K k[kI];
+      uint32_t v[kI], g[kI];
 #pragma unroll
-      for (int r = 0; r < kItems; ++r) {
+      for (int r = 0; r < kI; ++r) {
         const int i = tid + r * kSB;
         k[r] = i < n_here ? s_keys[i] : (K)0;
         v[r] = i < n_here ? s_vals[i] : 0u;
         const uint32_t d = digit_of(k[r], shift, mask);
         g[r] = sm.run[d] + (uint32_t)i - sm.lbase[d];
       }
-      uint32_t gv[kItems];
+      uint32_t gv[kI];
 #pragma unroll
-      for (int r = 0; r < kItems; ++r)
+      for (int r = 0; r < kI; ++r)
         gv[r] = (gather && tid + r * kSB < n_here) ? gather[v[r]] : v[r];
 #pragma unroll
-      for (int r = 0; r < kItems; ++r) {
+      for (int r = 0; r < kI; ++r) {
         if (tid + r * kSB >= n_here) continue;
         kout[g[r]] = k[r];
         vout[g[r]] = gv[r];
@@ -397,7 +401,7 @@ __device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restr
 }
 
 // ---- one full radix pass (3 phases, 3 grid barriers)
-template <typename K>
+template <typename K, int kI = kItems>
 __device__ void radix_pass(const IndexArgs& a, int& nb, const K* kin, const uint32_t* vin,
                            K* kout, uint32_t* vout, long long n, int shift, int bits,
                            SortSmem& sm, unsigned char* dyn,
@@ -405,11 +409,11 @@ __device__ void radix_pass(const IndexArgs& a, int& nb, const K* kin, const uint
   const int G = gridDim.x, bid = blockIdx.x;
   long long lo, hi;
   slice(n, bid, G, lo, hi);
-  count_phase<K>(kin, lo, hi, shift, (1u << bits) - 1u, a.cnt + (long long)bid * kBins, sm);
+  count_phase<K, kI>(kin, lo, hi, shift, (1u << bits) - 1u, a.cnt + (long long)bid * kBins, sm);
   grid_barrier(a.bar + nb++, G);
   colscan_phase(a.cnt, a.colscan, a.dtotal, G, sm);
   grid_barrier(a.bar + nb++, G);
-  scatter_phase<K>(kin, vin, kout, vout, lo, hi, shift, bits, a.colscan + (long long)bid * kBins,
+  scatter_phase<K, kI>(kin, vin, kout, vout, lo, hi, shift, bits, a.colscan + (long long)bid * kBins,
                    a.dtotal, sm, dyn, gather, inv, nb / 3);
   grid_barrier(a.bar + nb++, G);
 }
@@ -642,7 +646,7 @@ __global__ void __launch_bounds__(kSB, 3) build_index_kernel(IndexArgs a) {
     int par = 0;
     for (int q = 0; q < 4; ++q) {
       if (sm.skip[q]) continue;
-      radix_pass<uint32_t>(a, nb, dkey, drow, ko[par], vo[par], m, 8 * q, 8, sm, dyn);
+      radix_pass<uint32_t, kDepthItems>(a, nb, dkey, drow, ko[par], vo[par], m, 8 * q, 8, sm, dyn);
       dkey = ko[par];
       drow = vo[par];
       par ^= 1;
