@@ -58,7 +58,7 @@ static_assert((kSB / 32) * sizeof(LbWarp) <= kDynSmem, "LB re-walk scratch in th
 constexpr int kMaxGrid = 2048;
 constexpr int kMaxBarriers = 32;
 constexpr int kMaxTiles = 1 << 16;
-constexpr unsigned long long kNoPair = ~0ull;
+constexpr uint32_t kNoPair = ~0u;
 
 struct IndexArgs {
   const float* rec;
@@ -74,7 +74,7 @@ struct IndexArgs {
   int64_t* ckpt_base;
   int* overflow;
   uint32_t *dk0, *dv0, *dk1, *dv1;   // depth sort ping-pong (M_cap)
-  unsigned long long *pk0, *pk1;     // pair keys (tile << 32 | depth bits) ping-pong (P_cap)
+  uint32_t *pk0, *pk1;               // pair tile keys ping-pong (P_cap)
   uint32_t *pv0, *pv1;               // pair values (row) ping-pong (P_cap)
   uint32_t* cnt;                     // kMaxGrid x 256 per-CTA digit counts
   uint32_t* colscan;                 // kMaxGrid x 256 exclusive prefix over CTAs
@@ -285,14 +285,15 @@ __device__ void colscan_phase(const uint32_t* __restrict__ cnt, uint32_t* __rest
 // ---- radix pass, phase 3: stable scatter of the slice.
 // K = u32 depth bits (values: rows; vin == nullptr -> value = index) or
 // u64 pair keys tile << 32 | depth bits (values: rows).
-template <typename K, int kI>
+template <typename K, int kI, typename KO = K>
 __device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
-                              K* __restrict__ kout, uint32_t* __restrict__ vout, long long lo,
+                              KO* __restrict__ kout, uint32_t* __restrict__ vout, long long lo,
                               long long hi, int shift, int bits,
                               const uint32_t* __restrict__ colscan_row,
                               const uint32_t* __restrict__ dtotal, SortSmem& sm,
                               unsigned char* dyn, const uint32_t* __restrict__ gather = nullptr,
-                              uint32_t* __restrict__ inv = nullptr, int call = 0) {
+                              uint32_t* __restrict__ inv = nullptr, int call = 0,
+                              const uint32_t* __restrict__ depth_of_row = nullptr) {
   constexpr bool kVals = true;
   K* s_keys = reinterpret_cast<K*>(dyn);
   uint32_t* s_vals = reinterpret_cast<uint32_t*>(dyn + (kSB * kI) * sizeof(K));
@@ -383,10 +384,21 @@ __device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restr
 #pragma unroll
       for (int r = 0; r < kI; ++r)
         gv[r] = (gather && tid + r * kSB < n_here) ? gather[v[r]] : v[r];
+      // the last tile pass writes the reference's keys: tile << 32 | depth
+      // bits of the row (random 4-byte reads of an L2-resident array)
+      KO ko[kI];
+#pragma unroll
+      for (int r = 0; r < kI; ++r) {
+        if constexpr (sizeof(KO) > sizeof(K))
+          ko[r] = tid + r * kSB < n_here
+                      ? ((KO)k[r] << 32) | (KO)depth_of_row[gv[r]] : (KO)0;
+        else
+          ko[r] = k[r];
+      }
 #pragma unroll
       for (int r = 0; r < kI; ++r) {
         if (tid + r * kSB >= n_here) continue;
-        kout[g[r]] = k[r];
+        kout[g[r]] = ko[r];
         vout[g[r]] = gv[r];
         if (gather) inv[v[r]] = g[r];  // values carry emission indices: inverse permutation
       }
@@ -401,11 +413,12 @@ __device__ void scatter_phase(const K* __restrict__ kin, const uint32_t* __restr
 }
 
 // ---- one full radix pass (3 phases, 3 grid barriers)
-template <typename K, int kI = kItems>
+template <typename K, int kI = kItems, typename KO = K>
 __device__ void radix_pass(const IndexArgs& a, int& nb, const K* kin, const uint32_t* vin,
-                           K* kout, uint32_t* vout, long long n, int shift, int bits,
+                           KO* kout, uint32_t* vout, long long n, int shift, int bits,
                            SortSmem& sm, unsigned char* dyn,
-                           const uint32_t* gather = nullptr, uint32_t* inv = nullptr) {
+                           const uint32_t* gather = nullptr, uint32_t* inv = nullptr,
+                           const uint32_t* depth_of_row = nullptr) {
   const int G = gridDim.x, bid = blockIdx.x;
   long long lo, hi;
   slice(n, bid, G, lo, hi);
@@ -413,8 +426,9 @@ __device__ void radix_pass(const IndexArgs& a, int& nb, const K* kin, const uint
   grid_barrier(a.bar + nb++, G);
   colscan_phase(a.cnt, a.colscan, a.dtotal, G, sm);
   grid_barrier(a.bar + nb++, G);
-  scatter_phase<K, kI>(kin, vin, kout, vout, lo, hi, shift, bits, a.colscan + (long long)bid * kBins,
-                   a.dtotal, sm, dyn, gather, inv, nb / 3);
+  scatter_phase<K, kI, KO>(kin, vin, kout, vout, lo, hi, shift, bits,
+                           a.colscan + (long long)bid * kBins, a.dtotal, sm, dyn, gather, inv,
+                           nb / 3, depth_of_row);
   grid_barrier(a.bar + nb++, G);
 }
 
@@ -429,11 +443,11 @@ __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, lon
                            long long p_cap, const uint32_t* __restrict__ depth_by_rank,
                            const uint32_t* __restrict__ row_by_rank, SortSmem& sm,
                            unsigned char* dyn) {
-  unsigned long long* s_stage = reinterpret_cast<unsigned long long*>(dyn);
-  uint32_t* s_sval = reinterpret_cast<uint32_t*>(dyn + kStage * sizeof(unsigned long long));
+  uint32_t* s_stage = reinterpret_cast<uint32_t*>(dyn);  // tile of each staged pair
+  uint32_t* s_sval = reinterpret_cast<uint32_t*>(dyn + kStage * sizeof(uint32_t));
   const int tid = threadIdx.x;
   const int tiles_x = a.tiles_x, tiles_y = a.tiles_y, strategy = a.strategy;
-  unsigned long long* __restrict__ pairs = a.pk0;
+  uint32_t* __restrict__ pairs = a.pk0;
   uint32_t* __restrict__ pair_rows = a.pv0;
   for (long long r0 = rlo; r0 < rhi; r0 += kEmitRanks) {
     uint32_t row[kEmitPer], cnt[kEmitPer], off[kEmitPer], dep[kEmitPer];
@@ -490,7 +504,6 @@ __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, lon
         }
         // one flat loop over the rank's pairs (column-major, K1's order);
         // (column, row-in-column) advance incrementally
-        const unsigned long long depk = dep[k];
         const uint32_t rowk = row[k];
         const uint32_t tx0 = sp[k].x & 0xffffu, ty_base = sp[k].y & 0xffffu;
         unsigned long long codes = ((unsigned long long)sp[k].w << 32) | sp[k].z;
@@ -504,7 +517,7 @@ __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, lon
 #pragma unroll 1
         for (uint32_t p = lo; p < hi; ++p) {
           if (p >= w0 && p < w1) {
-            s_stage[p - w0] = ((unsigned long long)t << 32) | depk;
+            s_stage[p - w0] = t;
             s_sval[p - w0] = rowk;
           }
           t += (uint32_t)tiles_x;
@@ -522,7 +535,7 @@ __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, lon
       __syncthreads();
       if (r0 == rlo && w0 == 0) TSR_TRACE_AT(45);
       for (uint32_t j = tid; j < w1 - w0; j += kSB) {
-        const unsigned long long v = s_stage[j];
+        const uint32_t v = s_stage[j];
         const long long g = O + w0 + j;
         if (v != kNoPair && g < p_cap) {
           pairs[g] = v;
@@ -545,14 +558,13 @@ __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, lon
         const bool v = r < rhi && (sp[k].y >> 31) && cnt[k] != 0;
         SplatF64 s{};
         if (v) s = load_splat_f64(a.rec + (long long)row[k] * 12);
-        warp_emit_lb(s, v, tiles_x, tiles_y, dep[k], row[k], O + off[k], p_cap, pairs,
+        warp_emit_lb(s, v, tiles_x, tiles_y, row[k], O + off[k], p_cap, pairs,
                      pair_rows, *lbw);
       }
     }
 #pragma unroll
     for (int k = 0; k < kEmitPer; ++k) {
       if (strategy == 1 || !(sp[k].y >> 31) || cnt[k] == 0) continue;
-      const unsigned long long depk = dep[k];
       long long out = O + off[k];
       SplatF64 s = load_splat_f64(a.rec + (long long)row[k] * 12);
       if (strategy == 2) {  // bin_aabb rectangle, column-major
@@ -561,7 +573,7 @@ __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, lon
         for (long long tx = tx0; tx <= tx1; ++tx)
           for (long long ty = ty0; ty <= ty1; ++ty, ++out)
             if (out < p_cap) {
-              pairs[out] = ((unsigned long long)(ty * tiles_x + tx) << 32) | depk;
+              pairs[out] = (uint32_t)(ty * tiles_x + tx);
               pair_rows[out] = row[k];
             }
         continue;
@@ -575,7 +587,7 @@ __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, lon
             const double ry0 = dsub((double)(16 * ty), s.my);
             if (min_q_box(s, rx0, dadd(rx0, 16.0), ry0, dadd(ry0, 16.0)) <= s.t) {
               if (out < p_cap) {
-                pairs[out] = ((unsigned long long)(ty * tiles_x + tx) << 32) | depk;
+                pairs[out] = (uint32_t)(ty * tiles_x + tx);
                 pair_rows[out] = row[k];
               }
               ++out;
@@ -586,7 +598,7 @@ __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, lon
           const int nr = column_rows(s, box, tx, tiles_y, ty0, ty1);
           for (int q = 0; q < nr; ++q, ++out)
             if (out < p_cap) {
-              pairs[out] = ((unsigned long long)((ty0 + q) * tiles_x + tx) << 32) | depk;
+              pairs[out] = (uint32_t)((ty0 + q) * tiles_x + tx);
               pair_rows[out] = row[k];
             }
         }
@@ -723,12 +735,14 @@ __global__ void __launch_bounds__(kSB, 3) build_index_kernel(IndexArgs a) {
   const uint32_t* gat = det ? a.pv0 : nullptr;
   if (a.tile_bits > 8) {  // two passes of ~half the tile bits each
     const int b1 = (a.tile_bits + 1) / 2, b2 = a.tile_bits - b1;
-    radix_pass<unsigned long long>(a, nb, a.pk0, v0, a.pk1, a.pv1, np, 32, b1, sm, dyn);
-    radix_pass<unsigned long long>(a, nb, a.pk1, a.pv1, keys_out, vals_out, np, 32 + b1, b2, sm,
-                                   dyn, gat, a.inv_perm);
+    radix_pass<uint32_t>(a, nb, a.pk0, v0, a.pk1, a.pv1, np, 0, b1, sm, dyn);
+    radix_pass<uint32_t, kItems, unsigned long long>(a, nb, a.pk1, a.pv1, keys_out, vals_out, np,
+                                                     b1, b2, sm, dyn, gat, a.inv_perm,
+                                                     a.depth_bits);
   } else {
-    radix_pass<unsigned long long>(a, nb, a.pk0, v0, keys_out, vals_out, np, 32, a.tile_bits,
-                                   sm, dyn, gat, a.inv_perm);
+    radix_pass<uint32_t, kItems, unsigned long long>(a, nb, a.pk0, v0, keys_out, vals_out, np, 0,
+                                                     a.tile_bits, sm, dyn, gat, a.inv_perm,
+                                                     a.depth_bits);
   }
 
   // ---- 4. per-tile ranges (binning.py:156-157) + checkpoint bases
@@ -778,8 +792,8 @@ static Plan plan(long long m_cap, long long p_cap) {
   p.dv0 = take(4 * mc);
   p.dk1 = take(4 * mc);
   p.dv1 = take(4 * mc);
-  p.pk0 = take(8 * pc);
-  p.pk1 = take(8 * pc);
+  p.pk0 = take(4 * pc);
+  p.pk1 = take(4 * pc);
   p.pv0 = take(4 * pc);
   p.pv1 = take(4 * pc);
   p.cnt = take(4 * (size_t)kMaxGrid * kBins);
@@ -850,8 +864,8 @@ static int build_index_impl(const float* rec, const uint32_t* depth_bits, const 
   a.dv0 = (uint32_t*)(w + pl.dv0);
   a.dk1 = (uint32_t*)(w + pl.dk1);
   a.dv1 = (uint32_t*)(w + pl.dv1);
-  a.pk0 = (unsigned long long*)(w + pl.pk0);
-  a.pk1 = (unsigned long long*)(w + pl.pk1);
+  a.pk0 = (uint32_t*)(w + pl.pk0);
+  a.pk1 = (uint32_t*)(w + pl.pk1);
   a.pv0 = (uint32_t*)(w + pl.pv0);
   a.pv1 = (uint32_t*)(w + pl.pv1);
   a.cnt = (uint32_t*)(w + pl.cnt);

@@ -399,14 +399,13 @@ __device__ __forceinline__ long long warp_count_lb(const SplatF64& s, bool valid
 
 
 // The same round-robin walk, emitting: every passing candidate of splat o is
-// written as (tile << 32 | key_lo[o], row[o]) at out_base[o] + (passing
+// written as (tile, row[o]) at out_base[o] + (passing
 // candidates of o before it, column-major) -- the rank-major emission's
 // FP64 re-walk for rows whose span record overflowed (sort.cu).  All 32
 // lanes call; `valid` lanes own a splat.
 __device__ __forceinline__ void warp_emit_lb(const SplatF64& s, bool valid, int tiles_x,
-                                             int tiles_y, unsigned long long key_lo,
-                                             uint32_t row, long long out_base, long long p_cap,
-                                             unsigned long long* __restrict__ pairs,
+                                             int tiles_y, uint32_t row, long long out_base,
+                                             long long p_cap, uint32_t* __restrict__ pairs,
                                              uint32_t* __restrict__ pair_rows, LbWarp& w) {
   const int lane = threadIdx.x & 31;
   SnugRect r;
@@ -441,7 +440,6 @@ __device__ __forceinline__ void warp_emit_lb(const SplatF64& s, bool valid, int 
     }
     const int ob = __shfl_sync(0xffffffffu, offs, o);
     const long long ob_out = __shfl_sync(0xffffffffu, out_base, o);
-    const unsigned long long ok = __shfl_sync(0xffffffffu, key_lo, o);
     const uint32_t orow = __shfl_sync(0xffffffffu, row, o);
     bool pass = false;
     int tile = 0;
@@ -467,7 +465,7 @@ __device__ __forceinline__ void warp_emit_lb(const SplatF64& s, bool valid, int 
     if (pass) {
       const long long g = ob_out + w.cnt[o] + __popc(pb & below);
       if (g < p_cap) {
-        pairs[g] = ((unsigned long long)(uint32_t)tile << 32) | ok;
+        pairs[g] = (uint32_t)tile;
         pair_rows[g] = orow;
       }
     }
