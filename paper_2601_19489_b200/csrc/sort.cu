@@ -440,7 +440,7 @@ __device__ __forceinline__ uint32_t rank_row(const uint32_t* row_by_rank, long l
 }
 
 __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, long long O,
-                           long long p_cap, const uint32_t* __restrict__ depth_by_rank,
+                           long long p_cap,
                            const uint32_t* __restrict__ row_by_rank, SortSmem& sm,
                            unsigned char* dyn) {
   uint32_t* s_stage = reinterpret_cast<uint32_t*>(dyn);  // tile of each staged pair
@@ -450,7 +450,7 @@ __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, lon
   uint32_t* __restrict__ pairs = a.pk0;
   uint32_t* __restrict__ pair_rows = a.pv0;
   for (long long r0 = rlo; r0 < rhi; r0 += kEmitRanks) {
-    uint32_t row[kEmitPer], cnt[kEmitPer], off[kEmitPer], dep[kEmitPer];
+    uint32_t row[kEmitPer], cnt[kEmitPer], off[kEmitPer];
     uint4 sp[kEmitPer];
     uint32_t sum = 0;
 #pragma unroll
@@ -463,7 +463,6 @@ __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, lon
         sp[k] = a.rank_span[r];
       }
       row[k] = r < rhi ? rank_row(row_by_rank, r) : 0u;
-      dep[k] = r < rhi ? depth_by_rank[r] : 0u;
       sum += cnt[k];
     }
     if (r0 == rlo) TSR_TRACE_AT(40);
@@ -720,7 +719,7 @@ __global__ void __launch_bounds__(kSB, 3) build_index_kernel(IndexArgs a) {
     P = (long long)t1;
   }
   if (bid == 0 && tid == 0 && P > a.p_cap && a.overflow) *a.overflow = 1;  // sticky
-  emit_phase(a, rlo, rhi, O, a.p_cap, dkey, drow, sm, dyn);
+  emit_phase(a, rlo, rhi, O, a.p_cap, drow, sm, dyn);
   grid_barrier(a.bar + nb++, G);
 
   // ---- 3. stable sort of the pairs by tile; the last pass writes keys/values
