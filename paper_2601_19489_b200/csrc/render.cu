@@ -73,7 +73,7 @@ __device__ __forceinline__ float2 bc2(float x) { return make_float2(x, x); }
 // alive flag.  Pixels outside the image start at T = 0 (never written).
 struct PixPair {
   float2 T, Cr, Cg, Cb, D;
-  float2 nc;  // blends so far (exact small integers; one packed add per entry)
+  int nc0, nc1;  // blends so far (popcounts of the per-chunk participation masks)
   int ncons0, ncons1;
   bool strong0, strong1;  // last blend was a strong contribution (w >= 1/255)
   bool part0, part1;      // last entry blended (the backward's participation)
@@ -117,9 +117,6 @@ __device__ __forceinline__ void blend_pair(const float4 g, const float4 c, const
   s.Cb = __ffma2_rn(w, bc2(col.z), s.Cb);
   s.D = __ffma2_rn(w, bc2(col.w), s.D);
   s.T = __fmul2_rn(s.T, __fadd2_rn(bc2(1.f), make_float2(-a.x, -a.y)));
-  s.nc = __fadd2_rn(s.nc, make_float2(b0 ? 1.f : 0.f, b1 ? 1.f : 0.f));
-  s.ncons0 = live0 ? pos + 1 : s.ncons0;
-  s.ncons1 = live1 ? pos + 1 : s.ncons1;
 }
 
 // Region lists for the region-culled backward (kCkpt 3/4, backward_regions.cu):
@@ -191,7 +188,7 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
   PixPair s;
   s.T = make_float2(in0 ? 1.f : 0.f, in1 ? 1.f : 0.f);
   s.Cr = s.Cg = s.Cb = s.D = bc2(0.f);
-  s.nc = bc2(0.f);
+  s.nc0 = s.nc1 = 0;
   s.ncons0 = s.ncons1 = 0;
   s.strong0 = s.strong1 = false;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -274,22 +271,28 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
         const float4 g = s_spl[c0 + lane][0], rw = s_raw[c0 + lane];
         hit = strip_hit(g.x, g.y, rw.x, rw.y, rw.z, rw.w, bx0, bx1, by0, by1);
       }
-      unsigned mask = __ballot_sync(0xffffffffu, hit);
+      // hits in list order from the bit-reversed ballot: entry j is the
+      // leading one (clz, no per-hit bit reversal), and its bit is reused to
+      // clear it and to mark the region lists
+      unsigned rev = __brev(__ballot_sync(0xffffffffu, hit));
       // region lists: the chunk's positions that blend at >= 1 pixel of the
       // region (exactly the backward's participating entries), from the
-      // blends below
-      unsigned pm0 = 0u, pm1 = 0u;
-      while (mask) {
-        const int j = __ffs(mask) - 1;
-        mask &= mask - 1u;
-        const float4* sp = s_spl[c0 + j];
+      // blends below (bit-reversed like rev)
+      unsigned pm0r = 0u, pm1r = 0u;
+      const bool live_c0 = s.alive0(), live_c1 = s.alive1();
+      const float4* cbase = s_spl[c0];
+      while (rev) {
+        const int f = 31 - __clz(rev);  // FLO
+        const unsigned bit = 1u << f;
+        const int j = 31 - f;
+        rev ^= bit;
+        const float4* sp = cbase + 3 * j;
         blend_pair(sp[0], sp[1], sp[2], pxf, pyf, pos0 + j, s);
-        if (kCkpt == 4) {  // 8x4 halves: rows of the lanes' first / second pixels
-          if (__any_sync(0xffffffffu, s.part0)) pm0 |= 1u << j;
-          if (__any_sync(0xffffffffu, s.part1)) pm1 |= 1u << j;
-        } else if (kRegions) {
-          if (__any_sync(0xffffffffu, s.part0 || s.part1)) pm0 |= 1u << j;
-        }
+        // per-pixel participation bits of the chunk (bit-reversed): their
+        // popcounts are the blend counts, the last one a dead pixel's death
+        // entry, and their warp OR the region lists' entries
+        if (s.part0) pm0r |= bit;
+        if (s.part1) pm1r |= bit;
         if (kScore) {
           const unsigned q0 = __ballot_sync(0xffffffffu, kScore == 3 ? s.strong0 && m0 : s.strong0);
           const unsigned q1 = __ballot_sync(0xffffffffu, kScore == 3 ? s.strong1 && m1 : s.strong1);
@@ -314,6 +317,16 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
           }
         }
       }
+      s.nc0 += __popc(pm0r);
+      s.nc1 += __popc(pm1r);
+      // a pixel alive at the chunk start that is dead now died at its last
+      // blend of the chunk (death needs a blend): it considered the list up
+      // to and including that entry (pos0 + j, j = 32 - ffs(reversed bits) - 1)
+      if (live_c0 && !s.alive0()) s.ncons0 = pos0 + 33 - __ffs(pm0r);
+      if (live_c1 && !s.alive1()) s.ncons1 = pos0 + 33 - __ffs(pm1r);
+      const unsigned pm0 =
+          kRegions ? __brev(__reduce_or_sync(0xffffffffu, kCkpt == 4 ? pm0r : (pm0r | pm1r))) : 0u;
+      const unsigned pm1 = kCkpt == 4 ? __brev(__reduce_or_sync(0xffffffffu, pm1r)) : 0u;
       if (kRegions) {
         if ((pm0 >> lane) & 1u) rl[r_count + __popc(pm0 & lt_mask)] = (uint32_t)(pos0 + lane);
         r_count += __popc(pm0);
@@ -364,7 +377,7 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
     out_color[3 * pix + 2] = fmaf(s.T.x, bg_b, s.Cb.x);
     out_depth[pix] = s.D.x;
     out_T[pix] = s.T.x;
-    out_ncontrib[pix] = (int)s.nc.x;
+    out_ncontrib[pix] = s.nc0;
     out_ncons[pix] = s.ncons0;
   }
   if (in1) {
@@ -374,7 +387,7 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
     out_color[3 * pix + 2] = fmaf(s.T.y, bg_b, s.Cb.y);
     out_depth[pix] = s.D.y;
     out_T[pix] = s.T.y;
-    out_ncontrib[pix] = (int)s.nc.y;
+    out_ncontrib[pix] = s.nc1;
     out_ncons[pix] = s.ncons1;
   }
 }
