@@ -377,14 +377,10 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
         dyy[g] = __fmul2_rn(dy[g], dy[g]);
         cyy[g] = __fmul2_rn(bc(cc), dyy[g]);
       }
+      // accumulators start from their first term (no adds of zero)
       float2 G[kNRG], H[kNRG];  // per row pair: sum gq, sum gq dx (over the two columns)
-      float Sq[2] = {0.f, 0.f};  // per column: sum gq
-      float2 wr = bc(0.f), wg = bc(0.f), wbl = bc(0.f), wd = bc(0.f);
-#pragma unroll
-      for (int g = 0; g < kNRG; ++g) {
-        G[g] = bc(0.f);
-        H[g] = bc(0.f);
-      }
+      float Sq[2];              // per column: sum gq
+      float2 wr, wg, wbl, wd = bc(0.f);
 #pragma unroll
       for (int q = 0; q < kNQ; ++q) {
         const int c = q / kNRG, g = q % kNRG;
@@ -408,18 +404,36 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
         // for them; a non-participant with raw == 0 has gauss == 0
         const float2 ld = f2(a.x == raw.x ? dL.x : 0.f, a.y == raw.y ? dL.y : 0.f);
         const float2 gq = __fmul2_rn(ld, al);
-        G[g] = __fadd2_rn(G[g], gq);
-        H[g] = __ffma2_rn(gq, bc(dx[c]), H[g]);
-        Sq[c] += gq.x + gq.y;
-        wr = __ffma2_rn(w, gr[q], wr);
-        wg = __ffma2_rn(w, gg[q], wg);
-        wbl = __ffma2_rn(w, gb[q], wbl);
-        if (kDepth) wd = __ffma2_rn(w, gd[q], wd);
+        if (c == 0) {
+          G[g] = gq;
+          H[g] = __fmul2_rn(gq, bc(dx[c]));
+        } else {
+          G[g] = __fadd2_rn(G[g], gq);
+          H[g] = __ffma2_rn(gq, bc(dx[c]), H[g]);
+        }
+        if (g == 0)
+          Sq[c] = gq.x + gq.y;
+        else
+          Sq[c] += gq.x + gq.y;
+        if (q == 0) {
+          wr = __fmul2_rn(w, gr[q]);
+          wg = __fmul2_rn(w, gg[q]);
+          wbl = __fmul2_rn(w, gb[q]);
+          if (kDepth) wd = __fmul2_rn(w, gd[q]);
+        } else {
+          wr = __ffma2_rn(w, gr[q], wr);
+          wg = __ffma2_rn(w, gg[q], wg);
+          wbl = __ffma2_rn(w, gb[q], wbl);
+          if (kDepth) wd = __ffma2_rn(w, gd[q], wd);
+        }
       }
       // region sums of this lane's pixels, added to the incoming sums
-      float t_mx = 0.f, t_b = 0.f, t_my = 0.f, t_c = 0.f, t_o = 0.f;
+      float t_mx = H[0].x + H[0].y, t_o = G[0].x + G[0].y;
+      float t_b = fmaf(H[0].x, dy[0].x, __fmul_rn(H[0].y, dy[0].y));
+      float t_my = fmaf(G[0].x, dy[0].x, __fmul_rn(G[0].y, dy[0].y));
+      float t_c = fmaf(G[0].x, dyy[0].x, __fmul_rn(G[0].y, dyy[0].y));
 #pragma unroll
-      for (int g = 0; g < kNRG; ++g) {
+      for (int g = 1; g < kNRG; ++g) {
         t_mx += H[g].x + H[g].y;
         t_b = fmaf(H[g].x, dy[g].x, fmaf(H[g].y, dy[g].y, t_b));
         t_my = fmaf(G[g].x, dy[g].x, fmaf(G[g].y, dy[g].y, t_my));
