@@ -21,7 +21,10 @@
 // bit for bit.  Every other entry contributes exact zeros to every pixel of
 // the region, so skipping it changes nothing.
 //
-// Layout.  A warp is one work unit (tile, pair p, segment): its two 16-lane
+// Layout (shown for 8x8 regions, 16-lane groups; the default 8x4 regions
+// run four 8-lane groups per warp over the tile's eight regions, lane j
+// owning (x0, y0), (x0, y0 + 2), (x0 + 4, y0), (x0 + 4, y0 + 2) of its 8x4
+// region, the same arithmetic).  A warp is one work unit (tile, pair p, segment): its two 16-lane
 // halves run two of the tile's four 8x8 regions (bx, by) -- the segment's two
 // longest region lists for p = 0, the other two for p = 1, so the lockstep
 // halves have similar step counts; lane j of a half owns

@@ -157,12 +157,13 @@ def render_raw(rec, values, offsets, ckpt_base, width: int, height: int, backgro
         _lib.ptr(tile_order), _lib.stream_handle()), "tsr_render_fwd_ordered")
 
 
-REGION_HEIGHT = int(os.environ.get("TSR_K4R_REGION", 8))
+# 8x4 regions by default (8 per tile, 8-lane K4r pipelines); 8x8 with TSR_K4R_REGION=8
+REGION_HEIGHT = int(os.environ.get("TSR_K4R_REGION", 4))
 
 
 class RegionLists:
-    """Per-(tile, 8x8 region) list positions K3 writes for the region-culled
-    K4 (tsr_render_fwd_regions): 4 x p_bound uint32 entries, the
+    """Per-(tile, region) list positions K3 writes for the region-culled
+    K4 (tsr_render_fwd_regions): one list slot per region and pair, the
     segment-boundary offsets and the backward's work-unit queue; sized for a
     pair bound, reused across steps."""
 
