@@ -23,7 +23,30 @@ for _ in range(5):
 torch.cuda.synchronize()
 
 
+# every variant replays the same training segment (the scene trains during
+# the run and per-step work drifts: tools/drift_probe.py)
+snap = {k: v.clone() for k, v in g.params().items()}
+snap_m = {k: v.clone() for k, v in st.opt._m.items()}
+snap_v = {k: v.clone() for k, v in st.opt._v.items()}
+snap_steps = dict(st.opt._steps)
+snap_it = st.iteration
+
+
+def restore():
+    torch.cuda.synchronize()
+    for k, v in g.params().items():
+        v.copy_(snap[k])
+    for k in snap_m:
+        st.opt._m[k].copy_(snap_m[k])
+        st.opt._v[k].copy_(snap_v[k])
+    st.opt._steps.update(snap_steps)
+    st.iteration = snap_it
+    torch.cuda.synchronize()
+
+
 def timed(fn):
+    fn()  # graphs for every buffer captured before timing
+    restore()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     fn()
@@ -67,6 +90,38 @@ def double():
         consumed[cur].record()
 
 
+loss_host = torch.zeros(K, dtype=torch.float32).pin_memory()
+
+
+def double_d2h(on_copy_stream):
+    """bench.py's e2e loop: double-buffered GT H2D plus a per-step loss D2H,
+    on the compute stream (as bench.py) or on the copy stream after the step."""
+    done = [torch.cuda.Event() for _ in range(2)]
+    with torch.cuda.stream(cs):
+        bufs[0].copy_(gt_host, non_blocking=True)
+        copied[0].record(cs)
+    for k in range(K):
+        cur, nxt = k % 2, (k + 1) % 2
+        torch.cuda.current_stream().wait_event(copied[cur])
+        if k + 1 < K:
+            if k >= 1:
+                cs.wait_event(consumed[nxt])
+            with torch.cuda.stream(cs):
+                bufs[nxt].copy_(gt_host, non_blocking=True)
+                copied[nxt].record(cs)
+        loss = st.step(c, bufs[cur])
+        consumed[cur].record()
+        if on_copy_stream:
+            cs.wait_event(consumed[cur])
+            with torch.cuda.stream(cs):
+                loss_host[k:k + 1].copy_(loss.reshape(1), non_blocking=True)
+                done[cur].record(cs)
+        else:
+            loss_host[k:k + 1].copy_(loss.reshape(1), non_blocking=True)
+
+
 for name, fn in (("resident", resident), ("double-buffered H2D", double), ("serial H2D", serial),
+                 ("double + D2H (compute)", lambda: double_d2h(False)),
+                 ("double + D2H (copy)", lambda: double_d2h(True)),
                  ("resident again", resident)):
     print(f"{name:22s} {timed(fn):.3f} ms/step")
