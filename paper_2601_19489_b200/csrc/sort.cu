@@ -234,12 +234,17 @@ __device__ __forceinline__ uint32_t digit_of(K k, int shift, uint32_t mask) {
 }
 
 // ---- radix pass, phase 1: per-CTA digit histogram of the slice
+// or_bits (first depth pass only): OR of the keys and OR of their
+// complements (= ~AND) into or_bits[0..1], one atomic pair per warp -- which
+// depth bytes are the same for every row (those passes are skipped)
 template <typename K, int kI>
 __device__ void count_phase(const K* __restrict__ kin, long long lo, long long hi, int shift,
-                            uint32_t mask, uint32_t* __restrict__ cnt_out, SortSmem& sm) {
+                            uint32_t mask, uint32_t* __restrict__ cnt_out, SortSmem& sm,
+                            uint32_t* __restrict__ or_bits = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   sm.h[0][tid] = 0;
   __syncthreads();
+  uint32_t o = 0u, no = 0u;
   for (long long base = lo; base < hi; base += (kSB * kI)) {
     const long long wb = base + (long long)warp * (32 * kI);
     K k[kI];
@@ -249,8 +254,24 @@ __device__ void count_phase(const K* __restrict__ kin, long long lo, long long h
       k[r] = i < hi ? kin[i] : (K)0;
     }
 #pragma unroll
-    for (int r = 0; r < kI; ++r)
-      hist_add(sm.h[0], digit_of(k[r], shift, mask), wb + r * 32 + lane < hi);
+    for (int r = 0; r < kI; ++r) {
+      const bool valid = wb + r * 32 + lane < hi;
+      hist_add(sm.h[0], digit_of(k[r], shift, mask), valid);
+      if (or_bits && valid) {
+        o |= (uint32_t)k[r];
+        no |= ~(uint32_t)k[r];
+      }
+    }
+  }
+  if (or_bits) {
+    for (int d = 16; d > 0; d >>= 1) {
+      o |= __shfl_xor_sync(0xffffffffu, o, d);
+      no |= __shfl_xor_sync(0xffffffffu, no, d);
+    }
+    if (lane == 0 && (o | no)) {
+      atomicOr(&or_bits[0], o);
+      atomicOr(&or_bits[1], no);
+    }
   }
   __syncthreads();
   cnt_out[tid] = sm.h[0][tid];
@@ -418,11 +439,13 @@ __device__ void radix_pass(const IndexArgs& a, int& nb, const K* kin, const uint
                            KO* kout, uint32_t* vout, long long n, int shift, int bits,
                            SortSmem& sm, unsigned char* dyn,
                            const uint32_t* gather = nullptr, uint32_t* inv = nullptr,
-                           const uint32_t* depth_of_row = nullptr) {
+                           const uint32_t* depth_of_row = nullptr,
+                           uint32_t* or_bits = nullptr) {
   const int G = gridDim.x, bid = blockIdx.x;
   long long lo, hi;
   slice(n, bid, G, lo, hi);
-  count_phase<K, kI>(kin, lo, hi, shift, (1u << bits) - 1u, a.cnt + (long long)bid * kBins, sm);
+  count_phase<K, kI>(kin, lo, hi, shift, (1u << bits) - 1u, a.cnt + (long long)bid * kBins, sm,
+                     or_bits);
   grid_barrier(a.bar + nb++, G);
   colscan_phase(a.cnt, a.colscan, a.dtotal, G, sm);
   grid_barrier(a.bar + nb++, G);
@@ -621,42 +644,24 @@ __global__ void __launch_bounds__(kSB, 3) build_index_kernel(IndexArgs a) {
 #endif
 
   // ---- 1. depth ranks
-  // which depth bytes are the same for every row (those passes are
-  // trivial): OR of the keys and OR of their complements (= ~AND), one
-  // atomic pair per CTA
-  {
-    long long lo, hi;
-    slice(m, bid, G, lo, hi);
-    uint32_t o = 0u, no = 0u;
-    for (long long i = lo + tid; i < hi; i += kSB) {
-      const uint32_t k = a.depth_bits[i];
-      o |= k;
-      no |= ~k;
-    }
-    for (int d = 16; d > 0; d >>= 1) {
-      o |= __shfl_xor_sync(0xffffffffu, o, d);
-      no |= __shfl_xor_sync(0xffffffffu, no, d);
-    }
-    if ((tid & 31) == 0 && lo < hi) {
-      atomicOr(&a.hist4[0], o);
-      atomicOr(&a.hist4[1], no);
-    }
-  }
-  grid_barrier(a.bar + nb++, G);
-  if (tid < 4) {
-    // byte q is constant iff no bit of it is 1 in some row and 0 in another
-    const uint32_t var = a.hist4[0] & a.hist4[1];
-    sm.skip[tid] = m == 0 || ((var >> (8 * tid)) & 255u) == 0u;
-  }
-  __syncthreads();
+  // byte 0 (the mantissa's low byte) is sorted unconditionally -- a
+  // constant digit makes the stable pass the identity -- and its count phase
+  // finds which of bytes 1-3 are the same for every row (no separate pass
+  // over the keys, no extra barrier); those passes are skipped
   const uint32_t* dkey = a.depth_bits;
   const uint32_t* drow = nullptr;  // identity
   {
     uint32_t* ko[2] = {a.dk0, a.dk1};
     uint32_t* vo[2] = {a.dv0, a.dv1};
-    int par = 0;
-    for (int q = 0; q < 4; ++q) {
-      if (sm.skip[q]) continue;
+    radix_pass<uint32_t, kDepthItems>(a, nb, dkey, drow, ko[0], vo[0], m, 0, 8, sm, dyn, nullptr,
+                                      nullptr, nullptr, a.hist4);
+    dkey = ko[0];
+    drow = vo[0];
+    // byte q is constant iff no bit of it is 1 in some row and 0 in another
+    const uint32_t var = a.hist4[0] & a.hist4[1];
+    int par = 1;
+    for (int q = 1; q < 4; ++q) {
+      if (m == 0 || ((var >> (8 * q)) & 255u) == 0u) continue;  // CTA-uniform
       radix_pass<uint32_t, kDepthItems>(a, nb, dkey, drow, ko[par], vo[par], m, 8 * q, 8, sm, dyn);
       dkey = ko[par];
       drow = vo[par];
