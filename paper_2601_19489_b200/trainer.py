@@ -255,6 +255,10 @@ class TrainStep:
         self.redone_steps = 0
         self.merges = torch.zeros(1, dtype=torch.int64, device=dev)
         self.loss_ws = losses.PhotometricWorkspace()
+        # recorded once the step's loss kernels have read the GT image (also
+        # inside a captured step: an external event node), so a host-fed loop
+        # may refill that GT buffer while the backward still runs
+        self.gt_consumed = torch.cuda.Event(external=True)
         from .backward import BackwardWorkspace
         self.bwd_ws = BackwardWorkspace()
         self.regions = None
@@ -438,6 +442,7 @@ class TrainStep:
         e, l1, s, grad_color = losses.photometric_device(out.color, gt_image, self.cfg.lambda_,
                                                          grad=self.grad_color,
                                                          workspace=self.loss_ws)
+        self.gt_consumed.record()  # the GT image's last reader is the loss pair
         gd = gt = None
         dl = None
         # (a tensor weight comes from graph capture: no host read of it)

@@ -120,7 +120,29 @@ def double_d2h(on_copy_stream):
             loss_host[k:k + 1].copy_(loss.reshape(1), non_blocking=True)
 
 
+def early_refill():
+    """GT buffer refilled once the step's loss kernels have read it
+    (TrainStep.gt_consumed): the copy for step k + 2 runs under step k's
+    backward."""
+    with torch.cuda.stream(cs):
+        bufs[0].copy_(gt_host, non_blocking=True)
+        copied[0].record(cs)
+        bufs[1].copy_(gt_host, non_blocking=True)
+        copied[1].record(cs)
+    for k in range(K):
+        cur = k % 2
+        torch.cuda.current_stream().wait_event(copied[cur])
+        loss = st.step(c, bufs[cur])
+        if k + 2 < K:
+            cs.wait_event(st.gt_consumed)
+            with torch.cuda.stream(cs):
+                bufs[cur].copy_(gt_host, non_blocking=True)
+                copied[cur].record(cs)
+        loss_host[k:k + 1].copy_(loss.reshape(1), non_blocking=True)
+
+
 for name, fn in (("resident", resident), ("double-buffered H2D", double), ("serial H2D", serial),
+                 ("early refill (gt_consumed)", early_refill),
                  ("double + D2H (compute)", lambda: double_d2h(False)),
                  ("double + D2H (copy)", lambda: double_d2h(True)),
                  ("resident again", resident)):
