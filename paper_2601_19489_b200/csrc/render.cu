@@ -124,8 +124,9 @@ __device__ __forceinline__ void blend_pair(const float4 g, const float4 c, const
 // list position that blends at >= 1 pixel of the region is appended to the
 // region's list, in list order -- exactly the entries with a participating
 // pixel (p < n_considered, alpha >= 1/255) in the backward; the others
-// contribute exact zeros there.  Region r of tile t stores its
-// positions at list[4 start_t + r n_t ...]; seg[4 (segbase_t + s - 1) + r]
+// contribute exact zeros there.  With kNR regions per tile (4: 8x8, 8: 8x4
+// halves) region r of tile t stores its positions at
+// list[kNR start_t + r n_t ...]; seg[kNR (segbase_t + s - 1) + r]
 // holds the number of entries with position < kSeg s for s = 1..ceil(n/kSeg)
 // (segbase_t = (start_t >> 10) + t: floor((O + n) / kSeg) - floor(O / kSeg)
 // + 1 >= ceil(n / kSeg), so the tiles' segment slots never overlap).
