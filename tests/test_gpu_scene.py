@@ -241,3 +241,55 @@ def test_deterministic_train_step_is_bitwise_reproducible():
     for k in runs[0]:
         assert np.array_equal(runs[0][k], runs[1][k]), k
         assert np.array_equal(runs[0][k], runs[2][k]), k
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+def test_gt_refilled_after_gt_consumed_trains_like_resident_gt(graphs):
+    """A host-fed loop that refills each of two GT buffers as soon as
+    TrainStep.gt_consumed fires (the copy of view k + 2 overlaps step k's
+    backward; bench.py's e2e loop) trains exactly like device-resident GT
+    images: deterministic merge, a different GT every step, bitwise-equal
+    parameters and losses.  A GT buffer overwritten before its step's loss
+    kernels read it would change them."""
+    import torch
+    import paper_2601_19489_b200 as ts
+    from oracle.raster import make_scene
+    params, cam, gt = make_scene(20_000, 320, 240, seed=11)
+    camera = ts.Camera(cam["fx"], cam["fy"], cam["cx"], cam["cy"], 320, 240, cam["R"], cam["t"])
+    rng = np.random.default_rng(5)
+    host = [torch.from_numpy(np.clip(np.asarray(gt, np.float32)
+                                     + rng.normal(0, 0.1, gt.shape).astype(np.float32), 0, 1))
+            .pin_memory() for _ in range(5)]
+    steps = 8
+    # resident: every step's GT already on the device
+    g = ts.GaussianSet(**params)
+    st = ts.TrainStep(g, ts.TrainConfig(max_iters=100), deterministic=True, graphs=graphs)
+    dev = [h.cuda() for h in host]
+    ref_losses = [float(st.step(camera, dev[k % 5])) for k in range(steps)]
+    torch.cuda.synchronize()
+    ref = g.to_numpy()
+    # host-fed: two device buffers refilled after gt_consumed
+    g = ts.GaussianSet(**params)
+    st = ts.TrainStep(g, ts.TrainConfig(max_iters=100), deterministic=True, graphs=graphs)
+    cs = torch.cuda.Stream()
+    bufs = [torch.empty_like(dev[0]) for _ in range(2)]
+    copied = [torch.cuda.Event() for _ in range(2)]
+    with torch.cuda.stream(cs):
+        for b in range(2):
+            bufs[b].copy_(host[b], non_blocking=True)
+            copied[b].record(cs)
+    losses = []
+    for k in range(steps):
+        cur = k % 2
+        torch.cuda.current_stream().wait_event(copied[cur])
+        losses.append(st.step(camera, bufs[cur]).clone())  # a replay reuses its output
+        if k + 2 < steps:
+            cs.wait_event(st.gt_consumed)
+            with torch.cuda.stream(cs):
+                bufs[cur].copy_(host[(k + 2) % 5], non_blocking=True)
+                copied[cur].record(cs)
+    torch.cuda.synchronize()
+    assert [float(e) for e in losses] == ref_losses
+    out = g.to_numpy()
+    for name in ref:
+        assert np.array_equal(out[name], ref[name]), name
