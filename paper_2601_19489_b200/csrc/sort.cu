@@ -5,18 +5,19 @@
 // (binning.py:137-158), so ties resolve by emission (= batch row) order.  The
 // same order is produced here with far less traffic:
 //   1. stable LSD radix sort of the M rows by their 32-bit depth bits (8-bit
-//      digits; a pass whose digit is the same for every row -- e.g. the
-//      exponent byte -- is skipped) -> depth rank of every row; rank order
-//      == (depth bits, row) order, exactly the reference's tie rule;
-//   2. rank-major emission of (key = tile << 32 | depth bits, value = row)
-//      pairs from K1's compact column spans (written by both SnugBox
-//      strategies; rows whose span did not fit the 16-byte record re-walk
-//      in FP64),
-//      staged in shared memory so every CTA stores its contiguous output
-//      range coalesced;
+//      digits; byte 0 always, bytes 1-3 unless the first pass's count phase
+//      finds them the same for every row -- e.g. the exponent byte; 2,560-
+//      item sub-tiles) -> depth rank of every row; rank order == (depth
+//      bits, row) order, exactly the reference's tie rule;
+//   2. rank-major emission of (tile, row) pairs -- 4-byte tile keys -- from
+//      K1's compact column spans (written by both SnugBox strategies; rows
+//      whose span did not fit the 16-byte record re-walk in FP64), staged
+//      in shared memory so every CTA stores its contiguous output range
+//      coalesced;
 //   3. stable LSD radix sort of the pairs by the tile bits only (1-2 passes
-//      of ~half the tile bits each): within a tile, rank order.  The last
-//      pass writes the final int64 keys and int32 rows;
+//      of ~half the tile bits each, 2,048-item sub-tiles): within a tile,
+//      rank order.  The last pass writes the final int64 keys tile << 32 |
+//      depth bits of the row and the int32 rows;
 //   4. per-tile ranges from the boundaries of the sorted keys; checkpoint
 //      bases ckpt_base[t] = offsets[t] >> 5 (record r of tile t lives at
 //      ckpt_base[t] + r: floor((O + n) / 32) - floor(O / 32) >= floor(n / 32),

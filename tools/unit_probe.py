@@ -1,5 +1,7 @@
-"""Distribution of the region-culled K4's unit spans (max list length of the
-unit's two regions) at C2 after a few training steps."""
+"""Lockstep efficiency of the region-culled K4's units at C2 after a few
+training steps: per unit (a tile's segment, half of its regions, sorted by
+list length) the groups of a warp run max(L) + kGL - 1 steps; efficiency =
+sum(L) / (groups x steps)."""
 import sys
 from pathlib import Path
 
@@ -18,26 +20,32 @@ gt = torch.from_numpy(np.asarray(gt, np.float32)).cuda()
 for _ in range(6):
     st.step(c, gt)
 torch.cuda.synchronize()
+nr = 8 if st.regions.height == 4 else 4   # regions per tile
+gl = 8 if st.regions.height == 4 else 16  # lanes per region pipeline
+per_unit = nr // 2
 off = st.index.offsets.cpu().numpy()
 seg = st.regions.seg.cpu().numpy()
-spans = []
+work = steps = 0
+lmax_all, eff_units = [], []
 for t in range(len(off) - 1):
     lo, n = int(off[t]), int(off[t + 1] - off[t])
     if n == 0:
         continue
     nseg = -(-n // 1024)
-    prev = np.zeros(4, np.int64)
+    prev = np.zeros(nr, np.int64)
     for s in range(1, nseg + 1):
-        cur = seg[4 * ((lo >> 10) + t + s - 1): 4 * ((lo >> 10) + t + s - 1) + 4].astype(np.int64)
+        b = nr * ((lo >> 10) + t + s - 1)
+        cur = seg[b:b + nr].astype(np.int64)
         L = np.sort(cur - prev)[::-1]
         prev = cur
-        for pair in (L[:2], L[2:]):
-            spans.append(int(pair.max()))
-spans = np.array(spans)
-nz = spans[spans > 0]
-print("units", len(spans), "nonempty", len(nz), "sum span", int(nz.sum()), "fill 15/unit", 15 * len(nz))
-for q in (5, 10, 25, 50, 75, 90):
-    print(f"p{q}", np.percentile(nz, q))
-print("units with span < 17:", int((nz < 17).sum()), " < 32:", int((nz < 32).sum()))
-pad32 = np.maximum(nz, 32).sum()
-print("current steps ~", int((nz + 15).sum()), " chained (pad 32) ~", int(pad32 + 15 * 0))
+        for u in range(2):
+            Lu = L[u * per_unit:(u + 1) * per_unit]
+            if Lu.max() == 0:
+                continue
+            work += int(Lu.sum())
+            steps += per_unit * int(Lu.max() + gl - 1)
+            lmax_all.append(int(Lu.max()))
+print(f"regions/tile {nr}, lanes {gl}: units {len(lmax_all)}, entries {work}, "
+      f"group-steps {steps}, lockstep efficiency {work / max(steps, 1):.3f}")
+la = np.array(lmax_all)
+print("unit max length percentiles:", {q: float(np.percentile(la, q)) for q in (10, 50, 90)})
