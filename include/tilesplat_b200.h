@@ -207,19 +207,20 @@ size_t tsr_render_bwd_workspace(int32_t width, int32_t height, int64_t p_bound);
  * tsr_render_fwd_ordered(ckpt_stride 2) + tsr_render_bwd_ordered pair behind
  * backward_per_gaussian, backward.py:137-223).  tsr_render_fwd_regions is K3
  * writing checkpoint records only at segment starts (every 1024 list
- * positions) plus, per (tile, region), the list positions whose splat
- * passes the region's conservative alpha >= 1/255 test (regions of 8 x
- * region_height pixels, region_height 8 or 4; both calls take the same
- * value), and the work units of
- * the backward (tile, row pair, segment), queued as the tiles finish:
+ * positions) plus, per (tile, region), the list positions that blend at >= 1
+ * pixel of the region (regions of 8 x region_height pixels, region_height 8
+ * or 4; both calls take the same value), and the work units of the backward
+ * (tile, segment, row pair), filed as each tile finishes under the bucket
+ * of the unit's longest region list (32 entries per bucket):
  *   region_list   tsr_region_list_entries(...) uint32
  *   region_seg    tsr_region_seg_entries(...) int32
- *   region_units  tsr_region_unit_entries(...) uint32
- *   region_ctl    2 int32 (unit count, grab counter; zeroed by the call).
+ *   region_units  tsr_region_unit_entries(...) uint32 (16 buckets)
+ *   region_ctl    tsr_region_ctl_entries() int32 (bucket counts, grab
+ *                 counter; zeroed by tsr_render_fwd_regions).
  * tsr_render_bwd_regions streams each region's list past its pixels (one
- * 16-lane systolic pipeline per region, units drawn from the queue) and
- * merges the same Grad2D sums with atomics.  p_bound >= the pair count (a
- * capacity is fine). */
+ * systolic pipeline of 8 (region_height 4) or 16 lanes per region, units
+ * drawn longest first) and merges the same Grad2D sums with atomics.
+ * p_bound >= the pair count (a capacity is fine). */
 int tsr_render_fwd_regions(const float* rec, const int32_t* values, const int64_t* offsets,
                            int32_t width, int32_t height, const float* background_host,
                            float* out_color, float* out_depth, float* out_final_T,
@@ -230,6 +231,7 @@ int tsr_render_fwd_regions(const float* rec, const int32_t* values, const int64_
 size_t tsr_region_list_entries(int32_t width, int32_t height, int64_t p_bound);
 size_t tsr_region_seg_entries(int32_t width, int32_t height, int64_t p_bound);
 size_t tsr_region_unit_entries(int32_t width, int32_t height, int64_t p_bound);
+size_t tsr_region_ctl_entries(void);
 int tsr_render_bwd_regions(const float* rec, const int32_t* values, const int64_t* offsets,
                            int32_t width, int32_t height, const float* color, const float* depth,
                            const float* final_T, const int32_t* n_considered, const float* ckpt,

@@ -88,6 +88,7 @@ _SIGNATURES = {
     "tsr_region_list_entries": (c_sz, [c_i32, c_i32, c_i64]),
     "tsr_region_seg_entries": (c_sz, [c_i32, c_i32, c_i64]),
     "tsr_region_unit_entries": (c_sz, [c_i32, c_i32, c_i64]),
+    "tsr_region_ctl_entries": (c_sz, []),
     "tsr_render_bwd_regions": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp,
                                        c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                        c_vp, c_vp, c_i32, c_vp]),

@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
     const float* __restrict__ grad_color, const float* __restrict__ grad_depth,
     const float* __restrict__ grad_final_T, float* __restrict__ grad2d,
     unsigned long long* __restrict__ merges, const uint32_t* __restrict__ units,
-    const int32_t* __restrict__ n_units_dev, int32_t* __restrict__ counter) {
+    const int32_t* __restrict__ bucket_counts, int32_t* __restrict__ counter) {
   constexpr int kGPW = 32 / kGL;               // regions (lane groups) per warp
   constexpr int kRS = kGL / 4;                 // row stride of a lane's pixels
   constexpr int kRH = kRS * (kPX / 2);         // region height
@@ -177,14 +177,32 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
   const float4 sent_b = make_float4(1.f, 1.f, 0.f, 0.f);
   const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
   const float keep = j != 0 ? 1.f : 0.f;  // lane 0 of a group starts each entry's sums
-  const int n_units = *n_units_dev;
+  // units are drawn longest first: bucket kUnitBuckets - 1 down to 0 (K3
+  // filed each unit under its step count); lane b < kUnitBuckets holds the
+  // bucket's count, its units start at units[b * cap]
+  const int cap = (int)tsr_unit_bucket_cap(offsets[tiles_x * ((height + kTile - 1) / kTile)],
+                                           tiles_x * ((height + kTile - 1) / kTile));
+  const int bcount = lane < kUnitBuckets ? bucket_counts[lane] : 0;
+  // lane b: units in buckets b .. kUnitBuckets - 1 (incl) and above b (above)
+  int incl = bcount;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int v = __shfl_down_sync(0xffffffffu, incl, d);
+    if (lane + d < 32) incl += v;
+  }
+  const int above = incl - bcount;
+  const int n_units = __shfl_sync(0xffffffffu, incl, 0);
 
   for (;;) {
     int u = 0;
     if (lane == 0) u = atomicAdd(counter, 1);
     u = __shfl_sync(0xffffffffu, u, 0);
     if (u >= n_units) break;
-    const uint32_t code = units[u];
+    // grab index u's bucket: the buckets in descending order
+    const unsigned hit = __ballot_sync(0xffffffffu, lane < kUnitBuckets && u >= above && u < incl);
+    const int b = __ffs(hit) - 1;
+    const int b_above = __shfl_sync(0xffffffffu, above, b);
+    const uint32_t code = units[(long long)b * cap + (u - b_above)];
     const int tile = (int)(code >> 16), seg = (int)((code >> 1) & 0x7fffu), rp = (int)(code & 1u);
     if (rp >= kUPS) continue;  // K3 queues two units per segment; this shape runs one
     const long long start = offsets[tile];
@@ -541,8 +559,12 @@ extern "C" size_t tsr_region_list_entries(int32_t width, int32_t height, int64_t
 
 extern "C" size_t tsr_region_unit_entries(int32_t width, int32_t height, int64_t p_bound) {
   if (width <= 0 || height <= 0) return 0;
-  return 2 * ((size_t)(p_bound > 0 ? p_bound : 0) / kSeg + (size_t)tiles_of(width) * tiles_of(height) + 1);
+  // kUnitBuckets buckets, each able to hold every unit of a P <= p_bound list
+  return (size_t)kUnitBuckets *
+         (size_t)tsr_unit_bucket_cap(p_bound > 0 ? p_bound : 0, tiles_of(width) * tiles_of(height));
 }
+
+extern "C" size_t tsr_region_ctl_entries(void) { return kUnitCtl; }
 
 extern "C" size_t tsr_region_seg_entries(int32_t width, int32_t height, int64_t p_bound) {
   if (width <= 0 || height <= 0) return 0;
@@ -586,11 +608,11 @@ extern "C" int tsr_render_bwd_regions(const float* rec, const int32_t* values,
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k, kRThreads, 0);
     if (ps < 1) ps = 1;
   }
-  // region_ctl = (n_units written by K3, grab counter zeroed with it)
+  // region_ctl = (bucket counts filed by K3, grab counter; zeroed by K3's launch)
   k<<<sms * ps, kRThreads, 0, s>>>((const float4*)rec, values, offsets, width, height, tx, color,
                                    depth, final_T, n_considered, ckpt, ckpt_base, region_list,
                                    region_seg, grad_color, grad_depth, grad_final_T, grad2d, merges,
-                                   region_units, region_ctl, region_ctl + 1);
+                                   region_units, region_ctl, region_ctl + kUnitBuckets);
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }

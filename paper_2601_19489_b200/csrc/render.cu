@@ -130,11 +130,11 @@ __device__ __forceinline__ void blend_pair(const float4 g, const float4 c, const
 // holds the number of entries with position < kSeg s for s = 1..ceil(n/kSeg)
 // (segbase_t = (start_t >> 10) + t: floor((O + n) / kSeg) - floor(O / kSeg)
 // + 1 >= ceil(n / kSeg), so the tiles' segment slots never overlap).
-// It also enqueues the tile's work units for the region-culled K4: unit =
-// tile << 16 | segment << 1 | row pair, 2 ceil(n / kSeg) per tile, appended
-// at units[atomicAdd(ctl[0])] as the tiles start (so the queue order is the
-// K3 launch order: heavy tiles first); ctl (n_units, grab counter) is zeroed
-// before K3 by the launch.
+// It also files the tile's work units for the region-culled K4: unit =
+// tile << 16 | segment << 1 | row pair, 2 ceil(n / kSeg) per tile, under
+// the bucket of the unit's step count once the tile's lists are complete
+// (tsr_unit_bucket; K4r draws them longest first); the control block
+// (bucket counts, grab counter) is zeroed before K3 by the launch.
 struct RegionArgs {
   uint32_t* list;
   int32_t* seg;
@@ -208,12 +208,6 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
   const long long segbase = (start >> kSegShift) + tile;
   if (kRegions) rl = rg.list + kNR * start + (long long)reg0 * n;
   if (kCkpt == 4) rl2 = rg.list + kNR * start + (long long)reg1 * n;
-  if (kRegions && tid == 0 && n > 0) {  // the tile's K4r work units, in K3's launch order
-    const int nu = 2 * ((n + kSeg - 1) >> kSegShift);
-    const int base = atomicAdd(rg.ctl, nu);
-    for (int k = 0; k < nu; ++k)
-      rg.units[base + k] = ((uint32_t)tile << 16) | (uint32_t)k;  // k = segment << 1 | row pair
-  }
   bool m0 = false, m1 = false;
   if (kScore == 3) {
     m0 = in0 && sc.mask[pix0];
@@ -366,6 +360,38 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
       rg.seg[kNR * (segbase + s_next - 1) + reg0] = r_count;
       if (kCkpt == 4) rg.seg[kNR * (segbase + s_next - 1) + reg1] = r_count2;
     }
+  if (kRegions) {
+    // the tile's K4r work units, filed longest first: unit (segment, row
+    // pair 0) runs the segment's kNR / 2 longest region lists, (segment, 1)
+    // the others (backward_regions.cu groups them the same way), so their
+    // step counts are the longest and the (kNR / 2 + 1)-th longest list
+    __syncthreads();  // every warp's segment counts are written
+    const int nseg = (n + kSeg - 1) >> kSegShift;
+    const int cap = (int)tsr_unit_bucket_cap(offsets[gridDim.x], gridDim.x);
+    for (int sg = tid; sg < nseg; sg += kFwdThreads) {
+      int len[kNR];
+#pragma unroll
+      for (int q = 0; q < kNR; ++q) {
+        const int cur = rg.seg[kNR * (segbase + sg) + q];
+        len[q] = cur - (sg > 0 ? rg.seg[kNR * (segbase + sg - 1) + q] : 0);
+      }
+      int top = 0, mid = 0;  // the longest and the (kNR / 2 + 1)-th longest
+#pragma unroll
+      for (int q = 0; q < kNR; ++q) {
+        int rank = 0;
+#pragma unroll
+        for (int o = 0; o < kNR; ++o) rank += (len[o] > len[q]) || (len[o] == len[q] && o < q);
+        if (rank == 0) top = len[q];
+        if (rank == kNR / 2) mid = len[q];
+      }
+#pragma unroll
+      for (int rp = 0; rp < 2; ++rp) {
+        const int b = tsr_unit_bucket(rp == 0 ? top : mid);
+        const int at = atomicAdd(rg.ctl + b, 1);
+        rg.units[(long long)b * cap + at] = ((uint32_t)tile << 16) | ((uint32_t)sg << 1) | (uint32_t)rp;
+      }
+    }
+  }
 
   // a pixel that never terminated considered the whole list (skipped
   // entries included); a terminated one stopped at its death position
@@ -516,7 +542,7 @@ extern "C" int tsr_render_fwd_regions(const float* rec, const int32_t* values,
   const int n_tiles = tx * ty;
   cudaStream_t s = (cudaStream_t)stream;
   const ScoreArgs none{};
-  if (cudaMemsetAsync(region_ctl, 0, 2 * sizeof(int32_t), s) != cudaSuccess) return TSR_E_CUDA;
+  if (cudaMemsetAsync(region_ctl, 0, kUnitCtl * sizeof(int32_t), s) != cudaSuccess) return TSR_E_CUDA;
   auto* k = region_height == 8 ? render_fwd_kernel<3, 0> : render_fwd_kernel<4, 0>;
   k<<<n_tiles, kFwdThreads, 0, s>>>(
       (const float4*)rec, values, offsets, width, height, tx, background_host[0],

@@ -24,6 +24,21 @@ constexpr int kGroup = 32;  // CHECKPOINT_INTERVAL (forward.py:28)
 // of 2 kGroup; K3 writes a checkpoint record at every segment start)
 constexpr int kSegShift = 10;
 constexpr int kSeg = 1 << kSegShift;
+// Region-culled K4 work units are queued longest first: K3 files each unit
+// (tile, segment, row pair) under its longest list's bucket (32 entries per
+// bucket, kUnitBuckets buckets, the last open-ended) once the tile's region
+// lists are complete; bucket b holds up to tsr_unit_bucket_cap(P, tiles)
+// units at units[b * cap ...], its count at ctl[b]; ctl[kUnitBuckets] is
+// the backward's grab counter.
+constexpr int kUnitBuckets = 16;
+constexpr int kUnitCtl = 32;  // ints in the control block (zeroed by K3's launch)
+__host__ __device__ inline long long tsr_unit_bucket_cap(long long pairs, int n_tiles) {
+  return 2 * (pairs / kSeg + n_tiles + 1);
+}
+__host__ __device__ inline int tsr_unit_bucket(int length) {  // the unit's longest list
+  const int b = length >> 5;
+  return b < kUnitBuckets - 1 ? b : kUnitBuckets - 1;
+}
 constexpr float kAlphaCap = 0.99f;                 // forward.py:25
 constexpr float kMinAlpha = 1.0f / 255.0f;         // forward.py:26
 constexpr float kTTerminate = 1e-4f;               // forward.py:27

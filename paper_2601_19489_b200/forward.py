@@ -178,7 +178,8 @@ class RegionLists:
                                dtype=torch.int32, device=dev)
         self.units = torch.empty(int(lib.tsr_region_unit_entries(width, height, p_bound)),
                                  dtype=torch.int32, device=dev)
-        self.ctl = torch.zeros(2, dtype=torch.int32, device=dev)  # unit count, grab counter
+        # per-bucket unit counts + the backward's grab counter (zeroed by K3's launch)
+        self.ctl = torch.zeros(int(lib.tsr_region_ctl_entries()), dtype=torch.int32, device=dev)
         self.shape = (width, height, p_bound)
 
 

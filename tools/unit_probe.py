@@ -49,3 +49,4 @@ print(f"regions/tile {nr}, lanes {gl}: units {len(lmax_all)}, entries {work}, "
       f"group-steps {steps}, lockstep efficiency {work / max(steps, 1):.3f}")
 la = np.array(lmax_all)
 print("unit max length percentiles:", {q: float(np.percentile(la, q)) for q in (10, 50, 90)})
+
