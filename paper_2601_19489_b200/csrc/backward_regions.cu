@@ -44,7 +44,8 @@
 // tile (K3 writes a checkpoint record at every segment start and the region
 // list offsets at every segment boundary), so a heavy tile's work spreads
 // over many warps (the paper's redistribution across heavy tiles,
-// PAPER.md:121/145); units are drawn from a global queue, long tiles first.
+// PAPER.md:121/145); K3 files the units under their longest list's bucket
+// and they are drawn longest first (the tail holds the short ones).
 #include <climits>
 #include <cstdlib>
 
