@@ -427,6 +427,9 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
 // time (L2 reuse of the splat records); a heavy tile launched in the middle
 // of the frame would finish last and set the tail (the low-opacity cluster
 // of C3-lo: thousands of blends per pixel).  One CTA.
+#ifndef TSR_ORDER_HEAVY_X2
+#define TSR_ORDER_HEAVY_X2 8  // heavy: a list longer than (this / 2) x the mean tile list
+#endif
 constexpr int kOrderThreads = 1024;
 constexpr int kOrderMaxTiles = 11264;  // 44 KB of list lengths in shared memory
 __global__ void __launch_bounds__(kOrderThreads) tile_order_kernel(const int64_t* __restrict__ offsets,
@@ -443,7 +446,7 @@ __global__ void __launch_bounds__(kOrderThreads) tile_order_kernel(const int64_t
       s_len[t] = (int)(offsets[t + 1] - offsets[t]);
   }
   const long long P = offsets[n_tiles] - offsets[0];
-  const long long thr = max(4 * P / max(n_tiles, 1), 64ll);
+  const long long thr = max(TSR_ORDER_HEAVY_X2 * P / (2 * max(n_tiles, 1)), 64ll);
   __syncthreads();
   auto len = [&](int t) -> long long {
     return staged ? (long long)s_len[t] : offsets[t + 1] - offsets[t];
