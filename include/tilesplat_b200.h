@@ -209,17 +209,18 @@ size_t tsr_render_bwd_workspace(int32_t width, int32_t height, int64_t p_bound);
  * writing checkpoint records only at segment starts (every 1024 list
  * positions) plus, per (tile, region), the list positions that blend at >= 1
  * pixel of the region (regions of 8 x region_height pixels, region_height 8
- * or 4; both calls take the same value), and the work units of the backward
- * (tile, segment, row pair), filed as each tile finishes under the bucket
- * of the unit's longest region list (32 entries per bucket):
+ * or 4; both calls take the same value), and the backward's streams (one
+ * per (tile, 1024-position segment, region) with entries), filed as each
+ * tile finishes under the bucket of the stream's length:
  *   region_list   tsr_region_list_entries(...) uint32
  *   region_seg    tsr_region_seg_entries(...) int32
- *   region_units  tsr_region_unit_entries(...) uint32 (16 buckets)
+ *   region_units  tsr_region_unit_entries(...) uint32 (72 length buckets)
  *   region_ctl    tsr_region_ctl_entries() int32 (bucket counts, grab
  *                 counter; zeroed by tsr_render_fwd_regions).
  * tsr_render_bwd_regions streams each region's list past its pixels (one
- * systolic pipeline of 8 (region_height 4) or 16 lanes per region, units
- * drawn longest first) and merges the same Grad2D sums with atomics.
+ * systolic pipeline of 8 (region_height 4) or 16 lanes per stream; a warp's
+ * lane groups take streams of near-equal length, longest first) and merges
+ * the same Grad2D sums with atomics.
  * p_bound >= the pair count (a capacity is fine). */
 int tsr_render_fwd_regions(const float* rec, const int32_t* values, const int64_t* offsets,
                            int32_t width, int32_t height, const float* background_host,

@@ -44,8 +44,10 @@
 // tile (K3 writes a checkpoint record at every segment start and the region
 // list offsets at every segment boundary), so a heavy tile's work spreads
 // over many warps (the paper's redistribution across heavy tiles,
-// PAPER.md:121/145); K3 files the units under their longest list's bucket
-// and they are drawn longest first (the tail holds the short ones).
+// PAPER.md:121/145).  Scheduling: K3 files one stream per (tile, segment,
+// region) under its length's bucket; a warp's lane groups take kGPW streams
+// of near-equal length at a time, longest first, so the groups that run in
+// lockstep rarely idle and the tail holds the short streams.
 #include <climits>
 #include <cstdlib>
 
@@ -178,70 +180,56 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
   const float4 sent_b = make_float4(1.f, 1.f, 0.f, 0.f);
   const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
   const float keep = j != 0 ? 1.f : 0.f;  // lane 0 of a group starts each entry's sums
-  // units are drawn longest first: bucket kUnitBuckets - 1 down to 0 (K3
-  // filed each unit under its step count); lane b < kUnitBuckets holds the
-  // bucket's count, its units start at units[b * cap]
-  const int cap = (int)tsr_unit_bucket_cap(offsets[tiles_x * ((height + kTile - 1) / kTile)],
-                                           tiles_x * ((height + kTile - 1) / kTile));
-  const int bcount = lane < kUnitBuckets ? bucket_counts[lane] : 0;
-  // lane b: units in buckets b .. kUnitBuckets - 1 (incl) and above b (above)
-  int incl = bcount;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int v = __shfl_down_sync(0xffffffffu, incl, d);
-    if (lane + d < 32) incl += v;
+  // streams (tsr_common.cuh) are drawn longest first: kGPW at a time per
+  // warp, one per lane group, in descending bucket order; s_spre[b] = the
+  // streams in buckets above b (bucket kStreamBuckets - 1 first)
+  __shared__ int s_spre[kStreamBuckets + 1];
+  const int n_tiles_all = tiles_x * ((height + kTile - 1) / kTile);
+  const long long cap = tsr_stream_bucket_cap(offsets[n_tiles_all], n_tiles_all);
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int bk = kStreamBuckets - 1; bk >= 0; --bk) {
+      s_spre[bk] = acc;
+      acc += bucket_counts[bk];
+    }
+    s_spre[kStreamBuckets] = acc;  // all streams
   }
-  const int above = incl - bcount;
-  const int n_units = __shfl_sync(0xffffffffu, incl, 0);
+  __syncthreads();
+  const int n_streams = s_spre[kStreamBuckets];
 
   for (;;) {
     int u = 0;
     if (lane == 0) u = atomicAdd(counter, 1);
     u = __shfl_sync(0xffffffffu, u, 0);
-    if (u >= n_units) break;
-    // grab index u's bucket: the buckets in descending order
-    const unsigned hit = __ballot_sync(0xffffffffu, lane < kUnitBuckets && u >= above && u < incl);
-    const int b = __ffs(hit) - 1;
-    const int b_above = __shfl_sync(0xffffffffu, above, b);
-    const uint32_t code = units[(long long)b * cap + (u - b_above)];
-    const int tile = (int)(code >> 16), seg = (int)((code >> 1) & 0x7fffu), rp = (int)(code & 1u);
-    if (rp >= kUPS) continue;  // K3 queues two units per segment; this shape runs one
-    const long long start = offsets[tile];
-    const int n = (int)(offsets[tile + 1] - start);
-    // The segment's region lists are grouped by length (the longest kGPW in
-    // unit 0, the others in unit 1): a warp's groups run in lockstep, so the
-    // group's longest list sets its step count.  Both units of a segment
-    // read the same lengths and make the same choice.
-    const long long sb = kNR * ((start >> kSegShift) + tile);
-    int len[kNR], beg[kNR];
-#pragma unroll
-    for (int q = 0; q < kNR; ++q) {
-      beg[q] = seg > 0 ? rseg[sb + kNR * (seg - 1) + q] : 0;
-      len[q] = rseg[sb + kNR * seg + q] - beg[q];
-    }
-    int r = 0, r_other = 0;  // this group's region, and the other unit's region for this group
-#pragma unroll
-    for (int q = 0; q < kNR; ++q) {
-      int rank = 0;
-#pragma unroll
-      for (int o = 0; o < kNR; ++o) rank += (len[o] > len[q]) || (len[o] == len[q] && o < q);
-      if (rank == kGPW * rp + h) r = q;
-      if (kUPS > 1 && rank == kGPW * (1 - rp) + h) r_other = q;
-    }
-    int e0 = 0, L = 0;
-#pragma unroll
-    for (int q = 0; q < kNR; ++q)
-      if (q == r) {
-        e0 = beg[q];
-        L = len[q];
+    if (u * kGPW >= n_streams) break;
+    // this group's stream: index u kGPW + h in descending bucket order
+    const int si = u * kGPW + h;
+    int tile = 0, seg = 0, r = 0;
+    const bool has = si < n_streams;
+    if (has) {
+      // s_spre is non-increasing in b; si lies in the smallest bucket b with
+      // s_spre[b] <= si (si < s_spre[b - 1] = s_spre[b] + count[b])
+      int lo = 0, hi = kStreamBuckets - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s_spre[mid] <= si) hi = mid;
+        else lo = mid + 1;
       }
-    int Lmax = L;
-#pragma unroll
-    for (int m = kGL; m < 32; m <<= 1) Lmax = max(Lmax, __shfl_xor_sync(0xffffffffu, Lmax, m));
+      const uint32_t code = units[lo * cap + (si - s_spre[lo])];
+      tile = (int)(code >> 16);
+      seg = (int)((code >> 3) & 0x1fffu);
+      r = (int)(code & 7u);
+    }
+    const long long start = offsets[tile];
+    const int n = has ? (int)(offsets[tile + 1] - start) : 0;
+    const long long sb = kNR * ((start >> kSegShift) + tile);
+    const int e0 = has && seg > 0 ? rseg[sb + kNR * (seg - 1) + r] : 0;
+    int L = has ? rseg[sb + kNR * seg + r] - e0 : 0;
+    const bool counts_merges = has && seg == 0 && r == 0;  // the tile's merge count
     const int tyi = tile / tiles_x, txi = tile - tyi * tiles_x;
     const int X0 = txi * kTile + 8 * (r & 1) + (j & 3), Y0 = tyi * kTile + kRH * (r >> 1) + (j >> 2);
     const int p0 = seg << kSegShift;
-    if (Lmax == 0 && !(seg == 0 && rp == 0)) continue;  // nothing to stream (no merge count either)
+    if (!__any_sync(0xffffffffu, L > 0 || counts_merges)) continue;  // nothing to stream
 
     // ---- pixel state: pair q = (column c = q / kNRG, row pair g = q % kNRG):
     // pixels (X0 + 4c, Y0 + 2g kRS) and (X0 + 4c, Y0 + (2g + 1) kRS)
@@ -294,19 +282,29 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
       gb[q] = f2(v[0][4], v[1][4]);
       gd[q] = f2(v[0][5], v[1][5]);
     }
-    const bool nz = __any_sync(0xffffffffu, nzl);
     // merges follow the reference's count: every pair of a tile whose
-    // upstream is not all zero (backward.py:156-158, 214-222)
-    if (seg == 0 && rp == 0) {
-      bool other = false;
-      if (kUPS > 1)
-        other = quad_nz(grad_color, kDepth ? grad_depth : nullptr, grad_final_T, width, height,
-                        txi * kTile + 8 * (r_other & 1) + (j & 3),
-                        tyi * kTile + kRH * (r_other >> 1) + (j >> 2), kRS);
-      if (__any_sync(0xffffffffu, nzl || other) && lane == 0)
-        atomicAdd(merges, (unsigned long long)n);
+    // upstream is not all zero (backward.py:156-158, 214-222); the tile's
+    // (segment 0, region 0) stream checks all of its regions
+    const unsigned gmask = (kGL == 32 ? 0xffffffffu : ((1u << kGL) - 1u)) << (h * kGL);
+    if (__any_sync(0xffffffffu, counts_merges)) {
+      bool tnz = false;
+      if (counts_merges) {
+#pragma unroll 1
+        for (int q = 0; q < kNR; ++q)
+          tnz |= quad_nz(grad_color, kDepth ? grad_depth : nullptr, grad_final_T, width, height,
+                         txi * kTile + 8 * (q & 1) + (j & 3), tyi * kTile + kRH * (q >> 1) + (j >> 2),
+                         kRS);
+      }
+      const unsigned any_nz = __ballot_sync(0xffffffffu, tnz) & gmask;
+      if (counts_merges && j == 0 && any_nz) atomicAdd(merges, (unsigned long long)n);
     }
-    if (!nz || Lmax == 0) continue;  // exact zeros
+    // a group whose pixels have no upstream streams exact zeros: skip it
+    const bool gnz = (__ballot_sync(0xffffffffu, nzl) & gmask) != 0u;
+    if (!gnz) L = 0;
+    int Lmax = L;
+#pragma unroll
+    for (int m = kGL; m < 32; m <<= 1) Lmax = max(Lmax, __shfl_xor_sync(0xffffffffu, Lmax, m));
+    if (Lmax == 0) continue;  // exact zeros
 
     const uint32_t* lst = rlist + kNR * start + (long long)r * n + e0;
     const int32_t* vals = values + start;
@@ -560,9 +558,9 @@ extern "C" size_t tsr_region_list_entries(int32_t width, int32_t height, int64_t
 
 extern "C" size_t tsr_region_unit_entries(int32_t width, int32_t height, int64_t p_bound) {
   if (width <= 0 || height <= 0) return 0;
-  // kUnitBuckets buckets, each able to hold every unit of a P <= p_bound list
-  return (size_t)kUnitBuckets *
-         (size_t)tsr_unit_bucket_cap(p_bound > 0 ? p_bound : 0, tiles_of(width) * tiles_of(height));
+  // kStreamBuckets buckets, each able to hold every stream of a P <= p_bound list
+  return (size_t)kStreamBuckets *
+         (size_t)tsr_stream_bucket_cap(p_bound > 0 ? p_bound : 0, tiles_of(width) * tiles_of(height));
 }
 
 extern "C" size_t tsr_region_ctl_entries(void) { return kUnitCtl; }
@@ -609,11 +607,11 @@ extern "C" int tsr_render_bwd_regions(const float* rec, const int32_t* values,
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k, kRThreads, 0);
     if (ps < 1) ps = 1;
   }
-  // region_ctl = (bucket counts filed by K3, grab counter; zeroed by K3's launch)
+  // region_ctl = (stream bucket counts filed by K3, grab counter; zeroed by K3's launch)
   k<<<sms * ps, kRThreads, 0, s>>>((const float4*)rec, values, offsets, width, height, tx, color,
                                    depth, final_T, n_considered, ckpt, ckpt_base, region_list,
                                    region_seg, grad_color, grad_depth, grad_final_T, grad2d, merges,
-                                   region_units, region_ctl, region_ctl + kUnitBuckets);
+                                   region_units, region_ctl, region_ctl + kStreamBuckets);
   TSR_CHECK_LAUNCH();
   return TSR_OK;
 }

@@ -130,11 +130,10 @@ __device__ __forceinline__ void blend_pair(const float4 g, const float4 c, const
 // holds the number of entries with position < kSeg s for s = 1..ceil(n/kSeg)
 // (segbase_t = (start_t >> 10) + t: floor((O + n) / kSeg) - floor(O / kSeg)
 // + 1 >= ceil(n / kSeg), so the tiles' segment slots never overlap).
-// It also files the tile's work units for the region-culled K4: unit =
-// tile << 16 | segment << 1 | row pair, 2 ceil(n / kSeg) per tile, under
-// the bucket of the unit's step count once the tile's lists are complete
-// (tsr_unit_bucket; K4r draws them longest first); the control block
-// (bucket counts, grab counter) is zeroed before K3 by the launch.
+// It also files the tile's streams for the region-culled K4 (one per
+// (segment, region) with entries, tsr_common.cuh) under their length's
+// bucket once the tile's lists are complete; the control block (bucket
+// counts, grab counter) is zeroed before K3 by the launch.
 struct RegionArgs {
   uint32_t* list;
   int32_t* seg;
@@ -361,37 +360,23 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
       if (kCkpt == 4) rg.seg[kNR * (segbase + s_next - 1) + reg1] = r_count2;
     }
   if (kRegions) {
-    // the tile's K4r work units, filed longest first: unit (segment, row
-    // pair 0) runs the segment's kNR / 2 longest region lists, (segment, 1)
-    // the others (backward_regions.cu groups them the same way), so their
-    // step counts are the longest and the (kNR / 2 + 1)-th longest list
+    // the tile's K4r streams (tsr_common.cuh): one per (segment, region)
+    // with entries, plus (segment 0, region 0) always (it counts merges)
     __syncthreads();  // every warp's segment counts are written
     const int nseg = (n + kSeg - 1) >> kSegShift;
-    const int cap = (int)tsr_unit_bucket_cap(offsets[gridDim.x], gridDim.x);
-    for (int sg = tid; sg < nseg; sg += kFwdThreads) {
-      int len[kNR];
-#pragma unroll
-      for (int q = 0; q < kNR; ++q) {
-        const int cur = rg.seg[kNR * (segbase + sg) + q];
-        len[q] = cur - (sg > 0 ? rg.seg[kNR * (segbase + sg - 1) + q] : 0);
-      }
-      int top = 0, mid = 0;  // the longest and the (kNR / 2 + 1)-th longest
-#pragma unroll
-      for (int q = 0; q < kNR; ++q) {
-        int rank = 0;
-#pragma unroll
-        for (int o = 0; o < kNR; ++o) rank += (len[o] > len[q]) || (len[o] == len[q] && o < q);
-        if (rank == 0) top = len[q];
-        if (rank == kNR / 2) mid = len[q];
-      }
-#pragma unroll
-      for (int rp = 0; rp < 2; ++rp) {
-        const int b = tsr_unit_bucket(rp == 0 ? top : mid);
+    const long long cap = tsr_stream_bucket_cap(offsets[gridDim.x], gridDim.x);
+    for (int i = tid; i < nseg * kNR; i += kFwdThreads) {
+      const int sg = i / kNR, q = i - sg * kNR;
+      const int len = rg.seg[kNR * (segbase + sg) + q] -
+                      (sg > 0 ? rg.seg[kNR * (segbase + sg - 1) + q] : 0);
+      if (len > 0 || i == 0) {
+        const int b = tsr_stream_bucket(len);
         const int at = atomicAdd(rg.ctl + b, 1);
-        rg.units[(long long)b * cap + at] = ((uint32_t)tile << 16) | ((uint32_t)sg << 1) | (uint32_t)rp;
+        rg.units[b * cap + at] = ((uint32_t)tile << 16) | ((uint32_t)sg << 3) | (uint32_t)q;
       }
     }
   }
+
 
   // a pixel that never terminated considered the whole list (skipped
   // entries included); a terminated one stopped at its death position

@@ -24,20 +24,26 @@ constexpr int kGroup = 32;  // CHECKPOINT_INTERVAL (forward.py:28)
 // of 2 kGroup; K3 writes a checkpoint record at every segment start)
 constexpr int kSegShift = 10;
 constexpr int kSeg = 1 << kSegShift;
-// Region-culled K4 work units are queued longest first: K3 files each unit
-// (tile, segment, row pair) under its longest list's bucket (32 entries per
-// bucket, kUnitBuckets buckets, the last open-ended) once the tile's region
-// lists are complete; bucket b holds up to tsr_unit_bucket_cap(P, tiles)
-// units at units[b * cap ...], its count at ctl[b]; ctl[kUnitBuckets] is
-// the backward's grab counter.
-constexpr int kUnitBuckets = 16;
-constexpr int kUnitCtl = 32;  // ints in the control block (zeroed by K3's launch)
-__host__ __device__ inline long long tsr_unit_bucket_cap(long long pairs, int n_tiles) {
-  return 2 * (pairs / kSeg + n_tiles + 1);
+// Region-culled K4 work: one STREAM per (tile, segment, region) -- the
+// region's list entries in that 1024-position segment.  K3 files each
+// stream with entries (and every tile's (segment 0, region 0) stream, which
+// also counts the tile's merges) under its length's bucket once the tile's
+// lists are complete: width 4 below 256 entries (64 buckets), width 128
+// above (8 more, the last open-ended).  K4r's warps take kGPW streams at a
+// time in descending bucket order, one per lane group, so the groups that
+// run in lockstep have near-equal lengths and the longest run first.
+// Bucket b holds up to tsr_stream_bucket_cap(P, tiles) streams at
+// streams[b * cap ...], its count at ctl[b]; ctl[kStreamBuckets] is the
+// backward's grab counter.  Code: tile << 16 | segment << 3 | region.
+constexpr int kStreamBuckets = 72;
+constexpr int kUnitCtl = 128;  // ints in the control block (zeroed by K3's launch)
+__host__ __device__ inline long long tsr_stream_bucket_cap(long long pairs, int n_tiles) {
+  return 8 * (pairs / kSeg + n_tiles + 1);
 }
-__host__ __device__ inline int tsr_unit_bucket(int length) {  // the unit's longest list
-  const int b = length >> 5;
-  return b < kUnitBuckets - 1 ? b : kUnitBuckets - 1;
+__host__ __device__ inline int tsr_stream_bucket(int length) {
+  if (length < 256) return length >> 2;
+  const int b = 64 + ((length - 256) >> 7);
+  return b < kStreamBuckets - 1 ? b : kStreamBuckets - 1;
 }
 constexpr float kAlphaCap = 0.99f;                 // forward.py:25
 constexpr float kMinAlpha = 1.0f / 255.0f;         // forward.py:26
