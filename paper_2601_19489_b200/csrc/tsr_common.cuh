@@ -22,7 +22,10 @@ constexpr int kTilePixels = kTile * kTile;
 constexpr int kGroup = 32;  // CHECKPOINT_INTERVAL (forward.py:28)
 // region-culled backward segments: list positions per work unit (a multiple
 // of 2 kGroup; K3 writes a checkpoint record at every segment start)
-constexpr int kSegShift = 10;
+#ifndef TSR_SEG_SHIFT
+#define TSR_SEG_SHIFT 10
+#endif
+constexpr int kSegShift = TSR_SEG_SHIFT;
 constexpr int kSeg = 1 << kSegShift;
 // Region-culled K4 work: one STREAM per (tile, segment, region) -- the
 // region's list entries in that 1024-position segment.  K3 files each

@@ -1,7 +1,8 @@
-"""Lockstep efficiency of the region-culled K4's units at C2 after a few
-training steps: per unit (a tile's segment, half of its regions, sorted by
-list length) the groups of a warp run max(L) + kGL - 1 steps; efficiency =
-sum(L) / (groups x steps)."""
+"""Lockstep efficiency of the region-culled K4's former (tile, segment, half
+of the regions) units at C2 after a few training steps: the groups of a
+warp run max(L) + kGL - 1 steps; efficiency = sum(L) / (groups x steps).
+(K4r now takes length-sorted (tile, segment, region) streams per group:
+DESIGN.md §8.)"""
 import sys
 from pathlib import Path
 
