@@ -21,33 +21,30 @@
 // bit for bit.  Every other entry contributes exact zeros to every pixel of
 // the region, so skipping it changes nothing.
 //
-// Layout (shown for 8x8 regions, 16-lane groups; the default 8x4 regions
-// run four 8-lane groups per warp over the tile's eight regions, lane j
-// owning (x0, y0), (x0, y0 + 2), (x0 + 4, y0), (x0 + 4, y0 + 2) of its 8x4
-// region, the same arithmetic).  A warp is one work unit (tile, pair p, segment): its two 16-lane
-// halves run two of the tile's four 8x8 regions (bx, by) -- the segment's two
-// longest region lists for p = 0, the other two for p = 1, so the lockstep
-// halves have similar step counts; lane j of a half owns
-// the four pixels (x0, y0), (x0, y1), (x0 + 4, y0), (x0 + 4, y1) with
-// x0 = 8 bx + (j & 3), y0 = 8 by + (j >> 2), y1 = y0 + 4 -- two vertical pairs
-// sharing dy, so the alpha and chain arithmetic is packed FP32x2.  Each half
-// is a 16-stage systolic pipeline: at step t lane j processes the region
-// list entry e = t - j for its four pixels; the ten per-splat partial sums
-// flow lane to lane (one shuffle each), so lane 15 holds entry t - 15's
-// complete region sums.  The pixel state (T, R) never leaves its lane.
-// Splat records are staged per group in a shared-memory ring of 4 kGL entries
-// (cp.async straight from rec, one block of 16 entries a round ahead; the
-// list position and row are loaded two rounds ahead); finished sums go to a
-// 32-entry buffer and are merged 16 at a time, one lane per entry.
+// Layout.  A warp's lanes form kGPW groups of kGL lanes; each group runs one
+// STREAM -- the entries of one region's list inside one 1024-position
+// segment of its tile -- as a kGL-stage systolic pipeline: at step t lane j
+// processes stream entry e = t - j for its four pixels; the ten per-splat
+// partial sums flow lane to lane (one shuffle each), so lane kGL - 1 holds
+// entry t - kGL + 1's complete region sums.  The pixel state (T, R) never
+// leaves its lane.  Default 8x4 regions: 8-lane groups, four per warp, lane
+// j of a group owning (x0, y0), (x0, y0 + 2), (x0 + 4, y0), (x0 + 4, y0 + 2)
+// with x0 = 8 bx + (j & 3), y0 = 4 ry + (j >> 2); 8x8 regions: 16-lane
+// groups, rows y0 and y0 + 4.  Two vertical pairs share dy, so the alpha and
+// chain arithmetic is packed FP32x2.  Splat records are staged per group in
+// a shared-memory ring of 4 kGL entries (cp.async straight from rec, one
+// block of kGL entries a round ahead; the list position and row two and
+// three rounds ahead); finished sums go to a kGL-entry buffer and are merged
+// kGL at a time, one lane per entry.
 //
-// Segments.  A unit covers the list positions [1024 s, 1024 (s + 1)) of its
-// tile (K3 writes a checkpoint record at every segment start and the region
-// list offsets at every segment boundary), so a heavy tile's work spreads
-// over many warps (the paper's redistribution across heavy tiles,
-// PAPER.md:121/145).  Scheduling: K3 files one stream per (tile, segment,
-// region) under its length's bucket; a warp's lane groups take kGPW streams
-// of near-equal length at a time, longest first, so the groups that run in
-// lockstep rarely idle and the tail holds the short streams.
+// Segments and scheduling.  K3 writes a checkpoint record at every segment
+// start and the region list offsets at every segment boundary, so a heavy
+// tile's work spreads over many streams and warps (the paper's
+// redistribution across heavy tiles).  K3 files each
+// stream under its length's bucket; a warp's groups take kGPW streams of
+// near-equal length at a time, longest first, so the groups that run in
+// lockstep rarely idle and the tail holds the short streams.  The tile's
+// (segment 0, region 0) stream also counts the tile's merges.
 #include <climits>
 #include <cstdlib>
 
