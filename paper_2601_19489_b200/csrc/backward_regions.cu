@@ -24,13 +24,14 @@
 // Layout.  A warp's lanes form kGPW groups of kGL lanes; each group runs one
 // STREAM -- the entries of one region's list inside one 1024-position
 // segment of its tile -- as a kGL-stage systolic pipeline: at step t lane j
-// processes stream entry e = t - j for its four pixels; the ten per-splat
+// processes stream entry e = t - j for its pixels; the ten per-splat
 // partial sums flow lane to lane (one shuffle each), so lane kGL - 1 holds
 // entry t - kGL + 1's complete region sums.  The pixel state (T, R) never
-// leaves its lane.  Default 8x4 regions: 8-lane groups, four per warp, lane
-// j of a group owning (x0, y0), (x0, y0 + 2), (x0 + 4, y0), (x0 + 4, y0 + 2)
-// with x0 = 8 bx + (j & 3), y0 = 4 ry + (j >> 2); 8x8 regions: 16-lane
-// groups, rows y0 and y0 + 4.  Two vertical pairs share dy, so the alpha and
+// leaves its lane.  Default 8x8 regions: 8-lane groups of 8 pixels per
+// lane, four per warp, lane j owning columns x0 = 8 bx + (j & 3), x0 + 4 and
+// rows y0 + 2k (k < 4), y0 = 8 by + (j >> 2); 16-lane groups of 4 pixels
+// (TSR_K4R_PX=4) and 8x4 regions (TSR_K4R_REGION=4) follow the same pattern
+// (rows kGL / 4 apart).  Vertical pixel pairs share dy, so the alpha and
 // chain arithmetic is packed FP32x2.  Splat records are staged per group in
 // a shared-memory ring of 4 kGL entries (cp.async straight from rec, one
 // block of kGL entries a round ahead; the list position and row two and
@@ -98,15 +99,17 @@ __device__ __forceinline__ float participate(int p, int nc, float alpha) {
   return a;
 }
 
-// upstream of four pixels (x0 / x1, y0 / y1) is not all zero
-__device__ __forceinline__ bool quad_nz(const float* __restrict__ grad_color,
+// upstream of a lane's kPX pixels (columns X0, X0 + 4; rows Y0 + k dy) is
+// not all zero
+template <int kPX>
+__device__ __forceinline__ bool lane_nz(const float* __restrict__ grad_color,
                                         const float* __restrict__ grad_depth,
                                         const float* __restrict__ grad_final_T, int width,
                                         int height, int X0, int Y0, int dy) {
   bool nz = false;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int x = X0 + (q >> 1) * 4, y = Y0 + (q & 1) * dy;
+  for (int q = 0; q < kPX; ++q) {
+    const int x = X0 + (q & 1) * 4, y = Y0 + (q >> 1) * dy;
     if (x < width && y < height) {
       const long long pix = (long long)y * width + x;
       nz |= grad_color[3 * pix] != 0.f || grad_color[3 * pix + 1] != 0.f ||
@@ -121,8 +124,9 @@ __device__ __forceinline__ bool quad_nz(const float* __restrict__ grad_color,
 // rows; rows of a lane are kGL/4 apart): kGL x kPX = the region's pixels.
 //   (16, 4): 8x8 regions, 4 per tile, 2 per warp
 //   ( 8, 4): 8x4 regions, 8 per tile, 4 per warp
-//   ( 8, 8): 8x8 regions, 4 per tile, all 4 in one warp (half the fill and
-//            half the per-step shuffles / loads per pixel)
+//   ( 8, 8): 8x8 regions, 4 per tile, 4 per warp (half the fill and half
+//            the per-step shuffles / loads per pixel)
+//   ( 4, 8): 8x4 regions, 8 per tile, 8 per warp
 template <bool kDepth, int kGL, int kPX>
 __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_kernel(
     const float4* __restrict__ rec, const int32_t* __restrict__ values,
@@ -288,7 +292,7 @@ __global__ void __launch_bounds__(kRThreads, TSR_K4R_CTAS) render_bwd_regions_ke
       if (counts_merges) {
 #pragma unroll 1
         for (int q = 0; q < kNR; ++q)
-          tnz |= quad_nz(grad_color, kDepth ? grad_depth : nullptr, grad_final_T, width, height,
+          tnz |= lane_nz<kPX>(grad_color, kDepth ? grad_depth : nullptr, grad_final_T, width, height,
                          txi * kTile + 8 * (q & 1) + (j & 3), tyi * kTile + kRH * (q >> 1) + (j >> 2),
                          kRS);
       }
@@ -586,16 +590,17 @@ extern "C" int tsr_render_bwd_regions(const float* rec, const int32_t* values,
   if (n_tiles >= (1 << 16)) return TSR_E_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
   // 8x8 regions: 16 lanes x 4 pixels (TSR_K4R_PX=4) or 8 lanes x 8 pixels
-  // (TSR_K4R_PX=8); 8x4 regions: 8 lanes x 4 pixels
-  static const int px = getenv("TSR_K4R_PX") ? atoi(getenv("TSR_K4R_PX")) : 4;
-  const int shape = region_height == 4 ? 2 : (px == 8 ? 1 : 0);
+  // (TSR_K4R_PX=8); 8x4 regions: 8 lanes x 4 pixels or 4 lanes x 8 pixels
+  static const int px = getenv("TSR_K4R_PX") ? atoi(getenv("TSR_K4R_PX")) : 8;
+  const int shape = region_height == 4 ? (px == 8 ? 3 : 2) : (px == 8 ? 1 : 0);
   using KFn = decltype(&render_bwd_regions_kernel<false, 16, 4>);
-  KFn table[3][2] = {
+  KFn table[4][2] = {
       {render_bwd_regions_kernel<false, 16, 4>, render_bwd_regions_kernel<true, 16, 4>},
       {render_bwd_regions_kernel<false, 8, 8>, render_bwd_regions_kernel<true, 8, 8>},
-      {render_bwd_regions_kernel<false, 8, 4>, render_bwd_regions_kernel<true, 8, 4>}};
+      {render_bwd_regions_kernel<false, 8, 4>, render_bwd_regions_kernel<true, 8, 4>},
+      {render_bwd_regions_kernel<false, 4, 8>, render_bwd_regions_kernel<true, 4, 8>}};
   KFn k = table[shape][grad_depth ? 1 : 0];
-  static int per_sm[6] = {0, 0, 0, 0, 0, 0}, sms = 0;
+  static int per_sm[8] = {0, 0, 0, 0, 0, 0, 0, 0}, sms = 0;
   int& ps = per_sm[2 * shape + (grad_depth ? 1 : 0)];
   if (ps == 0) {
     int dev = 0;

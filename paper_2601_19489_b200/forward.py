@@ -157,8 +157,9 @@ def render_raw(rec, values, offsets, ckpt_base, width: int, height: int, backgro
         _lib.ptr(tile_order), _lib.stream_handle()), "tsr_render_fwd_ordered")
 
 
-# 8x4 regions by default (8 per tile, 8-lane K4r pipelines); 8x8 with TSR_K4R_REGION=8
-REGION_HEIGHT = int(os.environ.get("TSR_K4R_REGION", 4))
+# 8x8 regions by default (4 per tile; K4r: 8-lane pipelines of 8 pixels per
+# lane, TSR_K4R_PX=4: 16 lanes of 4); 8x4 with TSR_K4R_REGION=4
+REGION_HEIGHT = int(os.environ.get("TSR_K4R_REGION", 8))
 
 
 class RegionLists:
