@@ -43,6 +43,9 @@
 
 namespace tsr {
 
+#ifndef TSR_K2_CTAS
+#define TSR_K2_CTAS 3  // CTAs per SM (co-resident: cooperative launch)
+#endif
 constexpr int kSB = 256;                 // threads per CTA
 constexpr int kBins = 256;               // 8-bit digits
 constexpr int kItems = 8;                // items per thread per sub-tile
@@ -634,7 +637,7 @@ __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, lon
 }
 
 // ---- the persistent index kernel
-__global__ void __launch_bounds__(kSB, 3) build_index_kernel(IndexArgs a) {
+__global__ void __launch_bounds__(kSB, TSR_K2_CTAS) build_index_kernel(IndexArgs a) {
   __shared__ SortSmem sm;
   extern __shared__ __align__(16) unsigned char dyn[];
   const int G = gridDim.x, bid = blockIdx.x, tid = threadIdx.x;
@@ -894,7 +897,7 @@ static int build_index_impl(const float* rec, const uint32_t* depth_bits, const 
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, build_index_kernel, kSB,
                                                     kDynSmem) != cudaSuccess)
     return TSR_E_CUDA;
-  int grid = sms * (per_sm < 3 ? per_sm : 3);
+  int grid = sms * (per_sm < TSR_K2_CTAS ? per_sm : TSR_K2_CTAS);
   // small problems: fewer CTAs (each grid barrier costs ~ one arrival per
   // CTA, and a slice of a few hundred items cannot use a whole CTA)
   const long long work = (p_cap > m_cap ? p_cap : m_cap) / 4096 + 8;
