@@ -59,6 +59,9 @@ namespace {
 constexpr int kRWarps = 4;
 // 8 pixels per lane: 3 CTAs/SM (167 registers, no spill) measured faster
 // than 4 (128 registers with a spill): 345 vs 353 us
+#ifndef TSR_K4R_SETUP_FLAT
+#define TSR_K4R_SETUP_FLAT 1
+#endif
 #ifndef TSR_K4R_CTAS_PX8
 #define TSR_K4R_CTAS_PX8 3
 #endif
@@ -246,6 +249,81 @@ __global__ void __launch_bounds__(kRThreads, kPX == 8 ? TSR_K4R_CTAS_PX8 : TSR_K
     const float* ck = seg > 0 ? ckpt + (ckpt_base[tile] + ((long long)seg << (kSegShift - 5)) - 1) *
                                            (5 * kTilePixels)
                               : nullptr;
+#if TSR_K4R_SETUP_FLAT
+    // every load of the lane's pixels first (one round trip instead of a
+    // load -> test -> load chain per pixel); out-of-frame pixels read pixel 0
+    // and are masked below -- the arithmetic of the active ones is unchanged
+    float l_gr[kPX], l_gg[kPX], l_gb[kPX], l_gd[kPX], l_gt[kPX], l_cr[kPX], l_cg[kPX], l_cb[kPX],
+        l_ft[kPX], l_dp[kPX], l_kt[kPX], l_kr[kPX], l_kg[kPX], l_kb[kPX], l_kd[kPX];
+    int l_nc[kPX];
+    bool l_in[kPX];
+#pragma unroll
+    for (int pp = 0; pp < kPX; ++pp) {
+      const int q = pp >> 1, e = pp & 1;
+      const int x = X0 + 4 * (q / kNRG), y = Y0 + (2 * (q % kNRG) + e) * kRS;
+      l_in[pp] = x < width && y < height;
+      const long long pix = l_in[pp] ? (long long)y * width + x : 0;
+      l_gr[pp] = grad_color[3 * pix];
+      l_gg[pp] = grad_color[3 * pix + 1];
+      l_gb[pp] = grad_color[3 * pix + 2];
+      l_gd[pp] = (kDepth && grad_depth) ? grad_depth[pix] : 0.f;
+      l_gt[pp] = grad_final_T ? grad_final_T[pix] : 0.f;
+      l_nc[pp] = n_considered[pix];
+      l_cr[pp] = color[3 * pix];
+      l_cg[pp] = color[3 * pix + 1];
+      l_cb[pp] = color[3 * pix + 2];
+      l_ft[pp] = final_T[pix];
+      l_dp[pp] = kDepth ? depth[pix] : 0.f;
+      l_kt[pp] = l_kr[pp] = l_kg[pp] = l_kb[pp] = l_kd[pp] = 0.f;
+      if (ck) {
+        const int lp = l_in[pp] ? (y - tyi * kTile) * kTile + (x - txi * kTile) : 0;
+        l_kt[pp] = ck[lp];
+        l_kr[pp] = ck[kTilePixels + lp];
+        l_kg[pp] = ck[2 * kTilePixels + lp];
+        l_kb[pp] = ck[3 * kTilePixels + lp];
+        if (kDepth) l_kd[pp] = ck[4 * kTilePixels + lp];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kNQ; ++q) {
+      float v[2][6];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int pp = 2 * q + e;
+        float t0 = 0.f, r0 = 0.f, g_r = 0.f, g_g = 0.f, g_b = 0.f, g_d = 0.f;
+        int ncv = 0;
+        if (l_in[pp]) {
+          g_r = l_gr[pp];
+          g_g = l_gg[pp];
+          g_b = l_gb[pp];
+          g_d = l_gd[pp];
+          const float gt = l_gt[pp];
+          nzl |= (g_r != 0.f) || (g_g != 0.f) || (g_b != 0.f) || (g_d != 0.f) || (gt != 0.f);
+          ncv = l_nc[pp];
+          if (ncv > p0) {  // active in this segment
+            float k = g_r * l_cr[pp] + g_g * l_cg[pp] + g_b * l_cb[pp] + gt * l_ft[pp];
+            if (kDepth) k += g_d * l_dp[pp];
+            float T0 = 1.f, K0 = 0.f;
+            if (ck) {
+              T0 = l_kt[pp];
+              K0 = g_r * l_kr[pp] + g_g * l_kg[pp] + g_b * l_kb[pp];
+              if (kDepth) K0 += g_d * l_kd[pp];
+            }
+            t0 = T0;
+            r0 = k - K0;
+          }
+        }
+        v[e][0] = t0; v[e][1] = r0; v[e][2] = g_r; v[e][3] = g_g; v[e][4] = g_b; v[e][5] = g_d;
+        nc[q][e] = ncv;
+      }
+      T[q] = f2(v[0][0], v[1][0]);
+      R[q] = f2(v[0][1], v[1][1]);
+      gr[q] = f2(v[0][2], v[1][2]);
+      gg[q] = f2(v[0][3], v[1][3]);
+      gb[q] = f2(v[0][4], v[1][4]);
+      gd[q] = f2(v[0][5], v[1][5]);
+    }
+#else
 #pragma unroll
     for (int q = 0; q < kNQ; ++q) {
       float v[2][6];
@@ -289,6 +367,7 @@ __global__ void __launch_bounds__(kRThreads, kPX == 8 ? TSR_K4R_CTAS_PX8 : TSR_K
       gb[q] = f2(v[0][4], v[1][4]);
       gd[q] = f2(v[0][5], v[1][5]);
     }
+#endif
     // merges follow the reference's count: every pair of a tile whose
     // upstream is not all zero (backward.py:156-158, 214-222); the tile's
     // (segment 0, region 0) stream checks all of its regions
