@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(kRThreads, kPX == 8 ? TSR_K4R_CTAS_PX8 : TSR_K
   __shared__ int s_spre[kStreamBuckets + 1];
   const int n_tiles_all = tiles_x * ((height + kTile - 1) / kTile);
   const long long cap = tsr_stream_bucket_cap(offsets[n_tiles_all], n_tiles_all);
+  const uint4* __restrict__ recs = reinterpret_cast<const uint4*>(units + kStreamBuckets * cap);
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int bk = kStreamBuckets - 1; bk >= 0; --bk) {
@@ -214,7 +215,8 @@ __global__ void __launch_bounds__(kRThreads, kPX == 8 ? TSR_K4R_CTAS_PX8 : TSR_K
     if (u * kGPW >= n_streams) break;
     // this group's stream: index u kGPW + h in descending bucket order
     const int si = u * kGPW + h;
-    int tile = 0, seg = 0, r = 0;
+    int tile = 0, seg = 0, r = 0, s_n = 0, s_e0 = 0, s_L = 0;
+    uint32_t s_start = 0;
     const bool has = si < n_streams;
     if (has) {
       // s_spre is non-increasing in b; si lies in the smallest bucket b with
@@ -225,16 +227,20 @@ __global__ void __launch_bounds__(kRThreads, kPX == 8 ? TSR_K4R_CTAS_PX8 : TSR_K
         if (s_spre[mid] <= si) hi = mid;
         else lo = mid + 1;
       }
-      const uint32_t code = units[lo * cap + (si - s_spre[lo])];
-      tile = (int)(code >> 16);
-      seg = (int)((code >> 3) & 0x1fffu);
-      r = (int)(code & 7u);
+      const uint32_t id = units[lo * cap + (si - s_spre[lo])];
+      const uint4 ra0 = recs[2 * id], ra1 = recs[2 * id + 1];
+      tile = (int)(ra0.x >> 16);
+      seg = (int)((ra0.x >> 3) & 0x1fffu);
+      r = (int)(ra0.x & 7u);
+      s_start = ra0.y;
+      s_n = (int)ra0.z;
+      s_e0 = (int)ra0.w;
+      s_L = (int)ra1.x;
     }
-    const long long start = offsets[tile];
-    const int n = has ? (int)(offsets[tile + 1] - start) : 0;
-    const long long sb = kNR * ((start >> kSegShift) + tile);
-    const int e0 = has && seg > 0 ? rseg[sb + kNR * (seg - 1) + r] : 0;
-    int L = has ? rseg[sb + kNR * seg + r] - e0 : 0;
+    const long long start = s_start;
+    const int n = s_n;
+    const int e0 = s_e0;
+    int L = s_L;
     const bool counts_merges = has && seg == 0 && r == 0;  // the tile's merge count
     const int tyi = tile / tiles_x, txi = tile - tyi * tiles_x;
     const int X0 = txi * kTile + 8 * (r & 1) + (j & 3), Y0 = tyi * kTile + kRH * (r >> 1) + (j >> 2);
@@ -246,7 +252,8 @@ __global__ void __launch_bounds__(kRThreads, kPX == 8 ? TSR_K4R_CTAS_PX8 : TSR_K
     float2 T[kNQ], R[kNQ], gr[kNQ], gg[kNQ], gb[kNQ], gd[kNQ];
     int nc[kNQ][2];
     bool nzl = false;
-    const float* ck = seg > 0 ? ckpt + (ckpt_base[tile] + ((long long)seg << (kSegShift - 5)) - 1) *
+    // ckpt_base[tile] == offsets[tile] >> 5 (the index's record base)
+    const float* ck = seg > 0 ? ckpt + ((start >> 5) + ((long long)seg << (kSegShift - 5)) - 1) *
                                            (5 * kTilePixels)
                               : nullptr;
 #if TSR_K4R_SETUP_FLAT
@@ -644,8 +651,9 @@ extern "C" size_t tsr_region_list_entries(int32_t width, int32_t height, int64_t
 
 extern "C" size_t tsr_region_unit_entries(int32_t width, int32_t height, int64_t p_bound) {
   if (width <= 0 || height <= 0) return 0;
-  // kStreamBuckets buckets, each able to hold every stream of a P <= p_bound list
-  return (size_t)kStreamBuckets *
+  // kStreamBuckets buckets, each able to hold every stream id of a P <= p_bound
+  // list, then the stream records (8 uint32 each)
+  return (size_t)(kStreamBuckets + 8) *
          (size_t)tsr_stream_bucket_cap(p_bound > 0 ? p_bound : 0, tiles_of(width) * tiles_of(height));
 }
 

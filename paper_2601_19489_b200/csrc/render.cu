@@ -365,14 +365,21 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
     __syncthreads();  // every warp's segment counts are written
     const int nseg = (n + kSeg - 1) >> kSegShift;
     const long long cap = tsr_stream_bucket_cap(offsets[gridDim.x], gridDim.x);
+    // stream records after the buckets (tsr_common.cuh): the buckets hold
+    // record ids, so the backward's setup needs no offsets / segment reads
+    uint4* recs = reinterpret_cast<uint4*>(rg.units + (long long)kStreamBuckets * cap);
     for (int i = tid; i < nseg * kNR; i += kFwdThreads) {
       const int sg = i / kNR, q = i - sg * kNR;
-      const int len = rg.seg[kNR * (segbase + sg) + q] -
-                      (sg > 0 ? rg.seg[kNR * (segbase + sg - 1) + q] : 0);
+      const int e0 = sg > 0 ? rg.seg[kNR * (segbase + sg - 1) + q] : 0;
+      const int len = rg.seg[kNR * (segbase + sg) + q] - e0;
       if (len > 0 || i == 0) {
+        const int id = atomicAdd(rg.ctl + kStreamBuckets + 1, 1);
+        recs[2 * id] = make_uint4(((uint32_t)tile << 16) | ((uint32_t)sg << 3) | (uint32_t)q,
+                                  (uint32_t)start, (uint32_t)n, (uint32_t)e0);
+        recs[2 * id + 1] = make_uint4((uint32_t)len, 0u, 0u, 0u);
         const int b = tsr_stream_bucket(len);
         const int at = atomicAdd(rg.ctl + b, 1);
-        rg.units[b * cap + at] = ((uint32_t)tile << 16) | ((uint32_t)sg << 3) | (uint32_t)q;
+        rg.units[b * cap + at] = (uint32_t)id;
       }
     }
   }

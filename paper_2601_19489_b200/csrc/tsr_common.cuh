@@ -35,9 +35,12 @@ constexpr int kSeg = 1 << kSegShift;
 // above (8 more, the last open-ended).  K4r's warps take kGPW streams at a
 // time in descending bucket order, one per lane group, so the groups that
 // run in lockstep have near-equal lengths and the longest run first.
-// Bucket b holds up to tsr_stream_bucket_cap(P, tiles) streams at
-// streams[b * cap ...], its count at ctl[b]; ctl[kStreamBuckets] is the
-// backward's grab counter.  Code: tile << 16 | segment << 3 | region.
+// Bucket b holds up to tsr_stream_bucket_cap(P, tiles) stream ids at
+// units[b * cap ...], its count at ctl[b]; ctl[kStreamBuckets] is the
+// backward's grab counter, ctl[kStreamBuckets + 1] the id counter.  Stream
+// record id (two uint4 after the buckets, units + kStreamBuckets * cap):
+// {tile << 16 | segment << 3 | region, tile list start, tile list length,
+// first region-list entry of the segment}, {entries, -, -, -}.
 constexpr int kStreamBuckets = 72;
 constexpr int kUnitCtl = 128;  // ints in the control block (zeroed by K3's launch)
 __host__ __device__ inline long long tsr_stream_bucket_cap(long long pairs, int n_tiles) {
