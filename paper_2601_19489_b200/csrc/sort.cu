@@ -43,6 +43,9 @@
 
 namespace tsr {
 
+#ifndef TSR_K2_RANGE_ITEMS
+#define TSR_K2_RANGE_ITEMS 8  // boundary tests per thread in flight in the ranges phase
+#endif
 #ifndef TSR_K2_CTAS
 #define TSR_K2_CTAS 3  // CTAs per SM (co-resident: cooperative launch)
 #endif
@@ -756,7 +759,7 @@ __global__ void __launch_bounds__(kSB, TSR_K2_CTAS) build_index_kernel(IndexArgs
   // ---- 4. per-tile ranges (binning.py:156-157) + checkpoint bases
   // 8 boundary tests per thread in flight per round (independent loads)
   const int* khi = reinterpret_cast<const int*>(a.keys) + 1;  // tile = high word
-  constexpr int kR = 8;
+  constexpr int kR = TSR_K2_RANGE_ITEMS;
   for (long long i0 = (long long)bid * kSB * kR + tid; i0 <= np; i0 += (long long)G * kSB * kR) {
     int cur[kR], prev[kR];
 #pragma unroll
