@@ -83,6 +83,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
@@ -174,8 +178,7 @@ __global__ void __launch_bounds__(kRThreads, kPX == 8 ? TSR_K4R_CTAS_PX8 : TSR_K
   // rounds ahead, read by the staging and the merge); block b's slots are
   // reused by block b + 8, whose position is fetched at round b + 5, after
   // block b's last step (round b + 1) and merge (end of round b + 1)
-  __shared__ int s_pos[kRWarps][kGPW][kPR];
-  __shared__ int s_row[kRWarps][kGPW][kPR];
+  __shared__ int2 s_pr[kRWarps][kGPW][kPR];  // (list position, batch row)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, h = lane / kGL, j = lane % kGL;
   float4* ra = s_ring[warp][h].a;
   float4* rb = s_ring[warp][h].b;
@@ -183,8 +186,7 @@ __global__ void __launch_bounds__(kRThreads, kPX == 8 ? TSR_K4R_CTAS_PX8 : TSR_K
   float4(*oa)[kGPW] = s_oa[warp];
   float4(*ob)[kGPW] = s_ob[warp];
   float2(*oc)[kGPW] = s_oc[warp];
-  int* spos = s_pos[warp][h];
-  int* srow = s_row[warp][h];
+  int2* spr = s_pr[warp][h];
   // sentinel splat: alpha = gauss = 0 at every pixel, finite products
   const float4 sent_a = make_float4(-65536.f, -65536.f, 1.f, 0.f);
   const float4 sent_b = make_float4(1.f, 1.f, 0.f, 0.f);
@@ -399,25 +401,19 @@ __global__ void __launch_bounds__(kRThreads, kPX == 8 ? TSR_K4R_CTAS_PX8 : TSR_K
     for (int m = kGL; m < 32; m <<= 1) Lmax = max(Lmax, __shfl_xor_sync(0xffffffffu, Lmax, m));
     if (Lmax == 0) continue;  // exact zeros
 
-    const uint32_t* lst = rlist + kNR * start + (long long)r * n + e0;
-    const int32_t* vals = values + start;
+    // the region list holds (position, row) pairs (render.cu)
+    const uint2* lst = reinterpret_cast<const uint2*>(rlist) + kNR * start + (long long)r * n + e0;
     // Every list access is asynchronous (cp.async into shared memory, waited
     // once per round), three stages per entry e of this lane's group:
-    //   position  lst[e]          -> spos  (3 rounds ahead)
-    //   row       values[pos]     -> srow  (2 rounds ahead)
+    //   (position, row) lst[e]    -> spr   (3 rounds ahead; K3 wrote the rows)
     //   record    rec[row] x 3    -> ring  (1 round ahead)
     auto fetch_pos = [&](int e) {
-      if (e < L) cp_async4(&spos[e & (kPR - 1)], lst + e);
-      else spos[e & (kPR - 1)] = INT_MAX;
-    };
-    auto fetch_row = [&](int e) {
-      const int pos = spos[e & (kPR - 1)];
-      if (pos != INT_MAX) cp_async4(&srow[e & (kPR - 1)], vals + pos);
-      else srow[e & (kPR - 1)] = -1;
+      if (e < L) cp_async8(&spr[e & (kPR - 1)], lst + e);
+      else spr[e & (kPR - 1)] = make_int2(INT_MAX, -1);
     };
     auto stage = [&](int e) {
       const int slot = e & (kRing - 1);
-      const int row = srow[e & (kPR - 1)];
+      const int row = spr[e & (kPR - 1)].y;
       if (row >= 0) {
         cp_async16(&ra[slot], rec + 3 * (long long)row);
         cp_async16(&rb[slot], rec + 3 * (long long)row + 1);
@@ -433,15 +429,10 @@ __global__ void __launch_bounds__(kRThreads, kPX == 8 ? TSR_K4R_CTAS_PX8 : TSR_K
     ra[kRing - kGL + j] = sent_a;
     rb[kRing - kGL + j] = sent_b;
     rc[kRing - kGL + j] = zero4;
-    spos[kPR - kGL + j] = INT_MAX;
+    spr[kPR - kGL + j] = make_int2(INT_MAX, -1);
     fetch_pos(j);
     fetch_pos(kGL + j);
     fetch_pos(2 * kGL + j);
-    cp_async_commit();
-    cp_async_wait_all();
-    __syncwarp();
-    fetch_row(j);
-    fetch_row(kGL + j);
     cp_async_commit();
     cp_async_wait_all();
     __syncwarp();
@@ -586,7 +577,7 @@ __global__ void __launch_bounds__(kRThreads, kPX == 8 ? TSR_K4R_CTAS_PX8 : TSR_K
       const float4 sbr = rb[slot];
       const float cc = __fmul_rn(sbr.x, kQScale);
       const float ca = __fmul_rn(sa.z, kQScale), hb = __fmul_rn(sa.w, kQScale);  // (2b') / 2
-      const int row = srow[e & (kPR - 1)];
+      const int row = spr[e & (kPR - 1)].y;
       // sum gq u = a' sum gq dx + b' sum gq dy, likewise v (the conic's rows)
       const float uu = fmaf(ca, A.x, hb * A.y), vv = fmaf(hb, A.x, cc * A.y);
       // five 8-byte vector atomics per row (rows are 40 B: 8-B aligned)
@@ -602,7 +593,7 @@ __global__ void __launch_bounds__(kRThreads, kPX == 8 ? TSR_K4R_CTAS_PX8 : TSR_K
       const int slot = (t - j) & (kRing - 1);
       A = ra[slot];
       B = rb[slot];
-      pos = spos[(t - j) & (kPR - 1)];
+      pos = spr[(t - j) & (kPR - 1)].x;
     };
     const int steps = Lmax + kGL - 1;  // entry Lmax - 1 leaves the last lane at step Lmax + kGL - 2
     const int rounds = (steps + kGL - 1) / kGL;
@@ -612,10 +603,9 @@ __global__ void __launch_bounds__(kRThreads, kPX == 8 ? TSR_K4R_CTAS_PX8 : TSR_K
     int q0, q1;
     load(A0, B0, q0, 0);
     for (int k = 0; k < rounds; ++k) {
-      // block k's records, k + 1's rows, k + 2's positions landed (waited
-      // at the previous round's second-to-last step)
+      // block k's records and k + 1, k + 2's (position, row) pairs landed
+      // (waited at the previous round's second-to-last step)
       stage(kGL * (k + 1) + j);
-      fetch_row(kGL * (k + 2) + j);
       fetch_pos(kGL * (k + 3) + j);
       cp_async_commit();
 #pragma unroll 1
@@ -646,7 +636,8 @@ using namespace tsr;
 extern "C" size_t tsr_region_list_entries(int32_t width, int32_t height, int64_t p_bound) {
   (void)width;
   (void)height;
-  return 8 * (size_t)(p_bound > 0 ? p_bound : 0) + 1;  // up to 8 regions per tile
+  // up to 8 regions per tile, (position, row) pairs of uint32
+  return 2 * (8 * (size_t)(p_bound > 0 ? p_bound : 0) + 1);
 }
 
 extern "C" size_t tsr_region_unit_entries(int32_t width, int32_t height, int64_t p_bound) {

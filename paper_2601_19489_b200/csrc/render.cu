@@ -126,7 +126,8 @@ __device__ __forceinline__ void blend_pair(const float4 g, const float4 c, const
 // pixel (p < n_considered, alpha >= 1/255) in the backward; the others
 // contribute exact zeros there.  With kNR regions per tile (4: 8x8, 8: 8x4
 // halves) region r of tile t stores its positions at
-// list[kNR start_t + r n_t ...]; seg[kNR (segbase_t + s - 1) + r]
+// list[kNR start_t + r n_t ...] (entries: (list position, batch row) pairs);
+// seg[kNR (segbase_t + s - 1) + r]
 // holds the number of entries with position < kSeg s for s = 1..ceil(n/kSeg)
 // (segbase_t = (start_t >> 10) + t: floor((O + n) / kSeg) - floor(O / kSeg)
 // + 1 >= ceil(n / kSeg), so the tiles' segment slots never overlap).
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
   // 2b', c'  [2] r, g, b, depth -- one base address per list entry
   __shared__ float4 s_spl[kBatch][3];
   __shared__ float4 s_raw[kBatch];  // a, b, c (unscaled), level t
-  __shared__ int s_row[kScore ? kBatch : 1];
+  __shared__ int s_row[(kScore || kCkpt >= 3) ? kBatch : 1];
 
   // heavy tiles first when an order is given (tile_order_kernel; its last
   // entry flags whether it differs from raster order)
@@ -200,13 +201,14 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
   // pixels) are two regions, (2 by + half) * 2 + bx (8 per tile)
   constexpr bool kRegions = kCkpt >= 3;
   constexpr int kNR = kCkpt == 4 ? 8 : 4;
-  uint32_t* rl = nullptr;
-  uint32_t* rl2 = nullptr;
+  // region list entries are (list position, batch row) pairs
+  uint2* rl = nullptr;
+  uint2* rl2 = nullptr;
   int r_count = 0, r_count2 = 0, s_next = 1;
   const int reg0 = kCkpt == 4 ? (2 * by) * 2 + bx : warp, reg1 = (2 * by + 1) * 2 + bx;
   const long long segbase = (start >> kSegShift) + tile;
-  if (kRegions) rl = rg.list + kNR * start + (long long)reg0 * n;
-  if (kCkpt == 4) rl2 = rg.list + kNR * start + (long long)reg1 * n;
+  if (kRegions) rl = reinterpret_cast<uint2*>(rg.list) + kNR * start + (long long)reg0 * n;
+  if (kCkpt == 4) rl2 = reinterpret_cast<uint2*>(rg.list) + kNR * start + (long long)reg1 * n;
   bool m0 = false, m1 = false;
   if (kScore == 3) {
     m0 = in0 && sc.mask[pix0];
@@ -228,7 +230,7 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
                                   __fmul_rn(r1.x, kQScale), 0.f);
         s_spl[i][2] = make_float4(r2.x, r2.y, r2.z, r1.z);
         s_raw[i] = make_float4(r0.z, r0.w, r1.x, r1.w);
-        if (kScore) s_row[i] = row;
+        if (kScore || kCkpt >= 3) s_row[i] = row;
       }
     }
     __syncthreads();
@@ -322,11 +324,13 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
           kRegions ? __brev(__reduce_or_sync(0xffffffffu, kCkpt == 4 ? pm0r : (pm0r | pm1r))) : 0u;
       const unsigned pm1 = kCkpt == 4 ? __brev(__reduce_or_sync(0xffffffffu, pm1r)) : 0u;
       if (kRegions) {
-        if ((pm0 >> lane) & 1u) rl[r_count + __popc(pm0 & lt_mask)] = (uint32_t)(pos0 + lane);
+        if ((pm0 >> lane) & 1u)
+          rl[r_count + __popc(pm0 & lt_mask)] = make_uint2((uint32_t)(pos0 + lane), (uint32_t)s_row[c0 + lane]);
         r_count += __popc(pm0);
       }
       if (kCkpt == 4) {
-        if ((pm1 >> lane) & 1u) rl2[r_count2 + __popc(pm1 & lt_mask)] = (uint32_t)(pos0 + lane);
+        if ((pm1 >> lane) & 1u)
+          rl2[r_count2 + __popc(pm1 & lt_mask)] = make_uint2((uint32_t)(pos0 + lane), (uint32_t)s_row[c0 + lane]);
         r_count2 += __popc(pm1);
       }
       if (kCkpt && cend == kGroup &&

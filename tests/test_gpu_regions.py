@@ -115,7 +115,8 @@ def test_regions_zero_upstream_half_tile(region_height):
 
 @pytest.mark.parametrize("region_height", [4, 8])
 def test_region_lists_cover_every_blend(region_height):
-    """Each region list is increasing, within [0, n), and holds exactly the
+    """Each region list is increasing, within [0, n), pairs every position
+    with its batch row, and holds exactly the
     list positions that blend at >= 1 pixel of the region (the backward's
     participation, oracle alphas; positions whose alpha is within 1e-5 of
     the 1/255 threshold at every such pixel may go either way in FP32)."""
@@ -123,7 +124,9 @@ def test_region_lists_cover_every_blend(region_height):
     hb, hi = host_batch(vr.batch), host_index(vr.tiles)
     tgt, reg, _ = regions_pass(vr, np.zeros((64, 96, 3)), region_height=region_height)
     nr = 64 // (2 * region_height)
-    lst, seg = reg.list.cpu().numpy(), reg.seg.cpu().numpy()
+    # entries are (list position, batch row) pairs
+    pairs, seg = reg.list.cpu().numpy().reshape(-1, 2), reg.seg.cpu().numpy()
+    lst, lrow = pairs[:, 0], pairs[:, 1]
     off = hi["offsets"]
     for tile in range(hi["tiles_x"] * hi["tiles_y"]):
         lo, n = int(off[tile]), int(off[tile + 1] - off[tile])
@@ -135,6 +138,8 @@ def test_region_lists_cover_every_blend(region_height):
             total = seg[nr * ((lo >> 10) + tile + nseg - 1) + r]
             ent = lst[nr * lo + r * n: nr * lo + r * n + total].astype(np.int64)
             assert np.all(np.diff(ent) > 0) and (total == 0 or (ent[0] >= 0 and ent[-1] < n))
+            rows = lrow[nr * lo + r * n: nr * lo + r * n + total].astype(np.int64)
+            assert np.array_equal(rows, np.asarray(hi["values"])[lo + ent]), (tile, r)
             x0, y0 = tx * 16 + 8 * (r & 1), ty * 16 + region_height * (r >> 1)
             x1, y1 = min(x0 + 8, 96), min(y0 + region_height, 64)
             if x0 >= 96 or y0 >= 64:
