@@ -212,7 +212,7 @@ size_t tsr_render_bwd_workspace(int32_t width, int32_t height, int64_t p_bound);
  * or 4; both calls take the same value), and the backward's streams (one
  * per (tile, 1024-position segment, region) with entries), filed as each
  * tile finishes under the bucket of the stream's length:
- *   region_list   tsr_region_list_entries(...) uint32
+ *   region_list   tsr_region_list_entries(...) uint32 ((position, row) pairs)
  *   region_seg    tsr_region_seg_entries(...) int32
  *   region_units  tsr_region_unit_entries(...) uint32 (72 length buckets)
  *   region_ctl    tsr_region_ctl_entries() int32 (bucket counts, grab
