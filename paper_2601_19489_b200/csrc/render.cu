@@ -33,6 +33,8 @@
 //      to a pixel whose error mask is set (one atomic per warp and splat);
 //      the density pass of the trainer uses this form and never materialises
 //      the contribution lists.
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 #include "tsr_common.cuh"
@@ -415,6 +417,224 @@ __global__ void __launch_bounds__(kFwdThreads) render_fwd_kernel(
   }
 }
 
+// (Opt-in, TSR_K3_HW=1; measured slower: 301 vs 237 us at C2 -- 94 registers
+// and 64-thread CTAs leave 20 warps per SM against 36, and the halves' hit
+// counts differ.)  K3 for the training step's region mode with two 8x8
+// blocks per warp: the
+// CTA is 2 warps per tile, each warp half (16 lanes) owns one 8x8 block =
+// one K4r region, 4 pixels per lane (column 8 bx + (l & 7), rows ry, ry + 2,
+// ry + 4, ry + 6 with ry = 8 by + (l >> 3), as two vertical pairs).  The two
+// halves walk their own blocks' hits in the same loop trip (a half whose
+// block has no hit left idles), so one trip blends one splat into each of
+// two blocks and the per-hit loop overhead is shared by 128 pixels.  Same
+// arithmetic per pixel as render_fwd_kernel<3, 0>: outputs, checkpoint
+// records, region lists (position, row), segment counts and K4r streams are
+// identical.
+constexpr int kHwThreads = 64;
+__global__ void __launch_bounds__(kHwThreads) render_fwd_hw_kernel(
+    const float4* __restrict__ rec, const int32_t* __restrict__ values,
+    const int64_t* __restrict__ offsets, int width, int height, int tiles_x, float bg_r,
+    float bg_g, float bg_b, float* __restrict__ out_color, float* __restrict__ out_depth,
+    float* __restrict__ out_T, int32_t* __restrict__ out_ncontrib,
+    int32_t* __restrict__ out_ncons, float* __restrict__ ckpt,
+    const int64_t* __restrict__ ckpt_base, const int32_t* __restrict__ order, RegionArgs rg) {
+  constexpr int kNR = 4;
+  __shared__ float4 s_spl[kBatch][3];
+  __shared__ float4 s_raw[kBatch];
+  __shared__ int s_row[kBatch];
+  const int tile = (order && order[gridDim.x]) ? order[blockIdx.x] : (int)blockIdx.x;
+  const int tyi = tile / tiles_x, txi = tile - tyi * tiles_x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int hh = lane >> 4, l = lane & 15;
+  const int bx = hh, by = warp, reg = 2 * by + bx;
+  const int lx = 8 * bx + (l & 7), ry = 8 * by + (l >> 3);
+  const int x = txi * kTile + lx;
+  const int ya0 = tyi * kTile + ry, ya1 = ya0 + 4, yb0 = ya0 + 2, yb1 = ya0 + 6;
+  const bool ina0 = x < width && ya0 < height, ina1 = x < width && ya1 < height;
+  const bool inb0 = x < width && yb0 < height, inb1 = x < width && yb1 < height;
+  const float pxf = (float)x + 0.5f;
+  const float2 pya = make_float2((float)ya0 + 0.5f, (float)ya1 + 0.5f);
+  const float2 pyb = make_float2((float)yb0 + 0.5f, (float)yb1 + 0.5f);
+  const float sx0 = (float)(txi * kTile + 8 * bx) + 0.5f, sy0 = (float)(tyi * kTile + 8 * by) + 0.5f;
+  const long long start = offsets[tile], end = offsets[tile + 1];
+  const int n = (int)(end - start);
+  float* ck0 = ckpt + ckpt_base[tile] * (5 * kTilePixels) + ry * kTile + lx;
+
+  PixPair sa, sb;
+  sa.T = make_float2(ina0 ? 1.f : 0.f, ina1 ? 1.f : 0.f);
+  sb.T = make_float2(inb0 ? 1.f : 0.f, inb1 ? 1.f : 0.f);
+  sa.Cr = sa.Cg = sa.Cb = sa.D = bc2(0.f);
+  sb.Cr = sb.Cg = sb.Cb = sb.D = bc2(0.f);
+  sa.nc0 = sa.nc1 = sb.nc0 = sb.nc1 = 0;
+  sa.ncons0 = sa.ncons1 = sb.ncons0 = sb.ncons1 = 0;
+  const unsigned half_bits = 0xffffu << (16 * hh);
+  uint2* rl = reinterpret_cast<uint2*>(rg.list) + kNR * start + (long long)reg * n;
+  int r_count = 0, s_next = 1;
+  const long long segbase = (start >> kSegShift) + tile;
+  // rows of the half's block held by the four pixel slots: ry - 8 by + {0, 4, 2, 6}
+  const int r0 = l >> 3;
+
+  for (int b0 = 0; b0 < n; b0 += kBatch) {
+    if (!__syncthreads_or(sa.alive0() || sa.alive1() || sb.alive0() || sb.alive1())) break;
+#pragma unroll
+    for (int h = 0; h < kBatch / kHwThreads; ++h) {
+      const int i = tid + h * kHwThreads;
+      const int k = b0 + i;
+      if (k < n) {
+        const int row = values[start + k];
+        const float4 q0 = __ldg(rec + 3 * row), q1 = __ldg(rec + 3 * row + 1),
+                     q2 = __ldg(rec + 3 * row + 2);
+        s_spl[i][0] = make_float4(q0.x, q0.y, q1.y, q1.z);
+        s_spl[i][1] = make_float4(__fmul_rn(q0.z, kQScale), __fmul_rn(q0.w, 2.0f * kQScale),
+                                  __fmul_rn(q1.x, kQScale), 0.f);
+        s_spl[i][2] = make_float4(q2.x, q2.y, q2.z, q1.z);
+        s_raw[i] = make_float4(q0.z, q0.w, q1.x, q1.w);
+        s_row[i] = row;
+      }
+    }
+    __syncthreads();
+    const int cnt = min(kBatch, n - b0);
+    for (int c0 = 0; c0 < cnt; c0 += kGroup) {
+      const unsigned la0 = __ballot_sync(0xffffffffu, sa.alive0()),
+                     la1 = __ballot_sync(0xffffffffu, sa.alive1()),
+                     lb0 = __ballot_sync(0xffffffffu, sb.alive0()),
+                     lb1 = __ballot_sync(0xffffffffu, sb.alive1());
+      if (!(la0 | la1 | lb0 | lb1)) break;  // warp-level early exit (both blocks dead)
+      // this half's live rectangle: lane l holds column l & 7 and rows
+      // r0 + {0, 4, 2, 6} of the block (r0 = l >> 3)
+      const unsigned ma0 = (la0 >> (16 * hh)) & 0xffffu, ma1 = (la1 >> (16 * hh)) & 0xffffu,
+                     mb0 = (lb0 >> (16 * hh)) & 0xffffu, mb1 = (lb1 >> (16 * hh)) & 0xffffu;
+      const unsigned mm = ma0 | ma1 | mb0 | mb1;
+      const unsigned cols = (mm | (mm >> 8)) & 0xffu;
+      auto rows2 = [](unsigned m, int off) {  // rows off (lanes 0-7) and off + 1 (lanes 8-15)
+        return (((m & 0xffu) != 0u) ? (1u << off) : 0u) | (((m & 0xff00u) != 0u) ? (2u << off) : 0u);
+      };
+      const unsigned rows = rows2(ma0, 0) | rows2(ma1, 4) | rows2(mb0, 2) | rows2(mb1, 6);
+      const float bx0 = sx0 + (float)(__ffs(cols) - 1), bx1 = sx0 + (float)(31 - __clz(cols));
+      const float by0 = sy0 + (float)(__ffs(rows) - 1), by1 = sy0 + (float)(31 - __clz(rows));
+      const int cend = min(kGroup, cnt - c0);
+      const int pos0 = b0 + c0;
+      if (pos0 > 0 && (pos0 & (kSeg - 1)) == 0) {  // segment boundary
+        if (l == 0) rg.seg[kNR * (segbase + s_next - 1) + reg] = r_count;
+        ++s_next;
+      }
+      // lane l tests splats c0 + l and c0 + 16 + l against this half's block
+      bool h1 = false, h2 = false;
+      if (mm) {
+        if (l < cend) {
+          const float4 g = s_spl[c0 + l][0], rw = s_raw[c0 + l];
+          h1 = strip_hit(g.x, g.y, rw.x, rw.y, rw.z, rw.w, bx0, bx1, by0, by1);
+        }
+        if (l + 16 < cend) {
+          const float4 g = s_spl[c0 + 16 + l][0], rw = s_raw[c0 + 16 + l];
+          h2 = strip_hit(g.x, g.y, rw.x, rw.y, rw.z, rw.w, bx0, bx1, by0, by1);
+        }
+      }
+      const unsigned q1 = __ballot_sync(0xffffffffu, h1), q2 = __ballot_sync(0xffffffffu, h2);
+      const unsigned hm = ((q1 >> (16 * hh)) & 0xffffu) | (((q2 >> (16 * hh)) & 0xffffu) << 16);
+      unsigned rev = __brev(hm);
+      unsigned pa0 = 0u, pa1 = 0u, pb0 = 0u, pb1 = 0u;  // participation bits (bit-reversed)
+      const bool lca0 = sa.alive0(), lca1 = sa.alive1(), lcb0 = sb.alive0(), lcb1 = sb.alive1();
+      while (__any_sync(0xffffffffu, rev != 0u)) {
+        if (rev) {
+          const int f = 31 - __clz(rev);
+          const unsigned bit = 1u << f;
+          const int j = 31 - f;
+          rev ^= bit;
+          const float4* sp = s_spl[c0 + j];
+          const float4 g0 = sp[0], g1 = sp[1], g2 = sp[2];
+          blend_pair(g0, g1, g2, pxf, pya, pos0 + j, sa);
+          if (sa.part0) pa0 |= bit;
+          if (sa.part1) pa1 |= bit;
+          blend_pair(g0, g1, g2, pxf, pyb, pos0 + j, sb);
+          if (sb.part0) pb0 |= bit;
+          if (sb.part1) pb1 |= bit;
+        }
+      }
+      sa.nc0 += __popc(pa0);
+      sa.nc1 += __popc(pa1);
+      sb.nc0 += __popc(pb0);
+      sb.nc1 += __popc(pb1);
+      if (lca0 && !sa.alive0()) sa.ncons0 = pos0 + 33 - __ffs(pa0);
+      if (lca1 && !sa.alive1()) sa.ncons1 = pos0 + 33 - __ffs(pa1);
+      if (lcb0 && !sb.alive0()) sb.ncons0 = pos0 + 33 - __ffs(pb0);
+      if (lcb1 && !sb.alive1()) sb.ncons1 = pos0 + 33 - __ffs(pb1);
+      // region list entries of this half's block: the OR over its 16 lanes
+      const unsigned pr = pa0 | pa1 | pb0 | pb1;
+      const unsigned or_lo = __reduce_or_sync(0xffffffffu, hh == 0 ? pr : 0u);
+      const unsigned or_hi = __reduce_or_sync(0xffffffffu, hh == 1 ? pr : 0u);
+      const unsigned pm = __brev(hh ? or_hi : or_lo);
+      const unsigned lt_l = (1u << l) - 1u;
+      if ((pm >> l) & 1u)
+        rl[r_count + __popc(pm & lt_l)] = make_uint2((uint32_t)(pos0 + l), (uint32_t)s_row[c0 + l]);
+      if ((pm >> (l + 16)) & 1u)
+        rl[r_count + __popc(pm & ((1u << (l + 16)) - 1u))] =
+            make_uint2((uint32_t)(pos0 + 16 + l), (uint32_t)s_row[c0 + 16 + l]);
+      r_count += __popc(pm);
+      if (cend == kGroup && ((pos0 + kGroup) & (kSeg - 1)) == 0) {
+        // segment-start record: the state after position pos0 + 31 of every
+        // pixel that consumed it (still alive, or died there)
+        float* dst = ck0 + (long long)(pos0 >> 5) * (5 * kTilePixels);
+        auto put = [&](float* d, float T, float Cr, float Cg, float Cb, float D) {
+          d[0] = T;
+          d[kTilePixels] = Cr;
+          d[2 * kTilePixels] = Cg;
+          d[3 * kTilePixels] = Cb;
+          d[4 * kTilePixels] = D;
+        };
+        if (sa.alive0() || sa.ncons0 == pos0 + kGroup) put(dst, sa.T.x, sa.Cr.x, sa.Cg.x, sa.Cb.x, sa.D.x);
+        if (sa.alive1() || sa.ncons1 == pos0 + kGroup)
+          put(dst + 4 * kTile, sa.T.y, sa.Cr.y, sa.Cg.y, sa.Cb.y, sa.D.y);
+        if (sb.alive0() || sb.ncons0 == pos0 + kGroup)
+          put(dst + 2 * kTile, sb.T.x, sb.Cr.x, sb.Cg.x, sb.Cb.x, sb.D.x);
+        if (sb.alive1() || sb.ncons1 == pos0 + kGroup)
+          put(dst + 6 * kTile, sb.T.y, sb.Cr.y, sb.Cg.y, sb.Cb.y, sb.D.y);
+      }
+    }
+  }
+  if (l == 0)  // the remaining segment ends (after an early exit)
+    for (const int nseg = (n + kSeg - 1) >> kSegShift; s_next <= nseg; ++s_next)
+      rg.seg[kNR * (segbase + s_next - 1) + reg] = r_count;
+  {
+    // the tile's K4r streams (as render_fwd_kernel)
+    __syncthreads();
+    const int nseg = (n + kSeg - 1) >> kSegShift;
+    const long long cap = tsr_stream_bucket_cap(offsets[gridDim.x], gridDim.x);
+    uint4* recs = reinterpret_cast<uint4*>(rg.units + (long long)kStreamBuckets * cap);
+    for (int i = tid; i < nseg * kNR; i += kHwThreads) {
+      const int sg = i / kNR, q = i - sg * kNR;
+      const int e0 = sg > 0 ? rg.seg[kNR * (segbase + sg - 1) + q] : 0;
+      const int len = rg.seg[kNR * (segbase + sg) + q] - e0;
+      if (len > 0 || i == 0) {
+        const int id = atomicAdd(rg.ctl + kStreamBuckets + 1, 1);
+        recs[2 * id] = make_uint4(((uint32_t)tile << 16) | ((uint32_t)sg << 3) | (uint32_t)q,
+                                  (uint32_t)start, (uint32_t)n, (uint32_t)e0);
+        recs[2 * id + 1] = make_uint4((uint32_t)len, 0u, 0u, 0u);
+        const int b = tsr_stream_bucket(len);
+        const int at = atomicAdd(rg.ctl + b, 1);
+        rg.units[b * cap + at] = (uint32_t)id;
+      }
+    }
+  }
+  auto out = [&](bool in, int y, float T, float Cr, float Cg, float Cb, float D, int ncb, int ncs) {
+    if (!in) return;
+    const long long pix = (long long)y * width + x;
+    out_color[3 * pix] = fmaf(T, bg_r, Cr);
+    out_color[3 * pix + 1] = fmaf(T, bg_g, Cg);
+    out_color[3 * pix + 2] = fmaf(T, bg_b, Cb);
+    out_depth[pix] = D;
+    out_T[pix] = T;
+    out_ncontrib[pix] = ncb;
+    out_ncons[pix] = ncs;
+  };
+  out(ina0, ya0, sa.T.x, sa.Cr.x, sa.Cg.x, sa.Cb.x, sa.D.x, sa.nc0, sa.alive0() ? n : sa.ncons0);
+  out(ina1, ya1, sa.T.y, sa.Cr.y, sa.Cg.y, sa.Cb.y, sa.D.y, sa.nc1, sa.alive1() ? n : sa.ncons1);
+  out(inb0, yb0, sb.T.x, sb.Cr.x, sb.Cg.x, sb.Cb.x, sb.D.x, sb.nc0, sb.alive0() ? n : sb.ncons0);
+  out(inb1, yb1, sb.T.y, sb.Cr.y, sb.Cg.y, sb.Cb.y, sb.D.y, sb.nc1, sb.alive1() ? n : sb.ncons1);
+  (void)r0;
+  (void)half_bits;
+}
+
 // Launch order of the per-tile kernels (K3, K4): the heavy tiles (list longer
 // than 4x the mean) first, in raster order, then the others in raster order.
 // order has n_tiles + 1 entries; order[n_tiles] = 0 when there is no heavy
@@ -542,6 +762,17 @@ extern "C" int tsr_render_fwd_regions(const float* rec, const int32_t* values,
   cudaStream_t s = (cudaStream_t)stream;
   const ScoreArgs none{};
   if (cudaMemsetAsync(region_ctl, 0, kUnitCtl * sizeof(int32_t), s) != cudaSuccess) return TSR_E_CUDA;
+  // the two-blocks-per-warp form is opt-in (TSR_K3_HW=1): measured 301 vs 237 us
+  static const bool hw = getenv("TSR_K3_HW") && atoi(getenv("TSR_K3_HW")) == 1;
+  if (region_height == 8 && hw) {
+    render_fwd_hw_kernel<<<n_tiles, kHwThreads, 0, s>>>(
+        (const float4*)rec, values, offsets, width, height, tx, background_host[0],
+        background_host[1], background_host[2], out_color, out_depth, out_final_T, out_n_contrib,
+        out_n_considered, ckpt, ckpt_base, tile_order,
+        RegionArgs{region_list, region_seg, region_units, region_ctl});
+    TSR_CHECK_LAUNCH();
+    return TSR_OK;
+  }
   auto* k = region_height == 8 ? render_fwd_kernel<3, 0> : render_fwd_kernel<4, 0>;
   k<<<n_tiles, kFwdThreads, 0, s>>>(
       (const float4*)rec, values, offsets, width, height, tx, background_host[0],
