@@ -185,3 +185,50 @@ def test_train_step_region_k4_matches_tile_k4(monkeypatch):
                   ("color", slice(6, 9))):
         assert rel_err(g_r[:, sl], g_t[:, sl]) < GRAD_RTOL, f
     assert out["regions"][3] == out["tiles"][3]
+
+
+def test_streams_filed_once_with_their_lengths():
+    """K3 files one K4r stream per (tile, segment, region) with entries --
+    plus every tile's (segment 0, region 0) stream, which counts merges --
+    under its length's bucket (width 4 below 256 entries); each record holds
+    (tile << 16 | segment << 3 | region, list start, list length, first
+    entry, entries) consistent with the index and the segment counts."""
+    ts, vr, gt = _scene(30_000, 64, 64, seed=3, clustered=True, cluster_opacity=(0.004, 0.02))
+    b, t = vr.batch, vr.tiles
+    g = np.zeros((64, 64, 3))
+    g[:] = 1e-3
+    tgt, reg, _ = regions_pass(vr, g, region_height=8)
+    nr, nb = 4, 72
+    ctl = reg.ctl.cpu().numpy()
+    off = t.offsets.cpu().numpy()
+    P, tiles = int(off[-1]), len(off) - 1
+    cap = 8 * (P // 1024 + tiles + 1)
+    units = reg.units.cpu().numpy().view(np.uint32)
+    recs = units[nb * cap:].reshape(-1, 8)
+    seg = reg.seg.cpu().numpy()
+
+    def bucket(n):
+        return n >> 2 if n < 256 else min(64 + ((n - 256) >> 7), nb - 1)
+
+    seen = {}
+    for bk in range(nb):
+        for sid in units[bk * cap: bk * cap + int(ctl[bk])]:
+            code, start, n, e0, ln = (int(v) for v in recs[sid][:5])
+            key = (code >> 16, (code >> 3) & 0x1fff, code & 7)
+            assert key not in seen, key
+            seen[key] = (start, n, e0, ln)
+            assert bucket(ln) == bk, (key, ln, bk)
+    assert int(ctl[nb + 1]) == len(seen)  # record ids handed out
+    expect = set()
+    for tile in range(tiles):
+        lo, n = int(off[tile]), int(off[tile + 1] - off[tile])
+        if n == 0:
+            continue
+        for s in range(-(-n // 1024)):
+            for r in range(nr):
+                cur = int(seg[nr * ((lo >> 10) + tile + s) + r])
+                prev = int(seg[nr * ((lo >> 10) + tile + s - 1) + r]) if s else 0
+                if cur - prev > 0 or (s == 0 and r == 0):
+                    expect.add((tile, s, r))
+                    assert seen[(tile, s, r)] == (lo, n, prev, cur - prev), (tile, s, r)
+    assert set(seen) == expect
