@@ -41,12 +41,23 @@ constexpr int kSeg = 1 << kSegShift;
 // record id (two uint4 after the buckets, units + kStreamBuckets * cap):
 // {tile << 16 | segment << 3 | region, tile list start, tile list length,
 // first region-list entry of the segment}, {entries, -, -, -}.
-constexpr int kStreamBuckets = 72;
-constexpr int kUnitCtl = 128;  // ints in the control block (zeroed by K3's launch)
+#ifndef TSR_STREAM_BUCKETS_W8
+#define TSR_STREAM_BUCKETS_W8 0
+#endif
+// 0: width 4 below 256 entries (72 buckets); 1: width 8 below 1024 (129);
+// 2: width 2 below 256, then 64 (144)
+constexpr int kStreamBuckets = TSR_STREAM_BUCKETS_W8 == 1 ? 129 : (TSR_STREAM_BUCKETS_W8 == 2 ? 144 : 72);
+constexpr int kUnitCtl = 192;  // ints in the control block (zeroed by K3's launch)
 __host__ __device__ inline long long tsr_stream_bucket_cap(long long pairs, int n_tiles) {
   return 8 * (pairs / kSeg + n_tiles + 1);
 }
 __host__ __device__ inline int tsr_stream_bucket(int length) {
+  if (TSR_STREAM_BUCKETS_W8 == 1) return length < 1024 ? length >> 3 : 128;  // width 8
+  if (TSR_STREAM_BUCKETS_W8 == 2) {
+    if (length < 256) return length >> 1;
+    const int b2 = 128 + ((length - 256) >> 6);
+    return b2 < kStreamBuckets - 1 ? b2 : kStreamBuckets - 1;
+  }
   if (length < 256) return length >> 2;
   const int b = 64 + ((length - 256) >> 7);
   return b < kStreamBuckets - 1 ? b : kStreamBuckets - 1;
