@@ -51,7 +51,10 @@ namespace tsr {
 #endif
 constexpr int kSB = 256;                 // threads per CTA
 constexpr int kBins = 256;               // 8-bit digits
-constexpr int kItems = 8;                // items per thread per sub-tile
+#ifndef TSR_K2_PAIR_ITEMS
+#define TSR_K2_PAIR_ITEMS 8
+#endif
+constexpr int kItems = TSR_K2_PAIR_ITEMS;  // items per thread per sub-tile (pair passes)
 constexpr int kSub = kSB * kItems;       // 2048-item sub-tiles
 #ifndef TSR_K2_DEPTH_ITEMS
 #define TSR_K2_DEPTH_ITEMS 10
