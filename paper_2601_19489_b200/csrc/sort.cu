@@ -472,6 +472,9 @@ __device__ __forceinline__ uint32_t rank_row(const uint32_t* row_by_rank, long l
   return row_by_rank ? row_by_rank[r] : (uint32_t)r;
 }
 
+// kLB: the instantiation for the load-balanced strategy (its warp-
+// cooperative re-walk); the others never hold its registers
+template <bool kLB>
 __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, long long O,
                            long long p_cap,
                            const uint32_t* __restrict__ row_by_rank, SortSmem& sm,
@@ -579,7 +582,7 @@ __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, lon
     }
     if (r0 == rlo) TSR_TRACE_AT(42);
     // exact FP64 re-walk of the rows whose span record overflowed
-    if (strategy == 1) {
+    if (kLB) {
       // load-balanced strategy: the warp-cooperative round-robin min-q walk
       // (bin_load_balanced, binning.py:262-298), writing each splat's passing
       // tiles at its emission offset; the staging area is free here
@@ -643,6 +646,7 @@ __device__ void emit_phase(const IndexArgs& a, long long rlo, long long rhi, lon
 }
 
 // ---- the persistent index kernel
+template <bool kLB>
 __global__ void __launch_bounds__(kSB, TSR_K2_CTAS) build_index_kernel(IndexArgs a) {
   __shared__ SortSmem sm;
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -734,7 +738,7 @@ __global__ void __launch_bounds__(kSB, TSR_K2_CTAS) build_index_kernel(IndexArgs
     P = (long long)t1;
   }
   if (bid == 0 && tid == 0 && P > a.p_cap && a.overflow) *a.overflow = 1;  // sticky
-  emit_phase(a, rlo, rhi, O, a.p_cap, drow, sm, dyn);
+  emit_phase<kLB>(a, rlo, rhi, O, a.p_cap, drow, sm, dyn);
   grid_barrier(a.bar + nb++, G);
 
   // ---- 3. stable sort of the pairs by tile; the last pass writes keys/values
@@ -895,13 +899,13 @@ static int build_index_impl(const float* rec, const uint32_t* depth_bits, const 
   a.hist4 = (uint32_t*)(w + pl.hist4);
   a.bar = (unsigned int*)(w + pl.bar);
 
+  auto* kern = a.strategy == 1 ? build_index_kernel<true> : build_index_kernel<false>;
   int dev = 0, sms = 0, per_sm = 0;
   if (cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-      cudaFuncSetAttribute(build_index_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kDynSmem) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, build_index_kernel, kSB,
-                                                    kDynSmem) != cudaSuccess)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem) !=
+          cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSB, kDynSmem) != cudaSuccess)
     return TSR_E_CUDA;
   int grid = sms * (per_sm < TSR_K2_CTAS ? per_sm : TSR_K2_CTAS);
   // small problems: fewer CTAs (each grid barrier costs ~ one arrival per
@@ -912,7 +916,7 @@ static int build_index_impl(const float* rec, const uint32_t* depth_bits, const 
   if (grid < 1) return TSR_E_CUDA;
   if (cudaMemsetAsync(w + pl.ctl_off, 0, pl.ctl_bytes, s) != cudaSuccess) return TSR_E_CUDA;
   void* args[] = {&a};
-  if (cudaLaunchCooperativeKernel((const void*)build_index_kernel, dim3(grid), dim3(kSB), args,
+  if (cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kSB), args,
                                   kDynSmem, s) != cudaSuccess)
     return TSR_E_CUDA;
   return TSR_OK;
